@@ -1,0 +1,224 @@
+"""Generate the golden fixtures that pin the oracle (run in the build container).
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Imports the UNMODIFIED reference package ``fusedbeam`` read-only from
+``/root/reference/pkg/src`` and records its outputs on seeded inputs:
+
+* ``trie.pkl.gz``      -- ``build_trie`` arrays on random lexicons
+                          (lexicon_trie.py:227-276);
+* ``lookahead.pkl.gz`` -- ``LookaheadFusion.char_scores/advance/reorder`` rows on
+                          random lexicons, TableLM rows and random walks
+                          (fusion.py:109-233);
+* ``decode.pkl.gz``    -- ``decode_batch`` results over random acoustic tables
+                          (plain / original / improved coverage / EOS gate /
+                          look-ahead fusion, quantised ties) (decoder.py:339-480);
+* ``neural.pkl.gz``    -- ``decode_batch`` + ``LookaheadFusion`` driving the
+                          oracle's PyTorch-CPU attention-LSTM scorer and LSTM
+                          word LM at a small size.
+
+The GPU box never reads /root/reference: the tests only read these files.
+"""
+
+from __future__ import annotations
+
+import gzip
+import os
+import pickle
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from fusedbeam.decoder import DecodeConfig, TraceScorer, _TraceTable, decode_batch  # noqa: E402
+from fusedbeam.fusion import LookaheadBatch, LookaheadFusion  # noqa: E402
+from fusedbeam.kaldi_io import FeatureMatrix  # noqa: E402
+from fusedbeam.lexicon_trie import build_trie  # noqa: E402
+from fusedbeam.token_dict import TokenDictionary  # noqa: E402
+from fusedbeam.word_lm import TableLM  # noqa: E402
+
+from oracle.neural import OracleAttnLstmScorer, OracleLstmWordLM  # noqa: E402
+from paper_1909_08723_b200 import synth  # noqa: E402
+
+
+def dump(name, obj):
+    with gzip.open(os.path.join(HERE, name), "wb") as f:
+        pickle.dump(obj, f, protocol=4)
+
+
+def rand_vocab(rng, max_words, alphabet, max_len=6):
+    letters = list("abcdefghij"[:alphabet])
+    distinct = sum(alphabet ** k for k in range(1, max_len + 1))
+    n = int(rng.integers(2, min(max_words, distinct) + 1))
+    words = set()
+    while len(words) < n:
+        words.add("".join(rng.choice(letters, size=int(rng.integers(1, max_len + 1)))))
+    return letters, sorted(words)
+
+
+def trie_cases():
+    rng = np.random.default_rng(11)
+    cases = []
+    for i in range(40):
+        letters, words = rand_vocab(rng, 200, int(rng.integers(2, 11)))
+        d = TokenDictionary(letters)
+        t = build_trie(words, d)
+        cases.append(dict(letters=letters, words=words,
+                          transitions=t.transitions.copy(), edge_labels=t.edge_labels.copy(),
+                          is_final=t.is_final.copy(), word_index=t.word_index.copy(),
+                          ub=t.ub_index.copy(), lb=t.lb_index.copy(),
+                          children=t.char_children.copy(), ranked=t.words(d)))
+    dump("trie.pkl.gz", cases)
+
+
+def lookahead_cases():
+    rng = np.random.default_rng(22)
+    cases = []
+    for i in range(30):
+        letters, words = rand_vocab(rng, 120, int(rng.integers(2, 9)))
+        d = TokenDictionary(letters)
+        t = build_trie(words, d)
+        ranked = t.words(d)
+        V = len(ranked)
+        rows = {(): rng.dirichlet(np.ones(V))}
+        for w in ranked[: min(V, 5)]:
+            rows[(w,)] = rng.dirichlet(np.ones(V)) * (0 if i % 7 == 3 else 1)
+        eos = {(): 0.05, (ranked[0],): 0.2}
+        lm = TableLM(vocab=tuple(ranked), rows=rows, eos=eos)
+        fus = LookaheadFusion(t, lm, d)
+        n = 6
+        st = fus.start(n)
+        walk = []
+        char_ids = [d.index(c) for c in letters]
+        for step in range(8):
+            sc = fus.char_scores(st)
+            toks = []
+            for b in range(n):
+                s = int(st.trie_states[b])
+                opts = [c for c in char_ids if s >= 0 and t.char_children[s, c] >= 0]
+                u = rng.random()
+                if u < 0.2 or not opts:
+                    toks.append(d.space_id)
+                elif u < 0.27:
+                    toks.append(int(rng.choice(char_ids)))     # may leave the lexicon
+                elif u < 0.3:
+                    toks.append(d.eos_id)
+                else:
+                    toks.append(int(rng.choice(opts)))
+            parents = sorted(rng.integers(0, n, size=n).tolist())
+            walk.append(dict(scores=sc, tokens=np.array(toks), parents=np.array(parents),
+                             states=st.trie_states.copy(), g=st.g.copy(),
+                             floored=fus.diagnostics["floored_scores"]))
+            st = fus.advance(st, np.array(toks))
+            st = fus.reorder(st, parents)
+        cases.append(dict(letters=letters, words=words, rows=rows, eos=eos, walk=walk))
+    dump("lookahead.pkl.gz", cases)
+
+
+def rand_table(rng, d, uid, t_enc, depth=2, quantized=False):
+    V = len(d)
+
+    def dist():
+        if quantized:
+            raw = rng.choice([1.0, 2.0, 4.0], size=V)
+            return raw / raw.sum()
+        return rng.dirichlet(np.ones(V))
+
+    rows = {}
+    prefixes = [()]
+    frontier = [()]
+    for _ in range(depth):
+        nxt = [p + (tok,) for p in frontier for tok in range(V)
+               if tok not in (d.pad_id, d.eos_id)]
+        frontier = nxt
+        prefixes.extend(nxt)
+    for p in prefixes:
+        rows[p] = (np.log(dist()), rng.dirichlet(np.ones(t_enc)))
+    default = (np.log(dist()), rng.dirichlet(np.ones(t_enc)))
+    return _TraceTable(uid, t_enc, V, rows, default)
+
+
+def decode_cases():
+    rng = np.random.default_rng(33)
+    d = TokenDictionary(["a", "b", "c"])
+    t = build_trie(["a", "ab", "abc", "b", "bc", "ca", "cab"], d)
+    ranked = t.words(d)
+    cases = []
+    for i in range(24):
+        mode = i % 6
+        nutt = int(rng.integers(1, 5))
+        tables = {}
+        for u in range(nutt):
+            uid = f"u{i}_{u}"
+            tables[uid] = rand_table(rng, d, uid, int(rng.integers(2, 7)),
+                                     depth=2, quantized=bool(i % 2))
+        lm_rows = {(): rng.dirichlet(np.ones(len(ranked)))}
+        for w in ranked[:3]:
+            lm_rows[(w,)] = rng.dirichlet(np.ones(len(ranked)))
+        cfg = dict(beam_size=int(rng.integers(1, 9)),
+                   lm_weight=[0.0, 0.0, 0.0, 0.9, 0.7, 0.5][mode],
+                   coverage_mode=["off", "original", "improved", "improved", "off", "improved"][mode],
+                   coverage_weight=0.05, tau1=0.4, tau2=0.9, cov_margin=0.7,
+                   eos_gamma=[None, None, 1.5, 1.5, None, 1.2][mode],
+                   max_len_ratio=[1.0, 1.5, 1.0, 2.0, 1.0, 1.0][mode])
+        fused = mode >= 3
+        fus = None
+        if fused:
+            lm = TableLM(vocab=tuple(ranked), rows=lm_rows, eos={(): 0.1})
+            fus = LookaheadFusion(t, lm, d)
+        feats = [FeatureMatrix(uid, np.zeros((1, 1), np.float32)) for uid in tables]
+        res = decode_batch(feats, TraceScorer(tables), fus, DecodeConfig(**cfg), d)
+        cases.append(dict(tables={k: (v.t_enc, v.rows, v.default) for k, v in tables.items()},
+                          order=list(tables), cfg=cfg, fused=fused, lm_rows=lm_rows,
+                          lm_eos={(): 0.1},
+                          results=[(r.utt_id, r.tokens, r.score, r.attn_accum.copy(),
+                                    r.finished, r.steps) for r in res]))
+    dump("decode.pkl.gz", dict(letters=["a", "b", "c"],
+                               words=["a", "ab", "abc", "b", "bc", "ca", "cab"],
+                               cases=cases))
+
+
+def neural_cases():
+    import torch
+    torch.set_num_threads(4)
+    d = TokenDictionary(synth.wsj_token_list())
+    words = synth.synth_lexicon(300, seed=5)
+    t = build_trie(words, d)
+    ranked = t.words(d)
+    adims = synth.AsrDims(enc_layers=2, enc_hidden=32, dec_layers=2, dec_hidden=32,
+                          emb=16, att=32, out_scale=0.6)
+    ldims = synth.LmDims(layers=2, hidden=48, words=len(ranked), emb_scale=0.3,
+                         eos_bias=2.0)
+    W = synth.asr_weights(adims, seed=7, eos_id=d.eos_id)
+    W.update(synth.lm_weights(ldims, seed=8))
+    utts = synth.synth_fbank(4, seed=9, frames=(40, 64))
+    feats = [FeatureMatrix(u, x) for u, x in utts]
+    cases = []
+    for k, cfg in enumerate([
+            dict(beam_size=4, lm_weight=0.5),
+            dict(beam_size=6, lm_weight=0.9, coverage_mode="improved",
+                 coverage_weight=0.02, eos_gamma=1.5),
+            dict(beam_size=3, lm_weight=0.0)]):
+        sc = OracleAttnLstmScorer(W, adims.enc_layers, adims.dec_layers,
+                                  adims.subsample, d.eos_id)
+        lm = OracleLstmWordLM(W, ldims.layers, len(ranked))
+        fus = LookaheadFusion(t, lm, d) if cfg["lm_weight"] > 0 else None
+        res = decode_batch(feats, sc, fus, DecodeConfig(**cfg), d)
+        cases.append(dict(cfg=cfg, results=[(r.utt_id, r.tokens, r.score,
+                                             np.asarray(r.attn_accum).copy(), r.finished,
+                                             r.steps) for r in res]))
+    dump("neural.pkl.gz", dict(words=words, adims=adims.__dict__, ldims=ldims.__dict__,
+                               asr_seed=7, lm_seed=8, fbank_seed=9, frames=(40, 64),
+                               n_utts=4, cases=cases))
+
+
+if __name__ == "__main__":
+    trie_cases()
+    lookahead_cases()
+    decode_cases()
+    neural_cases()
+    print("golden fixtures written to", HERE)
