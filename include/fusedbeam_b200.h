@@ -1,0 +1,166 @@
+/*
+ * fusedbeam_b200 -- C ABI of the B200 (sm_100a) kernels behind the
+ * reference's decoder / look-ahead-fusion plugin API.
+ *
+ * Conventions
+ *  - Every entry point returns an int status (FB_OK = 0) and never throws;
+ *    fb_last_error() gives a thread-local message for the last failure.
+ *  - All array arguments are DEVICE pointers owned by the caller (the Python
+ *    host allocates them with torch); sizes are plain integers.  `stream` is a
+ *    cudaStream_t passed as void*.  No entry point allocates or synchronises.
+ *  - Optional "device count" arguments (`*_dev`) let a CUDA graph replay a
+ *    launch whose row count is only known on the device: the grid is sized
+ *    for the host maximum and blocks past the device count exit at once.
+ *
+ * Reference interfaces each group replaces are cited per function
+ * (paths relative to /root/reference/pkg/src/fusedbeam/).
+ */
+#ifndef FUSEDBEAM_B200_H
+#define FUSEDBEAM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  FB_OK = 0,
+  FB_ERR_VALUE = 1,   /* bad argument / shape      -> ValueError       */
+  FB_ERR_CONFIG = 2,  /* unusable configuration    -> ConfigError      */
+  FB_ERR_CUDA = 3     /* CUDA launch/runtime error -> RuntimeError     */
+};
+
+const char* fb_last_error(void);
+int fb_abi_version(void);
+/* Number of kernel launches issued through this library by the calling
+ * process (for bench.py's gpu_launches claim); reset with fb_launch_reset. */
+unsigned long long fb_launch_count(void);
+void fb_launch_reset(void);
+
+/* ---- prefix-tree automaton, CSR packed (lexicon_trie.py:47-129) ---------- */
+typedef struct {
+  const int32_t* row_ptr;    /* [S+1] edge offsets per state                 */
+  const int32_t* edge_label; /* [E]   token id, ascending within a state     */
+  const int32_t* edge_child; /* [E]   child state                            */
+  const int32_t* info;       /* [S*4] {ub, lb, rank (-1 if not final), 0}   */
+  int32_t num_states;
+  int32_t num_words;
+  int32_t alphabet;          /* == len(token_dict)                          */
+} fb_trie_t;
+
+/* LookaheadFusion.char_scores (fusion.py:118-185), Eq. 4 of PAPER.md.
+ * Row r = rows ? rows[i] : i for i < (n_dev ? *n_dev : n_max).
+ *   trie_state[r] >= 0 (OOV_STATE = -2 scores the penalty everywhere),
+ *   g row = g_pool + hist_slot[r]*g_stride (cumulative word mass, fp64),
+ *   LM eos term: state 0 -> hist_eos[hist_slot[r]] (or ext_eos[r] when
+ *   hist_eos is NULL); final state -> word_end + ext_eos[r].
+ * Writes out[r*out_stride + c] for all c < alphabet (fp64, natural log) and
+ * adds the number of floored scores to *floored (may be NULL). */
+int fb_lookahead_scores(const fb_trie_t* trie, int32_t n_max, const int32_t* n_dev,
+                        const int32_t* rows, const int32_t* trie_state,
+                        const int32_t* hist_slot, const double* g_pool, int64_t g_stride,
+                        const double* hist_eos, const double* ext_eos,
+                        int32_t space_id, int32_t eos_id, double oov_penalty,
+                        double score_floor, double* out, int64_t out_stride,
+                        unsigned long long* floored, void* stream);
+
+/* Trie half of LookaheadFusion.advance (fusion.py:187-207): for row r with
+ * parent p = parent ? parent[r] : r:
+ *   state_out[r] = child(state_in[p], tok) for in-word tokens (OOV_STATE when
+ *   missing), 0 for <space>, state_in[p] for <eos>/<pad>;
+ *   boundary_rank[r] = rank of the closed word (final state), -1 (<unk>) or
+ *   -2 (no boundary).  hist_out[r] = hist_in[p] when both are non-NULL. */
+int fb_trie_advance(const fb_trie_t* trie, int32_t n_max, const int32_t* n_dev,
+                    const int32_t* rows, const int32_t* parent, const int32_t* state_in,
+                    const int32_t* hist_in, const int32_t* tokens, int32_t space_id,
+                    int32_t eos_id, int32_t pad_id, int32_t* state_out, int32_t* hist_out,
+                    int32_t* boundary_rank, void* stream);
+
+/* cumsum_distribution (fusion.py:40-42, :223): g_pool[slots[m]] = running
+ * fp64 sum of probs[m, :vw]. */
+int fb_cumsum_rows(int32_t m, const double* probs, int64_t p_stride, int32_t vw,
+                   const int32_t* slots, double* g_pool, int64_t g_stride, void* stream);
+
+/* Word-LM logits -> look-ahead mass (word_lm.py:169-179 for an LSTM LM):
+ * g_pool[slots[m]] = cumsum(softmax(logits[m, :vw])) in fp64 and
+ * eos_out[slots[m]] = logits[m, vw] - logsumexp(logits[m, :v_out]). */
+int fb_logits_to_g(int32_t m_max, const int32_t* m_dev, const float* logits,
+                   int64_t l_stride, int32_t vw, int32_t v_out, const int32_t* slots,
+                   double* g_pool, int64_t g_stride, double* eos_out, void* stream);
+
+/* ---- beam search step (decoder.py:339-480) ------------------------------ */
+typedef struct {
+  int32_t beam, vocab, pad_id, eos_id;
+  int32_t cov_mode;            /* 0 off, 1 original (Eq.5), 2 improved (Eq.6) */
+  int32_t gate_on;             /* EOS threshold (Eq.7) on/off               */
+  int32_t early_stop;          /* fusion is None or nonpositive_scores       */
+  int32_t has_fusion;
+  int32_t am_f32;              /* am rows are fp32 (else fp64)               */
+  int32_t max_tokens;          /* token row capacity (>= max_len + 1)        */
+  int32_t t_max;               /* attention accumulator row capacity         */
+  int32_t pad0;
+  double lm_weight, cov_weight, tau1, tau2, cov_margin, gamma;
+} fb_search_cfg_t;
+
+typedef struct {
+  /* per utterance [B] */
+  int32_t* active;
+  int32_t* n_live;
+  int32_t* steps;
+  const int32_t* max_len;
+  const int32_t* t_enc;
+  /* per slot [B*beam]: entering-step values, ping-pong pairs (in -> out) */
+  const double* base_in;  double* base_out;
+  const double* total_in; double* total_out;
+  const int32_t* tok_in;  int32_t* tok_out;      /* [B*beam][max_tokens] */
+  int32_t* parent;        /* [B*beam] out: parent slot of the new row      */
+  int32_t* last_tok;      /* [B*beam] out: chosen token of the new row     */
+  /* per row accumulated attention AFTER this step (accum + attn), and its
+   * coverage -- produced by fb_attend_coverage or the attention kernel   */
+  const double* acc_post; /* [B*beam][t_max] */
+  const double* cov_post; /* [B*beam]        */
+  /* finished pool [B][2*beam] */
+  int32_t* fin_valid; double* fin_total; int32_t* fin_len;
+  int32_t* fin_tokens;    /* [B][2*beam][max_tokens] */
+  double* fin_acc;        /* [B][2*beam][t_max]      */
+  /* results [B] (written when an utterance terminates) */
+  int32_t* res_len; double* res_score; int32_t* res_finished; int32_t* res_steps;
+  int32_t* res_tokens;    /* [B][max_tokens] */
+  double* res_acc;        /* [B][t_max]      */
+  /* compact list of the rows that enter the NEXT step (active utterances) */
+  int32_t* next_rows; int32_t* next_count;
+  /* per-utterance decision margin (see oracle/search.py), may be NULL */
+  double* margin;
+} fb_search_state_t;
+
+/* One lock-step selection over every active utterance: combine am + lm_weight
+ * * fusion, pad -> -inf, EOS gate, token-major stable top-beam with the
+ * reference tie-break, coverage bonus, finished-set cap, early stop and
+ * result pick.  am/fusion rows are indexed by slot. */
+int fb_search_step(const fb_search_cfg_t* cfg, const fb_search_state_t* st,
+                   int32_t num_utts, const void* am, int64_t am_stride,
+                   const double* fusion, int64_t fusion_stride, void* stream);
+
+/* accum_post[r] = accum_in[parent(r)] + attn[r] (fp64) and its coverage
+ * (decoder.py:36-48 and :421-425); attn is fp32 or fp64 (attn_f32).  Rows with
+ * t >= t_enc[row/beam] are left untouched. */
+int fb_attend_coverage(const fb_search_cfg_t* cfg, int32_t n_max, const int32_t* n_dev,
+                       const int32_t* rows, const int32_t* parent, const int32_t* t_enc,
+                       const double* acc_in, const void* attn, int32_t attn_f32,
+                       int64_t attn_stride, double* acc_out, double* cov_out, void* stream);
+
+/* Initialise the per-utterance search state for a new batch (one live row per
+ * utterance, decoder.py:350-359). */
+int fb_search_init(const fb_search_cfg_t* cfg, const fb_search_state_t* st,
+                   int32_t num_utts, void* stream);
+
+/* Row gather (the reorder of fusion.py:226-233 / an AcousticScorer): for r <
+ * n: dst[r*row_bytes..] = src[idx[r]*row_bytes..]. */
+int fb_gather_rows(int32_t n, const int32_t* idx, const void* src, void* dst,
+                   int64_t row_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FUSEDBEAM_B200_H */

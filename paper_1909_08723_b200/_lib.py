@@ -1,0 +1,132 @@
+"""ctypes binding of the in-tree C-ABI library ``libfusedbeam_b200.so``.
+
+The product path has no CPU fallback: every entry point raises when the
+library is missing or was built for another architecture.  Status codes map to
+the reference's exception types (``errors.py:4-13``): FB_ERR_VALUE ->
+ValueError, FB_ERR_CONFIG -> ConfigError, FB_ERR_CUDA -> RuntimeError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .errors import ConfigError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfusedbeam_b200.so")
+
+i32, i64, f64, vp = C.c_int32, C.c_int64, C.c_double, C.c_void_p
+
+
+class FbTrie(C.Structure):
+    _fields_ = [("row_ptr", vp), ("edge_label", vp), ("edge_child", vp), ("info", vp),
+                ("num_states", i32), ("num_words", i32), ("alphabet", i32)]
+
+
+class FbSearchCfg(C.Structure):
+    _fields_ = [("beam", i32), ("vocab", i32), ("pad_id", i32), ("eos_id", i32),
+                ("cov_mode", i32), ("gate_on", i32), ("early_stop", i32), ("has_fusion", i32),
+                ("am_f32", i32), ("max_tokens", i32), ("t_max", i32), ("pad0", i32),
+                ("lm_weight", f64), ("cov_weight", f64), ("tau1", f64), ("tau2", f64),
+                ("cov_margin", f64), ("gamma", f64)]
+
+
+class FbSearchState(C.Structure):
+    _fields_ = [(n, vp) for n in (
+        "active", "n_live", "steps", "max_len", "t_enc",
+        "base_in", "base_out", "total_in", "total_out", "tok_in", "tok_out",
+        "parent", "last_tok", "acc_post", "cov_post",
+        "fin_valid", "fin_total", "fin_len", "fin_tokens", "fin_acc",
+        "res_len", "res_score", "res_finished", "res_steps", "res_tokens", "res_acc",
+        "next_rows", "next_count")]
+
+
+class FbLstmLayer(C.Structure):
+    _fields_ = [("w", vp), ("bias", vp), ("k_in", i32), ("k_pad", i32), ("hidden", i32),
+                ("residual", i32)]
+
+
+_SIGS = {
+    "fb_last_error": (C.c_char_p, []),
+    "fb_abi_version": (C.c_int, []),
+    "fb_launch_count": (C.c_ulonglong, []),
+    "fb_launch_reset": (None, []),
+    "fb_lookahead_scores": (C.c_int, [C.POINTER(FbTrie), i32, vp, vp, vp, vp, vp, i64, vp, vp,
+                                      i32, i32, f64, f64, vp, i64, vp, vp]),
+    "fb_trie_advance": (C.c_int, [C.POINTER(FbTrie), i32, vp, vp, vp, vp, vp, vp, i32, i32, i32,
+                                  vp, vp, vp, vp]),
+    "fb_cumsum_rows": (C.c_int, [i32, vp, i64, i32, vp, vp, i64, vp]),
+    "fb_logits_to_g": (C.c_int, [i32, vp, vp, i64, i32, i32, vp, vp, i64, vp, vp]),
+    "fb_search_init": (C.c_int, [C.POINTER(FbSearchCfg), C.POINTER(FbSearchState), i32, vp]),
+    "fb_search_step": (C.c_int, [C.POINTER(FbSearchCfg), C.POINTER(FbSearchState), i32, vp, i64,
+                                 vp, i64, vp]),
+    "fb_attend_coverage": (C.c_int, [C.POINTER(FbSearchCfg), i32, vp, vp, vp, vp, vp, vp, i32,
+                                     i64, vp, vp, vp]),
+    "fb_gather_rows": (C.c_int, [i32, vp, vp, vp, i64, vp]),
+}
+
+_OPTIONAL = {}
+_lock = threading.Lock()
+_lib = None
+
+
+def lib():
+    """Load (once) and return the library; raise loudly if it is unusable."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"CUDA library {LIB_PATH} is missing: run "
+                "`python -m paper_1909_08723_b200.csrc.build` (there is no CPU fallback)")
+        handle = C.CDLL(LIB_PATH)
+        for name, (res, args) in list(_SIGS.items()) + list(_OPTIONAL.items()):
+            fn = getattr(handle, name, None)
+            if fn is None:
+                if name in _OPTIONAL:
+                    continue
+                raise RuntimeError(f"{LIB_PATH} does not export {name}")
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def register(name: str, restype, argtypes) -> None:
+    """Declare an additional exported symbol (used by sibling modules)."""
+    _SIGS[name] = (restype, argtypes)
+    if _lib is not None:
+        fn = getattr(_lib, name)
+        fn.restype = restype
+        fn.argtypes = argtypes
+
+
+def check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = lib().fb_last_error().decode(errors="replace")
+    if rc == 1:
+        raise ValueError(msg)
+    if rc == 2:
+        raise ConfigError(msg)
+    raise RuntimeError(f"CUDA error: {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args))
+
+
+def ptr(t) -> int:
+    """Device pointer of a torch tensor (or 0 for None)."""
+    return 0 if t is None else int(t.data_ptr())
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)

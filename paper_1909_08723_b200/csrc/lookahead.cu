@@ -1,0 +1,353 @@
+// Look-ahead word-LM fusion kernels: CSR trie gather (Eq. 4), trie advance,
+// fp64 prefix sums of word distributions.
+//
+// Reference semantics: fusion.py:118-185 (char_scores), :187-224 (advance),
+// :40-42 / :223 (cumsum_distribution).  HBM-bound integer/byte gathers; no
+// tensor-core work here.
+#include "common.cuh"
+
+namespace fb {
+
+__device__ __forceinline__ double mass(const double* __restrict__ g, int hi, int lo) {
+  // g[hi] - g[lo] with g[-1] := 0   (fusion.py:135-146)
+  double up = __ldg(g + hi);
+  double low = lo >= 0 ? __ldg(g + lo) : 0.0;
+  return dsub(up, low);
+}
+
+// One warp per hypothesis row; the row's scores are staged in shared memory
+// (penalty fill -> edge columns -> <space>/<eos>) and written out coalesced.
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+lookahead_scores_kernel(fb_trie_t trie, int n_max, const int32_t* __restrict__ n_dev,
+                        const int32_t* __restrict__ rows, const int32_t* __restrict__ tstate,
+                        const int32_t* __restrict__ hslot, const double* __restrict__ g_pool,
+                        int64_t g_stride, const double* __restrict__ hist_eos,
+                        const double* __restrict__ ext_eos, int space_id, int eos_id,
+                        double pen, double floor_v, double* __restrict__ out,
+                        int64_t out_stride, unsigned long long* floored) {
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int V = trie.alphabet;
+  double* srow = smem + warp * V;
+  const int n = row_count(n_max, n_dev);
+  unsigned nfloor = 0;
+  for (int i = blockIdx.x * WARPS + warp; i < n; i += gridDim.x * WARPS) {
+    const int r = row_at(rows, i);
+    const int s = tstate[r];
+    for (int c = lane; c < V; c += 32) srow[c] = pen;
+    __syncwarp();
+    if (s >= 0) {
+      const double* g = g_pool + (int64_t)hslot[r] * g_stride;
+      const int4 inf = reinterpret_cast<const int4*>(trie.info)[s];
+      const double denom = mass(g, inf.x, inf.y);
+      const double ldenom = log(denom);
+      const int e0 = trie.row_ptr[s], e1 = trie.row_ptr[s + 1];
+      for (int e = e0 + lane; e < e1; e += 32) {
+        const int c = trie.edge_label[e];
+        const int4 ci = reinterpret_cast<const int4*>(trie.info)[trie.edge_child[e]];
+        const double numer = mass(g, ci.x, ci.y);
+        double v;
+        if (numer > 0.0 && denom > 0.0) {
+          v = dsub(log(numer), ldenom);
+        } else {
+          v = floor_v;
+          ++nfloor;
+        }
+        srow[c] = v;
+      }
+      if (lane == 0) {
+        double wend = pen;
+        const bool fin = inf.z >= 0;
+        if (fin) {
+          const int rk = inf.z;
+          const double wm = mass(g, rk, rk - 1);
+          if (wm > 0.0 && denom > 0.0) {
+            wend = dsub(log(wm), ldenom);
+          } else {
+            wend = floor_v;
+            ++nfloor;
+          }
+        }
+        srow[space_id] = fin ? wend : pen;
+        double ecol = pen;
+        if (s == 0) {
+          ecol = hist_eos ? hist_eos[hslot[r]] : ext_eos[r];
+        } else if (fin) {
+          ecol = dadd(wend, ext_eos[r]);
+        }
+        srow[eos_id] = ecol;
+      }
+    }
+    __syncwarp();
+    double* o = out + (int64_t)r * out_stride;
+    for (int c = lane; c < V; c += 32) o[c] = srow[c];
+    __syncwarp();
+  }
+  if (floored) {
+    for (int off = 16; off; off >>= 1) nfloor += __shfl_xor_sync(0xffffffffu, nfloor, off);
+    if (lane == 0 && nfloor) atomicAdd(floored, (unsigned long long)nfloor);
+  }
+}
+
+__device__ __forceinline__ int find_child(const fb_trie_t& t, int s, int c) {
+  int lo = t.row_ptr[s], hi = t.row_ptr[s + 1] - 1;
+  while (lo <= hi) {  // labels ascend within a state
+    const int mid = (lo + hi) >> 1;
+    const int l = t.edge_label[mid];
+    if (l == c) return t.edge_child[mid];
+    if (l < c) lo = mid + 1; else hi = mid - 1;
+  }
+  return -1;
+}
+
+__global__ void trie_advance_kernel(fb_trie_t trie, int n_max, const int32_t* __restrict__ n_dev,
+                                    const int32_t* __restrict__ rows,
+                                    const int32_t* __restrict__ parent,
+                                    const int32_t* __restrict__ sin,
+                                    const int32_t* __restrict__ hin,
+                                    const int32_t* __restrict__ tokens, int space_id,
+                                    int eos_id, int pad_id, int32_t* __restrict__ sout,
+                                    int32_t* __restrict__ hout, int32_t* __restrict__ brank) {
+  const int n = row_count(n_max, n_dev);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int r = row_at(rows, i);
+    const int p = parent ? parent[r] : r;
+    const int s = sin[p];
+    const int tok = tokens[r];
+    int ns = s;
+    int rk = -2;
+    if (tok == space_id) {
+      ns = 0;
+      rk = -1;                                  // <unk> unless s is final
+      if (s >= 0) {
+        const int wr = trie.info[4 * s + 2];
+        if (wr >= 0) rk = wr;
+      }
+    } else if (tok != eos_id && tok != pad_id) {
+      int c = -1;
+      if (s >= 0) {
+        const int tc = min(max(tok, 0), trie.alphabet - 1);
+        c = find_child(trie, s, tc);
+      }
+      ns = c >= 0 ? c : -2;                     // OOV_STATE
+    }
+    sout[r] = ns;
+    if (brank) brank[r] = rk;
+    if (hout && hin) hout[r] = hin[p];
+  }
+}
+
+// ---- fp64 running sums over word-distribution rows ----------------------
+// One CTA per row, tiles of TILE elements staged in shared memory; each thread
+// scans ITEMS consecutive values, the block scans the thread totals, and the
+// carry crosses tiles.  Bandwidth-bound: 8 B read (or 4 B logits) + 8 B write
+// per word.
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ double block_exclusive_scan(double v, double* wsum, double& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double x = v;
+  for (int off = 1; off < 32; off <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= off) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    double w = lane < nw ? wsum[lane] : 0.0;
+    for (int off = 1; off < 32; off <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, w, off);
+      if (lane >= off) w += y;
+    }
+    if (lane < nw) wsum[lane] = w;
+  }
+  __syncthreads();
+  total = wsum[(blockDim.x >> 5) - 1];
+  const double before = warp ? wsum[warp - 1] : 0.0;
+  double excl = __shfl_up_sync(0xffffffffu, x, 1);
+  if (lane == 0) excl = 0.0;
+  __syncthreads();
+  return before + excl;
+}
+
+template <bool FROM_LOGITS>
+__global__ void __launch_bounds__(kScanThreads)
+row_scan_kernel(int m_max, const int32_t* __restrict__ m_dev, const void* __restrict__ src,
+                int64_t s_stride, int vw, int v_out, const int32_t* __restrict__ slots,
+                double* __restrict__ g_pool, int64_t g_stride, double* __restrict__ eos_out) {
+  __shared__ double tile[kScanTile];
+  __shared__ double wsum[32];
+  __shared__ float red_f[32];
+  __shared__ float red_g[32];
+  __shared__ double red_d[32];
+  const int m = row_count(m_max, m_dev);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int row = blockIdx.x; row < m; row += gridDim.x) {
+    double* g = g_pool + (int64_t)slots[row] * g_stride;
+    float mw = 0.f;
+    double sw = 1.0;
+    const float* lg = nullptr;
+    if constexpr (FROM_LOGITS) {
+      lg = reinterpret_cast<const float*>(src) + (int64_t)row * s_stride;
+      // pass A: max over the words and over all outputs (for </s>)
+      float mx = -INFINITY, mall = -INFINITY;
+      for (int j = threadIdx.x; j < v_out; j += blockDim.x) {
+        const float z = lg[j];
+        if (j < vw) mx = fmaxf(mx, z);
+        mall = fmaxf(mall, z);
+      }
+      for (int off = 16; off; off >>= 1) {
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        mall = fmaxf(mall, __shfl_xor_sync(0xffffffffu, mall, off));
+      }
+      if (lane == 0) { red_f[warp] = mx; red_g[warp] = mall; }
+      __syncthreads();
+      mx = -INFINITY; mall = -INFINITY;
+      for (int w = 0; w < nw; ++w) { mx = fmaxf(mx, red_f[w]); mall = fmaxf(mall, red_g[w]); }
+      mw = mx;
+      // pass B: word mass relative to the word max (fp64 accumulation)
+      double part = 0.0;
+      for (int j = threadIdx.x; j < vw; j += blockDim.x) part += (double)expf(lg[j] - mw);
+      for (int off = 16; off; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+      if (lane == 0) red_d[warp] = part;
+      __syncthreads();
+      sw = 0.0;
+      for (int w = 0; w < nw; ++w) sw += red_d[w];
+      if (threadIdx.x == 0 && eos_out) {
+        // log-softmax of </s> over all outputs: words rescaled + the specials
+        double sall = sw * exp((double)mw - (double)mall);
+        for (int j = vw; j < v_out; ++j) sall += exp((double)lg[j] - (double)mall);
+        eos_out[slots[row]] = (double)lg[vw] - ((double)mall + log(sall));
+      }
+      __syncthreads();
+    }
+    // pass: running sums tile by tile
+    double carry = 0.0;
+    for (int base = 0; base < vw; base += kScanTile) {
+      const int cnt = min(kScanTile, vw - base);
+      for (int j = threadIdx.x; j < kScanTile; j += blockDim.x) {
+        double v = 0.0;
+        if (j < cnt) {
+          if constexpr (FROM_LOGITS) v = (double)expf(lg[base + j] - mw) / sw;
+          else v = reinterpret_cast<const double*>(src)[(int64_t)row * s_stride + base + j];
+        }
+        tile[j] = v;
+      }
+      __syncthreads();
+      double loc[kScanItems];
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < kScanItems; ++k) {
+        acc += tile[threadIdx.x * kScanItems + k];
+        loc[k] = acc;
+      }
+      double total;
+      const double pre = block_exclusive_scan(acc, wsum, total) + carry;
+#pragma unroll
+      for (int k = 0; k < kScanItems; ++k) tile[threadIdx.x * kScanItems + k] = pre + loc[k];
+      __syncthreads();
+      for (int j = threadIdx.x; j < cnt; j += blockDim.x) g[base + j] = tile[j];
+      carry += total;
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void gather_rows_kernel(int n, const int32_t* __restrict__ idx, const char* __restrict__ src,
+                                   char* __restrict__ dst, int64_t row_bytes) {
+  const bool vec = (row_bytes % 16 == 0) && ((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 16 == 0);
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    const char* s = src + (int64_t)idx[r] * row_bytes;
+    char* d = dst + (int64_t)r * row_bytes;
+    if (vec) {
+      const int64_t nv = row_bytes / 16;
+      for (int64_t j = threadIdx.x; j < nv; j += blockDim.x)
+        reinterpret_cast<int4*>(d)[j] = reinterpret_cast<const int4*>(s)[j];
+    } else {
+      for (int64_t j = threadIdx.x; j < row_bytes; j += blockDim.x) d[j] = s[j];
+    }
+  }
+}
+
+}  // namespace fb
+
+using namespace fb;
+
+extern "C" int fb_lookahead_scores(const fb_trie_t* trie, int32_t n_max, const int32_t* n_dev,
+                                   const int32_t* rows, const int32_t* trie_state,
+                                   const int32_t* hist_slot, const double* g_pool,
+                                   int64_t g_stride, const double* hist_eos,
+                                   const double* ext_eos, int32_t space_id, int32_t eos_id,
+                                   double oov_penalty, double score_floor, double* out,
+                                   int64_t out_stride, unsigned long long* floored,
+                                   void* stream) {
+  FB_CHECK_ARG(trie && trie->row_ptr && trie->info, "trie is null");
+  FB_CHECK_ARG(n_max >= 0, "negative row count");
+  FB_CHECK_ARG(out_stride >= trie->alphabet, "out stride smaller than the alphabet");
+  FB_CHECK_ARG(hist_eos || ext_eos, "need hist_eos or ext_eos");
+  if (n_max == 0) return FB_OK;
+  constexpr int W = 8;
+  const int blocks = std::min((n_max + W - 1) / W, kNumSMs * 16);
+  const size_t sm = sizeof(double) * W * trie->alphabet;
+  lookahead_scores_kernel<W><<<blocks, W * 32, sm, (cudaStream_t)stream>>>(
+      *trie, n_max, n_dev, rows, trie_state, hist_slot, g_pool, g_stride, hist_eos, ext_eos,
+      space_id, eos_id, oov_penalty, score_floor, out, out_stride, floored);
+  count_launch();
+  return check_launch("lookahead_scores");
+}
+
+extern "C" int fb_trie_advance(const fb_trie_t* trie, int32_t n_max, const int32_t* n_dev,
+                               const int32_t* rows, const int32_t* parent,
+                               const int32_t* state_in, const int32_t* hist_in,
+                               const int32_t* tokens, int32_t space_id, int32_t eos_id,
+                               int32_t pad_id, int32_t* state_out, int32_t* hist_out,
+                               int32_t* boundary_rank, void* stream) {
+  FB_CHECK_ARG(trie && trie->row_ptr, "trie is null");
+  if (n_max <= 0) return FB_OK;
+  const int threads = 256;
+  const int blocks = std::min((n_max + threads - 1) / threads, kNumSMs * 8);
+  trie_advance_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
+      *trie, n_max, n_dev, rows, parent, state_in, hist_in, tokens, space_id, eos_id, pad_id,
+      state_out, hist_out, boundary_rank);
+  count_launch();
+  return check_launch("trie_advance");
+}
+
+extern "C" int fb_cumsum_rows(int32_t m, const double* probs, int64_t p_stride, int32_t vw,
+                              const int32_t* slots, double* g_pool, int64_t g_stride,
+                              void* stream) {
+  FB_CHECK_ARG(vw > 0 && p_stride >= vw && g_stride >= vw, "bad cumsum sizes");
+  if (m <= 0) return FB_OK;
+  const int blocks = std::min(m, kNumSMs * 4);
+  row_scan_kernel<false><<<blocks, kScanThreads, 0, (cudaStream_t)stream>>>(
+      m, nullptr, probs, p_stride, vw, vw, slots, g_pool, g_stride, nullptr);
+  count_launch();
+  return check_launch("cumsum_rows");
+}
+
+extern "C" int fb_logits_to_g(int32_t m_max, const int32_t* m_dev, const float* logits,
+                              int64_t l_stride, int32_t vw, int32_t v_out, const int32_t* slots,
+                              double* g_pool, int64_t g_stride, double* eos_out, void* stream) {
+  FB_CHECK_ARG(vw > 0 && v_out > vw && l_stride >= v_out && g_stride >= vw, "bad logits sizes");
+  if (m_max <= 0) return FB_OK;
+  const int blocks = std::min(m_max, kNumSMs * 4);
+  row_scan_kernel<true><<<blocks, kScanThreads, 0, (cudaStream_t)stream>>>(
+      m_max, m_dev, logits, l_stride, vw, v_out, slots, g_pool, g_stride, eos_out);
+  count_launch();
+  return check_launch("logits_to_g");
+}
+
+extern "C" int fb_gather_rows(int32_t n, const int32_t* idx, const void* src, void* dst,
+                              int64_t row_bytes, void* stream) {
+  FB_CHECK_ARG(row_bytes > 0, "bad row size");
+  if (n <= 0) return FB_OK;
+  const int blocks = std::min(n, kNumSMs * 8);
+  gather_rows_kernel<<<blocks, 128, 0, (cudaStream_t)stream>>>(
+      n, idx, (const char*)src, (char*)dst, row_bytes);
+  count_launch();
+  return check_launch("gather_rows");
+}

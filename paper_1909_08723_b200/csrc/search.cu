@@ -1,0 +1,495 @@
+// Beam-search step kernels: score combine + EOS gate + token-major stable
+// top-beam + coverage bonus + finished-set cap + early stop + result pick, and
+// the attention-accumulator / coverage update.
+//
+// Reference semantics: decoder.py:339-480 (loop body :382-456), coverage
+// decoder.py:36-48, gate :396-398, finished key :322-323.  All score arithmetic
+// is IEEE float64 without FMA contraction so results equal numpy's.
+#include "common.cuh"
+
+#include <algorithm>
+
+namespace fb {
+
+constexpr int kSelThreads = 256;
+
+// numpy's pairwise summation (loops_utils.h pairwise_sum, PW_BLOCKSIZE 128)
+// over f(a[i]); reproduces np.sum bit-for-bit for contiguous float64.
+template <typename F>
+__device__ double pairwise_sum(const double* a, int n, F f) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) res = dadd(res, f(a[i]));
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = f(a[j]);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = dadd(r[j], f(a[i + j]));
+    }
+    double res = dadd(dadd(dadd(r[0], r[1]), dadd(r[2], r[3])),
+                      dadd(dadd(r[4], r[5]), dadd(r[6], r[7])));
+    for (; i < n; ++i) res = dadd(res, f(a[i]));
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return dadd(pairwise_sum(a, n2, f), pairwise_sum(a + n2, n - n2, f));
+}
+
+__device__ __forceinline__ double coverage_of(const fb_search_cfg_t& c, const double* acc, int T,
+                                              int count_above_tau1) {
+  if (c.cov_mode == 1) return (double)count_above_tau1;
+  const double tau2 = c.tau2, mg = c.cov_margin;
+  const double pen = pairwise_sum(acc, T, [=](double x) {
+    return x > tau2 ? dsub(dadd(mg, x), tau2) : 0.0;
+  });
+  return dsub((double)count_above_tau1, pen);
+}
+
+// acc_out[r] = acc_in[parent[r]] + attn[r]; cov_out[r] = coverage(acc_out[r]).
+template <typename AT>
+__global__ void attend_coverage_kernel(fb_search_cfg_t cfg, int n_max, const int32_t* n_dev,
+                                       const int32_t* rows, const int32_t* parent,
+                                       const int32_t* t_enc, const double* acc_in,
+                                       const AT* attn, int64_t attn_stride, double* acc_out,
+                                       double* cov_out) {
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  const int n = row_count(n_max, n_dev);
+  for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < n; i += gridDim.x * wpb) {
+    const int r = row_at(rows, i);
+    const int p = parent ? parent[r] : r;
+    const int T = t_enc[r / cfg.beam];
+    const double* a0 = acc_in + (int64_t)p * cfg.t_max;
+    const AT* at = attn + (int64_t)r * attn_stride;
+    double* a1 = acc_out + (int64_t)r * cfg.t_max;
+    int cnt = 0;
+    for (int k = lane; k < T; k += 32) {
+      const double v = dadd(a0[k], (double)at[k]);
+      a1[k] = v;
+      cnt += v > cfg.tau1;
+    }
+    if (cfg.cov_mode != 0) {
+      for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+      __syncwarp();
+      if (lane == 0) cov_out[r] = coverage_of(cfg, a1, T, cnt);
+    }
+    __syncwarp();
+  }
+}
+
+struct Cand {
+  double s;
+  int j;  // flat token-major index; INT_MAX = none
+};
+
+__device__ __forceinline__ bool better(const Cand& a, const Cand& b) {
+  if (b.j == INT_MAX) return a.j != INT_MAX;
+  if (a.j == INT_MAX) return false;
+  return a.s > b.s || (a.s == b.s && a.j < b.j);
+}
+
+__device__ __forceinline__ Cand warp_best(Cand c) {
+  for (int off = 16; off; off >>= 1) {
+    Cand o;
+    o.s = __shfl_xor_sync(0xffffffffu, c.s, off);
+    o.j = __shfl_xor_sync(0xffffffffu, c.j, off);
+    if (better(o, c)) c = o;
+  }
+  return c;
+}
+
+// Lexicographic compare of two token rows of equal length L: -1, 0, 1.
+__device__ __forceinline__ int lex_cmp(const int32_t* a, const int32_t* b, int L) {
+  for (int i = 0; i < L; ++i) {
+    if (a[i] != b[i]) return a[i] < b[i] ? -1 : 1;
+  }
+  return 0;
+}
+
+// (-total, len, tokens) ordering of decoder.py:322-323: true if a sorts first.
+__device__ __forceinline__ bool key_less(double ta, int la, const int32_t* ka, double tb, int lb,
+                                         const int32_t* kb) {
+  if (ta != tb) return ta > tb;
+  if (la != lb) return la < lb;
+  return lex_cmp(ka, kb, la) < 0;
+}
+
+template <typename AM>
+__device__ __forceinline__ double step_score(const fb_search_cfg_t& c, const AM* am,
+                                             int64_t am_stride, const double* fus,
+                                             int64_t f_stride, int slot, int t, bool gated) {
+  if (t == c.pad_id) return -INFINITY;
+  if (t == c.eos_id && gated) return -INFINITY;
+  double s = (double)am[(int64_t)slot * am_stride + t];
+  if (c.has_fusion) s = dadd(s, dmul(c.lm_weight, fus[(int64_t)slot * f_stride + t]));
+  return s;
+}
+
+struct SelPlan {
+  int n_sel;
+  int n_new;
+  int fin_new[64];      // finished-pool index per selected eos child (or -1)
+};
+
+template <typename AM>
+__global__ void __launch_bounds__(kSelThreads)
+search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict__ am,
+                   int64_t am_stride, const double* __restrict__ fus, int64_t f_stride) {
+  extern __shared__ unsigned char sm_raw[];
+  const int u = blockIdx.x;
+  if (!st.active[u]) return;
+  const int K = c.beam, V = c.vocab;
+  const int n = st.n_live[u];
+  const int base = u * K;
+  const int steps = st.steps[u];
+  const int MT = c.max_tokens;
+  const int NV = n * V;
+
+  double* cand = reinterpret_cast<double*>(sm_raw);                    // [NV]
+  unsigned char* taken = sm_raw + sizeof(double) * NV;                 // [NV]
+  __shared__ int gated[64];
+  __shared__ int sel[64];
+  __shared__ Cand wbest[kSelThreads / 32];
+  __shared__ int s_nsel, s_stop;
+  // new-row plan
+  __shared__ int new_par[64], new_tok[64];
+  __shared__ double new_base[64], new_total[64];
+  __shared__ int fin_slot[64], fin_par[64];
+  __shared__ int n_new, n_fin_new;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // EOS gate per parent (decoder.py:396-398), compared in the AM row dtype.
+  if (c.gate_on) {
+    for (int p = warp; p < n; p += kSelThreads / 32) {
+      const AM* row = am + (int64_t)(base + p) * am_stride;
+      AM mx = row[0];
+      for (int t = lane; t < V; t += 32) mx = row[t] > mx ? row[t] : mx;
+      for (int off = 16; off; off >>= 1) {
+        const AM o = __shfl_xor_sync(0xffffffffu, mx, off);
+        mx = o > mx ? o : mx;
+      }
+      if (lane == 0) gated[p] = row[c.eos_id] <= (AM)c.gamma * mx;
+    }
+  } else if (tid < 64) {
+    gated[tid] = 0;
+  }
+  __syncthreads();
+
+  // candidates, token-major flat index j = t * n + p (decoder.py:404)
+  for (int j = tid; j < NV; j += kSelThreads) {
+    const int t = j / n, p = j % n;
+    const double s = step_score(c, am, am_stride, fus, f_stride, base + p, t, gated[p]);
+    cand[j] = dadd(st.total_in[base + p], s);
+    taken[j] = 0;
+  }
+  if (tid == 0) s_nsel = 0, s_stop = 0;
+  __syncthreads();
+
+  // K rounds of block argmax == the first K entries of argsort(-flat, stable)
+  for (int k = 0; k < K; ++k) {
+    Cand b{-INFINITY, INT_MAX};
+    for (int j = tid; j < NV; j += kSelThreads) {
+      if (!taken[j]) {
+        Cand x{cand[j], j};
+        if (better(x, b)) b = x;
+      }
+    }
+    b = warp_best(b);
+    if (lane == 0) wbest[warp] = b;
+    __syncthreads();
+    if (tid == 0) {
+      Cand w = wbest[0];
+      for (int q = 1; q < kSelThreads / 32; ++q)
+        if (better(wbest[q], w)) w = wbest[q];
+      if (w.j == INT_MAX || w.s == -INFINITY) {
+        s_stop = 1;
+      } else {
+        sel[s_nsel++] = w.j;
+        taken[w.j] = 1;
+      }
+    }
+    __syncthreads();
+    if (s_stop) break;
+  }
+
+  // plan children in selection order (decoder.py:410-432)
+  if (tid == 0) {
+    int nn = 0, nf = 0;
+    const bool cov_on = c.cov_mode != 0;
+    const int cap = 2 * K;
+    int free_slot = 0;
+    for (int k = 0; k < s_nsel; ++k) {
+      const int j = sel[k];
+      const int t = j / n, p = j % n;
+      const int ps = base + p;
+      const double s = step_score(c, am, am_stride, fus, f_stride, ps, t, gated[p]);
+      const double nb = dadd(st.base_in[ps], s);
+      const double tt = cov_on ? dadd(nb, dmul(c.cov_weight, st.cov_post[ps])) : nb;
+      if (t == c.eos_id) {
+        while (free_slot < cap && st.fin_valid[u * cap + free_slot]) ++free_slot;
+        const int f = free_slot++;
+        st.fin_valid[u * cap + f] = 1;
+        st.fin_total[u * cap + f] = tt;
+        st.fin_len[u * cap + f] = steps + 1;
+        fin_slot[nf] = f;
+        fin_par[nf] = ps;
+        ++nf;
+      } else {
+        new_par[nn] = ps;
+        new_tok[nn] = t;
+        new_base[nn] = nb;
+        new_total[nn] = tt;
+        ++nn;
+      }
+    }
+    n_new = nn;
+    n_fin_new = nf;
+  }
+  __syncthreads();
+
+  // token rows and accumulators (parallel copies)
+  for (int i = 0; i < n_new; ++i) {
+    const int32_t* src = st.tok_in + (int64_t)new_par[i] * MT;
+    int32_t* dst = st.tok_out + (int64_t)(base + i) * MT;
+    for (int q = tid; q < steps; q += kSelThreads) dst[q] = src[q];
+    if (tid == 0) {
+      dst[steps] = new_tok[i];
+      st.base_out[base + i] = new_base[i];
+      st.total_out[base + i] = new_total[i];
+      st.parent[base + i] = new_par[i];
+      st.last_tok[base + i] = new_tok[i];
+    }
+  }
+  const int T = st.t_enc[u];
+  for (int i = 0; i < n_fin_new; ++i) {
+    const int f = fin_slot[i];
+    const int64_t fe = (int64_t)u * 2 * K + f;
+    const int32_t* src = st.tok_in + (int64_t)fin_par[i] * MT;
+    int32_t* dst = st.fin_tokens + fe * MT;
+    for (int q = tid; q < steps; q += kSelThreads) dst[q] = src[q];
+    if (tid == 0) dst[steps] = c.eos_id;
+    const double* as = st.acc_post + (int64_t)fin_par[i] * c.t_max;
+    double* ad = st.fin_acc + fe * c.t_max;
+    for (int q = tid; q < T; q += kSelThreads) ad[q] = as[q];
+  }
+  __syncthreads();
+
+  // finished-set cap, stop tests, result pick (decoder.py:433-450, :464-480)
+  __shared__ int res_src, res_is_fin, res_L;
+  if (tid == 0) {
+    const int cap = 2 * K;
+    int* fv = st.fin_valid + u * cap;
+    const double* ft = st.fin_total + u * cap;
+    const int* fl = st.fin_len + u * cap;
+    const int32_t* fk = st.fin_tokens + (int64_t)u * cap * MT;
+    int cnt = 0;
+    for (int f = 0; f < cap; ++f) cnt += fv[f];
+    while (cnt > K) {  // drop the entry that sorts last
+      int worst = -1;
+      for (int f = 0; f < cap; ++f) {
+        if (!fv[f]) continue;
+        if (worst < 0 || key_less(ft[worst], fl[worst], fk + (int64_t)worst * MT, ft[f], fl[f],
+                                  fk + (int64_t)f * MT))
+          worst = f;
+      }
+      fv[worst] = 0;
+      --cnt;
+    }
+    const int steps1 = steps + 1;
+    st.steps[u] = steps1;
+    st.n_live[u] = n_new;
+    bool on = true;
+    if (n_new == 0 || steps1 >= st.max_len[u]) {
+      on = false;
+    } else if (cnt > 0 && c.early_stop) {
+      const double slack = c.cov_mode != 0 ? dmul(c.cov_weight, (double)T) : 0.0;
+      double best = new_base[0];
+      for (int i = 1; i < n_new; ++i) best = fmax(best, new_base[i]);
+      best = dadd(best, slack);
+      double worst = INFINITY;
+      for (int f = 0; f < cap; ++f)
+        if (fv[f]) worst = fmin(worst, ft[f]);
+      if (best < worst) on = false;
+    }
+    st.active[u] = on ? 1 : 0;
+    res_src = -1;
+    if (!on) {
+      if (cnt > 0) {
+        int b = -1;
+        for (int f = 0; f < cap; ++f) {
+          if (!fv[f]) continue;
+          if (b < 0 || key_less(ft[f], fl[f], fk + (int64_t)f * MT, ft[b], fl[b],
+                                fk + (int64_t)b * MT))
+            b = f;
+        }
+        res_src = b;
+        res_is_fin = 1;
+        res_L = fl[b];
+        st.res_score[u] = ft[b];
+      } else if (n_new > 0) {
+        int b = 0;
+        for (int i = 1; i < n_new; ++i) {
+          if (key_less(new_total[i], steps1, st.tok_out + (int64_t)(base + i) * MT,
+                       new_total[b], steps1, st.tok_out + (int64_t)(base + b) * MT))
+            b = i;
+        }
+        res_src = b;
+        res_is_fin = 0;
+        res_L = steps1;
+        st.res_score[u] = new_total[b];
+      }
+      st.res_finished[u] = cnt > 0;
+      st.res_steps[u] = steps1;
+      st.res_len[u] = -1;  // "no hypotheses survived" unless set below
+    }
+  }
+  __syncthreads();
+  if (res_src >= 0) {
+    const int32_t* src;
+    const double* asrc;
+    if (res_is_fin) {
+      const int64_t fe = (int64_t)u * 2 * K + res_src;
+      src = st.fin_tokens + fe * MT;
+      asrc = st.fin_acc + fe * c.t_max;
+    } else {
+      src = st.tok_out + (int64_t)(base + res_src) * MT;
+      asrc = st.acc_post + (int64_t)new_par[res_src] * c.t_max;
+    }
+    int L = res_L;
+    if (L > 0 && src[L - 1] == c.eos_id) --L;   // strip trailing <eos>
+    int32_t* dst = st.res_tokens + (int64_t)u * MT;
+    for (int q = tid; q < L; q += kSelThreads) dst[q] = src[q];
+    double* ad = st.res_acc + (int64_t)u * c.t_max;
+    for (int q = tid; q < T; q += kSelThreads) ad[q] = asrc[q];
+    if (tid == 0) st.res_len[u] = L;
+  }
+}
+
+// Deterministic compact list of rows that enter the next step.
+__global__ void compact_rows_kernel(int B, int K, const int32_t* active, const int32_t* n_live,
+                                    int32_t* rows, int32_t* count) {
+  __shared__ int wsum[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int b0 = 0; b0 < B; b0 += blockDim.x) {
+    const int u = b0 + threadIdx.x;
+    const int c = (u < B && active[u]) ? n_live[u] : 0;
+    int x = c;
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, off);
+        if (lane >= off) w += y;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    const int pos = carry + (warp ? wsum[warp - 1] : 0) + x - c;
+    for (int i = 0; i < c; ++i) rows[pos + i] = u * K + i;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += wsum[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = carry;
+}
+
+__global__ void search_init_kernel(fb_search_cfg_t c, fb_search_state_t st, int B) {
+  const int K = c.beam;
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < B; u += gridDim.x * blockDim.x) {
+    st.active[u] = 1;
+    st.n_live[u] = 1;
+    st.steps[u] = 0;
+    st.res_len[u] = -1;
+    for (int f = 0; f < 2 * K; ++f) st.fin_valid[u * 2 * K + f] = 0;
+    // entering-step row of the first step (decoder.py:358)
+    const_cast<double*>(st.base_in)[u * K] = 0.0;
+    const_cast<double*>(st.total_in)[u * K] = 0.0;
+    st.parent[u * K] = u * K;
+    st.last_tok[u * K] = -1;
+    st.next_rows[u] = u * K;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *st.next_count = B;
+}
+
+}  // namespace fb
+
+using namespace fb;
+
+extern "C" int fb_search_init(const fb_search_cfg_t* cfg, const fb_search_state_t* st,
+                              int32_t num_utts, void* stream) {
+  FB_CHECK_ARG(cfg && st && num_utts >= 0, "null search state");
+  if (num_utts == 0) return FB_OK;
+  search_init_kernel<<<std::min((num_utts + 255) / 256, kNumSMs), 256, 0,
+                       (cudaStream_t)stream>>>(*cfg, *st, num_utts);
+  count_launch();
+  return check_launch("search_init");
+}
+
+extern "C" int fb_attend_coverage(const fb_search_cfg_t* cfg, int32_t n_max, const int32_t* n_dev,
+                                  const int32_t* rows, const int32_t* parent,
+                                  const int32_t* t_enc, const double* acc_in, const void* attn,
+                                  int32_t attn_f32, int64_t attn_stride, double* acc_out,
+                                  double* cov_out, void* stream) {
+  FB_CHECK_ARG(cfg && acc_in && attn && acc_out, "null accumulator buffers");
+  FB_CHECK_ARG(cfg->cov_mode == 0 || cov_out, "coverage output required");
+  if (n_max <= 0) return FB_OK;
+  const int threads = 256;
+  const int blocks = std::min((n_max + 7) / 8, kNumSMs * 8);
+  if (attn_f32)
+    attend_coverage_kernel<float><<<blocks, threads, 0, (cudaStream_t)stream>>>(
+        *cfg, n_max, n_dev, rows, parent, t_enc, acc_in, (const float*)attn, attn_stride,
+        acc_out, cov_out);
+  else
+    attend_coverage_kernel<double><<<blocks, threads, 0, (cudaStream_t)stream>>>(
+        *cfg, n_max, n_dev, rows, parent, t_enc, acc_in, (const double*)attn, attn_stride,
+        acc_out, cov_out);
+  count_launch();
+  return check_launch("attend_coverage");
+}
+
+extern "C" int fb_search_step(const fb_search_cfg_t* cfg, const fb_search_state_t* st,
+                              int32_t num_utts, const void* am, int64_t am_stride,
+                              const double* fusion, int64_t fusion_stride, void* stream) {
+  FB_CHECK_ARG(cfg && st && am, "null search arguments");
+  FB_CHECK_ARG(cfg->beam >= 1 && cfg->beam <= 64, "beam must be in [1, 64] on this path");
+  FB_CHECK_ARG(!cfg->has_fusion || fusion, "fusion rows required");
+  const int64_t nv = (int64_t)cfg->beam * cfg->vocab;
+  const size_t smem = (size_t)nv * (sizeof(double) + 1);
+  if (smem > 200 * 1024)
+    return fail(FB_ERR_CONFIG, "beam x vocabulary too large for the shared-memory top-k");
+  if (num_utts <= 0) return FB_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cfg->am_f32) {
+    auto k = search_step_kernel<float>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<num_utts, kSelThreads, smem, s>>>(*cfg, *st, (const float*)am, am_stride, fusion,
+                                          fusion_stride);
+  } else {
+    auto k = search_step_kernel<double>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<num_utts, kSelThreads, smem, s>>>(*cfg, *st, (const double*)am, am_stride, fusion,
+                                          fusion_stride);
+  }
+  count_launch();
+  int rc = check_launch("search_step");
+  if (rc) return rc;
+  compact_rows_kernel<<<1, 1024, 0, s>>>(num_utts, cfg->beam, st->active, st->n_live,
+                                         st->next_rows, st->next_count);
+  count_launch();
+  return check_launch("compact_rows");
+}
