@@ -82,12 +82,14 @@ int fb_trie_advance(const fb_trie_t* trie, int32_t n_max, const int32_t* n_dev,
 int fb_cumsum_rows(int32_t m, const double* probs, int64_t p_stride, int32_t vw,
                    const int32_t* slots, double* g_pool, int64_t g_stride, void* stream);
 
-/* Word-LM logits -> look-ahead mass (word_lm.py:169-179 for an LSTM LM):
- * g_pool[slots[m]] = cumsum(softmax(logits[m, :vw])) in fp64 and
- * eos_out[slots[m]] = logits[m, vw] - logsumexp(logits[m, :v_out]). */
+/* Word-LM logits -> look-ahead mass (word_lm.py:169-179 for an LSTM LM).
+ * For row i < m: logits row src_rows ? src_rows[i] : i, destination
+ * d = slots ? slots[i] : i.  If g_pool: g_pool[d] = cumsum(softmax(logits[:vw]))
+ * in fp64; if eos_out: eos_out[d] = logits[vw] - logsumexp(logits[:v_out]). */
 int fb_logits_to_g(int32_t m_max, const int32_t* m_dev, const float* logits,
-                   int64_t l_stride, int32_t vw, int32_t v_out, const int32_t* slots,
-                   double* g_pool, int64_t g_stride, double* eos_out, void* stream);
+                   int64_t l_stride, const int32_t* src_rows, int32_t vw, int32_t v_out,
+                   const int32_t* slots, double* g_pool, int64_t g_stride, double* eos_out,
+                   void* stream);
 
 /* ---- beam search step (decoder.py:339-480) ------------------------------ */
 typedef struct {
@@ -130,8 +132,6 @@ typedef struct {
   double* res_acc;        /* [B][t_max]      */
   /* compact list of the rows that enter the NEXT step (active utterances) */
   int32_t* next_rows; int32_t* next_count;
-  /* per-utterance decision margin (see oracle/search.py), may be NULL */
-  double* margin;
 } fb_search_state_t;
 
 /* One lock-step selection over every active utterance: combine am + lm_weight
@@ -154,6 +154,105 @@ int fb_attend_coverage(const fb_search_cfg_t* cfg, int32_t n_max, const int32_t*
  * utterance, decoder.py:350-359). */
 int fb_search_init(const fb_search_cfg_t* cfg, const fb_search_state_t* st,
                    int32_t num_utts, void* stream);
+
+
+/* ---- dense contractions (attention-LSTM decoder step, word-LM step) ------ */
+/* C = A . W^T (+ bias) with a fused epilogue.  A [m, k] fp32 row-major
+ * (compact rows), W [n, k] row-major.
+ *   mode 0: out row = rows ? rows[i] : i ;  c[out*ldc + j] = acc + bias[j]
+ *   mode 1: LSTM cell.  n == 4*hidden with gate columns interleaved
+ *           (column 4u+q, q = i,f,g,o); slot = rows ? rows[i] : i,
+ *           p = parent ? parent[slot] : slot;
+ *           gates += addend[i*ld_add + ..] (if addend);
+ *           c = sig(f)*c_in[p] + sig(i)*tanh(g); h = sig(o)*tanh(c)
+ *           (+ h_res[slot] if h_res);  c_out[slot], h_out[slot]. */
+typedef struct {
+  int32_t m_max;
+  const int32_t* m_dev;
+  int32_t n, k;
+  const void* a; int64_t lda;
+  const void* w; int64_t ldw;
+  const float* bias;
+  float* c; int64_t ldc;
+  int32_t mode;
+  int32_t hidden;
+  const int32_t* rows;
+  const int32_t* parent;
+  const float* c_in; int64_t ld_cin;
+  float* c_out; int64_t ld_cout;
+  float* h_out; int64_t ld_h;
+  const float* h_res; int64_t ld_res;
+  const float* addend; int64_t ld_add;
+} fb_gemm_t;
+
+int fb_gemm(const fb_gemm_t* g, void* stream);
+
+/* Row gather-concatenate into a GEMM A operand:
+ *   out[i, :] = [seg0 | seg1 | ... | zero pad up to k_pad], i < m.
+ * Segment source row: mode 0 -> i, 1 -> slot = rows[i], 2 -> parent[slot],
+ * 3 -> token id tokens[slot] (negative -> tok_default) for embeddings,
+ * 4 -> rank from ranks[i] (negative -> tok_default). */
+typedef struct {
+  const float* src; int64_t ld; int32_t width; int32_t mode;
+} fb_seg_t;
+typedef struct {
+  fb_seg_t seg[4];
+  int32_t nseg;
+  int32_t k_pad;
+  int32_t tok_default;
+  int32_t pad0;
+} fb_pack_t;
+
+int fb_pack_rows(const fb_pack_t* p, int32_t m_max, const int32_t* m_dev, const int32_t* rows,
+                 const int32_t* parent, const int32_t* tokens, const int32_t* ranks,
+                 float* out, int64_t ld_out, void* stream);
+
+/* Row log-softmax of x[slot, :n] into out[slot, :n] (slot = rows[i]). */
+int fb_log_softmax_rows(int32_t m_max, const int32_t* m_dev, const int32_t* rows,
+                        const float* x, int64_t ldx, int32_t n, float* out, int64_t ldo,
+                        void* stream);
+
+/* Bahdanau attention step for every active utterance:
+ * e[r,t] = v . tanh(keys[u,t] + q[r]); a = softmax_t(e) over t < t_enc[u];
+ * ctx[r] = sum_t a[r,t] enc[u,t]; acc_out[r] = acc_in[parent[r]] + a[r]
+ * (fp64) and its coverage (cfg->cov_mode).  Rows r = u*beam + i, i < n_live[u]. */
+int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts, const int32_t* active,
+                      const int32_t* n_live, const int32_t* t_enc, const float* keys,
+                      const float* enc, int32_t att_dim, int32_t ctx_dim, const float* v,
+                      const float* q, int64_t ldq, const int32_t* parent, const double* acc_in,
+                      double* acc_out, double* cov_out, float* ctx_out, int64_t ld_ctx,
+                      float* attn_out, int64_t ld_attn, void* stream);
+
+/* ---- word-LM bookkeeping for the fused engine ---------------------------- */
+/* Speculative <eos> events (fusion.py:181-183): for every listed row whose
+ * trie state is final: e = next event index; ev_row[e] = row, ev_rank[e] =
+ * word rank, ev_slot[e] = hist_slot[row] (LM state to extend), row_ev[row] = e;
+ * other rows get row_ev = -1.  *ev_count is reset first. */
+int fb_spec_events(const fb_trie_t* trie, int32_t n_max, const int32_t* n_dev,
+                   const int32_t* rows, const int32_t* trie_state, const int32_t* hist_slot,
+                   int32_t* ev_row, int32_t* ev_rank, int32_t* ev_slot, int32_t* ev_count,
+                   int32_t* row_ev, void* stream);
+
+/* Word-boundary plan after selection (fusion.py:206-223).  New rows
+ * rows[i] (i < *n_dev) whose boundary_rank >= -1 closed a word: each gets a
+ * fresh history slot (slots referenced by the rows that entered this step,
+ * cur_rows/hist_cur, stay live), in row order.  Entry b: bnd_slot[b] = slot,
+ * bnd_src[b] = event row holding its LM state and logits = row_ev[parent]
+ * for a final parent state, else unk_base + k for the k-th <unk> event, whose
+ * LM input state is unk_slot[k] = hist_cur[parent].  hist_next[row] = slot.
+ * slot_mark is scratch of 2*num_slots int32. */
+int fb_boundary_plan(int32_t n_max, const int32_t* n_dev, const int32_t* rows,
+                     const int32_t* parent, const int32_t* boundary_rank,
+                     const int32_t* row_ev, const int32_t* cur_rows, const int32_t* cur_count,
+                     const int32_t* hist_cur, int32_t* hist_next, int32_t num_slots,
+                     int32_t* slot_mark, int32_t* bnd_slot, int32_t* bnd_src,
+                     int32_t* bnd_count, int32_t* unk_slot, int32_t* unk_count,
+                     int32_t unk_base, void* stream);
+
+/* Copy n rows of row_bytes: dst[dst_idx[i]] = src[src_idx[i]] (NULL = i). */
+int fb_copy_rows(int32_t n_max, const int32_t* n_dev, const int32_t* src_idx,
+                 const int32_t* dst_idx, const void* src, void* dst, int64_t row_bytes,
+                 void* stream);
 
 /* Row gather (the reorder of fusion.py:226-233 / an AcousticScorer): for r <
  * n: dst[r*row_bytes..] = src[idx[r]*row_bytes..]. */

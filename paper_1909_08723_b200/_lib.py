@@ -43,9 +43,22 @@ class FbSearchState(C.Structure):
         "next_rows", "next_count")]
 
 
-class FbLstmLayer(C.Structure):
-    _fields_ = [("w", vp), ("bias", vp), ("k_in", i32), ("k_pad", i32), ("hidden", i32),
-                ("residual", i32)]
+class FbGemm(C.Structure):
+    _fields_ = [("m_max", i32), ("m_dev", vp), ("n", i32), ("k", i32),
+                ("a", vp), ("lda", i64), ("w", vp), ("ldw", i64), ("bias", vp),
+                ("c", vp), ("ldc", i64), ("mode", i32), ("hidden", i32),
+                ("rows", vp), ("parent", vp), ("c_in", vp), ("ld_cin", i64),
+                ("c_out", vp), ("ld_cout", i64), ("h_out", vp), ("ld_h", i64),
+                ("h_res", vp), ("ld_res", i64), ("addend", vp), ("ld_add", i64)]
+
+
+class FbSeg(C.Structure):
+    _fields_ = [("src", vp), ("ld", i64), ("width", i32), ("mode", i32)]
+
+
+class FbPack(C.Structure):
+    _fields_ = [("seg", FbSeg * 4), ("nseg", i32), ("k_pad", i32), ("tok_default", i32),
+                ("pad0", i32)]
 
 
 _SIGS = {
@@ -58,13 +71,23 @@ _SIGS = {
     "fb_trie_advance": (C.c_int, [C.POINTER(FbTrie), i32, vp, vp, vp, vp, vp, vp, i32, i32, i32,
                                   vp, vp, vp, vp]),
     "fb_cumsum_rows": (C.c_int, [i32, vp, i64, i32, vp, vp, i64, vp]),
-    "fb_logits_to_g": (C.c_int, [i32, vp, vp, i64, i32, i32, vp, vp, i64, vp, vp]),
+    "fb_logits_to_g": (C.c_int, [i32, vp, vp, i64, vp, i32, i32, vp, vp, i64, vp, vp]),
     "fb_search_init": (C.c_int, [C.POINTER(FbSearchCfg), C.POINTER(FbSearchState), i32, vp]),
     "fb_search_step": (C.c_int, [C.POINTER(FbSearchCfg), C.POINTER(FbSearchState), i32, vp, i64,
                                  vp, i64, vp]),
     "fb_attend_coverage": (C.c_int, [C.POINTER(FbSearchCfg), i32, vp, vp, vp, vp, vp, vp, i32,
                                      i64, vp, vp, vp]),
     "fb_gather_rows": (C.c_int, [i32, vp, vp, vp, i64, vp]),
+    "fb_gemm": (C.c_int, [C.POINTER(FbGemm), vp]),
+    "fb_pack_rows": (C.c_int, [C.POINTER(FbPack), i32, vp, vp, vp, vp, vp, vp, i64, vp]),
+    "fb_log_softmax_rows": (C.c_int, [i32, vp, vp, vp, i64, i32, vp, i64, vp]),
+    "fb_attention_step": (C.c_int, [C.POINTER(FbSearchCfg), i32, vp, vp, vp, vp, vp, i32, i32,
+                                    vp, vp, i64, vp, vp, vp, vp, vp, i64, vp, i64, vp]),
+    "fb_spec_events": (C.c_int, [C.POINTER(FbTrie), i32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                 vp]),
+    "fb_boundary_plan": (C.c_int, [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp,
+                                   vp, vp, i32, vp]),
+    "fb_copy_rows": (C.c_int, [i32, vp, vp, vp, vp, vp, i64, vp]),
 }
 
 _OPTIONAL = {}

@@ -1,0 +1,455 @@
+// Attention-LSTM decoder step pieces (operand packing, Bahdanau attention with
+// the fp64 attention accumulator + coverage, row log-softmax) and the word-LM
+// bookkeeping of the fused engine (speculative <eos> events, word-boundary
+// slot plan, row copies).
+//
+// Model equations: DESIGN.md §3; search semantics:
+// decoder.py:419-425 (accumulator), fusion.py:177-223 (LM events).
+#include "common.cuh"
+
+namespace fb {
+
+// ---------------------------------------------------------------- packing --
+__global__ void pack_rows_kernel(fb_pack_t p, int m_max, const int32_t* __restrict__ m_dev,
+                                 const int32_t* __restrict__ rows,
+                                 const int32_t* __restrict__ parent,
+                                 const int32_t* __restrict__ tokens,
+                                 const int32_t* __restrict__ ranks, float* __restrict__ out,
+                                 int64_t ld_out) {
+  const int m = row_count(m_max, m_dev);
+  for (int i = blockIdx.x; i < m; i += gridDim.x) {
+    float* o = out + (int64_t)i * ld_out;
+    int col = 0;
+    for (int s = 0; s < p.nseg; ++s) {
+      const fb_seg_t& sg = p.seg[s];
+      int64_t r;
+      switch (sg.mode) {
+        case 0: r = i; break;
+        case 1: r = rows ? rows[i] : i; break;
+        case 2: { const int sl = rows ? rows[i] : i; r = parent ? parent[sl] : sl; break; }
+        case 3: { const int sl = rows ? rows[i] : i; const int t = tokens[sl];
+                  r = t < 0 ? p.tok_default : t; break; }
+        default: { const int t = ranks ? ranks[i] : -1; r = t < 0 ? p.tok_default : t; break; }
+      }
+      const float* src = sg.src ? sg.src + r * sg.ld : nullptr;
+      for (int j = threadIdx.x; j < sg.width; j += blockDim.x) o[col + j] = src ? src[j] : 0.f;
+      col += sg.width;
+    }
+    for (int j = col + threadIdx.x; j < p.k_pad; j += blockDim.x) o[j] = 0.f;
+  }
+}
+
+// ------------------------------------------------------------ log-softmax --
+__global__ void log_softmax_kernel(int m_max, const int32_t* __restrict__ m_dev,
+                                   const int32_t* __restrict__ rows, const float* __restrict__ x,
+                                   int64_t ldx, int n, float* __restrict__ out, int64_t ldo) {
+  const int m = row_count(m_max, m_dev);
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < m; i += gridDim.x * wpb) {
+    const int r = rows ? rows[i] : i;
+    const float* xr = x + (int64_t)r * ldx;
+    float mx = -INFINITY;
+    for (int j = lane; j < n; j += 32) mx = fmaxf(mx, xr[j]);
+    for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    float s = 0.f;
+    for (int j = lane; j < n; j += 32) s += expf(xr[j] - mx);
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    const float lse = logf(s);
+    float* o = out + (int64_t)r * ldo;
+    for (int j = lane; j < n; j += 32) o[j] = (xr[j] - mx) - lse;
+  }
+}
+
+// -------------------------------------------------------------- attention --
+__device__ __forceinline__ float tanh_fast(float x) {
+  // 1 - 2/(e^{2x}+1): absolute error ~1e-7, saturates cleanly at +-1
+  const float e = __expf(2.0f * x);
+  return 1.0f - 2.0f / (e + 1.0f);
+}
+
+constexpr int kAttThreads = 256;
+constexpr int kAChunk = 32;
+
+template <typename F>
+__device__ double pairwise_sum_d(const double* a, int n, F f) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) res = dadd(res, f(a[i]));
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = f(a[j]);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = dadd(r[j], f(a[i + j]));
+    }
+    double res = dadd(dadd(dadd(r[0], r[1]), dadd(r[2], r[3])), dadd(dadd(r[4], r[5]), dadd(r[6], r[7])));
+    for (; i < n; ++i) res = dadd(res, f(a[i]));
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return dadd(pairwise_sum_d(a, n2, f), pairwise_sum_d(a + n2, n - n2, f));
+}
+
+// One CTA per active utterance: its live rows share the keys/enc reads.
+// dynamic smem: q[n][A] | v[A] | e[n][T] | kc[kAChunk][T]
+__global__ void __launch_bounds__(kAttThreads)
+attention_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
+                 const int32_t* __restrict__ n_live, const int32_t* __restrict__ t_enc,
+                 const float* __restrict__ keys, const float* __restrict__ enc, int A, int C,
+                 const float* __restrict__ v, const float* __restrict__ q, int64_t ldq,
+                 const int32_t* __restrict__ parent, const double* __restrict__ acc_in,
+                 double* __restrict__ acc_out, double* __restrict__ cov_out,
+                 float* __restrict__ ctx_out, int64_t ld_ctx, float* __restrict__ attn_out,
+                 int64_t ld_attn) {
+  const int u = blockIdx.x;
+  if (!active[u]) return;
+  extern __shared__ float sm[];
+  const int K = cfg.beam, TM = cfg.t_max;
+  const int n = n_live[u];
+  const int T = t_enc[u];
+  float* qs = sm;                       // [n][A]
+  float* vs = qs + n * A;               // [A]
+  float* es = vs + A;                   // [n][T]
+  float* kc = es + n * T;               // [kAChunk][T]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kAttThreads / 32;
+  const int slot0 = u * K;
+  for (int j = tid; j < n * A; j += kAttThreads) {
+    const int i = j / A, a = j % A;
+    qs[j] = q[(int64_t)(slot0 + i) * ldq + a];
+  }
+  for (int a = tid; a < A; a += kAttThreads) vs[a] = v[a];
+  for (int j = tid; j < n * T; j += kAttThreads) es[j] = 0.f;
+  const float* ku = keys + (int64_t)u * TM * A;
+  const float* eu = enc + (int64_t)u * TM * C;
+  // energies, accumulated over chunks of the attention dimension
+  for (int a0 = 0; a0 < A; a0 += kAChunk) {
+    const int ac = min(kAChunk, A - a0);
+    __syncthreads();
+    for (int j = tid; j < T * kAChunk; j += kAttThreads) {
+      const int t = j / kAChunk, a = j % kAChunk;
+      if (a < ac) kc[a * T + t] = ku[(int64_t)t * A + a0 + a];
+    }
+    __syncthreads();
+    for (int pidx = tid; pidx < n * T; pidx += kAttThreads) {
+      const int i = pidx / T, t = pidx % T;
+      const float* qi = qs + i * A + a0;
+      float s = 0.f;
+      for (int a = 0; a < ac; ++a) s = fmaf(vs[a0 + a], tanh_fast(kc[a * T + t] + qi[a]), s);
+      es[pidx] += s;
+    }
+  }
+  __syncthreads();
+  // softmax over frames, one warp per row
+  for (int i = warp; i < n; i += nw) {
+    float* e = es + i * T;
+    float mx = -INFINITY;
+    for (int t = lane; t < T; t += 32) mx = fmaxf(mx, e[t]);
+    for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    float s = 0.f;
+    for (int t = lane; t < T; t += 32) {
+      const float x = expf(e[t] - mx);
+      e[t] = x;
+      s += x;
+    }
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    const float inv = 1.0f / s;
+    for (int t = lane; t < T; t += 32) e[t] *= inv;
+  }
+  __syncthreads();
+  // context vectors: ctx[i][c] = sum_t a[i][t] enc[t][c]
+  constexpr int RB = 16;
+  for (int i0 = 0; i0 < n; i0 += RB) {
+    const int nb = min(RB, n - i0);
+    for (int c = tid; c < C; c += kAttThreads) {
+      float acc[RB];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) acc[r] = 0.f;
+      for (int t = 0; t < T; ++t) {
+        const float x = eu[(int64_t)t * C + c];
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+          if (r < nb) acc[r] = fmaf(es[(i0 + r) * T + t], x, acc[r]);
+      }
+      for (int r = 0; r < nb; ++r) ctx_out[(int64_t)(slot0 + i0 + r) * ld_ctx + c] = acc[r];
+    }
+  }
+  // fp64 accumulator + coverage, one warp per row
+  for (int i = warp; i < n; i += nw) {
+    const int r = slot0 + i;
+    const int p = parent ? parent[r] : r;
+    const double* a0 = acc_in + (int64_t)p * TM;
+    double* a1 = acc_out + (int64_t)r * TM;
+    const float* e = es + i * T;
+    int cnt = 0;
+    for (int t = lane; t < T; t += 32) {
+      const double x = dadd(a0[t], (double)e[t]);
+      a1[t] = x;
+      cnt += x > cfg.tau1;
+      if (attn_out) attn_out[(int64_t)r * ld_attn + t] = e[t];
+    }
+    if (cfg.cov_mode != 0) {
+      for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+      __syncwarp();
+      if (lane == 0) {
+        double cov;
+        if (cfg.cov_mode == 1) {
+          cov = (double)cnt;
+        } else {
+          const double tau2 = cfg.tau2, mg = cfg.cov_margin;
+          const double pen = pairwise_sum_d(a1, T, [=](double x) {
+            return x > tau2 ? dsub(dadd(mg, x), tau2) : 0.0;
+          });
+          cov = dsub((double)cnt, pen);
+        }
+        cov_out[r] = cov;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------- LM bookkeeping --
+__global__ void spec_events_kernel(fb_trie_t trie, int n_max, const int32_t* __restrict__ n_dev,
+                                   const int32_t* __restrict__ rows,
+                                   const int32_t* __restrict__ tstate,
+                                   const int32_t* __restrict__ hslot, int32_t* ev_row,
+                                   int32_t* ev_rank, int32_t* ev_slot, int32_t* ev_count,
+                                   int32_t* row_ev) {
+  const int n = row_count(n_max, n_dev);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int r = row_at(rows, i);
+    const int s = tstate[r];
+    int e = -1;
+    if (s > 0) {
+      const int rk = trie.info[4 * s + 2];
+      if (rk >= 0) {
+        e = atomicAdd(ev_count, 1);
+        ev_row[e] = r;
+        ev_rank[e] = rk;
+        ev_slot[e] = hslot[r];
+      }
+    }
+    row_ev[r] = e;
+  }
+}
+
+// Single CTA: mark live slots, list free slots in order, hand them to the
+// boundary rows in row order.
+__global__ void __launch_bounds__(1024)
+boundary_plan_kernel(int n_max, const int32_t* __restrict__ n_dev, const int32_t* __restrict__ rows,
+                     const int32_t* __restrict__ parent, const int32_t* __restrict__ brank,
+                     const int32_t* __restrict__ row_ev, const int32_t* __restrict__ cur_rows,
+                     const int32_t* __restrict__ cur_count, const int32_t* __restrict__ hist_cur,
+                     int32_t* __restrict__ hist_next, int num_slots, int32_t* __restrict__ mark,
+                     int32_t* __restrict__ bnd_slot, int32_t* __restrict__ bnd_src,
+                     int32_t* __restrict__ bnd_count, int32_t* __restrict__ unk_slot,
+                     int32_t* __restrict__ unk_count, int unk_base) {
+  __shared__ int wsum[32];
+  __shared__ int wsum2[32];
+  __shared__ int carry, carry2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  int32_t* freel = mark + num_slots;   // second half of the scratch: free list
+  for (int s = tid; s < num_slots; s += blockDim.x) mark[s] = 0;
+  __syncthreads();
+  const int nc = *cur_count;
+  for (int i = tid; i < nc; i += blockDim.x) mark[hist_cur[cur_rows[i]]] = 1;
+  __syncthreads();
+  // free list: unmarked slots in ascending order -> stored (negated+1) in mark
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < num_slots; b0 += blockDim.x) {
+    const int s = b0 + tid;
+    const int f = (s < num_slots && mark[s] == 0) ? 1 : 0;
+    int x = f;
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int w = lane < nw ? wsum[lane] : 0;
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, off);
+        if (lane >= off) w += y;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    const int pos = carry + (warp ? wsum[warp - 1] : 0) + x - f;
+    if (f) freel[pos] = s;              // k-th free slot, ascending
+    __syncthreads();
+    if (tid == 0) carry += wsum[nw - 1];
+    __syncthreads();
+  }
+  const int n = row_count(n_max, n_dev);
+  if (tid == 0) { carry = 0; carry2 = 0; }
+  __syncthreads();
+  for (int b0 = 0; b0 < n; b0 += blockDim.x) {
+    const int i = b0 + tid;
+    int is_b = 0, is_unk = 0, r = -1;
+    if (i < n) {
+      r = rows[i];
+      const int br = brank[r];
+      is_b = br >= -1;
+      is_unk = br == -1;
+    }
+    int x = is_b, y = is_unk;
+    for (int off = 1; off < 32; off <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, x, off);
+      const int b = __shfl_up_sync(0xffffffffu, y, off);
+      if (lane >= off) { x += a; y += b; }
+    }
+    if (lane == 31) { wsum[warp] = x; wsum2[warp] = y; }
+    __syncthreads();
+    if (warp == 0) {
+      int w = lane < nw ? wsum[lane] : 0;
+      int w2 = lane < nw ? wsum2[lane] : 0;
+      for (int off = 1; off < 32; off <<= 1) {
+        const int a = __shfl_up_sync(0xffffffffu, w, off);
+        const int b = __shfl_up_sync(0xffffffffu, w2, off);
+        if (lane >= off) { w += a; w2 += b; }
+      }
+      wsum[lane] = w;
+      wsum2[lane] = w2;
+    }
+    __syncthreads();
+    if (is_b) {
+      const int k = carry + (warp ? wsum[warp - 1] : 0) + x - 1;     // boundary index
+      const int slot = freel[k];
+      bnd_slot[k] = slot;
+      hist_next[r] = slot;
+      const int p = parent[r];
+      if (is_unk) {
+        const int ku = carry2 + (warp ? wsum2[warp - 1] : 0) + y - 1;
+        unk_slot[ku] = hist_cur[p];
+        bnd_src[k] = unk_base + ku;
+      } else {
+        bnd_src[k] = row_ev[p];
+      }
+    }
+    __syncthreads();
+    if (tid == 0) { carry += wsum[nw - 1]; carry2 += wsum2[nw - 1]; }
+    __syncthreads();
+  }
+  if (tid == 0) { *bnd_count = carry; *unk_count = carry2; }
+}
+
+__global__ void copy_rows_kernel(int n_max, const int32_t* __restrict__ n_dev,
+                                 const int32_t* __restrict__ si, const int32_t* __restrict__ di,
+                                 const char* __restrict__ src, char* __restrict__ dst,
+                                 int64_t row_bytes) {
+  const int n = row_count(n_max, n_dev);
+  const bool vec = (row_bytes % 16 == 0) && ((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 16 == 0);
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const char* s = src + (int64_t)(si ? si[i] : i) * row_bytes;
+    char* d = dst + (int64_t)(di ? di[i] : i) * row_bytes;
+    if (vec) {
+      for (int64_t j = threadIdx.x; j < row_bytes / 16; j += blockDim.x)
+        reinterpret_cast<int4*>(d)[j] = reinterpret_cast<const int4*>(s)[j];
+    } else {
+      for (int64_t j = threadIdx.x; j < row_bytes; j += blockDim.x) d[j] = s[j];
+    }
+  }
+}
+
+}  // namespace fb
+
+using namespace fb;
+
+extern "C" int fb_pack_rows(const fb_pack_t* p, int32_t m_max, const int32_t* m_dev,
+                            const int32_t* rows, const int32_t* parent, const int32_t* tokens,
+                            const int32_t* ranks, float* out, int64_t ld_out, void* stream) {
+  FB_CHECK_ARG(p && out && p->nseg >= 1 && p->nseg <= 4, "bad pack description");
+  int w = 0;
+  for (int s = 0; s < p->nseg; ++s) w += p->seg[s].width;
+  FB_CHECK_ARG(w <= p->k_pad && p->k_pad <= ld_out, "pack width exceeds k_pad / ld_out");
+  if (m_max <= 0) return FB_OK;
+  pack_rows_kernel<<<std::min(m_max, kNumSMs * 16), 128, 0, (cudaStream_t)stream>>>(
+      *p, m_max, m_dev, rows, parent, tokens, ranks, out, ld_out);
+  count_launch();
+  return check_launch("pack_rows");
+}
+
+extern "C" int fb_log_softmax_rows(int32_t m_max, const int32_t* m_dev, const int32_t* rows,
+                                   const float* x, int64_t ldx, int32_t n, float* out,
+                                   int64_t ldo, void* stream) {
+  FB_CHECK_ARG(x && out && n > 0, "bad log-softmax arguments");
+  if (m_max <= 0) return FB_OK;
+  log_softmax_kernel<<<std::min((m_max + 7) / 8, kNumSMs * 8), 256, 0, (cudaStream_t)stream>>>(
+      m_max, m_dev, rows, x, ldx, n, out, ldo);
+  count_launch();
+  return check_launch("log_softmax_rows");
+}
+
+extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
+                                 const int32_t* active, const int32_t* n_live,
+                                 const int32_t* t_enc, const float* keys, const float* enc,
+                                 int32_t att_dim, int32_t ctx_dim, const float* v, const float* q,
+                                 int64_t ldq, const int32_t* parent, const double* acc_in,
+                                 double* acc_out, double* cov_out, float* ctx_out,
+                                 int64_t ld_ctx, float* attn_out, int64_t ld_attn,
+                                 void* stream) {
+  FB_CHECK_ARG(cfg && keys && enc && v && q && acc_in && acc_out && ctx_out, "null attention args");
+  FB_CHECK_ARG(cfg->cov_mode == 0 || cov_out, "coverage output required");
+  if (num_utts <= 0) return FB_OK;
+  const size_t smem = sizeof(float) * ((size_t)cfg->beam * att_dim + att_dim +
+                                       (size_t)cfg->beam * cfg->t_max + (size_t)kAChunk * cfg->t_max);
+  if (smem > 220 * 1024) return fail(FB_ERR_CONFIG, "attention working set exceeds shared memory");
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  attention_kernel<<<num_utts, kAttThreads, smem, (cudaStream_t)stream>>>(
+      *cfg, active, n_live, t_enc, keys, enc, att_dim, ctx_dim, v, q, ldq, parent, acc_in,
+      acc_out, cov_out, ctx_out, ld_ctx, attn_out, ld_attn);
+  count_launch();
+  return check_launch("attention_step");
+}
+
+extern "C" int fb_spec_events(const fb_trie_t* trie, int32_t n_max, const int32_t* n_dev,
+                              const int32_t* rows, const int32_t* trie_state,
+                              const int32_t* hist_slot, int32_t* ev_row, int32_t* ev_rank,
+                              int32_t* ev_slot, int32_t* ev_count, int32_t* row_ev,
+                              void* stream) {
+  FB_CHECK_ARG(trie && ev_count && row_ev, "null spec-event arguments");
+  cudaMemsetAsync(ev_count, 0, sizeof(int32_t), (cudaStream_t)stream);
+  if (n_max <= 0) return check_launch("spec_events");
+  spec_events_kernel<<<std::min((n_max + 255) / 256, kNumSMs * 4), 256, 0, (cudaStream_t)stream>>>(
+      *trie, n_max, n_dev, rows, trie_state, hist_slot, ev_row, ev_rank, ev_slot, ev_count,
+      row_ev);
+  count_launch();
+  return check_launch("spec_events");
+}
+
+extern "C" int fb_boundary_plan(int32_t n_max, const int32_t* n_dev, const int32_t* rows,
+                                const int32_t* parent, const int32_t* boundary_rank,
+                                const int32_t* row_ev, const int32_t* cur_rows,
+                                const int32_t* cur_count, const int32_t* hist_cur,
+                                int32_t* hist_next, int32_t num_slots, int32_t* slot_mark,
+                                int32_t* bnd_slot, int32_t* bnd_src, int32_t* bnd_count,
+                                int32_t* unk_slot, int32_t* unk_count, int32_t unk_base,
+                                void* stream) {
+  FB_CHECK_ARG(rows && parent && boundary_rank && cur_rows && cur_count && hist_cur && hist_next,
+               "null boundary-plan arguments");
+  boundary_plan_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(
+      n_max, n_dev, rows, parent, boundary_rank, row_ev, cur_rows, cur_count, hist_cur,
+      hist_next, num_slots, slot_mark, bnd_slot, bnd_src, bnd_count, unk_slot, unk_count,
+      unk_base);
+  count_launch();
+  return check_launch("boundary_plan");
+}
+
+extern "C" int fb_copy_rows(int32_t n_max, const int32_t* n_dev, const int32_t* src_idx,
+                            const int32_t* dst_idx, const void* src, void* dst, int64_t row_bytes,
+                            void* stream) {
+  FB_CHECK_ARG(src && dst && row_bytes > 0, "bad copy arguments");
+  if (n_max <= 0) return FB_OK;
+  copy_rows_kernel<<<std::min(n_max, kNumSMs * 8), 256, 0, (cudaStream_t)stream>>>(
+      n_max, n_dev, src_idx, dst_idx, (const char*)src, (char*)dst, row_bytes);
+  count_launch();
+  return check_launch("copy_rows");
+}

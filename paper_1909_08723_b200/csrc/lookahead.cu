@@ -177,8 +177,9 @@ __device__ __forceinline__ double block_exclusive_scan(double v, double* wsum, d
 template <bool FROM_LOGITS>
 __global__ void __launch_bounds__(kScanThreads)
 row_scan_kernel(int m_max, const int32_t* __restrict__ m_dev, const void* __restrict__ src,
-                int64_t s_stride, int vw, int v_out, const int32_t* __restrict__ slots,
-                double* __restrict__ g_pool, int64_t g_stride, double* __restrict__ eos_out) {
+                int64_t s_stride, const int32_t* __restrict__ src_rows, int vw, int v_out,
+                const int32_t* __restrict__ slots, double* __restrict__ g_pool, int64_t g_stride,
+                double* __restrict__ eos_out) {
   __shared__ double tile[kScanTile];
   __shared__ double wsum[32];
   __shared__ float red_f[32];
@@ -187,12 +188,14 @@ row_scan_kernel(int m_max, const int32_t* __restrict__ m_dev, const void* __rest
   const int m = row_count(m_max, m_dev);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int row = blockIdx.x; row < m; row += gridDim.x) {
-    double* g = g_pool + (int64_t)slots[row] * g_stride;
+    const int dst = slots ? slots[row] : row;
+    const int64_t srow = src_rows ? src_rows[row] : row;
+    double* g = g_pool ? g_pool + (int64_t)dst * g_stride : nullptr;
     float mw = 0.f;
     double sw = 1.0;
     const float* lg = nullptr;
     if constexpr (FROM_LOGITS) {
-      lg = reinterpret_cast<const float*>(src) + (int64_t)row * s_stride;
+      lg = reinterpret_cast<const float*>(src) + srow * s_stride;
       // pass A: max over the words and over all outputs (for </s>)
       float mx = -INFINITY, mall = -INFINITY;
       for (int j = threadIdx.x; j < v_out; j += blockDim.x) {
@@ -221,10 +224,11 @@ row_scan_kernel(int m_max, const int32_t* __restrict__ m_dev, const void* __rest
         // log-softmax of </s> over all outputs: words rescaled + the specials
         double sall = sw * exp((double)mw - (double)mall);
         for (int j = vw; j < v_out; ++j) sall += exp((double)lg[j] - (double)mall);
-        eos_out[slots[row]] = (double)lg[vw] - ((double)mall + log(sall));
+        eos_out[dst] = (double)lg[vw] - ((double)mall + log(sall));
       }
       __syncthreads();
     }
+    if (!g) continue;
     // pass: running sums tile by tile
     double carry = 0.0;
     for (int base = 0; base < vw; base += kScanTile) {
@@ -233,7 +237,7 @@ row_scan_kernel(int m_max, const int32_t* __restrict__ m_dev, const void* __rest
         double v = 0.0;
         if (j < cnt) {
           if constexpr (FROM_LOGITS) v = (double)expf(lg[base + j] - mw) / sw;
-          else v = reinterpret_cast<const double*>(src)[(int64_t)row * s_stride + base + j];
+          else v = reinterpret_cast<const double*>(src)[srow * s_stride + base + j];
         }
         tile[j] = v;
       }
@@ -324,19 +328,21 @@ extern "C" int fb_cumsum_rows(int32_t m, const double* probs, int64_t p_stride, 
   if (m <= 0) return FB_OK;
   const int blocks = std::min(m, kNumSMs * 4);
   row_scan_kernel<false><<<blocks, kScanThreads, 0, (cudaStream_t)stream>>>(
-      m, nullptr, probs, p_stride, vw, vw, slots, g_pool, g_stride, nullptr);
+      m, nullptr, probs, p_stride, nullptr, vw, vw, slots, g_pool, g_stride, nullptr);
   count_launch();
   return check_launch("cumsum_rows");
 }
 
 extern "C" int fb_logits_to_g(int32_t m_max, const int32_t* m_dev, const float* logits,
-                              int64_t l_stride, int32_t vw, int32_t v_out, const int32_t* slots,
-                              double* g_pool, int64_t g_stride, double* eos_out, void* stream) {
-  FB_CHECK_ARG(vw > 0 && v_out > vw && l_stride >= v_out && g_stride >= vw, "bad logits sizes");
+                              int64_t l_stride, const int32_t* src_rows, int32_t vw,
+                              int32_t v_out, const int32_t* slots, double* g_pool,
+                              int64_t g_stride, double* eos_out, void* stream) {
+  FB_CHECK_ARG(vw > 0 && v_out > vw && l_stride >= v_out, "bad logits sizes");
+  FB_CHECK_ARG(!g_pool || g_stride >= vw, "bad g stride");
   if (m_max <= 0) return FB_OK;
   const int blocks = std::min(m_max, kNumSMs * 4);
   row_scan_kernel<true><<<blocks, kScanThreads, 0, (cudaStream_t)stream>>>(
-      m_max, m_dev, logits, l_stride, vw, v_out, slots, g_pool, g_stride, eos_out);
+      m_max, m_dev, logits, l_stride, src_rows, vw, v_out, slots, g_pool, g_stride, eos_out);
   count_launch();
   return check_launch("logits_to_g");
 }

@@ -1,0 +1,176 @@
+"""Fused device decode: the whole lock-step loop of ``decode_batch``
+(reference ``decoder.py:363-462`` + ``fusion.py:118-233``) on the GPU.
+
+Per step, for the compact list of live rows of active utterances:
+
+ 1. attention-LSTM decoder step  (pack -> GEMM+LSTM-cell x L -> query GEMM ->
+    attention + fp64 accumulator + coverage -> output GEMM -> log-softmax);
+ 2. speculative word-LM events for rows at final trie states (the ``<eos>``
+    column, fusion.py:181-183): LSTM-LM step + logits + log P(</s>);
+ 3. look-ahead scores over the CSR trie and fp64 g rows (Eq. 4);
+ 4. selection kernel (combine, EOS gate, stable top-beam, coverage, finished
+    set, early stop, results) -> parent/token per new row, next row list;
+ 5. trie advance + word-boundary plan; ``<unk>`` LM events; new history slots
+    get the LM state and g row of their event.
+
+State never leaves the device; rows index per-slot buffers through ``parent``
+(no physical reorder).  The host only polls the live-row count.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from typing import List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import kernels as K
+from .decoder import DecodeConfig, DecodeResult, SearchBuffers, search_cfg
+from .errors import ConfigError
+from .models import AmState, lm_step
+
+P = _lib.ptr
+
+
+class _LmPool:
+    """History slots (LM state + g row + eos) and per-step LM events."""
+
+    def __init__(self, lw, N: int, device):
+        d = lw.d
+        self.lw = lw
+        self.N = N
+        self.P = 2 * N + 2
+        L, H = d.layers, d.hidden
+        f32, i32 = torch.float32, torch.int32
+        z = lambda *s, dt=i32: torch.zeros(s, dtype=dt, device=device)  # noqa: E731
+        self.state = torch.zeros((self.P, L, 2, H), dtype=f32, device=device)
+        self.g = torch.empty((self.P, d.words), dtype=torch.float64, device=device)
+        self.eos = torch.zeros(self.P, dtype=torch.float64, device=device)
+        E = 2 * N
+        self.ev_state = torch.zeros((E, L, 2, H), dtype=f32, device=device)
+        self.ev_logits = torch.empty((E, lw.v_out), dtype=f32, device=device)
+        self.ev_row, self.ev_rank, self.ev_slot, self.row_ev = z(N), z(N), z(N), z(N)
+        self.ev_count = z(1)
+        self.trie = [z(N), z(N)]
+        self.hist = [z(N), z(N)]
+        self.brank = z(N)
+        self.bnd_slot, self.bnd_src, self.unk_slot = z(N), z(N), z(N)
+        self.bnd_count, self.unk_count = z(1), z(1)
+        self.mark = z(2 * self.P)
+        self.ext_eos = torch.zeros(N, dtype=torch.float64, device=device)
+        self.scratch = torch.empty((N, lw.k_max), dtype=f32, device=device)
+
+    def start(self) -> None:
+        """Slot 0 = LM state after <s> from the zero state (word_lm start_history)."""
+        lw = self.lw
+        lm_step(lw, m=1, m_dev=None, state_src=None, src_idx=None, state_dst=self.ev_state,
+                ranks=None, tok_default=lw.bos_tok, scratch=self.scratch, logits=self.ev_logits)
+        self.state[0].copy_(self.ev_state[0])
+        K.logits_to_g(self.ev_logits, lw.d.words, lw.v_out, m=1, g_pool=self.g, eos_out=self.eos)
+
+
+def decode_fused(features, scorer, fusion, config: DecodeConfig, token_dict
+                 ) -> List[DecodeResult]:
+    dev = scorer.device
+    w = scorer.weights
+    d = w.d
+    if len(token_dict) != d.vocab:
+        raise ConfigError(f"acoustic model scores {d.vocab} tokens but the dictionary has"
+                          f" {len(token_dict)}")
+    B = len(features)
+    if B == 0:
+        return []
+    Kb = config.beam_size
+    N = B * Kb
+    V = len(token_dict)
+    stream = _lib.stream_ptr()
+    enc, keys, T = scorer.encoder([np.asarray(f.data, np.float32) for f in features])
+    TM = max(T)
+    max_len = [max(1, int(math.floor(config.max_len_ratio * t))) for t in T]
+    MT = max(max_len) + 1
+    buf = SearchBuffers(B, Kb, MT, TM, dev)
+    buf.max_len.copy_(torch.as_tensor(max_len, dtype=torch.int32))
+    buf.t_enc.copy_(torch.as_tensor(T, dtype=torch.int32))
+    has_fusion = fusion is not None
+    early = (not has_fusion) or bool(fusion.nonpositive_scores)
+    cfg = search_cfg(config, token_dict, has_fusion, early, True, MT, TM)
+    cfg_ref = C.byref(cfg)
+    _lib.call("fb_search_init", cfg_ref, C.byref(buf.view(0)), B, stream)
+    rows = [torch.zeros(N, dtype=torch.int32, device=dev) for _ in range(2)]
+    count = [torch.zeros(1, dtype=torch.int32, device=dev) for _ in range(2)]
+    rows[0][:B] = torch.arange(B, dtype=torch.int32, device=dev) * Kb
+    count[0].fill_(B)
+    views = [_view_with_rows(buf, p, rows[1 - p], count[1 - p]) for p in range(2)]
+
+    L, H, C_ = d.dec_layers, d.dec_hidden, d.ctx
+    X = [AmState(L, N, H, C_, dev), AmState(L, N, H, C_, dev)]
+    scratch = torch.empty((N, w.k_max), dtype=torch.float32, device=dev)
+    q = torch.empty((N, d.att), dtype=torch.float32, device=dev)
+    logits = torch.empty((N, V), dtype=torch.float32, device=dev)
+    am_logp = torch.zeros((N, V), dtype=torch.float32, device=dev)
+
+    lm = None
+    fus_buf = None
+    if has_fusion:
+        lw = fusion.word_lm.weights
+        lm = _LmPool(lw, N, dev)
+        lm.start()
+        fus_buf = torch.zeros((N, V), dtype=torch.float64, device=dev)
+        dtrie = fusion.dtrie
+        Vw = lw.d.words
+
+    parity = 0
+    while True:
+        c = parity
+        rc, nc = rows[c], count[c]
+        scorer.step_fn(N=N, rows=rc, m=N, m_dev=nc, parent=buf.parent, last_tok=buf.last_tok,
+                       prev=X[1 - c], cur=X[c], scratch=scratch, q=q, logits=logits,
+                       am_logp=am_logp, cfg_ref=cfg_ref, num_utts=B, active=buf.active,
+                       n_live=buf.n_live, t_enc=buf.t_enc, keys=keys, enc=enc,
+                       acc_in=buf.acc[c], acc_out=buf.acc[1 - c], cov=buf.cov)
+        if has_fusion:
+            _lib.call("fb_spec_events", dtrie.ref, N, P(nc), P(rc), P(lm.trie[c]), P(lm.hist[c]),
+                      P(lm.ev_row), P(lm.ev_rank), P(lm.ev_slot), P(lm.ev_count), P(lm.row_ev),
+                      stream)
+            lm_step(lw, m=N, m_dev=lm.ev_count, state_src=lm.state, src_idx=lm.ev_slot,
+                    state_dst=lm.ev_state, ranks=lm.ev_rank, tok_default=0, scratch=lm.scratch,
+                    logits=lm.ev_logits)
+            K.logits_to_g(lm.ev_logits, Vw, lw.v_out, m=N, m_dev=lm.ev_count, slots=lm.ev_row,
+                          eos_out=lm.ext_eos)
+            _lib.call("fb_lookahead_scores", dtrie.ref, N, P(nc), P(rc), P(lm.trie[c]),
+                      P(lm.hist[c]), P(lm.g), Vw, P(lm.eos), P(lm.ext_eos), fusion.space_id,
+                      fusion.eos_id, fusion.oov_penalty, fusion.score_floor, P(fus_buf), V,
+                      P(fusion._floored), stream)
+        _lib.call("fb_search_step", cfg_ref, C.byref(views[c]), B, P(am_logp), V, P(fus_buf), V,
+                  stream)
+        if has_fusion:
+            rn, cn = rows[1 - c], count[1 - c]
+            _lib.call("fb_trie_advance", dtrie.ref, N, P(cn), P(rn), P(buf.parent),
+                      P(lm.trie[c]), P(lm.hist[c]), P(buf.last_tok), fusion.space_id,
+                      fusion.eos_id, fusion.pad_id, P(lm.trie[1 - c]), P(lm.hist[1 - c]),
+                      P(lm.brank), stream)
+            _lib.call("fb_boundary_plan", N, P(cn), P(rn), P(buf.parent), P(lm.brank),
+                      P(lm.row_ev), P(rc), P(nc), P(lm.hist[c]), P(lm.hist[1 - c]), lm.P,
+                      P(lm.mark), P(lm.bnd_slot), P(lm.bnd_src), P(lm.bnd_count),
+                      P(lm.unk_slot), P(lm.unk_count), N, stream)
+            lm_step(lw, m=N, m_dev=lm.unk_count, state_src=lm.state, src_idx=lm.unk_slot,
+                    state_dst=lm.ev_state[N:], ranks=None, tok_default=lw.unk_tok,
+                    scratch=lm.scratch, logits=lm.ev_logits[N:])
+            K.copy_rows(lm.ev_state, lm.state, m=N, m_dev=lm.bnd_count, src_idx=lm.bnd_src,
+                        dst_idx=lm.bnd_slot)
+            K.logits_to_g(lm.ev_logits, Vw, lw.v_out, m=N, m_dev=lm.bnd_count,
+                          src_rows=lm.bnd_src, slots=lm.bnd_slot, g_pool=lm.g, eos_out=lm.eos)
+        parity ^= 1
+        if int(count[parity].item()) == 0:
+            break
+    return buf.results([f.utt_id for f in features], T)
+
+
+def _view_with_rows(buf: SearchBuffers, p: int, next_rows, next_count):
+    out = _lib.FbSearchState.from_buffer_copy(buf.view(p))
+    out.next_rows = P(next_rows)
+    out.next_count = P(next_count)
+    return out

@@ -1,0 +1,79 @@
+"""Thin typed wrappers over the C-ABI launchers (device tensors in, no sync).
+
+Every function here launches exactly one library entry point on the current
+torch stream; shapes are validated by the C side (ValueError/ConfigError).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence, Tuple
+
+import torch
+
+from . import _lib
+
+P = _lib.ptr
+
+
+def _ld(t: Optional[torch.Tensor]) -> int:
+    return 0 if t is None else t.stride(0)
+
+
+def gemm(a: torch.Tensor, w: torch.Tensor, *, m: Optional[int] = None, m_dev=None,
+         k: Optional[int] = None, bias=None, out=None, rows=None, mode: int = 0, hidden: int = 0,
+         parent=None, c_in=None, c_out=None, h_out=None, h_res=None, addend=None,
+         lda: Optional[int] = None) -> None:
+    """C = A . W^T with the epilogues of fb_gemm (see include/fusedbeam_b200.h)."""
+    g = _lib.FbGemm()
+    g.m_max = a.shape[0] if m is None else m
+    g.m_dev = P(m_dev)
+    g.n = w.shape[0]
+    g.k = w.shape[1] if k is None else k
+    g.a, g.lda = P(a), (a.stride(0) if lda is None else lda)
+    g.w, g.ldw = P(w), w.stride(0)
+    g.bias = P(bias)
+    g.c, g.ldc = P(out), _ld(out)
+    g.mode, g.hidden = mode, hidden
+    g.rows, g.parent = P(rows), P(parent)
+    g.c_in, g.ld_cin = P(c_in), _ld(c_in)
+    g.c_out, g.ld_cout = P(c_out), _ld(c_out)
+    g.h_out, g.ld_h = P(h_out), _ld(h_out)
+    g.h_res, g.ld_res = P(h_res), _ld(h_res)
+    g.addend, g.ld_add = P(addend), _ld(addend)
+    _lib.call("fb_gemm", C.byref(g), _lib.stream_ptr())
+
+
+def pack(out: torch.Tensor, segs: Sequence[Tuple], *, m: int, m_dev=None, rows=None,
+         parent=None, tokens=None, ranks=None, tok_default: int = 0,
+         k_pad: Optional[int] = None) -> None:
+    """out[i] = concat(segments) zero-padded; segs = (src|None, width, mode, ld?)."""
+    p = _lib.FbPack()
+    for j, s in enumerate(segs):
+        src, width, mode = s[0], s[1], s[2]
+        ld = s[3] if len(s) > 3 else (src.stride(0) if src is not None else 0)
+        p.seg[j] = _lib.FbSeg(P(src), ld, width, mode)
+    p.nseg = len(segs)
+    p.k_pad = out.shape[1] if k_pad is None else k_pad
+    p.tok_default = tok_default
+    _lib.call("fb_pack_rows", C.byref(p), m, P(m_dev), P(rows), P(parent), P(tokens), P(ranks),
+              P(out), out.stride(0), _lib.stream_ptr())
+
+
+def log_softmax_rows(x: torch.Tensor, out: torch.Tensor, n: int, *, m: int, m_dev=None,
+                     rows=None) -> None:
+    _lib.call("fb_log_softmax_rows", m, P(m_dev), P(rows), P(x), x.stride(0), n, P(out),
+              out.stride(0), _lib.stream_ptr())
+
+
+def copy_rows(src: torch.Tensor, dst: torch.Tensor, *, m: int, m_dev=None, src_idx=None,
+              dst_idx=None, row_bytes: Optional[int] = None) -> None:
+    rb = row_bytes if row_bytes is not None else src.stride(0) * src.element_size()
+    _lib.call("fb_copy_rows", m, P(m_dev), P(src_idx), P(dst_idx), P(src), P(dst), rb,
+              _lib.stream_ptr())
+
+
+def logits_to_g(logits: torch.Tensor, vw: int, v_out: int, *, m: int, m_dev=None,
+                src_rows=None, slots=None, g_pool=None, eos_out=None) -> None:
+    _lib.call("fb_logits_to_g", m, P(m_dev), P(logits), logits.stride(0), P(src_rows), vw, v_out,
+              P(slots), P(g_pool), _ld(g_pool), P(eos_out), _lib.stream_ptr())

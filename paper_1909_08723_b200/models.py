@@ -1,0 +1,387 @@
+"""Random-init neural scorers on the device, behind the reference contracts.
+
+* ``AttnLstmScorer`` -- ``AcousticScorer`` (reference ``decoder.py:109-128``):
+  BiLSTM encoder + attention-LSTM decoder (equations in
+  DESIGN.md §3).  ``is_device_scorer`` routes ``decode_batch`` to the fused
+  engine; ``init/step/reorder`` also work one utterance at a time for the
+  plugin driver and the kernel parity tests.
+* ``LstmWordLM`` -- ``WordLM`` (reference ``word_lm.py:160-186``): tied-
+  embedding LSTM LM.  ``is_device_lm`` makes a
+  ``LookaheadFusion`` over it device-native.
+
+Weights are stored for the kernels: LSTM gate rows interleaved (row 4u+q =
+gate q of unit u), input and recurrent matrices concatenated along K so one
+GEMM produces all gates, K zero-padded to the GEMM granule.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import itertools
+import math
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import kernels as K
+from .fusion import _device
+from .synth import AsrDims, LmDims
+
+KGRAN = 16           # K granule of the GEMM kernels
+
+
+def _pad(k: int, g: int = KGRAN) -> int:
+    return (k + g - 1) // g * g
+
+
+def interleave_gates(w: np.ndarray, hidden: int) -> np.ndarray:
+    """Rows (q*H + u) -> (4u + q) for q in (i, f, g, o)."""
+    tail = w.shape[1:]
+    return np.ascontiguousarray(
+        w.reshape(4, hidden, *tail).swapaxes(0, 1).reshape(4 * hidden, *tail))
+
+
+def _dev(a, device, cols: Optional[int] = None) -> torch.Tensor:
+    a = np.ascontiguousarray(a, np.float32)
+    if cols is not None and a.ndim == 2 and a.shape[1] != cols:
+        z = np.zeros((a.shape[0], cols), np.float32)
+        z[:, :a.shape[1]] = a
+        a = z
+    return torch.as_tensor(a, device=device)
+
+
+@dataclass
+class LstmLayer:
+    w: torch.Tensor        # [4H, k_pad] gate-interleaved, [W_ih | W_hh] along K
+    b: torch.Tensor        # [4H]
+    k_in: int
+    hidden: int
+
+    @property
+    def k_pad(self) -> int:
+        return self.w.shape[1]
+
+
+class AsrWeights:
+    """Device copies of the encoder/decoder weights in kernel layout."""
+
+    def __init__(self, W: Dict[str, np.ndarray], d: AsrDims, device):
+        self.d = d
+        He, H, C_, A = d.enc_hidden, d.dec_hidden, d.ctx, d.att
+        self.enc = []
+        for l in range(d.enc_layers):
+            fin = d.feat_dim * d.subsample if l == 0 else 2 * He
+            dirs = []
+            for r in range(2):
+                w_ih = interleave_gates(W[f"enc.{l}.{r}.w_ih"], He)
+                w_hh = interleave_gates(W[f"enc.{l}.{r}.w_hh"], He)
+                b = interleave_gates(W[f"enc.{l}.{r}.b"], He)
+                dirs.append((_dev(w_ih, device, _pad(fin)), _dev(w_hh, device, _pad(He)),
+                             _dev(b, device)))
+            self.enc.append(dirs)
+        self.emb = _dev(W["dec.emb"], device)
+        self.dec: List[LstmLayer] = []
+        for l in range(d.dec_layers):
+            fin = (d.emb + C_) if l == 0 else (H + C_)
+            w = np.concatenate([W[f"dec.{l}.w_ih"], W[f"dec.{l}.w_hh"]], axis=1)
+            self.dec.append(LstmLayer(_dev(interleave_gates(w, H), device, _pad(fin + H)),
+                                      _dev(interleave_gates(W[f"dec.{l}.b"], H), device),
+                                      fin + H, H))
+        self.w_k = _dev(W["dec.att.w_k"], device, _pad(C_))
+        self.b_k = _dev(W["dec.att.b_k"], device)
+        self.w_q = _dev(W["dec.att.w_q"], device, _pad(H))
+        self.v = _dev(W["dec.att.v"], device)
+        self.w_out = _dev(W["dec.out.w"], device, _pad(H + C_))
+        self.b_out = _dev(W["dec.out.b"], device)
+        self.k_max = max([l.k_pad for l in self.dec] + [self.w_q.shape[1], self.w_out.shape[1],
+                                                        self.w_k.shape[1]])
+
+
+class AmState:
+    """Decoder state per slot: h/c per layer, attention context."""
+
+    def __init__(self, L: int, N: int, H: int, C_: int, device):
+        self.h = torch.zeros((L, N, H), dtype=torch.float32, device=device)
+        self.c = torch.zeros((L, N, H), dtype=torch.float32, device=device)
+        self.ctx = torch.zeros((N, C_), dtype=torch.float32, device=device)
+
+
+class Encoder:
+    """Frame stacking + stacked BiLSTM on the device.  The backward direction
+    runs forward over per-utterance reversed frames, so variable lengths need
+    no masking (frames past an utterance's end are never attended)."""
+
+    def __init__(self, w: AsrWeights, device):
+        self.w = w
+        self.device = device
+
+    def __call__(self, feats: Sequence[np.ndarray]):
+        d = self.w.d
+        dev = self.device
+        B = len(feats)
+        T = [int(x.shape[0]) // d.subsample for x in feats]
+        if min(T) < 1:
+            raise ValueError("utterance shorter than the subsampling factor")
+        TM = max(T)
+        Din = d.feat_dim * d.subsample
+        x = np.zeros((B, TM, _pad(Din)), np.float32)
+        for u, f in enumerate(feats):
+            x[u, :T[u], :Din] = f[:T[u] * d.subsample].reshape(T[u], Din)
+        X = torch.as_tensor(x, device=dev).reshape(B * TM, -1)
+        rev = np.arange(B * TM, dtype=np.int32).reshape(B, TM)
+        for u in range(B):
+            rev[u, :T[u]] = u * TM + np.arange(T[u] - 1, -1, -1)
+        rev_t = torch.as_tensor(rev.reshape(-1), device=dev)
+        He = d.enc_hidden
+        Xr = torch.empty_like(X)
+        for l, dirs in enumerate(self.w.enc):
+            kin = X.shape[1]
+            K.copy_rows(X, Xr, m=B * TM, src_idx=rev_t)
+            ys = []
+            for r, (w_ih, w_hh, b) in enumerate(dirs):
+                src = X if r == 0 else Xr
+                xp = torch.empty((B * TM, 4 * He), dtype=torch.float32, device=dev)
+                K.gemm(src, w_ih, k=kin, bias=b, out=xp)
+                y = torch.zeros((B, TM, He), dtype=torch.float32, device=dev)
+                cbuf = [torch.zeros((B, He), dtype=torch.float32, device=dev) for _ in range(2)]
+                zero_h = torch.zeros((B, _pad(He)), dtype=torch.float32, device=dev)
+                xp3 = xp.view(B, TM, 4 * He)
+                for t in range(TM):
+                    a = zero_h if t == 0 else y[:, t - 1, :]
+                    K.gemm(a, w_hh, m=B, k=w_hh.shape[1], mode=1, hidden=He,
+                           c_in=None if t == 0 else cbuf[t % 2], c_out=cbuf[(t + 1) % 2],
+                           h_out=y[:, t, :], addend=xp3[:, t, :])
+                ys.append(y.reshape(B * TM, He))
+            kout = _pad(2 * He)
+            Xn = torch.empty((B * TM, kout), dtype=torch.float32, device=dev)
+            K.pack(Xn, [(ys[0], He, 0), (ys[1], He, 1)], m=B * TM, rows=rev_t)
+            X = Xn
+            Xr = torch.empty_like(X)
+        C_ = 2 * He
+        enc = X[:, :C_].contiguous()
+        keys = torch.empty((B * TM, d.att), dtype=torch.float32, device=dev)
+        K.gemm(X, self.w.w_k, k=self.w.w_k.shape[1], bias=self.w.b_k, out=keys)
+        return enc.view(B, TM, C_), keys.view(B, TM, d.att), T
+
+
+class DecoderStep:
+    """One attention-LSTM decoder step over a compact row list (slot layout)."""
+
+    def __init__(self, w: AsrWeights, eos_id: int, device):
+        self.w = w
+        self.eos = eos_id
+        self.device = device
+
+    def __call__(self, *, N: int, rows, m: int, m_dev, parent, last_tok, prev: AmState,
+                 cur: AmState, scratch: torch.Tensor, q: torch.Tensor, logits: torch.Tensor,
+                 am_logp: torch.Tensor, cfg_ref, num_utts: int, active, n_live, t_enc,
+                 keys, enc, acc_in, acc_out, cov, attn_out=None) -> None:
+        w, d = self.w, self.w.d
+        H, C_, E = d.dec_hidden, d.ctx, d.emb
+        L = d.dec_layers
+        kw = dict(m=m, m_dev=m_dev, rows=rows, parent=parent)
+        for l, lay in enumerate(w.dec):
+            if l == 0:
+                segs = [(w.emb, E, 3), (prev.ctx, C_, 2), (prev.h[0], H, 2)]
+            else:
+                segs = [(cur.h[l - 1], H, 1), (prev.ctx, C_, 2), (prev.h[l], H, 2)]
+            K.pack(scratch, segs, tokens=last_tok, tok_default=self.eos, k_pad=lay.k_pad, **kw)
+            K.gemm(scratch, lay.w, k=lay.k_pad, bias=lay.b, mode=1, hidden=H,
+                   c_in=prev.c[l], c_out=cur.c[l], h_out=cur.h[l],
+                   h_res=cur.h[l - 1] if l > 0 else None, **kw)
+        top = cur.h[L - 1]
+        kq = w.w_q.shape[1]
+        K.pack(scratch, [(top, H, 1)], k_pad=kq, **kw)
+        K.gemm(scratch, w.w_q, k=kq, out=q, m=m, m_dev=m_dev, rows=rows)
+        _lib.call("fb_attention_step", cfg_ref, num_utts, _lib.ptr(active), _lib.ptr(n_live),
+                  _lib.ptr(t_enc), _lib.ptr(keys), _lib.ptr(enc), d.att, C_, _lib.ptr(w.v),
+                  _lib.ptr(q), q.stride(0), _lib.ptr(parent), _lib.ptr(acc_in),
+                  _lib.ptr(acc_out), _lib.ptr(cov), _lib.ptr(cur.ctx), cur.ctx.stride(0),
+                  _lib.ptr(attn_out), 0 if attn_out is None else attn_out.stride(0),
+                  _lib.stream_ptr())
+        ko = w.w_out.shape[1]
+        K.pack(scratch, [(top, H, 1), (cur.ctx, C_, 1)], k_pad=ko, **kw)
+        K.gemm(scratch, w.w_out, k=ko, bias=w.b_out, out=logits, m=m, m_dev=m_dev, rows=rows)
+        K.log_softmax_rows(logits, am_logp, d.vocab, m=m, m_dev=m_dev, rows=rows)
+
+
+@dataclass
+class _UttState:
+    enc: torch.Tensor      # [1, T, C]
+    keys: torch.Tensor     # [1, T, A]
+    T: int
+    am: AmState            # n rows
+
+
+class AttnLstmScorer:
+    """AcousticScorer over the device attention-LSTM model."""
+
+    is_device_scorer = True
+
+    def __init__(self, W: Dict[str, np.ndarray], dims: AsrDims, eos_id: int, device=None):
+        self.device = _device(device)
+        self.dims = dims
+        self.eos_id = eos_id
+        self.weights = AsrWeights(W, dims, self.device)
+        self.encoder = Encoder(self.weights, self.device)
+        self.step_fn = DecoderStep(self.weights, eos_id, self.device)
+
+    # ---- reference AcousticScorer protocol (one utterance) ------------------
+    def init(self, features) -> _UttState:
+        enc, keys, T = self.encoder([np.asarray(features.data, np.float32)])
+        d = self.dims
+        return _UttState(enc, keys, T[0], AmState(d.dec_layers, 1, d.dec_hidden, d.ctx,
+                                                  self.device))
+
+    def enc_length(self, state: _UttState) -> int:
+        return state.T
+
+    def step(self, state: _UttState, last_tokens: Sequence[int]):
+        d, dev = self.dims, self.device
+        n = len(last_tokens)
+        cur = AmState(d.dec_layers, n, d.dec_hidden, d.ctx, dev)
+        rows = torch.arange(n, dtype=torch.int32, device=dev)
+        tok = torch.as_tensor(np.asarray(last_tokens, np.int32), device=dev)
+        cfg = _lib.FbSearchCfg(beam=n, vocab=d.vocab, t_max=state.T)
+        one = torch.ones(1, dtype=torch.int32, device=dev)
+        nl = torch.full((1,), n, dtype=torch.int32, device=dev)
+        te = torch.full((1,), state.T, dtype=torch.int32, device=dev)
+        acc0 = torch.zeros((n, state.T), dtype=torch.float64, device=dev)
+        acc1 = torch.empty_like(acc0)
+        attn = torch.empty((n, state.T), dtype=torch.float32, device=dev)
+        scratch = torch.empty((n, self.weights.k_max), dtype=torch.float32, device=dev)
+        q = torch.empty((n, d.att), dtype=torch.float32, device=dev)
+        logits = torch.empty((n, d.vocab), dtype=torch.float32, device=dev)
+        logp = torch.empty((n, d.vocab), dtype=torch.float32, device=dev)
+        self.step_fn(N=n, rows=rows, m=n, m_dev=None, parent=rows, last_tok=tok, prev=state.am,
+                     cur=cur, scratch=scratch, q=q, logits=logits, am_logp=logp,
+                     cfg_ref=C.byref(cfg), num_utts=1, active=one, n_live=nl, t_enc=te,
+                     keys=state.keys, enc=state.enc, acc_in=acc0, acc_out=acc1, cov=None,
+                     attn_out=attn)
+        return (logp.cpu().numpy(), attn.cpu().numpy(),
+                _UttState(state.enc, state.keys, state.T, cur))
+
+    def reorder(self, state: _UttState, parent_indices: Sequence[int]) -> _UttState:
+        idx = torch.as_tensor(np.asarray(parent_indices, np.int64), device=self.device)
+        am = AmState(self.dims.dec_layers, len(idx), self.dims.dec_hidden, self.dims.ctx,
+                     self.device)
+        am.h = state.am.h[:, idx].contiguous()
+        am.c = state.am.c[:, idx].contiguous()
+        am.ctx = state.am.ctx[idx].contiguous()
+        return _UttState(state.enc, state.keys, state.T, am)
+
+
+# ---- word LM -----------------------------------------------------------------
+class LmWeights:
+    def __init__(self, W: Dict[str, np.ndarray], d: LmDims, device):
+        self.d = d
+        H = d.hidden
+        self.v_out = d.words + 3
+        self.k_out = _pad(H)
+        self.emb = _dev(W["lm.emb"], device, self.k_out)      # [V+3, k_out] (tied in/out)
+        self.b_out = _dev(W["lm.b_out"], device)
+        self.layers: List[LstmLayer] = []
+        for l in range(d.layers):
+            w = np.concatenate([W[f"lm.{l}.w_ih"], W[f"lm.{l}.w_hh"]], axis=1)
+            self.layers.append(LstmLayer(_dev(interleave_gates(w, H), device, _pad(2 * H)),
+                                         _dev(interleave_gates(W[f"lm.{l}.b"], H), device),
+                                         2 * H, H))
+        self.k_max = max([l.k_pad for l in self.layers] + [self.k_out])
+        self.eos_tok, self.unk_tok, self.bos_tok = d.words, d.words + 1, d.words + 2
+
+
+def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks,
+            tok_default: int, scratch: torch.Tensor, logits: Optional[torch.Tensor]) -> None:
+    """Batched LSTM-LM step.  Row i: input token ranks[i] (or tok_default),
+    recurrent state from state_src[src_idx[i]] (None -> zero state), new state
+    into state_dst[i]; state tensors are [rows, L, 2, H] (h then c per layer).
+    Optionally logits[i] = E . h_top + b."""
+    H = w.d.hidden
+    L = len(w.layers)
+    for l, lay in enumerate(w.layers):
+        if l == 0:
+            x = (w.emb, H, 4, w.emb.stride(0))
+        else:
+            x = (state_dst[:, l - 1, 0], H, 0, state_dst.stride(0))
+        if state_src is None:
+            hseg = (None, H, 1, 0)
+            c_in = None
+        else:
+            hseg = (state_src[:, l, 0], H, 1, state_src.stride(0))
+            c_in = state_src[:, l, 1]
+        K.pack(scratch, [x, hseg], m=m, m_dev=m_dev, rows=src_idx, ranks=ranks,
+               tok_default=tok_default, k_pad=lay.k_pad)
+        K.gemm(scratch, lay.w, m=m, m_dev=m_dev, k=lay.k_pad, bias=lay.b, mode=1, hidden=H,
+               parent=src_idx, c_in=c_in, c_out=state_dst[:, l, 1], h_out=state_dst[:, l, 0])
+    if logits is not None:
+        K.pack(scratch, [(state_dst[:, L - 1, 0], H, 0, state_dst.stride(0))], m=m, m_dev=m_dev,
+               k_pad=w.k_out)
+        K.gemm(scratch, w.emb, m=m, m_dev=m_dev, k=w.k_out, bias=w.b_out, out=logits)
+
+
+class _DevHist:
+    __slots__ = ("uid", "state", "logits", "_eos")
+    _ids = itertools.count()
+
+    def __init__(self, state, logits):
+        self.uid = next(_DevHist._ids)
+        self.state = state            # [1, L, 2, H]
+        self.logits = logits          # [1, V+3]
+        self._eos = None
+
+
+class LstmWordLM:
+    """WordLM over the device LSTM LM (outputs: ranks, </s>, <unk>, <s>)."""
+
+    is_device_lm = True
+
+    def __init__(self, W: Dict[str, np.ndarray], dims: LmDims, device=None):
+        self.device = _device(device)
+        self.dims = dims
+        self.vocab_size = dims.words
+        self.weights = LmWeights(W, dims, self.device)
+        self._kids: Dict[tuple, _DevHist] = {}
+        self._root = self._run(None, self.weights.bos_tok)
+
+    def _run(self, parent: Optional[_DevHist], token: int) -> _DevHist:
+        w, d, dev = self.weights, self.dims, self.device
+        st = torch.empty((1, d.layers, 2, d.hidden), dtype=torch.float32, device=dev)
+        lg = torch.empty((1, w.v_out), dtype=torch.float32, device=dev)
+        scratch = torch.empty((1, w.k_max), dtype=torch.float32, device=dev)
+        lm_step(w, m=1, m_dev=None, state_src=None if parent is None else parent.state,
+                src_idx=None, state_dst=st, ranks=None, tok_default=token, scratch=scratch,
+                logits=lg)
+        return _DevHist(st, lg)
+
+    def start_history(self) -> _DevHist:
+        return self._root
+
+    def extend_history(self, hist: _DevHist, rank: int) -> _DevHist:
+        if rank != -1 and not 0 <= rank < self.vocab_size:
+            raise ValueError(f"word rank {rank} out of range")
+        key = (hist.uid, rank)
+        kid = self._kids.get(key)
+        if kid is None:
+            kid = self._run(hist, self.weights.unk_tok if rank == -1 else rank)
+            self._kids[key] = kid
+        return kid
+
+    def full_distribution(self, hist: _DevHist) -> np.ndarray:
+        g = torch.empty((1, self.vocab_size), dtype=torch.float64, device=self.device)
+        K.logits_to_g(hist.logits, self.vocab_size, self.weights.v_out, m=1, g_pool=g)
+        return np.diff(g[0].cpu().numpy(), prepend=0.0)
+
+    def eos_log_prob(self, hist: _DevHist) -> float:
+        if hist._eos is None:
+            out = torch.empty(1, dtype=torch.float64, device=self.device)
+            K.logits_to_g(hist.logits, self.vocab_size, self.weights.v_out, m=1, eos_out=out)
+            hist._eos = float(out.item())
+        return hist._eos
+
+    def write_g_rows(self, hists: List[_DevHist], pool: torch.Tensor, slots: torch.Tensor) -> None:
+        lg = torch.cat([h.logits for h in hists], dim=0)
+        K.logits_to_g(lg, self.vocab_size, self.weights.v_out, m=len(hists), slots=slots,
+                      g_pool=pool)

@@ -1,0 +1,141 @@
+"""GPU parity of the neural scorers and the fused engine against the CPU oracle
+(PyTorch-CPU fp32 restatement, oracle/neural.py) on the same random-init
+weights and synthetic fbank (BASELINE.json north_star: identical hypotheses
+except on near-ties, per-hypothesis scores within 1e-4)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle.lexicon import OracleDict, build_trie as oracle_build_trie
+from oracle.lookahead import OracleLookahead
+from oracle.neural import OracleAttnLstmScorer, OracleLstmWordLM
+from oracle.search import OracleConfig, decode_batch as oracle_decode
+from test_oracle_golden import _Feat
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+SCORE_TOL = 1e-4       # north star: per-hypothesis scores within 1e-4 absolute
+TIE_TOL = 1e-4         # decisions closer than this are near-ties (exempt)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu(cuda_lib):
+    return cuda_lib
+
+
+def small_setup(n_words=300, seed=5):
+    from paper_1909_08723_b200 import synth
+    import paper_1909_08723_b200 as fb
+    d = fb.TokenDictionary(synth.wsj_token_list())
+    words = synth.synth_lexicon(n_words, seed=seed)
+    ad = synth.AsrDims(enc_layers=2, enc_hidden=32, dec_layers=2, dec_hidden=32, emb=16, att=32,
+                       out_scale=0.6)
+    ld = synth.LmDims(layers=2, hidden=48, words=n_words, emb_scale=0.3, eos_bias=2.0)
+    W = synth.asr_weights(ad, seed=7, eos_id=d.eos_id)
+    W.update(synth.lm_weights(ld, seed=8))
+    return fb, synth, d, words, ad, ld, W
+
+
+def test_scorer_rows_match_oracle():
+    fb, synth, d, words, ad, ld, W = small_setup()
+    from paper_1909_08723_b200.models import AttnLstmScorer
+    gpu = AttnLstmScorer(W, ad, d.eos_id)
+    cpu = OracleAttnLstmScorer(W, ad.enc_layers, ad.dec_layers, ad.subsample, d.eos_id)
+    for uid, x in synth.synth_fbank(3, seed=9, frames=(40, 90)):
+        f = fb.FeatureMatrix(uid, x)
+        sg, sc = gpu.init(f), cpu.init(f)
+        assert gpu.enc_length(sg) == cpu.enc_length(sc)
+        last = [-1]
+        rng = np.random.default_rng(0)
+        for step in range(6):
+            lg, ag, sg = gpu.step(sg, last)
+            lc, ac, sc = cpu.step(sc, last)
+            np.testing.assert_allclose(lg, lc, rtol=0, atol=2e-5)
+            np.testing.assert_allclose(ag, ac, rtol=0, atol=2e-6)
+            par = sorted(rng.integers(0, len(last), size=3).tolist())
+            sg, sc = gpu.reorder(sg, par), cpu.reorder(sc, par)
+            last = rng.integers(0, len(d), size=3).tolist()
+
+
+def test_word_lm_matches_oracle():
+    fb, synth, d, words, ad, ld, W = small_setup()
+    from paper_1909_08723_b200.models import LstmWordLM
+    gpu = LstmWordLM(W, ld)
+    cpu = OracleLstmWordLM(W, ld.layers, ld.words)
+    hg, hc = gpu.start_history(), cpu.start_history()
+    for r in [3, -1, 17, 299, 0]:
+        np.testing.assert_allclose(gpu.full_distribution(hg), cpu.full_distribution(hc),
+                                   rtol=2e-5, atol=1e-12)
+        assert abs(gpu.eos_log_prob(hg) - cpu.eos_log_prob(hc)) < 2e-5
+        hg, hc = gpu.extend_history(hg, r), cpu.extend_history(hc, r)
+
+
+def _compare(got, want, what):
+    exempt = 0
+    for a, b in zip(got, want):
+        assert a.utt_id == b.utt_id
+        if a.tokens != b.tokens or a.finished != b.finished:
+            assert b.margin < TIE_TOL, (what, a.utt_id, a.tokens, b.tokens, b.margin)
+            exempt += 1
+            continue
+        assert abs(a.score - b.score) <= SCORE_TOL, (what, a.utt_id, a.score, b.score)
+        np.testing.assert_allclose(a.attn_accum, b.attn_accum, atol=1e-4)
+    assert exempt <= max(1, len(got) // 5), (what, exempt)
+    return exempt
+
+
+@pytest.mark.parametrize("cfg", [
+    dict(beam_size=4, lm_weight=0.5),
+    dict(beam_size=6, lm_weight=0.9, coverage_mode="improved", coverage_weight=0.02, eos_gamma=1.5),
+    dict(beam_size=3, lm_weight=0.0),
+    dict(beam_size=5, lm_weight=0.0, coverage_mode="original", coverage_weight=0.05),
+])
+def test_fused_engine_matches_oracle(cfg):
+    fb, synth, d, words, ad, ld, W = small_setup()
+    from paper_1909_08723_b200.models import AttnLstmScorer, LstmWordLM
+    utts = synth.synth_fbank(6, seed=9, frames=(40, 96))
+    feats = [fb.FeatureMatrix(u, x) for u, x in utts]
+    trie = fb.build_trie(words, d)
+    gpu_sc = AttnLstmScorer(W, ad, d.eos_id)
+    fus = None
+    if cfg["lm_weight"] > 0:
+        fus = fb.LookaheadFusion(trie, LstmWordLM(W, ld), d)
+    got = fb.decode_batch(feats, gpu_sc, fus, fb.DecodeConfig(**cfg), d)
+    od = OracleDict(synth.wsj_token_list())
+    cpu_sc = OracleAttnLstmScorer(W, ad.enc_layers, ad.dec_layers, ad.subsample, od.eos_id)
+    ofus = None
+    if cfg["lm_weight"] > 0:
+        ofus = OracleLookahead(oracle_build_trie(words, od), OracleLstmWordLM(W, ld.layers, ld.words), od)
+    want = oracle_decode([_Feat(u, x) for u, x in utts], cpu_sc, ofus, OracleConfig(**cfg), od)
+    _compare(got, want, cfg)
+
+
+def test_plugin_driver_agrees_with_fused_engine():
+    """Same device scorer through the generic plugin driver (host rows) and the
+    fused engine: both GPU paths must agree."""
+    fb, synth, d, words, ad, ld, W = small_setup()
+    from paper_1909_08723_b200.models import AttnLstmScorer, LstmWordLM
+
+    class Plain:                        # hides is_device_scorer -> plugin driver
+        def __init__(self, s):
+            self.s = s
+
+        def __getattr__(self, k):
+            if k == "is_device_scorer":
+                raise AttributeError(k)
+            return getattr(self.s, k)
+
+    utts = synth.synth_fbank(4, seed=19, frames=(40, 80))
+    feats = [fb.FeatureMatrix(u, x) for u, x in utts]
+    trie = fb.build_trie(words, d)
+    sc = AttnLstmScorer(W, ad, d.eos_id)
+    lm = LstmWordLM(W, ld)
+    cfg = fb.DecodeConfig(beam_size=4, lm_weight=0.5)
+    a = fb.decode_batch(feats, sc, fb.LookaheadFusion(trie, lm, d), cfg, d)
+    b = fb.decode_batch(feats, Plain(sc), fb.LookaheadFusion(trie, lm, d), cfg, d)
+    for x, y in zip(a, b):
+        assert x.tokens == y.tokens
+        assert abs(x.score - y.score) < 1e-6
