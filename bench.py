@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark of the fused look-ahead beam decoder (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (BASELINE.json configs[1], "c2"): WSJ-shaped random-init model
+(4-layer BiLSTM 320 encoder, 3-layer attention-LSTM decoder, 52 tokens),
+beam 10, look-ahead fusion with a 65k-word random-init 3x1200 LSTM LM over the
+character prefix trie, 512 synthetic 80-dim fbank utterances of 700..900
+frames per GPU (weak scaling: every rank decodes its own 512-utterance
+shard, only a final host gather).  One "step" = one decode of the whole
+512-utterance batch (encoder + lock-step beam search + LM fusion).
+
+Output: ONE JSON line on rank 0 (see the task contract): utt/s (value = device-
+resident inputs, e2e = public decode_batch API with host features), RTF, the
+dominant kernel's roofline fraction, the same-run CPU baseline (the oracle
+port on the host cores), launch count and clocks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--utts", type=int, default=None, help="override utterances per GPU")
+    ap.add_argument("--words", type=int, default=None, help="override LM vocabulary (debug)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-utts", type=int, default=0, help="CPU baseline sample (0 = auto)")
+    ap.add_argument("--stats", action="store_true", help="print decode statistics to stderr")
+    ap.add_argument("--set", action="append", default=[],
+                    help="calibration override, e.g. asr.out_scale=0.7 or lm.eos_bias=5")
+    ap.add_argument("--profile-only", action="store_true",
+                    help="one decode for ncu (no timing, no JSON)")
+    return ap.parse_args()
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------- workload --
+def build_inputs(wl_name: str, rank: int, n_utts=None, words=None, overrides=()):
+    from paper_1909_08723_b200 import synth
+    from paper_1909_08723_b200.token_dict import TokenDictionary
+    from paper_1909_08723_b200.lexicon_trie import build_trie
+    import dataclasses
+    wl = synth.WORKLOADS[wl_name]
+    if n_utts is not None:
+        wl = dataclasses.replace(wl, n_utts=n_utts, batch_size=min(wl.batch_size, n_utts))
+    if words is not None and wl.lm is not None:
+        wl = dataclasses.replace(wl, lm=dataclasses.replace(wl.lm, words=words))
+    for ov in overrides:
+        key, val = ov.split("=")
+        part, field = key.split(".")
+        if part == "wl":
+            wl = dataclasses.replace(wl, **{field: type(getattr(wl, field))(val)})
+        else:
+            sub = getattr(wl, part)
+            wl = dataclasses.replace(wl, **{part: dataclasses.replace(sub, **{field: float(val)})})
+    d = TokenDictionary(synth.wsj_token_list())
+    W = synth.asr_weights(wl.asr, seed=wl.seed, eos_id=d.eos_id)
+    words_l, trie = None, None
+    if wl.lm is not None:
+        W.update(synth.lm_weights(wl.lm, seed=wl.seed + 1))
+        words_l = synth.synth_lexicon(wl.lm.words, seed=wl.seed + 2)
+        trie = build_trie(words_l, d)
+    utts = synth.synth_fbank(wl.n_utts, seed=wl.seed + 100 + rank, frames=wl.frames,
+                             feat_dim=wl.asr.feat_dim, sort_by_length=True)
+    return wl, d, W, words_l, trie, utts
+
+
+def decode_config(wl):
+    from paper_1909_08723_b200.decoder import DecodeConfig
+    return DecodeConfig(beam_size=wl.beam, lm_weight=wl.lm_weight,
+                        coverage_mode=wl.coverage_mode, coverage_weight=wl.coverage_weight,
+                        eos_gamma=wl.eos_gamma, max_len_ratio=wl.max_len_ratio)
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms (timed region)."""
+
+    Q = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        sm, mx = [], None
+        for r in self.rows:
+            try:
+                s, m, util = float(r[0]), float(r[1]), float(r[2])
+            except ValueError:
+                continue
+            mx = m
+            if util > 0:
+                sm.append(s)
+            for k, name in enumerate(names):
+                if r[3 + k].lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------- CPU baseline --
+def cpu_decode(wl, d, W, words, utts, n: int, threads: int):
+    """The oracle CPU decoder (restated reference search + PyTorch-CPU fp32
+    adapters) on the first n utterances; returns (seconds, results)."""
+    import torch
+    from oracle.lexicon import OracleDict, build_trie as obuild
+    from oracle.lookahead import OracleLookahead
+    from oracle.neural import OracleAttnLstmScorer, OracleLstmWordLM
+    from oracle.search import OracleConfig, decode_batch as odecode
+    torch.set_num_threads(threads)
+    od = OracleDict(_file_tokens(d))
+    sc = OracleAttnLstmScorer(W, wl.asr.enc_layers, wl.asr.dec_layers, wl.asr.subsample,
+                              od.eos_id)
+    fus = None
+    if wl.lm is not None:
+        lm = OracleLstmWordLM(W, wl.lm.layers, wl.lm.words)
+        fus = OracleLookahead(obuild(words, od), lm, od)
+    cfg = OracleConfig(beam_size=wl.beam, lm_weight=wl.lm_weight,
+                       coverage_mode=wl.coverage_mode, coverage_weight=wl.coverage_weight,
+                       eos_gamma=wl.eos_gamma, max_len_ratio=wl.max_len_ratio)
+
+    class F:
+        def __init__(self, u, x):
+            self.utt_id, self.data = u, x
+
+    feats = [F(u, x) for u, x in utts[:n]]
+    t0 = time.perf_counter()
+    res = odecode(feats, sc, fus, cfg, od)
+    return time.perf_counter() - t0, res
+
+
+def _file_tokens(d):
+    from paper_1909_08723_b200 import synth
+    return synth.wsj_token_list()
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU algorithm (oracle port; the
+    reference is pure Python and does not compile) on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    wl, d, W, words, trie, utts = build_inputs(args.config, 0, args.utts, args.words, args.set)
+    threads = len(os.sched_getaffinity(0))
+    n = args.cpu_utts or 1
+    times = []
+    for i in range(args.warmup + args.steps):
+        dt, _ = cpu_decode(wl, d, W, words, utts, n, threads)
+        if i >= args.warmup:
+            times.append(dt)
+    value = n * len(times) / sum(times)
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "utt/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
+        "config": workload_config(wl),
+        "cpu_baseline": {"value": value, "unit": "utt/s", "cores": threads, "kind": "port",
+                         "sample": f"{n} of the {wl.n_utts} {wl.name} utterances per step"},
+        "e2e": {"value": value, "unit": "utt/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+METRIC = "utterances/sec and RTF, beam-10 look-ahead word-LM decode"
+
+
+def workload_config(wl):
+    return {"workload": f"{wl.name}: WSJ-shaped 4x BiLSTM-320 encoder + 3x LSTM-320 attention "
+                        f"decoder (52 tokens), beam {wl.beam}, look-ahead fusion with a "
+                        f"{wl.lm.words if wl.lm else 0}-word 3x1200 LSTM LM, "
+                        f"{wl.n_utts} utts/GPU of {wl.frames[0]}-{wl.frames[1]} frames",
+            "utts_per_gpu": wl.n_utts, "frames": list(wl.frames), "beam": wl.beam,
+            "lm_words": wl.lm.words if wl.lm else 0, "lm_weight": wl.lm_weight,
+            "coverage": wl.coverage_mode, "eos_gamma": wl.eos_gamma,
+            "l2": "working set >> L2 (LM weights 312 MB, g pool GBs): no flush needed",
+            "length_sorted": True}
+
+
+# ------------------------------------------------------------------- main --
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+
+    from paper_1909_08723_b200 import _lib
+    from paper_1909_08723_b200.fusion import LookaheadFusion
+    from paper_1909_08723_b200.models import AttnLstmScorer, LstmWordLM
+    from paper_1909_08723_b200.engine import FusedDecoder, StageTimer
+    from paper_1909_08723_b200.decoder import decode_batch
+    from paper_1909_08723_b200.kaldi_io import FeatureMatrix
+
+    t_setup = time.perf_counter()
+    wl, d, W, words, trie, utts = build_inputs(args.config, rank, args.utts, args.words, args.set)
+    cfg = decode_config(wl)
+    scorer = AttnLstmScorer(W, wl.asr, d.eos_id)
+    fusion = None
+    if wl.lm is not None:
+        fusion = LookaheadFusion(trie, LstmWordLM(W, wl.lm), d)
+    feats = [FeatureMatrix(u, x) for u, x in utts]
+    frames = sum(x.shape[0] for _, x in utts)
+    X_host, T = scorer.encoder.stage([x for _, x in utts], pin=True)
+    X_dev = X_host.to(scorer.device)
+    ids = [u for u, _ in utts]
+    dec = FusedDecoder(scorer, fusion, cfg, d)
+    log(f"[rank {rank}] setup {time.perf_counter() - t_setup:.1f}s; {len(utts)} utts, "
+        f"{frames} frames")
+
+    if args.profile_only:
+        dec.run(X_dev, T, ids)
+        torch.cuda.synchronize()
+        return 0
+
+    for _ in range(args.warmup):
+        res = dec.run(X_dev, T, ids)
+    torch.cuda.synchronize()
+
+    # ---- timed: device-resident inputs ----
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = _lib.lib().fb_launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        res = dec.run(X_dev, T, ids)
+    ev1.record()
+    torch.cuda.synchronize()
+    launches = (_lib.lib().fb_launch_count() - l0) // args.steps
+    ms = ev0.elapsed_time(ev1) / args.steps
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * len(utts) / (ms / 1000.0)
+    rtf = (ms / 1000.0) / (frames * 0.010)
+
+    # ---- e2e: the public decode_batch API, host features in, results out ----
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        res_e2e = decode_batch(feats, scorer, fusion, cfg, d)
+    e1.record()
+    torch.cuda.synchronize()
+    ms_e2e = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms_e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    h2d = X_host.numel() * 4
+    d2h = sum(4 * (len(r.tokens) + 4) + 8 * r.attn_accum.size for r in res_e2e)
+
+    # ---- instrumented pass: stage breakdown + dominant kernel roofline ----
+    timer = StageTimer()
+    dec.run(X_dev, T, ids, timer=timer, record_counts=True)
+    stages = timer.summary()
+    peaks = _peaks()
+    roof = None
+    if "lm_out_gemm" in stages and dec.spec_counts is not None:
+        cnt = dec.spec_counts.numpy()
+        H, vout = wl.lm.hidden, wl.lm.words + 3
+        flops = 2.0 * float(cnt[:, 0].sum() + cnt[:, 2].sum()) * vout * H
+        tms, nl = stages["lm_out_gemm"]
+        ach = flops / (tms / 1000.0) / 1e12
+        peak = peaks.get("bf16_tflops_sustained") or 1398.2
+        roof = {"kernel": "lm_out_gemm (word-LM output projection, fp32 SIMT v1)",
+                "bound": "tensor", "achieved": round(ach, 2), "peak": peak, "unit": "TFLOP/s",
+                "frac": round(ach / peak, 4), "traffic": None,
+                "flops_per_launch": flops / nl, "launches": nl,
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"}
+    step_total = sum(v[0] for k, v in stages.items() if k != "lm_out_gemm")
+
+    out_res = res
+    steps_mean = float(np.mean([r.steps for r in out_res]))
+    fin_frac = float(np.mean([r.finished for r in out_res]))
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        n = args.cpu_utts or 1
+        dt, cres = cpu_decode(wl, d, W, words, utts, n, threads)
+        cpu = {"value": n / dt, "unit": "utt/s", "cores": threads, "kind": "port",
+               "sample": f"{n} of the {len(utts)} {wl.name} utterances (shortest), same "
+                         f"weights/inputs, oracle restatement of the reference decoder"}
+        match = sum(a.tokens == b.tokens for a, b in zip(res, cres))
+        cpu["tokens_match_gpu"] = f"{match}/{n}"
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": "utt/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 model / f64 scores", "data": "synthetic (seeded random-init weights, "
+            "N(0,1) fbank)", "config": workload_config(wl),
+            "rtf": rtf, "audio_seconds_per_step": frames * 0.010 * world,
+            "e2e": {"value": round(world * len(utts) / (ms_e2e / 1000.0), 3), "unit": "utt/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "paper_1909_08723_b200.decode_batch (host FeatureMatrix list)"},
+            "roofline": roof, "cpu_baseline": cpu, "gpu_launches": int(launches),
+            "clocks": clk,
+            "stages_ms_per_decode": {k: round(v[0], 3) for k, v in stages.items()},
+            "decode_steps_mean": steps_mean, "finished_frac": fin_frac,
+        }
+        print(json.dumps(out), flush=True)
+        if args.stats:
+            log("distinct outputs:", len({tuple(r.tokens) for r in out_res}), "of", len(out_res),
+                "mean len", float(np.mean([len(r.tokens) for r in out_res])))
+            for r in out_res[:5]:
+                log(r.utt_id, r.steps, r.finished, round(r.score, 3), d.detokenize(r.tokens)[:120])
+            if dec.spec_counts is not None:
+                c = dec.spec_counts.numpy()
+                log("spec/bnd/unk per step mean:", c.mean(axis=0), "max:", c.max(axis=0))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -72,101 +72,184 @@ class _LmPool:
         K.logits_to_g(self.ev_logits, lw.d.words, lw.v_out, m=1, g_pool=self.g, eos_out=self.eos)
 
 
+class StageTimer:
+    """CUDA-event spans per named stage on the current stream (instrumented
+    runs only; the timed bench pass runs without it)."""
+
+    def __init__(self):
+        self.spans = {}
+
+    def __call__(self, name: str):
+        return _Span(self, name)
+
+    def summary(self):
+        torch.cuda.synchronize()
+        out = {}
+        for k, lst in self.spans.items():
+            out[k] = (sum(a.elapsed_time(b) for a, b in lst), len(lst))
+        return out
+
+
+class _Span:
+    def __init__(self, t: StageTimer, name: str):
+        self.t, self.name = t, name
+
+    def __enter__(self):
+        self.a = torch.cuda.Event(enable_timing=True)
+        self.b = torch.cuda.Event(enable_timing=True)
+        self.a.record()
+        return self
+
+    def __exit__(self, *exc):
+        self.b.record()
+        self.t.spans.setdefault(self.name, []).append((self.a, self.b))
+
+
+class _NoTimer:
+    def __call__(self, name):
+        return self
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
 def decode_fused(features, scorer, fusion, config: DecodeConfig, token_dict
                  ) -> List[DecodeResult]:
-    dev = scorer.device
-    w = scorer.weights
-    d = w.d
-    if len(token_dict) != d.vocab:
-        raise ConfigError(f"acoustic model scores {d.vocab} tokens but the dictionary has"
-                          f" {len(token_dict)}")
-    B = len(features)
-    if B == 0:
-        return []
-    Kb = config.beam_size
-    N = B * Kb
-    V = len(token_dict)
-    stream = _lib.stream_ptr()
-    enc, keys, T = scorer.encoder([np.asarray(f.data, np.float32) for f in features])
-    TM = max(T)
-    max_len = [max(1, int(math.floor(config.max_len_ratio * t))) for t in T]
-    MT = max(max_len) + 1
-    buf = SearchBuffers(B, Kb, MT, TM, dev)
-    buf.max_len.copy_(torch.as_tensor(max_len, dtype=torch.int32))
-    buf.t_enc.copy_(torch.as_tensor(T, dtype=torch.int32))
-    has_fusion = fusion is not None
-    early = (not has_fusion) or bool(fusion.nonpositive_scores)
-    cfg = search_cfg(config, token_dict, has_fusion, early, True, MT, TM)
-    cfg_ref = C.byref(cfg)
-    _lib.call("fb_search_init", cfg_ref, C.byref(buf.view(0)), B, stream)
-    rows = [torch.zeros(N, dtype=torch.int32, device=dev) for _ in range(2)]
-    count = [torch.zeros(1, dtype=torch.int32, device=dev) for _ in range(2)]
-    rows[0][:B] = torch.arange(B, dtype=torch.int32, device=dev) * Kb
-    count[0].fill_(B)
-    views = [_view_with_rows(buf, p, rows[1 - p], count[1 - p]) for p in range(2)]
+    """decode_batch entry: host features -> staged device batch -> engine."""
+    X, T = scorer.encoder.stage([np.asarray(f.data, np.float32) for f in features])
+    X = X.to(scorer.device)
+    return FusedDecoder(scorer, fusion, config, token_dict).run(
+        X, T, [f.utt_id for f in features])
 
-    L, H, C_ = d.dec_layers, d.dec_hidden, d.ctx
-    X = [AmState(L, N, H, C_, dev), AmState(L, N, H, C_, dev)]
-    scratch = torch.empty((N, w.k_max), dtype=torch.float32, device=dev)
-    q = torch.empty((N, d.att), dtype=torch.float32, device=dev)
-    logits = torch.empty((N, V), dtype=torch.float32, device=dev)
-    am_logp = torch.zeros((N, V), dtype=torch.float32, device=dev)
 
-    lm = None
-    fus_buf = None
-    if has_fusion:
-        lw = fusion.word_lm.weights
-        lm = _LmPool(lw, N, dev)
-        lm.start()
-        fus_buf = torch.zeros((N, V), dtype=torch.float64, device=dev)
-        dtrie = fusion.dtrie
-        Vw = lw.d.words
+class FusedDecoder:
+    def __init__(self, scorer, fusion, config: DecodeConfig, token_dict):
+        d = scorer.weights.d
+        if len(token_dict) != d.vocab:
+            raise ConfigError(f"acoustic model scores {d.vocab} tokens but the dictionary"
+                              f" has {len(token_dict)}")
+        self.scorer, self.fusion, self.config, self.token_dict = scorer, fusion, config, token_dict
+        self.spec_counts: Optional[torch.Tensor] = None
+        self.steps_run = 0
 
-    parity = 0
-    while True:
-        c = parity
-        rc, nc = rows[c], count[c]
-        scorer.step_fn(N=N, rows=rc, m=N, m_dev=nc, parent=buf.parent, last_tok=buf.last_tok,
-                       prev=X[1 - c], cur=X[c], scratch=scratch, q=q, logits=logits,
-                       am_logp=am_logp, cfg_ref=cfg_ref, num_utts=B, active=buf.active,
-                       n_live=buf.n_live, t_enc=buf.t_enc, keys=keys, enc=enc,
-                       acc_in=buf.acc[c], acc_out=buf.acc[1 - c], cov=buf.cov)
+    def run(self, X: torch.Tensor, T: Sequence[int], utt_ids: Sequence[str], timer=None,
+            record_counts: bool = False) -> List[DecodeResult]:
+        scorer, fusion, config, token_dict = self.scorer, self.fusion, self.config, self.token_dict
+        tm = timer if timer is not None else _NoTimer()
+        dev = scorer.device
+        w = scorer.weights
+        d = w.d
+        B = len(T)
+        if B == 0:
+            return []
+        Kb = config.beam_size
+        N = B * Kb
+        V = len(token_dict)
+        stream = _lib.stream_ptr()
+        with tm("encoder"):
+            enc, keys, T = scorer.encoder(X, T)
+        TM = max(T)
+        max_len = [max(1, int(math.floor(config.max_len_ratio * t))) for t in T]
+        MT = max(max_len) + 1
+        buf = SearchBuffers(B, Kb, MT, TM, dev)
+        buf.max_len.copy_(torch.as_tensor(max_len, dtype=torch.int32))
+        buf.t_enc.copy_(torch.as_tensor(T, dtype=torch.int32))
+        has_fusion = fusion is not None
+        early = (not has_fusion) or bool(fusion.nonpositive_scores)
+        cfg = search_cfg(config, token_dict, has_fusion, early, True, MT, TM)
+        cfg_ref = C.byref(cfg)
+        _lib.call("fb_search_init", cfg_ref, C.byref(buf.view(0)), B, stream)
+        rows = [torch.zeros(N, dtype=torch.int32, device=dev) for _ in range(2)]
+        count = [torch.zeros(1, dtype=torch.int32, device=dev) for _ in range(2)]
+        rows[0][:B] = torch.arange(B, dtype=torch.int32, device=dev) * Kb
+        count[0].fill_(B)
+        views = [_view_with_rows(buf, p, rows[1 - p], count[1 - p]) for p in range(2)]
+
+        L, H, C_ = d.dec_layers, d.dec_hidden, d.ctx
+        X2 = [AmState(L, N, H, C_, dev), AmState(L, N, H, C_, dev)]
+        scratch = torch.empty((N, w.k_max), dtype=torch.float32, device=dev)
+        q = torch.empty((N, d.att), dtype=torch.float32, device=dev)
+        logits = torch.empty((N, V), dtype=torch.float32, device=dev)
+        am_logp = torch.zeros((N, V), dtype=torch.float32, device=dev)
+
+        fus_buf = None
         if has_fusion:
-            _lib.call("fb_spec_events", dtrie.ref, N, P(nc), P(rc), P(lm.trie[c]), P(lm.hist[c]),
-                      P(lm.ev_row), P(lm.ev_rank), P(lm.ev_slot), P(lm.ev_count), P(lm.row_ev),
-                      stream)
-            lm_step(lw, m=N, m_dev=lm.ev_count, state_src=lm.state, src_idx=lm.ev_slot,
-                    state_dst=lm.ev_state, ranks=lm.ev_rank, tok_default=0, scratch=lm.scratch,
-                    logits=lm.ev_logits)
-            K.logits_to_g(lm.ev_logits, Vw, lw.v_out, m=N, m_dev=lm.ev_count, slots=lm.ev_row,
-                          eos_out=lm.ext_eos)
-            _lib.call("fb_lookahead_scores", dtrie.ref, N, P(nc), P(rc), P(lm.trie[c]),
-                      P(lm.hist[c]), P(lm.g), Vw, P(lm.eos), P(lm.ext_eos), fusion.space_id,
-                      fusion.eos_id, fusion.oov_penalty, fusion.score_floor, P(fus_buf), V,
-                      P(fusion._floored), stream)
-        _lib.call("fb_search_step", cfg_ref, C.byref(views[c]), B, P(am_logp), V, P(fus_buf), V,
-                  stream)
-        if has_fusion:
-            rn, cn = rows[1 - c], count[1 - c]
-            _lib.call("fb_trie_advance", dtrie.ref, N, P(cn), P(rn), P(buf.parent),
-                      P(lm.trie[c]), P(lm.hist[c]), P(buf.last_tok), fusion.space_id,
-                      fusion.eos_id, fusion.pad_id, P(lm.trie[1 - c]), P(lm.hist[1 - c]),
-                      P(lm.brank), stream)
-            _lib.call("fb_boundary_plan", N, P(cn), P(rn), P(buf.parent), P(lm.brank),
-                      P(lm.row_ev), P(rc), P(nc), P(lm.hist[c]), P(lm.hist[1 - c]), lm.P,
-                      P(lm.mark), P(lm.bnd_slot), P(lm.bnd_src), P(lm.bnd_count),
-                      P(lm.unk_slot), P(lm.unk_count), N, stream)
-            lm_step(lw, m=N, m_dev=lm.unk_count, state_src=lm.state, src_idx=lm.unk_slot,
-                    state_dst=lm.ev_state[N:], ranks=None, tok_default=lw.unk_tok,
-                    scratch=lm.scratch, logits=lm.ev_logits[N:])
-            K.copy_rows(lm.ev_state, lm.state, m=N, m_dev=lm.bnd_count, src_idx=lm.bnd_src,
-                        dst_idx=lm.bnd_slot)
-            K.logits_to_g(lm.ev_logits, Vw, lw.v_out, m=N, m_dev=lm.bnd_count,
-                          src_rows=lm.bnd_src, slots=lm.bnd_slot, g_pool=lm.g, eos_out=lm.eos)
-        parity ^= 1
-        if int(count[parity].item()) == 0:
-            break
-    return buf.results([f.utt_id for f in features], T)
+            lw = fusion.word_lm.weights
+            lm = _LmPool(lw, N, dev)
+            lm.start()
+            fus_buf = torch.zeros((N, V), dtype=torch.float64, device=dev)
+            dtrie = fusion.dtrie
+            Vw = lw.d.words
+        counts = [] if record_counts else None
+
+        parity = 0
+        steps = 0
+        while True:
+            c = parity
+            rc, nc = rows[c], count[c]
+            with tm("am_step"):
+                scorer.step_fn(N=N, rows=rc, m=N, m_dev=nc, parent=buf.parent,
+                               last_tok=buf.last_tok, prev=X2[1 - c], cur=X2[c], scratch=scratch,
+                               q=q, logits=logits, am_logp=am_logp, cfg_ref=cfg_ref, num_utts=B,
+                               active=buf.active, n_live=buf.n_live, t_enc=buf.t_enc, keys=keys,
+                               enc=enc, acc_in=buf.acc[c], acc_out=buf.acc[1 - c], cov=buf.cov)
+            if has_fusion:
+                with tm("lm_spec"):
+                    _lib.call("fb_spec_events", dtrie.ref, N, P(nc), P(rc), P(lm.trie[c]),
+                              P(lm.hist[c]), P(lm.ev_row), P(lm.ev_rank), P(lm.ev_slot),
+                              P(lm.ev_count), P(lm.row_ev), stream)
+                    lm_step(lw, m=N, m_dev=lm.ev_count, state_src=lm.state, src_idx=lm.ev_slot,
+                            state_dst=lm.ev_state, ranks=lm.ev_rank, tok_default=0,
+                            scratch=lm.scratch, logits=lm.ev_logits, timer=tm)
+                with tm("lm_eos"):
+                    K.logits_to_g(lm.ev_logits, Vw, lw.v_out, m=N, m_dev=lm.ev_count,
+                                  slots=lm.ev_row, eos_out=lm.ext_eos)
+                with tm("lookahead"):
+                    _lib.call("fb_lookahead_scores", dtrie.ref, N, P(nc), P(rc), P(lm.trie[c]),
+                              P(lm.hist[c]), P(lm.g), Vw, P(lm.eos), P(lm.ext_eos),
+                              fusion.space_id, fusion.eos_id, fusion.oov_penalty,
+                              fusion.score_floor, P(fus_buf), V, P(fusion._floored), stream)
+                if counts is not None:
+                    counts.append(lm.ev_count.clone())
+            with tm("select"):
+                _lib.call("fb_search_step", cfg_ref, C.byref(views[c]), B, P(am_logp), V,
+                          P(fus_buf), V, stream)
+            if has_fusion:
+                rn, cn = rows[1 - c], count[1 - c]
+                with tm("advance"):
+                    _lib.call("fb_trie_advance", dtrie.ref, N, P(cn), P(rn), P(buf.parent),
+                              P(lm.trie[c]), P(lm.hist[c]), P(buf.last_tok), fusion.space_id,
+                              fusion.eos_id, fusion.pad_id, P(lm.trie[1 - c]),
+                              P(lm.hist[1 - c]), P(lm.brank), stream)
+                    _lib.call("fb_boundary_plan", N, P(cn), P(rn), P(buf.parent), P(lm.brank),
+                              P(lm.row_ev), P(rc), P(nc), P(lm.hist[c]), P(lm.hist[1 - c]),
+                              lm.P, P(lm.mark), P(lm.bnd_slot), P(lm.bnd_src), P(lm.bnd_count),
+                              P(lm.unk_slot), P(lm.unk_count), N, stream)
+                with tm("lm_unk"):
+                    lm_step(lw, m=N, m_dev=lm.unk_count, state_src=lm.state,
+                            src_idx=lm.unk_slot, state_dst=lm.ev_state[N:], ranks=None,
+                            tok_default=lw.unk_tok, scratch=lm.scratch,
+                            logits=lm.ev_logits[N:], timer=tm)
+                with tm("g_build"):
+                    K.copy_rows(lm.ev_state, lm.state, m=N, m_dev=lm.bnd_count,
+                                src_idx=lm.bnd_src, dst_idx=lm.bnd_slot)
+                    K.logits_to_g(lm.ev_logits, Vw, lw.v_out, m=N, m_dev=lm.bnd_count,
+                                  src_rows=lm.bnd_src, slots=lm.bnd_slot, g_pool=lm.g,
+                                  eos_out=lm.eos)
+                if counts is not None:
+                    counts.append(lm.bnd_count.clone())
+                    counts.append(lm.unk_count.clone())
+            parity ^= 1
+            steps += 1
+            if int(count[parity].item()) == 0:
+                break
+        self.steps_run = steps
+        if counts is not None:
+            self.spec_counts = torch.cat(counts).view(steps, 3).cpu() if counts else None
+        return buf.results(list(utt_ids), T)
 
 
 def _view_with_rows(buf: SearchBuffers, p: int, next_rows, next_count):

@@ -118,23 +118,37 @@ class Encoder:
         self.w = w
         self.device = device
 
-    def __call__(self, feats: Sequence[np.ndarray]):
+    def stage(self, feats: Sequence[np.ndarray], pin: bool = False):
+        """Host-side frame stacking into one [B*TM, Din_pad] array (+ lengths)."""
         d = self.w.d
-        dev = self.device
         B = len(feats)
         T = [int(x.shape[0]) // d.subsample for x in feats]
         if min(T) < 1:
             raise ValueError("utterance shorter than the subsampling factor")
         TM = max(T)
         Din = d.feat_dim * d.subsample
-        x = np.zeros((B, TM, _pad(Din)), np.float32)
+        x = torch.zeros((B, TM, _pad(Din)), dtype=torch.float32, pin_memory=pin)
+        xn = x.numpy()
         for u, f in enumerate(feats):
-            x[u, :T[u], :Din] = f[:T[u] * d.subsample].reshape(T[u], Din)
-        X = torch.as_tensor(x, device=dev).reshape(B * TM, -1)
+            xn[u, :T[u], :Din] = np.asarray(f, np.float32)[:T[u] * d.subsample].reshape(T[u], Din)
+        return x.reshape(B * TM, -1), T
+
+    def __call__(self, feats, lengths: Optional[Sequence[int]] = None):
+        """feats: list of [T, feat_dim] arrays, or a staged device tensor
+        [B*TM, Din_pad] with ``lengths`` (encoder frames per utterance)."""
+        d = self.w.d
+        dev = self.device
+        if lengths is None:
+            X, T = self.stage(feats)
+            X = X.to(dev, non_blocking=False)
+        else:
+            X, T = feats, list(lengths)
+        B = len(T)
+        TM = X.shape[0] // B
         rev = np.arange(B * TM, dtype=np.int32).reshape(B, TM)
         for u in range(B):
             rev[u, :T[u]] = u * TM + np.arange(T[u] - 1, -1, -1)
-        rev_t = torch.as_tensor(rev.reshape(-1), device=dev)
+        rev_t = torch.as_tensor(rev.reshape(-1)).to(dev, non_blocking=True)
         He = d.enc_hidden
         Xr = torch.empty_like(X)
         for l, dirs in enumerate(self.w.enc):
@@ -294,7 +308,8 @@ class LmWeights:
 
 
 def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks,
-            tok_default: int, scratch: torch.Tensor, logits: Optional[torch.Tensor]) -> None:
+            tok_default: int, scratch: torch.Tensor, logits: Optional[torch.Tensor],
+            timer=None) -> None:
     """Batched LSTM-LM step.  Row i: input token ranks[i] (or tok_default),
     recurrent state from state_src[src_idx[i]] (None -> zero state), new state
     into state_dst[i]; state tensors are [rows, L, 2, H] (h then c per layer).
@@ -319,7 +334,11 @@ def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks
     if logits is not None:
         K.pack(scratch, [(state_dst[:, L - 1, 0], H, 0, state_dst.stride(0))], m=m, m_dev=m_dev,
                k_pad=w.k_out)
-        K.gemm(scratch, w.emb, m=m, m_dev=m_dev, k=w.k_out, bias=w.b_out, out=logits)
+        if timer is not None:
+            with timer("lm_out_gemm"):
+                K.gemm(scratch, w.emb, m=m, m_dev=m_dev, k=w.k_out, bias=w.b_out, out=logits)
+        else:
+            K.gemm(scratch, w.emb, m=m, m_dev=m_dev, k=w.k_out, bias=w.b_out, out=logits)
 
 
 class _DevHist:
