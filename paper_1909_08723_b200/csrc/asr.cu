@@ -248,7 +248,8 @@ boundary_plan_kernel(int n_max, const int32_t* __restrict__ n_dev, const int32_t
                      int32_t* __restrict__ hist_next, int num_slots, int32_t* __restrict__ mark,
                      int32_t* __restrict__ bnd_slot, int32_t* __restrict__ bnd_src,
                      int32_t* __restrict__ bnd_count, int32_t* __restrict__ unk_slot,
-                     int32_t* __restrict__ unk_count, int unk_base) {
+                     int32_t* __restrict__ unk_tok, int32_t* __restrict__ unk_count,
+                     int unk_base) {
   __shared__ int wsum[32];
   __shared__ int wsum2[32];
   __shared__ int carry, carry2;
@@ -292,12 +293,13 @@ boundary_plan_kernel(int n_max, const int32_t* __restrict__ n_dev, const int32_t
   __syncthreads();
   for (int b0 = 0; b0 < n; b0 += blockDim.x) {
     const int i = b0 + tid;
-    int is_b = 0, is_unk = 0, r = -1;
+    int is_b = 0, is_unk = 0, r = -1, br = -2;
     if (i < n) {
       r = rows[i];
-      const int br = brank[r];
+      br = brank[r];
       is_b = br >= -1;
-      is_unk = br == -1;
+      // a late LM event unless the parent already ran a speculative one
+      is_unk = is_b && (br == -1 || row_ev[parent[r]] < 0);
     }
     int x = is_b, y = is_unk;
     for (int off = 1; off < 32; off <<= 1) {
@@ -328,6 +330,7 @@ boundary_plan_kernel(int n_max, const int32_t* __restrict__ n_dev, const int32_t
       if (is_unk) {
         const int ku = carry2 + (warp ? wsum2[warp - 1] : 0) + y - 1;
         unk_slot[ku] = hist_cur[p];
+        unk_tok[ku] = br;
         bnd_src[k] = unk_base + ku;
       } else {
         bnd_src[k] = row_ev[p];
@@ -431,14 +434,14 @@ extern "C" int fb_boundary_plan(int32_t n_max, const int32_t* n_dev, const int32
                                 const int32_t* cur_count, const int32_t* hist_cur,
                                 int32_t* hist_next, int32_t num_slots, int32_t* slot_mark,
                                 int32_t* bnd_slot, int32_t* bnd_src, int32_t* bnd_count,
-                                int32_t* unk_slot, int32_t* unk_count, int32_t unk_base,
-                                void* stream) {
+                                int32_t* unk_slot, int32_t* unk_tok, int32_t* unk_count,
+                                int32_t unk_base, void* stream) {
   FB_CHECK_ARG(rows && parent && boundary_rank && cur_rows && cur_count && hist_cur && hist_next,
                "null boundary-plan arguments");
   boundary_plan_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(
       n_max, n_dev, rows, parent, boundary_rank, row_ev, cur_rows, cur_count, hist_cur,
-      hist_next, num_slots, slot_mark, bnd_slot, bnd_src, bnd_count, unk_slot, unk_count,
-      unk_base);
+      hist_next, num_slots, slot_mark, bnd_slot, bnd_src, bnd_count, unk_slot, unk_tok,
+      unk_count, unk_base);
   count_launch();
   return check_launch("boundary_plan");
 }

@@ -372,6 +372,121 @@ search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict
   }
 }
 
+// Exact pruning of speculative <eos> LM events (see fb_spec_select in the
+// header).  One CTA per active utterance; candidates as in search_step.
+template <typename AM>
+__global__ void __launch_bounds__(kSelThreads)
+spec_select_kernel(fb_search_cfg_t c, fb_search_state_t st, fb_trie_t trie,
+                   const int32_t* __restrict__ tstate, const int32_t* __restrict__ hslot,
+                   const AM* __restrict__ am, int64_t am_stride, double* __restrict__ fus,
+                   int64_t f_stride, int32_t* ev_row, int32_t* ev_rank, int32_t* ev_slot,
+                   int32_t* ev_count, int32_t* row_ev) {
+  extern __shared__ unsigned char sm_raw[];
+  const int u = blockIdx.x;
+  if (!st.active[u]) return;
+  const int K = c.beam, V = c.vocab;
+  const int n = st.n_live[u];
+  const int base = u * K;
+  const int NV = n * V;
+  double* cand = reinterpret_cast<double*>(sm_raw);
+  unsigned char* taken = sm_raw + sizeof(double) * NV;
+  __shared__ int gated[64], fin[64], rank_of[64];
+  __shared__ Cand wbest[kSelThreads / 32];
+  __shared__ double s_thr;
+  __shared__ int s_found;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int p = warp; p < n; p += kSelThreads / 32) {
+    const AM* row = am + (int64_t)(base + p) * am_stride;
+    int g = 0;
+    if (c.gate_on) {
+      AM mx = row[0];
+      for (int t = lane; t < V; t += 32) mx = row[t] > mx ? row[t] : mx;
+      for (int off = 16; off; off >>= 1) {
+        const AM o = __shfl_xor_sync(0xffffffffu, mx, off);
+        mx = o > mx ? o : mx;
+      }
+      g = row[c.eos_id] <= (AM)c.gamma * mx;
+    }
+    if (lane == 0) {
+      const int s = tstate[base + p];
+      const int rk = s > 0 ? trie.info[4 * s + 2] : -1;
+      gated[p] = g;
+      fin[p] = rk >= 0;
+      rank_of[p] = rk;
+    }
+  }
+  __syncthreads();
+  // exactly known candidates; uncertain eos-at-final entries are excluded
+  for (int j = tid; j < NV; j += kSelThreads) {
+    const int t = j / n, p = j % n;
+    const bool unsure = (t == c.eos_id) && fin[p] && !gated[p];
+    cand[j] = dadd(st.total_in[base + p],
+                   step_score(c, am, am_stride, fus, f_stride, base + p, t, gated[p]));
+    taken[j] = unsure ? 1 : 0;
+  }
+  __syncthreads();
+  // beam-th best of the known candidates
+  if (tid == 0) { s_thr = -INFINITY; s_found = 0; }
+  __syncthreads();
+  for (int k = 0; k < K; ++k) {
+    Cand b{-INFINITY, INT_MAX};
+    for (int j = tid; j < NV; j += kSelThreads)
+      if (!taken[j]) {
+        Cand x{cand[j], j};
+        if (better(x, b)) b = x;
+      }
+    b = warp_best(b);
+    if (lane == 0) wbest[warp] = b;
+    __syncthreads();
+    if (tid == 0) {
+      Cand w = wbest[0];
+      for (int q = 1; q < kSelThreads / 32; ++q)
+        if (better(wbest[q], w)) w = wbest[q];
+      if (w.j != INT_MAX && w.s != -INFINITY) {
+        taken[w.j] = 1;
+        ++s_found;
+        s_thr = w.s;
+      }
+    }
+    __syncthreads();
+  }
+  const bool prune_ok = s_found == K;   // else every uncertain row must be resolved
+  for (int p = tid; p < n; p += kSelThreads) {
+    const int r = base + p;
+    int e = -1;
+    if (fin[p]) {
+      bool need = true;
+      if (gated[p]) {
+        need = false;                     // -inf either way: no LM step
+      } else if (prune_ok) {
+        const double ub = cand[c.eos_id * n + p];   // total + am + lm_weight * word_end
+        need = !(ub < s_thr);
+      }
+      if (need) {
+        e = atomicAdd(ev_count, 1);
+        ev_row[e] = r;
+        ev_rank[e] = rank_of[p];
+        ev_slot[e] = hslot[r];
+      } else {
+        fus[(int64_t)r * f_stride + c.eos_id] = -INFINITY;
+      }
+    }
+    row_ev[r] = e;
+  }
+}
+
+__global__ void eos_fixup_kernel(int n_max, const int32_t* __restrict__ cnt,
+                                 const int32_t* __restrict__ ev_row,
+                                 const double* __restrict__ eos_lp, double* __restrict__ fus,
+                                 int64_t f_stride, int eos_id) {
+  const int n = row_count(n_max, cnt);
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int r = ev_row[e];
+    double* f = fus + (int64_t)r * f_stride + eos_id;
+    *f = dadd(*f, eos_lp[r]);
+  }
+}
+
 // Deterministic compact list of rows that enter the next step.
 __global__ void compact_rows_kernel(int B, int K, const int32_t* active, const int32_t* n_live,
                                     int32_t* rows, int32_t* count) {
@@ -492,4 +607,44 @@ extern "C" int fb_search_step(const fb_search_cfg_t* cfg, const fb_search_state_
                                          st->next_rows, st->next_count);
   count_launch();
   return check_launch("compact_rows");
+}
+
+extern "C" int fb_spec_select(const fb_search_cfg_t* cfg, const fb_search_state_t* st,
+                              int32_t num_utts, const fb_trie_t* trie, const int32_t* trie_state,
+                              const int32_t* hist_slot, const void* am, int64_t am_stride,
+                              double* fusion, int64_t fusion_stride, int32_t* ev_row,
+                              int32_t* ev_rank, int32_t* ev_slot, int32_t* ev_count,
+                              int32_t* row_ev, void* stream) {
+  FB_CHECK_ARG(cfg && st && trie && am && fusion && ev_count && row_ev, "null spec-select args");
+  const size_t smem = (size_t)cfg->beam * cfg->vocab * (sizeof(double) + 1);
+  if (smem > 200 * 1024) return fail(FB_ERR_CONFIG, "beam x vocabulary too large");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaMemsetAsync(ev_count, 0, sizeof(int32_t), s);
+  if (num_utts <= 0) return check_launch("spec_select");
+  if (cfg->am_f32) {
+    auto k = spec_select_kernel<float>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<num_utts, kSelThreads, smem, s>>>(*cfg, *st, *trie, trie_state, hist_slot,
+                                          (const float*)am, am_stride, fusion, fusion_stride,
+                                          ev_row, ev_rank, ev_slot, ev_count, row_ev);
+  } else {
+    auto k = spec_select_kernel<double>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<num_utts, kSelThreads, smem, s>>>(*cfg, *st, *trie, trie_state, hist_slot,
+                                          (const double*)am, am_stride, fusion, fusion_stride,
+                                          ev_row, ev_rank, ev_slot, ev_count, row_ev);
+  }
+  count_launch();
+  return check_launch("spec_select");
+}
+
+extern "C" int fb_eos_fixup(int32_t n_max, const int32_t* ev_count, const int32_t* ev_row,
+                            const double* eos_lp, double* fusion, int64_t fusion_stride,
+                            int32_t eos_id, void* stream) {
+  FB_CHECK_ARG(ev_row && eos_lp && fusion, "null eos-fixup args");
+  if (n_max <= 0) return FB_OK;
+  eos_fixup_kernel<<<std::min((n_max + 255) / 256, kNumSMs), 256, 0, (cudaStream_t)stream>>>(
+      n_max, ev_count, ev_row, eos_lp, fusion, fusion_stride, eos_id);
+  count_launch();
+  return check_launch("eos_fixup");
 }

@@ -57,10 +57,11 @@ class _LmPool:
         self.trie = [z(N), z(N)]
         self.hist = [z(N), z(N)]
         self.brank = z(N)
-        self.bnd_slot, self.bnd_src, self.unk_slot = z(N), z(N), z(N)
+        self.bnd_slot, self.bnd_src, self.unk_slot, self.unk_tok = z(N), z(N), z(N), z(N)
         self.bnd_count, self.unk_count = z(1), z(1)
         self.mark = z(2 * self.P)
         self.ext_eos = torch.zeros(N, dtype=torch.float64, device=device)
+        self.zero_eos = torch.zeros(N, dtype=torch.float64, device=device)
         self.scratch = torch.empty((N, lw.k_max), dtype=f32, device=device)
 
     def start(self) -> None:
@@ -134,6 +135,7 @@ class FusedDecoder:
         self.scorer, self.fusion, self.config, self.token_dict = scorer, fusion, config, token_dict
         self.spec_counts: Optional[torch.Tensor] = None
         self.steps_run = 0
+        self.prune_spec = True      # exact pruning of speculative <eos> LM events
 
     def run(self, X: torch.Tensor, T: Sequence[int], utt_ids: Sequence[str], timer=None,
             record_counts: bool = False) -> List[DecodeResult]:
@@ -197,21 +199,30 @@ class FusedDecoder:
                                active=buf.active, n_live=buf.n_live, t_enc=buf.t_enc, keys=keys,
                                enc=enc, acc_in=buf.acc[c], acc_out=buf.acc[1 - c], cov=buf.cov)
             if has_fusion:
+                with tm("lookahead"):
+                    # word_end in the eos column of final rows; log P(</s>) added below
+                    _lib.call("fb_lookahead_scores", dtrie.ref, N, P(nc), P(rc), P(lm.trie[c]),
+                              P(lm.hist[c]), P(lm.g), Vw, P(lm.eos), P(lm.zero_eos),
+                              fusion.space_id, fusion.eos_id, fusion.oov_penalty,
+                              fusion.score_floor, P(fus_buf), V, P(fusion._floored), stream)
                 with tm("lm_spec"):
-                    _lib.call("fb_spec_events", dtrie.ref, N, P(nc), P(rc), P(lm.trie[c]),
-                              P(lm.hist[c]), P(lm.ev_row), P(lm.ev_rank), P(lm.ev_slot),
-                              P(lm.ev_count), P(lm.row_ev), stream)
+                    if self.prune_spec:
+                        _lib.call("fb_spec_select", cfg_ref, C.byref(views[c]), B, dtrie.ref,
+                                  P(lm.trie[c]), P(lm.hist[c]), P(am_logp), V, P(fus_buf), V,
+                                  P(lm.ev_row), P(lm.ev_rank), P(lm.ev_slot), P(lm.ev_count),
+                                  P(lm.row_ev), stream)
+                    else:
+                        _lib.call("fb_spec_events", dtrie.ref, N, P(nc), P(rc), P(lm.trie[c]),
+                                  P(lm.hist[c]), P(lm.ev_row), P(lm.ev_rank), P(lm.ev_slot),
+                                  P(lm.ev_count), P(lm.row_ev), stream)
                     lm_step(lw, m=N, m_dev=lm.ev_count, state_src=lm.state, src_idx=lm.ev_slot,
                             state_dst=lm.ev_state, ranks=lm.ev_rank, tok_default=0,
                             scratch=lm.scratch, logits=lm.ev_logits, timer=tm)
                 with tm("lm_eos"):
                     K.logits_to_g(lm.ev_logits, Vw, lw.v_out, m=N, m_dev=lm.ev_count,
                                   slots=lm.ev_row, eos_out=lm.ext_eos)
-                with tm("lookahead"):
-                    _lib.call("fb_lookahead_scores", dtrie.ref, N, P(nc), P(rc), P(lm.trie[c]),
-                              P(lm.hist[c]), P(lm.g), Vw, P(lm.eos), P(lm.ext_eos),
-                              fusion.space_id, fusion.eos_id, fusion.oov_penalty,
-                              fusion.score_floor, P(fus_buf), V, P(fusion._floored), stream)
+                    _lib.call("fb_eos_fixup", N, P(lm.ev_count), P(lm.ev_row), P(lm.ext_eos),
+                              P(fus_buf), V, fusion.eos_id, stream)
                 if counts is not None:
                     counts.append(lm.ev_count.clone())
             with tm("select"):
@@ -227,10 +238,11 @@ class FusedDecoder:
                     _lib.call("fb_boundary_plan", N, P(cn), P(rn), P(buf.parent), P(lm.brank),
                               P(lm.row_ev), P(rc), P(nc), P(lm.hist[c]), P(lm.hist[1 - c]),
                               lm.P, P(lm.mark), P(lm.bnd_slot), P(lm.bnd_src), P(lm.bnd_count),
-                              P(lm.unk_slot), P(lm.unk_count), N, stream)
-                with tm("lm_unk"):
+                              P(lm.unk_slot), P(lm.unk_tok), P(lm.unk_count), N, stream)
+                with tm("lm_late"):
+                    # boundary rows without a speculative event: (h, rank) or (h, <unk>)
                     lm_step(lw, m=N, m_dev=lm.unk_count, state_src=lm.state,
-                            src_idx=lm.unk_slot, state_dst=lm.ev_state[N:], ranks=None,
+                            src_idx=lm.unk_slot, state_dst=lm.ev_state[N:], ranks=lm.unk_tok,
                             tok_default=lw.unk_tok, scratch=lm.scratch,
                             logits=lm.ev_logits[N:], timer=tm)
                 with tm("g_build"):

@@ -139,3 +139,26 @@ def test_plugin_driver_agrees_with_fused_engine():
     for x, y in zip(a, b):
         assert x.tokens == y.tokens
         assert abs(x.score - y.score) < 1e-6
+
+
+def test_spec_pruning_is_exact():
+    """Pruned speculative <eos> LM events give bit-identical decodes."""
+    fb, synth, d, words, ad, ld, W = small_setup()
+    from paper_1909_08723_b200.models import AttnLstmScorer, LstmWordLM
+    from paper_1909_08723_b200.engine import FusedDecoder
+    utts = synth.synth_fbank(8, seed=29, frames=(40, 120))
+    trie = fb.build_trie(words, d)
+    sc = AttnLstmScorer(W, ad, d.eos_id)
+    fus = fb.LookaheadFusion(trie, LstmWordLM(W, ld), d)
+    for cfg in (fb.DecodeConfig(beam_size=5, lm_weight=0.7),
+                fb.DecodeConfig(beam_size=8, lm_weight=0.3, eos_gamma=1.2)):
+        X, T = sc.encoder.stage([x for _, x in utts])
+        X = X.to(sc.device)
+        ids = [u for u, _ in utts]
+        outs = []
+        for prune in (False, True):
+            dec = FusedDecoder(sc, fus, cfg, d)
+            dec.prune_spec = prune
+            outs.append(dec.run(X, T, ids, record_counts=True))
+        for a, b in zip(*outs):
+            assert a.tokens == b.tokens and a.score == b.score and a.steps == b.steps
