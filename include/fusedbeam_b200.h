@@ -187,6 +187,12 @@ typedef struct {
 
 int fb_gemm(const fb_gemm_t* g, void* stream);
 
+/* Same contract on the 5th-gen tensor cores (tcgen05 + TMEM + TMA): A is
+ * a_planes bf16 planes of [a_plane_rows, lda] (the fp32 activation split
+ * hi/mid/lo by fb_pack_rows out_mode 1), W is bf16 [n, ldw]; fp32
+ * accumulation in TMEM.  k % 64 == 0, lda/ldw % 8 == 0. */
+int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_rows, void* stream);
+
 /* Row gather-concatenate into a GEMM A operand:
  *   out[i, :] = [seg0 | seg1 | ... | zero pad up to k_pad], i < m.
  * Segment source row: mode 0 -> i, 1 -> slot = rows[i], 2 -> parent[slot],
@@ -200,7 +206,8 @@ typedef struct {
   int32_t nseg;
   int32_t k_pad;
   int32_t tok_default;
-  int32_t pad0;
+  int32_t out_mode;      /* 0: fp32 rows; 1: three bf16 planes hi/mid/lo     */
+  int64_t plane_rows;    /* out_mode 1: rows per plane ([3][plane_rows][ld])  */
 } fb_pack_t;
 
 int fb_pack_rows(const fb_pack_t* p, int32_t m_max, const int32_t* m_dev, const int32_t* rows,

@@ -58,7 +58,7 @@ class FbSeg(C.Structure):
 
 class FbPack(C.Structure):
     _fields_ = [("seg", FbSeg * 4), ("nseg", i32), ("k_pad", i32), ("tok_default", i32),
-                ("pad0", i32)]
+                ("out_mode", i32), ("plane_rows", i64)]
 
 
 _SIGS = {
@@ -79,6 +79,7 @@ _SIGS = {
                                      i64, vp, vp, vp]),
     "fb_gather_rows": (C.c_int, [i32, vp, vp, vp, i64, vp]),
     "fb_gemm": (C.c_int, [C.POINTER(FbGemm), vp]),
+    "fb_gemm_tc": (C.c_int, [C.POINTER(FbGemm), i32, i64, vp]),
     "fb_pack_rows": (C.c_int, [C.POINTER(FbPack), i32, vp, vp, vp, vp, vp, vp, i64, vp]),
     "fb_log_softmax_rows": (C.c_int, [i32, vp, vp, vp, i64, i32, vp, i64, vp]),
     "fb_attention_step": (C.c_int, [C.POINTER(FbSearchCfg), i32, vp, vp, vp, vp, vp, i32, i32,

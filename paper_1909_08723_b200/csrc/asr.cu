@@ -7,6 +7,8 @@
 // decoder.py:419-425 (accumulator), fusion.py:177-223 (LM events).
 #include "common.cuh"
 
+#include <cuda_bf16.h>
+
 namespace fb {
 
 // ---------------------------------------------------------------- packing --
@@ -17,8 +19,27 @@ __global__ void pack_rows_kernel(fb_pack_t p, int m_max, const int32_t* __restri
                                  const int32_t* __restrict__ ranks, float* __restrict__ out,
                                  int64_t ld_out) {
   const int m = row_count(m_max, m_dev);
+  const bool split = p.out_mode == 1;
+  __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(out);
   for (int i = blockIdx.x; i < m; i += gridDim.x) {
     float* o = out + (int64_t)i * ld_out;
+    __nv_bfloat16* o0 = ob + (int64_t)i * ld_out;
+    __nv_bfloat16* o1 = o0 + p.plane_rows * ld_out;
+    __nv_bfloat16* o2 = o1 + p.plane_rows * ld_out;
+    auto put = [&](int j, float x) {
+      if (!split) {
+        o[j] = x;
+      } else {
+        // x = hi + mid + lo exactly (8+8+8 mantissa bits of the fp32 value)
+        const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+        const float r1 = x - __bfloat162float(hi);
+        const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+        const float r2 = r1 - __bfloat162float(mid);
+        o0[j] = hi;
+        o1[j] = mid;
+        o2[j] = __float2bfloat16_rn(r2);
+      }
+    };
     int col = 0;
     for (int s = 0; s < p.nseg; ++s) {
       const fb_seg_t& sg = p.seg[s];
@@ -32,10 +53,10 @@ __global__ void pack_rows_kernel(fb_pack_t p, int m_max, const int32_t* __restri
         default: { const int t = ranks ? ranks[i] : -1; r = t < 0 ? p.tok_default : t; break; }
       }
       const float* src = sg.src ? sg.src + r * sg.ld : nullptr;
-      for (int j = threadIdx.x; j < sg.width; j += blockDim.x) o[col + j] = src ? src[j] : 0.f;
+      for (int j = threadIdx.x; j < sg.width; j += blockDim.x) put(col + j, src ? src[j] : 0.f);
       col += sg.width;
     }
-    for (int j = col + threadIdx.x; j < p.k_pad; j += blockDim.x) o[j] = 0.f;
+    for (int j = col + threadIdx.x; j < p.k_pad; j += blockDim.x) put(j, 0.f);
   }
 }
 

@@ -1,0 +1,295 @@
+// tcgen05 tensor-core GEMM for sm_100a with the decoder/LM epilogues.
+//
+//   C[m, n] = sum_p sum_k A_p[m, k] * W[n, k]        (p over the bf16 planes)
+//
+// A is the fp32 activation split into 3 bf16 planes (hi/mid/lo: 24 mantissa
+// bits, written by fb_pack_rows), W holds bf16-exact weights, accumulation is
+// fp32 in TMEM -- an fp32-accurate product on the 5th-gen tensor cores
+// (SURVEY.md §7 "GEMM precision").  Algorithmic FLOPs count the product once.
+//
+// Structure (one 128 x BN output tile per CTA, 4 warps):
+//   warp 0 lane 0 : TMA producer, 3-stage smem ring (128B swizzle, K block 64)
+//   warp 1 lane 0 : MMA issuer (tcgen05.mma.cta_group::1.kind::f16, M=128)
+//   warp 1        : TMEM allocator (BN fp32 columns)
+//   all 4 warps   : epilogue, tcgen05.ld 32x32b (warp w owns TMEM lanes 32w..)
+#include "common.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+namespace fb {
+
+constexpr int TC_BM = 128;
+constexpr int TC_BK = 64;            // 64 bf16 = 128 B = one swizzle atom
+constexpr int TC_STAGES = 3;
+constexpr int TC_THREADS = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
+  // K-major, SWIZZLE_128B: start>>4 | SBO (8 rows x 128 B = 1024 B)>>4 << 32 |
+  // version 1 << 46 | layout 2 << 61 (cute::UMMA::SmemDescriptor)
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32"
+      " {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float sigm_tc(float x) { return 1.0f / (1.0f + expf(-x)); }
+
+template <int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
+               fb_gemm_t g, int a_planes, int a_plane_rows, int num_kb) {
+  const int M = row_count(g.m_max, g.m_dev);
+  const int m0 = blockIdx.x * TC_BM, n0 = blockIdx.y * BN;
+  if (m0 >= M) return;
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int A_TILE = TC_BM * TC_BK * 2;         // 16 KB
+  constexpr int W_TILE = BN * TC_BK * 2;
+  const int stage_bytes = a_planes * A_TILE + W_TILE;
+  __shared__ __align__(8) uint64_t bar_full[TC_STAGES], bar_empty[TC_STAGES], bar_done;
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(smem_u32(&bar_full[s]), 1);
+      mbar_init(smem_u32(&bar_empty[s]), 1);
+    }
+    mbar_init(smem_u32(&bar_done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_sh)),
+                 "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer ----
+    for (int kb = 0; kb < num_kb; ++kb) {
+      const int s = kb % TC_STAGES;
+      const uint32_t ph = (kb / TC_STAGES) & 1;
+      mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
+      const uint32_t full = smem_u32(&bar_full[s]);
+      mbar_expect_tx(full, stage_bytes);
+      unsigned char* st = base + (size_t)s * stage_bytes;
+      for (int p = 0; p < a_planes; ++p)
+        tma_load_2d(smem_u32(st + p * A_TILE), &tmA, full, kb * TC_BK, p * a_plane_rows + m0);
+      tma_load_2d(smem_u32(st + a_planes * A_TILE), &tmW, full, kb * TC_BK, n0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer ----
+    // bf16 x bf16 -> f32, K-major A/B, M = 128, N = BN (cute::UMMA::InstrDescriptor)
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(TC_BM >> 4) << 24);
+    for (int kb = 0; kb < num_kb; ++kb) {
+      const int s = kb % TC_STAGES;
+      const uint32_t ph = (kb / TC_STAGES) & 1;
+      mbar_wait(smem_u32(&bar_full[s]), ph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      unsigned char* st = base + (size_t)s * stage_bytes;
+      const uint64_t bdesc0 = smem_desc_sw128(smem_u32(st + a_planes * A_TILE));
+      for (int p = 0; p < a_planes; ++p) {
+        const uint64_t adesc0 = smem_desc_sw128(smem_u32(st + p * A_TILE));
+#pragma unroll
+        for (int k = 0; k < TC_BK / 16; ++k) {
+          // advance 16 elements (32 B) inside the 128 B swizzle atom
+          mma_bf16(tmem, adesc0 + 2 * k, bdesc0 + 2 * k, idesc, (kb | p | k) != 0);
+        }
+      }
+      mma_commit(smem_u32(&bar_empty[s]));
+    }
+    mma_commit(smem_u32(&bar_done));
+  }
+  __syncwarp();
+
+  // ---- epilogue: TMEM -> registers -> fused epilogue ----
+  mbar_wait(smem_u32(&bar_done), 0);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const int row = m0 + warp * 32 + lane;
+  const bool row_ok = row < M;
+  __syncwarp();
+  for (int cb = 0; cb < BN / 32; ++cb) {
+    float v[32];
+    __syncwarp();
+    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + cb * 32, v);
+    const int nb = n0 + cb * 32;
+    if (row_ok && nb < g.n) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int n = nb + j;
+        if (n < g.n) {
+          if (g.bias) v[j] += g.bias[n];
+          if (g.addend) v[j] += g.addend[(int64_t)row * g.ld_add + n];
+        }
+      }
+      if (g.mode == 1) {
+        const int slot = g.rows ? g.rows[row] : row;
+        const int pr = g.parent ? g.parent[slot] : slot;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int unit = (nb >> 2) + u;
+          if (unit * 4 < g.n) {
+            const float cp = g.c_in ? g.c_in[(int64_t)pr * g.ld_cin + unit] : 0.0f;
+            const float c =
+                sigm_tc(v[4 * u + 1]) * cp + sigm_tc(v[4 * u]) * tanhf(v[4 * u + 2]);
+            float h = sigm_tc(v[4 * u + 3]) * tanhf(c);
+            if (g.h_res) h += g.h_res[(int64_t)slot * g.ld_res + unit];
+            g.c_out[(int64_t)slot * g.ld_cout + unit] = c;
+            g.h_out[(int64_t)slot * g.ld_h + unit] = h;
+          }
+        }
+      } else {
+        const int orow = g.rows ? g.rows[row] : row;
+        float* c = g.c + (int64_t)orow * g.ldc;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (nb + j < g.n) c[nb + j] = v[j];
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+  }
+}
+
+// ---- host: tensor maps through the driver entry point (no -lcuda needed) ----
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static int make_map(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld,
+                    uint32_t box_rows) {
+  auto enc = get_encode();
+  if (!enc) return fail(FB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {TC_BK, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FB_ERR_VALUE, "cuTensorMapEncodeTiled failed (alignment?)");
+  return FB_OK;
+}
+
+template <int BN>
+static int launch_tc(const fb_gemm_t* g, int a_planes, int64_t a_plane_rows, int64_t w_rows,
+                     cudaStream_t s) {
+  CUtensorMap ta, tw;
+  int rc = make_map(&ta, g->a, (uint64_t)a_planes * a_plane_rows, g->k, g->lda, TC_BM);
+  if (rc) return rc;
+  rc = make_map(&tw, g->w, w_rows, g->k, g->ldw, BN);
+  if (rc) return rc;
+  const int stage_bytes = a_planes * TC_BM * TC_BK * 2 + BN * TC_BK * 2;
+  const size_t smem = (size_t)TC_STAGES * stage_bytes + 1024;
+  auto k = gemm_tc_kernel<BN>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid((g->m_max + TC_BM - 1) / TC_BM, (g->n + BN - 1) / BN);
+  k<<<grid, TC_THREADS, smem, s>>>(ta, tw, *g, a_planes, (int)a_plane_rows, g->k / TC_BK);
+  count_launch();
+  return check_launch("gemm_tc");
+}
+
+}  // namespace fb
+
+using namespace fb;
+
+extern "C" int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_rows,
+                          void* stream) {
+  FB_CHECK_ARG(g && g->a && g->w, "null GEMM operands");
+  FB_CHECK_ARG(a_planes >= 1 && a_planes <= 3, "a_planes must be 1..3");
+  FB_CHECK_ARG(g->k % TC_BK == 0 && g->k > 0, "tensor-core GEMM needs k % 64 == 0");
+  FB_CHECK_ARG(g->lda % 8 == 0 && g->ldw % 8 == 0, "leading dims must be multiples of 8");
+  FB_CHECK_ARG(((uintptr_t)g->a % 16) == 0 && ((uintptr_t)g->w % 16) == 0, "16B alignment");
+  FB_CHECK_ARG(a_plane_rows >= g->m_max, "plane stride smaller than m_max");
+  FB_CHECK_ARG(g->mode == 0 || g->mode == 1, "unknown GEMM epilogue");
+  FB_CHECK_ARG(g->mode != 1 || (g->n == 4 * g->hidden && g->h_out && g->c_out),
+               "LSTM epilogue needs n == 4*hidden and state outputs");
+  FB_CHECK_ARG(g->mode != 0 || g->c, "GEMM output is null");
+  if (g->m_max <= 0) return FB_OK;
+  return launch_tc<128>(g, a_planes, a_plane_rows, g->n, (cudaStream_t)stream);
+}

@@ -46,18 +46,46 @@ def gemm(a: torch.Tensor, w: torch.Tensor, *, m: Optional[int] = None, m_dev=Non
 
 def pack(out: torch.Tensor, segs: Sequence[Tuple], *, m: int, m_dev=None, rows=None,
          parent=None, tokens=None, ranks=None, tok_default: int = 0,
-         k_pad: Optional[int] = None) -> None:
-    """out[i] = concat(segments) zero-padded; segs = (src|None, width, mode, ld?)."""
+         k_pad: Optional[int] = None, split: bool = False) -> None:
+    """out[i] = concat(segments) zero-padded; segs = (src|None, width, mode, ld?).
+    split=True: out is bf16 [3, plane_rows, k_pad] (hi/mid/lo planes)."""
     p = _lib.FbPack()
     for j, s in enumerate(segs):
         src, width, mode = s[0], s[1], s[2]
         ld = s[3] if len(s) > 3 else (src.stride(0) if src is not None else 0)
         p.seg[j] = _lib.FbSeg(P(src), ld, width, mode)
     p.nseg = len(segs)
-    p.k_pad = out.shape[1] if k_pad is None else k_pad
+    p.k_pad = out.shape[-1] if k_pad is None else k_pad
     p.tok_default = tok_default
+    p.out_mode = 1 if split else 0
+    p.plane_rows = out.shape[1] if split else 0
+    ld = out.stride(1) if split else out.stride(0)
     _lib.call("fb_pack_rows", C.byref(p), m, P(m_dev), P(rows), P(parent), P(tokens), P(ranks),
-              P(out), out.stride(0), _lib.stream_ptr())
+              P(out), ld, _lib.stream_ptr())
+
+
+def gemm_tc(ap: torch.Tensor, w: torch.Tensor, *, m: Optional[int] = None, m_dev=None,
+            k: Optional[int] = None, bias=None, out=None, rows=None, mode: int = 0,
+            hidden: int = 0, parent=None, c_in=None, c_out=None, h_out=None, h_res=None,
+            addend=None) -> None:
+    """Tensor-core GEMM: ap = bf16 planes [P, rows, k_pad], w = bf16 [n, k_pad]."""
+    g = _lib.FbGemm()
+    g.m_max = ap.shape[1] if m is None else m
+    g.m_dev = P(m_dev)
+    g.n = w.shape[0]
+    g.k = w.shape[1] if k is None else k
+    g.a, g.lda = P(ap), ap.stride(1)
+    g.w, g.ldw = P(w), w.stride(0)
+    g.bias = P(bias)
+    g.c, g.ldc = P(out), _ld(out)
+    g.mode, g.hidden = mode, hidden
+    g.rows, g.parent = P(rows), P(parent)
+    g.c_in, g.ld_cin = P(c_in), _ld(c_in)
+    g.c_out, g.ld_cout = P(c_out), _ld(c_out)
+    g.h_out, g.ld_h = P(h_out), _ld(h_out)
+    g.h_res, g.ld_res = P(h_res), _ld(h_res)
+    g.addend, g.ld_add = P(addend), _ld(addend)
+    _lib.call("fb_gemm_tc", C.byref(g), ap.shape[0], ap.shape[1], _lib.stream_ptr())
 
 
 def log_softmax_rows(x: torch.Tensor, out: torch.Tensor, n: int, *, m: int, m_dev=None,
