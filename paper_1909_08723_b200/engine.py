@@ -30,7 +30,7 @@ from . import _lib
 from . import kernels as K
 from .decoder import DecodeConfig, DecodeResult, SearchBuffers, search_cfg
 from .errors import ConfigError
-from .models import AmState, lm_step
+from .models import AmState, lm_step, split_scratch
 
 P = _lib.ptr
 
@@ -62,7 +62,7 @@ class _LmPool:
         self.mark = z(2 * self.P)
         self.ext_eos = torch.zeros(N, dtype=torch.float64, device=device)
         self.zero_eos = torch.zeros(N, dtype=torch.float64, device=device)
-        self.scratch = torch.empty((N, lw.k_max), dtype=f32, device=device)
+        self.scratch = split_scratch(N, lw.k_max, device)
 
     def start(self) -> None:
         """Slot 0 = LM state after <s> from the zero state (word_lm start_history)."""
@@ -172,7 +172,7 @@ class FusedDecoder:
 
         L, H, C_ = d.dec_layers, d.dec_hidden, d.ctx
         X2 = [AmState(L, N, H, C_, dev), AmState(L, N, H, C_, dev)]
-        scratch = torch.empty((N, w.k_max), dtype=torch.float32, device=dev)
+        scratch = split_scratch(N, w.k_max, dev)
         q = torch.empty((N, d.att), dtype=torch.float32, device=dev)
         logits = torch.empty((N, V), dtype=torch.float32, device=dev)
         am_logp = torch.zeros((N, V), dtype=torch.float32, device=dev)

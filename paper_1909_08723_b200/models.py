@@ -30,7 +30,7 @@ from . import kernels as K
 from .fusion import _device
 from .synth import AsrDims, LmDims
 
-KGRAN = 16           # K granule of the GEMM kernels
+KGRAN = 64           # K granule of the tensor-core GEMM (one 128 B swizzle atom of bf16)
 
 
 def _pad(k: int, g: int = KGRAN) -> int:
@@ -51,6 +51,17 @@ def _dev(a, device, cols: Optional[int] = None) -> torch.Tensor:
         z[:, :a.shape[1]] = a
         a = z
     return torch.as_tensor(a, device=device)
+
+
+def _devw(a, device, cols: Optional[int] = None) -> torch.Tensor:
+    """GEMM weight operand: bf16 (exact -- the synthesizer rounds weights to
+    bf16), K zero-padded to the tensor-core granule."""
+    return _dev(a, device, cols).to(torch.bfloat16)
+
+
+def split_scratch(rows: int, k: int, device) -> torch.Tensor:
+    """bf16 [3, rows, k] buffer for hi/mid/lo activation planes."""
+    return torch.empty((3, rows, k), dtype=torch.bfloat16, device=device)
 
 
 @dataclass
@@ -79,7 +90,7 @@ class AsrWeights:
                 w_ih = interleave_gates(W[f"enc.{l}.{r}.w_ih"], He)
                 w_hh = interleave_gates(W[f"enc.{l}.{r}.w_hh"], He)
                 b = interleave_gates(W[f"enc.{l}.{r}.b"], He)
-                dirs.append((_dev(w_ih, device, _pad(fin)), _dev(w_hh, device, _pad(He)),
+                dirs.append((_devw(w_ih, device, _pad(fin)), _devw(w_hh, device, _pad(He)),
                              _dev(b, device)))
             self.enc.append(dirs)
         self.emb = _dev(W["dec.emb"], device)
@@ -87,14 +98,14 @@ class AsrWeights:
         for l in range(d.dec_layers):
             fin = (d.emb + C_) if l == 0 else (H + C_)
             w = np.concatenate([W[f"dec.{l}.w_ih"], W[f"dec.{l}.w_hh"]], axis=1)
-            self.dec.append(LstmLayer(_dev(interleave_gates(w, H), device, _pad(fin + H)),
+            self.dec.append(LstmLayer(_devw(interleave_gates(w, H), device, _pad(fin + H)),
                                       _dev(interleave_gates(W[f"dec.{l}.b"], H), device),
                                       fin + H, H))
-        self.w_k = _dev(W["dec.att.w_k"], device, _pad(C_))
+        self.w_k = _devw(W["dec.att.w_k"], device, _pad(C_))
         self.b_k = _dev(W["dec.att.b_k"], device)
-        self.w_q = _dev(W["dec.att.w_q"], device, _pad(H))
+        self.w_q = _devw(W["dec.att.w_q"], device, _pad(H))
         self.v = _dev(W["dec.att.v"], device)
-        self.w_out = _dev(W["dec.out.w"], device, _pad(H + C_))
+        self.w_out = _devw(W["dec.out.w"], device, _pad(H + C_))
         self.b_out = _dev(W["dec.out.b"], device)
         self.k_max = max([l.k_pad for l in self.dec] + [self.w_q.shape[1], self.w_out.shape[1],
                                                         self.w_k.shape[1]])
@@ -150,7 +161,10 @@ class Encoder:
             rev[u, :T[u]] = u * TM + np.arange(T[u] - 1, -1, -1)
         rev_t = torch.as_tensor(rev.reshape(-1)).to(dev, non_blocking=True)
         He = d.enc_hidden
+        kr = _pad(He)
         Xr = torch.empty_like(X)
+        big = split_scratch(B * TM, max(X.shape[1], _pad(2 * He)), dev)
+        rec = split_scratch(B, kr, dev)
         for l, dirs in enumerate(self.w.enc):
             kin = X.shape[1]
             K.copy_rows(X, Xr, m=B * TM, src_idx=rev_t)
@@ -158,16 +172,19 @@ class Encoder:
             for r, (w_ih, w_hh, b) in enumerate(dirs):
                 src = X if r == 0 else Xr
                 xp = torch.empty((B * TM, 4 * He), dtype=torch.float32, device=dev)
-                K.gemm(src, w_ih, k=kin, bias=b, out=xp)
+                K.pack(big, [(src, kin, 0)], m=B * TM, k_pad=kin, split=True)
+                K.gemm_tc(big[:, :, :kin], w_ih, m=B * TM, k=kin, bias=b, out=xp)
                 y = torch.zeros((B, TM, He), dtype=torch.float32, device=dev)
                 cbuf = [torch.zeros((B, He), dtype=torch.float32, device=dev) for _ in range(2)]
-                zero_h = torch.zeros((B, _pad(He)), dtype=torch.float32, device=dev)
                 xp3 = xp.view(B, TM, 4 * He)
                 for t in range(TM):
-                    a = zero_h if t == 0 else y[:, t - 1, :]
-                    K.gemm(a, w_hh, m=B, k=w_hh.shape[1], mode=1, hidden=He,
-                           c_in=None if t == 0 else cbuf[t % 2], c_out=cbuf[(t + 1) % 2],
-                           h_out=y[:, t, :], addend=xp3[:, t, :])
+                    if t == 0:
+                        K.pack(rec, [(None, He, 0, 0)], m=B, k_pad=kr, split=True)
+                    else:
+                        K.pack(rec, [(y[:, t - 1, :], He, 0, TM * He)], m=B, k_pad=kr, split=True)
+                    K.gemm_tc(rec, w_hh, m=B, k=kr, mode=1, hidden=He,
+                              c_in=None if t == 0 else cbuf[t % 2], c_out=cbuf[(t + 1) % 2],
+                              h_out=y[:, t, :], addend=xp3[:, t, :])
                 ys.append(y.reshape(B * TM, He))
             kout = _pad(2 * He)
             Xn = torch.empty((B * TM, kout), dtype=torch.float32, device=dev)
@@ -177,7 +194,9 @@ class Encoder:
         C_ = 2 * He
         enc = X[:, :C_].contiguous()
         keys = torch.empty((B * TM, d.att), dtype=torch.float32, device=dev)
-        K.gemm(X, self.w.w_k, k=self.w.w_k.shape[1], bias=self.w.b_k, out=keys)
+        kk = self.w.w_k.shape[1]
+        K.pack(big, [(X, kk, 0)], m=B * TM, k_pad=kk, split=True)
+        K.gemm_tc(big[:, :, :kk], self.w.w_k, m=B * TM, k=kk, bias=self.w.b_k, out=keys)
         return enc.view(B, TM, C_), keys.view(B, TM, d.att), T
 
 
@@ -202,14 +221,15 @@ class DecoderStep:
                 segs = [(w.emb, E, 3), (prev.ctx, C_, 2), (prev.h[0], H, 2)]
             else:
                 segs = [(cur.h[l - 1], H, 1), (prev.ctx, C_, 2), (prev.h[l], H, 2)]
-            K.pack(scratch, segs, tokens=last_tok, tok_default=self.eos, k_pad=lay.k_pad, **kw)
-            K.gemm(scratch, lay.w, k=lay.k_pad, bias=lay.b, mode=1, hidden=H,
-                   c_in=prev.c[l], c_out=cur.c[l], h_out=cur.h[l],
-                   h_res=cur.h[l - 1] if l > 0 else None, **kw)
+            K.pack(scratch, segs, tokens=last_tok, tok_default=self.eos, k_pad=lay.k_pad,
+                   split=True, **kw)
+            K.gemm_tc(scratch, lay.w, k=lay.k_pad, bias=lay.b, mode=1, hidden=H,
+                      c_in=prev.c[l], c_out=cur.c[l], h_out=cur.h[l],
+                      h_res=cur.h[l - 1] if l > 0 else None, **kw)
         top = cur.h[L - 1]
         kq = w.w_q.shape[1]
-        K.pack(scratch, [(top, H, 1)], k_pad=kq, **kw)
-        K.gemm(scratch, w.w_q, k=kq, out=q, m=m, m_dev=m_dev, rows=rows)
+        K.pack(scratch, [(top, H, 1)], k_pad=kq, split=True, **kw)
+        K.gemm_tc(scratch, w.w_q, k=kq, out=q, m=m, m_dev=m_dev, rows=rows)
         _lib.call("fb_attention_step", cfg_ref, num_utts, _lib.ptr(active), _lib.ptr(n_live),
                   _lib.ptr(t_enc), _lib.ptr(keys), _lib.ptr(enc), d.att, C_, _lib.ptr(w.v),
                   _lib.ptr(q), q.stride(0), _lib.ptr(parent), _lib.ptr(acc_in),
@@ -217,8 +237,8 @@ class DecoderStep:
                   _lib.ptr(attn_out), 0 if attn_out is None else attn_out.stride(0),
                   _lib.stream_ptr())
         ko = w.w_out.shape[1]
-        K.pack(scratch, [(top, H, 1), (cur.ctx, C_, 1)], k_pad=ko, **kw)
-        K.gemm(scratch, w.w_out, k=ko, bias=w.b_out, out=logits, m=m, m_dev=m_dev, rows=rows)
+        K.pack(scratch, [(top, H, 1), (cur.ctx, C_, 1)], k_pad=ko, split=True, **kw)
+        K.gemm_tc(scratch, w.w_out, k=ko, bias=w.b_out, out=logits, m=m, m_dev=m_dev, rows=rows)
         K.log_softmax_rows(logits, am_logp, d.vocab, m=m, m_dev=m_dev, rows=rows)
 
 
@@ -266,7 +286,7 @@ class AttnLstmScorer:
         acc0 = torch.zeros((n, state.T), dtype=torch.float64, device=dev)
         acc1 = torch.empty_like(acc0)
         attn = torch.empty((n, state.T), dtype=torch.float32, device=dev)
-        scratch = torch.empty((n, self.weights.k_max), dtype=torch.float32, device=dev)
+        scratch = split_scratch(n, self.weights.k_max, dev)
         q = torch.empty((n, d.att), dtype=torch.float32, device=dev)
         logits = torch.empty((n, d.vocab), dtype=torch.float32, device=dev)
         logp = torch.empty((n, d.vocab), dtype=torch.float32, device=dev)
@@ -295,12 +315,13 @@ class LmWeights:
         H = d.hidden
         self.v_out = d.words + 3
         self.k_out = _pad(H)
-        self.emb = _dev(W["lm.emb"], device, self.k_out)      # [V+3, k_out] (tied in/out)
+        self.emb = _dev(W["lm.emb"], device, self.k_out)      # [V+3, k_out] fp32 input rows
+        self.emb_w = self.emb.to(torch.bfloat16)               # tied output weight operand
         self.b_out = _dev(W["lm.b_out"], device)
         self.layers: List[LstmLayer] = []
         for l in range(d.layers):
             w = np.concatenate([W[f"lm.{l}.w_ih"], W[f"lm.{l}.w_hh"]], axis=1)
-            self.layers.append(LstmLayer(_dev(interleave_gates(w, H), device, _pad(2 * H)),
+            self.layers.append(LstmLayer(_devw(interleave_gates(w, H), device, _pad(2 * H)),
                                          _dev(interleave_gates(W[f"lm.{l}.b"], H), device),
                                          2 * H, H))
         self.k_max = max([l.k_pad for l in self.layers] + [self.k_out])
@@ -328,17 +349,19 @@ def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks
             hseg = (state_src[:, l, 0], H, 1, state_src.stride(0))
             c_in = state_src[:, l, 1]
         K.pack(scratch, [x, hseg], m=m, m_dev=m_dev, rows=src_idx, ranks=ranks,
-               tok_default=tok_default, k_pad=lay.k_pad)
-        K.gemm(scratch, lay.w, m=m, m_dev=m_dev, k=lay.k_pad, bias=lay.b, mode=1, hidden=H,
-               parent=src_idx, c_in=c_in, c_out=state_dst[:, l, 1], h_out=state_dst[:, l, 0])
+               tok_default=tok_default, k_pad=lay.k_pad, split=True)
+        K.gemm_tc(scratch, lay.w, m=m, m_dev=m_dev, k=lay.k_pad, bias=lay.b, mode=1, hidden=H,
+                  parent=src_idx, c_in=c_in, c_out=state_dst[:, l, 1],
+                  h_out=state_dst[:, l, 0])
     if logits is not None:
         K.pack(scratch, [(state_dst[:, L - 1, 0], H, 0, state_dst.stride(0))], m=m, m_dev=m_dev,
-               k_pad=w.k_out)
+               k_pad=w.k_out, split=True)
         if timer is not None:
             with timer("lm_out_gemm"):
-                K.gemm(scratch, w.emb, m=m, m_dev=m_dev, k=w.k_out, bias=w.b_out, out=logits)
+                K.gemm_tc(scratch, w.emb_w, m=m, m_dev=m_dev, k=w.k_out, bias=w.b_out,
+                          out=logits)
         else:
-            K.gemm(scratch, w.emb, m=m, m_dev=m_dev, k=w.k_out, bias=w.b_out, out=logits)
+            K.gemm_tc(scratch, w.emb_w, m=m, m_dev=m_dev, k=w.k_out, bias=w.b_out, out=logits)
 
 
 class _DevHist:
@@ -369,7 +392,7 @@ class LstmWordLM:
         w, d, dev = self.weights, self.dims, self.device
         st = torch.empty((1, d.layers, 2, d.hidden), dtype=torch.float32, device=dev)
         lg = torch.empty((1, w.v_out), dtype=torch.float32, device=dev)
-        scratch = torch.empty((1, w.k_max), dtype=torch.float32, device=dev)
+        scratch = split_scratch(1, w.k_max, dev)
         lm_step(w, m=1, m_dev=None, state_src=None if parent is None else parent.state,
                 src_idx=None, state_dst=st, ranks=None, tok_default=token, scratch=scratch,
                 logits=lg)
