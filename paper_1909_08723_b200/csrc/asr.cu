@@ -84,9 +84,11 @@ __global__ void log_softmax_kernel(int m_max, const int32_t* __restrict__ m_dev,
 
 // -------------------------------------------------------------- attention --
 __device__ __forceinline__ float tanh_fast(float x) {
-  // 1 - 2/(e^{2x}+1): absolute error ~1e-7, saturates cleanly at +-1
+  // 1 - 2/(e^{2x}+1) with MUFU ex2/rcp: absolute error ~2e-7; the clamp keeps
+  // __fdividef in range (tanh(15) == 1 in fp32)
+  x = fminf(fmaxf(x, -15.0f), 15.0f);
   const float e = __expf(2.0f * x);
-  return 1.0f - 2.0f / (e + 1.0f);
+  return 1.0f - __fdividef(2.0f, e + 1.0f);
 }
 
 constexpr int kAttThreads = 256;
@@ -148,7 +150,8 @@ attention_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
   for (int j = tid; j < n * T; j += kAttThreads) es[j] = 0.f;
   const float* ku = keys + (int64_t)u * TM * A;
   const float* eu = enc + (int64_t)u * TM * C;
-  // energies, accumulated over chunks of the attention dimension
+  // energies e[i][t] = sum_a v[a] tanh(k[t][a] + q[i][a]); each thread owns
+  // frames t, keeps its key chunk in registers and reads q/v as broadcasts.
   for (int a0 = 0; a0 < A; a0 += kAChunk) {
     const int ac = min(kAChunk, A - a0);
     __syncthreads();
@@ -157,12 +160,18 @@ attention_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
       if (a < ac) kc[a * T + t] = ku[(int64_t)t * A + a0 + a];
     }
     __syncthreads();
-    for (int pidx = tid; pidx < n * T; pidx += kAttThreads) {
-      const int i = pidx / T, t = pidx % T;
-      const float* qi = qs + i * A + a0;
-      float s = 0.f;
-      for (int a = 0; a < ac; ++a) s = fmaf(vs[a0 + a], tanh_fast(kc[a * T + t] + qi[a]), s);
-      es[pidx] += s;
+    for (int t = tid; t < T; t += kAttThreads) {
+      float kr[kAChunk];
+#pragma unroll
+      for (int a = 0; a < kAChunk; ++a) kr[a] = a < ac ? kc[a * T + t] : 0.f;
+      for (int i = 0; i < n; ++i) {
+        const float* qi = qs + i * A + a0;
+        float s = 0.f;
+#pragma unroll
+        for (int a = 0; a < kAChunk; ++a)
+          if (a < ac) s = fmaf(vs[a0 + a], tanh_fast(kr[a] + qi[a]), s);
+        es[i * T + t] += s;
+      }
     }
   }
   __syncthreads();
@@ -183,16 +192,28 @@ attention_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
     for (int t = lane; t < T; t += 32) e[t] *= inv;
   }
   __syncthreads();
-  // context vectors: ctx[i][c] = sum_t a[i][t] enc[t][c]
-  constexpr int RB = 16;
+  // context vectors ctx[i][c] = sum_t a[i][t] enc[t][c]: 8 frames of enc in
+  // flight per thread (coalesced over c), attention weights broadcast
+  constexpr int RB = 16, TU = 8;
   for (int i0 = 0; i0 < n; i0 += RB) {
     const int nb = min(RB, n - i0);
     for (int c = tid; c < C; c += kAttThreads) {
       float acc[RB];
 #pragma unroll
       for (int r = 0; r < RB; ++r) acc[r] = 0.f;
-      for (int t = 0; t < T; ++t) {
-        const float x = eu[(int64_t)t * C + c];
+      int t = 0;
+      for (; t + TU <= T; t += TU) {
+        float x[TU];
+#pragma unroll
+        for (int j = 0; j < TU; ++j) x[j] = __ldg(eu + (int64_t)(t + j) * C + c);
+#pragma unroll
+        for (int j = 0; j < TU; ++j)
+#pragma unroll
+          for (int r = 0; r < RB; ++r)
+            if (r < nb) acc[r] = fmaf(es[(i0 + r) * T + t + j], x[j], acc[r]);
+      }
+      for (; t < T; ++t) {
+        const float x = __ldg(eu + (int64_t)t * C + c);
 #pragma unroll
         for (int r = 0; r < RB; ++r)
           if (r < nb) acc[r] = fmaf(es[(i0 + r) * T + t], x, acc[r]);

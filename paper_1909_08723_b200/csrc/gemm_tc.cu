@@ -7,11 +7,11 @@
 // fp32 in TMEM -- an fp32-accurate product on the 5th-gen tensor cores
 // (SURVEY.md §7 "GEMM precision").  Algorithmic FLOPs count the product once.
 //
-// Structure (one 128 x BN output tile per CTA, 4 warps):
+// Structure (persistent, one CTA per SM, 6 warps):
 //   warp 0 lane 0 : TMA producer, 3-stage smem ring (128B swizzle, K block 64)
 //   warp 1 lane 0 : MMA issuer (tcgen05.mma.cta_group::1.kind::f16, M=128)
-//   warp 1        : TMEM allocator (BN fp32 columns)
-//   all 4 warps   : epilogue, tcgen05.ld 32x32b (warp w owns TMEM lanes 32w..)
+//   warp 1        : TMEM allocator (2 x BN fp32 columns, double-buffered)
+//   warps 2..5    : epilogue, tcgen05.ld 32x32b (warp w owns TMEM lanes 32(w%4)..)
 #include "common.cuh"
 
 #include <cuda.h>
@@ -22,7 +22,8 @@ namespace fb {
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;            // 64 bf16 = 128 B = one swizzle atom
 constexpr int TC_STAGES = 3;
-constexpr int TC_THREADS = 128;
+constexpr int TC_EPI_THREADS = 128;
+constexpr int TC_THREADS = 64 + TC_EPI_THREADS;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -100,12 +101,63 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 __device__ __forceinline__ float sigm_tc(float x) { return 1.0f / (1.0f + expf(-x)); }
 
 template <int BN>
+__device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row, int n0,
+                                              uint32_t taddr) {
+  const bool row_ok = row < M;
+  for (int cb = 0; cb < BN / 32; ++cb) {
+    float v[32];
+    __syncwarp();
+    tmem_ld32(taddr + cb * 32, v);
+    const int nb = n0 + cb * 32;
+    if (!row_ok || nb >= g.n) continue;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int n = nb + j;
+      if (n < g.n) {
+        if (g.bias) v[j] += g.bias[n];
+        if (g.addend) v[j] += g.addend[(int64_t)row * g.ld_add + n];
+      }
+    }
+    if (g.mode == 1) {
+      const int slot = g.rows ? g.rows[row] : row;
+      const int pr = g.parent ? g.parent[slot] : slot;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int unit = (nb >> 2) + u;
+        if (unit * 4 < g.n) {
+          const float cp = g.c_in ? g.c_in[(int64_t)pr * g.ld_cin + unit] : 0.0f;
+          const float c = sigm_tc(v[4 * u + 1]) * cp + sigm_tc(v[4 * u]) * tanhf(v[4 * u + 2]);
+          float h = sigm_tc(v[4 * u + 3]) * tanhf(c);
+          if (g.h_res) h += g.h_res[(int64_t)slot * g.ld_res + unit];
+          g.c_out[(int64_t)slot * g.ld_cout + unit] = c;
+          g.h_out[(int64_t)slot * g.ld_h + unit] = h;
+        }
+      }
+    } else {
+      const int orow = g.rows ? g.rows[row] : row;
+      float* c = g.c + (int64_t)orow * g.ldc;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (nb + j < g.n) c[nb + j] = v[j];
+    }
+  }
+  __syncwarp();
+}
+
+// Persistent, warp-specialized: warp 0 = TMA producer, warp 1 = MMA issuer
+// (+ TMEM owner), warps 2..5 = epilogue.  Two TMEM accumulators (2 x BN
+// columns) let the epilogue of tile i overlap the MMAs of tile i+1.  The tile
+// count follows the device-side row count, so graph replays with few live rows
+// cost only the tiles they need.
+template <int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
                fb_gemm_t g, int a_planes, int a_plane_rows, int num_kb) {
   const int M = row_count(g.m_max, g.m_dev);
-  const int m0 = blockIdx.x * TC_BM, n0 = blockIdx.y * BN;
-  if (m0 >= M) return;
+  const int m_tiles = (M + TC_BM - 1) / TC_BM;
+  const int n_tiles = (g.n + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  if ((int)blockIdx.x >= num_tiles) return;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>(
@@ -113,7 +165,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   constexpr int A_TILE = TC_BM * TC_BK * 2;         // 16 KB
   constexpr int W_TILE = BN * TC_BK * 2;
   const int stage_bytes = a_planes * A_TILE + W_TILE;
-  __shared__ __align__(8) uint64_t bar_full[TC_STAGES], bar_empty[TC_STAGES], bar_done;
+  __shared__ __align__(8) uint64_t bar_full[TC_STAGES], bar_empty[TC_STAGES];
+  __shared__ __align__(8) uint64_t bar_tfull[2], bar_tempty[2];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -122,13 +175,16 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_init(smem_u32(&bar_full[s]), 1);
       mbar_init(smem_u32(&bar_empty[s]), 1);
     }
-    mbar_init(smem_u32(&bar_done), 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(smem_u32(&bar_tfull[a]), 1);
+      mbar_init(smem_u32(&bar_tempty[a]), TC_EPI_THREADS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_base_sh)),
-                 "r"(BN));
+                 "r"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -136,94 +192,76 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base_sh;
 
-  if (warp == 0 && lane == 0) {
-    // ---- TMA producer ----
-    for (int kb = 0; kb < num_kb; ++kb) {
-      const int s = kb % TC_STAGES;
-      const uint32_t ph = (kb / TC_STAGES) & 1;
-      mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
-      const uint32_t full = smem_u32(&bar_full[s]);
-      mbar_expect_tx(full, stage_bytes);
-      unsigned char* st = base + (size_t)s * stage_bytes;
-      for (int p = 0; p < a_planes; ++p)
-        tma_load_2d(smem_u32(st + p * A_TILE), &tmA, full, kb * TC_BK, p * a_plane_rows + m0);
-      tma_load_2d(smem_u32(st + a_planes * A_TILE), &tmW, full, kb * TC_BK, n0);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---- MMA issuer ----
-    // bf16 x bf16 -> f32, K-major A/B, M = 128, N = BN (cute::UMMA::InstrDescriptor)
-    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(TC_BM >> 4) << 24);
-    for (int kb = 0; kb < num_kb; ++kb) {
-      const int s = kb % TC_STAGES;
-      const uint32_t ph = (kb / TC_STAGES) & 1;
-      mbar_wait(smem_u32(&bar_full[s]), ph);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      unsigned char* st = base + (size_t)s * stage_bytes;
-      const uint64_t bdesc0 = smem_desc_sw128(smem_u32(st + a_planes * A_TILE));
-      for (int p = 0; p < a_planes; ++p) {
-        const uint64_t adesc0 = smem_desc_sw128(smem_u32(st + p * A_TILE));
-#pragma unroll
-        for (int k = 0; k < TC_BK / 16; ++k) {
-          // advance 16 elements (32 B) inside the 128 B swizzle atom
-          mma_bf16(tmem, adesc0 + 2 * k, bdesc0 + 2 * k, idesc, (kb | p | k) != 0);
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer ----
+      int gk = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m0 = (tile % m_tiles) * TC_BM, n0 = (tile / m_tiles) * BN;
+        for (int kb = 0; kb < num_kb; ++kb, ++gk) {
+          const int s = gk % TC_STAGES;
+          const uint32_t ph = (gk / TC_STAGES) & 1;
+          mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
+          const uint32_t full = smem_u32(&bar_full[s]);
+          mbar_expect_tx(full, stage_bytes);
+          unsigned char* st = base + (size_t)s * stage_bytes;
+          for (int p = 0; p < a_planes; ++p)
+            tma_load_2d(smem_u32(st + p * A_TILE), &tmA, full, kb * TC_BK,
+                        p * a_plane_rows + m0);
+          tma_load_2d(smem_u32(st + a_planes * A_TILE), &tmW, full, kb * TC_BK, n0);
         }
       }
-      mma_commit(smem_u32(&bar_empty[s]));
     }
-    mma_commit(smem_u32(&bar_done));
-  }
-  __syncwarp();
-
-  // ---- epilogue: TMEM -> registers -> fused epilogue ----
-  mbar_wait(smem_u32(&bar_done), 0);
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const int row = m0 + warp * 32 + lane;
-  const bool row_ok = row < M;
-  __syncwarp();
-  for (int cb = 0; cb < BN / 32; ++cb) {
-    float v[32];
-    __syncwarp();
-    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + cb * 32, v);
-    const int nb = n0 + cb * 32;
-    if (row_ok && nb < g.n) {
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---- MMA issuer: bf16 x bf16 -> f32, K-major, M = 128, N = BN ----
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(TC_BM >> 4) << 24);
+      int gk = 0, it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        mbar_wait(smem_u32(&bar_tempty[acc]), ((it >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb, ++gk) {
+          const int s = gk % TC_STAGES;
+          const uint32_t ph = (gk / TC_STAGES) & 1;
+          mbar_wait(smem_u32(&bar_full[s]), ph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          unsigned char* st = base + (size_t)s * stage_bytes;
+          const uint64_t bdesc0 = smem_desc_sw128(smem_u32(st + a_planes * A_TILE));
+          for (int p = 0; p < a_planes; ++p) {
+            const uint64_t adesc0 = smem_desc_sw128(smem_u32(st + p * A_TILE));
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int n = nb + j;
-        if (n < g.n) {
-          if (g.bias) v[j] += g.bias[n];
-          if (g.addend) v[j] += g.addend[(int64_t)row * g.ld_add + n];
-        }
-      }
-      if (g.mode == 1) {
-        const int slot = g.rows ? g.rows[row] : row;
-        const int pr = g.parent ? g.parent[slot] : slot;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int unit = (nb >> 2) + u;
-          if (unit * 4 < g.n) {
-            const float cp = g.c_in ? g.c_in[(int64_t)pr * g.ld_cin + unit] : 0.0f;
-            const float c =
-                sigm_tc(v[4 * u + 1]) * cp + sigm_tc(v[4 * u]) * tanhf(v[4 * u + 2]);
-            float h = sigm_tc(v[4 * u + 3]) * tanhf(c);
-            if (g.h_res) h += g.h_res[(int64_t)slot * g.ld_res + unit];
-            g.c_out[(int64_t)slot * g.ld_cout + unit] = c;
-            g.h_out[(int64_t)slot * g.ld_h + unit] = h;
+            for (int k = 0; k < TC_BK / 16; ++k)   // 16 elements = 32 B per UMMA_K
+              mma_bf16(d, adesc0 + 2 * k, bdesc0 + 2 * k, idesc, (kb | p | k) != 0);
           }
+          mma_commit(smem_u32(&bar_empty[s]));
         }
-      } else {
-        const int orow = g.rows ? g.rows[row] : row;
-        float* c = g.c + (int64_t)orow * g.ldc;
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (nb + j < g.n) c[nb + j] = v[j];
+        mma_commit(smem_u32(&bar_tfull[acc]));
       }
     }
+  } else {
+    // ---- epilogue warps 2..5 (TMEM lane quarter = warp % 4) ----
+    const int quarter = warp & 3;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const int m0 = (tile % m_tiles) * TC_BM, n0 = (tile / m_tiles) * BN;
+      mbar_wait(smem_u32(&bar_tfull[acc]), (it >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      epilogue_tile<BN>(g, M, m0 + quarter * 32 + lane, n0,
+                        tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN);
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[acc]))
+                   : "memory");
+    }
   }
-  asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(2 * BN));
   }
 }
 
@@ -268,8 +306,9 @@ static int launch_tc(const fb_gemm_t* g, int a_planes, int64_t a_plane_rows, int
   const size_t smem = (size_t)TC_STAGES * stage_bytes + 1024;
   auto k = gemm_tc_kernel<BN>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dim3 grid((g->m_max + TC_BM - 1) / TC_BM, (g->n + BN - 1) / BN);
-  k<<<grid, TC_THREADS, smem, s>>>(ta, tw, *g, a_planes, (int)a_plane_rows, g->k / TC_BK);
+  const int tiles = ((g->m_max + TC_BM - 1) / TC_BM) * ((g->n + BN - 1) / BN);
+  k<<<std::min(tiles, kNumSMs), TC_THREADS, smem, s>>>(ta, tw, *g, a_planes, (int)a_plane_rows,
+                                                      g->k / TC_BK);
   count_launch();
   return check_launch("gemm_tc");
 }

@@ -197,7 +197,8 @@ class FusedDecoder:
                                last_tok=buf.last_tok, prev=X2[1 - c], cur=X2[c], scratch=scratch,
                                q=q, logits=logits, am_logp=am_logp, cfg_ref=cfg_ref, num_utts=B,
                                active=buf.active, n_live=buf.n_live, t_enc=buf.t_enc, keys=keys,
-                               enc=enc, acc_in=buf.acc[c], acc_out=buf.acc[1 - c], cov=buf.cov)
+                               enc=enc, acc_in=buf.acc[c], acc_out=buf.acc[1 - c], cov=buf.cov,
+                               timer=timer)
             if has_fusion:
                 with tm("lookahead"):
                     # word_end in the eos column of final rows; log P(</s>) added below

@@ -211,11 +211,14 @@ class DecoderStep:
     def __call__(self, *, N: int, rows, m: int, m_dev, parent, last_tok, prev: AmState,
                  cur: AmState, scratch: torch.Tensor, q: torch.Tensor, logits: torch.Tensor,
                  am_logp: torch.Tensor, cfg_ref, num_utts: int, active, n_live, t_enc,
-                 keys, enc, acc_in, acc_out, cov, attn_out=None) -> None:
+                 keys, enc, acc_in, acc_out, cov, attn_out=None, timer=None) -> None:
         w, d = self.w, self.w.d
+        tm = timer if timer is not None else _null_timer
         H, C_, E = d.dec_hidden, d.ctx, d.emb
         L = d.dec_layers
         kw = dict(m=m, m_dev=m_dev, rows=rows, parent=parent)
+        span = tm("am_lstm")
+        span.__enter__()
         for l, lay in enumerate(w.dec):
             if l == 0:
                 segs = [(w.emb, E, 3), (prev.ctx, C_, 2), (prev.h[0], H, 2)]
@@ -226,20 +229,38 @@ class DecoderStep:
             K.gemm_tc(scratch, lay.w, k=lay.k_pad, bias=lay.b, mode=1, hidden=H,
                       c_in=prev.c[l], c_out=cur.c[l], h_out=cur.h[l],
                       h_res=cur.h[l - 1] if l > 0 else None, **kw)
+        span.__exit__(None, None, None)
         top = cur.h[L - 1]
         kq = w.w_q.shape[1]
         K.pack(scratch, [(top, H, 1)], k_pad=kq, split=True, **kw)
         K.gemm_tc(scratch, w.w_q, k=kq, out=q, m=m, m_dev=m_dev, rows=rows)
-        _lib.call("fb_attention_step", cfg_ref, num_utts, _lib.ptr(active), _lib.ptr(n_live),
-                  _lib.ptr(t_enc), _lib.ptr(keys), _lib.ptr(enc), d.att, C_, _lib.ptr(w.v),
-                  _lib.ptr(q), q.stride(0), _lib.ptr(parent), _lib.ptr(acc_in),
-                  _lib.ptr(acc_out), _lib.ptr(cov), _lib.ptr(cur.ctx), cur.ctx.stride(0),
-                  _lib.ptr(attn_out), 0 if attn_out is None else attn_out.stride(0),
-                  _lib.stream_ptr())
+        with tm("am_attention"):
+            _lib.call("fb_attention_step", cfg_ref, num_utts, _lib.ptr(active),
+                      _lib.ptr(n_live), _lib.ptr(t_enc), _lib.ptr(keys), _lib.ptr(enc), d.att, C_,
+                      _lib.ptr(w.v), _lib.ptr(q), q.stride(0), _lib.ptr(parent),
+                      _lib.ptr(acc_in), _lib.ptr(acc_out), _lib.ptr(cov), _lib.ptr(cur.ctx),
+                      cur.ctx.stride(0), _lib.ptr(attn_out),
+                      0 if attn_out is None else attn_out.stride(0), _lib.stream_ptr())
         ko = w.w_out.shape[1]
-        K.pack(scratch, [(top, H, 1), (cur.ctx, C_, 1)], k_pad=ko, split=True, **kw)
-        K.gemm_tc(scratch, w.w_out, k=ko, bias=w.b_out, out=logits, m=m, m_dev=m_dev, rows=rows)
-        K.log_softmax_rows(logits, am_logp, d.vocab, m=m, m_dev=m_dev, rows=rows)
+        with tm("am_output"):
+            K.pack(scratch, [(top, H, 1), (cur.ctx, C_, 1)], k_pad=ko, split=True, **kw)
+            K.gemm_tc(scratch, w.w_out, k=ko, bias=w.b_out, out=logits, m=m, m_dev=m_dev,
+                      rows=rows)
+            K.log_softmax_rows(logits, am_logp, d.vocab, m=m, m_dev=m_dev, rows=rows)
+
+
+class _NullSpan:
+    def __call__(self, name):
+        return self
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+_null_timer = _NullSpan()
 
 
 @dataclass
