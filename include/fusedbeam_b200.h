@@ -222,13 +222,14 @@ int fb_log_softmax_rows(int32_t m_max, const int32_t* m_dev, const int32_t* rows
 /* Bahdanau attention step for every active utterance:
  * e[r,t] = v . tanh(keys[u,t] + q[r]); a = softmax_t(e) over t < t_enc[u];
  * ctx[r] = sum_t a[r,t] enc[u,t]; acc_out[r] = acc_in[parent[r]] + a[r]
- * (fp64) and its coverage (cfg->cov_mode).  Rows r = u*beam + i, i < n_live[u]. */
+ * (fp64) and its coverage (cfg->cov_mode).  Rows r = u*beam + i, i < n_live[u].
+ * energy_ws: scratch [num_utts*beam, t_max] fp32. */
 int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts, const int32_t* active,
                       const int32_t* n_live, const int32_t* t_enc, const float* keys,
                       const float* enc, int32_t att_dim, int32_t ctx_dim, const float* v,
                       const float* q, int64_t ldq, const int32_t* parent, const double* acc_in,
                       double* acc_out, double* cov_out, float* ctx_out, int64_t ld_ctx,
-                      float* attn_out, int64_t ld_attn, void* stream);
+                      float* attn_out, int64_t ld_attn, float* energy_ws, void* stream);
 
 /* ---- word-LM bookkeeping for the fused engine ---------------------------- */
 /* Speculative <eos> events (fusion.py:181-183): for every listed row whose

@@ -83,7 +83,7 @@ _SIGS = {
     "fb_pack_rows": (C.c_int, [C.POINTER(FbPack), i32, vp, vp, vp, vp, vp, vp, i64, vp]),
     "fb_log_softmax_rows": (C.c_int, [i32, vp, vp, vp, i64, i32, vp, i64, vp]),
     "fb_attention_step": (C.c_int, [C.POINTER(FbSearchCfg), i32, vp, vp, vp, vp, vp, i32, i32,
-                                    vp, vp, i64, vp, vp, vp, vp, vp, i64, vp, i64, vp]),
+                                    vp, vp, i64, vp, vp, vp, vp, vp, i64, vp, i64, vp, vp]),
     "fb_spec_events": (C.c_int, [C.POINTER(FbTrie), i32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                  vp]),
     "fb_boundary_plan": (C.c_int, [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp,

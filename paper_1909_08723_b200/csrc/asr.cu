@@ -91,8 +91,6 @@ __device__ __forceinline__ float tanh_fast(float x) {
   return 1.0f - __fdividef(2.0f, e + 1.0f);
 }
 
-constexpr int kAttThreads = 256;
-constexpr int kAChunk = 32;
 
 template <typename F>
 __device__ double pairwise_sum_d(const double* a, int n, F f) {
@@ -119,85 +117,123 @@ __device__ double pairwise_sum_d(const double* a, int n, F f) {
   return dadd(pairwise_sum_d(a, n2, f), pairwise_sum_d(a + n2, n - n2, f));
 }
 
-// One CTA per active utterance: its live rows share the keys/enc reads.
-// dynamic smem: q[n][A] | v[A] | e[n][T] | kc[kAChunk][T]
-__global__ void __launch_bounds__(kAttThreads)
-attention_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
-                 const int32_t* __restrict__ n_live, const int32_t* __restrict__ t_enc,
-                 const float* __restrict__ keys, const float* __restrict__ enc, int A, int C,
-                 const float* __restrict__ v, const float* __restrict__ q, int64_t ldq,
-                 const int32_t* __restrict__ parent, const double* __restrict__ acc_in,
-                 double* __restrict__ acc_out, double* __restrict__ cov_out,
-                 float* __restrict__ ctx_out, int64_t ld_ctx, float* __restrict__ attn_out,
-                 int64_t ld_attn) {
+// Bahdanau attention in two balanced kernels.
+// (A) energies: CTA = (utterance, chunk of 8 x kEnWarps frames); warp = frame
+//     t; lanes split the attention dim; every live row's energy for frame t is
+//     a warp reduction.  MUFU-bound (ex2 + rcp per tanh).
+// (B) softmax / fp64 accumulator / coverage / context: CTA = (utterance, chunk
+//     of kCtxCols encoder columns); every CTA re-normalises its utterance's
+//     rows (cheap) and CTA 0 of the utterance owns the accumulator + coverage.
+constexpr int kEnWarps = 8;
+constexpr int kEnFrames = 4;          // frames per warp
+constexpr int kMaxBeam = 64;
+constexpr int kCtxCols = 128;
+
+__global__ void __launch_bounds__(kEnWarps * 32)
+att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
+                  const int32_t* __restrict__ n_live, const int32_t* __restrict__ t_enc,
+                  const float* __restrict__ keys, int A, const float* __restrict__ v,
+                  const float* __restrict__ q, int64_t ldq, float* __restrict__ energy) {
   const int u = blockIdx.x;
   if (!active[u]) return;
+  const int T = t_enc[u];
+  const int t_base = blockIdx.y * (kEnWarps * kEnFrames);
+  if (t_base >= T) return;
+  extern __shared__ float sm[];
+  const int K = cfg.beam, TM = cfg.t_max;
+  const int n = n_live[u];
+  float* qs = sm;                  // [n][A]
+  float* vs = qs + n * A;          // [A]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int slot0 = u * K;
+  for (int j = tid; j < n * A; j += blockDim.x) {
+    const int i = j / A, a = j % A;
+    qs[j] = q[(int64_t)(slot0 + i) * ldq + a];
+  }
+  for (int a = tid; a < A; a += blockDim.x) vs[a] = v[a];
+  __syncthreads();
+  const float* ku = keys + (int64_t)u * TM * A;
+  for (int f = 0; f < kEnFrames; ++f) {
+    const int t = t_base + warp * kEnFrames + f;
+    if (t >= T) break;
+    const float* kt = ku + (int64_t)t * A;
+    for (int i0 = 0; i0 < n; i0 += 16) {
+      const int nb = min(16, n - i0);
+      float e[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) e[r] = 0.f;
+      for (int a = lane; a < A; a += 32) {
+        const float k = __ldg(kt + a);
+        const float va = vs[a];
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+          if (r < nb) e[r] = fmaf(va, tanh_fast(k + qs[(i0 + r) * A + a]), e[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        float x = e[r];
+        for (int off = 16; off; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+        e[r] = x;
+      }
+      if (lane < nb) {
+        float x = 0.f;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) x = lane == r ? e[r] : x;
+        energy[(int64_t)(slot0 + i0 + lane) * TM + t] = x;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256)
+att_context_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
+                   const int32_t* __restrict__ n_live, const int32_t* __restrict__ t_enc,
+                   const float* __restrict__ enc, int C, const float* __restrict__ energy,
+                   const int32_t* __restrict__ parent, const double* __restrict__ acc_in,
+                   double* __restrict__ acc_out, double* __restrict__ cov_out,
+                   float* __restrict__ ctx_out, int64_t ld_ctx, float* __restrict__ attn_out,
+                   int64_t ld_attn) {
+  const int u = blockIdx.x;
+  if (!active[u]) return;
+  const int c0 = blockIdx.y * kCtxCols;
+  if (c0 >= C) return;
   extern __shared__ float sm[];
   const int K = cfg.beam, TM = cfg.t_max;
   const int n = n_live[u];
   const int T = t_enc[u];
-  float* qs = sm;                       // [n][A]
-  float* vs = qs + n * A;               // [A]
-  float* es = vs + A;                   // [n][T]
-  float* kc = es + n * T;               // [kAChunk][T]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kAttThreads / 32;
+  float* al = sm;                  // [n][T] attention weights
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int slot0 = u * K;
-  for (int j = tid; j < n * A; j += kAttThreads) {
-    const int i = j / A, a = j % A;
-    qs[j] = q[(int64_t)(slot0 + i) * ldq + a];
-  }
-  for (int a = tid; a < A; a += kAttThreads) vs[a] = v[a];
-  for (int j = tid; j < n * T; j += kAttThreads) es[j] = 0.f;
-  const float* ku = keys + (int64_t)u * TM * A;
-  const float* eu = enc + (int64_t)u * TM * C;
-  // energies e[i][t] = sum_a v[a] tanh(k[t][a] + q[i][a]); each thread owns
-  // frames t, keeps its key chunk in registers and reads q/v as broadcasts.
-  for (int a0 = 0; a0 < A; a0 += kAChunk) {
-    const int ac = min(kAChunk, A - a0);
-    __syncthreads();
-    for (int j = tid; j < T * kAChunk; j += kAttThreads) {
-      const int t = j / kAChunk, a = j % kAChunk;
-      if (a < ac) kc[a * T + t] = ku[(int64_t)t * A + a0 + a];
-    }
-    __syncthreads();
-    for (int t = tid; t < T; t += kAttThreads) {
-      float kr[kAChunk];
-#pragma unroll
-      for (int a = 0; a < kAChunk; ++a) kr[a] = a < ac ? kc[a * T + t] : 0.f;
-      for (int i = 0; i < n; ++i) {
-        const float* qi = qs + i * A + a0;
-        float s = 0.f;
-#pragma unroll
-        for (int a = 0; a < kAChunk; ++a)
-          if (a < ac) s = fmaf(vs[a0 + a], tanh_fast(kr[a] + qi[a]), s);
-        es[i * T + t] += s;
-      }
-    }
-  }
-  __syncthreads();
-  // softmax over frames, one warp per row
+  // softmax over frames, one warp per row (every column chunk recomputes it)
   for (int i = warp; i < n; i += nw) {
-    float* e = es + i * T;
+    const float* e = energy + (int64_t)(slot0 + i) * TM;
+    float* a = al + i * T;
     float mx = -INFINITY;
-    for (int t = lane; t < T; t += 32) mx = fmaxf(mx, e[t]);
+    for (int t = lane; t < T; t += 32) {
+      const float x = e[t];
+      a[t] = x;
+      mx = fmaxf(mx, x);
+    }
     for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
     float s = 0.f;
     for (int t = lane; t < T; t += 32) {
-      const float x = expf(e[t] - mx);
-      e[t] = x;
+      const float x = expf(a[t] - mx);
+      a[t] = x;
       s += x;
     }
     for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
     const float inv = 1.0f / s;
-    for (int t = lane; t < T; t += 32) e[t] *= inv;
+    for (int t = lane; t < T; t += 32) a[t] *= inv;
   }
   __syncthreads();
-  // context vectors ctx[i][c] = sum_t a[i][t] enc[t][c]: 8 frames of enc in
-  // flight per thread (coalesced over c), attention weights broadcast
+  // context columns [c0, c0 + kCtxCols): thread = (column, row half)
+  const float* eu = enc + (int64_t)u * TM * C;
   constexpr int RB = 16, TU = 8;
-  for (int i0 = 0; i0 < n; i0 += RB) {
-    const int nb = min(RB, n - i0);
-    for (int c = tid; c < C; c += kAttThreads) {
+  const int col = c0 + (tid % kCtxCols);
+  const int half = tid / kCtxCols;           // 0..1 -> interleaved row groups
+  if (col < C) {
+    for (int i0 = half * RB; i0 < n; i0 += 2 * RB) {
+      const int nb = min(RB, n - i0);
       float acc[RB];
 #pragma unroll
       for (int r = 0; r < RB; ++r) acc[r] = 0.f;
@@ -205,35 +241,36 @@ attention_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
       for (; t + TU <= T; t += TU) {
         float x[TU];
 #pragma unroll
-        for (int j = 0; j < TU; ++j) x[j] = __ldg(eu + (int64_t)(t + j) * C + c);
+        for (int j = 0; j < TU; ++j) x[j] = __ldg(eu + (int64_t)(t + j) * C + col);
 #pragma unroll
         for (int j = 0; j < TU; ++j)
 #pragma unroll
           for (int r = 0; r < RB; ++r)
-            if (r < nb) acc[r] = fmaf(es[(i0 + r) * T + t + j], x[j], acc[r]);
+            if (r < nb) acc[r] = fmaf(al[(i0 + r) * T + t + j], x[j], acc[r]);
       }
       for (; t < T; ++t) {
-        const float x = __ldg(eu + (int64_t)t * C + c);
+        const float x = __ldg(eu + (int64_t)t * C + col);
 #pragma unroll
         for (int r = 0; r < RB; ++r)
-          if (r < nb) acc[r] = fmaf(es[(i0 + r) * T + t], x, acc[r]);
+          if (r < nb) acc[r] = fmaf(al[(i0 + r) * T + t], x, acc[r]);
       }
-      for (int r = 0; r < nb; ++r) ctx_out[(int64_t)(slot0 + i0 + r) * ld_ctx + c] = acc[r];
+      for (int r = 0; r < nb; ++r) ctx_out[(int64_t)(slot0 + i0 + r) * ld_ctx + col] = acc[r];
     }
   }
-  // fp64 accumulator + coverage, one warp per row
+  if (blockIdx.y != 0) return;
+  // fp64 accumulator + coverage (decoder.py:421-425), one warp per row
   for (int i = warp; i < n; i += nw) {
     const int r = slot0 + i;
     const int p = parent ? parent[r] : r;
     const double* a0 = acc_in + (int64_t)p * TM;
     double* a1 = acc_out + (int64_t)r * TM;
-    const float* e = es + i * T;
+    const float* a = al + i * T;
     int cnt = 0;
     for (int t = lane; t < T; t += 32) {
-      const double x = dadd(a0[t], (double)e[t]);
+      const double x = dadd(a0[t], (double)a[t]);
       a1[t] = x;
       cnt += x > cfg.tau1;
-      if (attn_out) attn_out[(int64_t)r * ld_attn + t] = e[t];
+      if (attn_out) attn_out[(int64_t)r * ld_attn + t] = a[t];
     }
     if (cfg.cov_mode != 0) {
       for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
@@ -439,20 +476,33 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
                                  int64_t ldq, const int32_t* parent, const double* acc_in,
                                  double* acc_out, double* cov_out, float* ctx_out,
                                  int64_t ld_ctx, float* attn_out, int64_t ld_attn,
-                                 void* stream) {
-  FB_CHECK_ARG(cfg && keys && enc && v && q && acc_in && acc_out && ctx_out, "null attention args");
+                                 float* energy_ws, void* stream) {
+  FB_CHECK_ARG(cfg && keys && enc && v && q && acc_in && acc_out && ctx_out && energy_ws,
+               "null attention args");
   FB_CHECK_ARG(cfg->cov_mode == 0 || cov_out, "coverage output required");
+  FB_CHECK_ARG(cfg->beam <= kMaxBeam, "beam too large for the attention kernels");
   if (num_utts <= 0) return FB_OK;
-  const size_t smem = sizeof(float) * ((size_t)cfg->beam * att_dim + att_dim +
-                                       (size_t)cfg->beam * cfg->t_max + (size_t)kAChunk * cfg->t_max);
-  if (smem > 220 * 1024) return fail(FB_ERR_CONFIG, "attention working set exceeds shared memory");
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  attention_kernel<<<num_utts, kAttThreads, smem, (cudaStream_t)stream>>>(
-      *cfg, active, n_live, t_enc, keys, enc, att_dim, ctx_dim, v, q, ldq, parent, acc_in,
-      acc_out, cov_out, ctx_out, ld_ctx, attn_out, ld_attn);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t sm_e = sizeof(float) * ((size_t)cfg->beam * att_dim + att_dim);
+  const size_t sm_c = sizeof(float) * (size_t)cfg->beam * cfg->t_max;
+  if (sm_e > 200 * 1024 || sm_c > 200 * 1024)
+    return fail(FB_ERR_CONFIG, "attention working set exceeds shared memory");
+  if (sm_e > 48 * 1024)
+    cudaFuncSetAttribute(att_energy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_e);
+  if (sm_c > 48 * 1024)
+    cudaFuncSetAttribute(att_context_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c);
+  dim3 ge(num_utts, (cfg->t_max + kEnWarps * kEnFrames - 1) / (kEnWarps * kEnFrames));
+  att_energy_kernel<<<ge, kEnWarps * 32, sm_e, s>>>(*cfg, active, n_live, t_enc, keys, att_dim,
+                                                     v, q, ldq, energy_ws);
   count_launch();
-  return check_launch("attention_step");
+  int rc = check_launch("att_energy");
+  if (rc) return rc;
+  dim3 gc(num_utts, (ctx_dim + kCtxCols - 1) / kCtxCols);
+  att_context_kernel<<<gc, 256, sm_c, s>>>(*cfg, active, n_live, t_enc, enc, ctx_dim, energy_ws,
+                                           parent, acc_in, acc_out, cov_out, ctx_out, ld_ctx,
+                                           attn_out, ld_attn);
+  count_launch();
+  return check_launch("att_context");
 }
 
 extern "C" int fb_spec_events(const fb_trie_t* trie, int32_t n_max, const int32_t* n_dev,

@@ -176,6 +176,7 @@ class FusedDecoder:
         q = torch.empty((N, d.att), dtype=torch.float32, device=dev)
         logits = torch.empty((N, V), dtype=torch.float32, device=dev)
         am_logp = torch.zeros((N, V), dtype=torch.float32, device=dev)
+        energy = torch.empty((N, TM), dtype=torch.float32, device=dev)
 
         fus_buf = None
         if has_fusion:
@@ -198,7 +199,7 @@ class FusedDecoder:
                                q=q, logits=logits, am_logp=am_logp, cfg_ref=cfg_ref, num_utts=B,
                                active=buf.active, n_live=buf.n_live, t_enc=buf.t_enc, keys=keys,
                                enc=enc, acc_in=buf.acc[c], acc_out=buf.acc[1 - c], cov=buf.cov,
-                               timer=timer)
+                               energy=energy, timer=timer)
             if has_fusion:
                 with tm("lookahead"):
                     # word_end in the eos column of final rows; log P(</s>) added below

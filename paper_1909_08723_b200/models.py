@@ -211,7 +211,7 @@ class DecoderStep:
     def __call__(self, *, N: int, rows, m: int, m_dev, parent, last_tok, prev: AmState,
                  cur: AmState, scratch: torch.Tensor, q: torch.Tensor, logits: torch.Tensor,
                  am_logp: torch.Tensor, cfg_ref, num_utts: int, active, n_live, t_enc,
-                 keys, enc, acc_in, acc_out, cov, attn_out=None, timer=None) -> None:
+                 keys, enc, acc_in, acc_out, cov, energy, attn_out=None, timer=None) -> None:
         w, d = self.w, self.w.d
         tm = timer if timer is not None else _null_timer
         H, C_, E = d.dec_hidden, d.ctx, d.emb
@@ -240,7 +240,8 @@ class DecoderStep:
                       _lib.ptr(w.v), _lib.ptr(q), q.stride(0), _lib.ptr(parent),
                       _lib.ptr(acc_in), _lib.ptr(acc_out), _lib.ptr(cov), _lib.ptr(cur.ctx),
                       cur.ctx.stride(0), _lib.ptr(attn_out),
-                      0 if attn_out is None else attn_out.stride(0), _lib.stream_ptr())
+                      0 if attn_out is None else attn_out.stride(0), _lib.ptr(energy),
+                      _lib.stream_ptr())
         ko = w.w_out.shape[1]
         with tm("am_output"):
             K.pack(scratch, [(top, H, 1), (cur.ctx, C_, 1)], k_pad=ko, split=True, **kw)
@@ -308,6 +309,7 @@ class AttnLstmScorer:
         acc1 = torch.empty_like(acc0)
         attn = torch.empty((n, state.T), dtype=torch.float32, device=dev)
         scratch = split_scratch(n, self.weights.k_max, dev)
+        energy = torch.empty((n, state.T), dtype=torch.float32, device=dev)
         q = torch.empty((n, d.att), dtype=torch.float32, device=dev)
         logits = torch.empty((n, d.vocab), dtype=torch.float32, device=dev)
         logp = torch.empty((n, d.vocab), dtype=torch.float32, device=dev)
@@ -315,7 +317,7 @@ class AttnLstmScorer:
                      cur=cur, scratch=scratch, q=q, logits=logits, am_logp=logp,
                      cfg_ref=C.byref(cfg), num_utts=1, active=one, n_live=nl, t_enc=te,
                      keys=state.keys, enc=state.enc, acc_in=acc0, acc_out=acc1, cov=None,
-                     attn_out=attn)
+                     energy=energy, attn_out=attn)
         return (logp.cpu().numpy(), attn.cpu().numpy(),
                 _UttState(state.enc, state.keys, state.T, cur))
 
