@@ -183,6 +183,9 @@ typedef struct {
   float* h_out; int64_t ld_h;
   const float* h_res; int64_t ld_res;
   const float* addend; int64_t ld_add;
+  /* mode 1, optional: h also written as 3 bf16 planes (hi/mid/lo) at
+   * [p*hs_plane_rows + slot][unit] -- the A operand of a following GEMM */
+  void* h_split; int64_t hs_plane_rows; int64_t ld_hs;
 } fb_gemm_t;
 
 int fb_gemm(const fb_gemm_t* g, void* stream);
@@ -192,6 +195,14 @@ int fb_gemm(const fb_gemm_t* g, void* stream);
  * hi/mid/lo by fb_pack_rows out_mode 1), W is bf16 [n, ldw]; fp32
  * accumulation in TMEM.  k % 64 == 0, lda/ldw % 8 == 0. */
 int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_rows, void* stream);
+
+/* Encoder LSTM recurrence for one direction: for t < steps,
+ * gates = xp[:, t] + h_{t-1} W_hh^T (tensor cores, W_hh bf16 [4H, k]), cell
+ * epilogue, h_t -> y[:, t] (row stride ld_y) and, split into bf16 planes, into
+ * rec[(t+1)%2] ([2][3][batch][k] bf16, rec[0] zero on entry).  c_buf: [2][batch][H]. */
+int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden, const void* w_hh,
+                       int32_t k, const float* xp, int64_t ld_xp, float* y, int64_t ld_y,
+                       float* c_buf, void* rec, void* stream);
 
 /* Row gather-concatenate into a GEMM A operand:
  *   out[i, :] = [seg0 | seg1 | ... | zero pad up to k_pad], i < m.

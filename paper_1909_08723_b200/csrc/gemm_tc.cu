@@ -15,6 +15,7 @@
 #include "common.cuh"
 
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
 namespace fb {
@@ -100,45 +101,82 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 
 __device__ __forceinline__ float sigm_tc(float x) { return 1.0f / (1.0f + expf(-x)); }
 
+__device__ __forceinline__ float fsig(float x) { return __frcp_rn(1.0f + __expf(-x)); }
+
+__device__ __forceinline__ float ftanh(float x) {
+  x = fminf(fmaxf(x, -15.0f), 15.0f);
+  return 1.0f - 2.0f * __frcp_rn(1.0f + __expf(2.0f * x));
+}
+
+__device__ __forceinline__ void store_split(const fb_gemm_t& g, int64_t row, int col, float x) {
+  // hi/mid/lo bf16 planes of an fp32 value (the next GEMM's A operand)
+  __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.h_split) + row * g.ld_hs + col;
+  const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+  const float r1 = x - __bfloat162float(hi);
+  const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+  o[0] = hi;
+  o[g.hs_plane_rows * g.ld_hs] = mid;
+  o[2 * g.hs_plane_rows * g.ld_hs] = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+}
+
+// One warp drains its 32 TMEM lanes (rows) chunk by chunk; each 32x32 chunk is
+// transposed through shared memory so global loads/stores are row-contiguous
+// across the warp (plain mode: lane = column; LSTM mode: lane = (row, unit)).
 template <int BN>
-__device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row, int n0,
-                                              uint32_t taddr) {
-  const bool row_ok = row < M;
+__device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row0, int n0,
+                                              uint32_t taddr, float* st /* [32][33] */) {
+  const int lane = threadIdx.x & 31;
   for (int cb = 0; cb < BN / 32; ++cb) {
     float v[32];
     __syncwarp();
     tmem_ld32(taddr + cb * 32, v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) st[lane * 33 + j] = v[j];
+    __syncwarp();
     const int nb = n0 + cb * 32;
-    if (!row_ok || nb >= g.n) continue;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int n = nb + j;
-      if (n < g.n) {
-        if (g.bias) v[j] += g.bias[n];
-        if (g.addend) v[j] += g.addend[(int64_t)row * g.ld_add + n];
-      }
-    }
+    if (nb >= g.n) continue;
     if (g.mode == 1) {
-      const int slot = g.rows ? g.rows[row] : row;
-      const int pr = g.parent ? g.parent[slot] : slot;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int unit = (nb >> 2) + u;
-        if (unit * 4 < g.n) {
+      const int u = lane & 7, rs = lane >> 3;
+      const int unit = (nb >> 2) + u;
+      if (unit * 4 < g.n) {
+        float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (g.bias) b4 = *reinterpret_cast<const float4*>(g.bias + 4 * unit);
+#pragma unroll 2
+        for (int it = 0; it < 8; ++it) {
+          const int r = it * 4 + rs;
+          const int row = row0 + r;
+          if (row >= M) break;
+          float gi = st[r * 33 + 4 * u] + b4.x, gf = st[r * 33 + 4 * u + 1] + b4.y;
+          float gg = st[r * 33 + 4 * u + 2] + b4.z, go = st[r * 33 + 4 * u + 3] + b4.w;
+          if (g.addend) {
+            const float4 a4 =
+                *reinterpret_cast<const float4*>(g.addend + (int64_t)row * g.ld_add + 4 * unit);
+            gi += a4.x; gf += a4.y; gg += a4.z; go += a4.w;
+          }
+          const int slot = g.rows ? g.rows[row] : row;
+          const int pr = g.parent ? g.parent[slot] : slot;
           const float cp = g.c_in ? g.c_in[(int64_t)pr * g.ld_cin + unit] : 0.0f;
-          const float c = sigm_tc(v[4 * u + 1]) * cp + sigm_tc(v[4 * u]) * tanhf(v[4 * u + 2]);
-          float h = sigm_tc(v[4 * u + 3]) * tanhf(c);
+          const float c = fsig(gf) * cp + fsig(gi) * ftanh(gg);
+          float h = fsig(go) * ftanh(c);
           if (g.h_res) h += g.h_res[(int64_t)slot * g.ld_res + unit];
           g.c_out[(int64_t)slot * g.ld_cout + unit] = c;
           g.h_out[(int64_t)slot * g.ld_h + unit] = h;
+          if (g.h_split) store_split(g, slot, unit, h);
         }
       }
     } else {
-      const int orow = g.rows ? g.rows[row] : row;
-      float* c = g.c + (int64_t)orow * g.ldc;
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (nb + j < g.n) c[nb + j] = v[j];
+      const int col = nb + lane;
+      const float bj = (g.bias && col < g.n) ? g.bias[col] : 0.f;
+      for (int r = 0; r < 32; ++r) {
+        const int row = row0 + r;
+        if (row >= M) break;
+        if (col < g.n) {
+          float x = st[r * 33 + lane] + bj;
+          if (g.addend) x += g.addend[(int64_t)row * g.ld_add + col];
+          const int orow = g.rows ? g.rows[row] : row;
+          g.c[(int64_t)orow * g.ldc + col] = x;
+        }
+      }
     }
   }
   __syncwarp();
@@ -168,6 +206,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   __shared__ __align__(8) uint64_t bar_full[TC_STAGES], bar_empty[TC_STAGES];
   __shared__ __align__(8) uint64_t bar_tfull[2], bar_tempty[2];
   __shared__ uint32_t tmem_base_sh;
+  __shared__ float epi_stage[4][32 * 33];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -250,8 +289,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int m0 = (tile % m_tiles) * TC_BM, n0 = (tile / m_tiles) * BN;
       mbar_wait(smem_u32(&bar_tfull[acc]), (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      epilogue_tile<BN>(g, M, m0 + quarter * 32 + lane, n0,
-                        tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN);
+      epilogue_tile<BN>(g, M, m0 + quarter * 32, n0,
+                        tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN, epi_stage[warp - 2]);
       asm volatile("tcgen05.fence::before_thread_sync;");
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[acc]))
                    : "memory");
@@ -295,6 +334,25 @@ static int make_map(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t col
 }
 
 template <int BN>
+static int launch_tc_maps(const CUtensorMap& ta, const CUtensorMap& tw, const fb_gemm_t* g,
+                          int a_planes, int64_t a_plane_rows, cudaStream_t s) {
+  const int stage_bytes = a_planes * TC_BM * TC_BK * 2 + BN * TC_BK * 2;
+  const size_t smem = (size_t)TC_STAGES * stage_bytes + 1024;
+  auto k = gemm_tc_kernel<BN>;
+  static size_t smem_set = 0;                       // set once (graph-capture safe)
+  if (smem > smem_set) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(3 * (3 * TC_BM * TC_BK * 2 + BN * TC_BK * 2) + 1024));
+    smem_set = 3 * (3 * TC_BM * TC_BK * 2 + BN * TC_BK * 2) + 1024;
+  }
+  const int tiles = ((g->m_max + TC_BM - 1) / TC_BM) * ((g->n + BN - 1) / BN);
+  k<<<std::min(tiles, kNumSMs), TC_THREADS, smem, s>>>(ta, tw, *g, a_planes, (int)a_plane_rows,
+                                                      g->k / TC_BK);
+  count_launch();
+  return check_launch("gemm_tc");
+}
+
+template <int BN>
 static int launch_tc(const fb_gemm_t* g, int a_planes, int64_t a_plane_rows, int64_t w_rows,
                      cudaStream_t s) {
   CUtensorMap ta, tw;
@@ -302,15 +360,7 @@ static int launch_tc(const fb_gemm_t* g, int a_planes, int64_t a_plane_rows, int
   if (rc) return rc;
   rc = make_map(&tw, g->w, w_rows, g->k, g->ldw, BN);
   if (rc) return rc;
-  const int stage_bytes = a_planes * TC_BM * TC_BK * 2 + BN * TC_BK * 2;
-  const size_t smem = (size_t)TC_STAGES * stage_bytes + 1024;
-  auto k = gemm_tc_kernel<BN>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int tiles = ((g->m_max + TC_BM - 1) / TC_BM) * ((g->n + BN - 1) / BN);
-  k<<<std::min(tiles, kNumSMs), TC_THREADS, smem, s>>>(ta, tw, *g, a_planes, (int)a_plane_rows,
-                                                      g->k / TC_BK);
-  count_launch();
-  return check_launch("gemm_tc");
+  return launch_tc_maps<BN>(ta, tw, g, a_planes, a_plane_rows, s);
 }
 
 }  // namespace fb
@@ -329,6 +379,59 @@ extern "C" int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_
   FB_CHECK_ARG(g->mode != 1 || (g->n == 4 * g->hidden && g->h_out && g->c_out),
                "LSTM epilogue needs n == 4*hidden and state outputs");
   FB_CHECK_ARG(g->mode != 0 || g->c, "GEMM output is null");
+  FB_CHECK_ARG(g->mode != 1 || g->bias == nullptr || ((uintptr_t)g->bias % 16) == 0,
+               "LSTM bias must be 16B aligned");
+  FB_CHECK_ARG(g->mode != 1 || g->addend == nullptr ||
+                   (((uintptr_t)g->addend % 16) == 0 && g->ld_add % 4 == 0),
+               "LSTM addend must be 16B aligned");
   if (g->m_max <= 0) return FB_OK;
+  // small problems: half-width tiles so more SMs take part
+  const int tiles128 = ((g->m_max + TC_BM - 1) / TC_BM) * ((g->n + 127) / 128);
+  if (tiles128 < kNumSMs / 2 && g->n > 64)
+    return launch_tc<64>(g, a_planes, a_plane_rows, g->n, (cudaStream_t)stream);
   return launch_tc<128>(g, a_planes, a_plane_rows, g->n, (cudaStream_t)stream);
+}
+
+// LSTM recurrence over `steps` time steps for one direction (the encoder):
+// h_t = cell(xp[:, t] + h_{t-1} W_hh^T), h written to y[:, t] and, split into
+// bf16 planes, to rec[(t+1)%2] (the next step's A operand).  The host loop
+// lives here so a layer costs one C call; tensor maps are built once.
+extern "C" int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden,
+                                  const void* w_hh, int32_t k, const float* xp, int64_t ld_xp,
+                                  float* y, int64_t ld_y, float* c_buf, void* rec,
+                                  void* stream) {
+  FB_CHECK_ARG(w_hh && xp && y && c_buf && rec, "null recurrence buffers");
+  FB_CHECK_ARG(k % TC_BK == 0 && k >= hidden, "recurrence k must be a multiple of 64 >= hidden");
+  FB_CHECK_ARG(steps >= 0 && batch > 0, "bad recurrence sizes");
+  cudaStream_t s = (cudaStream_t)stream;
+  __nv_bfloat16* r = reinterpret_cast<__nv_bfloat16*>(rec);
+  const int64_t plane = (int64_t)batch * k;          // elements per plane
+  fb_gemm_t g{};
+  g.m_max = batch; g.m_dev = nullptr; g.n = 4 * hidden; g.k = k;
+  g.lda = k; g.w = w_hh; g.ldw = k; g.bias = nullptr;
+  g.mode = 1; g.hidden = hidden;
+  g.ld_cin = hidden; g.ld_cout = hidden; g.ld_h = ld_y; g.ld_add = ld_xp;
+  g.hs_plane_rows = batch; g.ld_hs = k;
+  const int tiles128 = ((batch + TC_BM - 1) / TC_BM) * ((g.n + 127) / 128);
+  const bool narrow = tiles128 < kNumSMs / 2;
+  CUtensorMap ta[2], tw;
+  for (int p = 0; p < 2; ++p) {
+    int rc = make_map(&ta[p], r + (int64_t)p * 3 * plane, 3ull * batch, k, k, TC_BM);
+    if (rc) return rc;
+  }
+  int rc = make_map(&tw, w_hh, g.n, k, k, narrow ? 64 : 128);
+  if (rc) return rc;
+  for (int t = 0; t < steps; ++t) {
+    const int cur = t & 1, nxt = cur ^ 1;
+    g.a = r + (int64_t)cur * 3 * plane;
+    g.c_in = t ? c_buf + (int64_t)cur * batch * hidden : nullptr;
+    g.c_out = c_buf + (int64_t)nxt * batch * hidden;
+    g.h_out = y + (int64_t)t * hidden;
+    g.addend = xp + (int64_t)t * 4 * hidden;
+    g.h_split = r + (int64_t)nxt * 3 * plane;
+    rc = narrow ? launch_tc_maps<64>(ta[cur], tw, &g, 3, batch, s)
+                : launch_tc_maps<128>(ta[cur], tw, &g, 3, batch, s);
+    if (rc) return rc;
+  }
+  return FB_OK;
 }

@@ -136,6 +136,8 @@ class FusedDecoder:
         self.spec_counts: Optional[torch.Tensor] = None
         self.steps_run = 0
         self.prune_spec = True      # exact pruning of speculative <eos> LM events
+        self.use_graphs = True      # one CUDA graph per step parity, replayed
+        self.poll_every = 8         # host polls the live-row count every k steps
 
     def run(self, X: torch.Tensor, T: Sequence[int], utt_ids: Sequence[str], timer=None,
             record_counts: bool = False) -> List[DecodeResult]:
@@ -188,11 +190,9 @@ class FusedDecoder:
             Vw = lw.d.words
         counts = [] if record_counts else None
 
-        parity = 0
-        steps = 0
-        while True:
-            c = parity
+        def step(c: int) -> None:
             rc, nc = rows[c], count[c]
+            stream = _lib.stream_ptr()          # the capture stream inside a graph
             with tm("am_step"):
                 scorer.step_fn(N=N, rows=rc, m=N, m_dev=nc, parent=buf.parent,
                                last_tok=buf.last_tok, prev=X2[1 - c], cur=X2[c], scratch=scratch,
@@ -256,10 +256,27 @@ class FusedDecoder:
                 if counts is not None:
                     counts.append(lm.bnd_count.clone())
                     counts.append(lm.unk_count.clone())
-            parity ^= 1
-            steps += 1
-            if int(count[parity].item()) == 0:
-                break
+        parity = 0
+        steps = 0
+        if self.use_graphs and timer is None and counts is None:
+            graphs = [torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()]
+            for p_ in (0, 1):
+                with torch.cuda.graph(graphs[p_]):
+                    step(p_)
+            while True:
+                for _ in range(self.poll_every):
+                    graphs[parity].replay()
+                    parity ^= 1
+                    steps += 1
+                if int(count[parity].item()) == 0:
+                    break
+        else:
+            while True:
+                step(parity)
+                parity ^= 1
+                steps += 1
+                if int(count[parity].item()) == 0:
+                    break
         self.steps_run = steps
         if counts is not None:
             self.spec_counts = torch.cat(counts).view(steps, 3).cpu() if counts else None

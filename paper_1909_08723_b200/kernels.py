@@ -67,8 +67,9 @@ def pack(out: torch.Tensor, segs: Sequence[Tuple], *, m: int, m_dev=None, rows=N
 def gemm_tc(ap: torch.Tensor, w: torch.Tensor, *, m: Optional[int] = None, m_dev=None,
             k: Optional[int] = None, bias=None, out=None, rows=None, mode: int = 0,
             hidden: int = 0, parent=None, c_in=None, c_out=None, h_out=None, h_res=None,
-            addend=None) -> None:
-    """Tensor-core GEMM: ap = bf16 planes [P, rows, k_pad], w = bf16 [n, k_pad]."""
+            addend=None, h_split=None) -> None:
+    """Tensor-core GEMM: ap = bf16 planes [P, rows, k_pad], w = bf16 [n, k_pad].
+    h_split: optional bf16 [3, rows, k] planes receiving h (next A operand)."""
     g = _lib.FbGemm()
     g.m_max = ap.shape[1] if m is None else m
     g.m_dev = P(m_dev)
@@ -85,6 +86,8 @@ def gemm_tc(ap: torch.Tensor, w: torch.Tensor, *, m: Optional[int] = None, m_dev
     g.h_out, g.ld_h = P(h_out), _ld(h_out)
     g.h_res, g.ld_res = P(h_res), _ld(h_res)
     g.addend, g.ld_add = P(addend), _ld(addend)
+    if h_split is not None:
+        g.h_split, g.hs_plane_rows, g.ld_hs = P(h_split), h_split.shape[1], h_split.stride(1)
     _lib.call("fb_gemm_tc", C.byref(g), ap.shape[0], ap.shape[1], _lib.stream_ptr())
 
 

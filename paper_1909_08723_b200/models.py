@@ -128,6 +128,7 @@ class Encoder:
     def __init__(self, w: AsrWeights, device):
         self.w = w
         self.device = device
+        self.streams = None
 
     def stage(self, feats: Sequence[np.ndarray], pin: bool = False):
         """Host-side frame stacking into one [B*TM, Din_pad] array (+ lengths)."""
@@ -164,28 +165,37 @@ class Encoder:
         kr = _pad(He)
         Xr = torch.empty_like(X)
         big = split_scratch(B * TM, max(X.shape[1], _pad(2 * He)), dev)
-        rec = split_scratch(B, kr, dev)
+        if self.streams is None:
+            self.streams = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
         for l, dirs in enumerate(self.w.enc):
             kin = X.shape[1]
             K.copy_rows(X, Xr, m=B * TM, src_idx=rev_t)
             ys = []
+            xps = []
             for r, (w_ih, w_hh, b) in enumerate(dirs):
                 src = X if r == 0 else Xr
                 xp = torch.empty((B * TM, 4 * He), dtype=torch.float32, device=dev)
                 K.pack(big, [(src, kin, 0)], m=B * TM, k_pad=kin, split=True)
                 K.gemm_tc(big[:, :, :kin], w_ih, m=B * TM, k=kin, bias=b, out=xp)
-                y = torch.zeros((B, TM, He), dtype=torch.float32, device=dev)
-                cbuf = [torch.zeros((B, He), dtype=torch.float32, device=dev) for _ in range(2)]
-                xp3 = xp.view(B, TM, 4 * He)
-                for t in range(TM):
-                    if t == 0:
-                        K.pack(rec, [(None, He, 0, 0)], m=B, k_pad=kr, split=True)
-                    else:
-                        K.pack(rec, [(y[:, t - 1, :], He, 0, TM * He)], m=B, k_pad=kr, split=True)
-                    K.gemm_tc(rec, w_hh, m=B, k=kr, mode=1, hidden=He,
-                              c_in=None if t == 0 else cbuf[t % 2], c_out=cbuf[(t + 1) % 2],
-                              h_out=y[:, t, :], addend=xp3[:, t, :])
+                xps.append(xp)
+            # the two directions are independent: one stream each
+            main = torch.cuda.current_stream(dev)
+            bufs = [(torch.empty((B, TM, He), dtype=torch.float32, device=dev),
+                     torch.empty((2, B, He), dtype=torch.float32, device=dev),
+                     torch.zeros((2, 3, B, kr), dtype=torch.bfloat16, device=dev))
+                    for _ in range(2)]
+            for r, (w_ih, w_hh, b) in enumerate(dirs):
+                st = self.streams[r]
+                st.wait_stream(main)
+                y, cbuf, rec = bufs[r]
+                for tns in (y, cbuf, rec, xps[r]):
+                    tns.record_stream(st)
+                _lib.call("fb_lstm_recurrence", TM, B, He, _lib.ptr(w_hh), kr, _lib.ptr(xps[r]),
+                          TM * 4 * He, _lib.ptr(y), TM * He, _lib.ptr(cbuf), _lib.ptr(rec),
+                          int(st.cuda_stream))
                 ys.append(y.reshape(B * TM, He))
+            for st in self.streams:
+                main.wait_stream(st)
             kout = _pad(2 * He)
             Xn = torch.empty((B * TM, kout), dtype=torch.float32, device=dev)
             K.pack(Xn, [(ys[0], He, 0), (ys[1], He, 1)], m=B * TM, rows=rev_t)
