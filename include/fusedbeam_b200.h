@@ -91,6 +91,18 @@ int fb_logits_to_g(int32_t m_max, const int32_t* m_dev, const float* logits,
                    const int32_t* slots, double* g_pool, int64_t g_stride, double* eos_out,
                    void* stream);
 
+/* Same quantities using the LM-output GEMM's per-tile statistics
+ * (fb_gemm_t.row_stats): eos_out[d] = logits[vw] - logsumexp(all outputs)
+ * without another pass over the logits; if g_pool, g_pool[d] =
+ * cumsum(softmax over the vw words) in fp64, segment-parallel over
+ * (rows x 4096-column segments) with exact fp64 segment offsets (two passes;
+ * seg_ws: scratch of m_max * ceil(vw/4096) doubles).  Row i < *m_dev reads
+ * logits/stats row src_rows[i]; d = slots ? slots[i] : i. */
+int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* logits, int64_t l_stride,
+                  const float* row_stats, int32_t n_out, const int32_t* src_rows, int32_t vw,
+                  const int32_t* slots, double* g_pool, int64_t g_stride, double* eos_out,
+                  double* seg_ws, void* stream);
+
 /* ---- beam search step (decoder.py:339-480) ------------------------------ */
 typedef struct {
   int32_t beam, vocab, pad_id, eos_id;
@@ -186,6 +198,10 @@ typedef struct {
   /* mode 1, optional: h also written as 3 bf16 planes (hi/mid/lo) at
    * [p*hs_plane_rows + slot][unit] -- the A operand of a following GEMM */
   void* h_split; int64_t hs_plane_rows; int64_t ld_hs;
+  /* mode 0, optional: per (output row, 128-column tile) softmax statistics
+   * {max, sum exp(x-max)} over columns < stats_vw and over all columns,
+   * float4 at row_stats[(orow * ceil(n/128) + tile)] (forces 128-wide tiles) */
+  float* row_stats; int32_t stats_vw; int32_t pad1;
 } fb_gemm_t;
 
 int fb_gemm(const fb_gemm_t* g, void* stream);

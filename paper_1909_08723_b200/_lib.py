@@ -50,7 +50,8 @@ class FbGemm(C.Structure):
                 ("rows", vp), ("parent", vp), ("c_in", vp), ("ld_cin", i64),
                 ("c_out", vp), ("ld_cout", i64), ("h_out", vp), ("ld_h", i64),
                 ("h_res", vp), ("ld_res", i64), ("addend", vp), ("ld_add", i64),
-                ("h_split", vp), ("hs_plane_rows", i64), ("ld_hs", i64)]
+                ("h_split", vp), ("hs_plane_rows", i64), ("ld_hs", i64),
+                ("row_stats", vp), ("stats_vw", i32), ("pad1", i32)]
 
 
 class FbSeg(C.Structure):
@@ -81,6 +82,7 @@ _SIGS = {
     "fb_gather_rows": (C.c_int, [i32, vp, vp, vp, i64, vp]),
     "fb_gemm": (C.c_int, [C.POINTER(FbGemm), vp]),
     "fb_gemm_tc": (C.c_int, [C.POINTER(FbGemm), i32, i64, vp]),
+    "fb_stats_to_g": (C.c_int, [i32, vp, vp, i64, vp, i32, vp, i32, vp, vp, i64, vp, vp, vp]),
     "fb_lstm_recurrence": (C.c_int, [i32, i32, i32, vp, i32, vp, i64, vp, i64, vp, vp, vp]),
     "fb_pack_rows": (C.c_int, [C.POINTER(FbPack), i32, vp, vp, vp, vp, vp, vp, i64, vp]),
     "fb_log_softmax_rows": (C.c_int, [i32, vp, vp, vp, i64, i32, vp, i64, vp]),

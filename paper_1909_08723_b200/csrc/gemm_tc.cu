@@ -126,14 +126,45 @@ template <int BN>
 __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row0, int n0,
                                               uint32_t taddr, float* st /* [32][33] */) {
   const int lane = threadIdx.x & 31;
+  // {max_all, sum_all, max_words, sum_words} of this lane's row over the tile
+  float4 st_stats = make_float4(-INFINITY, 0.f, -INFINITY, 0.f);
   for (int cb = 0; cb < BN / 32; ++cb) {
     float v[32];
     __syncwarp();
     tmem_ld32(taddr + cb * 32, v);
+    const int nb = n0 + cb * 32;
+    if (g.mode == 0 && g.bias) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] += (nb + j < g.n) ? __ldg(g.bias + nb + j) : 0.f;
+    }
+    if (g.row_stats) {
+      // lane = row: online (max, sum exp) over this chunk's valid columns
+      float mw = -INFINITY, ma = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (nb + j < g.n) ma = fmaxf(ma, v[j]);
+        if (nb + j < g.stats_vw) mw = fmaxf(mw, v[j]);
+      }
+      float sw = 0.f, sa = 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (nb + j < g.n) sa += __expf(v[j] - ma);
+        if (nb + j < g.stats_vw) sw += __expf(v[j] - mw);
+      }
+      if (ma > -INFINITY) {
+        const float m2 = fmaxf(st_stats.x, ma);
+        st_stats.y = st_stats.y * __expf(st_stats.x - m2) + sa * __expf(ma - m2);
+        st_stats.x = m2;
+      }
+      if (mw > -INFINITY) {
+        const float m2 = fmaxf(st_stats.z, mw);
+        st_stats.w = st_stats.w * __expf(st_stats.z - m2) + sw * __expf(mw - m2);
+        st_stats.z = m2;
+      }
+    }
 #pragma unroll
     for (int j = 0; j < 32; ++j) st[lane * 33 + j] = v[j];
     __syncwarp();
-    const int nb = n0 + cb * 32;
     if (nb >= g.n) continue;
     if (g.mode == 1) {
       const int u = lane & 7, rs = lane >> 3;
@@ -166,18 +197,23 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
       }
     } else {
       const int col = nb + lane;
-      const float bj = (g.bias && col < g.n) ? g.bias[col] : 0.f;
       for (int r = 0; r < 32; ++r) {
         const int row = row0 + r;
         if (row >= M) break;
         if (col < g.n) {
-          float x = st[r * 33 + lane] + bj;
+          float x = st[r * 33 + lane];
           if (g.addend) x += g.addend[(int64_t)row * g.ld_add + col];
           const int orow = g.rows ? g.rows[row] : row;
           g.c[(int64_t)orow * g.ldc + col] = x;
         }
       }
     }
+  }
+  if (g.row_stats && row0 + lane < M) {
+    const int row = row0 + lane;
+    const int orow = g.rows ? g.rows[row] : row;
+    const int ntiles = (g.n + 127) / 128;
+    reinterpret_cast<float4*>(g.row_stats)[(int64_t)orow * ntiles + n0 / 128] = st_stats;
   }
   __syncwarp();
 }
@@ -387,7 +423,7 @@ extern "C" int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_
   if (g->m_max <= 0) return FB_OK;
   // small problems: half-width tiles so more SMs take part
   const int tiles128 = ((g->m_max + TC_BM - 1) / TC_BM) * ((g->n + 127) / 128);
-  if (tiles128 < kNumSMs / 2 && g->n > 64)
+  if (tiles128 < kNumSMs / 2 && g->n > 64 && !g->row_stats)
     return launch_tc<64>(g, a_planes, a_plane_rows, g->n, (cudaStream_t)stream);
   return launch_tc<128>(g, a_planes, a_plane_rows, g->n, (cudaStream_t)stream);
 }

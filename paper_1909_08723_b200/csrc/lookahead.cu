@@ -261,6 +261,126 @@ row_scan_kernel(int m_max, const int32_t* __restrict__ m_dev, const void* __rest
   }
 }
 
+// ---- softmax statistics from the LM-output GEMM epilogue -------------------
+constexpr int kSegCols = kScanTile;          // 4096 columns per segment CTA
+
+// Row-wide word max (exact) and all-output log-sum-exp from the tile stats.
+__device__ __forceinline__ void row_norm(const float4* __restrict__ st, int ntiles, float& mw,
+                                         double& lse_all, float* red_f, double* red_d) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  float ma = -INFINITY;
+  mw = -INFINITY;
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
+    const float4 v = st[t];
+    ma = fmaxf(ma, v.x);
+    mw = fmaxf(mw, v.z);
+  }
+  for (int off = 16; off; off >>= 1) {
+    ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, off));
+    mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, off));
+  }
+  if (lane == 0) { red_f[warp] = ma; red_f[32 + warp] = mw; }
+  __syncthreads();
+  ma = -INFINITY; mw = -INFINITY;
+  for (int w = 0; w < nw; ++w) { ma = fmaxf(ma, red_f[w]); mw = fmaxf(mw, red_f[32 + w]); }
+  double sa = 0.0;
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
+    const float4 v = st[t];
+    if (v.x > -INFINITY) sa += (double)v.y * exp((double)v.x - (double)ma);
+  }
+  for (int off = 16; off; off >>= 1) sa += __shfl_xor_sync(0xffffffffu, sa, off);
+  __syncthreads();
+  if (lane == 0) red_d[warp] = sa;
+  __syncthreads();
+  sa = 0.0;
+  for (int w = 0; w < nw; ++w) sa += red_d[w];
+  lse_all = (double)ma + log(sa);
+  __syncthreads();
+}
+
+// pass 1 (g_pool): exact fp64 sum of exp(z - M_w) per 4096-column segment;
+// CTA (row, 0) also writes log P(</s>).
+__global__ void __launch_bounds__(kScanThreads)
+seg_sum_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __restrict__ logits,
+               int64_t ld, const float4* __restrict__ stats, int ntiles,
+               const int32_t* __restrict__ src_rows, int vw, const int32_t* __restrict__ slots,
+               double* __restrict__ seg_ws, int nseg, double* __restrict__ eos_out,
+               int do_segs) {
+  __shared__ float red_f[64];
+  __shared__ double red_d[32];
+  const int m = row_count(m_max, m_dev);
+  for (int i = blockIdx.x; i < m; i += gridDim.x) {
+    const int64_t srow = src_rows ? src_rows[i] : i;
+    float mw;
+    double lse;
+    row_norm(stats + srow * ntiles, ntiles, mw, lse, red_f, red_d);
+    const float* lg = logits + srow * ld;
+    if (blockIdx.y == 0 && threadIdx.x == 0 && eos_out)
+      eos_out[slots ? slots[i] : i] = (double)lg[vw] - lse;
+    if (!do_segs) continue;
+    const int c0 = blockIdx.y * kSegCols, c1 = min(vw, c0 + kSegCols);
+    double s = 0.0;
+    for (int j = c0 + threadIdx.x; j < c1; j += blockDim.x) s += (double)expf(lg[j] - mw);
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if ((threadIdx.x & 31) == 0) red_d[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red_d[w];
+      seg_ws[(int64_t)i * nseg + blockIdx.y] = t;
+    }
+    __syncthreads();
+  }
+}
+
+// pass 2: scan each segment with its exact fp64 offset; g = prefix / S_w.
+__global__ void __launch_bounds__(kScanThreads)
+seg_scan_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __restrict__ logits,
+                int64_t ld, const float4* __restrict__ stats, int ntiles,
+                const int32_t* __restrict__ src_rows, int vw, const int32_t* __restrict__ slots,
+                const double* __restrict__ seg_ws, int nseg, double* __restrict__ g_pool,
+                int64_t g_stride) {
+  __shared__ double tile[kScanTile];
+  __shared__ double wsum[32];
+  __shared__ float red_f[64];
+  __shared__ double red_d[32];
+  const int m = row_count(m_max, m_dev);
+  for (int i = blockIdx.x; i < m; i += gridDim.x) {
+  const int64_t srow = src_rows ? src_rows[i] : i;
+  float mw;
+  double lse;
+  row_norm(stats + srow * ntiles, ntiles, mw, lse, red_f, red_d);
+  const double* sw = seg_ws + (int64_t)i * nseg;
+  double off = 0.0, tot = 0.0;
+  for (int k = 0; k < nseg; ++k) {          // same order in every CTA: deterministic
+    if (k < (int)blockIdx.y) off += sw[k];
+    tot += sw[k];
+  }
+  const float* lg = logits + srow * ld;
+  double* g = g_pool + (int64_t)(slots ? slots[i] : i) * g_stride;
+  const int c0 = blockIdx.y * kSegCols;
+  const int cnt = min(kSegCols, vw - c0);
+  for (int j = threadIdx.x; j < kScanTile; j += blockDim.x)
+    tile[j] = j < cnt ? (double)expf(lg[c0 + j] - mw) : 0.0;
+  __syncthreads();
+  double loc[kScanItems];
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    acc += tile[threadIdx.x * kScanItems + k];
+    loc[k] = acc;
+  }
+  double total;
+  const double pre = block_exclusive_scan(acc, wsum, total) + off;
+  const double inv = 1.0 / tot;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) tile[threadIdx.x * kScanItems + k] = (pre + loc[k]) * inv;
+  __syncthreads();
+  for (int j = threadIdx.x; j < cnt; j += blockDim.x) g[c0 + j] = tile[j];
+  __syncthreads();
+  }
+}
+
 __global__ void gather_rows_kernel(int n, const int32_t* __restrict__ idx, const char* __restrict__ src,
                                    char* __restrict__ dst, int64_t row_bytes) {
   const bool vec = (row_bytes % 16 == 0) && ((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 16 == 0);
@@ -356,4 +476,30 @@ extern "C" int fb_gather_rows(int32_t n, const int32_t* idx, const void* src, vo
       n, idx, (const char*)src, (char*)dst, row_bytes);
   count_launch();
   return check_launch("gather_rows");
+}
+
+extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* logits,
+                             int64_t l_stride, const float* row_stats, int32_t n_out,
+                             const int32_t* src_rows, int32_t vw, const int32_t* slots,
+                             double* g_pool, int64_t g_stride, double* eos_out, double* seg_ws,
+                             void* stream) {
+  FB_CHECK_ARG(logits && row_stats && vw > 0 && n_out > vw, "bad stats_to_g arguments");
+  FB_CHECK_ARG(!g_pool || (seg_ws && g_stride >= vw), "g rows need seg_ws and g_stride");
+  if (m_max <= 0) return FB_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int ntiles = (n_out + 127) / 128;
+  const int nseg = (vw + kSegCols - 1) / kSegCols;
+  const float4* st = reinterpret_cast<const float4*>(row_stats);
+  const int gx = std::min(m_max, 64);
+  dim3 g1(gx, g_pool ? nseg : 1);
+  seg_sum_kernel<<<g1, kScanThreads, 0, s>>>(m_max, m_dev, logits, l_stride, st, ntiles, src_rows,
+                                             vw, slots, seg_ws, nseg, eos_out, g_pool != nullptr);
+  count_launch();
+  int rc = check_launch("seg_sum");
+  if (rc || !g_pool) return rc;
+  seg_scan_kernel<<<dim3(gx, nseg), kScanThreads, 0, s>>>(
+      m_max, m_dev, logits, l_stride, st, ntiles, src_rows, vw, slots, seg_ws, nseg, g_pool,
+      g_stride);
+  count_launch();
+  return check_launch("seg_scan");
 }

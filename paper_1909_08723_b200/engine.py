@@ -52,6 +52,10 @@ class _LmPool:
         E = 2 * N
         self.ev_state = torch.zeros((E, L, 2, H), dtype=f32, device=device)
         self.ev_logits = torch.empty((E, lw.v_out), dtype=f32, device=device)
+        self.ntiles = (lw.v_out + 127) // 128
+        self.ev_stats = torch.empty((E, self.ntiles, 4), dtype=f32, device=device)
+        self.seg_ws = torch.empty((N, (d.words + 4095) // 4096), dtype=torch.float64,
+                                  device=device)
         self.ev_row, self.ev_rank, self.ev_slot, self.row_ev = z(N), z(N), z(N), z(N)
         self.ev_count = z(1)
         self.trie = [z(N), z(N)]
@@ -120,8 +124,8 @@ class _NoTimer:
 def decode_fused(features, scorer, fusion, config: DecodeConfig, token_dict
                  ) -> List[DecodeResult]:
     """decode_batch entry: host features -> staged device batch -> engine."""
-    X, T = scorer.encoder.stage([np.asarray(f.data, np.float32) for f in features])
-    X = X.to(scorer.device)
+    X, T = scorer.encoder.stage([np.asarray(f.data, np.float32) for f in features], pin=True)
+    X = X.to(scorer.device, non_blocking=True)
     return FusedDecoder(scorer, fusion, config, token_dict).run(
         X, T, [f.utt_id for f in features])
 
@@ -135,6 +139,7 @@ class FusedDecoder:
         self.scorer, self.fusion, self.config, self.token_dict = scorer, fusion, config, token_dict
         self.spec_counts: Optional[torch.Tensor] = None
         self.steps_run = 0
+        self.kernel_launches = 0
         self.prune_spec = True      # exact pruning of speculative <eos> LM events
         self.use_graphs = True      # one CUDA graph per step parity, replayed
         self.poll_every = 8         # host polls the live-row count every k steps
@@ -143,6 +148,8 @@ class FusedDecoder:
             record_counts: bool = False) -> List[DecodeResult]:
         scorer, fusion, config, token_dict = self.scorer, self.fusion, self.config, self.token_dict
         tm = timer if timer is not None else _NoTimer()
+        lib = _lib.lib()
+        l0 = lib.fb_launch_count()
         dev = scorer.device
         w = scorer.weights
         d = w.d
@@ -219,10 +226,11 @@ class FusedDecoder:
                                   P(lm.ev_count), P(lm.row_ev), stream)
                     lm_step(lw, m=N, m_dev=lm.ev_count, state_src=lm.state, src_idx=lm.ev_slot,
                             state_dst=lm.ev_state, ranks=lm.ev_rank, tok_default=0,
-                            scratch=lm.scratch, logits=lm.ev_logits, timer=tm)
+                            scratch=lm.scratch, logits=lm.ev_logits, timer=tm,
+                            stats=lm.ev_stats)
                 with tm("lm_eos"):
-                    K.logits_to_g(lm.ev_logits, Vw, lw.v_out, m=N, m_dev=lm.ev_count,
-                                  slots=lm.ev_row, eos_out=lm.ext_eos)
+                    K.stats_to_g(lm.ev_logits, lm.ev_stats, Vw, lw.v_out, m=N,
+                                 m_dev=lm.ev_count, slots=lm.ev_row, eos_out=lm.ext_eos)
                     _lib.call("fb_eos_fixup", N, P(lm.ev_count), P(lm.ev_row), P(lm.ext_eos),
                               P(fus_buf), V, fusion.eos_id, stream)
                 if counts is not None:
@@ -246,28 +254,33 @@ class FusedDecoder:
                     lm_step(lw, m=N, m_dev=lm.unk_count, state_src=lm.state,
                             src_idx=lm.unk_slot, state_dst=lm.ev_state[N:], ranks=lm.unk_tok,
                             tok_default=lw.unk_tok, scratch=lm.scratch,
-                            logits=lm.ev_logits[N:], timer=tm)
+                            logits=lm.ev_logits[N:], timer=tm, stats=lm.ev_stats[N:])
                 with tm("g_build"):
                     K.copy_rows(lm.ev_state, lm.state, m=N, m_dev=lm.bnd_count,
                                 src_idx=lm.bnd_src, dst_idx=lm.bnd_slot)
-                    K.logits_to_g(lm.ev_logits, Vw, lw.v_out, m=N, m_dev=lm.bnd_count,
-                                  src_rows=lm.bnd_src, slots=lm.bnd_slot, g_pool=lm.g,
-                                  eos_out=lm.eos)
+                    K.stats_to_g(lm.ev_logits, lm.ev_stats, Vw, lw.v_out, m=N,
+                                 m_dev=lm.bnd_count, src_rows=lm.bnd_src, slots=lm.bnd_slot,
+                                 g_pool=lm.g, eos_out=lm.eos, seg_ws=lm.seg_ws)
                 if counts is not None:
                     counts.append(lm.bnd_count.clone())
                     counts.append(lm.unk_count.clone())
         parity = 0
         steps = 0
+        replayed = 0
         if self.use_graphs and timer is None and counts is None:
             graphs = [torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()]
+            c0 = lib.fb_launch_count()
             for p_ in (0, 1):
                 with torch.cuda.graph(graphs[p_]):
                     step(p_)
+            per_step = (lib.fb_launch_count() - c0) / 2.0
+            l0 += lib.fb_launch_count() - c0          # captures launch nothing
             while True:
                 for _ in range(self.poll_every):
                     graphs[parity].replay()
                     parity ^= 1
                     steps += 1
+                    replayed += 1
                 if int(count[parity].item()) == 0:
                     break
         else:
@@ -278,6 +291,9 @@ class FusedDecoder:
                 if int(count[parity].item()) == 0:
                     break
         self.steps_run = steps
+        # kernels this run put on the GPU (graph replays included)
+        self.kernel_launches = int(lib.fb_launch_count() - l0 +
+                                   (per_step * replayed if replayed else 0))
         if counts is not None:
             self.spec_counts = torch.cat(counts).view(steps, 3).cpu() if counts else None
         return buf.results(list(utt_ids), T)

@@ -67,7 +67,7 @@ def pack(out: torch.Tensor, segs: Sequence[Tuple], *, m: int, m_dev=None, rows=N
 def gemm_tc(ap: torch.Tensor, w: torch.Tensor, *, m: Optional[int] = None, m_dev=None,
             k: Optional[int] = None, bias=None, out=None, rows=None, mode: int = 0,
             hidden: int = 0, parent=None, c_in=None, c_out=None, h_out=None, h_res=None,
-            addend=None, h_split=None) -> None:
+            addend=None, h_split=None, row_stats=None, stats_vw: int = 0) -> None:
     """Tensor-core GEMM: ap = bf16 planes [P, rows, k_pad], w = bf16 [n, k_pad].
     h_split: optional bf16 [3, rows, k] planes receiving h (next A operand)."""
     g = _lib.FbGemm()
@@ -88,6 +88,8 @@ def gemm_tc(ap: torch.Tensor, w: torch.Tensor, *, m: Optional[int] = None, m_dev
     g.addend, g.ld_add = P(addend), _ld(addend)
     if h_split is not None:
         g.h_split, g.hs_plane_rows, g.ld_hs = P(h_split), h_split.shape[1], h_split.stride(1)
+    if row_stats is not None:
+        g.row_stats, g.stats_vw = P(row_stats), stats_vw
     _lib.call("fb_gemm_tc", C.byref(g), ap.shape[0], ap.shape[1], _lib.stream_ptr())
 
 
@@ -108,3 +110,11 @@ def logits_to_g(logits: torch.Tensor, vw: int, v_out: int, *, m: int, m_dev=None
                 src_rows=None, slots=None, g_pool=None, eos_out=None) -> None:
     _lib.call("fb_logits_to_g", m, P(m_dev), P(logits), logits.stride(0), P(src_rows), vw, v_out,
               P(slots), P(g_pool), _ld(g_pool), P(eos_out), _lib.stream_ptr())
+
+
+def stats_to_g(logits: torch.Tensor, stats: torch.Tensor, vw: int, v_out: int, *, m: int,
+               m_dev=None, src_rows=None, slots=None, g_pool=None, eos_out=None,
+               seg_ws=None) -> None:
+    _lib.call("fb_stats_to_g", m, P(m_dev), P(logits), logits.stride(0), P(stats), v_out,
+              P(src_rows), vw, P(slots), P(g_pool), _ld(g_pool), P(eos_out), P(seg_ws),
+              _lib.stream_ptr())

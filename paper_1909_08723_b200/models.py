@@ -363,7 +363,7 @@ class LmWeights:
 
 def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks,
             tok_default: int, scratch: torch.Tensor, logits: Optional[torch.Tensor],
-            timer=None) -> None:
+            timer=None, stats: Optional[torch.Tensor] = None) -> None:
     """Batched LSTM-LM step.  Row i: input token ranks[i] (or tok_default),
     recurrent state from state_src[src_idx[i]] (None -> zero state), new state
     into state_dst[i]; state tensors are [rows, L, 2, H] (h then c per layer).
@@ -389,12 +389,13 @@ def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks
     if logits is not None:
         K.pack(scratch, [(state_dst[:, L - 1, 0], H, 0, state_dst.stride(0))], m=m, m_dev=m_dev,
                k_pad=w.k_out, split=True)
+        kw = dict(m=m, m_dev=m_dev, k=w.k_out, bias=w.b_out, out=logits, row_stats=stats,
+                  stats_vw=w.d.words)
         if timer is not None:
             with timer("lm_out_gemm"):
-                K.gemm_tc(scratch, w.emb_w, m=m, m_dev=m_dev, k=w.k_out, bias=w.b_out,
-                          out=logits)
+                K.gemm_tc(scratch, w.emb_w, **kw)
         else:
-            K.gemm_tc(scratch, w.emb_w, m=m, m_dev=m_dev, k=w.k_out, bias=w.b_out, out=logits)
+            K.gemm_tc(scratch, w.emb_w, **kw)
 
 
 class _DevHist:

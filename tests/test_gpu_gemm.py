@@ -88,3 +88,35 @@ def test_tc_device_row_count():
     ref = a.double() @ w.double().T
     assert (out[:130].double() - ref[:130]).abs().max().item() < 1e-4
     assert (out[130:] == 7.0).all()
+
+
+def test_row_stats_feed_g_rows_and_eos():
+    """LM-output GEMM tile statistics -> fb_stats_to_g == single-pass fb_logits_to_g."""
+    from paper_1909_08723_b200 import kernels as K
+    dev = torch.device("cuda")
+    torch.manual_seed(11)
+    m, vw, k = 37, 9000, 128
+    n = vw + 3
+    a = torch.randn(m, k, device=dev)
+    w = _bf16_exact(torch.randn(n, k, device=dev) * 0.3)
+    b = torch.randn(n, device=dev) * 0.5
+    logits = torch.empty(m, n, device=dev)
+    stats = torch.empty(m, (n + 127) // 128, 4, device=dev)
+    K.gemm_tc(_packed(a, k), w.to(torch.bfloat16), m=m, k=k, bias=b, out=logits,
+              row_stats=stats, stats_vw=vw)
+    ref = a.double() @ w.double().T + b.double()
+    assert (logits.double() - ref).abs().max().item() < 1e-4
+    g_ref = torch.empty(m, vw, dtype=torch.float64, device=dev)
+    e_ref = torch.empty(m, dtype=torch.float64, device=dev)
+    K.logits_to_g(logits, vw, n, m=m, g_pool=g_ref, eos_out=e_ref)
+    g = torch.empty_like(g_ref)
+    e = torch.empty_like(e_ref)
+    seg = torch.empty(m, (vw + 4095) // 4096, dtype=torch.float64, device=dev)
+    cnt = torch.tensor([m], dtype=torch.int32, device=dev)
+    K.stats_to_g(logits, stats, vw, n, m=m, m_dev=cnt, g_pool=g, eos_out=e, seg_ws=seg)
+    assert (g - g_ref).abs().max().item() < 1e-13
+    assert (e - e_ref).abs().max().item() < 1e-5
+    # single-word masses from g differences agree to fp64 resolution of g (~1 ulp of 1.0)
+    p = torch.diff(g, dim=1, prepend=torch.zeros(m, 1, dtype=torch.float64, device=dev))
+    p_ref = torch.diff(g_ref, dim=1, prepend=torch.zeros(m, 1, dtype=torch.float64, device=dev))
+    assert (p - p_ref).abs().max().item() < 1e-15
