@@ -198,9 +198,9 @@ typedef struct {
   /* mode 1, optional: h also written as 3 bf16 planes (hi/mid/lo) at
    * [p*hs_plane_rows + slot][unit] -- the A operand of a following GEMM */
   void* h_split; int64_t hs_plane_rows; int64_t ld_hs;
-  /* mode 0, optional: per (output row, 128-column tile) softmax statistics
-   * {max, sum exp(x-max)} over columns < stats_vw and over all columns,
-   * float4 at row_stats[(orow * ceil(n/128) + tile)] (forces 128-wide tiles) */
+  /* mode 0, optional: per (output row, 64-column block) softmax statistics
+   * {max, sum exp(x-max)} over all columns and over columns < stats_vw,
+   * float4 at row_stats[orow * ceil(n/64) + block] (forces 128-wide tiles) */
   float* row_stats; int32_t stats_vw; int32_t pad1;
 } fb_gemm_t;
 

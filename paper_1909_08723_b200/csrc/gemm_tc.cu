@@ -7,11 +7,12 @@
 // fp32 in TMEM -- an fp32-accurate product on the 5th-gen tensor cores
 // (SURVEY.md §7 "GEMM precision").  Algorithmic FLOPs count the product once.
 //
-// Structure (persistent, one CTA per SM, 6 warps):
+// Structure (persistent, one CTA per SM, 10 warps):
 //   warp 0 lane 0 : TMA producer, 3-stage smem ring (128B swizzle, K block 64)
 //   warp 1 lane 0 : MMA issuer (tcgen05.mma.cta_group::1.kind::f16, M=128)
 //   warp 1        : TMEM allocator (2 x BN fp32 columns, double-buffered)
-//   warps 2..5    : epilogue, tcgen05.ld 32x32b (warp w owns TMEM lanes 32(w%4)..)
+//   warps 2..9    : epilogue, tcgen05.ld 32x32b (warp w owns TMEM lanes 32(w%4)..,
+//                   column half (w-2)/4 of the tile)
 #include "common.cuh"
 
 #include <cuda.h>
@@ -23,7 +24,7 @@ namespace fb {
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;            // 64 bf16 = 128 B = one swizzle atom
 constexpr int TC_STAGES = 3;
-constexpr int TC_EPI_THREADS = 128;
+constexpr int TC_EPI_THREADS = 256;     // 8 epilogue warps: 2 per TMEM lane quarter
 constexpr int TC_THREADS = 64 + TC_EPI_THREADS;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -101,11 +102,12 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 
 __device__ __forceinline__ float sigm_tc(float x) { return 1.0f / (1.0f + expf(-x)); }
 
-__device__ __forceinline__ float fsig(float x) { return __frcp_rn(1.0f + __expf(-x)); }
+// MUFU ex2 + rcp; __fdividef returns 0 for denominators > 2^126, which is the
+// correct limit here (sigmoid -> 0, tanh -> -1)
+__device__ __forceinline__ float fsig(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 
 __device__ __forceinline__ float ftanh(float x) {
-  x = fminf(fmaxf(x, -15.0f), 15.0f);
-  return 1.0f - 2.0f * __frcp_rn(1.0f + __expf(2.0f * x));
+  return 1.0f - __fdividef(2.0f, 1.0f + __expf(2.0f * x));
 }
 
 __device__ __forceinline__ void store_split(const fb_gemm_t& g, int64_t row, int col, float x) {
@@ -124,11 +126,14 @@ __device__ __forceinline__ void store_split(const fb_gemm_t& g, int64_t row, int
 // across the warp (plain mode: lane = column; LSTM mode: lane = (row, unit)).
 template <int BN>
 __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row0, int n0,
-                                              uint32_t taddr, float* st /* [32][33] */) {
+                                              uint32_t taddr, float* st /* [32][33] */,
+                                              int half) {
   const int lane = threadIdx.x & 31;
-  // {max_all, sum_all, max_words, sum_words} of this lane's row over the tile
+  // {max_all, sum_all, max_words, sum_words} of this lane's row over the
+  // warp's half of the tile (BN/2 columns)
   float4 st_stats = make_float4(-INFINITY, 0.f, -INFINITY, 0.f);
-  for (int cb = 0; cb < BN / 32; ++cb) {
+  constexpr int CH = BN / 64;                 // 32-column chunks per half
+  for (int cb = half * CH; cb < (half + 1) * CH; ++cb) {
     float v[32];
     __syncwarp();
     tmem_ld32(taddr + cb * 32, v);
@@ -169,31 +174,46 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
     if (g.mode == 1) {
       const int u = lane & 7, rs = lane >> 3;
       const int unit = (nb >> 2) + u;
-      if (unit * 4 < g.n) {
-        float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (g.bias) b4 = *reinterpret_cast<const float4*>(g.bias + 4 * unit);
-#pragma unroll 2
-        for (int it = 0; it < 8; ++it) {
-          const int r = it * 4 + rs;
-          const int row = row0 + r;
-          if (row >= M) break;
-          float gi = st[r * 33 + 4 * u] + b4.x, gf = st[r * 33 + 4 * u + 1] + b4.y;
-          float gg = st[r * 33 + 4 * u + 2] + b4.z, go = st[r * 33 + 4 * u + 3] + b4.w;
-          if (g.addend) {
-            const float4 a4 =
-                *reinterpret_cast<const float4*>(g.addend + (int64_t)row * g.ld_add + 4 * unit);
-            gi += a4.x; gf += a4.y; gg += a4.z; go += a4.w;
-          }
-          const int slot = g.rows ? g.rows[row] : row;
-          const int pr = g.parent ? g.parent[slot] : slot;
-          const float cp = g.c_in ? g.c_in[(int64_t)pr * g.ld_cin + unit] : 0.0f;
-          const float c = fsig(gf) * cp + fsig(gi) * ftanh(gg);
-          float h = fsig(go) * ftanh(c);
-          if (g.h_res) h += g.h_res[(int64_t)slot * g.ld_res + unit];
-          g.c_out[(int64_t)slot * g.ld_cout + unit] = c;
-          g.h_out[(int64_t)slot * g.ld_h + unit] = h;
-          if (g.h_split) store_split(g, slot, unit, h);
-        }
+      const bool uok = unit * 4 < g.n;
+      float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (g.bias && uok) b4 = *reinterpret_cast<const float4*>(g.bias + 4 * unit);
+      // gather everything the 8 rows of this lane need before any math, so the
+      // dependent loads (rows -> parent -> c_in) are in flight together
+      int slot[8];
+      bool ok[8];
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int row = row0 + it * 4 + rs;
+        ok[it] = uok && row < M;
+        slot[it] = ok[it] ? (g.rows ? __ldg(g.rows + row) : row) : 0;
+      }
+      int pr[8];
+#pragma unroll
+      for (int it = 0; it < 8; ++it) pr[it] = (ok[it] && g.parent) ? __ldg(g.parent + slot[it]) : slot[it];
+      float cp[8], hr[8];
+      float4 ad[8];
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        cp[it] = (ok[it] && g.c_in) ? __ldg(g.c_in + (int64_t)pr[it] * g.ld_cin + unit) : 0.f;
+        hr[it] = (ok[it] && g.h_res) ? __ldg(g.h_res + (int64_t)slot[it] * g.ld_res + unit) : 0.f;
+        ad[it] = (ok[it] && g.addend)
+                     ? __ldg(reinterpret_cast<const float4*>(
+                           g.addend + (int64_t)(row0 + it * 4 + rs) * g.ld_add + 4 * unit))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        if (!ok[it]) continue;
+        const int r = it * 4 + rs;
+        const float gi = st[r * 33 + 4 * u] + b4.x + ad[it].x;
+        const float gf = st[r * 33 + 4 * u + 1] + b4.y + ad[it].y;
+        const float gg = st[r * 33 + 4 * u + 2] + b4.z + ad[it].z;
+        const float go = st[r * 33 + 4 * u + 3] + b4.w + ad[it].w;
+        const float c = fsig(gf) * cp[it] + fsig(gi) * ftanh(gg);
+        const float h = fsig(go) * ftanh(c) + hr[it];
+        g.c_out[(int64_t)slot[it] * g.ld_cout + unit] = c;
+        g.h_out[(int64_t)slot[it] * g.ld_h + unit] = h;
+        if (g.h_split) store_split(g, slot[it], unit, h);
       }
     } else {
       const int col = nb + lane;
@@ -212,8 +232,8 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
   if (g.row_stats && row0 + lane < M) {
     const int row = row0 + lane;
     const int orow = g.rows ? g.rows[row] : row;
-    const int ntiles = (g.n + 127) / 128;
-    reinterpret_cast<float4*>(g.row_stats)[(int64_t)orow * ntiles + n0 / 128] = st_stats;
+    const int ntiles = (g.n + 63) / 64;      // statistics per 64-column half tile
+    reinterpret_cast<float4*>(g.row_stats)[(int64_t)orow * ntiles + n0 / 64 + half] = st_stats;
   }
   __syncwarp();
 }
@@ -242,7 +262,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   __shared__ __align__(8) uint64_t bar_full[TC_STAGES], bar_empty[TC_STAGES];
   __shared__ __align__(8) uint64_t bar_tfull[2], bar_tempty[2];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ float epi_stage[4][32 * 33];
+  __shared__ float epi_stage[8][32 * 33];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -317,8 +337,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
     }
   } else {
-    // ---- epilogue warps 2..5 (TMEM lane quarter = warp % 4) ----
+    // ---- epilogue warps 2..9: lane quarter = warp % 4, column half = (warp-2)/4 ----
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int acc = it & 1;
@@ -326,7 +347,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_wait(smem_u32(&bar_tfull[acc]), (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       epilogue_tile<BN>(g, M, m0 + quarter * 32, n0,
-                        tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN, epi_stage[warp - 2]);
+                        tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN, epi_stage[warp - 2],
+                        half);
       asm volatile("tcgen05.fence::before_thread_sync;");
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[acc]))
                    : "memory");

@@ -487,7 +487,7 @@ extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* l
   FB_CHECK_ARG(!g_pool || (seg_ws && g_stride >= vw), "g rows need seg_ws and g_stride");
   if (m_max <= 0) return FB_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  const int ntiles = (n_out + 127) / 128;
+  const int ntiles = (n_out + 63) / 64;       // GEMM epilogue statistics granule
   const int nseg = (vw + kSegCols - 1) / kSegCols;
   const float4* st = reinterpret_cast<const float4*>(row_stats);
   const int gx = std::min(m_max, 64);

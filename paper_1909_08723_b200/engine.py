@@ -52,7 +52,7 @@ class _LmPool:
         E = 2 * N
         self.ev_state = torch.zeros((E, L, 2, H), dtype=f32, device=device)
         self.ev_logits = torch.empty((E, lw.v_out), dtype=f32, device=device)
-        self.ntiles = (lw.v_out + 127) // 128
+        self.ntiles = (lw.v_out + 63) // 64
         self.ev_stats = torch.empty((E, self.ntiles, 4), dtype=f32, device=device)
         self.seg_ws = torch.empty((N, (d.words + 4095) // 4096), dtype=torch.float64,
                                   device=device)
@@ -124,10 +124,14 @@ class _NoTimer:
 def decode_fused(features, scorer, fusion, config: DecodeConfig, token_dict
                  ) -> List[DecodeResult]:
     """decode_batch entry: host features -> staged device batch -> engine."""
-    X, T = scorer.encoder.stage([np.asarray(f.data, np.float32) for f in features], pin=True)
-    X = X.to(scorer.device, non_blocking=True)
-    return FusedDecoder(scorer, fusion, config, token_dict).run(
+    Xh, T = scorer.encoder.stage([np.asarray(f.data, np.float32) for f in features], pin=True)
+    X = Xh.to(scorer.device, non_blocking=True)
+    done = torch.cuda.Event()
+    done.record()
+    out = FusedDecoder(scorer, fusion, config, token_dict).run(
         X, T, [f.utt_id for f in features])
+    done.synchronize()          # the pinned staging buffer may be reused afterwards
+    return out
 
 
 class FusedDecoder:

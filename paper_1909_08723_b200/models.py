@@ -129,6 +129,7 @@ class Encoder:
         self.w = w
         self.device = device
         self.streams = None
+        self._pinned = None
 
     def stage(self, feats: Sequence[np.ndarray], pin: bool = False):
         """Host-side frame stacking into one [B*TM, Din_pad] array (+ lengths)."""
@@ -139,7 +140,17 @@ class Encoder:
             raise ValueError("utterance shorter than the subsampling factor")
         TM = max(T)
         Din = d.feat_dim * d.subsample
-        x = torch.zeros((B, TM, _pad(Din)), dtype=torch.float32, pin_memory=pin)
+        shape = (B, TM, _pad(Din))
+        if pin:
+            # reuse one pinned staging buffer (cudaHostAlloc per call costs more
+            # than the copy); the caller must consume it before the next stage()
+            n = B * TM * _pad(Din)
+            if self._pinned is None or self._pinned.numel() < n:
+                self._pinned = torch.empty(n, dtype=torch.float32, pin_memory=True)
+            x = self._pinned[:n].view(shape)
+            x.zero_()
+        else:
+            x = torch.zeros(shape, dtype=torch.float32)
         xn = x.numpy()
         for u, f in enumerate(feats):
             xn[u, :T[u], :Din] = np.asarray(f, np.float32)[:T[u] * d.subsample].reshape(T[u], Din)

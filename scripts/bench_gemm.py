@@ -1,0 +1,49 @@
+"""Standalone timing of the tcgen05 GEMM at the decoder's shapes (CUDA events,
+warm L2 excluded by rotating 4 operand sets).  Algorithmic FLOPs = 2*M*N*K
+(the bf16x3 split is not counted)."""
+import sys, os, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_1909_08723_b200 import kernels as K
+
+SHAPES = {  # name: (M, N, K, mode)
+    "am_lstm": (5120, 1280, 1024, 1),
+    "lm_lstm": (256, 4800, 2432, 1),
+    "lm_out": (256, 65003, 1216, 0),
+    "enc_proj": (115200, 1280, 320, 0),
+    "enc_rec": (512, 1280, 320, 1),
+}
+
+def run(name, M, N, Kd, mode, reps=20):
+    dev = torch.device("cuda")
+    sets = []
+    for _ in range(4):
+        a = torch.randn(3, M, Kd, device=dev).to(torch.bfloat16)
+        w = (torch.randn(N, Kd, device=dev) * 0.05).to(torch.bfloat16)
+        b = torch.randn(N, device=dev)
+        if mode == 1:
+            H = N // 4
+            kw = dict(mode=1, hidden=H, c_in=torch.randn(M, H, device=dev),
+                      c_out=torch.empty(M, H, device=dev), h_out=torch.empty(M, H, device=dev))
+        else:
+            kw = dict(out=torch.empty(M, N, device=dev))
+        sets.append((a, w, b, kw))
+    for a, w, b, kw in sets:
+        K.gemm_tc(a, w, m=M, k=Kd, bias=b, **kw)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(reps):
+        a, w, b, kw = sets[i % 4]
+        K.gemm_tc(a, w, m=M, k=Kd, bias=b, **kw)
+    e1.record()
+    torch.cuda.synchronize()
+    us = 1000 * e0.elapsed_time(e1) / reps
+    tf = 2.0 * M * N * Kd / (us * 1e-6) / 1e12
+    return {"shape": name, "M": M, "N": N, "K": Kd, "us": round(us, 2),
+            "alg_tflops": round(tf, 1), "tensor_tflops_3x": round(3 * tf, 1)}
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(SHAPES)
+    for n in names:
+        print(json.dumps(run(n, *SHAPES[n])), flush=True)

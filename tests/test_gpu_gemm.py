@@ -101,7 +101,7 @@ def test_row_stats_feed_g_rows_and_eos():
     w = _bf16_exact(torch.randn(n, k, device=dev) * 0.3)
     b = torch.randn(n, device=dev) * 0.5
     logits = torch.empty(m, n, device=dev)
-    stats = torch.empty(m, (n + 127) // 128, 4, device=dev)
+    stats = torch.empty(m, (n + 63) // 64, 4, device=dev)
     K.gemm_tc(_packed(a, k), w.to(torch.bfloat16), m=m, k=k, bias=b, out=logits,
               row_stats=stats, stats_vw=vw)
     ref = a.double() @ w.double().T + b.double()
