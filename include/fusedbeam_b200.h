@@ -247,7 +247,8 @@ int fb_log_softmax_rows(int32_t m_max, const int32_t* m_dev, const int32_t* rows
                         void* stream);
 
 /* Bahdanau attention step for every active utterance:
- * e[r,t] = v . tanh(keys[u,t] + q[r]); a = softmax_t(e) over t < t_enc[u];
+ * e[r,t] = v . tanh(K[u,t] + q[r]); a = softmax_t(e) over t < t_enc[u];
+ * `keys` holds E_K = exp(2 K) (fb_exp2x), so tanh(k+q) = 1 - 2/(1 + E_k E_q);
  * ctx[r] = sum_t a[r,t] enc[u,t]; acc_out[r] = acc_in[parent[r]] + a[r]
  * (fp64) and its coverage (cfg->cov_mode).  Rows r = u*beam + i, i < n_live[u].
  * energy_ws: scratch [num_utts*beam, t_max] fp32. */
@@ -257,6 +258,9 @@ int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts, const int32_
                       const float* q, int64_t ldq, const int32_t* parent, const double* acc_in,
                       double* acc_out, double* cov_out, float* ctx_out, int64_t ld_ctx,
                       float* attn_out, int64_t ld_attn, float* energy_ws, void* stream);
+
+/* y[i] = exp(2 x[i]) (attention keys -> E_K, once per batch). */
+int fb_exp2x(int64_t n, const float* x, float* y, void* stream);
 
 /* ---- word-LM bookkeeping for the fused engine ---------------------------- */
 /* Speculative <eos> events (fusion.py:181-183): for every listed row whose

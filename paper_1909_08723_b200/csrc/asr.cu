@@ -129,10 +129,21 @@ constexpr int kEnFrames = 4;          // frames per warp
 constexpr int kMaxBeam = 64;
 constexpr int kCtxCols = 128;
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// keys arrive as E_k = exp(2 K) (fb_exp2x after the key projection) and the
+// query as E_q = exp(2 q) (here), so tanh(k + q) = 1 - 2 / (1 + E_k E_q) and
+// e_t = sum_a v_a - 2 sum_a v_a / (1 + E_k E_q).  The constant sum_a v_a
+// cancels in the softmax, so the kernel stores e'_t = -2 sum_a v_a / (1 + E_k E_q):
+// one FFMA + one MUFU.RCP + one FFMA per (row, frame, a).
 __global__ void __launch_bounds__(kEnWarps * 32)
 att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
                   const int32_t* __restrict__ n_live, const int32_t* __restrict__ t_enc,
-                  const float* __restrict__ keys, int A, const float* __restrict__ v,
+                  const float* __restrict__ ekeys, int A, const float* __restrict__ v,
                   const float* __restrict__ q, int64_t ldq, float* __restrict__ energy) {
   const int u = blockIdx.x;
   if (!active[u]) return;
@@ -142,17 +153,17 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
   extern __shared__ float sm[];
   const int K = cfg.beam, TM = cfg.t_max;
   const int n = n_live[u];
-  float* qs = sm;                  // [n][A]
+  float* qs = sm;                  // [n][A]  E_q = exp(2 q)
   float* vs = qs + n * A;          // [A]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int slot0 = u * K;
   for (int j = tid; j < n * A; j += blockDim.x) {
     const int i = j / A, a = j % A;
-    qs[j] = q[(int64_t)(slot0 + i) * ldq + a];
+    qs[j] = expf(2.0f * q[(int64_t)(slot0 + i) * ldq + a]);
   }
   for (int a = tid; a < A; a += blockDim.x) vs[a] = v[a];
   __syncthreads();
-  const float* ku = keys + (int64_t)u * TM * A;
+  const float* ku = ekeys + (int64_t)u * TM * A;
   for (int f = 0; f < kEnFrames; ++f) {
     const int t = t_base + warp * kEnFrames + f;
     if (t >= T) break;
@@ -163,11 +174,11 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
 #pragma unroll
       for (int r = 0; r < 16; ++r) e[r] = 0.f;
       for (int a = lane; a < A; a += 32) {
-        const float k = __ldg(kt + a);
+        const float ek = __ldg(kt + a);
         const float va = vs[a];
 #pragma unroll
         for (int r = 0; r < 16; ++r)
-          if (r < nb) e[r] = fmaf(va, tanh_fast(k + qs[(i0 + r) * A + a]), e[r]);
+          if (r < nb) e[r] = fmaf(va, rcp_approx(fmaf(ek, qs[(i0 + r) * A + a], 1.0f)), e[r]);
       }
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
@@ -179,12 +190,19 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
         float x = 0.f;
 #pragma unroll
         for (int r = 0; r < 16; ++r) x = lane == r ? e[r] : x;
-        energy[(int64_t)(slot0 + i0 + lane) * TM + t] = x;
+        energy[(int64_t)(slot0 + i0 + lane) * TM + t] = -2.0f * x;
       }
     }
   }
 }
 
+__global__ void exp2x_kernel(int64_t n, const float* __restrict__ x, float* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = expf(2.0f * x[i]);
+}
+
+template <int RB>
 __global__ void __launch_bounds__(256)
 att_context_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
                    const int32_t* __restrict__ n_live, const int32_t* __restrict__ t_enc,
@@ -201,7 +219,8 @@ att_context_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
   const int K = cfg.beam, TM = cfg.t_max;
   const int n = n_live[u];
   const int T = t_enc[u];
-  float* al = sm;                  // [n][T] attention weights
+  float* al = sm;                  // [n][T] attention weights (row-major)
+  float* at = al + ((n * T + 3) & ~3);  // [T][RB] transposed copy (16 B aligned)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int slot0 = u * K;
   // softmax over frames, one warp per row (every column chunk recomputes it)
@@ -226,35 +245,47 @@ att_context_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
     for (int t = lane; t < T; t += 32) a[t] *= inv;
   }
   __syncthreads();
-  // context columns [c0, c0 + kCtxCols): thread = (column, row half)
+  for (int j = tid; j < T * RB; j += blockDim.x) {
+    const int t = j / RB, r = j % RB;
+    at[j] = r < n ? al[r * T + t] : 0.f;
+  }
+  __syncthreads();
+  // context columns [c0, c0 + kCtxCols): thread = (column, row group of RB)
   const float* eu = enc + (int64_t)u * TM * C;
-  constexpr int RB = 16, TU = 8;
   const int col = c0 + (tid % kCtxCols);
-  const int half = tid / kCtxCols;           // 0..1 -> interleaved row groups
-  if (col < C) {
-    for (int i0 = half * RB; i0 < n; i0 += 2 * RB) {
-      const int nb = min(RB, n - i0);
-      float acc[RB];
+  const int grp = tid / kCtxCols;              // 0..1
+  if (col < C && grp * RB < n) {
+    float acc[RB];
 #pragma unroll
-      for (int r = 0; r < RB; ++r) acc[r] = 0.f;
-      int t = 0;
-      for (; t + TU <= T; t += TU) {
-        float x[TU];
+    for (int r = 0; r < RB; ++r) acc[r] = 0.f;
+    constexpr int TU = 8;
+    int t = 0;
+    for (; t + TU <= T; t += TU) {
+      float x[TU];
 #pragma unroll
-        for (int j = 0; j < TU; ++j) x[j] = __ldg(eu + (int64_t)(t + j) * C + col);
+      for (int j = 0; j < TU; ++j) x[j] = __ldg(eu + (int64_t)(t + j) * C + col);
 #pragma unroll
-        for (int j = 0; j < TU; ++j)
+      for (int j = 0; j < TU; ++j) {
+        const float4* a4 = reinterpret_cast<const float4*>(at + (t + j) * RB);
 #pragma unroll
-          for (int r = 0; r < RB; ++r)
-            if (r < nb) acc[r] = fmaf(al[(i0 + r) * T + t + j], x[j], acc[r]);
+        for (int q4 = 0; q4 < RB / 4; ++q4) {
+          const float4 w = a4[q4];
+          acc[4 * q4] = fmaf(w.x, x[j], acc[4 * q4]);
+          acc[4 * q4 + 1] = fmaf(w.y, x[j], acc[4 * q4 + 1]);
+          acc[4 * q4 + 2] = fmaf(w.z, x[j], acc[4 * q4 + 2]);
+          acc[4 * q4 + 3] = fmaf(w.w, x[j], acc[4 * q4 + 3]);
+        }
       }
-      for (; t < T; ++t) {
-        const float x = __ldg(eu + (int64_t)t * C + col);
+    }
+    for (; t < T; ++t) {
+      const float x = __ldg(eu + (int64_t)t * C + col);
 #pragma unroll
-        for (int r = 0; r < RB; ++r)
-          if (r < nb) acc[r] = fmaf(al[(i0 + r) * T + t], x, acc[r]);
-      }
-      for (int r = 0; r < nb; ++r) ctx_out[(int64_t)(slot0 + i0 + r) * ld_ctx + col] = acc[r];
+      for (int r = 0; r < RB; ++r) acc[r] = fmaf(at[t * RB + r], x, acc[r]);
+    }
+    if (grp == 0) {
+#pragma unroll
+      for (int r = 0; r < RB; ++r)
+        if (r < n) ctx_out[(int64_t)(slot0 + r) * ld_ctx + col] = acc[r];
     }
   }
   if (blockIdx.y != 0) return;
@@ -481,16 +512,24 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
                "null attention args");
   FB_CHECK_ARG(cfg->cov_mode == 0 || cov_out, "coverage output required");
   FB_CHECK_ARG(cfg->beam <= kMaxBeam, "beam too large for the attention kernels");
+  FB_CHECK_ARG(cfg->beam <= 16, "attention context kernel supports beam <= 16");
   if (num_utts <= 0) return FB_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const size_t sm_e = sizeof(float) * ((size_t)cfg->beam * att_dim + att_dim);
-  const size_t sm_c = sizeof(float) * (size_t)cfg->beam * cfg->t_max;
+  const int RB = cfg->beam <= 4 ? 4 : cfg->beam <= 8 ? 8 : cfg->beam <= 12 ? 12 : 16;
+  if (cfg->beam > 16) return fail(FB_ERR_CONFIG, "attention context kernel supports beam <= 16");
+  const size_t sm_c = sizeof(float) * ((size_t)cfg->beam * cfg->t_max + 4 + (size_t)RB * cfg->t_max);
   if (sm_e > 200 * 1024 || sm_c > 200 * 1024)
     return fail(FB_ERR_CONFIG, "attention working set exceeds shared memory");
-  if (sm_e > 48 * 1024)
-    cudaFuncSetAttribute(att_energy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_e);
-  if (sm_c > 48 * 1024)
-    cudaFuncSetAttribute(att_context_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(att_energy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(att_context_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(att_context_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(att_context_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(att_context_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
   dim3 ge(num_utts, (cfg->t_max + kEnWarps * kEnFrames - 1) / (kEnWarps * kEnFrames));
   att_energy_kernel<<<ge, kEnWarps * 32, sm_e, s>>>(*cfg, active, n_live, t_enc, keys, att_dim,
                                                      v, q, ldq, energy_ws);
@@ -498,9 +537,12 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
   int rc = check_launch("att_energy");
   if (rc) return rc;
   dim3 gc(num_utts, (ctx_dim + kCtxCols - 1) / kCtxCols);
-  att_context_kernel<<<gc, 256, sm_c, s>>>(*cfg, active, n_live, t_enc, enc, ctx_dim, energy_ws,
-                                           parent, acc_in, acc_out, cov_out, ctx_out, ld_ctx,
-                                           attn_out, ld_attn);
+#define FB_CTX(R)                                                                             \
+  att_context_kernel<R><<<gc, 256, sm_c, s>>>(*cfg, active, n_live, t_enc, enc, ctx_dim,       \
+                                              energy_ws, parent, acc_in, acc_out, cov_out,    \
+                                              ctx_out, ld_ctx, attn_out, ld_attn)
+  if (RB == 4) FB_CTX(4); else if (RB == 8) FB_CTX(8); else if (RB == 12) FB_CTX(12); else FB_CTX(16);
+#undef FB_CTX
   count_launch();
   return check_launch("att_context");
 }
@@ -547,4 +589,12 @@ extern "C" int fb_copy_rows(int32_t n_max, const int32_t* n_dev, const int32_t* 
       n_max, n_dev, src_idx, dst_idx, (const char*)src, (char*)dst, row_bytes);
   count_launch();
   return check_launch("copy_rows");
+}
+
+extern "C" int fb_exp2x(int64_t n, const float* x, float* y, void* stream) {
+  FB_CHECK_ARG(x && y && n >= 0, "bad exp2x arguments");
+  if (n == 0) return FB_OK;
+  exp2x_kernel<<<std::min<int64_t>((n + 255) / 256, kNumSMs * 16), 256, 0, (cudaStream_t)stream>>>(n, x, y);
+  count_launch();
+  return check_launch("exp2x");
 }

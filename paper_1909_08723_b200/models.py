@@ -218,6 +218,8 @@ class Encoder:
         kk = self.w.w_k.shape[1]
         K.pack(big, [(X, kk, 0)], m=B * TM, k_pad=kk, split=True)
         K.gemm_tc(big[:, :, :kk], self.w.w_k, m=B * TM, k=kk, bias=self.w.b_k, out=keys)
+        # the attention kernels consume E_K = exp(2 K) (tanh via one reciprocal)
+        _lib.call("fb_exp2x", keys.numel(), _lib.ptr(keys), _lib.ptr(keys), _lib.stream_ptr())
         return enc.view(B, TM, C_), keys.view(B, TM, d.att), T
 
 
