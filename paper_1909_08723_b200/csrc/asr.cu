@@ -12,51 +12,86 @@
 namespace fb {
 
 // ---------------------------------------------------------------- packing --
-__global__ void pack_rows_kernel(fb_pack_t p, int m_max, const int32_t* __restrict__ m_dev,
-                                 const int32_t* __restrict__ rows,
-                                 const int32_t* __restrict__ parent,
-                                 const int32_t* __restrict__ tokens,
-                                 const int32_t* __restrict__ ranks, float* __restrict__ out,
-                                 int64_t ld_out) {
+__device__ __forceinline__ void split3(float x, __nv_bfloat16& hi, __nv_bfloat16& mid,
+                                       __nv_bfloat16& lo) {
+  // x = hi + mid + lo exactly (8+8+8 mantissa bits of the fp32 value)
+  hi = __float2bfloat16_rn(x);
+  const float r1 = x - __bfloat162float(hi);
+  mid = __float2bfloat16_rn(r1);
+  lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+}
+
+// One warp per output row, 4 consecutive columns per lane (float4 in, 8-byte
+// bf16x4 per plane out) when the segment allows it.
+__global__ void __launch_bounds__(256)
+pack_rows_kernel(fb_pack_t p, int m_max, const int32_t* __restrict__ m_dev,
+                 const int32_t* __restrict__ rows, const int32_t* __restrict__ parent,
+                 const int32_t* __restrict__ tokens, const int32_t* __restrict__ ranks,
+                 float* __restrict__ out, int64_t ld_out) {
   const int m = row_count(m_max, m_dev);
   const bool split = p.out_mode == 1;
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
   __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(out);
-  for (int i = blockIdx.x; i < m; i += gridDim.x) {
-    float* o = out + (int64_t)i * ld_out;
-    __nv_bfloat16* o0 = ob + (int64_t)i * ld_out;
-    __nv_bfloat16* o1 = o0 + p.plane_rows * ld_out;
-    __nv_bfloat16* o2 = o1 + p.plane_rows * ld_out;
-    auto put = [&](int j, float x) {
-      if (!split) {
-        o[j] = x;
-      } else {
-        // x = hi + mid + lo exactly (8+8+8 mantissa bits of the fp32 value)
-        const __nv_bfloat16 hi = __float2bfloat16_rn(x);
-        const float r1 = x - __bfloat162float(hi);
-        const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-        const float r2 = r1 - __bfloat162float(mid);
-        o0[j] = hi;
-        o1[j] = mid;
-        o2[j] = __float2bfloat16_rn(r2);
-      }
-    };
+  const int64_t plane = p.plane_rows * ld_out;
+  for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < m; i += gridDim.x * wpb) {
     int col = 0;
-    for (int s = 0; s < p.nseg; ++s) {
-      const fb_seg_t& sg = p.seg[s];
-      int64_t r;
-      switch (sg.mode) {
-        case 0: r = i; break;
-        case 1: r = rows ? rows[i] : i; break;
-        case 2: { const int sl = rows ? rows[i] : i; r = parent ? parent[sl] : sl; break; }
-        case 3: { const int sl = rows ? rows[i] : i; const int t = tokens[sl];
-                  r = t < 0 ? p.tok_default : t; break; }
-        default: { const int t = ranks ? ranks[i] : -1; r = t < 0 ? p.tok_default : t; break; }
+    for (int s = 0; s <= p.nseg; ++s) {
+      const float* src = nullptr;
+      int width;
+      if (s < p.nseg) {
+        const fb_seg_t& sg = p.seg[s];
+        int64_t r;
+        switch (sg.mode) {
+          case 0: r = i; break;
+          case 1: r = rows ? rows[i] : i; break;
+          case 2: { const int sl = rows ? rows[i] : i; r = parent ? parent[sl] : sl; break; }
+          case 3: { const int sl = rows ? rows[i] : i; const int t = tokens[sl];
+                    r = t < 0 ? p.tok_default : t; break; }
+          default: { const int t = ranks ? ranks[i] : -1; r = t < 0 ? p.tok_default : t; break; }
+        }
+        src = sg.src ? sg.src + r * sg.ld : nullptr;
+        width = sg.width;
+      } else {
+        width = p.k_pad - col;                      // zero padding
       }
-      const float* src = sg.src ? sg.src + r * sg.ld : nullptr;
-      for (int j = threadIdx.x; j < sg.width; j += blockDim.x) put(col + j, src ? src[j] : 0.f);
-      col += sg.width;
+      const bool vec = ((width & 3) == 0) && ((col & 3) == 0) &&
+                       (!src || (reinterpret_cast<uintptr_t>(src) & 15) == 0);
+      if (vec) {
+        for (int j = lane * 4; j < width; j += 128) {
+          const float4 v = src ? *reinterpret_cast<const float4*>(src + j)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+          const int64_t o = (int64_t)i * ld_out + col + j;
+          if (!split) {
+            *reinterpret_cast<float4*>(out + o) = v;
+          } else {
+            __nv_bfloat16 h[4], md[4], lo[4];
+            split3(v.x, h[0], md[0], lo[0]);
+            split3(v.y, h[1], md[1], lo[1]);
+            split3(v.z, h[2], md[2], lo[2]);
+            split3(v.w, h[3], md[3], lo[3]);
+            *reinterpret_cast<uint2*>(ob + o) = *reinterpret_cast<uint2*>(h);
+            *reinterpret_cast<uint2*>(ob + plane + o) = *reinterpret_cast<uint2*>(md);
+            *reinterpret_cast<uint2*>(ob + 2 * plane + o) = *reinterpret_cast<uint2*>(lo);
+          }
+        }
+      } else {
+        for (int j = lane; j < width; j += 32) {
+          const float x = src ? src[j] : 0.f;
+          const int64_t o = (int64_t)i * ld_out + col + j;
+          if (!split) {
+            out[o] = x;
+          } else {
+            __nv_bfloat16 h, md, lo;
+            split3(x, h, md, lo);
+            ob[o] = h;
+            ob[plane + o] = md;
+            ob[2 * plane + o] = lo;
+          }
+        }
+      }
+      col += width;
     }
-    for (int j = col + threadIdx.x; j < p.k_pad; j += blockDim.x) put(j, 0.f);
   }
 }
 
@@ -483,7 +518,7 @@ extern "C" int fb_pack_rows(const fb_pack_t* p, int32_t m_max, const int32_t* m_
   for (int s = 0; s < p->nseg; ++s) w += p->seg[s].width;
   FB_CHECK_ARG(w <= p->k_pad && p->k_pad <= ld_out, "pack width exceeds k_pad / ld_out");
   if (m_max <= 0) return FB_OK;
-  pack_rows_kernel<<<std::min(m_max, kNumSMs * 16), 128, 0, (cudaStream_t)stream>>>(
+  pack_rows_kernel<<<std::min((m_max + 7) / 8, kNumSMs * 8), 256, 0, (cudaStream_t)stream>>>(
       *p, m_max, m_dev, rows, parent, tokens, ranks, out, ld_out);
   count_launch();
   return check_launch("pack_rows");

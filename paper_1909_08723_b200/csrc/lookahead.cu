@@ -174,13 +174,57 @@ __device__ __forceinline__ double block_exclusive_scan(double v, double* wsum, d
   return before + excl;
 }
 
+
+// Scan of one kScanTile-element tile held in registers: thread t owns elements
+// [8t, 8t+8) (consecutive -> vectorised, coalesced global access, no shared-
+// memory bank conflicts).  Returns the exclusive prefix of this thread's first
+// element and the tile total.
+__device__ __forceinline__ double tile_scan8(const double (&x)[kScanItems], double (&loc)[kScanItems],
+                                            double* wsum, double& total) {
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    acc += x[k];
+    loc[k] = acc;
+  }
+  return block_exclusive_scan(acc, wsum, total);
+}
+
+__device__ __forceinline__ void load8_exp(const float* __restrict__ src, int base, int cnt, float m,
+                                          double (&x)[kScanItems]) {
+  const int j0 = threadIdx.x * kScanItems;
+  if (j0 + kScanItems <= cnt && ((reinterpret_cast<uintptr_t>(src + base + j0) & 15) == 0)) {
+    const float4 a = *reinterpret_cast<const float4*>(src + base + j0);
+    const float4 b = *reinterpret_cast<const float4*>(src + base + j0 + 4);
+    x[0] = expf(a.x - m); x[1] = expf(a.y - m); x[2] = expf(a.z - m); x[3] = expf(a.w - m);
+    x[4] = expf(b.x - m); x[5] = expf(b.y - m); x[6] = expf(b.z - m); x[7] = expf(b.w - m);
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k)
+      x[k] = (j0 + k < cnt) ? (double)expf(src[base + j0 + k] - m) : 0.0;
+  }
+}
+
+__device__ __forceinline__ void store8(double* __restrict__ dst, int base, int cnt,
+                                       const double (&v)[kScanItems]) {
+  const int j0 = threadIdx.x * kScanItems;
+  if (j0 + kScanItems <= cnt && ((reinterpret_cast<uintptr_t>(dst + base + j0) & 15) == 0)) {
+#pragma unroll
+    for (int k = 0; k < kScanItems; k += 2)
+      *reinterpret_cast<double2*>(dst + base + j0 + k) = make_double2(v[k], v[k + 1]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k)
+      if (j0 + k < cnt) dst[base + j0 + k] = v[k];
+  }
+}
+
 template <bool FROM_LOGITS>
 __global__ void __launch_bounds__(kScanThreads)
 row_scan_kernel(int m_max, const int32_t* __restrict__ m_dev, const void* __restrict__ src,
                 int64_t s_stride, const int32_t* __restrict__ src_rows, int vw, int v_out,
                 const int32_t* __restrict__ slots, double* __restrict__ g_pool, int64_t g_stride,
                 double* __restrict__ eos_out) {
-  __shared__ double tile[kScanTile];
   __shared__ double wsum[32];
   __shared__ float red_f[32];
   __shared__ float red_g[32];
@@ -229,34 +273,27 @@ row_scan_kernel(int m_max, const int32_t* __restrict__ m_dev, const void* __rest
       __syncthreads();
     }
     if (!g) continue;
-    // pass: running sums tile by tile
+    // pass: running sums tile by tile (register-resident, see tile_scan8)
     double carry = 0.0;
     for (int base = 0; base < vw; base += kScanTile) {
       const int cnt = min(kScanTile, vw - base);
-      for (int j = threadIdx.x; j < kScanTile; j += blockDim.x) {
-        double v = 0.0;
-        if (j < cnt) {
-          if constexpr (FROM_LOGITS) v = (double)expf(lg[base + j] - mw) / sw;
-          else v = reinterpret_cast<const double*>(src)[srow * s_stride + base + j];
-        }
-        tile[j] = v;
-      }
-      __syncthreads();
-      double loc[kScanItems];
-      double acc = 0.0;
+      double x[kScanItems], loc[kScanItems];
+      if constexpr (FROM_LOGITS) {
+        load8_exp(lg, base, cnt, mw, x);
 #pragma unroll
-      for (int k = 0; k < kScanItems; ++k) {
-        acc += tile[threadIdx.x * kScanItems + k];
-        loc[k] = acc;
+        for (int k = 0; k < kScanItems; ++k) x[k] /= sw;
+      } else {
+        const double* pr = reinterpret_cast<const double*>(src) + srow * s_stride;
+        const int j0 = threadIdx.x * kScanItems;
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) x[k] = (j0 + k < cnt) ? pr[base + j0 + k] : 0.0;
       }
       double total;
-      const double pre = block_exclusive_scan(acc, wsum, total) + carry;
+      const double pre = tile_scan8(x, loc, wsum, total) + carry;
 #pragma unroll
-      for (int k = 0; k < kScanItems; ++k) tile[threadIdx.x * kScanItems + k] = pre + loc[k];
-      __syncthreads();
-      for (int j = threadIdx.x; j < cnt; j += blockDim.x) g[base + j] = tile[j];
+      for (int k = 0; k < kScanItems; ++k) loc[k] += pre;
+      store8(g, base, cnt, loc);
       carry += total;
-      __syncthreads();
     }
   }
 }
@@ -340,7 +377,6 @@ seg_scan_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __res
                 const int32_t* __restrict__ src_rows, int vw, const int32_t* __restrict__ slots,
                 const double* __restrict__ seg_ws, int nseg, double* __restrict__ g_pool,
                 int64_t g_stride) {
-  __shared__ double tile[kScanTile];
   __shared__ double wsum[32];
   __shared__ float red_f[64];
   __shared__ double red_d[32];
@@ -360,23 +396,14 @@ seg_scan_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __res
   double* g = g_pool + (int64_t)(slots ? slots[i] : i) * g_stride;
   const int c0 = blockIdx.y * kSegCols;
   const int cnt = min(kSegCols, vw - c0);
-  for (int j = threadIdx.x; j < kScanTile; j += blockDim.x)
-    tile[j] = j < cnt ? (double)expf(lg[c0 + j] - mw) : 0.0;
-  __syncthreads();
-  double loc[kScanItems];
-  double acc = 0.0;
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    acc += tile[threadIdx.x * kScanItems + k];
-    loc[k] = acc;
-  }
+  double x[kScanItems], loc[kScanItems];
+  load8_exp(lg, c0, cnt, mw, x);
   double total;
-  const double pre = block_exclusive_scan(acc, wsum, total) + off;
+  const double pre = tile_scan8(x, loc, wsum, total) + off;
   const double inv = 1.0 / tot;
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) tile[threadIdx.x * kScanItems + k] = (pre + loc[k]) * inv;
-  __syncthreads();
-  for (int j = threadIdx.x; j < cnt; j += blockDim.x) g[c0 + j] = tile[j];
+  for (int k = 0; k < kScanItems; ++k) loc[k] = (pre + loc[k]) * inv;
+  store8(g, c0, cnt, loc);
   __syncthreads();
   }
 }
@@ -490,7 +517,7 @@ extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* l
   const int ntiles = (n_out + 63) / 64;       // GEMM epilogue statistics granule
   const int nseg = (vw + kSegCols - 1) / kSegCols;
   const float4* st = reinterpret_cast<const float4*>(row_stats);
-  const int gx = std::min(m_max, 64);
+  const int gx = std::min(m_max, 256);
   dim3 g1(gx, g_pool ? nseg : 1);
   seg_sum_kernel<<<g1, kScanThreads, 0, s>>>(m_max, m_dev, logits, l_stride, st, ntiles, src_rows,
                                              vw, slots, seg_ws, nseg, eos_out, g_pool != nullptr);

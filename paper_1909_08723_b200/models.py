@@ -146,9 +146,10 @@ class Encoder:
             # than the copy); the caller must consume it before the next stage()
             n = B * TM * _pad(Din)
             if self._pinned is None or self._pinned.numel() < n:
-                self._pinned = torch.empty(n, dtype=torch.float32, pin_memory=True)
+                # zeroed once: later batches leave finite stale values in padding,
+                # which only meets zero weight columns / unattended frames
+                self._pinned = torch.zeros(n, dtype=torch.float32, pin_memory=True)
             x = self._pinned[:n].view(shape)
-            x.zero_()
         else:
             x = torch.zeros(shape, dtype=torch.float32)
         xn = x.numpy()
