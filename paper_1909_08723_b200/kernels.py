@@ -64,10 +64,32 @@ def pack(out: torch.Tensor, segs: Sequence[Tuple], *, m: int, m_dev=None, rows=N
               P(out), ld, _lib.stream_ptr())
 
 
+# Instrumentation (bench.py): when set to a list, every tensor-core GEMM launch
+# appends (start_event, end_event, rows (int or device tensor), n, k_alg).
+GEMM_LOG = None
+
+
+def log_gemm_begin():
+    if GEMM_LOG is None:
+        return None
+    e = torch.cuda.Event(enable_timing=True)
+    e.record()
+    return e
+
+
+def log_gemm_end(e0, m, m_dev, n: int, k_alg: int) -> None:
+    if e0 is None:
+        return
+    e1 = torch.cuda.Event(enable_timing=True)
+    e1.record()
+    GEMM_LOG.append((e0, e1, m_dev.clone() if m_dev is not None else m, n, k_alg))
+
+
 def gemm_tc(ap: torch.Tensor, w: torch.Tensor, *, m: Optional[int] = None, m_dev=None,
             k: Optional[int] = None, bias=None, out=None, rows=None, mode: int = 0,
             hidden: int = 0, parent=None, c_in=None, c_out=None, h_out=None, h_res=None,
-            addend=None, h_split=None, row_stats=None, stats_vw: int = 0) -> None:
+            addend=None, h_split=None, row_stats=None, stats_vw: int = 0,
+            k_alg: Optional[int] = None) -> None:
     """Tensor-core GEMM: ap = bf16 planes [P, rows, k_pad], w = bf16 [n, k_pad].
     h_split: optional bf16 [3, rows, k] planes receiving h (next A operand)."""
     g = _lib.FbGemm()
@@ -90,7 +112,9 @@ def gemm_tc(ap: torch.Tensor, w: torch.Tensor, *, m: Optional[int] = None, m_dev
         g.h_split, g.hs_plane_rows, g.ld_hs = P(h_split), h_split.shape[1], h_split.stride(1)
     if row_stats is not None:
         g.row_stats, g.stats_vw = P(row_stats), stats_vw
+    e0 = log_gemm_begin()
     _lib.call("fb_gemm_tc", C.byref(g), ap.shape[0], ap.shape[1], _lib.stream_ptr())
+    log_gemm_end(e0, g.m_max, m_dev, g.n, k_alg if k_alg is not None else g.k)
 
 
 def log_softmax_rows(x: torch.Tensor, out: torch.Tensor, n: int, *, m: int, m_dev=None,

@@ -188,7 +188,8 @@ class Encoder:
                 src = X if r == 0 else Xr
                 xp = torch.empty((B * TM, 4 * He), dtype=torch.float32, device=dev)
                 K.pack(big, [(src, kin, 0)], m=B * TM, k_pad=kin, split=True)
-                K.gemm_tc(big[:, :, :kin], w_ih, m=B * TM, k=kin, bias=b, out=xp)
+                K.gemm_tc(big[:, :, :kin], w_ih, m=B * TM, k=kin, bias=b, out=xp,
+                          k_alg=d.feat_dim * d.subsample if l == 0 else 2 * He)
                 xps.append(xp)
             # the two directions are independent: one stream each
             main = torch.cuda.current_stream(dev)
@@ -202,9 +203,12 @@ class Encoder:
                 y, cbuf, rec = bufs[r]
                 for tns in (y, cbuf, rec, xps[r]):
                     tns.record_stream(st)
-                _lib.call("fb_lstm_recurrence", TM, B, He, _lib.ptr(w_hh), kr, _lib.ptr(xps[r]),
-                          TM * 4 * He, _lib.ptr(y), TM * He, _lib.ptr(cbuf), _lib.ptr(rec),
-                          int(st.cuda_stream))
+                with torch.cuda.stream(st):
+                    e0 = K.log_gemm_begin()
+                    _lib.call("fb_lstm_recurrence", TM, B, He, _lib.ptr(w_hh), kr,
+                              _lib.ptr(xps[r]), TM * 4 * He, _lib.ptr(y), TM * He,
+                              _lib.ptr(cbuf), _lib.ptr(rec), int(st.cuda_stream))
+                    K.log_gemm_end(e0, TM * B, None, 4 * He, He)
                 ys.append(y.reshape(B * TM, He))
             for st in self.streams:
                 main.wait_stream(st)
@@ -218,7 +222,8 @@ class Encoder:
         keys = torch.empty((B * TM, d.att), dtype=torch.float32, device=dev)
         kk = self.w.w_k.shape[1]
         K.pack(big, [(X, kk, 0)], m=B * TM, k_pad=kk, split=True)
-        K.gemm_tc(big[:, :, :kk], self.w.w_k, m=B * TM, k=kk, bias=self.w.b_k, out=keys)
+        K.gemm_tc(big[:, :, :kk], self.w.w_k, m=B * TM, k=kk, bias=self.w.b_k, out=keys,
+                  k_alg=C_)
         # the attention kernels consume E_K = exp(2 K) (tanh via one reciprocal)
         _lib.call("fb_exp2x", keys.numel(), _lib.ptr(keys), _lib.ptr(keys), _lib.stream_ptr())
         return enc.view(B, TM, C_), keys.view(B, TM, d.att), T
@@ -252,12 +257,12 @@ class DecoderStep:
                    split=True, **kw)
             K.gemm_tc(scratch, lay.w, k=lay.k_pad, bias=lay.b, mode=1, hidden=H,
                       c_in=prev.c[l], c_out=cur.c[l], h_out=cur.h[l],
-                      h_res=cur.h[l - 1] if l > 0 else None, **kw)
+                      h_res=cur.h[l - 1] if l > 0 else None, k_alg=lay.k_in, **kw)
         span.__exit__(None, None, None)
         top = cur.h[L - 1]
         kq = w.w_q.shape[1]
         K.pack(scratch, [(top, H, 1)], k_pad=kq, split=True, **kw)
-        K.gemm_tc(scratch, w.w_q, k=kq, out=q, m=m, m_dev=m_dev, rows=rows)
+        K.gemm_tc(scratch, w.w_q, k=kq, out=q, m=m, m_dev=m_dev, rows=rows, k_alg=H)
         with tm("am_attention"):
             _lib.call("fb_attention_step", cfg_ref, num_utts, _lib.ptr(active),
                       _lib.ptr(n_live), _lib.ptr(t_enc), _lib.ptr(keys), _lib.ptr(enc), d.att, C_,
@@ -270,7 +275,7 @@ class DecoderStep:
         with tm("am_output"):
             K.pack(scratch, [(top, H, 1), (cur.ctx, C_, 1)], k_pad=ko, split=True, **kw)
             K.gemm_tc(scratch, w.w_out, k=ko, bias=w.b_out, out=logits, m=m, m_dev=m_dev,
-                      rows=rows)
+                      rows=rows, k_alg=H + C_)
             K.log_softmax_rows(logits, am_logp, d.vocab, m=m, m_dev=m_dev, rows=rows)
 
 
@@ -399,12 +404,12 @@ def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks
                tok_default=tok_default, k_pad=lay.k_pad, split=True)
         K.gemm_tc(scratch, lay.w, m=m, m_dev=m_dev, k=lay.k_pad, bias=lay.b, mode=1, hidden=H,
                   parent=src_idx, c_in=c_in, c_out=state_dst[:, l, 1],
-                  h_out=state_dst[:, l, 0])
+                  h_out=state_dst[:, l, 0], k_alg=lay.k_in)
     if logits is not None:
         K.pack(scratch, [(state_dst[:, L - 1, 0], H, 0, state_dst.stride(0))], m=m, m_dev=m_dev,
                k_pad=w.k_out, split=True)
         kw = dict(m=m, m_dev=m_dev, k=w.k_out, bias=w.b_out, out=logits, row_stats=stats,
-                  stats_vw=w.d.words)
+                  stats_vw=w.d.words, k_alg=H)
         if timer is not None:
             with timer("lm_out_gemm"):
                 K.gemm_tc(scratch, w.emb_w, **kw)
