@@ -279,12 +279,13 @@ int fb_spec_events(const fb_trie_t* trie, int32_t n_max, const int32_t* n_dev,
  * < T_K cannot be selected: its fusion eos entry is set to -inf and no LM
  * event is made.  Other final rows become events as in fb_spec_events.
  * `fusion` must hold word_end (not yet + log P(</s>)) in the eos column of
- * final rows (fb_lookahead_scores with ext_eos = 0). */
+ * final rows (fb_lookahead_scores with ext_eos = 0).  Event numbering starts
+ * at *ev_start (late events already queued) when ev_start is non-NULL. */
 int fb_spec_select(const fb_search_cfg_t* cfg, const fb_search_state_t* st, int32_t num_utts,
                    const fb_trie_t* trie, const int32_t* trie_state, const int32_t* hist_slot,
                    const void* am, int64_t am_stride, double* fusion, int64_t fusion_stride,
                    int32_t* ev_row, int32_t* ev_rank, int32_t* ev_slot, int32_t* ev_count,
-                   int32_t* row_ev, void* stream);
+                   int32_t* row_ev, const int32_t* ev_start, void* stream);
 
 /* fusion[ev_row[e], eos_id] += eos_lp[ev_row[e]] for e < *ev_count. */
 int fb_eos_fixup(int32_t n_max, const int32_t* ev_count, const int32_t* ev_row,
@@ -294,19 +295,20 @@ int fb_eos_fixup(int32_t n_max, const int32_t* ev_count, const int32_t* ev_row,
 /* Word-boundary plan after selection (fusion.py:206-223).  New rows
  * rows[i] (i < *n_dev) whose boundary_rank >= -1 closed a word: each gets a
  * fresh history slot (slots referenced by the rows that entered this step,
- * cur_rows/hist_cur, stay live), in row order.  Entry b: bnd_slot[b] = slot,
- * bnd_src[b] = event row holding its LM state and logits: row_ev[parent] when
- * the parent had a speculative event, else late_base + k for the k-th late
- * event, whose LM input is late_slot[k] = hist_cur[parent] and token
- * late_tok[k] = closed word rank (or -1 = <unk>).  hist_next[row] = slot.
- * slot_mark is scratch of 2*num_slots int32. */
+ * cur_rows/hist_cur, stay live), in row order; hist_next[row] = slot.
+ * Rows whose parent ran a speculative LM event (row_ev[parent] >= 0) reuse it:
+ * bnd_slot/bnd_src (event row) list, *bnd_count.  The others become late
+ * events for the next step's LM batch: late_slot[k] = hist_cur[parent] (LM
+ * input state), late_tok[k] = rank or -1 (<unk>), late_row[k] = late_sink_row,
+ * late_dst[k] = slot, *late_count.  slot_mark: scratch of 2*num_slots int32. */
 int fb_boundary_plan(int32_t n_max, const int32_t* n_dev, const int32_t* rows,
                      const int32_t* parent, const int32_t* boundary_rank,
                      const int32_t* row_ev, const int32_t* cur_rows, const int32_t* cur_count,
                      const int32_t* hist_cur, int32_t* hist_next, int32_t num_slots,
                      int32_t* slot_mark, int32_t* bnd_slot, int32_t* bnd_src,
                      int32_t* bnd_count, int32_t* late_slot, int32_t* late_tok,
-                     int32_t* late_count, int32_t late_base, void* stream);
+                     int32_t* late_row, int32_t* late_dst, int32_t* late_count,
+                     int32_t late_sink_row, void* stream);
 
 /* Copy n rows of row_bytes: dst[dst_idx[i]] = src[src_idx[i]] (NULL = i). */
 int fb_copy_rows(int32_t n_max, const int32_t* n_dev, const int32_t* src_idx,

@@ -91,10 +91,10 @@ _SIGS = {
     "fb_spec_events": (C.c_int, [C.POINTER(FbTrie), i32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                  vp]),
     "fb_boundary_plan": (C.c_int, [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp,
-                                   vp, vp, vp, i32, vp]),
+                                   vp, vp, vp, vp, vp, i32, vp]),
     "fb_spec_select": (C.c_int, [C.POINTER(FbSearchCfg), C.POINTER(FbSearchState), i32,
                                  C.POINTER(FbTrie), vp, vp, vp, i64, vp, i64, vp, vp, vp, vp, vp,
-                                 vp]),
+                                 vp, vp]),
     "fb_eos_fixup": (C.c_int, [i32, vp, vp, vp, vp, i64, i32, vp]),
     "fb_copy_rows": (C.c_int, [i32, vp, vp, vp, vp, vp, i64, vp]),
     "fb_exp2x": (C.c_int, [i64, vp, vp, vp]),

@@ -384,7 +384,9 @@ __global__ void spec_events_kernel(fb_trie_t trie, int n_max, const int32_t* __r
 }
 
 // Single CTA: mark live slots, list free slots in order, hand them to the
-// boundary rows in row order.
+// boundary rows in row order.  Rows whose parent ran a speculative LM event
+// reuse it now (bnd list); the others become "late" events that the next
+// step's LM batch runs first (late lists, written where that batch reads them).
 __global__ void __launch_bounds__(1024)
 boundary_plan_kernel(int n_max, const int32_t* __restrict__ n_dev, const int32_t* __restrict__ rows,
                      const int32_t* __restrict__ parent, const int32_t* __restrict__ brank,
@@ -392,9 +394,10 @@ boundary_plan_kernel(int n_max, const int32_t* __restrict__ n_dev, const int32_t
                      const int32_t* __restrict__ cur_count, const int32_t* __restrict__ hist_cur,
                      int32_t* __restrict__ hist_next, int num_slots, int32_t* __restrict__ mark,
                      int32_t* __restrict__ bnd_slot, int32_t* __restrict__ bnd_src,
-                     int32_t* __restrict__ bnd_count, int32_t* __restrict__ unk_slot,
-                     int32_t* __restrict__ unk_tok, int32_t* __restrict__ unk_count,
-                     int unk_base) {
+                     int32_t* __restrict__ bnd_count, int32_t* __restrict__ late_slot,
+                     int32_t* __restrict__ late_tok, int32_t* __restrict__ late_row,
+                     int32_t* __restrict__ late_dst, int32_t* __restrict__ late_count,
+                     int late_sink_row) {
   __shared__ int wsum[32];
   __shared__ int wsum2[32];
   __shared__ int carry, carry2;
@@ -405,7 +408,6 @@ boundary_plan_kernel(int n_max, const int32_t* __restrict__ n_dev, const int32_t
   const int nc = *cur_count;
   for (int i = tid; i < nc; i += blockDim.x) mark[hist_cur[cur_rows[i]]] = 1;
   __syncthreads();
-  // free list: unmarked slots in ascending order -> stored (negated+1) in mark
   if (tid == 0) carry = 0;
   __syncthreads();
   for (int b0 = 0; b0 < num_slots; b0 += blockDim.x) {
@@ -438,15 +440,15 @@ boundary_plan_kernel(int n_max, const int32_t* __restrict__ n_dev, const int32_t
   __syncthreads();
   for (int b0 = 0; b0 < n; b0 += blockDim.x) {
     const int i = b0 + tid;
-    int is_b = 0, is_unk = 0, r = -1, br = -2;
+    int is_b = 0, is_late = 0, r = -1, br = -2;
     if (i < n) {
       r = rows[i];
       br = brank[r];
       is_b = br >= -1;
-      // a late LM event unless the parent already ran a speculative one
-      is_unk = is_b && (br == -1 || row_ev[parent[r]] < 0);
+      is_late = is_b && (br == -1 || row_ev[parent[r]] < 0);
     }
-    int x = is_b, y = is_unk;
+    // prefix counts: all boundaries (slot order), spec-sourced, late
+    int x = is_b, y = is_late;
     for (int off = 1; off < 32; off <<= 1) {
       const int a = __shfl_up_sync(0xffffffffu, x, off);
       const int b = __shfl_up_sync(0xffffffffu, y, off);
@@ -467,25 +469,27 @@ boundary_plan_kernel(int n_max, const int32_t* __restrict__ n_dev, const int32_t
     }
     __syncthreads();
     if (is_b) {
-      const int k = carry + (warp ? wsum[warp - 1] : 0) + x - 1;     // boundary index
+      const int k = carry + (warp ? wsum[warp - 1] : 0) + x - 1;      // k-th boundary
+      const int kl = carry2 + (warp ? wsum2[warp - 1] : 0) + y - 1;   // late index if late
       const int slot = freel[k];
-      bnd_slot[k] = slot;
       hist_next[r] = slot;
       const int p = parent[r];
-      if (is_unk) {
-        const int ku = carry2 + (warp ? wsum2[warp - 1] : 0) + y - 1;
-        unk_slot[ku] = hist_cur[p];
-        unk_tok[ku] = br;
-        bnd_src[k] = unk_base + ku;
+      if (is_late) {
+        late_slot[kl] = hist_cur[p];
+        late_tok[kl] = br;
+        late_row[kl] = late_sink_row;
+        late_dst[kl] = slot;
       } else {
-        bnd_src[k] = row_ev[p];
+        const int ks = k - (kl + 1);                 // spec index = k - #late rows before it
+        bnd_slot[ks] = slot;
+        bnd_src[ks] = row_ev[p];
       }
     }
     __syncthreads();
     if (tid == 0) { carry += wsum[nw - 1]; carry2 += wsum2[nw - 1]; }
     __syncthreads();
   }
-  if (tid == 0) { *bnd_count = carry; *unk_count = carry2; }
+  if (tid == 0) { *bnd_count = carry - carry2; *late_count = carry2; }
 }
 
 __global__ void copy_rows_kernel(int n_max, const int32_t* __restrict__ n_dev,
@@ -603,14 +607,15 @@ extern "C" int fb_boundary_plan(int32_t n_max, const int32_t* n_dev, const int32
                                 const int32_t* cur_count, const int32_t* hist_cur,
                                 int32_t* hist_next, int32_t num_slots, int32_t* slot_mark,
                                 int32_t* bnd_slot, int32_t* bnd_src, int32_t* bnd_count,
-                                int32_t* unk_slot, int32_t* unk_tok, int32_t* unk_count,
-                                int32_t unk_base, void* stream) {
+                                int32_t* late_slot, int32_t* late_tok, int32_t* late_row,
+                                int32_t* late_dst, int32_t* late_count, int32_t late_sink_row,
+                                void* stream) {
   FB_CHECK_ARG(rows && parent && boundary_rank && cur_rows && cur_count && hist_cur && hist_next,
                "null boundary-plan arguments");
   boundary_plan_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(
       n_max, n_dev, rows, parent, boundary_rank, row_ev, cur_rows, cur_count, hist_cur,
-      hist_next, num_slots, slot_mark, bnd_slot, bnd_src, bnd_count, unk_slot, unk_tok,
-      unk_count, unk_base);
+      hist_next, num_slots, slot_mark, bnd_slot, bnd_src, bnd_count, late_slot, late_tok,
+      late_row, late_dst, late_count, late_sink_row);
   count_launch();
   return check_launch("boundary_plan");
 }

@@ -614,12 +614,15 @@ extern "C" int fb_spec_select(const fb_search_cfg_t* cfg, const fb_search_state_
                               const int32_t* hist_slot, const void* am, int64_t am_stride,
                               double* fusion, int64_t fusion_stride, int32_t* ev_row,
                               int32_t* ev_rank, int32_t* ev_slot, int32_t* ev_count,
-                              int32_t* row_ev, void* stream) {
+                              int32_t* row_ev, const int32_t* ev_start, void* stream) {
   FB_CHECK_ARG(cfg && st && trie && am && fusion && ev_count && row_ev, "null spec-select args");
   const size_t smem = (size_t)cfg->beam * cfg->vocab * (sizeof(double) + 1);
   if (smem > 200 * 1024) return fail(FB_ERR_CONFIG, "beam x vocabulary too large");
   cudaStream_t s = (cudaStream_t)stream;
-  cudaMemsetAsync(ev_count, 0, sizeof(int32_t), s);
+  if (ev_start)   // events appended after the late events queued by the last step
+    cudaMemcpyAsync(ev_count, ev_start, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+  else
+    cudaMemsetAsync(ev_count, 0, sizeof(int32_t), s);
   if (num_utts <= 0) return check_launch("spec_select");
   if (cfg->am_f32) {
     auto k = spec_select_kernel<float>;

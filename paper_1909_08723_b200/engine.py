@@ -62,6 +62,7 @@ class _LmPool:
         self.hist = [z(N), z(N)]
         self.brank = z(N)
         self.bnd_slot, self.bnd_src, self.unk_slot, self.unk_tok = z(N), z(N), z(N), z(N)
+        self.late_row, self.late_dst = z(N), z(N)
         self.bnd_count, self.unk_count = z(1), z(1)
         self.mark = z(2 * self.P)
         self.ext_eos = torch.zeros(N, dtype=torch.float64, device=device)
@@ -123,15 +124,85 @@ class _NoTimer:
 
 def decode_fused(features, scorer, fusion, config: DecodeConfig, token_dict
                  ) -> List[DecodeResult]:
-    """decode_batch entry: host features -> staged device batch -> engine."""
+    """decode_batch entry: host features -> staged device batch -> engine.
+    The FusedDecoder (and its device session) is cached on the scorer, so
+    repeated calls with the same batch shape reuse buffers and CUDA graphs."""
     Xh, T = scorer.encoder.stage([np.asarray(f.data, np.float32) for f in features], pin=True)
     X = Xh.to(scorer.device, non_blocking=True)
     done = torch.cuda.Event()
     done.record()
-    out = FusedDecoder(scorer, fusion, config, token_dict).run(
-        X, T, [f.utt_id for f in features])
+    key = (id(fusion), tuple(sorted(vars(config).items())), id(token_dict))
+    cache = scorer.__dict__.setdefault("_fused_cache", {})
+    dec = cache.get(key)
+    if dec is None or dec.fusion is not fusion:
+        cache.clear()
+        dec = cache[key] = FusedDecoder(scorer, fusion, config, token_dict)
+    out = dec.run(X, T, [f.utt_id for f in features])
     done.synchronize()          # the pinned staging buffer may be reused afterwards
     return out
+
+
+class _Session:
+    """All device buffers of one batch shape (B, T_max, max_tokens) plus the two
+    captured step graphs; reused by every decode of that shape."""
+
+    def __init__(self, dec: "FusedDecoder", B: int, TM: int, MT: int):
+        scorer, fusion, config, token_dict = dec.scorer, dec.fusion, dec.config, dec.token_dict
+        dev = scorer.device
+        w = scorer.weights
+        d = w.d
+        self.B, self.TM, self.MT = B, TM, MT
+        Kb = config.beam_size
+        self.K = Kb
+        N = self.N = B * Kb
+        V = self.V = len(token_dict)
+        self.buf = SearchBuffers(B, Kb, MT, TM, dev)
+        self.has_fusion = fusion is not None
+        early = (not self.has_fusion) or bool(fusion.nonpositive_scores)
+        self.cfg = search_cfg(config, token_dict, self.has_fusion, early, True, MT, TM)
+        self.cfg_ref = C.byref(self.cfg)
+        self.rows = [torch.zeros(N, dtype=torch.int32, device=dev) for _ in range(2)]
+        self.count = [torch.zeros(1, dtype=torch.int32, device=dev) for _ in range(2)]
+        self.views = [_view_with_rows(self.buf, p, self.rows[1 - p], self.count[1 - p])
+                      for p in range(2)]
+        L, H, C_ = d.dec_layers, d.dec_hidden, d.ctx
+        self.X2 = [AmState(L, N, H, C_, dev), AmState(L, N, H, C_, dev)]
+        self.scratch = split_scratch(N, w.k_max, dev)
+        self.q = torch.empty((N, d.att), dtype=torch.float32, device=dev)
+        self.logits = torch.empty((N, V), dtype=torch.float32, device=dev)
+        self.am_logp = torch.zeros((N, V), dtype=torch.float32, device=dev)
+        self.energy = torch.empty((N, TM), dtype=torch.float32, device=dev)
+        self.enc = torch.empty((B, TM, C_), dtype=torch.float32, device=dev)
+        self.keys = torch.empty((B * TM, d.att), dtype=torch.float32, device=dev)
+        self.slots0 = torch.arange(B, dtype=torch.int32, device=dev) * Kb
+        self.fus_buf = None
+        self.lm = None
+        if self.has_fusion:
+            self.lm = _LmPool(fusion.word_lm.weights, N, dev)
+            self.fus_buf = torch.zeros((N + 1, V), dtype=torch.float64, device=dev)
+        self.graphs = None
+        self.per_step_launches = 0.0
+
+    def reset(self, T: Sequence[int], max_len: Sequence[int]) -> None:
+        """Per-decode initial state (decoder.py:350-361): one live row per
+        utterance, zero decoder state, root trie state, <s> word history."""
+        buf = self.buf
+        stream = _lib.stream_ptr()
+        buf.max_len.copy_(torch.as_tensor(list(max_len), dtype=torch.int32), non_blocking=True)
+        buf.t_enc.copy_(torch.as_tensor(list(T), dtype=torch.int32), non_blocking=True)
+        _lib.call("fb_search_init", self.cfg_ref, C.byref(buf.view(0)), self.B, stream)
+        buf.acc[0].zero_()
+        prev = self.X2[1]
+        prev.h.zero_()
+        prev.c.zero_()
+        prev.ctx.zero_()
+        self.rows[0][:self.B] = self.slots0
+        self.count[0].fill_(self.B)
+        if self.lm is not None:
+            lm = self.lm
+            lm.trie[0].zero_()
+            lm.hist[0].zero_()
+            lm.start()
 
 
 class FusedDecoder:
@@ -147,160 +218,148 @@ class FusedDecoder:
         self.prune_spec = True      # exact pruning of speculative <eos> LM events
         self.use_graphs = True      # one CUDA graph per step parity, replayed
         self.poll_every = 8         # host polls the live-row count every k steps
+        self._sess: Optional[_Session] = None
+
+    def _session(self, B: int, TM: int, MT: int) -> _Session:
+        s = self._sess
+        if s is None or (s.B, s.TM, s.MT) != (B, TM, MT):
+            self._sess = None           # release the previous shape first
+            s = self._sess = _Session(self, B, TM, MT)
+        return s
+
+    def _step(self, S: _Session, c: int, tm, counts) -> None:
+        """One lock-step decode step on parity c (capturable: no host reads)."""
+        scorer, fusion = self.scorer, self.fusion
+        buf, N, V, B = S.buf, S.N, S.V, S.B
+        rc, nc = S.rows[c], S.count[c]
+        stream = _lib.stream_ptr()              # the capture stream inside a graph
+        with tm("am_step"):
+            scorer.step_fn(N=N, rows=rc, m=N, m_dev=nc, parent=buf.parent,
+                           last_tok=buf.last_tok, prev=S.X2[1 - c], cur=S.X2[c],
+                           scratch=S.scratch, q=S.q, logits=S.logits, am_logp=S.am_logp,
+                           cfg_ref=S.cfg_ref, num_utts=B, active=buf.active,
+                           n_live=buf.n_live, t_enc=buf.t_enc, keys=S.keys, enc=S.enc,
+                           acc_in=buf.acc[c], acc_out=buf.acc[1 - c], cov=buf.cov,
+                           energy=S.energy, timer=None if isinstance(tm, _NoTimer) else tm)
+        fus_buf = S.fus_buf
+        if S.has_fusion:
+            lm, dtrie = S.lm, fusion.dtrie
+            lw = lm.lw
+            Vw = lw.d.words
+            with tm("lookahead"):
+                # word_end in the eos column of final rows; log P(</s>) added below
+                _lib.call("fb_lookahead_scores", dtrie.ref, N, P(nc), P(rc), P(lm.trie[c]),
+                          P(lm.hist[c]), P(lm.g), Vw, P(lm.eos), P(lm.zero_eos),
+                          fusion.space_id, fusion.eos_id, fusion.oov_penalty,
+                          fusion.score_floor, P(fus_buf), V, P(fusion._floored), stream)
+            with tm("lm_spec"):
+                if self.prune_spec:
+                    _lib.call("fb_spec_select", S.cfg_ref, C.byref(S.views[c]), B, dtrie.ref,
+                              P(lm.trie[c]), P(lm.hist[c]), P(S.am_logp), V, P(fus_buf), V,
+                              P(lm.ev_row), P(lm.ev_rank), P(lm.ev_slot), P(lm.ev_count),
+                              P(lm.row_ev), None, stream)
+                else:
+                    _lib.call("fb_spec_events", dtrie.ref, N, P(nc), P(rc), P(lm.trie[c]),
+                              P(lm.hist[c]), P(lm.ev_row), P(lm.ev_rank), P(lm.ev_slot),
+                              P(lm.ev_count), P(lm.row_ev), stream)
+                lm_step(lw, m=N, m_dev=lm.ev_count, state_src=lm.state, src_idx=lm.ev_slot,
+                        state_dst=lm.ev_state, ranks=lm.ev_rank, tok_default=0,
+                        scratch=lm.scratch, logits=lm.ev_logits, timer=tm, stats=lm.ev_stats)
+            with tm("lm_eos"):
+                K.stats_to_g(lm.ev_logits, lm.ev_stats, Vw, lw.v_out, m=N, m_dev=lm.ev_count,
+                             slots=lm.ev_row, eos_out=lm.ext_eos)
+                _lib.call("fb_eos_fixup", N, P(lm.ev_count), P(lm.ev_row), P(lm.ext_eos),
+                          P(fus_buf), V, fusion.eos_id, stream)
+            if counts is not None:
+                counts.append(lm.ev_count.clone())
+        with tm("select"):
+            _lib.call("fb_search_step", S.cfg_ref, C.byref(S.views[c]), B, P(S.am_logp), V,
+                      P(fus_buf), V, stream)
+        if S.has_fusion:
+            rn, cn = S.rows[1 - c], S.count[1 - c]
+            with tm("advance"):
+                _lib.call("fb_trie_advance", dtrie.ref, N, P(cn), P(rn), P(buf.parent),
+                          P(lm.trie[c]), P(lm.hist[c]), P(buf.last_tok), fusion.space_id,
+                          fusion.eos_id, fusion.pad_id, P(lm.trie[1 - c]), P(lm.hist[1 - c]),
+                          P(lm.brank), stream)
+                _lib.call("fb_boundary_plan", N, P(cn), P(rn), P(buf.parent), P(lm.brank),
+                          P(lm.row_ev), P(rc), P(nc), P(lm.hist[c]), P(lm.hist[1 - c]),
+                          lm.P, P(lm.mark), P(lm.bnd_slot), P(lm.bnd_src), P(lm.bnd_count),
+                          P(lm.unk_slot), P(lm.unk_tok), P(lm.late_row), P(lm.late_dst),
+                          P(lm.unk_count), N, stream)
+            with tm("lm_late"):
+                # boundary rows without a speculative event: (h, rank) or (h, <unk>)
+                lm_step(lw, m=N, m_dev=lm.unk_count, state_src=lm.state, src_idx=lm.unk_slot,
+                        state_dst=lm.ev_state[N:], ranks=lm.unk_tok, tok_default=lw.unk_tok,
+                        scratch=lm.scratch, logits=lm.ev_logits[N:], timer=tm,
+                        stats=lm.ev_stats[N:])
+            with tm("g_build"):
+                K.copy_rows(lm.ev_state, lm.state, m=N, m_dev=lm.bnd_count, src_idx=lm.bnd_src,
+                            dst_idx=lm.bnd_slot)
+                K.stats_to_g(lm.ev_logits, lm.ev_stats, Vw, lw.v_out, m=N, m_dev=lm.bnd_count,
+                             src_rows=lm.bnd_src, slots=lm.bnd_slot, g_pool=lm.g,
+                             eos_out=lm.eos, seg_ws=lm.seg_ws)
+                K.copy_rows(lm.ev_state[N:], lm.state, m=N, m_dev=lm.unk_count,
+                            dst_idx=lm.late_dst)
+                K.stats_to_g(lm.ev_logits[N:], lm.ev_stats[N:], Vw, lw.v_out, m=N,
+                             m_dev=lm.unk_count, slots=lm.late_dst, g_pool=lm.g,
+                             eos_out=lm.eos, seg_ws=lm.seg_ws)
+            if counts is not None:
+                counts.append(lm.bnd_count.clone())
+                counts.append(lm.unk_count.clone())
 
     def run(self, X: torch.Tensor, T: Sequence[int], utt_ids: Sequence[str], timer=None,
             record_counts: bool = False) -> List[DecodeResult]:
-        scorer, fusion, config, token_dict = self.scorer, self.fusion, self.config, self.token_dict
+        config = self.config
         tm = timer if timer is not None else _NoTimer()
         lib = _lib.lib()
         l0 = lib.fb_launch_count()
-        dev = scorer.device
-        w = scorer.weights
-        d = w.d
         B = len(T)
         if B == 0:
             return []
-        Kb = config.beam_size
-        N = B * Kb
-        V = len(token_dict)
-        stream = _lib.stream_ptr()
-        with tm("encoder"):
-            enc, keys, T = scorer.encoder(X, T)
-        TM = max(T)
-        max_len = [max(1, int(math.floor(config.max_len_ratio * t))) for t in T]
+        Tenc = list(T)
+        TM = max(Tenc)
+        max_len = [max(1, int(math.floor(config.max_len_ratio * t))) for t in Tenc]
         MT = max(max_len) + 1
-        buf = SearchBuffers(B, Kb, MT, TM, dev)
-        buf.max_len.copy_(torch.as_tensor(max_len, dtype=torch.int32))
-        buf.t_enc.copy_(torch.as_tensor(T, dtype=torch.int32))
-        has_fusion = fusion is not None
-        early = (not has_fusion) or bool(fusion.nonpositive_scores)
-        cfg = search_cfg(config, token_dict, has_fusion, early, True, MT, TM)
-        cfg_ref = C.byref(cfg)
-        _lib.call("fb_search_init", cfg_ref, C.byref(buf.view(0)), B, stream)
-        rows = [torch.zeros(N, dtype=torch.int32, device=dev) for _ in range(2)]
-        count = [torch.zeros(1, dtype=torch.int32, device=dev) for _ in range(2)]
-        rows[0][:B] = torch.arange(B, dtype=torch.int32, device=dev) * Kb
-        count[0].fill_(B)
-        views = [_view_with_rows(buf, p, rows[1 - p], count[1 - p]) for p in range(2)]
-
-        L, H, C_ = d.dec_layers, d.dec_hidden, d.ctx
-        X2 = [AmState(L, N, H, C_, dev), AmState(L, N, H, C_, dev)]
-        scratch = split_scratch(N, w.k_max, dev)
-        q = torch.empty((N, d.att), dtype=torch.float32, device=dev)
-        logits = torch.empty((N, V), dtype=torch.float32, device=dev)
-        am_logp = torch.zeros((N, V), dtype=torch.float32, device=dev)
-        energy = torch.empty((N, TM), dtype=torch.float32, device=dev)
-
-        fus_buf = None
-        if has_fusion:
-            lw = fusion.word_lm.weights
-            lm = _LmPool(lw, N, dev)
-            lm.start()
-            fus_buf = torch.zeros((N, V), dtype=torch.float64, device=dev)
-            dtrie = fusion.dtrie
-            Vw = lw.d.words
+        S = self._session(B, TM, MT)
+        with tm("encoder"):
+            _, _, Tenc = self.scorer.encoder(X, Tenc, out=(S.enc, S.keys))
+        S.reset(Tenc, max_len)
         counts = [] if record_counts else None
-
-        def step(c: int) -> None:
-            rc, nc = rows[c], count[c]
-            stream = _lib.stream_ptr()          # the capture stream inside a graph
-            with tm("am_step"):
-                scorer.step_fn(N=N, rows=rc, m=N, m_dev=nc, parent=buf.parent,
-                               last_tok=buf.last_tok, prev=X2[1 - c], cur=X2[c], scratch=scratch,
-                               q=q, logits=logits, am_logp=am_logp, cfg_ref=cfg_ref, num_utts=B,
-                               active=buf.active, n_live=buf.n_live, t_enc=buf.t_enc, keys=keys,
-                               enc=enc, acc_in=buf.acc[c], acc_out=buf.acc[1 - c], cov=buf.cov,
-                               energy=energy, timer=timer)
-            if has_fusion:
-                with tm("lookahead"):
-                    # word_end in the eos column of final rows; log P(</s>) added below
-                    _lib.call("fb_lookahead_scores", dtrie.ref, N, P(nc), P(rc), P(lm.trie[c]),
-                              P(lm.hist[c]), P(lm.g), Vw, P(lm.eos), P(lm.zero_eos),
-                              fusion.space_id, fusion.eos_id, fusion.oov_penalty,
-                              fusion.score_floor, P(fus_buf), V, P(fusion._floored), stream)
-                with tm("lm_spec"):
-                    if self.prune_spec:
-                        _lib.call("fb_spec_select", cfg_ref, C.byref(views[c]), B, dtrie.ref,
-                                  P(lm.trie[c]), P(lm.hist[c]), P(am_logp), V, P(fus_buf), V,
-                                  P(lm.ev_row), P(lm.ev_rank), P(lm.ev_slot), P(lm.ev_count),
-                                  P(lm.row_ev), stream)
-                    else:
-                        _lib.call("fb_spec_events", dtrie.ref, N, P(nc), P(rc), P(lm.trie[c]),
-                                  P(lm.hist[c]), P(lm.ev_row), P(lm.ev_rank), P(lm.ev_slot),
-                                  P(lm.ev_count), P(lm.row_ev), stream)
-                    lm_step(lw, m=N, m_dev=lm.ev_count, state_src=lm.state, src_idx=lm.ev_slot,
-                            state_dst=lm.ev_state, ranks=lm.ev_rank, tok_default=0,
-                            scratch=lm.scratch, logits=lm.ev_logits, timer=tm,
-                            stats=lm.ev_stats)
-                with tm("lm_eos"):
-                    K.stats_to_g(lm.ev_logits, lm.ev_stats, Vw, lw.v_out, m=N,
-                                 m_dev=lm.ev_count, slots=lm.ev_row, eos_out=lm.ext_eos)
-                    _lib.call("fb_eos_fixup", N, P(lm.ev_count), P(lm.ev_row), P(lm.ext_eos),
-                              P(fus_buf), V, fusion.eos_id, stream)
-                if counts is not None:
-                    counts.append(lm.ev_count.clone())
-            with tm("select"):
-                _lib.call("fb_search_step", cfg_ref, C.byref(views[c]), B, P(am_logp), V,
-                          P(fus_buf), V, stream)
-            if has_fusion:
-                rn, cn = rows[1 - c], count[1 - c]
-                with tm("advance"):
-                    _lib.call("fb_trie_advance", dtrie.ref, N, P(cn), P(rn), P(buf.parent),
-                              P(lm.trie[c]), P(lm.hist[c]), P(buf.last_tok), fusion.space_id,
-                              fusion.eos_id, fusion.pad_id, P(lm.trie[1 - c]),
-                              P(lm.hist[1 - c]), P(lm.brank), stream)
-                    _lib.call("fb_boundary_plan", N, P(cn), P(rn), P(buf.parent), P(lm.brank),
-                              P(lm.row_ev), P(rc), P(nc), P(lm.hist[c]), P(lm.hist[1 - c]),
-                              lm.P, P(lm.mark), P(lm.bnd_slot), P(lm.bnd_src), P(lm.bnd_count),
-                              P(lm.unk_slot), P(lm.unk_tok), P(lm.unk_count), N, stream)
-                with tm("lm_late"):
-                    # boundary rows without a speculative event: (h, rank) or (h, <unk>)
-                    lm_step(lw, m=N, m_dev=lm.unk_count, state_src=lm.state,
-                            src_idx=lm.unk_slot, state_dst=lm.ev_state[N:], ranks=lm.unk_tok,
-                            tok_default=lw.unk_tok, scratch=lm.scratch,
-                            logits=lm.ev_logits[N:], timer=tm, stats=lm.ev_stats[N:])
-                with tm("g_build"):
-                    K.copy_rows(lm.ev_state, lm.state, m=N, m_dev=lm.bnd_count,
-                                src_idx=lm.bnd_src, dst_idx=lm.bnd_slot)
-                    K.stats_to_g(lm.ev_logits, lm.ev_stats, Vw, lw.v_out, m=N,
-                                 m_dev=lm.bnd_count, src_rows=lm.bnd_src, slots=lm.bnd_slot,
-                                 g_pool=lm.g, eos_out=lm.eos, seg_ws=lm.seg_ws)
-                if counts is not None:
-                    counts.append(lm.bnd_count.clone())
-                    counts.append(lm.unk_count.clone())
         parity = 0
         steps = 0
         replayed = 0
         if self.use_graphs and timer is None and counts is None:
-            graphs = [torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()]
-            c0 = lib.fb_launch_count()
-            for p_ in (0, 1):
-                with torch.cuda.graph(graphs[p_]):
-                    step(p_)
-            per_step = (lib.fb_launch_count() - c0) / 2.0
-            l0 += lib.fb_launch_count() - c0          # captures launch nothing
+            if S.graphs is None:
+                g = [torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()]
+                c0 = lib.fb_launch_count()
+                for p_ in (0, 1):
+                    with torch.cuda.graph(g[p_]):
+                        self._step(S, p_, _NoTimer(), None)
+                S.per_step_launches = (lib.fb_launch_count() - c0) / 2.0
+                l0 += lib.fb_launch_count() - c0          # captures launch nothing
+                S.graphs = g
             while True:
                 for _ in range(self.poll_every):
-                    graphs[parity].replay()
+                    S.graphs[parity].replay()
                     parity ^= 1
                     steps += 1
                     replayed += 1
-                if int(count[parity].item()) == 0:
+                if int(S.count[parity].item()) == 0:
                     break
         else:
             while True:
-                step(parity)
+                self._step(S, parity, tm, counts)
                 parity ^= 1
                 steps += 1
-                if int(count[parity].item()) == 0:
+                if int(S.count[parity].item()) == 0:
                     break
         self.steps_run = steps
         # kernels this run put on the GPU (graph replays included)
-        self.kernel_launches = int(lib.fb_launch_count() - l0 +
-                                   (per_step * replayed if replayed else 0))
+        self.kernel_launches = int(lib.fb_launch_count() - l0 + S.per_step_launches * replayed)
         if counts is not None:
             self.spec_counts = torch.cat(counts).view(steps, 3).cpu() if counts else None
-        return buf.results(list(utt_ids), T)
+        return S.buf.results(list(utt_ids), Tenc)
 
 
 def _view_with_rows(buf: SearchBuffers, p: int, next_rows, next_count):

@@ -157,7 +157,7 @@ class Encoder:
             xn[u, :T[u], :Din] = np.asarray(f, np.float32)[:T[u] * d.subsample].reshape(T[u], Din)
         return x.reshape(B * TM, -1), T
 
-    def __call__(self, feats, lengths: Optional[Sequence[int]] = None):
+    def __call__(self, feats, lengths: Optional[Sequence[int]] = None, out=None):
         """feats: list of [T, feat_dim] arrays, or a staged device tensor
         [B*TM, Din_pad] with ``lengths`` (encoder frames per utterance)."""
         d = self.w.d
@@ -218,8 +218,12 @@ class Encoder:
             X = Xn
             Xr = torch.empty_like(X)
         C_ = 2 * He
-        enc = X[:, :C_].contiguous()
-        keys = torch.empty((B * TM, d.att), dtype=torch.float32, device=dev)
+        if out is not None:
+            enc, keys = out
+            enc.view(B * TM, C_).copy_(X[:, :C_])
+        else:
+            enc = X[:, :C_].contiguous()
+            keys = torch.empty((B * TM, d.att), dtype=torch.float32, device=dev)
         kk = self.w.w_k.shape[1]
         K.pack(big, [(X, kk, 0)], m=B * TM, k_pad=kk, split=True)
         K.gemm_tc(big[:, :, :kk], self.w.w_k, m=B * TM, k=kk, bias=self.w.b_k, out=keys,
