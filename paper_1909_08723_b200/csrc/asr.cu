@@ -175,6 +175,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // e_t = sum_a v_a - 2 sum_a v_a / (1 + E_k E_q).  The constant sum_a v_a
 // cancels in the softmax, so the kernel stores e'_t = -2 sum_a v_a / (1 + E_k E_q):
 // one FFMA + one MUFU.RCP + one FFMA per (row, frame, a).
+template <int R>
 __global__ void __launch_bounds__(kEnWarps * 32)
 att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
                   const int32_t* __restrict__ n_live, const int32_t* __restrict__ t_enc,
@@ -188,13 +189,13 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
   extern __shared__ float sm[];
   const int K = cfg.beam, TM = cfg.t_max;
   const int n = n_live[u];
-  float* qs = sm;                  // [n][A]  E_q = exp(2 q)
-  float* vs = qs + n * A;          // [A]
+  float* vs = sm;                  // [A]
+  float* qs = sm + A;              // [R][A]  E_q = exp(2 q); rows >= n are 0
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int slot0 = u * K;
-  for (int j = tid; j < n * A; j += blockDim.x) {
-    const int i = j / A, a = j % A;
-    qs[j] = expf(2.0f * q[(int64_t)(slot0 + i) * ldq + a]);
+  for (int j = tid; j < R * A; j += blockDim.x) {
+    const int i = j / A, a = j - i * A;
+    qs[j] = i < n ? expf(2.0f * q[(int64_t)(slot0 + i) * ldq + a]) : 0.f;
   }
   for (int a = tid; a < A; a += blockDim.x) vs[a] = v[a];
   __syncthreads();
@@ -203,30 +204,27 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
     const int t = t_base + warp * kEnFrames + f;
     if (t >= T) break;
     const float* kt = ku + (int64_t)t * A;
-    for (int i0 = 0; i0 < n; i0 += 16) {
-      const int nb = min(16, n - i0);
-      float e[16];
+    float e[R];
 #pragma unroll
-      for (int r = 0; r < 16; ++r) e[r] = 0.f;
-      for (int a = lane; a < A; a += 32) {
-        const float ek = __ldg(kt + a);
-        const float va = vs[a];
+    for (int r = 0; r < R; ++r) e[r] = 0.f;
+    for (int a = lane; a < A; a += 32) {
+      const float ek = __ldg(kt + a);
+      const float va = vs[a];
+      const float* qa = qs + a;
 #pragma unroll
-        for (int r = 0; r < 16; ++r)
-          if (r < nb) e[r] = fmaf(va, rcp_approx(fmaf(ek, qs[(i0 + r) * A + a], 1.0f)), e[r]);
-      }
+      for (int r = 0; r < R; ++r) e[r] = fmaf(va, rcp_approx(fmaf(ek, qa[r * A], 1.0f)), e[r]);
+    }
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        float x = e[r];
-        for (int off = 16; off; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-        e[r] = x;
-      }
-      if (lane < nb) {
-        float x = 0.f;
+    for (int r = 0; r < R; ++r) {
+      float x = e[r];
+      for (int off = 16; off; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+      e[r] = x;
+    }
+    if (lane < n && lane < R) {
+      float x = 0.f;
 #pragma unroll
-        for (int r = 0; r < 16; ++r) x = lane == r ? e[r] : x;
-        energy[(int64_t)(slot0 + i0 + lane) * TM + t] = -2.0f * x;
-      }
+      for (int r = 0; r < R; ++r) x = lane == r ? e[r] : x;
+      energy[(int64_t)(slot0 + lane) * TM + t] = -2.0f * x;
     }
   }
 }
@@ -285,42 +283,56 @@ att_context_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
     at[j] = r < n ? al[r * T + t] : 0.f;
   }
   __syncthreads();
-  // context columns [c0, c0 + kCtxCols): thread = (column, row group of RB)
+  // context columns [c0, c0 + kCtxCols): thread = 2 adjacent columns (float2),
+  // all rows; 8 frames of enc in flight per thread
   const float* eu = enc + (int64_t)u * TM * C;
-  const int col = c0 + (tid % kCtxCols);
-  const int grp = tid / kCtxCols;              // 0..1
-  if (col < C && grp * RB < n) {
-    float acc[RB];
+  const int col = c0 + 2 * tid;
+  if (tid < kCtxCols / 2 && col < C) {
+    const bool pair = col + 1 < C;
+    float acc0[RB], acc1[RB];
 #pragma unroll
-    for (int r = 0; r < RB; ++r) acc[r] = 0.f;
+    for (int r = 0; r < RB; ++r) acc0[r] = acc1[r] = 0.f;
     constexpr int TU = 8;
     int t = 0;
     for (; t + TU <= T; t += TU) {
-      float x[TU];
+      float2 x[TU];
 #pragma unroll
-      for (int j = 0; j < TU; ++j) x[j] = __ldg(eu + (int64_t)(t + j) * C + col);
+      for (int j = 0; j < TU; ++j)
+        x[j] = pair ? __ldg(reinterpret_cast<const float2*>(eu + (int64_t)(t + j) * C + col))
+                    : make_float2(__ldg(eu + (int64_t)(t + j) * C + col), 0.f);
 #pragma unroll
       for (int j = 0; j < TU; ++j) {
         const float4* a4 = reinterpret_cast<const float4*>(at + (t + j) * RB);
 #pragma unroll
         for (int q4 = 0; q4 < RB / 4; ++q4) {
           const float4 w = a4[q4];
-          acc[4 * q4] = fmaf(w.x, x[j], acc[4 * q4]);
-          acc[4 * q4 + 1] = fmaf(w.y, x[j], acc[4 * q4 + 1]);
-          acc[4 * q4 + 2] = fmaf(w.z, x[j], acc[4 * q4 + 2]);
-          acc[4 * q4 + 3] = fmaf(w.w, x[j], acc[4 * q4 + 3]);
+          acc0[4 * q4] = fmaf(w.x, x[j].x, acc0[4 * q4]);
+          acc0[4 * q4 + 1] = fmaf(w.y, x[j].x, acc0[4 * q4 + 1]);
+          acc0[4 * q4 + 2] = fmaf(w.z, x[j].x, acc0[4 * q4 + 2]);
+          acc0[4 * q4 + 3] = fmaf(w.w, x[j].x, acc0[4 * q4 + 3]);
+          acc1[4 * q4] = fmaf(w.x, x[j].y, acc1[4 * q4]);
+          acc1[4 * q4 + 1] = fmaf(w.y, x[j].y, acc1[4 * q4 + 1]);
+          acc1[4 * q4 + 2] = fmaf(w.z, x[j].y, acc1[4 * q4 + 2]);
+          acc1[4 * q4 + 3] = fmaf(w.w, x[j].y, acc1[4 * q4 + 3]);
         }
       }
     }
     for (; t < T; ++t) {
-      const float x = __ldg(eu + (int64_t)t * C + col);
+      const float x0 = __ldg(eu + (int64_t)t * C + col);
+      const float x1 = pair ? __ldg(eu + (int64_t)t * C + col + 1) : 0.f;
 #pragma unroll
-      for (int r = 0; r < RB; ++r) acc[r] = fmaf(at[t * RB + r], x, acc[r]);
+      for (int r = 0; r < RB; ++r) {
+        acc0[r] = fmaf(at[t * RB + r], x0, acc0[r]);
+        acc1[r] = fmaf(at[t * RB + r], x1, acc1[r]);
+      }
     }
-    if (grp == 0) {
 #pragma unroll
-      for (int r = 0; r < RB; ++r)
-        if (r < n) ctx_out[(int64_t)(slot0 + r) * ld_ctx + col] = acc[r];
+    for (int r = 0; r < RB; ++r) {
+      if (r < n) {
+        float* o = ctx_out + (int64_t)(slot0 + r) * ld_ctx + col;
+        o[0] = acc0[r];
+        if (pair) o[1] = acc1[r];
+      }
     }
   }
   if (blockIdx.y != 0) return;
@@ -554,7 +566,8 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
   FB_CHECK_ARG(cfg->beam <= 16, "attention context kernel supports beam <= 16");
   if (num_utts <= 0) return FB_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  const size_t sm_e = sizeof(float) * ((size_t)cfg->beam * att_dim + att_dim);
+  const int RE = (cfg->beam + 1) & ~1;            // rows per energy pass (even)
+  const size_t sm_e = sizeof(float) * ((size_t)RE * att_dim + att_dim);
   const int RB = cfg->beam <= 4 ? 4 : cfg->beam <= 8 ? 8 : cfg->beam <= 12 ? 12 : 16;
   if (cfg->beam > 16) return fail(FB_ERR_CONFIG, "attention context kernel supports beam <= 16");
   const size_t sm_c = sizeof(float) * ((size_t)cfg->beam * cfg->t_max + 4 + (size_t)RB * cfg->t_max);
@@ -562,7 +575,14 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
     return fail(FB_ERR_CONFIG, "attention working set exceeds shared memory");
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(att_energy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(att_energy_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(att_energy_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(att_energy_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(att_energy_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(att_energy_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(att_energy_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(att_energy_kernel<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(att_energy_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(att_context_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(att_context_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(att_context_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -570,8 +590,20 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
     attr_set = true;
   }
   dim3 ge(num_utts, (cfg->t_max + kEnWarps * kEnFrames - 1) / (kEnWarps * kEnFrames));
-  att_energy_kernel<<<ge, kEnWarps * 32, sm_e, s>>>(*cfg, active, n_live, t_enc, keys, att_dim,
-                                                     v, q, ldq, energy_ws);
+#define FB_EN(R)                                                                              \
+  att_energy_kernel<R><<<ge, kEnWarps * 32, sm_e, s>>>(*cfg, active, n_live, t_enc, keys, att_dim, \
+                                                        v, q, ldq, energy_ws)
+  switch (RE) {
+    case 2: FB_EN(2); break;
+    case 4: FB_EN(4); break;
+    case 6: FB_EN(6); break;
+    case 8: FB_EN(8); break;
+    case 10: FB_EN(10); break;
+    case 12: FB_EN(12); break;
+    case 14: FB_EN(14); break;
+    default: FB_EN(16); break;
+  }
+#undef FB_EN
   count_launch();
   int rc = check_launch("att_energy");
   if (rc) return rc;
