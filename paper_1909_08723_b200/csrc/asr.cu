@@ -161,7 +161,7 @@ __device__ double pairwise_sum_d(const double* a, int n, F f) {
 //     rows (cheap) and CTA 0 of the utterance owns the accumulator + coverage.
 constexpr int kEnWarps = 8;
 constexpr int kEnFrames = 4;          // frames per warp
-constexpr int kMaxBeam = 64;
+constexpr int kMaxBeam = 512;
 constexpr int kCtxCols = 128;
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -189,11 +189,12 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
   extern __shared__ float sm[];
   const int K = cfg.beam, TM = cfg.t_max;
   const int n = n_live[u];
+  const int npass = (n + R - 1) / R;
   float* vs = sm;                  // [A]
-  float* qs = sm + A;              // [R][A]  E_q = exp(2 q); rows >= n are 0
+  float* qs = sm + A;              // [npass*R][A]  E_q = exp(2 q); rows >= n are 0
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int slot0 = u * K;
-  for (int j = tid; j < R * A; j += blockDim.x) {
+  for (int j = tid; j < npass * R * A; j += blockDim.x) {
     const int i = j / A, a = j - i * A;
     qs[j] = i < n ? expf(2.0f * q[(int64_t)(slot0 + i) * ldq + a]) : 0.f;
   }
@@ -204,27 +205,30 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
     const int t = t_base + warp * kEnFrames + f;
     if (t >= T) break;
     const float* kt = ku + (int64_t)t * A;
-    float e[R];
+    for (int ps = 0; ps < npass; ++ps) {
+      float e[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) e[r] = 0.f;
-    for (int a = lane; a < A; a += 32) {
-      const float ek = __ldg(kt + a);
-      const float va = vs[a];
-      const float* qa = qs + a;
+      for (int r = 0; r < R; ++r) e[r] = 0.f;
+      for (int a = lane; a < A; a += 32) {
+        const float ek = __ldg(kt + a);
+        const float va = vs[a];
+        const float* qa = qs + (ps * R) * A + a;
 #pragma unroll
-      for (int r = 0; r < R; ++r) e[r] = fmaf(va, rcp_approx(fmaf(ek, qa[r * A], 1.0f)), e[r]);
-    }
+        for (int r = 0; r < R; ++r) e[r] = fmaf(va, rcp_approx(fmaf(ek, qa[r * A], 1.0f)), e[r]);
+      }
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      float x = e[r];
-      for (int off = 16; off; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-      e[r] = x;
-    }
-    if (lane < n && lane < R) {
-      float x = 0.f;
+      for (int r = 0; r < R; ++r) {
+        float x = e[r];
+        for (int off = 16; off; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+        e[r] = x;
+      }
+      const int row = ps * R + lane;
+      if (lane < R && row < n) {
+        float x = 0.f;
 #pragma unroll
-      for (int r = 0; r < R; ++r) x = lane == r ? e[r] : x;
-      energy[(int64_t)(slot0 + lane) * TM + t] = -2.0f * x;
+        for (int r = 0; r < R; ++r) x = lane == r ? e[r] : x;
+        energy[(int64_t)(slot0 + row) * TM + t] = -2.0f * x;
+      }
     }
   }
 }
@@ -277,16 +281,17 @@ att_context_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
     const float inv = 1.0f / s;
     for (int t = lane; t < T; t += 32) a[t] *= inv;
   }
+  const float* eu = enc + (int64_t)u * TM * C;
+  const int col = c0 + 2 * tid;
+  for (int g0 = 0; g0 < n; g0 += RB) {
   __syncthreads();
   for (int j = tid; j < T * RB; j += blockDim.x) {
     const int t = j / RB, r = j % RB;
-    at[j] = r < n ? al[r * T + t] : 0.f;
+    at[j] = g0 + r < n ? al[(g0 + r) * T + t] : 0.f;
   }
   __syncthreads();
   // context columns [c0, c0 + kCtxCols): thread = 2 adjacent columns (float2),
-  // all rows; 8 frames of enc in flight per thread
-  const float* eu = enc + (int64_t)u * TM * C;
-  const int col = c0 + 2 * tid;
+  // rows g0..g0+RB; 8 frames of enc in flight per thread
   if (tid < kCtxCols / 2 && col < C) {
     const bool pair = col + 1 < C;
     float acc0[RB], acc1[RB];
@@ -328,12 +333,13 @@ att_context_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
     }
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
-      if (r < n) {
-        float* o = ctx_out + (int64_t)(slot0 + r) * ld_ctx + col;
+      if (g0 + r < n) {
+        float* o = ctx_out + (int64_t)(slot0 + g0 + r) * ld_ctx + col;
         o[0] = acc0[r];
         if (pair) o[1] = acc1[r];
       }
     }
+  }
   }
   if (blockIdx.y != 0) return;
   // fp64 accumulator + coverage (decoder.py:421-425), one warp per row
@@ -563,13 +569,12 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
                "null attention args");
   FB_CHECK_ARG(cfg->cov_mode == 0 || cov_out, "coverage output required");
   FB_CHECK_ARG(cfg->beam <= kMaxBeam, "beam too large for the attention kernels");
-  FB_CHECK_ARG(cfg->beam <= 16, "attention context kernel supports beam <= 16");
   if (num_utts <= 0) return FB_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  const int RE = (cfg->beam + 1) & ~1;            // rows per energy pass (even)
-  const size_t sm_e = sizeof(float) * ((size_t)RE * att_dim + att_dim);
+  const int RE = cfg->beam >= 16 ? 16 : (cfg->beam + 1) & ~1;   // rows per energy pass
+  const int npass = (cfg->beam + RE - 1) / RE;
+  const size_t sm_e = sizeof(float) * ((size_t)npass * RE * att_dim + att_dim);
   const int RB = cfg->beam <= 4 ? 4 : cfg->beam <= 8 ? 8 : cfg->beam <= 12 ? 12 : 16;
-  if (cfg->beam > 16) return fail(FB_ERR_CONFIG, "attention context kernel supports beam <= 16");
   const size_t sm_c = sizeof(float) * ((size_t)cfg->beam * cfg->t_max + 4 + (size_t)RB * cfg->t_max);
   if (sm_e > 200 * 1024 || sm_c > 200 * 1024)
     return fail(FB_ERR_CONFIG, "attention working set exceeds shared memory");

@@ -131,11 +131,10 @@ __device__ __forceinline__ double step_score(const fb_search_cfg_t& c, const AM*
   return s;
 }
 
-struct SelPlan {
-  int n_sel;
-  int n_new;
-  int fin_new[64];      // finished-pool index per selected eos child (or -1)
-};
+__host__ __device__ inline size_t sel_smem_bytes(int beam, int vocab) {
+  const size_t nv = (size_t)beam * vocab;
+  return 8 * (nv + 2 * (size_t)beam) + 4 * 6 * (size_t)beam + nv;
+}
 
 template <typename AM>
 __global__ void __launch_bounds__(kSelThreads)
@@ -151,16 +150,19 @@ search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict
   const int MT = c.max_tokens;
   const int NV = n * V;
 
+  // dynamic layout: doubles | ints | bytes (any beam; see sel_smem_bytes)
   double* cand = reinterpret_cast<double*>(sm_raw);                    // [NV]
-  unsigned char* taken = sm_raw + sizeof(double) * NV;                 // [NV]
-  __shared__ int gated[64];
-  __shared__ int sel[64];
+  double* new_base = cand + NV;                                        // [K]
+  double* new_total = new_base + K;                                    // [K]
+  int* gated = reinterpret_cast<int*>(new_total + K);                  // [K]
+  int* sel = gated + K;                                                // [K]
+  int* new_par = sel + K;                                              // [K]
+  int* new_tok = new_par + K;                                          // [K]
+  int* fin_slot = new_tok + K;                                         // [K]
+  int* fin_par = fin_slot + K;                                         // [K]
+  unsigned char* taken = reinterpret_cast<unsigned char*>(fin_par + K); // [NV]
   __shared__ Cand wbest[kSelThreads / 32];
   __shared__ int s_nsel, s_stop;
-  // new-row plan
-  __shared__ int new_par[64], new_tok[64];
-  __shared__ double new_base[64], new_total[64];
-  __shared__ int fin_slot[64], fin_par[64];
   __shared__ int n_new, n_fin_new;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -177,8 +179,8 @@ search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict
       }
       if (lane == 0) gated[p] = row[c.eos_id] <= (AM)c.gamma * mx;
     }
-  } else if (tid < 64) {
-    gated[tid] = 0;
+  } else {
+    for (int p = tid; p < n; p += kSelThreads) gated[p] = 0;
   }
   __syncthreads();
 
@@ -388,9 +390,11 @@ spec_select_kernel(fb_search_cfg_t c, fb_search_state_t st, fb_trie_t trie,
   const int n = st.n_live[u];
   const int base = u * K;
   const int NV = n * V;
-  double* cand = reinterpret_cast<double*>(sm_raw);
-  unsigned char* taken = sm_raw + sizeof(double) * NV;
-  __shared__ int gated[64], fin[64], rank_of[64];
+  double* cand = reinterpret_cast<double*>(sm_raw);                    // [NV]
+  int* gated = reinterpret_cast<int*>(cand + NV);                      // [K]
+  int* fin = gated + K;                                                // [K]
+  int* rank_of = fin + K;                                              // [K]
+  unsigned char* taken = reinterpret_cast<unsigned char*>(rank_of + K); // [NV]
   __shared__ Cand wbest[kSelThreads / 32];
   __shared__ double s_thr;
   __shared__ int s_found;
@@ -581,22 +585,23 @@ extern "C" int fb_search_step(const fb_search_cfg_t* cfg, const fb_search_state_
                               int32_t num_utts, const void* am, int64_t am_stride,
                               const double* fusion, int64_t fusion_stride, void* stream) {
   FB_CHECK_ARG(cfg && st && am, "null search arguments");
-  FB_CHECK_ARG(cfg->beam >= 1 && cfg->beam <= 64, "beam must be in [1, 64] on this path");
+  FB_CHECK_ARG(cfg->beam >= 1, "beam must be positive");
   FB_CHECK_ARG(!cfg->has_fusion || fusion, "fusion rows required");
-  const int64_t nv = (int64_t)cfg->beam * cfg->vocab;
-  const size_t smem = (size_t)nv * (sizeof(double) + 1);
-  if (smem > 200 * 1024)
+  const size_t smem = sel_smem_bytes(cfg->beam, cfg->vocab);
+  if (smem > 220 * 1024)
     return fail(FB_ERR_CONFIG, "beam x vocabulary too large for the shared-memory top-k");
   if (num_utts <= 0) return FB_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (cfg->am_f32) {
     auto k = search_step_kernel<float>;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static bool set = false;
+    if (!set) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); set = true; }
     k<<<num_utts, kSelThreads, smem, s>>>(*cfg, *st, (const float*)am, am_stride, fusion,
                                           fusion_stride);
   } else {
     auto k = search_step_kernel<double>;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static bool set = false;
+    if (!set) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); set = true; }
     k<<<num_utts, kSelThreads, smem, s>>>(*cfg, *st, (const double*)am, am_stride, fusion,
                                           fusion_stride);
   }
@@ -616,8 +621,8 @@ extern "C" int fb_spec_select(const fb_search_cfg_t* cfg, const fb_search_state_
                               int32_t* ev_rank, int32_t* ev_slot, int32_t* ev_count,
                               int32_t* row_ev, const int32_t* ev_start, void* stream) {
   FB_CHECK_ARG(cfg && st && trie && am && fusion && ev_count && row_ev, "null spec-select args");
-  const size_t smem = (size_t)cfg->beam * cfg->vocab * (sizeof(double) + 1);
-  if (smem > 200 * 1024) return fail(FB_ERR_CONFIG, "beam x vocabulary too large");
+  const size_t smem = (size_t)cfg->beam * cfg->vocab * 9 + 12 * (size_t)cfg->beam;
+  if (smem > 220 * 1024) return fail(FB_ERR_CONFIG, "beam x vocabulary too large");
   cudaStream_t s = (cudaStream_t)stream;
   if (ev_start)   // events appended after the late events queued by the last step
     cudaMemcpyAsync(ev_count, ev_start, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
@@ -626,13 +631,15 @@ extern "C" int fb_spec_select(const fb_search_cfg_t* cfg, const fb_search_state_
   if (num_utts <= 0) return check_launch("spec_select");
   if (cfg->am_f32) {
     auto k = spec_select_kernel<float>;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static bool set = false;
+    if (!set) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); set = true; }
     k<<<num_utts, kSelThreads, smem, s>>>(*cfg, *st, *trie, trie_state, hist_slot,
                                           (const float*)am, am_stride, fusion, fusion_stride,
                                           ev_row, ev_rank, ev_slot, ev_count, row_ev);
   } else {
     auto k = spec_select_kernel<double>;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static bool set = false;
+    if (!set) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); set = true; }
     k<<<num_utts, kSelThreads, smem, s>>>(*cfg, *st, *trie, trie_state, hist_slot,
                                           (const double*)am, am_stride, fusion, fusion_stride,
                                           ev_row, ev_rank, ev_slot, ev_count, row_ev);

@@ -162,3 +162,27 @@ def test_spec_pruning_is_exact():
             outs.append(dec.run(X, T, ids, record_counts=True))
         for a, b in zip(*outs):
             assert a.tokens == b.tokens and a.score == b.score and a.steps == b.steps
+
+
+@pytest.mark.parametrize("name", ["c1", "c3"])
+def test_baseline_small_configs_match_oracle(name):
+    """BASELINE.json configs[0] (c1: small BiLSTM + 1-layer attn-LSTM, beam 5, no
+    LM) and c3 (c1 + improved coverage + EOS threshold 1.5, beam 20) at their
+    real model sizes, GPU fused engine vs the CPU oracle."""
+    import paper_1909_08723_b200 as fb
+    from paper_1909_08723_b200 import synth
+    from paper_1909_08723_b200.models import AttnLstmScorer
+    wl = synth.WORKLOADS[name]
+    d = fb.TokenDictionary(synth.wsj_token_list())
+    W = synth.asr_weights(wl.asr, seed=wl.seed, eos_id=d.eos_id)
+    utts = synth.synth_fbank(8, seed=wl.seed + 100, frames=wl.frames)
+    cfg = dict(beam_size=wl.beam, lm_weight=0.0, coverage_mode=wl.coverage_mode,
+               coverage_weight=wl.coverage_weight, eos_gamma=wl.eos_gamma)
+    got = fb.decode_batch([fb.FeatureMatrix(u, x) for u, x in utts],
+                          AttnLstmScorer(W, wl.asr, d.eos_id), None, fb.DecodeConfig(**cfg), d)
+    od = OracleDict(synth.wsj_token_list())
+    want = oracle_decode([_Feat(u, x) for u, x in utts],
+                         OracleAttnLstmScorer(W, wl.asr.enc_layers, wl.asr.dec_layers,
+                                              wl.asr.subsample, od.eos_id),
+                         None, OracleConfig(**cfg), od)
+    _compare(got, want, name)
