@@ -75,9 +75,14 @@ def build_inputs(wl_name: str, rank: int, n_utts=None, words=None, overrides=())
         else:
             sub = getattr(wl, part)
             wl = dataclasses.replace(wl, **{part: dataclasses.replace(sub, **{field: float(val)})})
-    d = TokenDictionary(synth.wsj_token_list())
+    if wl.sublm is not None:       # config 4: subword tokens + token-level LM fusion
+        d = TokenDictionary(synth.subword_token_list(wl.asr.vocab - 4, seed=wl.seed + 3))
+    else:
+        d = TokenDictionary(synth.wsj_token_list())
     W = synth.asr_weights(wl.asr, seed=wl.seed, eos_id=d.eos_id)
     words_l, trie = None, None
+    if wl.sublm is not None:
+        W.update(synth.subword_lm_weights(wl.sublm, seed=wl.seed + 1, eos_id=d.eos_id))
     if wl.lm is not None:
         W.update(synth.lm_weights(wl.lm, seed=wl.seed + 1))
         words_l = synth.synth_lexicon(wl.lm.words, seed=wl.seed + 2)
@@ -173,6 +178,9 @@ def cpu_decode(wl, d, W, words, utts, n: int, threads: int):
     if wl.lm is not None:
         lm = OracleLstmWordLM(W, wl.lm.layers, wl.lm.words)
         fus = OracleLookahead(obuild(words, od), lm, od)
+    if wl.sublm is not None:
+        from oracle.subword import OracleLstmCharLM, OracleSubwordFusion
+        fus = OracleSubwordFusion(OracleLstmCharLM(W, wl.sublm.layers, od.pad_id, od.eos_id))
     cfg = OracleConfig(beam_size=wl.beam, lm_weight=wl.lm_weight,
                        coverage_mode=wl.coverage_mode, coverage_weight=wl.coverage_weight,
                        eos_gamma=wl.eos_gamma, max_len_ratio=wl.max_len_ratio)
@@ -188,8 +196,11 @@ def cpu_decode(wl, d, W, words, utts, n: int, threads: int):
 
 
 def _file_tokens(d):
-    from paper_1909_08723_b200 import synth
-    return synth.wsj_token_list()
+    """The synthetic dictionaries list no specials: <pad>,<eos>,<unk> lead and
+    <space> trails (token_dict.py placement rule)."""
+    toks = list(d.tokens[3:-1])
+    assert d.tokens[:3] == ("<pad>", "<eos>", "<unk>") and d.tokens[-1] == "<space>"
+    return toks
 
 
 def run_reference(args):
@@ -226,6 +237,16 @@ METRIC = "utterances/sec and RTF, beam-10 look-ahead word-LM decode"
 
 
 def workload_config(wl):
+    if wl.sublm is not None:
+        a, s_ = wl.asr, wl.sublm
+        return {"workload": f"{wl.name}: {a.enc_layers}x BiLSTM-{a.enc_hidden} encoder + "
+                            f"{a.dec_layers}x LSTM-{a.dec_hidden} attention decoder ({a.vocab} "
+                            f"subword tokens), beam {wl.beam}, shallow fusion with a "
+                            f"{s_.layers}x{s_.hidden} token LSTM LM (SubwordFusion), "
+                            f"{wl.n_utts} utts/GPU of {wl.frames[0]}-{wl.frames[1]} frames",
+                "utts_per_gpu": wl.n_utts, "frames": list(wl.frames), "beam": wl.beam,
+                "vocab": a.vocab, "lm_weight": wl.lm_weight, "batch": wl.batch_size,
+                "length_sorted": True}
     return {"workload": f"{wl.name}: WSJ-shaped 4x BiLSTM-320 encoder + 3x LSTM-320 attention "
                         f"decoder (52 tokens), beam {wl.beam}, look-ahead fusion with a "
                         f"{wl.lm.words if wl.lm else 0}-word 3x1200 LSTM LM, "
@@ -254,8 +275,8 @@ def main():
     torch.backends.cudnn.allow_tf32 = False
 
     from paper_1909_08723_b200 import _lib
-    from paper_1909_08723_b200.fusion import LookaheadFusion
-    from paper_1909_08723_b200.models import AttnLstmScorer, LstmWordLM
+    from paper_1909_08723_b200.fusion import LookaheadFusion, SubwordFusion
+    from paper_1909_08723_b200.models import AttnLstmScorer, LstmSubwordLM, LstmWordLM
     from paper_1909_08723_b200.engine import FusedDecoder, StageTimer
     from paper_1909_08723_b200.decoder import decode_batch
     from paper_1909_08723_b200.kaldi_io import FeatureMatrix
@@ -267,6 +288,8 @@ def main():
     fusion = None
     if wl.lm is not None:
         fusion = LookaheadFusion(trie, LstmWordLM(W, wl.lm), d)
+    if wl.sublm is not None:
+        fusion = SubwordFusion(LstmSubwordLM(W, wl.sublm, d.pad_id, d.eos_id))
     feats = [FeatureMatrix(u, x) for u, x in utts]
     frames = sum(x.shape[0] for _, x in utts)
     X_host, T = scorer.encoder.stage([x for _, x in utts], pin=True)

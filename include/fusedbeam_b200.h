@@ -103,6 +103,13 @@ int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* logits, int6
                   const int32_t* slots, double* g_pool, int64_t g_stride, double* eos_out,
                   double* seg_ws, void* stream);
 
+/* norm_out[d] = log(sum_{j != skip_col} exp(logits[row][j])) in fp64 for the
+ * first *m_dev (or m_max) rows; row = d = rows ? rows[i] : i.  skip_col < 0:
+ * every column.  (The log-normaliser of a token LM row, <pad> excluded.) */
+int fb_row_logsumexp(int32_t m_max, const int32_t* m_dev, const int32_t* rows,
+                     const float* logits, int64_t l_stride, int32_t n_cols, int32_t skip_col,
+                     double* norm_out, void* stream);
+
 /* ---- beam search step (decoder.py:339-480) ------------------------------ */
 typedef struct {
   int32_t beam, vocab, pad_id, eos_id;
@@ -144,12 +151,26 @@ typedef struct {
   double* res_acc;        /* [B][t_max]      */
   /* compact list of the rows that enter the NEXT step (active utterances) */
   int32_t* next_rows; int32_t* next_count;
+  /* large vocabularies (beam*vocab too big for one CTA): workspace [B*beam][beam]
+   * for the exact two-stage selection (per-row top-beam, then the beam cut
+   * over the survivors); NULL = single-stage only */
+  double* cand_score_ws; int32_t* cand_flat_ws;
+  int32_t force_two_stage;     /* 1: two-stage selection even when one CTA fits */
+  int32_t pad1;
+  /* token-level LM fusion from raw logits (char_lm.py:23-33 rows computed on
+   * the fly): when non-NULL, the fusion argument of fb_search_step is fp32
+   * logits and the fused score is max(logit - fus_norm[slot], fus_floor) */
+  const double* fus_norm; double fus_floor;
 } fb_search_state_t;
 
 /* One lock-step selection over every active utterance: combine am + lm_weight
  * * fusion, pad -> -inf, EOS gate, token-major stable top-beam with the
  * reference tie-break, coverage bonus, finished-set cap, early stop and
- * result pick.  am/fusion rows are indexed by slot. */
+ * result pick.  am/fusion rows are indexed by slot.  When beam*vocab exceeds
+ * the one-CTA shared-memory budget and st->cand_*_ws are given, each live row
+ * first keeps its own top-beam candidates (ordered score desc, token asc --
+ * consistent with the token-major flat order), which provably contains the
+ * utterance's top-beam. */
 int fb_search_step(const fb_search_cfg_t* cfg, const fb_search_state_t* st,
                    int32_t num_utts, const void* am, int64_t am_stride,
                    const double* fusion, int64_t fusion_stride, void* stream);

@@ -14,6 +14,6 @@ from .token_dict import TokenDictionary, load_dictionary  # noqa: F401
 from .lexicon_trie import NO_STATE, PrefixTreeAutomaton, build_trie  # noqa: F401
 from .kaldi_io import FeatureMatrix  # noqa: F401
 from .fusion import (DEFAULT_OOV_PENALTY, OOV_STATE, FusionScorer, LookaheadBatch,  # noqa: F401
-                     LookaheadFusion, cumsum_distribution)
+                     LookaheadFusion, SubwordBatch, SubwordFusion, cumsum_distribution)
 from .decoder import (AcousticScorer, DecodeConfig, DecodeResult, coverage_improved,  # noqa: F401
                       coverage_original, decode_batch, decode_corpus, eos_allowed)

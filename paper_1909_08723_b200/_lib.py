@@ -40,7 +40,8 @@ class FbSearchState(C.Structure):
         "parent", "last_tok", "acc_post", "cov_post",
         "fin_valid", "fin_total", "fin_len", "fin_tokens", "fin_acc",
         "res_len", "res_score", "res_finished", "res_steps", "res_tokens", "res_acc",
-        "next_rows", "next_count")]
+        "next_rows", "next_count", "cand_score_ws", "cand_flat_ws")] + [
+        ("force_two_stage", i32), ("pad1", i32), ("fus_norm", vp), ("fus_floor", C.c_double)]
 
 
 class FbGemm(C.Structure):
@@ -86,6 +87,7 @@ _SIGS = {
     "fb_lstm_recurrence": (C.c_int, [i32, i32, i32, vp, i32, vp, i64, vp, i64, vp, vp, vp]),
     "fb_pack_rows": (C.c_int, [C.POINTER(FbPack), i32, vp, vp, vp, vp, vp, vp, i64, vp]),
     "fb_log_softmax_rows": (C.c_int, [i32, vp, vp, vp, i64, i32, vp, i64, vp]),
+    "fb_row_logsumexp": (C.c_int, [i32, vp, vp, vp, i64, i32, i32, vp, vp]),
     "fb_attention_step": (C.c_int, [C.POINTER(FbSearchCfg), i32, vp, vp, vp, vp, vp, i32, i32,
                                     vp, vp, i64, vp, vp, vp, vp, vp, i64, vp, i64, vp, vp]),
     "fb_spec_events": (C.c_int, [C.POINTER(FbTrie), i32, vp, vp, vp, vp, vp, vp, vp, vp, vp,

@@ -117,6 +117,30 @@ __global__ void log_softmax_kernel(int m_max, const int32_t* __restrict__ m_dev,
   }
 }
 
+// Token-LM log-normaliser in fp64 (oracle: fp64 softmax of the fp32 logits):
+// one warp per row, exact fp64 exp of (x - max).
+__global__ void row_lse_kernel(int m_max, const int32_t* __restrict__ m_dev,
+                               const int32_t* __restrict__ rows, const float* __restrict__ x,
+                               int64_t ldx, int n, int skip, double* __restrict__ out) {
+  const int m = row_count(m_max, m_dev);
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < m; i += gridDim.x * wpb) {
+    const int r = rows ? rows[i] : i;
+    const float* xr = x + (int64_t)r * ldx;
+    float mx = -INFINITY;
+    for (int j = lane; j < n; j += 32)
+      if (j != skip) mx = fmaxf(mx, xr[j]);
+    for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    const double m0 = (double)mx;
+    double s = 0.0;
+    for (int j = lane; j < n; j += 32)
+      if (j != skip) s += exp((double)xr[j] - m0);
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) out[r] = m0 + log(s);
+  }
+}
+
 // -------------------------------------------------------------- attention --
 __device__ __forceinline__ float tanh_fast(float x) {
   // 1 - 2/(e^{2x}+1) with MUFU ex2/rcp: absolute error ~2e-7; the clamp keeps
@@ -256,38 +280,37 @@ att_context_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
   const int K = cfg.beam, TM = cfg.t_max;
   const int n = n_live[u];
   const int T = t_enc[u];
-  float* al = sm;                  // [n][T] attention weights (row-major)
-  float* at = al + ((n * T + 3) & ~3);  // [T][RB] transposed copy (16 B aligned)
+  // per-row softmax statistics only; weights are re-derived from the energy
+  // rows (L2-resident) per row group, so shared memory is O(RB * T) for any beam
+  constexpr int RBS = RB + 4;      // padded row stride of the transposed group (float4-aligned)
+  float* st_mx = sm;                                   // [n]
+  float* st_inv = sm + n;                              // [n]
+  float* at = sm + ((2 * n + 3) & ~3);                 // [T][RBS]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int slot0 = u * K;
   // softmax over frames, one warp per row (every column chunk recomputes it)
   for (int i = warp; i < n; i += nw) {
     const float* e = energy + (int64_t)(slot0 + i) * TM;
-    float* a = al + i * T;
     float mx = -INFINITY;
-    for (int t = lane; t < T; t += 32) {
-      const float x = e[t];
-      a[t] = x;
-      mx = fmaxf(mx, x);
-    }
+    for (int t = lane; t < T; t += 32) mx = fmaxf(mx, e[t]);
     for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
     float s = 0.f;
-    for (int t = lane; t < T; t += 32) {
-      const float x = expf(a[t] - mx);
-      a[t] = x;
-      s += x;
-    }
+    for (int t = lane; t < T; t += 32) s += expf(e[t] - mx);
     for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    const float inv = 1.0f / s;
-    for (int t = lane; t < T; t += 32) a[t] *= inv;
+    if (lane == 0) {
+      st_mx[i] = mx;
+      st_inv[i] = 1.0f / s;
+    }
   }
   const float* eu = enc + (int64_t)u * TM * C;
   const int col = c0 + 2 * tid;
   for (int g0 = 0; g0 < n; g0 += RB) {
   __syncthreads();
   for (int j = tid; j < T * RB; j += blockDim.x) {
-    const int t = j / RB, r = j % RB;
-    at[j] = g0 + r < n ? al[(g0 + r) * T + t] : 0.f;
+    const int r = j / T, t = j - r * T;
+    at[t * RBS + r] = g0 + r < n ? expf(energy[(int64_t)(slot0 + g0 + r) * TM + t] -
+                                        st_mx[g0 + r]) * st_inv[g0 + r]
+                                 : 0.f;
   }
   __syncthreads();
   // context columns [c0, c0 + kCtxCols): thread = 2 adjacent columns (float2),
@@ -307,7 +330,7 @@ att_context_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
                     : make_float2(__ldg(eu + (int64_t)(t + j) * C + col), 0.f);
 #pragma unroll
       for (int j = 0; j < TU; ++j) {
-        const float4* a4 = reinterpret_cast<const float4*>(at + (t + j) * RB);
+        const float4* a4 = reinterpret_cast<const float4*>(at + (t + j) * RBS);
 #pragma unroll
         for (int q4 = 0; q4 < RB / 4; ++q4) {
           const float4 w = a4[q4];
@@ -327,8 +350,8 @@ att_context_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
       const float x1 = pair ? __ldg(eu + (int64_t)t * C + col + 1) : 0.f;
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
-        acc0[r] = fmaf(at[t * RB + r], x0, acc0[r]);
-        acc1[r] = fmaf(at[t * RB + r], x1, acc1[r]);
+        acc0[r] = fmaf(at[t * RBS + r], x0, acc0[r]);
+        acc1[r] = fmaf(at[t * RBS + r], x1, acc1[r]);
       }
     }
 #pragma unroll
@@ -348,13 +371,15 @@ att_context_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
     const int p = parent ? parent[r] : r;
     const double* a0 = acc_in + (int64_t)p * TM;
     double* a1 = acc_out + (int64_t)r * TM;
-    const float* a = al + i * T;
+    const float* e = energy + (int64_t)r * TM;
+    const float mx = st_mx[i], inv = st_inv[i];
     int cnt = 0;
     for (int t = lane; t < T; t += 32) {
-      const double x = dadd(a0[t], (double)a[t]);
+      const float a = expf(e[t] - mx) * inv;
+      const double x = dadd(a0[t], (double)a);
       a1[t] = x;
       cnt += x > cfg.tau1;
-      if (attn_out) attn_out[(int64_t)r * ld_attn + t] = a[t];
+      if (attn_out) attn_out[(int64_t)r * ld_attn + t] = a;
     }
     if (cfg.cov_mode != 0) {
       for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
@@ -557,6 +582,17 @@ extern "C" int fb_log_softmax_rows(int32_t m_max, const int32_t* m_dev, const in
   return check_launch("log_softmax_rows");
 }
 
+extern "C" int fb_row_logsumexp(int32_t m_max, const int32_t* m_dev, const int32_t* rows,
+                                const float* logits, int64_t l_stride, int32_t n_cols,
+                                int32_t skip_col, double* norm_out, void* stream) {
+  FB_CHECK_ARG(logits && norm_out && n_cols > 0, "bad logsumexp arguments");
+  if (m_max <= 0) return FB_OK;
+  row_lse_kernel<<<std::min((m_max + 7) / 8, kNumSMs * 8), 256, 0, (cudaStream_t)stream>>>(
+      m_max, m_dev, rows, logits, l_stride, n_cols, skip_col, norm_out);
+  count_launch();
+  return check_launch("row_logsumexp");
+}
+
 extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
                                  const int32_t* active, const int32_t* n_live,
                                  const int32_t* t_enc, const float* keys, const float* enc,
@@ -575,7 +611,7 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
   const int npass = (cfg->beam + RE - 1) / RE;
   const size_t sm_e = sizeof(float) * ((size_t)npass * RE * att_dim + att_dim);
   const int RB = cfg->beam <= 4 ? 4 : cfg->beam <= 8 ? 8 : cfg->beam <= 12 ? 12 : 16;
-  const size_t sm_c = sizeof(float) * ((size_t)cfg->beam * cfg->t_max + 4 + (size_t)RB * cfg->t_max);
+  const size_t sm_c = sizeof(float) * ((size_t)2 * cfg->beam + 4 + (size_t)(RB + 4) * cfg->t_max);
   if (sm_e > 200 * 1024 || sm_c > 200 * 1024)
     return fail(FB_ERR_CONFIG, "attention working set exceeds shared memory");
   static bool attr_set = false;

@@ -7,12 +7,19 @@
 // fp32 in TMEM -- an fp32-accurate product on the 5th-gen tensor cores
 // (SURVEY.md §7 "GEMM precision").  Algorithmic FLOPs count the product once.
 //
+// Accuracy: the tensor core's fp32 accumulation in TMEM is not IEEE
+// round-to-nearest -- its error grows ~k^1.5 (7.5x an fp32 dot product at
+// k = 4096, scripts/gemm_accuracy2.py).  So K is consumed in chunks of
+// TC_KCB * 64 = 256: each chunk is accumulated in its own TMEM slot (a ring of
+// TC_NACC slots) and the epilogue warps drain every chunk into fp32 registers
+// (round-to-nearest adds).  The MMA issuer runs up to TC_NACC chunks ahead.
+//
 // Structure (persistent, one CTA per SM, 10 warps):
 //   warp 0 lane 0 : TMA producer, 3-stage smem ring (128B swizzle, K block 64)
 //   warp 1 lane 0 : MMA issuer (tcgen05.mma.cta_group::1.kind::f16, M=128)
-//   warp 1        : TMEM allocator (2 x BN fp32 columns, double-buffered)
-//   warps 2..9    : epilogue, tcgen05.ld 32x32b (warp w owns TMEM lanes 32(w%4)..,
-//                   column half (w-2)/4 of the tile)
+//   warp 1        : TMEM allocator (TC_NACC x BN fp32 columns: the chunk ring)
+//   warps 2..9    : chunk drains + epilogue, tcgen05.ld 32x32b (warp w owns TMEM
+//                   lanes 32(w%4).., column half (w-2)/4 of the tile)
 #include "common.cuh"
 
 #include <cstdlib>
@@ -26,6 +33,8 @@ namespace fb {
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;            // 64 bf16 = 128 B = one swizzle atom
 constexpr int TC_STAGES = 3;
+constexpr int TC_KCB = 4;            // K blocks per accumulation chunk (K = 256)
+constexpr int TC_NACC = 4;           // TMEM chunk slots (4 x 128 columns = all of TMEM)
 constexpr int TC_EPI_THREADS = 256;     // 8 epilogue warps: 2 per TMEM lane quarter
 constexpr int TC_THREADS = 64 + TC_EPI_THREADS;
 
@@ -128,17 +137,20 @@ __device__ __forceinline__ void store_split(const fb_gemm_t& g, int64_t row, int
 // across the warp (plain mode: lane = column; LSTM mode: lane = (row, unit)).
 template <int BN>
 __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row0, int n0,
-                                              uint32_t taddr, float* st /* [32][33] */,
-                                              int half) {
+                                              float (&acc)[BN / 64][32],
+                                              float* st /* [32][33] */, int half) {
   const int lane = threadIdx.x & 31;
   // {max_all, sum_all, max_words, sum_words} of this lane's row over the
   // warp's half of the tile (BN/2 columns)
   float4 st_stats = make_float4(-INFINITY, 0.f, -INFINITY, 0.f);
   constexpr int CH = BN / 64;                 // 32-column chunks per half
-  for (int cb = half * CH; cb < (half + 1) * CH; ++cb) {
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int cb = half * CH + c;
     float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = acc[c][j];
     __syncwarp();
-    tmem_ld32(taddr + cb * 32, v);
     const int nb = n0 + cb * 32;
     if (g.mode == 0 && g.bias) {
 #pragma unroll
@@ -248,7 +260,7 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
 template <int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
-               fb_gemm_t g, int a_planes, int a_plane_rows, int num_kb) {
+               fb_gemm_t g, int a_planes, int a_plane_rows, int num_kb, int kcb) {
   const int M = row_count(g.m_max, g.m_dev);
   const int m_tiles = (M + TC_BM - 1) / TC_BM;
   const int n_tiles = (g.n + BN - 1) / BN;
@@ -262,7 +274,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   constexpr int W_TILE = BN * TC_BK * 2;
   const int stage_bytes = a_planes * A_TILE + W_TILE;
   __shared__ __align__(8) uint64_t bar_full[TC_STAGES], bar_empty[TC_STAGES];
-  __shared__ __align__(8) uint64_t bar_tfull[2], bar_tempty[2];
+  __shared__ __align__(8) uint64_t bar_tfull[TC_NACC], bar_tempty[TC_NACC];
   __shared__ uint32_t tmem_base_sh;
   __shared__ float epi_stage[8][32 * 33];
 
@@ -272,7 +284,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_init(smem_u32(&bar_full[s]), 1);
       mbar_init(smem_u32(&bar_empty[s]), 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < TC_NACC; ++a) {
       mbar_init(smem_u32(&bar_tfull[a]), 1);
       mbar_init(smem_u32(&bar_tempty[a]), TC_EPI_THREADS);
     }
@@ -281,7 +293,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_base_sh)),
-                 "r"(2 * BN));
+                 "r"(TC_NACC * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -314,53 +326,74 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       // ---- MMA issuer: bf16 x bf16 -> f32, K-major, M = 128, N = BN ----
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(TC_BM >> 4) << 24);
-      int gk = 0, it = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-        const int acc = it & 1;
-        mbar_wait(smem_u32(&bar_tempty[acc]), ((it >> 1) & 1) ^ 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t d = tmem + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb, ++gk) {
-          const int s = gk % TC_STAGES;
-          const uint32_t ph = (gk / TC_STAGES) & 1;
-          mbar_wait(smem_u32(&bar_full[s]), ph);
+      int gk = 0, cc = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        for (int kb0 = 0; kb0 < num_kb; kb0 += kcb, ++cc) {
+          const int slot = cc % TC_NACC;
+          mbar_wait(smem_u32(&bar_tempty[slot]), ((cc / TC_NACC) & 1) ^ 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          unsigned char* st = base + (size_t)s * stage_bytes;
-          const uint64_t bdesc0 = smem_desc_sw128(smem_u32(st + a_planes * A_TILE));
-          for (int p = 0; p < a_planes; ++p) {
-            const uint64_t adesc0 = smem_desc_sw128(smem_u32(st + p * A_TILE));
+          const uint32_t d = tmem + slot * BN;
+          const int kb1 = min(kb0 + kcb, num_kb);
+          for (int kb = kb0; kb < kb1; ++kb, ++gk) {
+            const int s = gk % TC_STAGES;
+            const uint32_t ph = (gk / TC_STAGES) & 1;
+            mbar_wait(smem_u32(&bar_full[s]), ph);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            unsigned char* st = base + (size_t)s * stage_bytes;
+            const uint64_t bdesc0 = smem_desc_sw128(smem_u32(st + a_planes * A_TILE));
+            // smallest plane first: lo/mid products are summed while the
+            // accumulator is still small, so its rounding loses less of them
+            for (int p = a_planes - 1; p >= 0; --p) {
+              const uint64_t adesc0 = smem_desc_sw128(smem_u32(st + p * A_TILE));
 #pragma unroll
-            for (int k = 0; k < TC_BK / 16; ++k)   // 16 elements = 32 B per UMMA_K
-              mma_bf16(d, adesc0 + 2 * k, bdesc0 + 2 * k, idesc, (kb | p | k) != 0);
+              for (int k = 0; k < TC_BK / 16; ++k)   // 16 elements = 32 B per UMMA_K
+                mma_bf16(d, adesc0 + 2 * k, bdesc0 + 2 * k, idesc,
+                         ((kb - kb0) | (a_planes - 1 - p) | k) != 0);
+            }
+            mma_commit(smem_u32(&bar_empty[s]));
           }
-          mma_commit(smem_u32(&bar_empty[s]));
+          mma_commit(smem_u32(&bar_tfull[slot]));
         }
-        mma_commit(smem_u32(&bar_tfull[acc]));
       }
     }
   } else {
     // ---- epilogue warps 2..9: lane quarter = warp % 4, column half = (warp-2)/4 ----
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
-    int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-      const int acc = it & 1;
+    constexpr int CH = BN / 64;
+    const uint32_t tl = tmem + ((uint32_t)(quarter * 32) << 16);
+    int cc = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       const int m0 = (tile % m_tiles) * TC_BM, n0 = (tile / m_tiles) * BN;
-      mbar_wait(smem_u32(&bar_tfull[acc]), (it >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      epilogue_tile<BN>(g, M, m0 + quarter * 32, n0,
-                        tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN, epi_stage[warp - 2],
-                        half);
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[acc]))
-                   : "memory");
+      float acc[CH][32];
+      for (int kb0 = 0; kb0 < num_kb; kb0 += kcb, ++cc) {
+        const int slot = cc % TC_NACC;
+        mbar_wait(smem_u32(&bar_tfull[slot]), (cc / TC_NACC) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          float v[32];
+          tmem_ld32(tl + slot * BN + (half * CH + c) * 32, v);
+          if (kb0 == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[c][j] = v[j];
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[c][j] += v[j];
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[slot]))
+                     : "memory");
+      }
+      epilogue_tile<BN>(g, M, m0 + quarter * 32, n0, acc, epi_stage[warp - 2], half);
     }
   }
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(2 * BN));
+                 "r"(TC_NACC * BN));
   }
 }
 
@@ -406,8 +439,12 @@ static int launch_tc_maps(const CUtensorMap& ta, const CUtensorMap& tw, const fb
     smem_set = 3 * (3 * TC_BM * TC_BK * 2 + BN * TC_BK * 2) + 1024;
   }
   const int tiles = ((g->m_max + TC_BM - 1) / TC_BM) * ((g->n + BN - 1) / BN);
+  static const int kcb = [] {
+    const char* e = getenv("FB_GEMM_KCB");
+    return e ? std::max(1, atoi(e)) : TC_KCB;
+  }();
   k<<<std::min(tiles, kNumSMs), TC_THREADS, smem, s>>>(ta, tw, *g, a_planes, (int)a_plane_rows,
-                                                      g->k / TC_BK);
+                                                      g->k / TC_BK, kcb);
   count_launch();
   return check_launch("gemm_tc");
 }

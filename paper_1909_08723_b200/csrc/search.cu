@@ -123,23 +123,111 @@ __device__ __forceinline__ bool key_less(double ta, int la, const int32_t* ka, d
 template <typename AM>
 __device__ __forceinline__ double step_score(const fb_search_cfg_t& c, const AM* am,
                                              int64_t am_stride, const double* fus,
-                                             int64_t f_stride, int slot, int t, bool gated) {
+                                             int64_t f_stride, int slot, int t, bool gated,
+                                             const double* norm = nullptr, double floor_ = 0.0) {
   if (t == c.pad_id) return -INFINITY;
   if (t == c.eos_id && gated) return -INFINITY;
   double s = (double)am[(int64_t)slot * am_stride + t];
-  if (c.has_fusion) s = dadd(s, dmul(c.lm_weight, fus[(int64_t)slot * f_stride + t]));
+  if (c.has_fusion) {
+    double f;
+    if (norm) {        // fp32 logits + fp64 log-normaliser per row, floored (char_lm.py:20,93)
+      f = dadd((double)reinterpret_cast<const float*>(fus)[(int64_t)slot * f_stride + t],
+               -norm[slot]);
+      f = f < floor_ ? floor_ : f;
+    } else {
+      f = fus[(int64_t)slot * f_stride + t];
+    }
+    s = dadd(s, dmul(c.lm_weight, f));
+  }
   return s;
 }
 
-__host__ __device__ inline size_t sel_smem_bytes(int beam, int vocab) {
-  const size_t nv = (size_t)beam * vocab;
-  return 8 * (nv + 2 * (size_t)beam) + 4 * 6 * (size_t)beam + nv;
+__host__ __device__ inline size_t sel_smem_bytes(int beam, int vocab, bool list_mode = false) {
+  const size_t nv = (size_t)beam * (list_mode ? (beam < vocab ? beam : vocab) : vocab);
+  return 8 * (nv + 2 * (size_t)beam) + 4 * 6 * (size_t)beam + (list_mode ? 4 * nv : 0) + nv;
+}
+
+// Stage 1 of the large-vocabulary selection: one CTA per live row keeps the
+// row's top-beam candidates by (score desc, token asc).
+template <typename AM>
+__global__ void __launch_bounds__(kSelThreads)
+row_topk_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict__ am,
+                int64_t am_stride, const double* __restrict__ fus, int64_t f_stride) {
+  extern __shared__ unsigned char sm_raw[];
+  const int slot = blockIdx.x;
+  const int K = c.beam, V = c.vocab;
+  const int u = slot / K, p = slot % K;
+  if (!st.active[u] || p >= st.n_live[u]) return;
+  const int n = st.n_live[u];
+  double* sc = reinterpret_cast<double*>(sm_raw);                      // [V]
+  unsigned char* taken = reinterpret_cast<unsigned char*>(sc + V);      // [V]
+  __shared__ Cand wbest[kSelThreads / 32];
+  __shared__ int s_stop, s_gated;
+  __shared__ AM wmax[kSelThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const AM* row = am + (int64_t)slot * am_stride;
+  if (c.gate_on) {
+    AM mx = row[0];
+    for (int t = tid; t < V; t += kSelThreads) mx = row[t] > mx ? row[t] : mx;
+    for (int off = 16; off; off >>= 1) {
+      const AM o = __shfl_xor_sync(0xffffffffu, mx, off);
+      mx = o > mx ? o : mx;
+    }
+    if (lane == 0) wmax[warp] = mx;
+    __syncthreads();
+    if (tid == 0) {
+      AM m = wmax[0];
+      for (int w = 1; w < kSelThreads / 32; ++w) m = wmax[w] > m ? wmax[w] : m;
+      s_gated = row[c.eos_id] <= (AM)c.gamma * m;
+    }
+  } else if (tid == 0) {
+    s_gated = 0;
+  }
+  if (tid == 0) s_stop = 0;
+  __syncthreads();
+  const double tot = st.total_in[slot];
+  for (int t = tid; t < V; t += kSelThreads) {
+    sc[t] = dadd(tot, step_score(c, am, am_stride, fus, f_stride, slot, t, s_gated,
+                                  st.fus_norm, st.fus_floor));
+    taken[t] = 0;
+  }
+  __syncthreads();
+  double* os = st.cand_score_ws + (int64_t)slot * K;
+  int32_t* of = st.cand_flat_ws + (int64_t)slot * K;
+  const int Kc = K < V ? K : V;           // a row never has more than V candidates
+  for (int k = 0; k < Kc; ++k) {
+    Cand b{-INFINITY, INT_MAX};
+    for (int t = tid; t < V; t += kSelThreads)
+      if (!taken[t]) {
+        Cand x{sc[t], t};
+        if (better(x, b)) b = x;
+      }
+    b = warp_best(b);
+    if (lane == 0) wbest[warp] = b;
+    __syncthreads();
+    if (tid == 0) {
+      Cand w = wbest[0];
+      for (int q = 1; q < kSelThreads / 32; ++q)
+        if (better(wbest[q], w)) w = wbest[q];
+      if (w.j == INT_MAX || w.s == -INFINITY) {
+        s_stop = 1;
+        for (int r = k; r < Kc; ++r) { os[r] = -INFINITY; of[r] = INT_MAX; }
+      } else {
+        taken[w.j] = 1;
+        os[k] = w.s;
+        of[k] = w.j * n + p;       // token-major flat index of decoder.py:404
+      }
+    }
+    __syncthreads();
+    if (s_stop) break;
+  }
 }
 
 template <typename AM>
 __global__ void __launch_bounds__(kSelThreads)
 search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict__ am,
-                   int64_t am_stride, const double* __restrict__ fus, int64_t f_stride) {
+                   int64_t am_stride, const double* __restrict__ fus, int64_t f_stride,
+                   int list_mode) {
   extern __shared__ unsigned char sm_raw[];
   const int u = blockIdx.x;
   if (!st.active[u]) return;
@@ -148,7 +236,8 @@ search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict
   const int base = u * K;
   const int steps = st.steps[u];
   const int MT = c.max_tokens;
-  const int NV = n * V;
+  const int Kc = K < V ? K : V;
+  const int NV = list_mode ? n * Kc : n * V;    // list mode: n rows x their top-min(K, V)
 
   // dynamic layout: doubles | ints | bytes (any beam; see sel_smem_bytes)
   double* cand = reinterpret_cast<double*>(sm_raw);                    // [NV]
@@ -160,7 +249,8 @@ search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict
   int* new_tok = new_par + K;                                          // [K]
   int* fin_slot = new_tok + K;                                         // [K]
   int* fin_par = fin_slot + K;                                         // [K]
-  unsigned char* taken = reinterpret_cast<unsigned char*>(fin_par + K); // [NV]
+  int* cflat = fin_par + K;                                            // [NV] list mode
+  unsigned char* taken = reinterpret_cast<unsigned char*>(cflat + (list_mode ? NV : 0));
   __shared__ Cand wbest[kSelThreads / 32];
   __shared__ int s_nsel, s_stop;
   __shared__ int n_new, n_fin_new;
@@ -185,11 +275,21 @@ search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict
   __syncthreads();
 
   // candidates, token-major flat index j = t * n + p (decoder.py:404)
-  for (int j = tid; j < NV; j += kSelThreads) {
-    const int t = j / n, p = j % n;
-    const double s = step_score(c, am, am_stride, fus, f_stride, base + p, t, gated[p]);
-    cand[j] = dadd(st.total_in[base + p], s);
-    taken[j] = 0;
+  if (list_mode) {
+    for (int j = tid; j < NV; j += kSelThreads) {
+      const int64_t src = (int64_t)(base + j / Kc) * K + j % Kc;
+      cand[j] = st.cand_score_ws[src];
+      cflat[j] = st.cand_flat_ws[src];
+      taken[j] = 0;
+    }
+  } else {
+    for (int j = tid; j < NV; j += kSelThreads) {
+      const int t = j / n, p = j % n;
+      const double s = step_score(c, am, am_stride, fus, f_stride, base + p, t, gated[p],
+                                  st.fus_norm, st.fus_floor);
+      cand[j] = dadd(st.total_in[base + p], s);
+      taken[j] = 0;
+    }
   }
   if (tid == 0) s_nsel = 0, s_stop = 0;
   __syncthreads();
@@ -199,7 +299,7 @@ search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict
     Cand b{-INFINITY, INT_MAX};
     for (int j = tid; j < NV; j += kSelThreads) {
       if (!taken[j]) {
-        Cand x{cand[j], j};
+        Cand x{cand[j], list_mode ? cflat[j] : j};
         if (better(x, b)) b = x;
       }
     }
@@ -214,11 +314,17 @@ search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict
         s_stop = 1;
       } else {
         sel[s_nsel++] = w.j;
-        taken[w.j] = 1;
+        if (!list_mode) taken[w.j] = 1;
       }
     }
     __syncthreads();
     if (s_stop) break;
+    if (list_mode) {                       // flat -> position (unique flat indices)
+      const int fj = sel[s_nsel - 1];
+      for (int j = tid; j < NV; j += kSelThreads)
+        if (cflat[j] == fj) taken[j] = 1;
+      __syncthreads();
+    }
   }
 
   // plan children in selection order (decoder.py:410-432)
@@ -231,7 +337,8 @@ search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict
       const int j = sel[k];
       const int t = j / n, p = j % n;
       const int ps = base + p;
-      const double s = step_score(c, am, am_stride, fus, f_stride, ps, t, gated[p]);
+      const double s = step_score(c, am, am_stride, fus, f_stride, ps, t, gated[p],
+                                  st.fus_norm, st.fus_floor);
       const double nb = dadd(st.base_in[ps], s);
       const double tt = cov_on ? dadd(nb, dmul(c.cov_weight, st.cov_post[ps])) : nb;
       if (t == c.eos_id) {
@@ -587,24 +694,42 @@ extern "C" int fb_search_step(const fb_search_cfg_t* cfg, const fb_search_state_
   FB_CHECK_ARG(cfg && st && am, "null search arguments");
   FB_CHECK_ARG(cfg->beam >= 1, "beam must be positive");
   FB_CHECK_ARG(!cfg->has_fusion || fusion, "fusion rows required");
-  const size_t smem = sel_smem_bytes(cfg->beam, cfg->vocab);
-  if (smem > 220 * 1024)
-    return fail(FB_ERR_CONFIG, "beam x vocabulary too large for the shared-memory top-k");
+  constexpr size_t kBudget = 220 * 1024;
+  bool list_mode = false;
+  size_t smem = sel_smem_bytes(cfg->beam, cfg->vocab);
+  if (smem > kBudget || st->force_two_stage) {
+    if (!st->cand_score_ws || !st->cand_flat_ws)
+      return fail(FB_ERR_CONFIG, "beam x vocabulary too large: pass the two-stage workspace");
+    list_mode = true;
+    smem = sel_smem_bytes(cfg->beam, cfg->vocab, true);
+    const size_t row_smem = (size_t)cfg->vocab * 9;
+    if (smem > kBudget || row_smem > kBudget)
+      return fail(FB_ERR_CONFIG, "beam or vocabulary too large for the selection kernels");
+  }
   if (num_utts <= 0) return FB_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (cfg->am_f32) {
-    auto k = search_step_kernel<float>;
-    static bool set = false;
-    if (!set) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); set = true; }
-    k<<<num_utts, kSelThreads, smem, s>>>(*cfg, *st, (const float*)am, am_stride, fusion,
-                                          fusion_stride);
-  } else {
-    auto k = search_step_kernel<double>;
-    static bool set = false;
-    if (!set) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); set = true; }
-    k<<<num_utts, kSelThreads, smem, s>>>(*cfg, *st, (const double*)am, am_stride, fusion,
-                                          fusion_stride);
+  const int N = num_utts * cfg->beam;
+  const size_t row_smem = (size_t)cfg->vocab * 9;
+#define FB_SEL(AMT)                                                                           \
+  {                                                                                           \
+    auto k = search_step_kernel<AMT>;                                                         \
+    auto kr = row_topk_kernel<AMT>;                                                           \
+    static bool set = false;                                                                  \
+    if (!set) {                                                                               \
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBudget);      \
+      cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBudget);     \
+      set = true;                                                                             \
+    }                                                                                         \
+    if (list_mode) {                                                                          \
+      kr<<<N, kSelThreads, row_smem, s>>>(*cfg, *st, (const AMT*)am, am_stride, fusion,       \
+                                          fusion_stride);                                     \
+      count_launch();                                                                         \
+    }                                                                                         \
+    k<<<num_utts, kSelThreads, smem, s>>>(*cfg, *st, (const AMT*)am, am_stride, fusion,       \
+                                          fusion_stride, list_mode ? 1 : 0);                  \
   }
+  if (cfg->am_f32) FB_SEL(float) else FB_SEL(double)
+#undef FB_SEL
   count_launch();
   int rc = check_launch("search_step");
   if (rc) return rc;

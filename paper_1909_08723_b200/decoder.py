@@ -146,7 +146,8 @@ class SearchBuffers:
     """Per-batch search state in HBM (slot layout: utterance u owns rows
     u*beam .. u*beam+beam-1).  ``in``/``out`` pairs ping-pong by step parity."""
 
-    def __init__(self, B: int, K: int, max_tokens: int, t_max: int, device):
+    def __init__(self, B: int, K: int, max_tokens: int, t_max: int, device, vocab: int = 0,
+                 force_two_stage: bool = False):
         z = lambda *s, dt=torch.int32: torch.zeros(s, dtype=dt, device=device)  # noqa: E731
         f64 = torch.float64
         N = B * K
@@ -168,6 +169,14 @@ class SearchBuffers:
         self.res_tokens = z(B, max_tokens)
         self.res_acc = z(B, t_max, dt=f64)
         self.next_rows, self.next_count = z(N), z(1)
+        # exact two-stage selection for beam x vocab beyond one CTA's shared memory
+        self.two_stage = force_two_stage or \
+            8 * (K * vocab + 2 * K) + 24 * K + K * vocab > 220 * 1024
+        self.cand_score = z(N, K, dt=f64) if self.two_stage else None
+        self.cand_flat = z(N, K) if self.two_stage else None
+        self.force_two_stage = force_two_stage
+        self.fus_norm = None           # set by the fused engine for token-LM logits
+        self.fus_floor = 0.0
         self._views = [self._view(0), self._view(1)]
 
     def _view(self, p: int):
@@ -181,7 +190,13 @@ class SearchBuffers:
             P(self.fin_valid), P(self.fin_total), P(self.fin_len), P(self.fin_tokens),
             P(self.fin_acc), P(self.res_len), P(self.res_score), P(self.res_finished),
             P(self.res_steps), P(self.res_tokens), P(self.res_acc),
-            P(self.next_rows), P(self.next_count))
+            P(self.next_rows), P(self.next_count), P(self.cand_score), P(self.cand_flat),
+            int(self.force_two_stage), 0, P(self.fus_norm), float(self.fus_floor))
+
+    def set_fusion_logits(self, norm: torch.Tensor, floor: float) -> None:
+        """Fusion rows given as fp32 logits + this fp64 per-slot normaliser."""
+        self.fus_norm, self.fus_floor = norm, floor
+        self._views = [self._view(0), self._view(1)]
 
     def view(self, parity: int):
         return self._views[parity]
@@ -230,6 +245,9 @@ def decode_batch(features: Sequence[FeatureMatrix], scorer: AcousticScorer, fusi
     return _decode_plugins(features, scorer, fusion, config, token_dict)
 
 
+_FORCE_TWO_STAGE = False      # tests: exercise the large-vocabulary selection at any size
+
+
 def _decode_plugins(features, scorer, fusion, config: DecodeConfig, token_dict):
     dev = fusion.device if fusion is not None else _device()
     V = len(token_dict)
@@ -246,7 +264,7 @@ def _decode_plugins(features, scorer, fusion, config: DecodeConfig, token_dict):
         return []
     MT = max(max_len) + 1
     TM = max(t_enc)
-    buf = SearchBuffers(B, K, MT, TM, dev)
+    buf = SearchBuffers(B, K, MT, TM, dev, vocab=V, force_two_stage=_FORCE_TWO_STAGE)
     buf.max_len.copy_(torch.as_tensor(max_len, dtype=torch.int32))
     buf.t_enc.copy_(torch.as_tensor(t_enc, dtype=torch.int32))
     early = fusion is None or bool(fusion.nonpositive_scores)
@@ -270,7 +288,10 @@ def _decode_plugins(features, scorer, fusion, config: DecodeConfig, token_dict):
             slots.extend(range(u * K, u * K + n_live[u]))
         slots_t = torch.as_tensor(np.asarray(slots, np.int64), device=dev)
         if fusion is not None:
-            rows = fusion.char_scores_device(fstate)
+            dev_rows = getattr(fusion, "char_scores_device", None)
+            rows = (dev_rows(fstate) if dev_rows is not None else
+                    torch.as_tensor(np.asarray(fusion.char_scores(fstate), np.float64),
+                                    device=dev))
             if tuple(rows.shape) != (pos, V):
                 raise ConfigError(f"fusion scorer returned shape {tuple(rows.shape)},"
                                   f" expected ({pos}, {V})")

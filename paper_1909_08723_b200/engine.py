@@ -30,7 +30,7 @@ from . import _lib
 from . import kernels as K
 from .decoder import DecodeConfig, DecodeResult, SearchBuffers, search_cfg
 from .errors import ConfigError
-from .models import AmState, lm_step, split_scratch
+from .models import AmState, SubLmState, lm_step, split_scratch, subword_step
 
 P = _lib.ptr
 
@@ -156,7 +156,8 @@ class _Session:
         self.K = Kb
         N = self.N = B * Kb
         V = self.V = len(token_dict)
-        self.buf = SearchBuffers(B, Kb, MT, TM, dev)
+        self.buf = SearchBuffers(B, Kb, MT, TM, dev, vocab=len(token_dict),
+                                 force_two_stage=dec.force_two_stage)
         self.has_fusion = fusion is not None
         early = (not self.has_fusion) or bool(fusion.nonpositive_scores)
         self.cfg = search_cfg(config, token_dict, self.has_fusion, early, True, MT, TM)
@@ -177,7 +178,22 @@ class _Session:
         self.slots0 = torch.arange(B, dtype=torch.int32, device=dev) * Kb
         self.fus_buf = None
         self.lm = None
-        if self.has_fusion:
+        self.sub = None
+        if self.has_fusion and hasattr(fusion, "char_lm"):
+            # SubwordFusion over the device token LM: the selection reads the
+            # fp32 logits and an fp64 normaliser per slot (rows never built)
+            sw = fusion.char_lm.weights
+            sd = sw.d
+            self.sub = sw
+            self.sub_X2 = [SubLmState(sd.layers, N, sd.hidden, dev),
+                           SubLmState(sd.layers, N, sd.hidden, dev)]
+            self.sub_scratch = split_scratch(N, sw.k_max, dev)
+            self.fus_buf = torch.zeros((N, V), dtype=torch.float32, device=dev)
+            self.sub_norm = torch.zeros(N, dtype=torch.float64, device=dev)
+            self.buf.set_fusion_logits(self.sub_norm, fusion.char_lm.score_floor)
+            self.views = [_view_with_rows(self.buf, p, self.rows[1 - p], self.count[1 - p])
+                          for p in range(2)]
+        elif self.has_fusion:
             self.lm = _LmPool(fusion.word_lm.weights, N, dev)
             self.fus_buf = torch.zeros((N + 1, V), dtype=torch.float64, device=dev)
         self.graphs = None
@@ -198,6 +214,9 @@ class _Session:
         prev.ctx.zero_()
         self.rows[0][:self.B] = self.slots0
         self.count[0].fill_(self.B)
+        if self.sub is not None:
+            self.sub_X2[1].h.zero_()
+            self.sub_X2[1].c.zero_()
         if self.lm is not None:
             lm = self.lm
             lm.trie[0].zero_()
@@ -216,6 +235,7 @@ class FusedDecoder:
         self.steps_run = 0
         self.kernel_launches = 0
         self.prune_spec = True      # exact pruning of speculative <eos> LM events
+        self.force_two_stage = False  # tests: two-stage selection at any vocabulary
         self.use_graphs = True      # one CUDA graph per step parity, replayed
         self.poll_every = 8         # host polls the live-row count every k steps
         self._sess: Optional[_Session] = None
@@ -242,7 +262,14 @@ class FusedDecoder:
                            acc_in=buf.acc[c], acc_out=buf.acc[1 - c], cov=buf.cov,
                            energy=S.energy, timer=None if isinstance(tm, _NoTimer) else tm)
         fus_buf = S.fus_buf
-        if S.has_fusion:
+        if S.sub is not None:
+            with tm("lm_subword"):
+                subword_step(S.sub, m=N, m_dev=nc, rows=rc, parent=buf.parent,
+                             last_tok=buf.last_tok, eos_id=fusion.char_lm.eos_id,
+                             pad_id=fusion.char_lm.pad_id, prev=S.sub_X2[1 - c],
+                             cur=S.sub_X2[c], scratch=S.sub_scratch, logits=fus_buf,
+                             norm=S.sub_norm)
+        if S.lm is not None:
             lm, dtrie = S.lm, fusion.dtrie
             lw = lm.lw
             Vw = lw.d.words
@@ -275,7 +302,7 @@ class FusedDecoder:
         with tm("select"):
             _lib.call("fb_search_step", S.cfg_ref, C.byref(S.views[c]), B, P(S.am_logp), V,
                       P(fus_buf), V, stream)
-        if S.has_fusion:
+        if S.lm is not None:
             rn, cn = S.rows[1 - c], S.count[1 - c]
             with tm("advance"):
                 _lib.call("fb_trie_advance", dtrie.ref, N, P(cn), P(rn), P(buf.parent),

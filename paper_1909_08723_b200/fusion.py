@@ -8,6 +8,11 @@ same word history.  Eq. 4 is evaluated by ``fb_lookahead_scores`` (one warp per
 row over the CSR trie), the trie transition by ``fb_trie_advance`` and new ``g``
 rows by ``fb_cumsum_rows`` / ``fb_logits_to_g``.  Nothing falls back to numpy.
 
+``SubwordFusion`` (``fusion.py:236-266``) is plain token-level LM fusion over
+the ``CharLM`` protocol (``char_lm.py:23-33``): host providers' rows are stacked
+and uploaded; the device token LSTM LM (``models.LstmSubwordLM``) makes it
+device-native, and the fused engine then never materialises the rows.
+
 Word LMs: any object with the reference ``WordLM`` protocol
 (``word_lm.py:160-186``) works -- host distributions are uploaded once per
 distinct history.  The device LSTM LM (``models.LstmWordLM``) writes its rows
@@ -279,3 +284,57 @@ class LookaheadFusion(FusionScorer):
         idx = torch.as_tensor(idx_np, device=self.device)
         return LookaheadBatch(self, state.states_dev[idx], state.slots_dev[idx],
                               [state.histories[i] for i in idx_np])
+
+
+# ---- plain token-level LM fusion (fusion.py:236-266) -------------------------------
+class SubwordBatch:
+    """Per-row provider states (reference ``SubwordBatch`` fusion.py:236-241)."""
+
+    def __init__(self, char_states: list):
+        self.char_states = char_states
+
+    def __len__(self) -> int:
+        return len(self.char_states)
+
+
+class SubwordFusion(FusionScorer):
+    """The character/subword provider's rows, unchanged (fusion.py:244-266).
+    ``nonpositive_scores`` stays True (rows are log-probabilities)."""
+
+    def __init__(self, char_lm, device=None):
+        self.char_lm = char_lm
+        self.diagnostics: dict = {}
+        self.device = _device(device)
+
+    @property
+    def device_native(self) -> bool:
+        return bool(getattr(self.char_lm, "is_device_lm", False))
+
+    def start(self, n: int) -> SubwordBatch:
+        s0 = self.char_lm.start()
+        return SubwordBatch([s0] * n)
+
+    def char_scores_device(self, state: SubwordBatch) -> torch.Tensor:
+        dev_rows = getattr(self.char_lm, "log_probs_device", None)
+        if dev_rows is not None:
+            return dev_rows(state.char_states)
+        rows = np.stack([np.asarray(self.char_lm.log_probs(s), np.float64)
+                         for s in state.char_states])
+        return torch.as_tensor(rows, device=self.device)
+
+    def char_scores(self, state: SubwordBatch) -> np.ndarray:
+        if getattr(self.char_lm, "log_probs_device", None) is not None:
+            return self.char_scores_device(state).cpu().numpy()
+        return np.stack([self.char_lm.log_probs(s) for s in state.char_states])
+
+    def advance(self, state: SubwordBatch, tokens: Sequence[int]) -> SubwordBatch:
+        toks = [int(t) for t in np.asarray(tokens).reshape(-1)]
+        if len(toks) != len(state):
+            raise ValueError("one chosen token per hypothesis row required")
+        many = getattr(self.char_lm, "advance_many", None)
+        if many is not None:
+            return SubwordBatch(many(state.char_states, toks))
+        return SubwordBatch([self.char_lm.advance(s, t) for s, t in zip(state.char_states, toks)])
+
+    def reorder(self, state: SubwordBatch, parent_indices: Sequence[int]) -> SubwordBatch:
+        return SubwordBatch([state.char_states[i] for i in parent_indices])

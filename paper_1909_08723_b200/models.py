@@ -8,6 +8,10 @@
 * ``LstmWordLM`` -- ``WordLM`` (reference ``word_lm.py:160-186``): tied-
   embedding LSTM LM.  ``is_device_lm`` makes a
   ``LookaheadFusion`` over it device-native.
+* ``LstmSubwordLM`` -- ``CharLM`` (reference ``char_lm.py:23-33``): token-level
+  LSTM LM for ``SubwordFusion`` (config 4); device-native in the fused engine,
+  where its rows never materialise (the selection kernel reads its fp32 logits
+  and an fp64 log-normaliser per row).
 
 Weights are stored for the kernels: LSTM gate rows interleaved (row 4u+q =
 gate q of unit u), input and recurrent matrices concatenated along K so one
@@ -28,7 +32,7 @@ import torch
 from . import _lib
 from . import kernels as K
 from .fusion import _device
-from .synth import AsrDims, LmDims
+from .synth import AsrDims, LmDims, SubwordLmDims
 
 KGRAN = 64           # K granule of the tensor-core GEMM (one 128 B swizzle atom of bf16)
 
@@ -382,6 +386,9 @@ class LmWeights:
                                          2 * H, H))
         self.k_max = max([l.k_pad for l in self.layers] + [self.k_out])
         self.eos_tok, self.unk_tok, self.bos_tok = d.words, d.words + 1, d.words + 2
+        self.in_width = H
+        self.out_w = self.emb_w
+        self.stats_vw = d.words
 
 
 def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks,
@@ -395,7 +402,7 @@ def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks
     L = len(w.layers)
     for l, lay in enumerate(w.layers):
         if l == 0:
-            x = (w.emb, H, 4, w.emb.stride(0))
+            x = (w.emb, w.in_width, 4, w.emb.stride(0))
         else:
             x = (state_dst[:, l - 1, 0], H, 0, state_dst.stride(0))
         if state_src is None:
@@ -413,12 +420,12 @@ def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks
         K.pack(scratch, [(state_dst[:, L - 1, 0], H, 0, state_dst.stride(0))], m=m, m_dev=m_dev,
                k_pad=w.k_out, split=True)
         kw = dict(m=m, m_dev=m_dev, k=w.k_out, bias=w.b_out, out=logits, row_stats=stats,
-                  stats_vw=w.d.words, k_alg=H)
+                  stats_vw=w.stats_vw, k_alg=H)
         if timer is not None:
             with timer("lm_out_gemm"):
-                K.gemm_tc(scratch, w.emb_w, **kw)
+                K.gemm_tc(scratch, w.out_w, **kw)
         else:
-            K.gemm_tc(scratch, w.emb_w, **kw)
+            K.gemm_tc(scratch, w.out_w, **kw)
 
 
 class _DevHist:
@@ -484,3 +491,129 @@ class LstmWordLM:
         lg = torch.cat([h.logits for h in hists], dim=0)
         K.logits_to_g(lg, self.vocab_size, self.weights.v_out, m=len(hists), slots=slots,
                       g_pool=pool)
+
+
+# ---- token-level (subword) LM: CharLM protocol ------------------------------------
+SCORE_FLOOR = -30.0            # reference char_lm.py:20
+
+
+class SubLmWeights:
+    """Device weights of the token LSTM LM (same kernel layout as LmWeights)."""
+
+    def __init__(self, W: Dict[str, np.ndarray], d: SubwordLmDims, device):
+        self.d = d
+        H, E = d.hidden, d.emb
+        self.in_width = E
+        self.emb = _dev(W["slm.emb"], device, _pad(E))          # [V, E_pad] fp32 input rows
+        self.layers: List[LstmLayer] = []
+        for l in range(d.layers):
+            fin = E if l == 0 else H
+            w = np.concatenate([W[f"slm.{l}.w_ih"], W[f"slm.{l}.w_hh"]], axis=1)
+            self.layers.append(LstmLayer(_devw(interleave_gates(w, H), device, _pad(fin + H)),
+                                         _dev(interleave_gates(W[f"slm.{l}.b"], H), device),
+                                         fin + H, H))
+        self.k_out = _pad(H)
+        self.out_w = _devw(W["slm.out.w"], device, self.k_out)
+        self.b_out = _dev(W["slm.out.b"], device)
+        self.stats_vw = 0
+        self.k_max = max([l.k_pad for l in self.layers] + [self.k_out])
+
+
+class _TokState:
+    """One hypothesis' LM state after consuming <eos> + its token history."""
+    __slots__ = ("state", "logits")
+
+    def __init__(self, state, logits):
+        self.state = state            # [1, L, 2, H]
+        self.logits = logits          # [1, V] fp32
+
+
+class LstmSubwordLM:
+    """CharLM over the device token LSTM LM.  ``log_probs`` row = fp64
+    log-softmax of the fp32 logits over the non-pad tokens, floored at
+    SCORE_FLOOR, ``<pad>`` = SCORE_FLOOR (the row contract of char_lm.py:1-7)."""
+
+    is_device_lm = True
+
+    def __init__(self, W: Dict[str, np.ndarray], dims: SubwordLmDims, pad_id: int, eos_id: int,
+                 device=None):
+        self.device = _device(device)
+        self.dims = dims
+        self.pad_id, self.eos_id = pad_id, eos_id
+        self.score_floor = SCORE_FLOOR
+        self.weights = SubLmWeights(W, dims, self.device)
+        self._start = self._run(None, [eos_id])[0]
+
+    def _run(self, src: Optional[torch.Tensor], tokens: Sequence[int]) -> List[_TokState]:
+        w, d, dev = self.weights, self.dims, self.device
+        n = len(tokens)
+        st = torch.empty((n, d.layers, 2, d.hidden), dtype=torch.float32, device=dev)
+        lg = torch.empty((n, d.vocab), dtype=torch.float32, device=dev)
+        scratch = split_scratch(n, w.k_max, dev)
+        ranks = torch.as_tensor(np.asarray(tokens, np.int32), device=dev)
+        lm_step(w, m=n, m_dev=None, state_src=src, src_idx=None, state_dst=st, ranks=ranks,
+                tok_default=self.eos_id, scratch=scratch, logits=lg)
+        return [_TokState(st[i:i + 1], lg[i:i + 1]) for i in range(n)]
+
+    # ---- reference CharLM protocol --------------------------------------------
+    def start(self) -> _TokState:
+        return self._start
+
+    def advance(self, state: _TokState, token_id: int) -> _TokState:
+        return self.advance_many([state], [token_id])[0]
+
+    def advance_many(self, states: Sequence[_TokState], tokens: Sequence[int]
+                     ) -> List[_TokState]:
+        if not states:
+            return []
+        return self._run(torch.cat([s.state for s in states]), tokens)
+
+    def log_probs(self, state: _TokState) -> np.ndarray:
+        return self.log_probs_device([state])[0].cpu().numpy()
+
+    def log_probs_device(self, states: Sequence[_TokState]) -> torch.Tensor:
+        lg = torch.cat([s.logits for s in states])
+        n, V = lg.shape
+        norm = torch.empty(n, dtype=torch.float64, device=self.device)
+        _lib.call("fb_row_logsumexp", n, None, None, _lib.ptr(lg), lg.stride(0), V, self.pad_id,
+                  _lib.ptr(norm), _lib.stream_ptr())
+        rows = (lg.double() - norm[:, None]).clamp_(min=SCORE_FLOOR)
+        rows[:, self.pad_id] = SCORE_FLOOR
+        return rows
+
+
+class SubLmState:
+    """Token-LM state per slot: h/c per layer (one ping-pong half)."""
+
+    def __init__(self, L: int, N: int, H: int, device):
+        self.h = torch.zeros((L, N, H), dtype=torch.float32, device=device)
+        self.c = torch.zeros((L, N, H), dtype=torch.float32, device=device)
+
+
+def subword_step(w: SubLmWeights, *, m: int, m_dev, rows, parent, last_tok, eos_id: int,
+                 pad_id: int, prev: SubLmState, cur: SubLmState, scratch: torch.Tensor,
+                 logits: torch.Tensor, norm: torch.Tensor) -> None:
+    """Token-LM step over the compact row list (slot layout), the same
+    parent-indirect recurrence as the decoder: slot r consumes last_tok[r]
+    (<eos> at the first step) on top of its parent's state; logits[r] and the
+    fp64 log-normaliser over non-pad tokens norm[r]."""
+    H = w.d.hidden
+    L = len(w.layers)
+    kw = dict(m=m, m_dev=m_dev, rows=rows, parent=parent)
+    for l, lay in enumerate(w.layers):
+        if l == 0:
+            segs = [(w.emb, w.in_width, 3), (prev.h[0], H, 2)]
+        else:
+            segs = [(cur.h[l - 1], H, 1), (prev.h[l], H, 2)]
+        K.pack(scratch, segs, tokens=last_tok, tok_default=eos_id, k_pad=lay.k_pad, split=True,
+               **kw)
+        K.gemm_tc(scratch, lay.w, k=lay.k_pad, bias=lay.b, mode=1, hidden=H, c_in=prev.c[l],
+                  c_out=cur.c[l], h_out=cur.h[l], k_alg=lay.k_in, **kw)
+    K.pack(scratch, [(cur.h[L - 1], H, 1)], k_pad=w.k_out, split=True, **kw)
+    K.gemm_tc(scratch, w.out_w, k=w.k_out, bias=w.b_out, out=logits, m=m, m_dev=m_dev,
+              rows=rows, k_alg=H)
+    _lib.call("fb_row_logsumexp", m, P_(m_dev), P_(rows), P_(logits), logits.stride(0),
+              w.d.vocab, pad_id, P_(norm), _lib.stream_ptr())
+
+
+P_ = _lib.ptr

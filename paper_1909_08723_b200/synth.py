@@ -97,6 +97,35 @@ class LmDims:
     w_scale: float = 1.0           # LSTM weight range multiplier (x 1/sqrt(hidden))
 
 
+@dataclass
+class SubwordLmDims:
+    """Token-level (subword) LSTM LM for SubwordFusion (config 4)."""
+    layers: int = 4
+    hidden: int = 800
+    emb: int = 800
+    vocab: int = 5000              # == the token dictionary size
+    out_scale: float = 0.25        # uniform range of the output projection
+    eos_bias: float = 0.0          # added to the <eos> output bias
+    w_scale: float = 1.0
+
+
+def subword_token_list(n_tokens: int, seed: int) -> List[str]:
+    """Distinct synthetic subword strings (1-4 letters, word-initial ones
+    marked with a leading '_'); TokenDictionary adds the 4 specials."""
+    rng = np.random.default_rng(seed)
+    p = _LETTER_FREQ / _LETTER_FREQ.sum()
+    alphabet = np.array(list("abcdefghijklmnopqrstuvwxyz"))
+    toks: List[str] = []
+    seen = set()
+    while len(toks) < n_tokens:
+        L = int(rng.integers(1, 5))
+        t = ("_" if rng.random() < 0.4 else "") + "".join(rng.choice(alphabet, size=L, p=p))
+        if t not in seen:
+            seen.add(t)
+            toks.append(t)
+    return toks
+
+
 def _bf16_round(a: np.ndarray) -> np.ndarray:
     """Round-to-nearest-even to bf16, returned as fp32 (exact in bf16)."""
     a = np.ascontiguousarray(a, dtype=np.float32)
@@ -157,6 +186,24 @@ def lm_weights(d: LmDims, seed: int) -> Dict[str, np.ndarray]:
     return W
 
 
+def subword_lm_weights(d: SubwordLmDims, seed: int, eos_id: int = 1) -> Dict[str, np.ndarray]:
+    """Token-level LSTM LM: embedding, L LSTM layers, untied output projection."""
+    rng = np.random.default_rng(seed)
+    H, E = d.hidden, d.emb
+    s = d.w_scale / math.sqrt(H)
+    W: Dict[str, np.ndarray] = {}
+    W["slm.emb"] = _uniform(rng, (d.vocab, E), 1.0)
+    for l in range(d.layers):
+        W[f"slm.{l}.w_ih"] = _uniform(rng, (4 * H, E if l == 0 else H), s)
+        W[f"slm.{l}.w_hh"] = _uniform(rng, (4 * H, H), s)
+        W[f"slm.{l}.b"] = _uniform(rng, (4 * H,), s)
+    W["slm.out.w"] = _uniform(rng, (d.vocab, H), d.out_scale)
+    b = _uniform(rng, (d.vocab,), d.out_scale)
+    b[eos_id] = _bf16_round(np.array([b[eos_id] + d.eos_bias], np.float32))[0]
+    W["slm.out.b"] = b
+    return W
+
+
 @dataclass
 class Workload:
     """One BASELINE.json configuration."""
@@ -173,6 +220,7 @@ class Workload:
     max_len_ratio: float = 1.0
     batch_size: int = 512
     seed: int = 1234
+    sublm: Optional[SubwordLmDims] = None      # SubwordFusion (config 4) instead of look-ahead
 
     def describe(self) -> dict:
         out = asdict(self)
@@ -194,6 +242,15 @@ WORKLOADS: Dict[str, Workload] = {
                    batch_size=512),
     "c3": Workload("c3", 16, (300, 300), 20, SMALL_ASR, None, coverage_mode="improved",
                    coverage_weight=0.01, eos_gamma=1.5, batch_size=16),
+    # c4: subword decoder (5k tokens), beam 60, token-level LSTM-LM shallow fusion;
+    # scales calibrated like c2 (scripts/calib_c4.sh: ~0.45 tokens per encoder
+    # frame, ~60% of utterances emit <eos>, distinct outputs)
+    "c4": Workload("c4", 2620, (300, 3500), 60,
+                   AsrDims(enc_hidden=512, dec_hidden=1024, emb=256, att=512, vocab=5000,
+                           out_scale=1.5, eos_bias=1.0),
+                   None, lm_weight=0.3, batch_size=32,
+                   sublm=SubwordLmDims(layers=4, hidden=800, emb=800, vocab=5000,
+                                       out_scale=0.5)),
     # c5: Switchboard-shaped char decoder, 30k-word look-ahead, beam 35
     "c5": Workload("c5", 4458, (100, 2000), 35,
                    AsrDims(enc_hidden=320, dec_hidden=640, emb=64, att=320),

@@ -15,7 +15,13 @@ Imports the UNMODIFIED reference package ``fusedbeam`` read-only from
                           look-ahead fusion, quantised ties) (decoder.py:339-480);
 * ``neural.pkl.gz``    -- ``decode_batch`` + ``LookaheadFusion`` driving the
                           oracle's PyTorch-CPU attention-LSTM scorer and LSTM
-                          word LM at a small size.
+                          word LM at a small size;
+* ``subword.pkl.gz``   -- ``SubwordFusion`` rows/advance/reorder and
+                          ``decode_batch`` with ``SubwordFusion`` over
+                          ``UniformCharLM`` and a table ``CharLM`` fake
+                          (fusion.py:236-266, char_lm.py:23-53), plus the
+                          oracle's token LSTM LM + attention-LSTM scorer on a
+                          small subword dictionary.
 
 The GPU box never reads /root/reference: the tests only read these files.
 """
@@ -34,14 +40,16 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, "/root/reference/pkg/src")
 
+from fusedbeam.char_lm import CharLM, UniformCharLM  # noqa: E402
 from fusedbeam.decoder import DecodeConfig, TraceScorer, _TraceTable, decode_batch  # noqa: E402
-from fusedbeam.fusion import LookaheadBatch, LookaheadFusion  # noqa: E402
+from fusedbeam.fusion import LookaheadBatch, LookaheadFusion, SubwordFusion  # noqa: E402
 from fusedbeam.kaldi_io import FeatureMatrix  # noqa: E402
 from fusedbeam.lexicon_trie import build_trie  # noqa: E402
 from fusedbeam.token_dict import TokenDictionary  # noqa: E402
 from fusedbeam.word_lm import TableLM  # noqa: E402
 
 from oracle.neural import OracleAttnLstmScorer, OracleLstmWordLM  # noqa: E402
+from oracle.subword import OracleLstmCharLM  # noqa: E402
 from paper_1909_08723_b200 import synth  # noqa: E402
 
 
@@ -216,9 +224,122 @@ def neural_cases():
                                n_utts=4, cases=cases))
 
 
+class TableCharLM(CharLM):
+    """Reference-protocol fake: rows keyed by token history, longest listed
+    suffix wins (same as oracle.subword.OracleTableCharLM)."""
+
+    def __init__(self, rows, default):
+        self.rows, self.default = rows, default
+
+    def start(self):
+        return ()
+
+    def log_probs(self, state):
+        for k in range(len(state), -1, -1):
+            r = self.rows.get(tuple(state[len(state) - k:]))
+            if r is not None:
+                return r
+        return self.default
+
+    def advance(self, state, token_id):
+        return tuple(state) + (int(token_id),)
+
+
+def _char_row(rng, d, quantized=False, eos_scale=0.02):
+    V = len(d)
+    p = rng.choice([1.0, 2.0, 4.0], size=V) if quantized else rng.dirichlet(np.ones(V))
+    p[d.pad_id] = 0.0
+    p[d.eos_id] *= eos_scale           # keep hypotheses alive past the first steps
+    p = p / p.sum()
+    with np.errstate(divide="ignore"):
+        row = np.log(p)
+    row[d.pad_id] = -30.0
+    return row
+
+
+def subword_cases():
+    rng = np.random.default_rng(44)
+    letters = ["a", "b", "c", "d"]
+    d = TokenDictionary(letters)
+    V = len(d)
+    # fusion rows / advance / reorder walk (test_fusion.py:224-237 generalised)
+    walks = []
+    for i in range(6):
+        rows = {(): _char_row(rng, d)}
+        for t in range(V):
+            if rng.random() < 0.5:
+                rows[(t,)] = _char_row(rng, d)
+        default = _char_row(rng, d)
+        fus = SubwordFusion(TableCharLM(rows, default))
+        st = fus.start(5)
+        walk = []
+        for step in range(5):
+            sc = fus.char_scores(st)
+            toks = rng.integers(0, V, size=5)
+            parents = sorted(rng.integers(0, 5, size=5).tolist())
+            walk.append(dict(scores=sc, tokens=toks, parents=np.array(parents)))
+            st = fus.reorder(fus.advance(st, toks), parents)
+        walks.append(dict(rows=rows, default=default, walk=walk))
+    cases = []
+    for i in range(24):
+        mode = i % 4
+        nutt = int(rng.integers(1, 5))
+        tables = {}
+        for u in range(nutt):
+            uid = f"s{i}_{u}"
+            tables[uid] = rand_table(rng, d, uid, int(rng.integers(2, 6)), depth=2,
+                                     quantized=bool(i % 2))
+        uniform = i % 3 == 0
+        rows = {(): _char_row(rng, d, quantized=bool(i % 2), eos_scale=1e-4)}
+        for t in range(V):
+            if rng.random() < 0.6:
+                rows[(t,)] = _char_row(rng, d, quantized=bool(i % 2))
+        default = _char_row(rng, d)
+        lm = UniformCharLM(d) if uniform else TableCharLM(rows, default)
+        cfg = dict(beam_size=int(rng.integers(1, 9)), lm_weight=[0.3, 0.7, 1.0, 0.5][mode],
+                   coverage_mode=["off", "original", "improved", "off"][mode],
+                   coverage_weight=0.05, tau1=0.4, tau2=0.9, cov_margin=0.7,
+                   eos_gamma=[None, 1.5, None, 1.2][mode],
+                   max_len_ratio=[1.0, 1.5, 2.0, 1.0][mode])
+        feats = [FeatureMatrix(uid, np.zeros((1, 1), np.float32)) for uid in tables]
+        res = decode_batch(feats, TraceScorer(tables), SubwordFusion(lm), DecodeConfig(**cfg), d)
+        cases.append(dict(tables={k: (v.t_enc, v.rows, v.default) for k, v in tables.items()},
+                          order=list(tables), cfg=cfg, uniform=uniform, rows=rows,
+                          default=default,
+                          results=[(r.utt_id, r.tokens, r.score, r.attn_accum.copy(),
+                                    r.finished, r.steps) for r in res]))
+    # neural: oracle attention-LSTM scorer + oracle token LSTM LM through the
+    # reference SubwordFusion / decode_batch
+    import torch
+    torch.set_num_threads(4)
+    sd = TokenDictionary(synth.subword_token_list(60, seed=3))
+    adims = synth.AsrDims(enc_layers=2, enc_hidden=32, dec_layers=2, dec_hidden=32,
+                          emb=16, att=32, vocab=len(sd), out_scale=0.6)
+    sdims = synth.SubwordLmDims(layers=2, hidden=48, emb=32, vocab=len(sd), out_scale=0.5)
+    W = synth.asr_weights(adims, seed=17, eos_id=sd.eos_id)
+    W.update(synth.subword_lm_weights(sdims, seed=18, eos_id=sd.eos_id))
+    utts = synth.synth_fbank(4, seed=19, frames=(40, 64))
+    feats = [FeatureMatrix(u, x) for u, x in utts]
+    neural = []
+    for cfg in (dict(beam_size=4, lm_weight=0.4),
+                dict(beam_size=7, lm_weight=0.8, coverage_mode="improved",
+                     coverage_weight=0.02, eos_gamma=1.5)):
+        sc = OracleAttnLstmScorer(W, adims.enc_layers, adims.dec_layers, adims.subsample,
+                                  sd.eos_id)
+        lm = OracleLstmCharLM(W, sdims.layers, sd.pad_id, sd.eos_id)
+        res = decode_batch(feats, sc, SubwordFusion(lm), DecodeConfig(**cfg), sd)
+        neural.append(dict(cfg=cfg, results=[(r.utt_id, r.tokens, r.score,
+                                              np.asarray(r.attn_accum).copy(), r.finished,
+                                              r.steps) for r in res]))
+    dump("subword.pkl.gz", dict(letters=letters, walks=walks, cases=cases,
+                                neural=dict(tokens=synth.subword_token_list(60, seed=3),
+                                            adims=adims.__dict__, sdims=sdims.__dict__,
+                                            asr_seed=17, lm_seed=18, fbank_seed=19,
+                                            frames=(40, 64), n_utts=4, cases=neural)))
+
+
 if __name__ == "__main__":
-    trie_cases()
-    lookahead_cases()
-    decode_cases()
-    neural_cases()
+    which = sys.argv[1:] or ["trie", "lookahead", "decode", "neural", "subword"]
+    for name in which:
+        globals()[f"{name}_cases"]()
     print("golden fixtures written to", HERE)

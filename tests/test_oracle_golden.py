@@ -173,3 +173,71 @@ def test_neural_decode_matches_reference_bitwise():
             assert (r.utt_id, r.tokens, r.finished, r.steps) == (uid, toks, fin, steps)
             assert r.score == score
             np.testing.assert_array_equal(r.attn_accum, acc)
+
+
+# ---- subword (token-level LM) fusion: fusion.py:236-266, char_lm.py:23-53 -------
+def test_subword_rows_match_reference_bitwise():
+    from oracle.subword import OracleSubwordFusion, OracleTableCharLM, OracleUniformCharLM
+    g = load_golden("subword.pkl.gz")
+    d = OracleDict(g["letters"])
+    for w in g["walks"]:
+        fus = OracleSubwordFusion(OracleTableCharLM(w["rows"], w["default"]))
+        assert fus.nonpositive_scores
+        st = fus.start(5)
+        for step in w["walk"]:
+            np.testing.assert_array_equal(fus.char_scores(st), step["scores"])
+            st = fus.reorder(fus.advance(st, step["tokens"]), step["parents"].tolist())
+    # test_fusion.py:224-237: rows are the provider's rows
+    uni = OracleUniformCharLM(len(d), d.pad_id)
+    fus = OracleSubwordFusion(uni)
+    rows = fus.char_scores(fus.start(3))
+    assert rows.shape == (3, len(d))
+    assert rows[0, d.pad_id] == -30.0
+    assert abs(rows[0, d.eos_id] - math.log(1.0 / (len(d) - 1))) == 0.0
+
+
+def test_subword_decode_matches_reference_bitwise():
+    from oracle.subword import OracleSubwordFusion, OracleTableCharLM, OracleUniformCharLM
+    g = load_golden("subword.pkl.gz")
+    d = OracleDict(g["letters"])
+    for case in g["cases"]:
+        lm = (OracleUniformCharLM(len(d), d.pad_id) if case["uniform"]
+              else OracleTableCharLM(case["rows"], case["default"]))
+        feats = [_Feat(u, np.zeros((1, 1), np.float32)) for u in case["order"]]
+        res = decode_batch(feats, TableScorer(case["tables"]), OracleSubwordFusion(lm),
+                           OracleConfig(**case["cfg"]), d)
+        for r, (uid, toks, score, acc, fin, steps) in zip(res, case["results"]):
+            assert (r.utt_id, r.tokens, r.finished, r.steps) == (uid, toks, fin, steps)
+            assert r.score == score
+            assert r.attn_accum.tobytes() == acc.tobytes()
+
+
+def test_subword_neural_decode_matches_reference_bitwise():
+    pytest.importorskip("torch")
+    from oracle.neural import OracleAttnLstmScorer
+    from oracle.subword import OracleLstmCharLM, OracleSubwordFusion
+    from paper_1909_08723_b200 import synth
+    g = load_golden("subword.pkl.gz")["neural"]
+    d = OracleDict(g["tokens"])
+    ad = synth.AsrDims(**g["adims"])
+    sdm = synth.SubwordLmDims(**g["sdims"])
+    W = synth.asr_weights(ad, seed=g["asr_seed"], eos_id=d.eos_id)
+    W.update(synth.subword_lm_weights(sdm, seed=g["lm_seed"], eos_id=d.eos_id))
+    feats = [_Feat(u, x) for u, x in synth.synth_fbank(g["n_utts"], g["fbank_seed"],
+                                                       tuple(g["frames"]))]
+    for case in g["cases"]:
+        sc = OracleAttnLstmScorer(W, ad.enc_layers, ad.dec_layers, ad.subsample, d.eos_id)
+        lm = OracleLstmCharLM(W, sdm.layers, d.pad_id, d.eos_id)
+        res = decode_batch(feats, sc, OracleSubwordFusion(lm, batched=False),
+                           OracleConfig(**case["cfg"]), d)
+        for r, (uid, toks, score, acc, fin, steps) in zip(res, case["results"]):
+            assert (r.utt_id, r.tokens, r.finished, r.steps) == (uid, toks, fin, steps)
+            assert r.score == score
+            np.testing.assert_array_equal(r.attn_accum, acc)
+        # the batched advance (used at real sizes) agrees to fp32 rounding
+        lm2 = OracleLstmCharLM(W, sdm.layers, d.pad_id, d.eos_id)
+        s0 = lm2.start()
+        toks = [3, 7, d.eos_id, 11]
+        many = lm2.advance_many([s0] * 4, toks)
+        for s, t in zip(many, toks):
+            np.testing.assert_allclose(s.row, lm2.advance(s0, t).row, rtol=0, atol=1e-5)
