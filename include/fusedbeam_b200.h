@@ -155,7 +155,8 @@ typedef struct {
    * for the exact two-stage selection (per-row top-beam, then the beam cut
    * over the survivors); NULL = single-stage only */
   double* cand_score_ws; int32_t* cand_flat_ws;
-  int32_t force_two_stage;     /* 1: two-stage selection even when one CTA fits */
+  int32_t force_two_stage;     /* test knobs: bit 0 two-stage selection even when one
+                                  CTA fits, bit 1 radix top-K at any candidate count */
   int32_t pad1;
   /* token-level LM fusion from raw logits (char_lm.py:23-33 rows computed on
    * the fly): when non-NULL, the fusion argument of fb_search_step is fp32
@@ -222,7 +223,11 @@ typedef struct {
   /* mode 0, optional: per (output row, 64-column block) softmax statistics
    * {max, sum exp(x-max)} over all columns and over columns < stats_vw,
    * float4 at row_stats[orow * ceil(n/64) + block] (forces 128-wide tiles) */
-  float* row_stats; int32_t stats_vw; int32_t pad1;
+  float* row_stats; int32_t stats_vw;
+  /* fb_gemm_tc: K blocks (64) per TMEM accumulation chunk, 0 = default (4).
+   * 1 = most accurate: the tensor core's in-TMEM accumulation truncates, so
+   * score-producing projections drain every 64-K chunk into fp32 registers. */
+  int32_t kcb;
 } fb_gemm_t;
 
 int fb_gemm(const fb_gemm_t* g, void* stream);

@@ -46,7 +46,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if (not force and os.path.exists(obj)
                 and os.path.getmtime(obj) >= max(os.path.getmtime(path), hdr_mtime)):
             continue
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", path, "-o", obj]
+        extra = os.environ.get("FB_NVCC_EXTRA", "").split()     # dev experiments only
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", path, "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

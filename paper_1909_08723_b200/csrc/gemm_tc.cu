@@ -115,11 +115,16 @@ __device__ __forceinline__ float sigm_tc(float x) { return 1.0f / (1.0f + expf(-
 
 // MUFU ex2 + rcp; __fdividef returns 0 for denominators > 2^126, which is the
 // correct limit here (sigmoid -> 0, tanh -> -1)
+#ifdef FB_PRECISE_ACT
+__device__ __forceinline__ float fsig(float x) { return 1.0f / (1.0f + expf(-x)); }
+__device__ __forceinline__ float ftanh(float x) { return tanhf(x); }
+#else
 __device__ __forceinline__ float fsig(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 
 __device__ __forceinline__ float ftanh(float x) {
   return 1.0f - __fdividef(2.0f, 1.0f + __expf(2.0f * x));
 }
+#endif
 
 __device__ __forceinline__ void store_split(const fb_gemm_t& g, int64_t row, int col, float x) {
   // hi/mid/lo bf16 planes of an fp32 value (the next GEMM's A operand)
@@ -439,10 +444,11 @@ static int launch_tc_maps(const CUtensorMap& ta, const CUtensorMap& tw, const fb
     smem_set = 3 * (3 * TC_BM * TC_BK * 2 + BN * TC_BK * 2) + 1024;
   }
   const int tiles = ((g->m_max + TC_BM - 1) / TC_BM) * ((g->n + BN - 1) / BN);
-  static const int kcb = [] {
+  static const int kcb_env = [] {                   // dev override of the default
     const char* e = getenv("FB_GEMM_KCB");
     return e ? std::max(1, atoi(e)) : TC_KCB;
   }();
+  const int kcb = g->kcb > 0 ? g->kcb : kcb_env;
   k<<<std::min(tiles, kNumSMs), TC_THREADS, smem, s>>>(ta, tw, *g, a_planes, (int)a_plane_rows,
                                                       g->k / TC_BK, kcb);
   count_launch();

@@ -104,6 +104,140 @@ __device__ __forceinline__ Cand warp_best(Cand c) {
   return c;
 }
 
+// ---- block-wide exact top-K for large candidate sets ---------------------------
+// The first K of (key desc, id asc) among the finite keys -- what K rounds of
+// block argmax produce -- without K passes over the keys:
+//  1. bucket = order-preserving bits of the key rounded DOWN to fp32 (monotone,
+//     so the K best keys lie in the K best buckets);
+//  2. radix select (4 x 8-bit digits) of the K-th largest bucket T;
+//  3. compact every key with bucket >= T (K plus fp32-bucket ties);
+//  4. exact rank of each survivor among the survivors (C^2 compares, C small).
+// More than cmax survivors (massive exact ties) falls back to argmax rounds.
+constexpr int kRadixMin = 1024;        // candidate count from which the radix path pays
+
+__host__ __device__ inline int topk_cmax(int K) { return 4 * K + 64; }
+
+__device__ __forceinline__ uint32_t key_bucket(double x) {
+  if (x == -INFINITY) return 0u;                     // never selected
+  const uint32_t u = __float_as_uint(__double2float_rd(x));
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);  // >= 0x007FFFFF for finite x
+}
+
+__device__ void block_topk(const double* key, const int* id, int n, int K, int* out,
+                           int* n_out, uint32_t* bkt, int* cl, int cmax, unsigned char* taken) {
+  __shared__ int hist[256];
+  __shared__ int s_cnt, s_need, s_elig;
+  __shared__ uint32_t s_prefix, s_mask;
+  __shared__ Cand wb[kSelThreads / 32];
+  __shared__ int s_stop, s_n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) { s_elig = 0; s_prefix = 0u; s_mask = 0u; s_need = K; s_cnt = 0; }
+  __syncthreads();
+  int el = 0;
+  for (int j = tid; j < n; j += kSelThreads) {
+    const uint32_t b = key_bucket(key[j]);
+    bkt[j] = b;
+    el += b != 0u;
+  }
+  for (int off = 16; off; off >>= 1) el += __shfl_xor_sync(0xffffffffu, el, off);
+  if (lane == 0) atomicAdd(&s_elig, el);
+  __syncthreads();
+  uint32_t T = 1u;                                   // every finite key
+  if (s_elig > K) {
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int i = tid; i < 256; i += kSelThreads) hist[i] = 0;
+      __syncthreads();
+      const uint32_t pre = s_prefix, msk = s_mask;
+      for (int j = tid; j < n; j += kSelThreads) {
+        const uint32_t b = bkt[j];
+        if (b != 0u && (b & msk) == pre) atomicAdd(&hist[(b >> shift) & 255u], 1);
+      }
+      __syncthreads();
+      if (warp == 0) {
+        // lane l owns digits 255-8l .. 248-8l (descending)
+        int c8[8], cs = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { c8[q] = hist[255 - 8 * lane - q]; cs += c8[q]; }
+        int incl = cs;
+        for (int off = 1; off < 32; off <<= 1) {
+          const int o = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += o;
+        }
+        const int need = s_need, excl = incl - cs;
+        if (excl < need && need <= incl) {
+          int run = excl;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            if (run + c8[q] >= need) {
+              const uint32_t d = 255u - 8u * lane - q;
+              s_prefix = pre | (d << shift);
+              s_mask = msk | (255u << shift);
+              s_need = need - run;
+              break;
+            }
+            run += c8[q];
+          }
+        }
+      }
+      __syncthreads();
+    }
+    T = s_prefix;
+  }
+  for (int j = tid; j < n; j += kSelThreads) {
+    if (bkt[j] >= T) {
+      const int pos = atomicAdd(&s_cnt, 1);
+      if (pos < cmax) cl[pos] = j;
+    }
+  }
+  __syncthreads();
+  const int C = s_cnt;
+  if (C <= cmax) {
+    for (int i = tid; i < C; i += kSelThreads) {
+      const int ci = cl[i];
+      const Cand a{key[ci], id ? id[ci] : ci};
+      int rank = 0;
+      for (int q = 0; q < C; ++q) {
+        const int cq = cl[q];
+        rank += better(Cand{key[cq], id ? id[cq] : cq}, a);
+      }
+      if (rank < K) out[rank] = a.j;
+    }
+    if (tid == 0) *n_out = C < K ? C : K;
+    __syncthreads();
+    return;
+  }
+  // fallback: K rounds of block argmax over the survivors' superset (all keys)
+  for (int j = tid; j < n; j += kSelThreads) taken[j] = 0;
+  if (tid == 0) { s_n = 0; s_stop = 0; }
+  __syncthreads();
+  for (int k = 0; k < K; ++k) {
+    Cand b{-INFINITY, INT_MAX};
+    for (int j = tid; j < n; j += kSelThreads)
+      if (!taken[j] && bkt[j] >= T) {
+        const Cand x{key[j], id ? id[j] : j};
+        if (better(x, b)) b = x;
+      }
+    b = warp_best(b);
+    if (lane == 0) wb[warp] = b;
+    __syncthreads();
+    if (tid == 0) {
+      Cand w = wb[0];
+      for (int q = 1; q < kSelThreads / 32; ++q)
+        if (better(wb[q], w)) w = wb[q];
+      if (w.j == INT_MAX || w.s == -INFINITY) s_stop = 1;
+      else out[s_n++] = w.j;
+    }
+    __syncthreads();
+    if (s_stop) break;
+    const int won = out[s_n - 1];
+    for (int j = tid; j < n; j += kSelThreads)
+      if ((id ? id[j] : j) == won) taken[j] = 1;
+    __syncthreads();
+  }
+  if (tid == 0) *n_out = s_n;
+  __syncthreads();
+}
+
 // Lexicographic compare of two token rows of equal length L: -1, 0, 1.
 __device__ __forceinline__ int lex_cmp(const int32_t* a, const int32_t* b, int L) {
   for (int i = 0; i < L; ++i) {
@@ -142,9 +276,13 @@ __device__ __forceinline__ double step_score(const fb_search_cfg_t& c, const AM*
   return s;
 }
 
+__host__ __device__ inline int topk_cmax(int K);
+
+// cand (8) + bucket (4) + taken (1) per candidate (+ flat index (4) in list mode)
 __host__ __device__ inline size_t sel_smem_bytes(int beam, int vocab, bool list_mode = false) {
   const size_t nv = (size_t)beam * (list_mode ? (beam < vocab ? beam : vocab) : vocab);
-  return 8 * (nv + 2 * (size_t)beam) + 4 * 6 * (size_t)beam + (list_mode ? 4 * nv : 0) + nv;
+  return 8 * (nv + 2 * (size_t)beam) + 4 * 6 * (size_t)beam + (list_mode ? 4 * nv : 0) +
+         4 * nv + 4 * (size_t)topk_cmax(beam) + nv + 16;
 }
 
 // Stage 1 of the large-vocabulary selection: one CTA per live row keeps the
@@ -159,10 +297,14 @@ row_topk_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict__ 
   const int u = slot / K, p = slot % K;
   if (!st.active[u] || p >= st.n_live[u]) return;
   const int n = st.n_live[u];
+  const int Kc = K < V ? K : V;           // a row never has more than V candidates
+  const int cmax = topk_cmax(K);
   double* sc = reinterpret_cast<double*>(sm_raw);                      // [V]
-  unsigned char* taken = reinterpret_cast<unsigned char*>(sc + V);      // [V]
-  __shared__ Cand wbest[kSelThreads / 32];
-  __shared__ int s_stop, s_gated;
+  uint32_t* bkt = reinterpret_cast<uint32_t*>(sc + V);                 // [V]
+  int* cl = reinterpret_cast<int*>(bkt + V);                           // [cmax]
+  int* win = cl + cmax;                                                // [K]
+  unsigned char* taken = reinterpret_cast<unsigned char*>(win + K);    // [V]
+  __shared__ int s_gated, s_nwin;
   __shared__ AM wmax[kSelThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const AM* row = am + (int64_t)slot * am_stride;
@@ -183,43 +325,24 @@ row_topk_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict__ 
   } else if (tid == 0) {
     s_gated = 0;
   }
-  if (tid == 0) s_stop = 0;
   __syncthreads();
   const double tot = st.total_in[slot];
-  for (int t = tid; t < V; t += kSelThreads) {
+  for (int t = tid; t < V; t += kSelThreads)
     sc[t] = dadd(tot, step_score(c, am, am_stride, fus, f_stride, slot, t, s_gated,
                                   st.fus_norm, st.fus_floor));
-    taken[t] = 0;
-  }
   __syncthreads();
+  block_topk(sc, nullptr, V, Kc, win, &s_nwin, bkt, cl, cmax, taken);
   double* os = st.cand_score_ws + (int64_t)slot * K;
   int32_t* of = st.cand_flat_ws + (int64_t)slot * K;
-  const int Kc = K < V ? K : V;           // a row never has more than V candidates
-  for (int k = 0; k < Kc; ++k) {
-    Cand b{-INFINITY, INT_MAX};
-    for (int t = tid; t < V; t += kSelThreads)
-      if (!taken[t]) {
-        Cand x{sc[t], t};
-        if (better(x, b)) b = x;
-      }
-    b = warp_best(b);
-    if (lane == 0) wbest[warp] = b;
-    __syncthreads();
-    if (tid == 0) {
-      Cand w = wbest[0];
-      for (int q = 1; q < kSelThreads / 32; ++q)
-        if (better(wbest[q], w)) w = wbest[q];
-      if (w.j == INT_MAX || w.s == -INFINITY) {
-        s_stop = 1;
-        for (int r = k; r < Kc; ++r) { os[r] = -INFINITY; of[r] = INT_MAX; }
-      } else {
-        taken[w.j] = 1;
-        os[k] = w.s;
-        of[k] = w.j * n + p;       // token-major flat index of decoder.py:404
-      }
+  for (int k = tid; k < Kc; k += kSelThreads) {
+    if (k < s_nwin) {
+      const int t = win[k];
+      os[k] = sc[t];
+      of[k] = t * n + p;                 // token-major flat index of decoder.py:404
+    } else {
+      os[k] = -INFINITY;
+      of[k] = INT_MAX;
     }
-    __syncthreads();
-    if (s_stop) break;
   }
 }
 
@@ -250,7 +373,10 @@ search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict
   int* fin_slot = new_tok + K;                                         // [K]
   int* fin_par = fin_slot + K;                                         // [K]
   int* cflat = fin_par + K;                                            // [NV] list mode
-  unsigned char* taken = reinterpret_cast<unsigned char*>(cflat + (list_mode ? NV : 0));
+  uint32_t* bkt = reinterpret_cast<uint32_t*>(cflat + (list_mode ? NV : 0));  // [NV]
+  const int cmax = topk_cmax(K);
+  int* cl = reinterpret_cast<int*>(bkt + NV);                          // [cmax]
+  unsigned char* taken = reinterpret_cast<unsigned char*>(cl + cmax);  // [NV]
   __shared__ Cand wbest[kSelThreads / 32];
   __shared__ int s_nsel, s_stop;
   __shared__ int n_new, n_fin_new;
@@ -294,6 +420,9 @@ search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict
   if (tid == 0) s_nsel = 0, s_stop = 0;
   __syncthreads();
 
+  if (NV >= kRadixMin || (st.force_two_stage & 2)) {
+    block_topk(cand, list_mode ? cflat : nullptr, NV, K, sel, &s_nsel, bkt, cl, cmax, taken);
+  } else
   // K rounds of block argmax == the first K entries of argsort(-flat, stable)
   for (int k = 0; k < K; ++k) {
     Cand b{-INFINITY, INT_MAX};
@@ -697,19 +826,19 @@ extern "C" int fb_search_step(const fb_search_cfg_t* cfg, const fb_search_state_
   constexpr size_t kBudget = 220 * 1024;
   bool list_mode = false;
   size_t smem = sel_smem_bytes(cfg->beam, cfg->vocab);
-  if (smem > kBudget || st->force_two_stage) {
+  if (smem > kBudget || (st->force_two_stage & 1)) {
     if (!st->cand_score_ws || !st->cand_flat_ws)
       return fail(FB_ERR_CONFIG, "beam x vocabulary too large: pass the two-stage workspace");
     list_mode = true;
     smem = sel_smem_bytes(cfg->beam, cfg->vocab, true);
-    const size_t row_smem = (size_t)cfg->vocab * 9;
+    const size_t row_smem = (size_t)cfg->vocab * 13 + 4 * (size_t)(topk_cmax(cfg->beam) + cfg->beam) + 16;
     if (smem > kBudget || row_smem > kBudget)
       return fail(FB_ERR_CONFIG, "beam or vocabulary too large for the selection kernels");
   }
   if (num_utts <= 0) return FB_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const int N = num_utts * cfg->beam;
-  const size_t row_smem = (size_t)cfg->vocab * 9;
+  const size_t row_smem = (size_t)cfg->vocab * 13 + 4 * (size_t)(topk_cmax(cfg->beam) + cfg->beam) + 16;
 #define FB_SEL(AMT)                                                                           \
   {                                                                                           \
     auto k = search_step_kernel<AMT>;                                                         \

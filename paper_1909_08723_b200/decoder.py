@@ -147,7 +147,7 @@ class SearchBuffers:
     u*beam .. u*beam+beam-1).  ``in``/``out`` pairs ping-pong by step parity."""
 
     def __init__(self, B: int, K: int, max_tokens: int, t_max: int, device, vocab: int = 0,
-                 force_two_stage: bool = False):
+                 select_flags: int = 0):
         z = lambda *s, dt=torch.int32: torch.zeros(s, dtype=dt, device=device)  # noqa: E731
         f64 = torch.float64
         N = B * K
@@ -170,11 +170,12 @@ class SearchBuffers:
         self.res_acc = z(B, t_max, dt=f64)
         self.next_rows, self.next_count = z(N), z(1)
         # exact two-stage selection for beam x vocab beyond one CTA's shared memory
-        self.two_stage = force_two_stage or \
-            8 * (K * vocab + 2 * K) + 24 * K + K * vocab > 220 * 1024
+        # (select_flags: test knobs, bit 0 force two-stage, bit 1 force radix top-K)
+        self.two_stage = bool(select_flags & 1) or \
+            13 * K * vocab + 16 * K + 24 * K + 4 * (4 * K + 64) + 16 > 220 * 1024
         self.cand_score = z(N, K, dt=f64) if self.two_stage else None
         self.cand_flat = z(N, K) if self.two_stage else None
-        self.force_two_stage = force_two_stage
+        self.select_flags = int(select_flags)
         self.fus_norm = None           # set by the fused engine for token-LM logits
         self.fus_floor = 0.0
         self._views = [self._view(0), self._view(1)]
@@ -191,7 +192,7 @@ class SearchBuffers:
             P(self.fin_acc), P(self.res_len), P(self.res_score), P(self.res_finished),
             P(self.res_steps), P(self.res_tokens), P(self.res_acc),
             P(self.next_rows), P(self.next_count), P(self.cand_score), P(self.cand_flat),
-            int(self.force_two_stage), 0, P(self.fus_norm), float(self.fus_floor))
+            self.select_flags, 0, P(self.fus_norm), float(self.fus_floor))
 
     def set_fusion_logits(self, norm: torch.Tensor, floor: float) -> None:
         """Fusion rows given as fp32 logits + this fp64 per-slot normaliser."""
@@ -245,7 +246,7 @@ def decode_batch(features: Sequence[FeatureMatrix], scorer: AcousticScorer, fusi
     return _decode_plugins(features, scorer, fusion, config, token_dict)
 
 
-_FORCE_TWO_STAGE = False      # tests: exercise the large-vocabulary selection at any size
+_SELECT_FLAGS = 0       # tests: bit 0 two-stage selection, bit 1 radix top-K, at any size
 
 
 def _decode_plugins(features, scorer, fusion, config: DecodeConfig, token_dict):
@@ -264,7 +265,7 @@ def _decode_plugins(features, scorer, fusion, config: DecodeConfig, token_dict):
         return []
     MT = max(max_len) + 1
     TM = max(t_enc)
-    buf = SearchBuffers(B, K, MT, TM, dev, vocab=V, force_two_stage=_FORCE_TWO_STAGE)
+    buf = SearchBuffers(B, K, MT, TM, dev, vocab=V, select_flags=_SELECT_FLAGS)
     buf.max_len.copy_(torch.as_tensor(max_len, dtype=torch.int32))
     buf.t_enc.copy_(torch.as_tensor(t_enc, dtype=torch.int32))
     early = fusion is None or bool(fusion.nonpositive_scores)

@@ -157,7 +157,7 @@ class _Session:
         N = self.N = B * Kb
         V = self.V = len(token_dict)
         self.buf = SearchBuffers(B, Kb, MT, TM, dev, vocab=len(token_dict),
-                                 force_two_stage=dec.force_two_stage)
+                                 select_flags=dec.select_flags)
         self.has_fusion = fusion is not None
         early = (not self.has_fusion) or bool(fusion.nonpositive_scores)
         self.cfg = search_cfg(config, token_dict, self.has_fusion, early, True, MT, TM)
@@ -235,7 +235,7 @@ class FusedDecoder:
         self.steps_run = 0
         self.kernel_launches = 0
         self.prune_spec = True      # exact pruning of speculative <eos> LM events
-        self.force_two_stage = False  # tests: two-stage selection at any vocabulary
+        self.select_flags = 0       # tests: bit 0 two-stage, bit 1 radix top-K (any size)
         self.use_graphs = True      # one CUDA graph per step parity, replayed
         self.poll_every = 8         # host polls the live-row count every k steps
         self._sess: Optional[_Session] = None

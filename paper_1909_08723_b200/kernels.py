@@ -89,9 +89,10 @@ def gemm_tc(ap: torch.Tensor, w: torch.Tensor, *, m: Optional[int] = None, m_dev
             k: Optional[int] = None, bias=None, out=None, rows=None, mode: int = 0,
             hidden: int = 0, parent=None, c_in=None, c_out=None, h_out=None, h_res=None,
             addend=None, h_split=None, row_stats=None, stats_vw: int = 0,
-            k_alg: Optional[int] = None) -> None:
+            k_alg: Optional[int] = None, kcb: int = 0) -> None:
     """Tensor-core GEMM: ap = bf16 planes [P, rows, k_pad], w = bf16 [n, k_pad].
-    h_split: optional bf16 [3, rows, k] planes receiving h (next A operand)."""
+    h_split: optional bf16 [3, rows, k] planes receiving h (next A operand).
+    kcb: K blocks per TMEM accumulation chunk (0 default; 1 for score logits)."""
     g = _lib.FbGemm()
     g.m_max = ap.shape[1] if m is None else m
     g.m_dev = P(m_dev)
@@ -112,6 +113,7 @@ def gemm_tc(ap: torch.Tensor, w: torch.Tensor, *, m: Optional[int] = None, m_dev
         g.h_split, g.hs_plane_rows, g.ld_hs = P(h_split), h_split.shape[1], h_split.stride(1)
     if row_stats is not None:
         g.row_stats, g.stats_vw = P(row_stats), stats_vw
+    g.kcb = kcb
     e0 = log_gemm_begin()
     _lib.call("fb_gemm_tc", C.byref(g), ap.shape[0], ap.shape[1], _lib.stream_ptr())
     log_gemm_end(e0, g.m_max, m_dev, g.n, k_alg if k_alg is not None else g.k)

@@ -35,6 +35,10 @@ from .fusion import _device
 from .synth import AsrDims, LmDims, SubwordLmDims
 
 KGRAN = 64           # K granule of the tensor-core GEMM (one 128 B swizzle atom of bf16)
+# Score-producing projections (AM / LM logits) drain the TMEM accumulator every
+# 64-K chunk: the tensor core's accumulation truncates, which otherwise biases
+# logits toward zero and shows up in long flat decodes.
+KCB_LOGITS = 1
 
 
 def _pad(k: int, g: int = KGRAN) -> int:
@@ -283,7 +287,7 @@ class DecoderStep:
         with tm("am_output"):
             K.pack(scratch, [(top, H, 1), (cur.ctx, C_, 1)], k_pad=ko, split=True, **kw)
             K.gemm_tc(scratch, w.w_out, k=ko, bias=w.b_out, out=logits, m=m, m_dev=m_dev,
-                      rows=rows, k_alg=H + C_)
+                      rows=rows, k_alg=H + C_, kcb=KCB_LOGITS)
             K.log_softmax_rows(logits, am_logp, d.vocab, m=m, m_dev=m_dev, rows=rows)
 
 
@@ -389,6 +393,10 @@ class LmWeights:
         self.in_width = H
         self.out_w = self.emb_w
         self.stats_vw = d.words
+        # the 65k-way output feeds look-ahead masses (sums over word ranges), not
+        # argmax-per-step scores: the default chunking is accurate enough there
+        # (c2 parity) and KCB_LOGITS would cost ~6% of the c2 decode
+        self.kcb_out = 0
 
 
 def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks,
@@ -420,7 +428,7 @@ def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks
         K.pack(scratch, [(state_dst[:, L - 1, 0], H, 0, state_dst.stride(0))], m=m, m_dev=m_dev,
                k_pad=w.k_out, split=True)
         kw = dict(m=m, m_dev=m_dev, k=w.k_out, bias=w.b_out, out=logits, row_stats=stats,
-                  stats_vw=w.stats_vw, k_alg=H)
+                  stats_vw=w.stats_vw, k_alg=H, kcb=w.kcb_out)
         if timer is not None:
             with timer("lm_out_gemm"):
                 K.gemm_tc(scratch, w.out_w, **kw)
@@ -516,6 +524,7 @@ class SubLmWeights:
         self.out_w = _devw(W["slm.out.w"], device, self.k_out)
         self.b_out = _dev(W["slm.out.b"], device)
         self.stats_vw = 0
+        self.kcb_out = KCB_LOGITS
         self.k_max = max([l.k_pad for l in self.layers] + [self.k_out])
 
 
@@ -611,7 +620,7 @@ def subword_step(w: SubLmWeights, *, m: int, m_dev, rows, parent, last_tok, eos_
                   c_out=cur.c[l], h_out=cur.h[l], k_alg=lay.k_in, **kw)
     K.pack(scratch, [(cur.h[L - 1], H, 1)], k_pad=w.k_out, split=True, **kw)
     K.gemm_tc(scratch, w.out_w, k=w.k_out, bias=w.b_out, out=logits, m=m, m_dev=m_dev,
-              rows=rows, k_alg=H)
+              rows=rows, k_alg=H, kcb=w.kcb_out)
     _lib.call("fb_row_logsumexp", m, P_(m_dev), P_(rows), P_(logits), logits.stride(0),
               w.d.vocab, pad_id, P_(norm), _lib.stream_ptr())
 
