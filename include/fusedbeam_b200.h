@@ -274,19 +274,27 @@ int fb_log_softmax_rows(int32_t m_max, const int32_t* m_dev, const int32_t* rows
 
 /* Bahdanau attention step for every active utterance:
  * e[r,t] = v . tanh(K[u,t] + q[r]); a = softmax_t(e) over t < t_enc[u];
- * `keys` holds E_K = exp(2 K) (fb_exp2x), so tanh(k+q) = 1 - 2/(1 + E_k E_q);
+ * `keys` holds E_K^T = exp(2 K) per utterance as [num_utts][att_dim][t_max]
+ * (fb_keys_exp2t), so tanh(k+q) = 1 - 2/(1 + E_k E_q);
  * ctx[r] = sum_t a[r,t] enc[u,t]; acc_out[r] = acc_in[parent[r]] + a[r]
  * (fp64) and its coverage (cfg->cov_mode).  Rows r = u*beam + i, i < n_live[u].
- * energy_ws: scratch [num_utts*beam, t_max] fp32. */
+ * q is consumed in place: its live rows are overwritten with E_q = exp(2 q).
+ * energy_ws: scratch [num_utts*beam, t_max] fp32; holds the attention
+ * weights a[r, t] on return. */
 int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts, const int32_t* active,
                       const int32_t* n_live, const int32_t* t_enc, const float* keys,
                       const float* enc, int32_t att_dim, int32_t ctx_dim, const float* v,
-                      const float* q, int64_t ldq, const int32_t* parent, const double* acc_in,
+                      float* q, int64_t ldq, const int32_t* parent, const double* acc_in,
                       double* acc_out, double* cov_out, float* ctx_out, int64_t ld_ctx,
                       float* attn_out, int64_t ld_attn, float* energy_ws, void* stream);
 
 /* y[i] = exp(2 x[i]) (attention keys -> E_K, once per batch). */
 int fb_exp2x(int64_t n, const float* x, float* y, void* stream);
+
+/* ekt[u][a][t] = exp(2 keys[u][t][a]) for u < num_utts, t < t_max, a < att_dim:
+ * the attention keys in the layout fb_attention_step reads (out of place). */
+int fb_keys_exp2t(int32_t num_utts, int32_t t_max, int32_t att_dim, const float* keys,
+                  float* ekt, void* stream);
 
 /* ---- word-LM bookkeeping for the fused engine ---------------------------- */
 /* Speculative <eos> events (fusion.py:181-183): for every listed row whose

@@ -100,6 +100,7 @@ _SIGS = {
     "fb_eos_fixup": (C.c_int, [i32, vp, vp, vp, vp, i64, i32, vp]),
     "fb_copy_rows": (C.c_int, [i32, vp, vp, vp, vp, vp, i64, vp]),
     "fb_exp2x": (C.c_int, [i64, vp, vp, vp]),
+    "fb_keys_exp2t": (C.c_int, [i32, i32, i32, vp, vp, vp]),
 }
 
 _OPTIONAL = {}

@@ -7,6 +7,8 @@
 // decoder.py:419-425 (accumulator), fusion.py:177-223 (LM events).
 #include "common.cuh"
 
+#include <cstdlib>
+
 #include <cuda_bf16.h>
 
 namespace fb {
@@ -180,13 +182,16 @@ __device__ double pairwise_sum_d(const double* a, int n, F f) {
 // (A) energies: CTA = (utterance, chunk of 8 x kEnWarps frames); warp = frame
 //     t; lanes split the attention dim; every live row's energy for frame t is
 //     a warp reduction.  MUFU-bound (ex2 + rcp per tanh).
-// (B) softmax / fp64 accumulator / coverage / context: CTA = (utterance, chunk
-//     of kCtxCols encoder columns); every CTA re-normalises its utterance's
-//     rows (cheap) and CTA 0 of the utterance owns the accumulator + coverage.
+// (B) softmax / fp64 accumulator / coverage / context: CTA = (utterance, group
+//     of RB rows), thread = 4 encoder columns: the encoder output is streamed
+//     from HBM once per row group (HBM-bound; it does not fit L2 at c2).
 constexpr int kEnWarps = 8;
-constexpr int kEnFrames = 4;          // frames per warp
+
 constexpr int kMaxBeam = 512;
-constexpr int kCtxCols = 128;
+constexpr int kCtxMaxThreads = 512;   // context CTA: one thread per 4 encoder columns
+// 1 + E_k E_q clamp: tanh is saturated (2/(1+1e18) = 2e-18) and a product of
+// two clamped terms (1e36) stays below FLT_MAX
+constexpr float kDMax2 = 1.0e18f;
 
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
@@ -199,61 +204,237 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // e_t = sum_a v_a - 2 sum_a v_a / (1 + E_k E_q).  The constant sum_a v_a
 // cancels in the softmax, so the kernel stores e'_t = -2 sum_a v_a / (1 + E_k E_q):
 // one FFMA + one MUFU.RCP + one FFMA per (row, frame, a).
+// Softmax over frames + fp64 accumulator + coverage (decoder.py:421-425) for
+// one row, by one warp: alpha[t] = softmax(e)[t] (e may live in shared memory,
+// alpha in global), acc_out = acc_in[parent] + alpha (fp64), coverage.
+__device__ __forceinline__ void softmax_row(const fb_search_cfg_t& cfg, int r, int T, int TM,
+                                            const float* e, float* alpha, const int32_t* parent,
+                                            const double* acc_in, double* acc_out,
+                                            double* cov_out, float* attn_out, int64_t ld_attn,
+                                            int lane) {
+  float mx = -INFINITY;
+  for (int t = lane; t < T; t += 32) mx = fmaxf(mx, e[t]);
+  for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  float sum = 0.f;
+  for (int t = lane; t < T; t += 32) sum += expf(e[t] - mx);
+  for (int off = 16; off; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+  const float inv = 1.0f / sum;
+  const int p = parent ? parent[r] : r;
+  const double* a0 = acc_in + (int64_t)p * TM;
+  double* a1 = acc_out + (int64_t)r * TM;
+  int cnt = 0;
+  for (int t = lane; t < T; t += 32) {
+    const float a = expf(e[t] - mx) * inv;
+    alpha[t] = a;
+    const double x = dadd(a0[t], (double)a);
+    a1[t] = x;
+    cnt += x > cfg.tau1;
+    if (attn_out) attn_out[(int64_t)r * ld_attn + t] = a;
+  }
+  if (cfg.cov_mode != 0) {
+    for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+    __syncwarp();
+    if (lane == 0) {
+      double cov;
+      if (cfg.cov_mode == 1) {
+        cov = (double)cnt;
+      } else {
+        const double tau2 = cfg.tau2, mg = cfg.cov_margin;
+        const double pen = pairwise_sum_d(a1, T, [=](double x) {
+          return x > tau2 ? dsub(dadd(mg, x), tau2) : 0.0;
+        });
+        cov = dsub((double)cnt, pen);
+      }
+      cov_out[r] = cov;
+    }
+  }
+}
+
+// Separate softmax pass (utterances longer than one energy CTA): one warp per
+// live row; alpha overwrites the energy row in place.
+__global__ void __launch_bounds__(256)
+att_softmax_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
+                   const int32_t* __restrict__ n_live, const int32_t* __restrict__ t_enc,
+                   float* __restrict__ energy, const int32_t* __restrict__ parent,
+                   const double* __restrict__ acc_in, double* __restrict__ acc_out,
+                   double* __restrict__ cov_out, float* __restrict__ attn_out, int64_t ld_attn) {
+  const int u = blockIdx.x;
+  if (!active[u]) return;
+  const int i = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= n_live[u]) return;
+  const int r = u * cfg.beam + i;
+  float* e = energy + (int64_t)r * cfg.t_max;
+  softmax_row(cfg, r, t_enc[u], cfg.t_max, e, e, parent, acc_in, acc_out, cov_out, attn_out,
+              ld_attn, threadIdx.x & 31);
+}
+
+// packed fp32 pairs (sm_100 FFMA2 / FMUL2: two lanes of work per issue)
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t pk2(float a, float b) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void up2(f2_t x, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x));
+}
+__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
+  f2_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) {
+  f2_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
 template <int R>
 __global__ void __launch_bounds__(kEnWarps * 32)
 att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
                   const int32_t* __restrict__ n_live, const int32_t* __restrict__ t_enc,
-                  const float* __restrict__ ekeys, int A, const float* __restrict__ v,
-                  const float* __restrict__ q, int64_t ldq, float* __restrict__ energy) {
+                  const float* __restrict__ ekt, int A, const float* __restrict__ v,
+                  const float* __restrict__ q, int64_t ldq, float* __restrict__ energy,
+                  int fuse, const int32_t* __restrict__ parent,
+                  const double* __restrict__ acc_in, double* __restrict__ acc_out,
+                  double* __restrict__ cov_out, float* __restrict__ attn_out, int64_t ld_attn) {
+  // CTA = (utterance, chunk of kEnWarps*32 frames, group of R rows); lane = one
+  // frame t, so every energy is a private register sum (no cross-lane
+  // reduction).  Keys are read transposed (E_K^T[u][a][t]: coalesced across
+  // lanes); E_q (row pairs interleaved) and v are shared-memory broadcasts.
+  // Work per (row pair, dim pair) = 4 terms v_a / d_a, d_a = 1 + E_k E_q:
+  //   v0/d0 + v1/d1 = (v0 d1 + v1 d0) / (d0 d1)   -- one reciprocal per two
+  // terms, rows paired in f32x2 registers (FFMA2/FMUL2); d clamped to kDMax2
+  // so the product stays finite (tanh is saturated long before).
+  static_assert(R % 2 == 0, "rows come in pairs");
   const int u = blockIdx.x;
   if (!active[u]) return;
   const int T = t_enc[u];
-  const int t_base = blockIdx.y * (kEnWarps * kEnFrames);
-  if (t_base >= T) return;
+  const int t0 = blockIdx.y * (kEnWarps * 32);
+  if (t0 >= T) return;
+  const int n = n_live[u];
+  const int r0 = blockIdx.z * R;
+  if (r0 >= n) return;
+  const int rows = min(R, n - r0);
   extern __shared__ float sm[];
   const int K = cfg.beam, TM = cfg.t_max;
-  const int n = n_live[u];
-  const int npass = (n + R - 1) / R;
-  float* vs = sm;                  // [A]
-  float* qs = sm + A;              // [npass*R][A]  E_q = exp(2 q); rows >= n are 0
+  float2* vs2 = reinterpret_cast<float2*>(sm);          // [A]  (v_a, v_a)
+  float2* qs2 = vs2 + A;                                // [R/2][A] (Eq_r, Eq_r+1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int slot0 = u * K;
-  for (int j = tid; j < npass * R * A; j += blockDim.x) {
-    const int i = j / A, a = j - i * A;
-    qs[j] = i < n ? expf(2.0f * q[(int64_t)(slot0 + i) * ldq + a]) : 0.f;
+  const int slot0 = u * K + r0;
+  for (int j = tid; j < (R / 2) * A; j += blockDim.x) {
+    const int rp = j / A, a = j - rp * A;
+    const int ra = 2 * rp, rb = ra + 1;
+    qs2[j] = make_float2(ra < rows ? q[(int64_t)(slot0 + ra) * ldq + a] : 0.f,
+                         rb < rows ? q[(int64_t)(slot0 + rb) * ldq + a] : 0.f);
   }
-  for (int a = tid; a < A; a += blockDim.x) vs[a] = v[a];
+  for (int a = tid; a < A; a += blockDim.x) vs2[a] = make_float2(v[a], v[a]);
   __syncthreads();
-  const float* ku = ekeys + (int64_t)u * TM * A;
-  for (int f = 0; f < kEnFrames; ++f) {
-    const int t = t_base + warp * kEnFrames + f;
-    if (t >= T) break;
-    const float* kt = ku + (int64_t)t * A;
-    for (int ps = 0; ps < npass; ++ps) {
-      float e[R];
+  const int t = t0 + warp * 32 + lane;
+  const bool valid = t < T;
+  // fuse: the whole utterance is this CTA's frame chunk (T <= 256), so the
+  // softmax / accumulator / coverage run here on the energies in shared memory
+  float* es = reinterpret_cast<float*>(qs2 + (R / 2) * A);   // [R][kEnWarps*32]
+  if (t0 + warp * 32 < T) {
+  const float* kt = ekt + (int64_t)u * A * TM + (valid ? t : T - 1);
+  const f2_t one2 = pk2(1.0f, 1.0f);
+  f2_t e2[R / 2];
 #pragma unroll
-      for (int r = 0; r < R; ++r) e[r] = 0.f;
-      for (int a = lane; a < A; a += 32) {
-        const float ek = __ldg(kt + a);
-        const float va = vs[a];
-        const float* qa = qs + (ps * R) * A + a;
+  for (int rp = 0; rp < R / 2; ++rp) e2[rp] = pk2(0.f, 0.f);
+  // keys for dims a..a+3 in registers, a+4..a+7 in flight (A % 4 == 0)
+  float kc[4], kn[4];
 #pragma unroll
-        for (int r = 0; r < R; ++r) e[r] = fmaf(va, rcp_approx(fmaf(ek, qa[r * A], 1.0f)), e[r]);
-      }
+  for (int j = 0; j < 4; ++j) kc[j] = __ldg(kt + (int64_t)j * TM);
+  for (int a = 0; a < A; a += 4) {
+    const bool more = a + 4 < A;
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        float x = e[r];
-        for (int off = 16; off; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-        e[r] = x;
-      }
-      const int row = ps * R + lane;
-      if (lane < R && row < n) {
-        float x = 0.f;
+    for (int j = 0; j < 4; ++j) kn[j] = more ? __ldg(kt + (int64_t)(a + 4 + j) * TM) : 0.f;
 #pragma unroll
-        for (int r = 0; r < R; ++r) x = lane == r ? e[r] : x;
-        energy[(int64_t)(slot0 + row) * TM + t] = -2.0f * x;
+    for (int h = 0; h < 2; ++h) {
+      const f2_t K0 = pk2(kc[2 * h], kc[2 * h]), K1 = pk2(kc[2 * h + 1], kc[2 * h + 1]);
+      const float4 vv = *reinterpret_cast<const float4*>(vs2 + a + 2 * h);   // (v0,v0,v1,v1)
+      const f2_t V0 = pk2(vv.x, vv.y), V1 = pk2(vv.z, vv.w);
+#pragma unroll
+      for (int rp = 0; rp < R / 2; ++rp) {
+        const float4 qq = *reinterpret_cast<const float4*>(qs2 + rp * A + a + 2 * h);
+        f2_t d0 = fma2(K0, pk2(qq.x, qq.y), one2);
+        f2_t d1 = fma2(K1, pk2(qq.z, qq.w), one2);
+        float x0, y0, x1, y1;
+        up2(d0, x0, y0);
+        up2(d1, x1, y1);
+        d0 = pk2(fminf(x0, kDMax2), fminf(y0, kDMax2));
+        d1 = pk2(fminf(x1, kDMax2), fminf(y1, kDMax2));
+        const f2_t num = fma2(V0, d1, mul2(V1, d0));
+        const f2_t den = mul2(d0, d1);
+        float dx, dy;
+        up2(den, dx, dy);
+        e2[rp] = fma2(num, pk2(rcp_approx(dx), rcp_approx(dy)), e2[rp]);
       }
     }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) kc[j] = kn[j];
+  }
+  if (valid) {
+#pragma unroll
+    for (int rp = 0; rp < R / 2; ++rp) {
+      float ea, eb;
+      up2(e2[rp], ea, eb);
+      if (fuse) {
+        es[(2 * rp) * (kEnWarps * 32) + t] = -2.0f * ea;
+        es[(2 * rp + 1) * (kEnWarps * 32) + t] = -2.0f * eb;
+      } else {
+        if (2 * rp < rows) energy[(int64_t)(slot0 + 2 * rp) * TM + t] = -2.0f * ea;
+        if (2 * rp + 1 < rows) energy[(int64_t)(slot0 + 2 * rp + 1) * TM + t] = -2.0f * eb;
+      }
+    }
+  }
+  }
+  if (!fuse) return;
+  __syncthreads();
+  for (int i = warp; i < rows; i += kEnWarps)
+    softmax_row(cfg, slot0 + i, T, TM, es + i * (kEnWarps * 32),
+                energy + (int64_t)(slot0 + i) * TM, parent, acc_in, acc_out, cov_out, attn_out,
+                ld_attn, lane);
+}
+
+// E_q = exp(2 q) in place for the live rows of active utterances (once per
+// step, instead of once per energy CTA)
+__global__ void query_exp_kernel(int num_utts, int beam, const int32_t* __restrict__ active,
+                                 const int32_t* __restrict__ n_live, float* __restrict__ q,
+                                 int64_t ldq, int nq4) {
+  const int64_t total = (int64_t)num_utts * beam * nq4;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / nq4), a4 = (int)(idx - (int64_t)r * nq4);
+    const int u = r / beam, i = r - u * beam;
+    if (!active[u] || i >= n_live[u]) continue;
+    float4* p = reinterpret_cast<float4*>(q + (int64_t)r * ldq) + a4;
+    float4 x = *p;
+    x.x = expf(2.0f * x.x);
+    x.y = expf(2.0f * x.y);
+    x.z = expf(2.0f * x.z);
+    x.w = expf(2.0f * x.w);
+    *p = x;
+  }
+}
+
+// ekt[u][a][t] = exp(2 k[u][t][a]): the attention keys in the layout the
+// energy kernel reads (32 x 32 tiles through shared memory)
+__global__ void keys_exp2t_kernel(int t_max, int A, const float* __restrict__ k,
+                                  float* __restrict__ ekt) {
+  __shared__ float tile[32][33];
+  const int u = blockIdx.z;
+  const int t0 = blockIdx.x * 32, a0 = blockIdx.y * 32;
+  const float* ku = k + (int64_t)u * t_max * A;
+  float* eu = ekt + (int64_t)u * A * t_max;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int t = t0 + i, a = a0 + threadIdx.x;
+    tile[i][threadIdx.x] = (t < t_max && a < A) ? expf(2.0f * ku[(int64_t)t * A + a]) : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int a = a0 + i, t = t0 + threadIdx.x;
+    if (a < A && t < t_max) eu[(int64_t)a * t_max + t] = tile[threadIdx.x][i];
   }
 }
 
@@ -263,142 +444,87 @@ __global__ void exp2x_kernel(int64_t n, const float* __restrict__ x, float* __re
     y[i] = expf(2.0f * x[i]);
 }
 
+
 template <int RB>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kCtxMaxThreads)
 att_context_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
                    const int32_t* __restrict__ n_live, const int32_t* __restrict__ t_enc,
-                   const float* __restrict__ enc, int C, const float* __restrict__ energy,
-                   const int32_t* __restrict__ parent, const double* __restrict__ acc_in,
-                   double* __restrict__ acc_out, double* __restrict__ cov_out,
-                   float* __restrict__ ctx_out, int64_t ld_ctx, float* __restrict__ attn_out,
-                   int64_t ld_attn) {
+                   const float* __restrict__ enc, int C, const float* __restrict__ alpha,
+                   float* __restrict__ ctx_out, int64_t ld_ctx) {
+  // CTA = (utterance, group of RB rows, column chunk); thread = 4 adjacent
+  // encoder columns (float4 loads, register double buffer), alpha tile in smem
   const int u = blockIdx.x;
   if (!active[u]) return;
-  const int c0 = blockIdx.y * kCtxCols;
-  if (c0 >= C) return;
+  const int n = n_live[u];
+  const int g0 = blockIdx.y * RB;
+  if (g0 >= n) return;
+  const int rows = min(RB, n - g0);
   extern __shared__ float sm[];
   const int K = cfg.beam, TM = cfg.t_max;
-  const int n = n_live[u];
   const int T = t_enc[u];
-  // per-row softmax statistics only; weights are re-derived from the energy
-  // rows (L2-resident) per row group, so shared memory is O(RB * T) for any beam
-  constexpr int RBS = RB + 4;      // padded row stride of the transposed group (float4-aligned)
-  float* st_mx = sm;                                   // [n]
-  float* st_inv = sm + n;                              // [n]
-  float* at = sm + ((2 * n + 3) & ~3);                 // [T][RBS]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int slot0 = u * K;
-  // softmax over frames, one warp per row (every column chunk recomputes it)
-  for (int i = warp; i < n; i += nw) {
-    const float* e = energy + (int64_t)(slot0 + i) * TM;
-    float mx = -INFINITY;
-    for (int t = lane; t < T; t += 32) mx = fmaxf(mx, e[t]);
-    for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    float s = 0.f;
-    for (int t = lane; t < T; t += 32) s += expf(e[t] - mx);
-    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) {
-      st_mx[i] = mx;
-      st_inv[i] = 1.0f / s;
-    }
+  float* at = sm;                                      // [T][RB] alpha, transposed
+  const int tid = threadIdx.x;
+  const int slot0 = u * K + g0;
+  const int col = 4 * (blockIdx.z * blockDim.x + tid);
+  const bool has_col = col < C;
+  const float* eu = enc + (int64_t)u * TM * C + (has_col ? col : 0);
+  constexpr int TU = 8;
+  float4 xn[TU];
+  if (has_col && TU <= T) {       // first frames in flight before the alpha tile
+#pragma unroll
+    for (int j = 0; j < TU; ++j) xn[j] = __ldg(reinterpret_cast<const float4*>(eu + (int64_t)j * C));
   }
-  const float* eu = enc + (int64_t)u * TM * C;
-  const int col = c0 + 2 * tid;
-  for (int g0 = 0; g0 < n; g0 += RB) {
-  __syncthreads();
   for (int j = tid; j < T * RB; j += blockDim.x) {
     const int r = j / T, t = j - r * T;
-    at[t * RBS + r] = g0 + r < n ? expf(energy[(int64_t)(slot0 + g0 + r) * TM + t] -
-                                        st_mx[g0 + r]) * st_inv[g0 + r]
-                                 : 0.f;
+    at[t * RB + r] = r < rows ? alpha[(int64_t)(slot0 + r) * TM + t] : 0.f;
   }
   __syncthreads();
-  // context columns [c0, c0 + kCtxCols): thread = 2 adjacent columns (float2),
-  // rows g0..g0+RB; 8 frames of enc in flight per thread
-  if (tid < kCtxCols / 2 && col < C) {
-    const bool pair = col + 1 < C;
-    float acc0[RB], acc1[RB];
+  if (!has_col) return;
+  float4 acc[RB];
 #pragma unroll
-    for (int r = 0; r < RB; ++r) acc0[r] = acc1[r] = 0.f;
-    constexpr int TU = 8;
-    int t = 0;
-    for (; t + TU <= T; t += TU) {
-      float2 x[TU];
+  for (int r = 0; r < RB; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+  int t = 0;
+  for (; t + TU <= T; t += TU) {
+    float4 x[TU];
+#pragma unroll
+    for (int j = 0; j < TU; ++j) x[j] = xn[j];
+    if (t + 2 * TU <= T) {
 #pragma unroll
       for (int j = 0; j < TU; ++j)
-        x[j] = pair ? __ldg(reinterpret_cast<const float2*>(eu + (int64_t)(t + j) * C + col))
-                    : make_float2(__ldg(eu + (int64_t)(t + j) * C + col), 0.f);
+        xn[j] = __ldg(reinterpret_cast<const float4*>(eu + (int64_t)(t + TU + j) * C));
+    }
 #pragma unroll
-      for (int j = 0; j < TU; ++j) {
-        const float4* a4 = reinterpret_cast<const float4*>(at + (t + j) * RBS);
+    for (int j = 0; j < TU; ++j) {
+      const float4* a4 = reinterpret_cast<const float4*>(at + (t + j) * RB);
 #pragma unroll
-        for (int q4 = 0; q4 < RB / 4; ++q4) {
-          const float4 w = a4[q4];
-          acc0[4 * q4] = fmaf(w.x, x[j].x, acc0[4 * q4]);
-          acc0[4 * q4 + 1] = fmaf(w.y, x[j].x, acc0[4 * q4 + 1]);
-          acc0[4 * q4 + 2] = fmaf(w.z, x[j].x, acc0[4 * q4 + 2]);
-          acc0[4 * q4 + 3] = fmaf(w.w, x[j].x, acc0[4 * q4 + 3]);
-          acc1[4 * q4] = fmaf(w.x, x[j].y, acc1[4 * q4]);
-          acc1[4 * q4 + 1] = fmaf(w.y, x[j].y, acc1[4 * q4 + 1]);
-          acc1[4 * q4 + 2] = fmaf(w.z, x[j].y, acc1[4 * q4 + 2]);
-          acc1[4 * q4 + 3] = fmaf(w.w, x[j].y, acc1[4 * q4 + 3]);
+      for (int q4 = 0; q4 < RB / 4; ++q4) {
+        const float4 w = a4[q4];
+        const float wr[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float4& o = acc[4 * q4 + k];
+          o.x = fmaf(wr[k], x[j].x, o.x);
+          o.y = fmaf(wr[k], x[j].y, o.y);
+          o.z = fmaf(wr[k], x[j].z, o.z);
+          o.w = fmaf(wr[k], x[j].w, o.w);
         }
       }
     }
-    for (; t < T; ++t) {
-      const float x0 = __ldg(eu + (int64_t)t * C + col);
-      const float x1 = pair ? __ldg(eu + (int64_t)t * C + col + 1) : 0.f;
-#pragma unroll
-      for (int r = 0; r < RB; ++r) {
-        acc0[r] = fmaf(at[t * RBS + r], x0, acc0[r]);
-        acc1[r] = fmaf(at[t * RBS + r], x1, acc1[r]);
-      }
-    }
+  }
+  for (; t < T; ++t) {
+    const float4 x = __ldg(reinterpret_cast<const float4*>(eu + (int64_t)t * C));
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
-      if (g0 + r < n) {
-        float* o = ctx_out + (int64_t)(slot0 + g0 + r) * ld_ctx + col;
-        o[0] = acc0[r];
-        if (pair) o[1] = acc1[r];
-      }
+      const float w = at[t * RB + r];
+      acc[r].x = fmaf(w, x.x, acc[r].x);
+      acc[r].y = fmaf(w, x.y, acc[r].y);
+      acc[r].z = fmaf(w, x.z, acc[r].z);
+      acc[r].w = fmaf(w, x.w, acc[r].w);
     }
   }
-  }
-  if (blockIdx.y != 0) return;
-  // fp64 accumulator + coverage (decoder.py:421-425), one warp per row
-  for (int i = warp; i < n; i += nw) {
-    const int r = slot0 + i;
-    const int p = parent ? parent[r] : r;
-    const double* a0 = acc_in + (int64_t)p * TM;
-    double* a1 = acc_out + (int64_t)r * TM;
-    const float* e = energy + (int64_t)r * TM;
-    const float mx = st_mx[i], inv = st_inv[i];
-    int cnt = 0;
-    for (int t = lane; t < T; t += 32) {
-      const float a = expf(e[t] - mx) * inv;
-      const double x = dadd(a0[t], (double)a);
-      a1[t] = x;
-      cnt += x > cfg.tau1;
-      if (attn_out) attn_out[(int64_t)r * ld_attn + t] = a;
-    }
-    if (cfg.cov_mode != 0) {
-      for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
-      __syncwarp();
-      if (lane == 0) {
-        double cov;
-        if (cfg.cov_mode == 1) {
-          cov = (double)cnt;
-        } else {
-          const double tau2 = cfg.tau2, mg = cfg.cov_margin;
-          const double pen = pairwise_sum_d(a1, T, [=](double x) {
-            return x > tau2 ? dsub(dadd(mg, x), tau2) : 0.0;
-          });
-          cov = dsub((double)cnt, pen);
-        }
-        cov_out[r] = cov;
-      }
-    }
-  }
+#pragma unroll
+  for (int r = 0; r < RB; ++r)
+    if (r < rows) *reinterpret_cast<float4*>(ctx_out + (int64_t)(slot0 + r) * ld_ctx + col) = acc[r];
 }
 
 // ---------------------------------------------------------- LM bookkeeping --
@@ -596,7 +722,7 @@ extern "C" int fb_row_logsumexp(int32_t m_max, const int32_t* m_dev, const int32
 extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
                                  const int32_t* active, const int32_t* n_live,
                                  const int32_t* t_enc, const float* keys, const float* enc,
-                                 int32_t att_dim, int32_t ctx_dim, const float* v, const float* q,
+                                 int32_t att_dim, int32_t ctx_dim, const float* v, float* q,
                                  int64_t ldq, const int32_t* parent, const double* acc_in,
                                  double* acc_out, double* cov_out, float* ctx_out,
                                  int64_t ld_ctx, float* attn_out, int64_t ld_attn,
@@ -605,35 +731,48 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
                "null attention args");
   FB_CHECK_ARG(cfg->cov_mode == 0 || cov_out, "coverage output required");
   FB_CHECK_ARG(cfg->beam <= kMaxBeam, "beam too large for the attention kernels");
+  FB_CHECK_ARG(att_dim % 4 == 0 && ldq % 4 == 0,
+               "attention dim and query stride must be multiples of 4");
   if (num_utts <= 0) return FB_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  const int RE = cfg->beam >= 16 ? 16 : (cfg->beam + 1) & ~1;   // rows per energy pass
-  const int npass = (cfg->beam + RE - 1) / RE;
-  const size_t sm_e = sizeof(float) * ((size_t)npass * RE * att_dim + att_dim);
+  static const int re_env = [] {                      // dev override (experiments)
+    const char* e = getenv("FB_ATT_RE");
+    return e ? atoi(e) : 0;
+  }();
+  const int RE = re_env > 0 ? re_env
+                            : (cfg->beam >= 16 ? 16 : (cfg->beam + 1) & ~1);   // rows per energy CTA
+  const bool fuse = cfg->t_max <= kEnWarps * 32;     // one energy CTA spans the utterance
+  const size_t sm_e = sizeof(float) * ((size_t)RE * att_dim + 2 * (size_t)att_dim +
+                                       (fuse ? (size_t)RE * kEnWarps * 32 : 0));
   const int RB = cfg->beam <= 4 ? 4 : cfg->beam <= 8 ? 8 : cfg->beam <= 12 ? 12 : 16;
-  const size_t sm_c = sizeof(float) * ((size_t)2 * cfg->beam + 4 + (size_t)(RB + 4) * cfg->t_max);
+  const size_t sm_c = sizeof(float) * (size_t)RB * cfg->t_max;
   if (sm_e > 200 * 1024 || sm_c > 200 * 1024)
     return fail(FB_ERR_CONFIG, "attention working set exceeds shared memory");
+  FB_CHECK_ARG(ctx_dim % 4 == 0 && ctx_dim <= 4 * kCtxMaxThreads && ld_ctx % 4 == 0,
+               "context dim must be a multiple of 4 and <= 2048");
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(att_energy_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(att_energy_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(att_energy_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(att_energy_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(att_energy_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(att_energy_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(att_energy_kernel<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(att_energy_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(att_context_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(att_context_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(att_context_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(att_context_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+#define FB_ATTR(R) cudaFuncSetAttribute(att_energy_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
+    FB_ATTR(2); FB_ATTR(4); FB_ATTR(6); FB_ATTR(8); FB_ATTR(10); FB_ATTR(12); FB_ATTR(14); FB_ATTR(16);
+#undef FB_ATTR
     attr_set = true;
   }
-  dim3 ge(num_utts, (cfg->t_max + kEnWarps * kEnFrames - 1) / (kEnWarps * kEnFrames));
+  {
+    const int64_t total = (int64_t)num_utts * cfg->beam * (att_dim / 4);
+    query_exp_kernel<<<(int)std::min<int64_t>((total + 255) / 256, kNumSMs * 8), 256, 0, s>>>(
+        num_utts, cfg->beam, active, n_live, q, ldq, att_dim / 4);
+    count_launch();
+  }
+  dim3 ge(num_utts, (cfg->t_max + kEnWarps * 32 - 1) / (kEnWarps * 32), (cfg->beam + RE - 1) / RE);
 #define FB_EN(R)                                                                              \
   att_energy_kernel<R><<<ge, kEnWarps * 32, sm_e, s>>>(*cfg, active, n_live, t_enc, keys, att_dim, \
-                                                        v, q, ldq, energy_ws)
+                                                        v, q, ldq, energy_ws, fuse ? 1 : 0,    \
+                                                        parent, acc_in, acc_out, cov_out,      \
+                                                        attn_out, ld_attn)
   switch (RE) {
     case 2: FB_EN(2); break;
     case 4: FB_EN(4); break;
@@ -648,11 +787,28 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
   count_launch();
   int rc = check_launch("att_energy");
   if (rc) return rc;
-  dim3 gc(num_utts, (ctx_dim + kCtxCols - 1) / kCtxCols);
+  if (!fuse) {
+    dim3 gs(num_utts, (cfg->beam + 7) / 8);
+    att_softmax_kernel<<<gs, 256, 0, s>>>(*cfg, active, n_live, t_enc, energy_ws, parent, acc_in,
+                                         acc_out, cov_out, attn_out, ld_attn);
+    count_launch();
+    rc = check_launch("att_softmax");
+    if (rc) return rc;
+  }
+  // column split so that the grid covers the SMs a few times over (the kernel
+  // streams the encoder output; more CTAs = more bytes in flight)
+  const int groups = (cfg->beam + RB - 1) / RB;
+  const int quads = ctx_dim / 4;
+  int csplit = 1;
+  while (csplit < 8 && (int64_t)num_utts * groups * csplit < 4 * kNumSMs &&
+         quads / (2 * csplit) >= 32)
+    csplit *= 2;
+  const int qpc = (quads + csplit - 1) / csplit;
+  dim3 gc(num_utts, groups, csplit);
+  const int ctx_threads = ((qpc + 31) / 32) * 32;
 #define FB_CTX(R)                                                                             \
-  att_context_kernel<R><<<gc, 256, sm_c, s>>>(*cfg, active, n_live, t_enc, enc, ctx_dim,       \
-                                              energy_ws, parent, acc_in, acc_out, cov_out,    \
-                                              ctx_out, ld_ctx, attn_out, ld_attn)
+  att_context_kernel<R><<<gc, ctx_threads, sm_c, s>>>(*cfg, active, n_live, t_enc, enc, ctx_dim, \
+                                                      energy_ws, ctx_out, ld_ctx)
   if (RB == 4) FB_CTX(4); else if (RB == 8) FB_CTX(8); else if (RB == 12) FB_CTX(12); else FB_CTX(16);
 #undef FB_CTX
   count_launch();
@@ -702,6 +858,17 @@ extern "C" int fb_copy_rows(int32_t n_max, const int32_t* n_dev, const int32_t* 
       n_max, n_dev, src_idx, dst_idx, (const char*)src, (char*)dst, row_bytes);
   count_launch();
   return check_launch("copy_rows");
+}
+
+extern "C" int fb_keys_exp2t(int32_t num_utts, int32_t t_max, int32_t att_dim, const float* keys,
+                             float* ekt, void* stream) {
+  FB_CHECK_ARG(keys && ekt && keys != ekt && num_utts >= 0 && t_max > 0 && att_dim > 0,
+               "bad key transpose arguments");
+  if (num_utts == 0) return FB_OK;
+  dim3 g((t_max + 31) / 32, (att_dim + 31) / 32, num_utts);
+  keys_exp2t_kernel<<<g, dim3(32, 8), 0, (cudaStream_t)stream>>>(t_max, att_dim, keys, ekt);
+  count_launch();
+  return check_launch("keys_exp2t");
 }
 
 extern "C" int fb_exp2x(int64_t n, const float* x, float* y, void* stream) {

@@ -174,7 +174,7 @@ class _Session:
         self.am_logp = torch.zeros((N, V), dtype=torch.float32, device=dev)
         self.energy = torch.empty((N, TM), dtype=torch.float32, device=dev)
         self.enc = torch.empty((B, TM, C_), dtype=torch.float32, device=dev)
-        self.keys = torch.empty((B * TM, d.att), dtype=torch.float32, device=dev)
+        self.keys = torch.empty((B, d.att, TM), dtype=torch.float32, device=dev)   # E_K^T
         self.slots0 = torch.arange(B, dtype=torch.int32, device=dev) * Kb
         self.fus_buf = None
         self.lm = None

@@ -231,14 +231,17 @@ class Encoder:
             enc.view(B * TM, C_).copy_(X[:, :C_])
         else:
             enc = X[:, :C_].contiguous()
-            keys = torch.empty((B * TM, d.att), dtype=torch.float32, device=dev)
+            keys = torch.empty((B, d.att, TM), dtype=torch.float32, device=dev)
         kk = self.w.w_k.shape[1]
         K.pack(big, [(X, kk, 0)], m=B * TM, k_pad=kk, split=True)
-        K.gemm_tc(big[:, :, :kk], self.w.w_k, m=B * TM, k=kk, bias=self.w.b_k, out=keys,
+        kraw = torch.empty((B * TM, d.att), dtype=torch.float32, device=dev)
+        K.gemm_tc(big[:, :, :kk], self.w.w_k, m=B * TM, k=kk, bias=self.w.b_k, out=kraw,
                   k_alg=C_)
-        # the attention kernels consume E_K = exp(2 K) (tanh via one reciprocal)
-        _lib.call("fb_exp2x", keys.numel(), _lib.ptr(keys), _lib.ptr(keys), _lib.stream_ptr())
-        return enc.view(B, TM, C_), keys.view(B, TM, d.att), T
+        # the attention kernels consume E_K^T = exp(2 K) per utterance as [A, T]
+        # (tanh via one reciprocal; frames contiguous for the energy kernel)
+        _lib.call("fb_keys_exp2t", B, TM, d.att, _lib.ptr(kraw), _lib.ptr(keys),
+                  _lib.stream_ptr())
+        return enc.view(B, TM, C_), keys.view(B, d.att, TM), T
 
 
 class DecoderStep:
@@ -308,7 +311,7 @@ _null_timer = _NullSpan()
 @dataclass
 class _UttState:
     enc: torch.Tensor      # [1, T, C]
-    keys: torch.Tensor     # [1, T, A]
+    keys: torch.Tensor     # [1, A, T]  E_K^T = exp(2 K)
     T: int
     am: AmState            # n rows
 
