@@ -295,7 +295,13 @@ def main():
     X_host, T = scorer.encoder.stage([x for _, x in utts], pin=True)
     X_dev = X_host.to(scorer.device)
     ids = [u for u, _ in utts]
-    dec = FusedDecoder(scorer, fusion, cfg, d)
+    # the public API's cached engine: the device-resident timing and the e2e
+    # timing below share one session (buffers + captured step graphs)
+    if args.profile_only:
+        dec = FusedDecoder(scorer, fusion, cfg, d)
+    else:
+        decode_batch(feats[:1], scorer, fusion, cfg, d)
+        dec = next(iter(scorer._fused_cache.values()))
     log(f"[rank {rank}] setup {time.perf_counter() - t_setup:.1f}s; {len(utts)} utts, "
         f"{frames} frames")
 
@@ -308,6 +314,7 @@ def main():
     clocks.start()                       # process start-up stays out of the timed window
     for _ in range(args.warmup):
         res = dec.run(X_dev, T, ids)
+        decode_batch(feats, scorer, fusion, cfg, d)
     torch.cuda.synchronize()
 
     # ---- timed: device-resident inputs ----

@@ -280,13 +280,15 @@ int fb_log_softmax_rows(int32_t m_max, const int32_t* m_dev, const int32_t* rows
  * (fp64) and its coverage (cfg->cov_mode).  Rows r = u*beam + i, i < n_live[u].
  * q is consumed in place: its live rows are overwritten with E_q = exp(2 q).
  * energy_ws: scratch [num_utts*beam, t_max] fp32; holds the attention
- * weights a[r, t] on return. */
+ * weights a[r, t] on return.  sync_ws: num_utts*ceil(beam/2) int32, zero on the
+ * first call (the kernels leave it zeroed). */
 int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts, const int32_t* active,
                       const int32_t* n_live, const int32_t* t_enc, const float* keys,
                       const float* enc, int32_t att_dim, int32_t ctx_dim, const float* v,
                       float* q, int64_t ldq, const int32_t* parent, const double* acc_in,
                       double* acc_out, double* cov_out, float* ctx_out, int64_t ld_ctx,
-                      float* attn_out, int64_t ld_attn, float* energy_ws, void* stream);
+                      float* attn_out, int64_t ld_attn, float* energy_ws, int32_t* sync_ws,
+                      void* stream);
 
 /* y[i] = exp(2 x[i]) (attention keys -> E_K, once per batch). */
 int fb_exp2x(int64_t n, const float* x, float* y, void* stream);

@@ -89,7 +89,7 @@ _SIGS = {
     "fb_log_softmax_rows": (C.c_int, [i32, vp, vp, vp, i64, i32, vp, i64, vp]),
     "fb_row_logsumexp": (C.c_int, [i32, vp, vp, vp, i64, i32, i32, vp, vp]),
     "fb_attention_step": (C.c_int, [C.POINTER(FbSearchCfg), i32, vp, vp, vp, vp, vp, i32, i32,
-                                    vp, vp, i64, vp, vp, vp, vp, vp, i64, vp, i64, vp, vp]),
+                                    vp, vp, i64, vp, vp, vp, vp, vp, i64, vp, i64, vp, vp, vp]),
     "fb_spec_events": (C.c_int, [C.POINTER(FbTrie), i32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                  vp]),
     "fb_boundary_plan": (C.c_int, [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp,

@@ -185,7 +185,7 @@ __device__ double pairwise_sum_d(const double* a, int n, F f) {
 // (B) softmax / fp64 accumulator / coverage / context: CTA = (utterance, group
 //     of RB rows), thread = 4 encoder columns: the encoder output is streamed
 //     from HBM once per row group (HBM-bound; it does not fit L2 at c2).
-constexpr int kEnWarps = 8;
+
 
 constexpr int kMaxBeam = 512;
 constexpr int kCtxMaxThreads = 512;   // context CTA: one thread per 4 encoder columns
@@ -213,10 +213,10 @@ __device__ __forceinline__ void softmax_row(const fb_search_cfg_t& cfg, int r, i
                                             double* cov_out, float* attn_out, int64_t ld_attn,
                                             int lane) {
   float mx = -INFINITY;
-  for (int t = lane; t < T; t += 32) mx = fmaxf(mx, e[t]);
+  for (int t = lane; t < T; t += 32) mx = fmaxf(mx, __ldcg(e + t));
   for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
   float sum = 0.f;
-  for (int t = lane; t < T; t += 32) sum += expf(e[t] - mx);
+  for (int t = lane; t < T; t += 32) sum += expf(__ldcg(e + t) - mx);
   for (int off = 16; off; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
   const float inv = 1.0f / sum;
   const int p = parent ? parent[r] : r;
@@ -224,7 +224,7 @@ __device__ __forceinline__ void softmax_row(const fb_search_cfg_t& cfg, int r, i
   double* a1 = acc_out + (int64_t)r * TM;
   int cnt = 0;
   for (int t = lane; t < T; t += 32) {
-    const float a = expf(e[t] - mx) * inv;
+    const float a = expf(__ldcg(e + t) - mx) * inv;
     alpha[t] = a;
     const double x = dadd(a0[t], (double)a);
     a1[t] = x;
@@ -289,13 +289,13 @@ __device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) {
   return d;
 }
 
-template <int R>
+template <int R, int kEnWarps>
 __global__ void __launch_bounds__(kEnWarps * 32)
 att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
                   const int32_t* __restrict__ n_live, const int32_t* __restrict__ t_enc,
                   const float* __restrict__ ekt, int A, const float* __restrict__ v,
                   const float* __restrict__ q, int64_t ldq, float* __restrict__ energy,
-                  int fuse, const int32_t* __restrict__ parent,
+                  int32_t* __restrict__ sync_ws, const int32_t* __restrict__ parent,
                   const double* __restrict__ acc_in, double* __restrict__ acc_out,
                   double* __restrict__ cov_out, float* __restrict__ attn_out, int64_t ld_attn) {
   // CTA = (utterance, chunk of kEnWarps*32 frames, group of R rows); lane = one
@@ -322,19 +322,17 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
   float2* qs2 = vs2 + A;                                // [R/2][A] (Eq_r, Eq_r+1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int slot0 = u * K + r0;
-  for (int j = tid; j < (R / 2) * A; j += blockDim.x) {
-    const int rp = j / A, a = j - rp * A;
+  for (int rp = 0; rp < R / 2; ++rp) {
     const int ra = 2 * rp, rb = ra + 1;
-    qs2[j] = make_float2(ra < rows ? q[(int64_t)(slot0 + ra) * ldq + a] : 0.f,
-                         rb < rows ? q[(int64_t)(slot0 + rb) * ldq + a] : 0.f);
+    const float* qa = q + (int64_t)(slot0 + ra) * ldq;
+    const float* qb = q + (int64_t)(slot0 + rb) * ldq;
+    for (int a = tid; a < A; a += blockDim.x)
+      qs2[rp * A + a] = make_float2(ra < rows ? qa[a] : 0.f, rb < rows ? qb[a] : 0.f);
   }
   for (int a = tid; a < A; a += blockDim.x) vs2[a] = make_float2(v[a], v[a]);
   __syncthreads();
   const int t = t0 + warp * 32 + lane;
   const bool valid = t < T;
-  // fuse: the whole utterance is this CTA's frame chunk (T <= 256), so the
-  // softmax / accumulator / coverage run here on the energies in shared memory
-  float* es = reinterpret_cast<float*>(qs2 + (R / 2) * A);   // [R][kEnWarps*32]
   if (t0 + warp * 32 < T) {
   const float* kt = ekt + (int64_t)u * A * TM + (valid ? t : T - 1);
   const f2_t one2 = pk2(1.0f, 1.0f);
@@ -379,22 +377,31 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
     for (int rp = 0; rp < R / 2; ++rp) {
       float ea, eb;
       up2(e2[rp], ea, eb);
-      if (fuse) {
-        es[(2 * rp) * (kEnWarps * 32) + t] = -2.0f * ea;
-        es[(2 * rp + 1) * (kEnWarps * 32) + t] = -2.0f * eb;
-      } else {
-        if (2 * rp < rows) energy[(int64_t)(slot0 + 2 * rp) * TM + t] = -2.0f * ea;
-        if (2 * rp + 1 < rows) energy[(int64_t)(slot0 + 2 * rp + 1) * TM + t] = -2.0f * eb;
-      }
+      if (2 * rp < rows) energy[(int64_t)(slot0 + 2 * rp) * TM + t] = -2.0f * ea;
+      if (2 * rp + 1 < rows) energy[(int64_t)(slot0 + 2 * rp + 1) * TM + t] = -2.0f * eb;
     }
   }
   }
-  if (!fuse) return;
+  // the last frame chunk of (utterance, row group) to finish runs the softmax,
+  // fp64 accumulator and coverage of the group's rows (counter self-resets)
+  __shared__ int s_last;
+  __threadfence();
   __syncthreads();
-  for (int i = warp; i < rows; i += kEnWarps)
-    softmax_row(cfg, slot0 + i, T, TM, es + i * (kEnWarps * 32),
-                energy + (int64_t)(slot0 + i) * TM, parent, acc_in, acc_out, cov_out, attn_out,
+  if (tid == 0) {
+    int32_t* cnt = sync_ws + (int64_t)u * gridDim.z + blockIdx.z;
+    const int chunks = (T + kEnWarps * 32 - 1) / (kEnWarps * 32);
+    const int prev = atomicAdd(cnt, 1);
+    s_last = prev + 1 == chunks;
+    if (s_last) *cnt = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int i = warp; i < rows; i += kEnWarps) {
+    float* er = energy + (int64_t)(slot0 + i) * TM;
+    softmax_row(cfg, slot0 + i, T, TM, er, er, parent, acc_in, acc_out, cov_out, attn_out,
                 ld_attn, lane);
+  }
 }
 
 // E_q = exp(2 q) in place for the live rows of active utterances (once per
@@ -726,9 +733,9 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
                                  int64_t ldq, const int32_t* parent, const double* acc_in,
                                  double* acc_out, double* cov_out, float* ctx_out,
                                  int64_t ld_ctx, float* attn_out, int64_t ld_attn,
-                                 float* energy_ws, void* stream) {
-  FB_CHECK_ARG(cfg && keys && enc && v && q && acc_in && acc_out && ctx_out && energy_ws,
-               "null attention args");
+                                 float* energy_ws, int32_t* sync_ws, void* stream) {
+  FB_CHECK_ARG(cfg && keys && enc && v && q && acc_in && acc_out && ctx_out && energy_ws &&
+                   sync_ws, "null attention args");
   FB_CHECK_ARG(cfg->cov_mode == 0 || cov_out, "coverage output required");
   FB_CHECK_ARG(cfg->beam <= kMaxBeam, "beam too large for the attention kernels");
   FB_CHECK_ARG(att_dim % 4 == 0 && ldq % 4 == 0,
@@ -741,9 +748,7 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
   }();
   const int RE = re_env > 0 ? re_env
                             : (cfg->beam >= 16 ? 16 : (cfg->beam + 1) & ~1);   // rows per energy CTA
-  const bool fuse = cfg->t_max <= kEnWarps * 32;     // one energy CTA spans the utterance
-  const size_t sm_e = sizeof(float) * ((size_t)RE * att_dim + 2 * (size_t)att_dim +
-                                       (fuse ? (size_t)RE * kEnWarps * 32 : 0));
+  const size_t sm_e = sizeof(float) * ((size_t)RE * att_dim + 2 * (size_t)att_dim);
   const int RB = cfg->beam <= 4 ? 4 : cfg->beam <= 8 ? 8 : cfg->beam <= 12 ? 12 : 16;
   const size_t sm_c = sizeof(float) * (size_t)RB * cfg->t_max;
   if (sm_e > 200 * 1024 || sm_c > 200 * 1024)
@@ -756,7 +761,10 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
     cudaFuncSetAttribute(att_context_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(att_context_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(att_context_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-#define FB_ATTR(R) cudaFuncSetAttribute(att_energy_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
+#define FB_ATTR(R)                                                                                  \
+  cudaFuncSetAttribute(att_energy_kernel<R, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+  cudaFuncSetAttribute(att_energy_kernel<R, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+  cudaFuncSetAttribute(att_energy_kernel<R, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
     FB_ATTR(2); FB_ATTR(4); FB_ATTR(6); FB_ATTR(8); FB_ATTR(10); FB_ATTR(12); FB_ATTR(14); FB_ATTR(16);
 #undef FB_ATTR
     attr_set = true;
@@ -767,12 +775,23 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
         num_utts, cfg->beam, active, n_live, q, ldq, att_dim / 4);
     count_launch();
   }
-  dim3 ge(num_utts, (cfg->t_max + kEnWarps * 32 - 1) / (kEnWarps * 32), (cfg->beam + RE - 1) / RE);
-#define FB_EN(R)                                                                              \
-  att_energy_kernel<R><<<ge, kEnWarps * 32, sm_e, s>>>(*cfg, active, n_live, t_enc, keys, att_dim, \
-                                                        v, q, ldq, energy_ws, fuse ? 1 : 0,    \
-                                                        parent, acc_in, acc_out, cov_out,      \
-                                                        attn_out, ld_attn)
+  // frames per energy CTA: enough CTAs to fill the GPU a few times over
+  static const int ew_env = [] {
+    const char* e = getenv("FB_ATT_EW");
+    return e ? atoi(e) : 0;
+  }();
+  // (measured, scripts/bench_attention.py + the c2 decode: 256-frame CTAs win at
+  // c2 and c4; smaller chunks add more q staging than they recover in occupancy)
+  const int groups_e = (cfg->beam + RE - 1) / RE;
+  int EW = 8;
+  if (ew_env == 2 || ew_env == 4 || ew_env == 8) EW = ew_env;
+  dim3 ge(num_utts, (cfg->t_max + EW * 32 - 1) / (EW * 32), groups_e);
+#define FB_EN2(R, W)                                                                          \
+  att_energy_kernel<R, W><<<ge, W * 32, sm_e, s>>>(*cfg, active, n_live, t_enc, keys, att_dim, \
+                                                    v, q, ldq, energy_ws, sync_ws, parent,     \
+                                                    acc_in, acc_out, cov_out, attn_out, ld_attn)
+#define FB_EN(R) \
+  if (EW == 2) FB_EN2(R, 2); else if (EW == 4) FB_EN2(R, 4); else FB_EN2(R, 8)
   switch (RE) {
     case 2: FB_EN(2); break;
     case 4: FB_EN(4); break;
@@ -783,26 +802,25 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
     case 14: FB_EN(14); break;
     default: FB_EN(16); break;
   }
+#undef FB_EN2
 #undef FB_EN
   count_launch();
   int rc = check_launch("att_energy");
   if (rc) return rc;
-  if (!fuse) {
-    dim3 gs(num_utts, (cfg->beam + 7) / 8);
-    att_softmax_kernel<<<gs, 256, 0, s>>>(*cfg, active, n_live, t_enc, energy_ws, parent, acc_in,
-                                         acc_out, cov_out, attn_out, ld_attn);
-    count_launch();
-    rc = check_launch("att_softmax");
-    if (rc) return rc;
-  }
   // column split so that the grid covers the SMs a few times over (the kernel
   // streams the encoder output; more CTAs = more bytes in flight)
   const int groups = (cfg->beam + RB - 1) / RB;
   const int quads = ctx_dim / 4;
-  int csplit = 1;
-  while (csplit < 8 && (int64_t)num_utts * groups * csplit < 4 * kNumSMs &&
-         quads / (2 * csplit) >= 32)
-    csplit *= 2;
+  static const int cq_env = [] {
+    const char* e = getenv("FB_ATT_CQ");
+    return e ? atoi(e) : 0;
+  }();
+  // quads (4 columns) per context CTA: 64 when the row groups alone fill the GPU
+  // (c2), 160 otherwise (c4: 32 utterances x 4 groups)
+  const int cq = cq_env > 0 ? cq_env
+                            : ((int64_t)num_utts * ((cfg->beam + RB - 1) / RB) >= 2 * kNumSMs ? 64
+                                                                                          : 160);
+  const int csplit = (quads + cq - 1) / cq;
   const int qpc = (quads + csplit - 1) / csplit;
   dim3 gc(num_utts, groups, csplit);
   const int ctx_threads = ((qpc + 31) / 32) * 32;

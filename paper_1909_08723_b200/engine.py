@@ -173,6 +173,7 @@ class _Session:
         self.logits = torch.empty((N, V), dtype=torch.float32, device=dev)
         self.am_logp = torch.zeros((N, V), dtype=torch.float32, device=dev)
         self.energy = torch.empty((N, TM), dtype=torch.float32, device=dev)
+        self.att_sync = torch.zeros(B * ((Kb + 1) // 2), dtype=torch.int32, device=dev)
         self.enc = torch.empty((B, TM, C_), dtype=torch.float32, device=dev)
         self.keys = torch.empty((B, d.att, TM), dtype=torch.float32, device=dev)   # E_K^T
         self.slots0 = torch.arange(B, dtype=torch.int32, device=dev) * Kb
@@ -260,7 +261,8 @@ class FusedDecoder:
                            cfg_ref=S.cfg_ref, num_utts=B, active=buf.active,
                            n_live=buf.n_live, t_enc=buf.t_enc, keys=S.keys, enc=S.enc,
                            acc_in=buf.acc[c], acc_out=buf.acc[1 - c], cov=buf.cov,
-                           energy=S.energy, timer=None if isinstance(tm, _NoTimer) else tm)
+                           energy=S.energy, sync=S.att_sync,
+                           timer=None if isinstance(tm, _NoTimer) else tm)
         fus_buf = S.fus_buf
         if S.sub is not None:
             with tm("lm_subword"):

@@ -255,7 +255,8 @@ class DecoderStep:
     def __call__(self, *, N: int, rows, m: int, m_dev, parent, last_tok, prev: AmState,
                  cur: AmState, scratch: torch.Tensor, q: torch.Tensor, logits: torch.Tensor,
                  am_logp: torch.Tensor, cfg_ref, num_utts: int, active, n_live, t_enc,
-                 keys, enc, acc_in, acc_out, cov, energy, attn_out=None, timer=None) -> None:
+                 keys, enc, acc_in, acc_out, cov, energy, sync, attn_out=None,
+                 timer=None) -> None:
         w, d = self.w, self.w.d
         tm = timer if timer is not None else _null_timer
         H, C_, E = d.dec_hidden, d.ctx, d.emb
@@ -285,7 +286,7 @@ class DecoderStep:
                       _lib.ptr(acc_in), _lib.ptr(acc_out), _lib.ptr(cov), _lib.ptr(cur.ctx),
                       cur.ctx.stride(0), _lib.ptr(attn_out),
                       0 if attn_out is None else attn_out.stride(0), _lib.ptr(energy),
-                      _lib.stream_ptr())
+                      _lib.ptr(sync), _lib.stream_ptr())
         ko = w.w_out.shape[1]
         with tm("am_output"):
             K.pack(scratch, [(top, H, 1), (cur.ctx, C_, 1)], k_pad=ko, split=True, **kw)
@@ -361,7 +362,8 @@ class AttnLstmScorer:
                      cur=cur, scratch=scratch, q=q, logits=logits, am_logp=logp,
                      cfg_ref=C.byref(cfg), num_utts=1, active=one, n_live=nl, t_enc=te,
                      keys=state.keys, enc=state.enc, acc_in=acc0, acc_out=acc1, cov=None,
-                     energy=energy, attn_out=attn)
+                     energy=energy, sync=torch.zeros((n + 1) // 2 + 1, dtype=torch.int32,
+                                                     device=dev), attn_out=attn)
         return (logp.cpu().numpy(), attn.cpu().numpy(),
                 _UttState(state.enc, state.keys, state.T, cur))
 
