@@ -37,6 +37,11 @@ pack_rows_kernel(fb_pack_t p, int m_max, const int32_t* __restrict__ m_dev,
   __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(out);
   const int64_t plane = p.plane_rows * ld_out;
   for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < m; i += gridDim.x * wpb) {
+    // resolve every segment's source row first (the index loads overlap)
+    const int sl = rows ? rows[i] : i;
+    const int pr = (parent && (p.nseg > 0)) ? parent[sl] : sl;
+    const int tk = tokens ? tokens[sl] : -1;
+    const int rk = ranks ? ranks[i] : -1;
     int col = 0;
     for (int s = 0; s <= p.nseg; ++s) {
       const float* src = nullptr;
@@ -46,11 +51,10 @@ pack_rows_kernel(fb_pack_t p, int m_max, const int32_t* __restrict__ m_dev,
         int64_t r;
         switch (sg.mode) {
           case 0: r = i; break;
-          case 1: r = rows ? rows[i] : i; break;
-          case 2: { const int sl = rows ? rows[i] : i; r = parent ? parent[sl] : sl; break; }
-          case 3: { const int sl = rows ? rows[i] : i; const int t = tokens[sl];
-                    r = t < 0 ? p.tok_default : t; break; }
-          default: { const int t = ranks ? ranks[i] : -1; r = t < 0 ? p.tok_default : t; break; }
+          case 1: r = sl; break;
+          case 2: r = pr; break;
+          case 3: r = tk < 0 ? p.tok_default : tk; break;
+          default: r = rk < 0 ? p.tok_default : rk; break;
         }
         src = sg.src ? sg.src + r * sg.ld : nullptr;
         width = sg.width;
@@ -60,21 +64,32 @@ pack_rows_kernel(fb_pack_t p, int m_max, const int32_t* __restrict__ m_dev,
       const bool vec = ((width & 3) == 0) && ((col & 3) == 0) &&
                        (!src || (reinterpret_cast<uintptr_t>(src) & 15) == 0);
       if (vec) {
-        for (int j = lane * 4; j < width; j += 128) {
-          const float4 v = src ? *reinterpret_cast<const float4*>(src + j)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
-          const int64_t o = (int64_t)i * ld_out + col + j;
-          if (!split) {
-            *reinterpret_cast<float4*>(out + o) = v;
-          } else {
-            __nv_bfloat16 h[4], md[4], lo[4];
-            split3(v.x, h[0], md[0], lo[0]);
-            split3(v.y, h[1], md[1], lo[1]);
-            split3(v.z, h[2], md[2], lo[2]);
-            split3(v.w, h[3], md[3], lo[3]);
-            *reinterpret_cast<uint2*>(ob + o) = *reinterpret_cast<uint2*>(h);
-            *reinterpret_cast<uint2*>(ob + plane + o) = *reinterpret_cast<uint2*>(md);
-            *reinterpret_cast<uint2*>(ob + 2 * plane + o) = *reinterpret_cast<uint2*>(lo);
+        // four float4 per lane in flight before any store
+        for (int j0 = lane * 4; j0 < width; j0 += 512) {
+          float4 v[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int j = j0 + 128 * q;
+            v[q] = (src && j < width) ? __ldg(reinterpret_cast<const float4*>(src + j))
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int j = j0 + 128 * q;
+            if (j >= width) break;
+            const int64_t o = (int64_t)i * ld_out + col + j;
+            if (!split) {
+              *reinterpret_cast<float4*>(out + o) = v[q];
+            } else {
+              __nv_bfloat16 h[4], md[4], lo[4];
+              split3(v[q].x, h[0], md[0], lo[0]);
+              split3(v[q].y, h[1], md[1], lo[1]);
+              split3(v[q].z, h[2], md[2], lo[2]);
+              split3(v[q].w, h[3], md[3], lo[3]);
+              *reinterpret_cast<uint2*>(ob + o) = *reinterpret_cast<uint2*>(h);
+              *reinterpret_cast<uint2*>(ob + plane + o) = *reinterpret_cast<uint2*>(md);
+              *reinterpret_cast<uint2*>(ob + 2 * plane + o) = *reinterpret_cast<uint2*>(lo);
+            }
           }
         }
       } else {
