@@ -96,7 +96,7 @@ int fb_logits_to_g(int32_t m_max, const int32_t* m_dev, const float* logits,
  * without another pass over the logits; if g_pool, g_pool[d] =
  * cumsum(softmax over the vw words) in fp64, segment-parallel over
  * (rows x 4096-column segments) with exact fp64 segment offsets (two passes;
- * seg_ws: scratch of m_max * ceil(vw/4096) doubles).  Row i < *m_dev reads
+ * seg_ws: scratch of m_max * (ceil(vw/4096) + 2) doubles).  Row i < *m_dev reads
  * logits/stats row src_rows[i]; d = slots ? slots[i] : i. */
 int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* logits, int64_t l_stride,
                   const float* row_stats, int32_t n_out, const int32_t* src_rows, int32_t vw,

@@ -302,59 +302,56 @@ row_scan_kernel(int m_max, const int32_t* __restrict__ m_dev, const void* __rest
 constexpr int kSegCols = kScanTile;          // 4096 columns per segment CTA
 
 // Row-wide word max (exact) and all-output log-sum-exp from the tile stats.
-__device__ __forceinline__ void row_norm(const float4* __restrict__ st, int ntiles, float& mw,
-                                         double& lse_all, float* red_f, double* red_d) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  float ma = -INFINITY;
-  mw = -INFINITY;
-  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
-    const float4 v = st[t];
-    ma = fmaxf(ma, v.x);
-    mw = fmaxf(mw, v.z);
+
+// Per event row, once: M_w = max over the word logits (tile statistics),
+// lse = log-sum-exp over all outputs (fp64), log P(</s>) = z[vw] - lse.
+// One warp per row; norm_out[i] = M_w for the segment passes.
+__global__ void __launch_bounds__(256)
+row_norm_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __restrict__ logits,
+                int64_t ld, const float4* __restrict__ stats, int ntiles,
+                const int32_t* __restrict__ src_rows, int vw, const int32_t* __restrict__ slots,
+                double* __restrict__ eos_out, double* __restrict__ norm_out) {
+  const int m = row_count(m_max, m_dev);
+  const int lane = threadIdx.x & 31;
+  for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < m; i += gridDim.x * 8) {
+    const int64_t srow = src_rows ? src_rows[i] : i;
+    const float4* st = stats + srow * ntiles;
+    float ma = -INFINITY, mw = -INFINITY;
+    for (int t = lane; t < ntiles; t += 32) {
+      const float4 v = st[t];
+      ma = fmaxf(ma, v.x);
+      mw = fmaxf(mw, v.z);
+    }
+    for (int off = 16; off; off >>= 1) {
+      ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, off));
+      mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, off));
+    }
+    double sa = 0.0;
+    for (int t = lane; t < ntiles; t += 32) {
+      const float4 v = st[t];
+      if (v.x > -INFINITY) sa += (double)v.y * exp((double)v.x - (double)ma);
+    }
+    for (int off = 16; off; off >>= 1) sa += __shfl_xor_sync(0xffffffffu, sa, off);
+    const double lse = (double)ma + log(sa);
+    if (lane == 0) {
+      if (eos_out) eos_out[slots ? slots[i] : i] = (double)logits[srow * ld + vw] - lse;
+      if (norm_out) norm_out[i] = (double)mw;          // M_w per row (segment passes)
+    }
   }
-  for (int off = 16; off; off >>= 1) {
-    ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, off));
-    mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, off));
-  }
-  if (lane == 0) { red_f[warp] = ma; red_f[32 + warp] = mw; }
-  __syncthreads();
-  ma = -INFINITY; mw = -INFINITY;
-  for (int w = 0; w < nw; ++w) { ma = fmaxf(ma, red_f[w]); mw = fmaxf(mw, red_f[32 + w]); }
-  double sa = 0.0;
-  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
-    const float4 v = st[t];
-    if (v.x > -INFINITY) sa += (double)v.y * exp((double)v.x - (double)ma);
-  }
-  for (int off = 16; off; off >>= 1) sa += __shfl_xor_sync(0xffffffffu, sa, off);
-  __syncthreads();
-  if (lane == 0) red_d[warp] = sa;
-  __syncthreads();
-  sa = 0.0;
-  for (int w = 0; w < nw; ++w) sa += red_d[w];
-  lse_all = (double)ma + log(sa);
-  __syncthreads();
 }
 
 // pass 1 (g_pool): exact fp64 sum of exp(z - M_w) per 4096-column segment;
 // CTA (row, 0) also writes log P(</s>).
 __global__ void __launch_bounds__(kScanThreads)
 seg_sum_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __restrict__ logits,
-               int64_t ld, const float4* __restrict__ stats, int ntiles,
-               const int32_t* __restrict__ src_rows, int vw, const int32_t* __restrict__ slots,
-               double* __restrict__ seg_ws, int nseg, double* __restrict__ eos_out,
-               int do_segs) {
-  __shared__ float red_f[64];
+               int64_t ld, const int32_t* __restrict__ src_rows, int vw,
+               double* __restrict__ seg_ws, int nseg, const double* __restrict__ norm) {
   __shared__ double red_d[32];
   const int m = row_count(m_max, m_dev);
   for (int i = blockIdx.x; i < m; i += gridDim.x) {
     const int64_t srow = src_rows ? src_rows[i] : i;
-    float mw;
-    double lse;
-    row_norm(stats + srow * ntiles, ntiles, mw, lse, red_f, red_d);
+    const float mw = (float)norm[i];
     const float* lg = logits + srow * ld;
-    if (blockIdx.y == 0 && threadIdx.x == 0 && eos_out)
-      eos_out[slots ? slots[i] : i] = (double)lg[vw] - lse;
-    if (!do_segs) continue;
     const int c0 = blockIdx.y * kSegCols, c1 = min(vw, c0 + kSegCols);
     double s = 0.0;
     for (int j = c0 + threadIdx.x; j < c1; j += blockDim.x) s += (double)expf(lg[j] - mw);
@@ -373,19 +370,14 @@ seg_sum_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __rest
 // pass 2: scan each segment with its exact fp64 offset; g = prefix / S_w.
 __global__ void __launch_bounds__(kScanThreads)
 seg_scan_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __restrict__ logits,
-                int64_t ld, const float4* __restrict__ stats, int ntiles,
-                const int32_t* __restrict__ src_rows, int vw, const int32_t* __restrict__ slots,
-                const double* __restrict__ seg_ws, int nseg, double* __restrict__ g_pool,
-                int64_t g_stride) {
+                int64_t ld, const int32_t* __restrict__ src_rows, int vw,
+                const int32_t* __restrict__ slots, const double* __restrict__ seg_ws, int nseg,
+                const double* __restrict__ norm, double* __restrict__ g_pool, int64_t g_stride) {
   __shared__ double wsum[32];
-  __shared__ float red_f[64];
-  __shared__ double red_d[32];
   const int m = row_count(m_max, m_dev);
   for (int i = blockIdx.x; i < m; i += gridDim.x) {
   const int64_t srow = src_rows ? src_rows[i] : i;
-  float mw;
-  double lse;
-  row_norm(stats + srow * ntiles, ntiles, mw, lse, red_f, red_d);
+  const float mw = (float)norm[i];
   const double* sw = seg_ws + (int64_t)i * nseg;
   double off = 0.0, tot = 0.0;
   for (int k = 0; k < nseg; ++k) {          // same order in every CTA: deterministic
@@ -517,16 +509,21 @@ extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* l
   const int ntiles = (n_out + 63) / 64;       // GEMM epilogue statistics granule
   const int nseg = (vw + kSegCols - 1) / kSegCols;
   const float4* st = reinterpret_cast<const float4*>(row_stats);
-  const int gx = std::min(m_max, 256);
-  dim3 g1(gx, g_pool ? nseg : 1);
-  seg_sum_kernel<<<g1, kScanThreads, 0, s>>>(m_max, m_dev, logits, l_stride, st, ntiles, src_rows,
-                                             vw, slots, seg_ws, nseg, eos_out, g_pool != nullptr);
+  // seg_ws layout: [m_max][nseg] segment sums, then [m_max] M_w
+  double* norm = g_pool ? seg_ws + (int64_t)m_max * nseg : nullptr;
+  row_norm_kernel<<<std::min((m_max + 7) / 8, kNumSMs * 8), 256, 0, s>>>(
+      m_max, m_dev, logits, l_stride, st, ntiles, src_rows, vw, slots, eos_out, norm);
   count_launch();
-  int rc = check_launch("seg_sum");
+  int rc = check_launch("row_norm");
   if (rc || !g_pool) return rc;
+  const int gx = std::min(m_max, 256);
+  seg_sum_kernel<<<dim3(gx, nseg), kScanThreads, 0, s>>>(m_max, m_dev, logits, l_stride, src_rows,
+                                                         vw, seg_ws, nseg, norm);
+  count_launch();
+  rc = check_launch("seg_sum");
+  if (rc) return rc;
   seg_scan_kernel<<<dim3(gx, nseg), kScanThreads, 0, s>>>(
-      m_max, m_dev, logits, l_stride, st, ntiles, src_rows, vw, slots, seg_ws, nseg, g_pool,
-      g_stride);
+      m_max, m_dev, logits, l_stride, src_rows, vw, slots, seg_ws, nseg, norm, g_pool, g_stride);
   count_launch();
   return check_launch("seg_scan");
 }

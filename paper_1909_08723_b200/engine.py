@@ -54,8 +54,8 @@ class _LmPool:
         self.ev_logits = torch.empty((E, lw.v_out), dtype=f32, device=device)
         self.ntiles = (lw.v_out + 63) // 64
         self.ev_stats = torch.empty((E, self.ntiles, 4), dtype=f32, device=device)
-        self.seg_ws = torch.empty((N, (d.words + 4095) // 4096), dtype=torch.float64,
-                                  device=device)
+        self.seg_ws = torch.empty((N, (d.words + 4095) // 4096 + 2), dtype=torch.float64,
+                                  device=device)     # segment sums + per-row {M_w, lse}
         self.ev_row, self.ev_rank, self.ev_slot, self.row_ev = z(N), z(N), z(N), z(N)
         self.ev_count = z(1)
         self.trie = [z(N), z(N)]

@@ -111,7 +111,7 @@ def test_row_stats_feed_g_rows_and_eos():
     K.logits_to_g(logits, vw, n, m=m, g_pool=g_ref, eos_out=e_ref)
     g = torch.empty_like(g_ref)
     e = torch.empty_like(e_ref)
-    seg = torch.empty(m, (vw + 4095) // 4096, dtype=torch.float64, device=dev)
+    seg = torch.empty(m, (vw + 4095) // 4096 + 2, dtype=torch.float64, device=dev)
     cnt = torch.tensor([m], dtype=torch.int32, device=dev)
     K.stats_to_g(logits, stats, vw, n, m=m, m_dev=cnt, g_pool=g, eos_out=e, seg_ws=seg)
     assert (g - g_ref).abs().max().item() < 1e-13
