@@ -402,6 +402,170 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   }
 }
 
+// Encoder LSTM recurrence as ONE persistent launch per direction (PAPER.md:
+// 105-110): CTA = fixed (m-tile, n-tile) of gates = xp[:, t] + h_{t-1} W_hh^T,
+// looping over t with a grid barrier between steps (all CTAs co-resident: one
+// CTA per SM, m_tiles * n_tiles <= 74 so both directions fit together).  The
+// epilogue (LSTM cell, h -> y and -> the next step's bf16 planes) is the GEMM's.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
+                const __grid_constant__ CUtensorMap tmW, fb_gemm_t g0, int steps, int num_kb,
+                int kcb, float* c_buf, const float* xp, float* y, int64_t ld_y,
+                __nv_bfloat16* rec, int64_t plane, unsigned* sync) {
+  constexpr int BN = 128;
+  const int batch = g0.m_max, H = g0.hidden;
+  const int m_tiles = (batch + TC_BM - 1) / TC_BM;
+  const int n_ctas = gridDim.x;
+  const int tile = blockIdx.x;
+  const int m0 = (tile % m_tiles) * TC_BM, n0 = (tile / m_tiles) * BN;
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int A_TILE = TC_BM * TC_BK * 2;
+  constexpr int W_TILE = BN * TC_BK * 2;
+  constexpr int stage_bytes = 3 * A_TILE + W_TILE;
+  __shared__ __align__(8) uint64_t bar_full[TC_STAGES], bar_empty[TC_STAGES];
+  __shared__ __align__(8) uint64_t bar_tfull[TC_NACC], bar_tempty[TC_NACC];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ float epi_stage[8][32 * 33];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(smem_u32(&bar_full[s]), 1);
+      mbar_init(smem_u32(&bar_empty[s]), 1);
+    }
+    for (int a = 0; a < TC_NACC; ++a) {
+      mbar_init(smem_u32(&bar_tfull[a]), 1);
+      mbar_init(smem_u32(&bar_tempty[a]), TC_EPI_THREADS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_sh)),
+                 "r"(TC_NACC * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int gk = 0;
+      for (int t = 0; t < steps; ++t) {
+        // h_{t-1} complete in every CTA (grid barrier), then visible to TMA
+        const unsigned target = (unsigned)(n_ctas * t);
+        while (ld_acquire_u32(sync) < target) __nanosleep(32);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        const CUtensorMap* tmA = (t & 1) ? &tmA1 : &tmA0;
+        for (int kb = 0; kb < num_kb; ++kb, ++gk) {
+          const int s = gk % TC_STAGES;
+          const uint32_t ph = (gk / TC_STAGES) & 1;
+          mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
+          const uint32_t full = smem_u32(&bar_full[s]);
+          mbar_expect_tx(full, stage_bytes);
+          unsigned char* st = base + (size_t)s * stage_bytes;
+          for (int p = 0; p < 3; ++p)
+            tma_load_2d(smem_u32(st + p * A_TILE), tmA, full, kb * TC_BK, p * batch + m0);
+          tma_load_2d(smem_u32(st + 3 * A_TILE), &tmW, full, kb * TC_BK, n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(TC_BM >> 4) << 24);
+      int gk = 0, cc = 0;
+      for (int t = 0; t < steps; ++t) {
+        for (int kb0 = 0; kb0 < num_kb; kb0 += kcb, ++cc) {
+          const int slot = cc % TC_NACC;
+          mbar_wait(smem_u32(&bar_tempty[slot]), ((cc / TC_NACC) & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t d = tmem + slot * BN;
+          const int kb1 = min(kb0 + kcb, num_kb);
+          for (int kb = kb0; kb < kb1; ++kb, ++gk) {
+            const int s = gk % TC_STAGES;
+            const uint32_t ph = (gk / TC_STAGES) & 1;
+            mbar_wait(smem_u32(&bar_full[s]), ph);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            unsigned char* st = base + (size_t)s * stage_bytes;
+            const uint64_t bdesc0 = smem_desc_sw128(smem_u32(st + 3 * A_TILE));
+            for (int p = 2; p >= 0; --p) {
+              const uint64_t adesc0 = smem_desc_sw128(smem_u32(st + p * A_TILE));
+#pragma unroll
+              for (int k = 0; k < TC_BK / 16; ++k)
+                mma_bf16(d, adesc0 + 2 * k, bdesc0 + 2 * k, idesc, ((kb - kb0) | (2 - p) | k) != 0);
+            }
+            mma_commit(smem_u32(&bar_empty[s]));
+          }
+          mma_commit(smem_u32(&bar_tfull[slot]));
+        }
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    constexpr int CH = BN / 64;
+    const uint32_t tl = tmem + ((uint32_t)(quarter * 32) << 16);
+    int cc = 0;
+    for (int t = 0; t < steps; ++t) {
+      float acc[CH][32];
+      for (int kb0 = 0; kb0 < num_kb; kb0 += kcb, ++cc) {
+        const int slot = cc % TC_NACC;
+        mbar_wait(smem_u32(&bar_tfull[slot]), (cc / TC_NACC) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          float v[32];
+          tmem_ld32(tl + slot * BN + (half * CH + c) * 32, v);
+          if (kb0 == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[c][j] = v[j];
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[c][j] += v[j];
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[slot]))
+                     : "memory");
+      }
+      const int cur = t & 1, nxt = cur ^ 1;
+      fb_gemm_t g = g0;
+      g.c_in = t ? c_buf + (int64_t)cur * batch * H : nullptr;
+      g.c_out = c_buf + (int64_t)nxt * batch * H;
+      g.h_out = y + (int64_t)t * H;
+      g.ld_h = ld_y;
+      g.addend = xp + (int64_t)t * 4 * H;
+      g.h_split = rec + (int64_t)nxt * 3 * plane;
+      epilogue_tile<BN>(g, batch, m0 + quarter * 32, n0, acc, epi_stage[warp - 2], half);
+      // publish h_t: every epilogue thread's stores, then one release-increment
+      __threadfence();
+      asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI_THREADS));
+      if (warp == 2 && lane == 0) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        atomicAdd(sync, 1u);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TC_NACC * BN));
+  }
+}
+
 // ---- host: tensor maps through the driver entry point (no -lcuda needed) ----
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -510,10 +674,15 @@ extern "C" int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_
 extern "C" int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden,
                                   const void* w_hh, int32_t k, const float* xp, int64_t ld_xp,
                                   float* y, int64_t ld_y, float* c_buf, void* rec,
-                                  void* stream) {
-  FB_CHECK_ARG(w_hh && xp && y && c_buf && rec, "null recurrence buffers");
+                                  uint32_t* sync_ws, void* stream) {
+  FB_CHECK_ARG(w_hh && xp && y && c_buf && rec && sync_ws, "null recurrence buffers");
   FB_CHECK_ARG(k % TC_BK == 0 && k >= hidden, "recurrence k must be a multiple of 64 >= hidden");
   FB_CHECK_ARG(steps >= 0 && batch > 0, "bad recurrence sizes");
+  FB_CHECK_ARG((4 * hidden) % 128 == 0 && hidden % 32 == 0, "hidden must be a multiple of 32");
+  const int m_tiles = (batch + TC_BM - 1) / TC_BM, n_tiles = 4 * hidden / 128;
+  FB_CHECK_ARG(m_tiles * n_tiles <= kNumSMs / 2,
+               "recurrence too wide for one co-resident persistent grid per direction");
+  if (steps == 0) return FB_OK;
   cudaStream_t s = (cudaStream_t)stream;
   __nv_bfloat16* r = reinterpret_cast<__nv_bfloat16*>(rec);
   const int64_t plane = (int64_t)batch * k;          // elements per plane
@@ -523,27 +692,22 @@ extern "C" int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden,
   g.mode = 1; g.hidden = hidden;
   g.ld_cin = hidden; g.ld_cout = hidden; g.ld_h = ld_y; g.ld_add = ld_xp;
   g.hs_plane_rows = batch; g.ld_hs = k;
-  const int tiles128 = ((batch + TC_BM - 1) / TC_BM) * ((g.n + 127) / 128);
-  const bool narrow = false;
-  (void)tiles128;
   CUtensorMap ta[2], tw;
   for (int p = 0; p < 2; ++p) {
     int rc = make_map(&ta[p], r + (int64_t)p * 3 * plane, 3ull * batch, k, k, TC_BM);
     if (rc) return rc;
   }
-  int rc = make_map(&tw, w_hh, g.n, k, k, narrow ? 64 : 128);
+  int rc = make_map(&tw, w_hh, g.n, k, k, 128);
   if (rc) return rc;
-  for (int t = 0; t < steps; ++t) {
-    const int cur = t & 1, nxt = cur ^ 1;
-    g.a = r + (int64_t)cur * 3 * plane;
-    g.c_in = t ? c_buf + (int64_t)cur * batch * hidden : nullptr;
-    g.c_out = c_buf + (int64_t)nxt * batch * hidden;
-    g.h_out = y + (int64_t)t * hidden;
-    g.addend = xp + (int64_t)t * 4 * hidden;
-    g.h_split = r + (int64_t)nxt * 3 * plane;
-    rc = narrow ? launch_tc_maps<64>(ta[cur], tw, &g, 3, batch, s)
-                : launch_tc_maps<128>(ta[cur], tw, &g, 3, batch, s);
-    if (rc) return rc;
+  cudaMemsetAsync(sync_ws, 0, sizeof(uint32_t), s);
+  const size_t smem = (size_t)TC_STAGES * (3 * TC_BM * TC_BK * 2 + 128 * TC_BK * 2) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(lstm_rec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
   }
-  return FB_OK;
+  lstm_rec_kernel<<<m_tiles * n_tiles, TC_THREADS, smem, s>>>(
+      ta[0], ta[1], tw, g, steps, k / TC_BK, TC_KCB, c_buf, xp, y, ld_y, r, plane, sync_ws);
+  count_launch();
+  return check_launch("lstm_rec");
 }
