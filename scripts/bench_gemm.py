@@ -7,6 +7,8 @@ import torch
 from paper_1909_08723_b200 import kernels as K
 
 SHAPES = {  # name: (M, N, K, mode)
+    "lm_lstm_64": (64, 4800, 2432, 1),
+    "lm_lstm_300": (300, 4800, 2432, 1),
     "am_lstm_2k": (2048, 1280, 1024, 1),
     "lm_lstm_160": (160, 4800, 2432, 1),
     "lm_lstm_600": (600, 4800, 2432, 1),
