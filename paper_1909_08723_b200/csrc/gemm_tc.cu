@@ -88,6 +88,27 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// warp-uniform issue: every lane runs the loop (descriptors stay in uniform
+// registers), one elected lane issues -- avoids a per-MMA R2UR/ELECT sequence
+__device__ __forceinline__ void mma_bf16_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          bar)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    bar)
@@ -307,27 +328,29 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const uint32_t tmem = tmem_base_sh;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ---- TMA producer ----
-      int gk = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile % m_tiles) * TC_BM, n0 = (tile / m_tiles) * BN;
-        for (int kb = 0; kb < num_kb; ++kb, ++gk) {
-          const int s = gk % TC_STAGES;
-          const uint32_t ph = (gk / TC_STAGES) & 1;
+    // ---- TMA producer: lane p issues A plane p, lane a_planes the W tile ----
+    int gk = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int m0 = (tile % m_tiles) * TC_BM, n0 = (tile / m_tiles) * BN;
+      for (int kb = 0; kb < num_kb; ++kb, ++gk) {
+        const int s = gk % TC_STAGES;
+        const uint32_t ph = (gk / TC_STAGES) & 1;
+        if (lane == 0) {
           mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
-          const uint32_t full = smem_u32(&bar_full[s]);
-          mbar_expect_tx(full, stage_bytes);
-          unsigned char* st = base + (size_t)s * stage_bytes;
-          for (int p = 0; p < a_planes; ++p)
-            tma_load_2d(smem_u32(st + p * A_TILE), &tmA, full, kb * TC_BK,
-                        p * a_plane_rows + m0);
-          tma_load_2d(smem_u32(st + a_planes * A_TILE), &tmW, full, kb * TC_BK, n0);
+          mbar_expect_tx(smem_u32(&bar_full[s]), stage_bytes);
         }
+        __syncwarp();
+        const uint32_t full = smem_u32(&bar_full[s]);
+        unsigned char* st = base + (size_t)s * stage_bytes;
+        if (lane < a_planes)
+          tma_load_2d(smem_u32(st + lane * A_TILE), &tmA, full, kb * TC_BK,
+                      lane * a_plane_rows + m0);
+        else if (lane == a_planes)
+          tma_load_2d(smem_u32(st + a_planes * A_TILE), &tmW, full, kb * TC_BK, n0);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
       // ---- MMA issuer: bf16 x bf16 -> f32, K-major, M = 128, N = BN ----
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(TC_BM >> 4) << 24);
@@ -352,12 +375,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               const uint64_t adesc0 = smem_desc_sw128(smem_u32(st + p * A_TILE));
 #pragma unroll
               for (int k = 0; k < TC_BK / 16; ++k)   // 16 elements = 32 B per UMMA_K
-                mma_bf16(d, adesc0 + 2 * k, bdesc0 + 2 * k, idesc,
+                mma_bf16_elect(d, adesc0 + 2 * k, bdesc0 + 2 * k, idesc,
                          ((kb - kb0) | (a_planes - 1 - p) | k) != 0);
             }
-            mma_commit(smem_u32(&bar_empty[s]));
+            mma_commit_elect(smem_u32(&bar_empty[s]));
           }
-          mma_commit(smem_u32(&bar_tfull[slot]));
+          mma_commit_elect(smem_u32(&bar_tfull[slot]));
         }
       }
     }
@@ -482,7 +505,7 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(TC_BM >> 4) << 24);
       int gk = 0, cc = 0;
@@ -504,11 +527,11 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
               const uint64_t adesc0 = smem_desc_sw128(smem_u32(st + p * A_TILE));
 #pragma unroll
               for (int k = 0; k < TC_BK / 16; ++k)
-                mma_bf16(d, adesc0 + 2 * k, bdesc0 + 2 * k, idesc, ((kb - kb0) | (2 - p) | k) != 0);
+                mma_bf16_elect(d, adesc0 + 2 * k, bdesc0 + 2 * k, idesc, ((kb - kb0) | (2 - p) | k) != 0);
             }
-            mma_commit(smem_u32(&bar_empty[s]));
+            mma_commit_elect(smem_u32(&bar_empty[s]));
           }
-          mma_commit(smem_u32(&bar_tfull[slot]));
+          mma_commit_elect(smem_u32(&bar_tfull[slot]));
         }
       }
     }
