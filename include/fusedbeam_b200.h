@@ -28,7 +28,9 @@ enum {
   FB_OK = 0,
   FB_ERR_VALUE = 1,   /* bad argument / shape      -> ValueError       */
   FB_ERR_CONFIG = 2,  /* unusable configuration    -> ConfigError      */
-  FB_ERR_CUDA = 3     /* CUDA launch/runtime error -> RuntimeError     */
+  FB_ERR_CUDA = 3,    /* CUDA launch/runtime error -> RuntimeError     */
+  FB_ERR_FORMAT = 4,  /* malformed file / input    -> FormatError      */
+  FB_ERR_IO = 5       /* open / truncated read     -> OSError          */
 };
 
 const char* fb_last_error(void);
@@ -357,6 +359,39 @@ int fb_copy_rows(int32_t n_max, const int32_t* n_dev, const int32_t* src_idx,
  * n: dst[r*row_bytes..] = src[idx[r]*row_bytes..]. */
 int fb_gather_rows(int32_t n, const int32_t* idx, const void* src, void* dst,
                    int64_t row_bytes, void* stream);
+
+/* ---- host-side data formats (no GPU; csrc/host_io.cu) -------------------- */
+/* Kaldi binary ARK float32 matrix at `offset` (reference kaldi_io.py:82-130):
+ * rows/cols out; the payload goes to dst when dst != NULL (dst_capacity floats,
+ * e.g. pinned staging memory).  Reference messages: bad marker / token /
+ * size byte / shape / non-finite -> FB_ERR_FORMAT, truncation -> FB_ERR_IO. */
+int fb_ark_read_matrix(const char* ark_path, int64_t offset, float* dst, int64_t dst_capacity,
+                       int32_t* rows, int32_t* cols);
+/* n records on a host thread pool; record i -> dst + dst_offsets[i] (floats,
+ * capacities[i]); dst == NULL queries every record's rows/cols.  On failure
+ * the first failing record (input order) is reported. */
+int fb_ark_read_batch(int32_t n, const char* const* ark_paths, const int64_t* offsets,
+                      float* dst, const int64_t* dst_offsets, const int64_t* capacities,
+                      int32_t* rows, int32_t* cols, int32_t threads);
+/* PTA1 prefix-tree files (lexicon_trie.py:178-224): header, arrays, write. */
+int fb_pta1_read_header(const char* path, int32_t* num_states, int32_t* num_words,
+                        int32_t* max_out, int32_t* alphabet);
+int fb_pta1_read(const char* path, int32_t* transitions, int32_t* edge_labels,
+                 uint8_t* is_final, int32_t* word_index, int32_t* ub_index,
+                 int32_t* lb_index);
+int fb_pta1_write(const char* path, int32_t num_states, int32_t num_words, int32_t max_out,
+                  int32_t alphabet, const int32_t* transitions, const int32_t* edge_labels,
+                  const uint8_t* is_final, const int32_t* word_index, const int32_t* ub_index,
+                  const int32_t* lb_index);
+/* build_trie (lexicon_trie.py:227-276) over char-id sequences
+ * chars[word_offsets[i] .. word_offsets[i+1]): sizes first, then the arrays in
+ * the reference layout (transitions/edge_labels [S][max_out], -1 padded). */
+int fb_trie_build_sizes(int32_t n_words, const int32_t* chars, const int64_t* word_offsets,
+                        int32_t alphabet, int32_t* num_states, int32_t* max_out);
+int fb_trie_build(int32_t n_words, const int32_t* chars, const int64_t* word_offsets,
+                  int32_t alphabet, int32_t num_states, int32_t max_out, int32_t* transitions,
+                  int32_t* edge_labels, uint8_t* is_final, int32_t* word_index,
+                  int32_t* ub_index, int32_t* lb_index);
 
 #ifdef __cplusplus
 }

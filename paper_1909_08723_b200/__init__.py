@@ -12,7 +12,8 @@ __version__ = "0.1.0"
 from .errors import ConfigError, FormatError, FusedBeamError  # noqa: F401
 from .token_dict import TokenDictionary, load_dictionary  # noqa: F401
 from .lexicon_trie import NO_STATE, PrefixTreeAutomaton, build_trie  # noqa: F401
-from .kaldi_io import FeatureMatrix  # noqa: F401
+from .kaldi_io import (FeatureMatrix, ScpEntry, read_ark_matrix, read_feature,  # noqa: F401
+                       read_features_pinned, read_scp, write_ark_matrix)
 from .fusion import (DEFAULT_OOV_PENALTY, OOV_STATE, FusionScorer, LookaheadBatch,  # noqa: F401
                      LookaheadFusion, SubwordBatch, SubwordFusion, cumsum_distribution)
 from .decoder import (AcousticScorer, DecodeConfig, DecodeResult, coverage_improved,  # noqa: F401

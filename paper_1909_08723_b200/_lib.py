@@ -12,7 +12,7 @@ import ctypes as C
 import os
 import threading
 
-from .errors import ConfigError
+from .errors import ConfigError, FormatError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfusedbeam_b200.so")
@@ -100,6 +100,13 @@ _SIGS = {
     "fb_eos_fixup": (C.c_int, [i32, vp, vp, vp, vp, i64, i32, vp]),
     "fb_copy_rows": (C.c_int, [i32, vp, vp, vp, vp, vp, i64, vp]),
     "fb_exp2x": (C.c_int, [i64, vp, vp, vp]),
+    "fb_ark_read_matrix": (C.c_int, [C.c_char_p, i64, vp, i64, vp, vp]),
+    "fb_ark_read_batch": (C.c_int, [i32, vp, vp, vp, vp, vp, vp, vp, i32]),
+    "fb_pta1_read_header": (C.c_int, [C.c_char_p, vp, vp, vp, vp]),
+    "fb_pta1_read": (C.c_int, [C.c_char_p, vp, vp, vp, vp, vp, vp]),
+    "fb_pta1_write": (C.c_int, [C.c_char_p, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
+    "fb_trie_build_sizes": (C.c_int, [i32, vp, vp, i32, vp, vp]),
+    "fb_trie_build": (C.c_int, [i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
     "fb_keys_exp2t": (C.c_int, [i32, i32, i32, vp, vp, vp]),
 }
 
@@ -150,6 +157,10 @@ def check(rc: int) -> None:
         raise ValueError(msg)
     if rc == 2:
         raise ConfigError(msg)
+    if rc == 4:
+        raise FormatError(msg)
+    if rc == 5:
+        raise IOError(msg)
     raise RuntimeError(f"CUDA error: {msg}")
 
 

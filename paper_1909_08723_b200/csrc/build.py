@@ -24,7 +24,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", INCLUDE, "-I", HERE]
 
-SOURCES = ["capi.cu", "lookahead.cu", "search.cu", "gemm.cu", "gemm_tc.cu", "asr.cu"]
+SOURCES = ["capi.cu", "lookahead.cu", "search.cu", "gemm.cu", "gemm_tc.cu", "asr.cu",
+           "host_io.cu"]
 
 
 def _headers():

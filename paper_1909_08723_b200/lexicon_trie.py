@@ -123,6 +123,35 @@ class PrefixTreeAutomaton:
             out.append("".join(reversed(cs)))
         return out
 
+    # ---- PTA1 files (reference lexicon_trie.py:178-224), native I/O ----------
+    def save(self, path: str) -> None:
+        from . import _lib
+        a = lambda x, dt=np.int32: np.ascontiguousarray(x, dt)  # noqa: E731
+        t, e, f = a(self.transitions), a(self.edge_labels), a(self.is_final, np.uint8)
+        w, u, lb = a(self.word_index), a(self.ub_index), a(self.lb_index)
+        _lib.call("fb_pta1_write", path.encode(), self.num_states, self.num_words,
+                  self.max_out_degree, self.alphabet_size, t.ctypes.data, e.ctypes.data,
+                  f.ctypes.data, w.ctypes.data, u.ctypes.data, lb.ctypes.data)
+
+    @classmethod
+    def load(cls, path: str) -> "PrefixTreeAutomaton":
+        import ctypes as C
+        from . import _lib
+        S, W, D, A = (C.c_int32() for _ in range(4))
+        _lib.call("fb_pta1_read_header", path.encode(), C.byref(S), C.byref(W), C.byref(D),
+                  C.byref(A))
+        S, W, D, A = S.value, W.value, D.value, A.value
+        t = np.empty((S, D), np.int32)
+        e = np.empty((S, D), np.int32)
+        f = np.empty(S, np.uint8)
+        w, u, lb = (np.empty(S, np.int32) for _ in range(3))
+        _lib.call("fb_pta1_read", path.encode(), t.ctypes.data, e.ctypes.data, f.ctypes.data,
+                  w.ctypes.data, u.ctypes.data, lb.ctypes.data)
+        trie = cls(t, e, f.astype(bool), w, u, lb, A)
+        if trie.num_words != W:
+            raise FormatError(f"{path}: header word count mismatch")
+        return trie
+
     # ---- device pack --------------------------------------------------------
     def csr(self):
         """(row_ptr[S+1], edge_label[E], edge_child[E], info[S,4]) int32, labels
@@ -145,7 +174,12 @@ class PrefixTreeAutomaton:
 
 
 def build_trie(vocab: Sequence[str], token_dict) -> PrefixTreeAutomaton:
-    """Linear sweep over the rank-sorted vocabulary (see module docstring)."""
+    """Reference ``build_trie`` (lexicon_trie.py:227-276): word checks here (same
+    FormatErrors), the sort + longest-common-prefix sweep in C++
+    (``fb_trie_build``: ranks = lexicographic char-id order, states created along
+    the sweep, so each parent's edges come in ascending label order)."""
+    import ctypes as C
+    from . import _lib
     if not vocab:
         raise FormatError("empty vocabulary")
     seen = set()
@@ -155,42 +189,20 @@ def build_trie(vocab: Sequence[str], token_dict) -> PrefixTreeAutomaton:
             raise FormatError(f"duplicate word {w!r} in vocabulary")
         seen.add(w)
         seqs.append(word_char_ids(w, token_dict))
-    seqs.sort()
-    n_states = 1 + sum(len(q) for q in seqs)          # upper bound
-    first = np.zeros(n_states, np.int64)
-    last = np.zeros(n_states, np.int64)
-    rank_of = np.full(n_states, -1, np.int64)
-    parent = np.zeros(n_states, np.int64)
-    label = np.zeros(n_states, np.int64)
-    path = [0]                                         # state ids along the previous word
-    prev: Tuple[int, ...] = ()
-    nxt = 1
-    for r, q in enumerate(seqs):
-        lcp = 0
-        m = min(len(prev), len(q))
-        while lcp < m and prev[lcp] == q[lcp]:
-            lcp += 1
-        del path[lcp + 1:]
-        for pos in range(lcp, len(q)):
-            parent[nxt] = path[-1]
-            label[nxt] = q[pos]
-            first[nxt] = r
-            path.append(nxt)
-            nxt += 1
-        last[path] = r                                 # every state on the path covers rank r
-        rank_of[path[-1]] = r
-        prev = q
-    S = nxt
-    kids_per = np.bincount(parent[1:S], minlength=S)
-    D = int(kids_per.max())
-    trans = np.full((S, D), NO_STATE, np.int32)
-    labels = np.full((S, D), NO_STATE, np.int32)
-    slot = np.zeros(S, np.int64)
-    for st in range(1, S):                             # creation order == ascending label per parent
-        p = parent[st]
-        trans[p, slot[p]] = st
-        labels[p, slot[p]] = label[st]
-        slot[p] += 1
-    return PrefixTreeAutomaton(trans, labels, rank_of[:S] >= 0, rank_of[:S].astype(np.int32),
-                               last[:S].astype(np.int32), (first[:S] - 1).astype(np.int32),
-                               len(token_dict))
+    n = len(seqs)
+    lens = np.fromiter((len(q) for q in seqs), np.int64, count=n)
+    offs = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=offs[1:])
+    chars = np.fromiter((c for q in seqs for c in q), np.int32, count=int(offs[-1]))
+    A = len(token_dict)
+    S, D = C.c_int32(), C.c_int32()
+    _lib.call("fb_trie_build_sizes", n, chars.ctypes.data, offs.ctypes.data, A, C.byref(S),
+              C.byref(D))
+    S, D = S.value, D.value
+    t = np.empty((S, D), np.int32)
+    e = np.empty((S, D), np.int32)
+    f = np.empty(S, np.uint8)
+    wi, ub, lb = (np.empty(S, np.int32) for _ in range(3))
+    _lib.call("fb_trie_build", n, chars.ctypes.data, offs.ctypes.data, A, S, D, t.ctypes.data,
+              e.ctypes.data, f.ctypes.data, wi.ctypes.data, ub.ctypes.data, lb.ctypes.data)
+    return PrefixTreeAutomaton(t, e, f.astype(bool), wi, ub, lb, A)

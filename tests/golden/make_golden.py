@@ -16,6 +16,11 @@ Imports the UNMODIFIED reference package ``fusedbeam`` read-only from
 * ``neural.pkl.gz``    -- ``decode_batch`` + ``LookaheadFusion`` driving the
                           oracle's PyTorch-CPU attention-LSTM scorer and LSTM
                           word LM at a small size;
+* ``formats/``         -- PTA1 trie files saved by the reference
+                          (lexicon_trie.py:178-224) and a Kaldi ARK/SCP pair
+                          written by its ``write_ark_matrix`` (kaldi_io.py:137-160),
+                          plus corrupt records and the reference reader's
+                          exception type/message for each (``formats.pkl.gz``);
 * ``subword.pkl.gz``   -- ``SubwordFusion`` rows/advance/reorder and
                           ``decode_batch`` with ``SubwordFusion`` over
                           ``UniformCharLM`` and a table ``CharLM`` fake
@@ -31,6 +36,7 @@ from __future__ import annotations
 import gzip
 import os
 import pickle
+import struct
 import sys
 
 import numpy as np
@@ -338,8 +344,97 @@ def subword_cases():
                                             frames=(40, 64), n_utts=4, cases=neural)))
 
 
+def formats_cases():
+    from fusedbeam import kaldi_io as rk
+    from fusedbeam.lexicon_trie import PrefixTreeAutomaton as RefPTA
+    fdir = os.path.join(HERE, "formats")
+    os.makedirs(fdir, exist_ok=True)
+    for f in os.listdir(fdir):
+        os.remove(os.path.join(fdir, f))
+    rng = np.random.default_rng(55)
+    tries = []
+    for i in range(3):
+        letters, words = rand_vocab(rng, 150, int(rng.integers(2, 9)))
+        d = TokenDictionary(letters)
+        t = build_trie(words, d)
+        name = f"trie{i}.pta1"
+        t.save(os.path.join(fdir, name))
+        tries.append(dict(file=name, letters=letters, words=words,
+                          transitions=t.transitions.copy(), edge_labels=t.edge_labels.copy(),
+                          is_final=t.is_final.copy(), word_index=t.word_index.copy(),
+                          ub=t.ub_index.copy(), lb=t.lb_index.copy()))
+    cwd = os.getcwd()
+    os.chdir(fdir)
+    try:
+        mats = {}
+        for i, (rows, cols) in enumerate([(3, 5), (17, 80), (1, 1), (40, 13)]):
+            m = rng.standard_normal((rows, cols)).astype(np.float32)
+            uid = f"utt{i:02d}"
+            rk.write_ark_matrix(uid, m, "feats.ark", "feats.scp")
+            mats[uid] = m
+        # corrupt records: every reader error path the reference defines
+        bad = {}
+        good_off = rk.read_scp("feats.scp")[1].offset
+        blob = open("feats.ark", "rb").read()
+        rec = blob[good_off:good_off + 15 + 17 * 80 * 4]
+
+        def put(name, data):
+            with open(name, "wb") as f:
+                f.write(b"x " + data)
+            return 2
+        cases = {
+            "bad_marker.ark": b"\x00C" + rec[2:],
+            "double.ark": rec[:2] + b"DM " + rec[5:],
+            "compressed.ark": rec[:2] + b"CM2" + rec[5:],
+            "bad_token.ark": rec[:2] + b"XY " + rec[5:],
+            "bad_size.ark": rec[:5] + b"\x08" + rec[6:],
+            "bad_shape.ark": rec[:5] + b"\x04" + struct.pack("<i", 0) + rec[10:],
+            "truncated.ark": rec[:-7],
+            "nonfinite.ark": rec[:15] + struct.pack("<f", float("nan")) + rec[19:],
+        }
+        for name, data in cases.items():
+            off = put(name, data)
+            try:
+                rk.read_ark_matrix(name, off)
+                bad[name] = (off, None, None)
+            except Exception as e:  # noqa: BLE001 - record the reference behaviour
+                bad[name] = (off, type(e).__name__, str(e))
+        scp_bad = {
+            "noff.scp": "u1 feats.ark\n",
+            "badint.scp": "u1 feats.ark:x12\n",
+            "neg.scp": "u1 feats.ark:-4\n",
+            "dup.scp": "u1 feats.ark:3\nu1 feats.ark:9\n",
+            "onefield.scp": "u1\n",
+        }
+        scp_res = {}
+        for name, text in scp_bad.items():
+            with open(name, "w") as f:
+                f.write(text)
+            try:
+                rk.read_scp(name)
+                scp_res[name] = (None, None)
+            except Exception as e:  # noqa: BLE001
+                scp_res[name] = (type(e).__name__, str(e))
+        # PTA1 error paths
+        pta_bad = {}
+        raw = open("trie0.pta1", "rb").read()
+        for name, data in {"magic.pta1": b"XXXX" + raw[4:], "short.pta1": raw[:12],
+                           "trunc.pta1": raw[:-3], "trail.pta1": raw + b"\x00\x00"}.items():
+            with open(name, "wb") as f:
+                f.write(data)
+            try:
+                RefPTA.load(name)
+                pta_bad[name] = (None, None)
+            except Exception as e:  # noqa: BLE001
+                pta_bad[name] = (type(e).__name__, str(e))
+    finally:
+        os.chdir(cwd)
+    dump("formats.pkl.gz", dict(tries=tries, mats=mats, ark_bad=bad, scp_bad=scp_res,
+                                pta_bad=pta_bad))
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["trie", "lookahead", "decode", "neural", "subword"]
+    which = sys.argv[1:] or ["trie", "lookahead", "decode", "neural", "subword", "formats"]
     for name in which:
         globals()[f"{name}_cases"]()
     print("golden fixtures written to", HERE)
