@@ -360,6 +360,25 @@ int fb_copy_rows(int32_t n_max, const int32_t* n_dev, const int32_t* src_idx,
 int fb_gather_rows(int32_t n, const int32_t* idx, const void* src, void* dst,
                    int64_t row_bytes, void* stream);
 
+/* ---- multilevel fusion (reference fusion.py:268-380) -------------------- */
+/* rows[b][space_id], rows[b][eos_id] += the word-boundary adjustment of row b:
+ * 0 for an empty word, log dist_pool[slots[b]][rank(state)] - accum[b] at a
+ * final trie state (score_floor for zero probability), oov_factor otherwise. */
+int fb_multilevel_rows(const fb_trie_t* trie, int32_t n, const int32_t* states,
+                       const int32_t* slots, const double* dist_pool, int64_t d_stride,
+                       const double* accum, int32_t space_id, int32_t eos_id,
+                       double oov_factor, double score_floor, double* rows, int64_t r_stride,
+                       void* stream);
+/* Per-row state update for chosen tokens; char_rows = the unadjusted char-LM
+ * rows of the previous states; boundary_rank[b] = word rank, -1 (<unk>) or -2
+ * (no boundary); empty_words counts boundaries that close an empty word. */
+int fb_multilevel_advance(const fb_trie_t* trie, int32_t n, const int32_t* states_in,
+                          const double* accum_in, const int32_t* tokens,
+                          const double* char_rows, int64_t c_stride, int32_t space_id,
+                          int32_t eos_id, int32_t pad_id, int32_t* states_out,
+                          double* accum_out, int32_t* boundary_rank,
+                          unsigned long long* empty_words, void* stream);
+
 /* ---- host-side data formats (no GPU; csrc/host_io.cu) -------------------- */
 /* Kaldi binary ARK float32 matrix at `offset` (reference kaldi_io.py:82-130):
  * rows/cols out; the payload goes to dst when dst != NULL (dst_capacity floats,

@@ -167,3 +167,88 @@ class OracleLstmCharLM:
         h = torch.cat([s.h for s in states])
         c = torch.cat([s.c for s in states])
         return self._run(h, c, list(tokens))
+
+
+# ---- multilevel fusion (fusion.py:268-380) ----------------------------------------
+OOV_STATE = -2
+UNK_RANK = -1
+
+
+@dataclass
+class OracleMultilevelBatch:
+    char_states: list
+    trie_states: np.ndarray
+    histories: list
+    char_accum: np.ndarray
+
+    def __len__(self) -> int:
+        return len(self.char_states)
+
+
+class OracleMultilevelFusion:
+    """fusion.py:280-380: char-LM rows, word-LM rescoring at word boundaries."""
+
+    nonpositive_scores = False
+
+    def __init__(self, char_lm, word_lm, trie, token_dict, oov_factor: float = -10.0):
+        self.char_lm, self.word_lm, self.trie = char_lm, word_lm, trie
+        self.oov_factor = float(oov_factor)
+        self.space_id, self.eos_id, self.pad_id = (token_dict.space_id, token_dict.eos_id,
+                                                   token_dict.pad_id)
+        self.diagnostics = {"empty_words": 0}
+        kids = trie.children_dense() if hasattr(trie, "children_dense") else trie.char_children
+        self._children = kids.astype(np.int64)
+        self._final = trie.is_final.copy()
+        self._rank = trie.word_index.astype(np.int64)
+
+    def start(self, n: int) -> OracleMultilevelBatch:
+        return OracleMultilevelBatch([self.char_lm.start()] * n, np.zeros(n, np.int64),
+                                     [self.word_lm.start_history()] * n, np.zeros(n))
+
+    def _adjust(self, state, b: int) -> float:                       # fusion.py:321-330
+        st = int(state.trie_states[b])
+        if st == 0 and state.char_accum[b] == 0.0:
+            return 0.0
+        if st >= 0 and self._final[st]:
+            p = float(self.word_lm.full_distribution(state.histories[b])[int(self._rank[st])])
+            return float((np.log(p) if p > 0 else SCORE_FLOOR) - state.char_accum[b])
+        return self.oov_factor
+
+    def char_scores(self, state) -> np.ndarray:                      # fusion.py:332-339
+        rows = np.stack([self.char_lm.log_probs(s) for s in state.char_states]).astype(
+            np.float64, copy=True)
+        for b in range(len(state)):
+            adj = self._adjust(state, b)
+            rows[b, self.space_id] += adj
+            rows[b, self.eos_id] += adj
+        return rows
+
+    def advance(self, state, tokens) -> OracleMultilevelBatch:       # fusion.py:341-371
+        tokens = np.asarray(tokens, dtype=np.int64)
+        cs = [self.char_lm.advance(s, int(t)) for s, t in zip(state.char_states, tokens)]
+        ts = state.trie_states.copy()
+        hs = list(state.histories)
+        acc = state.char_accum.copy()
+        for b in range(len(state)):
+            tok = int(tokens[b])
+            if tok == self.pad_id:
+                continue
+            if tok == self.space_id or tok == self.eos_id:
+                st = int(ts[b])
+                if st == 0 and acc[b] == 0.0:
+                    self.diagnostics["empty_words"] += 1
+                rank = int(self._rank[st]) if st >= 0 and self._final[st] else UNK_RANK
+                hs[b] = self.word_lm.extend_history(hs[b], rank)
+                ts[b] = 0
+                acc[b] = 0.0
+                continue
+            acc[b] += float(self.char_lm.log_probs(state.char_states[b])[tok])
+            st = int(ts[b])
+            nxt = int(self._children[st, tok]) if st >= 0 else -1
+            ts[b] = nxt if nxt != -1 else OOV_STATE
+        return OracleMultilevelBatch(cs, ts, hs, acc)
+
+    def reorder(self, state, parent_indices) -> OracleMultilevelBatch:
+        idx = np.asarray(parent_indices, dtype=np.int64)
+        return OracleMultilevelBatch([state.char_states[i] for i in idx], state.trie_states[idx],
+                                     [state.histories[i] for i in idx], state.char_accum[idx])

@@ -15,6 +15,7 @@ from .lexicon_trie import NO_STATE, PrefixTreeAutomaton, build_trie  # noqa: F40
 from .kaldi_io import (FeatureMatrix, ScpEntry, read_ark_matrix, read_feature,  # noqa: F401
                        read_features_pinned, read_scp, write_ark_matrix)
 from .fusion import (DEFAULT_OOV_PENALTY, OOV_STATE, FusionScorer, LookaheadBatch,  # noqa: F401
-                     LookaheadFusion, SubwordBatch, SubwordFusion, cumsum_distribution)
+                     LookaheadFusion, MultilevelBatch, MultilevelFusion, SubwordBatch,
+                     SubwordFusion, cumsum_distribution)
 from .decoder import (AcousticScorer, DecodeConfig, DecodeResult, coverage_improved,  # noqa: F401
                       coverage_original, decode_batch, decode_corpus, eos_allowed)

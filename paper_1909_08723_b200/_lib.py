@@ -100,6 +100,10 @@ _SIGS = {
     "fb_eos_fixup": (C.c_int, [i32, vp, vp, vp, vp, i64, i32, vp]),
     "fb_copy_rows": (C.c_int, [i32, vp, vp, vp, vp, vp, i64, vp]),
     "fb_exp2x": (C.c_int, [i64, vp, vp, vp]),
+    "fb_multilevel_rows": (C.c_int, [C.POINTER(FbTrie), i32, vp, vp, vp, i64, vp, i32, i32,
+                                     C.c_double, C.c_double, vp, i64, vp]),
+    "fb_multilevel_advance": (C.c_int, [C.POINTER(FbTrie), i32, vp, vp, vp, vp, i64, i32, i32,
+                                        i32, vp, vp, vp, vp, vp]),
     "fb_ark_read_matrix": (C.c_int, [C.c_char_p, i64, vp, i64, vp, vp]),
     "fb_ark_read_batch": (C.c_int, [i32, vp, vp, vp, vp, vp, vp, vp, i32]),
     "fb_pta1_read_header": (C.c_int, [C.c_char_p, vp, vp, vp, vp]),

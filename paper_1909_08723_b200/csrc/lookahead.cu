@@ -138,6 +138,74 @@ __global__ void trie_advance_kernel(fb_trie_t trie, int n_max, const int32_t* __
   }
 }
 
+// ---- multilevel fusion (reference fusion.py:268-380) ---------------------
+// Row adjustment of the boundary columns (fusion.py:321-339): rows[b] holds the
+// char-LM row; <space> and <eos> get += adj with
+//   adj = 0                                 empty word (state 0, accum 0)
+//   adj = log P_W(w | h) - accum            known word (final state; P from the
+//                                           history's distribution row dist_pool[slot])
+//   adj = oov_factor                        otherwise (OOV / partial word)
+__global__ void multilevel_rows_kernel(fb_trie_t trie, int n, const int32_t* __restrict__ states,
+                                       const int32_t* __restrict__ slots,
+                                       const double* __restrict__ dist_pool, int64_t d_stride,
+                                       const double* __restrict__ accum, int space_id,
+                                       int eos_id, double oov_factor, double score_floor,
+                                       double* __restrict__ rows, int64_t r_stride) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += gridDim.x * blockDim.x) {
+    const int st = states[b];
+    const double acc = accum[b];
+    double adj;
+    if (st == 0 && acc == 0.0) {
+      adj = 0.0;
+    } else if (st >= 0 && trie.info[4 * st + 2] >= 0) {
+      const double p = dist_pool[(int64_t)slots[b] * d_stride + trie.info[4 * st + 2]];
+      adj = dsub(p > 0.0 ? log(p) : score_floor, acc);
+    } else {
+      adj = oov_factor;
+    }
+    double* r = rows + (int64_t)b * r_stride;
+    r[space_id] = dadd(r[space_id], adj);
+    r[eos_id] = dadd(r[eos_id], adj);
+  }
+}
+
+// State update (fusion.py:341-371): pad keeps the row; <space>/<eos> close the
+// word (brank = its rank or -1 for <unk>, state 0, accum 0, counting empty
+// words); a character adds the unadjusted char-LM log-prob of the token at the
+// previous state (char_rows) to accum and walks the trie (OOV_STATE = -2).
+__global__ void multilevel_advance_kernel(fb_trie_t trie, int n, const int32_t* __restrict__ sin,
+                                          const double* __restrict__ ain,
+                                          const int32_t* __restrict__ tokens,
+                                          const double* __restrict__ char_rows, int64_t c_stride,
+                                          int space_id, int eos_id, int pad_id,
+                                          int32_t* __restrict__ sout, double* __restrict__ aout,
+                                          int32_t* __restrict__ brank,
+                                          unsigned long long* __restrict__ empty_words) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += gridDim.x * blockDim.x) {
+    const int s = sin[b];
+    const double acc = ain[b];
+    const int tok = tokens[b];
+    int ns = s, rk = -2;
+    double na = acc;
+    if (tok == pad_id) {
+      // unchanged
+    } else if (tok == space_id || tok == eos_id) {
+      if (s == 0 && acc == 0.0) atomicAdd(empty_words, 1ull);
+      rk = (s >= 0 && trie.info[4 * s + 2] >= 0) ? trie.info[4 * s + 2] : -1;
+      ns = 0;
+      na = 0.0;
+    } else {
+      na = dadd(acc, char_rows[(int64_t)b * c_stride + tok]);
+      int c = -1;
+      if (s >= 0 && tok >= 0 && tok < trie.alphabet) c = find_child(trie, s, tok);
+      ns = c >= 0 ? c : -2;
+    }
+    sout[b] = ns;
+    aout[b] = na;
+    brank[b] = rk;
+  }
+}
+
 // ---- fp64 running sums over word-distribution rows ----------------------
 // One CTA per row, tiles of TILE elements staged in shared memory; each thread
 // scans ITEMS consecutive values, the block scans the thread totals, and the
@@ -441,6 +509,39 @@ extern "C" int fb_lookahead_scores(const fb_trie_t* trie, int32_t n_max, const i
       space_id, eos_id, oov_penalty, score_floor, out, out_stride, floored);
   count_launch();
   return check_launch("lookahead_scores");
+}
+
+extern "C" int fb_multilevel_rows(const fb_trie_t* trie, int32_t n, const int32_t* states,
+                                  const int32_t* slots, const double* dist_pool,
+                                  int64_t d_stride, const double* accum, int32_t space_id,
+                                  int32_t eos_id, double oov_factor, double score_floor,
+                                  double* rows, int64_t r_stride, void* stream) {
+  FB_CHECK_ARG(trie && trie->info && states && slots && dist_pool && accum && rows,
+               "null multilevel arguments");
+  if (n <= 0) return FB_OK;
+  multilevel_rows_kernel<<<std::min((n + 255) / 256, kNumSMs * 8), 256, 0, (cudaStream_t)stream>>>(
+      *trie, n, states, slots, dist_pool, d_stride, accum, space_id, eos_id, oov_factor,
+      score_floor, rows, r_stride);
+  count_launch();
+  return check_launch("multilevel_rows");
+}
+
+extern "C" int fb_multilevel_advance(const fb_trie_t* trie, int32_t n, const int32_t* states_in,
+                                     const double* accum_in, const int32_t* tokens,
+                                     const double* char_rows, int64_t c_stride, int32_t space_id,
+                                     int32_t eos_id, int32_t pad_id, int32_t* states_out,
+                                     double* accum_out, int32_t* boundary_rank,
+                                     unsigned long long* empty_words, void* stream) {
+  FB_CHECK_ARG(trie && trie->row_ptr && states_in && accum_in && tokens && char_rows &&
+                   states_out && accum_out && boundary_rank && empty_words,
+               "null multilevel arguments");
+  if (n <= 0) return FB_OK;
+  multilevel_advance_kernel<<<std::min((n + 255) / 256, kNumSMs * 8), 256, 0,
+                              (cudaStream_t)stream>>>(
+      *trie, n, states_in, accum_in, tokens, char_rows, c_stride, space_id, eos_id, pad_id,
+      states_out, accum_out, boundary_rank, empty_words);
+  count_launch();
+  return check_launch("multilevel_advance");
 }
 
 extern "C" int fb_trie_advance(const fb_trie_t* trie, int32_t n_max, const int32_t* n_dev,

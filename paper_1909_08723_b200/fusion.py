@@ -338,3 +338,150 @@ class SubwordFusion(FusionScorer):
 
     def reorder(self, state: SubwordBatch, parent_indices: Sequence[int]) -> SubwordBatch:
         return SubwordBatch([state.char_states[i] for i in parent_indices])
+
+
+# ---- multilevel fusion (fusion.py:268-380) ----------------------------------------
+class MultilevelBatch:
+    """Per-row state: provider states (host list), trie state / g... slot / char
+    accumulator on the device, word histories (host)."""
+
+    def __init__(self, fusion, char_states, states_dev, slots_dev, accum_dev, histories):
+        self._fusion = fusion
+        self.char_states = char_states
+        self.states_dev = states_dev          # int32 [n]: >= 0 or OOV_STATE
+        self.slots_dev = slots_dev            # int32 [n]: distribution-pool slot of histories[i]
+        self.accum_dev = accum_dev            # fp64 [n]: char log-prob mass of the open word
+        self.histories = histories
+
+    def __len__(self) -> int:
+        return len(self.char_states)
+
+    @property
+    def trie_states(self) -> np.ndarray:
+        return self.states_dev.cpu().numpy().astype(np.int64)
+
+    @property
+    def char_accum(self) -> np.ndarray:
+        return self.accum_dev.cpu().numpy()
+
+
+class MultilevelFusion(FusionScorer):
+    """Character-LM rows with word-LM rescoring at word boundaries (reference
+    fusion.py:280-380): the <space>/<eos> columns get log P_W(w|h) minus the char
+    mass paid for the word's spelling (known word), ``oov_factor`` (unknown or
+    partial word) or nothing (empty word).  Scores can be positive, so
+    ``nonpositive_scores`` is False (the decoder then never stops early).
+
+    Device side: the row adjustment (``fb_multilevel_rows``) and the per-row
+    state update (``fb_multilevel_advance``: accumulator, CSR trie walk,
+    boundary ranks, empty-word count); each distinct word history's
+    distribution row is uploaded once into a device pool."""
+
+    nonpositive_scores = False
+
+    def __init__(self, char_lm, word_lm, trie, token_dict,
+                 oov_factor: float = DEFAULT_OOV_PENALTY, device=None):
+        if word_lm.vocab_size != trie.num_words:
+            raise ConfigError(f"word LM vocabulary ({word_lm.vocab_size}) does not match"
+                              f" the automaton ({trie.num_words} words)")
+        if not isinstance(trie, PrefixTreeAutomaton):
+            trie = PrefixTreeAutomaton.from_reference(trie)
+        self.char_lm, self.word_lm, self.trie = char_lm, word_lm, trie
+        self.oov_factor = float(oov_factor)
+        self.space_id, self.eos_id, self.pad_id = (token_dict.space_id, token_dict.eos_id,
+                                                   token_dict.pad_id)
+        self.dict_size = len(token_dict)
+        self.device = _device(device)
+        self.dtrie = DeviceTrie(trie, self.device)
+        self._pool = GPool(trie.num_words, self.device)     # rows = distributions (not cumsum)
+        self._slot_of: Dict[tuple, int] = {}
+        self._empty = torch.zeros(1, dtype=torch.int64, device=self.device)
+
+    @property
+    def diagnostics(self) -> dict:
+        return {"empty_words": int(self._empty.item())}
+
+    def _slots_for(self, hists: list) -> List[int]:
+        todo = {}
+        for h in hists:
+            k = _hkey(h)
+            if k not in self._slot_of and k not in todo:
+                todo[k] = h
+        if todo:
+            keys = list(todo)
+            ids = self._pool.alloc(len(keys))
+            dists = np.stack([np.asarray(self.word_lm.full_distribution(todo[k]), np.float64)
+                              for k in keys])
+            self._pool.rows[torch.as_tensor(ids, device=self.device).long()] = torch.as_tensor(
+                dists, device=self.device)
+            for k, s_ in zip(keys, ids):
+                self._slot_of[k] = int(s_)
+        return [self._slot_of[_hkey(h)] for h in hists]
+
+    def _char_rows(self, char_states) -> torch.Tensor:
+        dev_rows = getattr(self.char_lm, "log_probs_device", None)
+        if dev_rows is not None:
+            return dev_rows(char_states).to(torch.float64).clone()
+        rows = np.stack([np.asarray(self.char_lm.log_probs(s), np.float64) for s in char_states])
+        return torch.as_tensor(rows, device=self.device)
+
+    def start(self, n: int) -> MultilevelBatch:
+        h0 = self.word_lm.start_history()
+        s0 = self._slots_for([h0])[0]
+        z32 = lambda v: torch.full((n,), v, dtype=torch.int32, device=self.device)  # noqa: E731
+        return MultilevelBatch(self, [self.char_lm.start()] * n, z32(0), z32(s0),
+                               torch.zeros(n, dtype=torch.float64, device=self.device), [h0] * n)
+
+    def char_scores_device(self, state: MultilevelBatch) -> torch.Tensor:
+        n = len(state)
+        rows = self._char_rows(state.char_states) if n else \
+            torch.empty((0, self.dict_size), dtype=torch.float64, device=self.device)
+        if n:
+            _lib.call("fb_multilevel_rows", self.dtrie.ref, n, _lib.ptr(state.states_dev),
+                      _lib.ptr(state.slots_dev), _lib.ptr(self._pool.rows), self._pool.vw,
+                      _lib.ptr(state.accum_dev), self.space_id, self.eos_id, self.oov_factor,
+                      SCORE_FLOOR, _lib.ptr(rows), rows.stride(0), _lib.stream_ptr())
+        return rows
+
+    def char_scores(self, state: MultilevelBatch) -> np.ndarray:
+        return self.char_scores_device(state).cpu().numpy()
+
+    def advance(self, state: MultilevelBatch, tokens: Sequence[int]) -> MultilevelBatch:
+        tok = np.asarray(tokens, dtype=np.int64).reshape(-1)
+        n = len(state)
+        if tok.shape != (n,):
+            raise ValueError("one chosen token per hypothesis row required")
+        if n == 0:
+            return MultilevelBatch(self, [], state.states_dev.clone(), state.slots_dev.clone(),
+                                   state.accum_dev.clone(), [])
+        char_rows = self._char_rows(state.char_states)      # unadjusted rows of the old states
+        tok_d = torch.as_tensor(tok.astype(np.int32), device=self.device)
+        s_out = torch.empty_like(state.states_dev)
+        a_out = torch.empty_like(state.accum_dev)
+        brank = torch.empty_like(state.states_dev)
+        _lib.call("fb_multilevel_advance", self.dtrie.ref, n, _lib.ptr(state.states_dev),
+                  _lib.ptr(state.accum_dev), _lib.ptr(tok_d), _lib.ptr(char_rows),
+                  char_rows.stride(0), self.space_id, self.eos_id, self.pad_id, _lib.ptr(s_out),
+                  _lib.ptr(a_out), _lib.ptr(brank), _lib.ptr(self._empty), _lib.stream_ptr())
+        many = getattr(self.char_lm, "advance_many", None)
+        toks = [int(t) for t in tok]
+        char_states = (many(state.char_states, toks) if many is not None else
+                       [self.char_lm.advance(s_, t) for s_, t in zip(state.char_states, toks)])
+        hist = list(state.histories)
+        slots = state.slots_dev.clone()
+        br = brank.cpu().numpy()
+        rows_b = np.nonzero(br != -2)[0]
+        if rows_b.size:
+            for b in rows_b:
+                hist[b] = self.word_lm.extend_history(hist[b], int(br[b]))
+            new = self._slots_for([hist[b] for b in rows_b])
+            slots[torch.as_tensor(rows_b, device=self.device)] = torch.as_tensor(
+                np.asarray(new, np.int32), device=self.device)
+        return MultilevelBatch(self, char_states, s_out, slots, a_out, hist)
+
+    def reorder(self, state: MultilevelBatch, parent_indices: Sequence[int]) -> MultilevelBatch:
+        idx_np = np.asarray(parent_indices, dtype=np.int64)
+        idx = torch.as_tensor(idx_np, device=self.device)
+        return MultilevelBatch(self, [state.char_states[i] for i in idx_np],
+                               state.states_dev[idx], state.slots_dev[idx], state.accum_dev[idx],
+                               [state.histories[i] for i in idx_np])

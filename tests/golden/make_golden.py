@@ -16,6 +16,7 @@ Imports the UNMODIFIED reference package ``fusedbeam`` read-only from
 * ``neural.pkl.gz``    -- ``decode_batch`` + ``LookaheadFusion`` driving the
                           oracle's PyTorch-CPU attention-LSTM scorer and LSTM
                           word LM at a small size;
+* ``multilevel.pkl.gz`` -- MultilevelFusion walks and decodes (fusion.py:268-380);
 * ``formats/``         -- PTA1 trie files saved by the reference
                           (lexicon_trie.py:178-224) and a Kaldi ARK/SCP pair
                           written by its ``write_ark_matrix`` (kaldi_io.py:137-160),
@@ -48,7 +49,8 @@ sys.path.insert(0, "/root/reference/pkg/src")
 
 from fusedbeam.char_lm import CharLM, UniformCharLM  # noqa: E402
 from fusedbeam.decoder import DecodeConfig, TraceScorer, _TraceTable, decode_batch  # noqa: E402
-from fusedbeam.fusion import LookaheadBatch, LookaheadFusion, SubwordFusion  # noqa: E402
+from fusedbeam.fusion import (LookaheadBatch, LookaheadFusion, MultilevelFusion,  # noqa: E402
+                              SubwordFusion)
 from fusedbeam.kaldi_io import FeatureMatrix  # noqa: E402
 from fusedbeam.lexicon_trie import build_trie  # noqa: E402
 from fusedbeam.token_dict import TokenDictionary  # noqa: E402
@@ -344,6 +346,78 @@ def subword_cases():
                                             frames=(40, 64), n_utts=4, cases=neural)))
 
 
+def multilevel_cases():
+    """Reference MultilevelFusion (fusion.py:268-380): walks of char_scores /
+    advance / reorder with diagnostics, and decode_batch results."""
+    rng = np.random.default_rng(66)
+    letters = ["a", "b", "c"]
+    d = TokenDictionary(letters)
+    words = ["a", "ab", "abc", "b", "bc", "ca", "cab"]
+    t = build_trie(words, d)
+    ranked = t.words(d)
+    V = len(d)
+    walks = []
+    for i in range(6):
+        rows = {(): _char_row(rng, d, eos_scale=0.3)}
+        for tk in range(V):
+            if rng.random() < 0.5:
+                rows[(tk,)] = _char_row(rng, d, eos_scale=0.3)
+        default = _char_row(rng, d)
+        lm_rows = {(): rng.dirichlet(np.ones(len(ranked)))}
+        for w in ranked[:3]:
+            lm_rows[(w,)] = rng.dirichlet(np.ones(len(ranked)))
+        lm = TableLM(vocab=tuple(ranked), rows=lm_rows, eos={})
+        fus = MultilevelFusion(TableCharLM(rows, default), lm, t, d, oov_factor=-7.5)
+        st = fus.start(5)
+        walk = []
+        char_ids = [d.index(c) for c in letters]
+        for step in range(10):
+            sc = fus.char_scores(st)
+            toks = []
+            for b in range(5):
+                u = rng.random()
+                toks.append(d.space_id if u < 0.25 else d.eos_id if u < 0.3 else
+                            d.pad_id if u < 0.33 else int(rng.choice(char_ids)))
+            parents = sorted(rng.integers(0, 5, size=5).tolist())
+            walk.append(dict(scores=sc, tokens=np.array(toks), parents=np.array(parents),
+                             states=st.trie_states.copy(), accum=st.char_accum.copy(),
+                             empty=fus.diagnostics["empty_words"]))
+            st = fus.reorder(fus.advance(st, np.array(toks)), parents)
+        walks.append(dict(rows=rows, default=default, lm_rows=lm_rows, walk=walk))
+    cases = []
+    for i in range(16):
+        nutt = int(rng.integers(1, 5))
+        tables = {}
+        for u in range(nutt):
+            uid = f"m{i}_{u}"
+            tables[uid] = rand_table(rng, d, uid, int(rng.integers(2, 6)), depth=2,
+                                     quantized=bool(i % 2))
+        rows = {(): _char_row(rng, d, eos_scale=0.2)}
+        for tk in range(V):
+            if rng.random() < 0.6:
+                rows[(tk,)] = _char_row(rng, d, eos_scale=0.2)
+        default = _char_row(rng, d)
+        lm_rows = {(): rng.dirichlet(np.ones(len(ranked)))}
+        for w in ranked[:4]:
+            lm_rows[(w,)] = rng.dirichlet(np.ones(len(ranked)))
+        uniform = i % 4 == 0
+        clm = UniformCharLM(d) if uniform else TableCharLM(rows, default)
+        lm = TableLM(vocab=tuple(ranked), rows=lm_rows, eos={})
+        cfg = dict(beam_size=int(rng.integers(1, 7)), lm_weight=[0.4, 0.8, 1.0, 0.6][i % 4],
+                   coverage_mode=["off", "improved", "original", "off"][i % 4],
+                   coverage_weight=0.05, tau1=0.4, tau2=0.9, cov_margin=0.7,
+                   eos_gamma=[None, 1.5, None, 1.2][i % 4], max_len_ratio=[1.0, 1.5, 2.0, 1.0][i % 4])
+        fus = MultilevelFusion(clm, lm, t, d, oov_factor=-6.0)
+        feats = [FeatureMatrix(uid, np.zeros((1, 1), np.float32)) for uid in tables]
+        res = decode_batch(feats, TraceScorer(tables), fus, DecodeConfig(**cfg), d)
+        cases.append(dict(tables={k: (v.t_enc, v.rows, v.default) for k, v in tables.items()},
+                          order=list(tables), cfg=cfg, uniform=uniform, rows=rows,
+                          default=default, lm_rows=lm_rows, empty=fus.diagnostics["empty_words"],
+                          results=[(r.utt_id, r.tokens, r.score, r.attn_accum.copy(),
+                                    r.finished, r.steps) for r in res]))
+    dump("multilevel.pkl.gz", dict(letters=letters, words=words, walks=walks, cases=cases))
+
+
 def formats_cases():
     from fusedbeam import kaldi_io as rk
     from fusedbeam.lexicon_trie import PrefixTreeAutomaton as RefPTA
@@ -434,7 +508,8 @@ def formats_cases():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["trie", "lookahead", "decode", "neural", "subword", "formats"]
+    which = sys.argv[1:] or ["trie", "lookahead", "decode", "neural", "subword", "formats",
+                             "multilevel"]
     for name in which:
         globals()[f"{name}_cases"]()
     print("golden fixtures written to", HERE)

@@ -241,3 +241,50 @@ def test_subword_neural_decode_matches_reference_bitwise():
         many = lm2.advance_many([s0] * 4, toks)
         for s, t in zip(many, toks):
             np.testing.assert_allclose(s.row, lm2.advance(s0, t).row, rtol=0, atol=1e-5)
+
+
+# ---- multilevel fusion: fusion.py:268-380 ------------------------------------------
+def _ml_parts(g, walk_or_case, d):
+    from oracle.lookahead import OracleTableLM
+    from oracle.subword import OracleTableCharLM, OracleUniformCharLM
+    t = build_trie(g["words"], d)
+    ranked = t.ranked_words(d)
+    lm = OracleTableLM(ranked, walk_or_case["lm_rows"], {})
+    if walk_or_case.get("uniform"):
+        clm = OracleUniformCharLM(len(d), d.pad_id)
+    else:
+        clm = OracleTableCharLM(walk_or_case["rows"], walk_or_case["default"])
+    return t, lm, clm
+
+
+def test_multilevel_walks_match_reference_bitwise():
+    from oracle.subword import OracleMultilevelFusion
+    g = load_golden("multilevel.pkl.gz")
+    d = OracleDict(g["letters"])
+    for w in g["walks"]:
+        t, lm, clm = _ml_parts(g, w, d)
+        fus = OracleMultilevelFusion(clm, lm, t, d, oov_factor=-7.5)
+        assert not fus.nonpositive_scores
+        st = fus.start(5)
+        for step in w["walk"]:
+            np.testing.assert_array_equal(st.trie_states, step["states"])
+            np.testing.assert_array_equal(st.char_accum, step["accum"])
+            assert fus.diagnostics["empty_words"] == step["empty"]
+            np.testing.assert_array_equal(fus.char_scores(st), step["scores"])
+            st = fus.reorder(fus.advance(st, step["tokens"]), step["parents"].tolist())
+
+
+def test_multilevel_decode_matches_reference_bitwise():
+    from oracle.subword import OracleMultilevelFusion
+    g = load_golden("multilevel.pkl.gz")
+    d = OracleDict(g["letters"])
+    for case in g["cases"]:
+        t, lm, clm = _ml_parts(g, case, d)
+        fus = OracleMultilevelFusion(clm, lm, t, d, oov_factor=-6.0)
+        feats = [_Feat(u, np.zeros((1, 1), np.float32)) for u in case["order"]]
+        res = decode_batch(feats, TableScorer(case["tables"]), fus, OracleConfig(**case["cfg"]), d)
+        assert fus.diagnostics["empty_words"] == case["empty"]
+        for r, (uid, toks, score, acc, fin, steps) in zip(res, case["results"]):
+            assert (r.utt_id, r.tokens, r.finished, r.steps) == (uid, toks, fin, steps)
+            assert r.score == score
+            assert r.attn_accum.tobytes() == acc.tobytes()
