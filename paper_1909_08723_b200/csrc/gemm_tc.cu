@@ -30,6 +30,19 @@
 
 namespace fb {
 
+#ifdef FB_GEMM_TRACE
+// dev experiment: per-k-block event times (ns, %globaltimer) of CTA 0
+__device__ unsigned long long g_trace[6][256];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(slot, i) do { if (blockIdx.x == 0 && (i) < 256 && (threadIdx.x & 31) == 0) g_trace[slot][i] = gtime(); } while (0)
+#else
+#define TRACE(slot, i) do {} while (0)
+#endif
+
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;            // 64 bf16 = 128 B = one swizzle atom
 constexpr int TC_STAGES = 3;
@@ -335,10 +348,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       for (int kb = 0; kb < num_kb; ++kb, ++gk) {
         const int s = gk % TC_STAGES;
         const uint32_t ph = (gk / TC_STAGES) & 1;
+        TRACE(0, gk);
         if (lane == 0) {
           mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
           mbar_expect_tx(smem_u32(&bar_full[s]), stage_bytes);
         }
+        TRACE(1, gk);
         __syncwarp();
         const uint32_t full = smem_u32(&bar_full[s]);
         unsigned char* st = base + (size_t)s * stage_bytes;
@@ -365,7 +380,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           for (int kb = kb0; kb < kb1; ++kb, ++gk) {
             const int s = gk % TC_STAGES;
             const uint32_t ph = (gk / TC_STAGES) & 1;
+            TRACE(2, gk);
             mbar_wait(smem_u32(&bar_full[s]), ph);
+            TRACE(3, gk);
             asm volatile("tcgen05.fence::after_thread_sync;");
             unsigned char* st = base + (size_t)s * stage_bytes;
             const uint64_t bdesc0 = smem_desc_sw128(smem_u32(st + a_planes * A_TILE));
@@ -379,6 +396,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                          ((kb - kb0) | (a_planes - 1 - p) | k) != 0);
             }
             mma_commit_elect(smem_u32(&bar_empty[s]));
+            TRACE(4, gk);
           }
           mma_commit_elect(smem_u32(&bar_tfull[slot]));
         }
@@ -656,6 +674,12 @@ static int launch_tc(const fb_gemm_t* g, int a_planes, int64_t a_plane_rows, int
 }  // namespace fb
 
 using namespace fb;
+
+#ifdef FB_GEMM_TRACE
+extern "C" int fb_gemm_trace_read(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace)) == cudaSuccess ? 0 : 3;
+}
+#endif
 
 extern "C" int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_rows,
                           void* stream) {
