@@ -32,7 +32,7 @@ namespace fb {
 
 #ifdef FB_GEMM_TRACE
 // dev experiment: per-k-block event times (ns, %globaltimer) of CTA 0
-__device__ unsigned long long g_trace[6][256];
+__device__ unsigned long long g_trace[10][256];
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -183,6 +183,15 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
   // warp's half of the tile (BN/2 columns)
   float4 st_stats = make_float4(-INFINITY, 0.f, -INFINITY, 0.f);
   constexpr int CH = BN / 64;                 // 32-column chunks per half
+  // vectorised LSTM cell when every per-row access is 16-byte aligned
+  const bool vec_cell =
+      g.mode == 1 && (g.hidden % 8) == 0 && (g.ld_cin % 4) == 0 && (g.ld_cout % 4) == 0 &&
+      (g.ld_h % 4) == 0 && (g.ld_res % 4) == 0 && (g.ld_add % 4) == 0 && (g.ld_hs % 8) == 0 &&
+      (g.hs_plane_rows * g.ld_hs) % 8 == 0 &&
+      ((reinterpret_cast<uintptr_t>(g.c_in) | reinterpret_cast<uintptr_t>(g.c_out) |
+        reinterpret_cast<uintptr_t>(g.h_out) | reinterpret_cast<uintptr_t>(g.h_res) |
+        reinterpret_cast<uintptr_t>(g.addend) | reinterpret_cast<uintptr_t>(g.h_split) |
+        reinterpret_cast<uintptr_t>(g.bias)) % 16) == 0;
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
     const int cb = half * CH + c;
@@ -220,10 +229,86 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
         st_stats.z = m2;
       }
     }
+    if (nb >= g.n) continue;
+    if (g.mode == 1 && vec_cell) {
+      // lane = row and its 32 accumulator columns = 8 whole units (gates 4u+q),
+      // straight from the TMEM load: vector loads/stores per row, no transpose
+      const int row = row0 + lane;
+      const int unit0 = nb >> 2;
+      if (row < M) {
+        const int slot = g.rows ? __ldg(g.rows + row) : row;
+        const int pr = g.parent ? __ldg(g.parent + slot) : slot;
+        float cp[8], hr[8], hv[8], cv[8];
+        if (g.c_in) {
+          const float4* s4 = reinterpret_cast<const float4*>(g.c_in + (int64_t)pr * g.ld_cin + unit0);
+          const float4 a = __ldg(s4), b = __ldg(s4 + 1);
+          cp[0] = a.x; cp[1] = a.y; cp[2] = a.z; cp[3] = a.w;
+          cp[4] = b.x; cp[5] = b.y; cp[6] = b.z; cp[7] = b.w;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) cp[u] = 0.f;
+        }
+        if (g.h_res) {
+          const float4* s4 = reinterpret_cast<const float4*>(g.h_res + (int64_t)slot * g.ld_res + unit0);
+          const float4 a = __ldg(s4), b = __ldg(s4 + 1);
+          hr[0] = a.x; hr[1] = a.y; hr[2] = a.z; hr[3] = a.w;
+          hr[4] = b.x; hr[5] = b.y; hr[6] = b.z; hr[7] = b.w;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) hr[u] = 0.f;
+        }
+        // every load of the row issued before any use (one memory round trip)
+        float4 b4[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          b4[u] = g.bias ? __ldg(reinterpret_cast<const float4*>(g.bias) + unit0 + u)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (g.addend) {
+          const float4* a4p = reinterpret_cast<const float4*>(g.addend + (int64_t)row * g.ld_add) + unit0;
+          float4 a4[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) a4[u] = __ldg(a4p + u);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            b4[u].x += a4[u].x; b4[u].y += a4[u].y; b4[u].z += a4[u].z; b4[u].w += a4[u].w;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const float gi = v[4 * u] + b4[u].x, gf = v[4 * u + 1] + b4[u].y;
+          const float gg = v[4 * u + 2] + b4[u].z, go = v[4 * u + 3] + b4[u].w;
+          cv[u] = fsig(gf) * cp[u] + fsig(gi) * ftanh(gg);
+          hv[u] = fsig(go) * ftanh(cv[u]) + hr[u];
+        }
+        float4* c4 = reinterpret_cast<float4*>(g.c_out + (int64_t)slot * g.ld_cout + unit0);
+        c4[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
+        c4[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
+        float4* h4 = reinterpret_cast<float4*>(g.h_out + (int64_t)slot * g.ld_h + unit0);
+        h4[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
+        h4[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
+        if (g.h_split) {
+          __nv_bfloat16 pl[3][8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const __nv_bfloat16 hi = __float2bfloat16_rn(hv[u]);
+            const float r1 = hv[u] - __bfloat162float(hi);
+            const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+            pl[0][u] = hi;
+            pl[1][u] = mid;
+            pl[2][u] = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+          }
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.h_split) + (int64_t)slot * g.ld_hs + unit0;
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            *reinterpret_cast<uint4*>(o + (int64_t)q * g.hs_plane_rows * g.ld_hs) =
+                *reinterpret_cast<const uint4*>(pl[q]);
+        }
+      }
+      continue;
+    }
 #pragma unroll
     for (int j = 0; j < 32; ++j) st[lane * 33 + j] = v[j];
     __syncwarp();
-    if (nb >= g.n) continue;
     if (g.mode == 1) {
       const int u = lane & 7, rs = lane >> 3;
       const int unit = (nb >> 2) + u;
@@ -457,8 +542,8 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 __global__ void __launch_bounds__(TC_THREADS, 1)
 lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                 const __grid_constant__ CUtensorMap tmW, fb_gemm_t g0, int steps, int num_kb,
-                int kcb, float* c_buf, const float* xp, float* y, int64_t ld_y,
-                __nv_bfloat16* rec, int64_t plane, unsigned* sync) {
+                int kcb, float* c_buf, const float* xp, int64_t step_xp, float* y,
+                int64_t ld_y, int64_t step_y, __nv_bfloat16* rec, int64_t plane, unsigned* sync) {
   constexpr int BN = 128;
   const int batch = g0.m_max, H = g0.hidden;
   const int m_tiles = (batch + TC_BM - 1) / TC_BM;
@@ -506,7 +591,9 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
       for (int t = 0; t < steps; ++t) {
         // h_{t-1} complete in every CTA (grid barrier), then visible to TMA
         const unsigned target = (unsigned)(n_ctas * t);
+        TRACE(0, t);
         while (ld_acquire_u32(sync) < target) __nanosleep(32);
+        TRACE(1, t);
         asm volatile("fence.proxy.async.global;" ::: "memory");
         const CUtensorMap* tmA = (t & 1) ? &tmA1 : &tmA0;
         for (int kb = 0; kb < num_kb; ++kb, ++gk) {
@@ -581,22 +668,26 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[slot]))
                      : "memory");
       }
+      TRACE(2, t);
       const int cur = t & 1, nxt = cur ^ 1;
       fb_gemm_t g = g0;
       g.c_in = t ? c_buf + (int64_t)cur * batch * H : nullptr;
       g.c_out = c_buf + (int64_t)nxt * batch * H;
-      g.h_out = y + (int64_t)t * H;
+      g.h_out = y + (int64_t)t * step_y;
       g.ld_h = ld_y;
-      g.addend = xp + (int64_t)t * 4 * H;
+      g.addend = xp + (int64_t)t * step_xp;
       g.h_split = rec + (int64_t)nxt * 3 * plane;
       epilogue_tile<BN>(g, batch, m0 + quarter * 32, n0, acc, epi_stage[warp - 2], half);
+      TRACE(4, t);
       // publish h_t: every epilogue thread's stores, then one release-increment
       __threadfence();
+      TRACE(5, t);
       asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI_THREADS));
       if (warp == 2 && lane == 0) {
         asm volatile("fence.proxy.async.global;" ::: "memory");
         atomicAdd(sync, 1u);
       }
+      TRACE(3, t);
     }
   }
   __syncthreads();
@@ -720,8 +811,8 @@ extern "C" int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_
 // lives here so a layer costs one C call; tensor maps are built once.
 extern "C" int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden,
                                   const void* w_hh, int32_t k, const float* xp, int64_t ld_xp,
-                                  float* y, int64_t ld_y, float* c_buf, void* rec,
-                                  uint32_t* sync_ws, void* stream) {
+                                  int64_t step_xp, float* y, int64_t ld_y, int64_t step_y,
+                                  float* c_buf, void* rec, uint32_t* sync_ws, void* stream) {
   FB_CHECK_ARG(w_hh && xp && y && c_buf && rec && sync_ws, "null recurrence buffers");
   FB_CHECK_ARG(k % TC_BK == 0 && k >= hidden, "recurrence k must be a multiple of 64 >= hidden");
   FB_CHECK_ARG(steps >= 0 && batch > 0, "bad recurrence sizes");
@@ -754,7 +845,8 @@ extern "C" int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden,
     attr = true;
   }
   lstm_rec_kernel<<<m_tiles * n_tiles, TC_THREADS, smem, s>>>(
-      ta[0], ta[1], tw, g, steps, k / TC_BK, TC_KCB, c_buf, xp, y, ld_y, r, plane, sync_ws);
+      ta[0], ta[1], tw, g, steps, k / TC_BK, TC_KCB, c_buf, xp, step_xp, y, ld_y, step_y, r,
+      plane, sync_ws);
   count_launch();
   return check_launch("lstm_rec");
 }

@@ -216,7 +216,7 @@ class Encoder:
                     # one persistent launch per direction (grid barrier per step)
                     e0 = K.log_gemm_begin()
                     _lib.call("fb_lstm_recurrence", TM, B, He, _lib.ptr(w_hh), kr,
-                              _lib.ptr(xps[r]), TM * 4 * He, _lib.ptr(y), TM * He,
+                              _lib.ptr(xps[r]), TM * 4 * He, 4 * He, _lib.ptr(y), TM * He, He,
                               _lib.ptr(cbuf), _lib.ptr(rec), _lib.ptr(sync),
                               int(st.cuda_stream))
                     K.log_gemm_end(e0, TM * B, None, 4 * He, He)
