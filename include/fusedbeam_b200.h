@@ -395,6 +395,10 @@ int fb_ark_read_matrix(const char* ark_path, int64_t offset, float* dst, int64_t
 int fb_ark_read_batch(int32_t n, const char* const* ark_paths, const int64_t* offsets,
                       float* dst, const int64_t* dst_offsets, const int64_t* capacities,
                       int32_t* rows, int32_t* cols, int32_t threads);
+/* n host memcpys (dsts[i] <- srcs[i], bytes[i]) on a thread pool: staging a
+ * batch of feature matrices into one pinned buffer. */
+int fb_host_copy_batch(int32_t n, const void* const* srcs, void* const* dsts,
+                       const int64_t* bytes, int32_t threads);
 /* PTA1 prefix-tree files (lexicon_trie.py:178-224): header, arrays, write. */
 int fb_pta1_read_header(const char* path, int32_t* num_states, int32_t* num_words,
                         int32_t* max_out, int32_t* alphabet);

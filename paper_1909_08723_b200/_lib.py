@@ -106,6 +106,7 @@ _SIGS = {
     "fb_multilevel_advance": (C.c_int, [C.POINTER(FbTrie), i32, vp, vp, vp, vp, i64, i32, i32,
                                         i32, vp, vp, vp, vp, vp]),
     "fb_ark_read_matrix": (C.c_int, [C.c_char_p, i64, vp, i64, vp, vp]),
+    "fb_host_copy_batch": (C.c_int, [i32, vp, vp, vp, i32]),
     "fb_ark_read_batch": (C.c_int, [i32, vp, vp, vp, vp, vp, vp, vp, i32]),
     "fb_pta1_read_header": (C.c_int, [C.c_char_p, vp, vp, vp, vp]),
     "fb_pta1_read": (C.c_int, [C.c_char_p, vp, vp, vp, vp, vp, vp]),

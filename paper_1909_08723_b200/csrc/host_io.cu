@@ -248,6 +248,24 @@ extern "C" int fb_pta1_write(const char* path, int32_t num_states, int32_t num_w
   return ok ? FB_OK : fail(FB_ERR_IO, std::string(path) + ": write failed");
 }
 
+// ---- batch staging ------------------------------------------------------------
+extern "C" int fb_host_copy_batch(int32_t n, const void* const* srcs, void* const* dsts,
+                                  const int64_t* bytes, int32_t threads) {
+  FB_CHECK_ARG(n >= 0 && srcs && dsts && bytes, "bad host copy arguments");
+  if (n == 0) return FB_OK;
+  const int nt = std::max(1, std::min<int>(threads > 0 ? threads : 8, n));
+  std::atomic<int> next(0);
+  auto work = [&]() {
+    for (int i = next++; i < n; i = next++)
+      if (bytes[i] > 0) memcpy(dsts[i], srcs[i], (size_t)bytes[i]);
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+  work();
+  for (auto& t : pool) t.join();
+  return FB_OK;
+}
+
 // ---- build_trie --------------------------------------------------------------
 // Words as char-id sequences (chars[word_offsets[i] .. word_offsets[i+1])), all
 // non-empty, distinct, ids in [0, alphabet).  Ranks = lexicographic order of the

@@ -161,8 +161,22 @@ class Encoder:
         else:
             x = torch.zeros(shape, dtype=torch.float32)
         xn = x.numpy()
-        for u, f in enumerate(feats):
-            xn[u, :T[u], :Din] = np.asarray(f, np.float32)[:T[u] * d.subsample].reshape(T[u], Din)
+        if _pad(Din) == Din:
+            # contiguous per-utterance copies on the C++ thread pool
+            srcs, keep = [], []
+            for f in feats:
+                a = np.ascontiguousarray(f, np.float32)
+                keep.append(a)
+                srcs.append(a.ctypes.data)
+            row = Din * 4
+            dsts = [xn.ctypes.data + u * TM * row for u in range(B)]
+            nbytes = np.asarray([T[u] * row for u in range(B)], np.int64)
+            n = len(srcs)
+            _lib.call("fb_host_copy_batch", n, (C.c_void_p * n)(*srcs), (C.c_void_p * n)(*dsts),
+                      nbytes.ctypes.data, 16)
+        else:
+            for u, f in enumerate(feats):
+                xn[u, :T[u], :Din] = np.asarray(f, np.float32)[:T[u] * d.subsample].reshape(T[u], Din)
         return x.reshape(B * TM, -1), T
 
     def __call__(self, feats, lengths: Optional[Sequence[int]] = None, out=None):
