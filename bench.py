@@ -415,6 +415,8 @@ def main():
                          f"the reference decoder"}
         match = sum(res[i].tokens == b.tokens for i, b in zip(idx, cres))
         cpu["tokens_match_gpu"] = f"{match}/{n}"
+        same = [abs(res[i].score - b.score) for i, b in zip(idx, cres) if res[i].tokens == b.tokens]
+        cpu["max_score_diff_gpu"] = float(max(same)) if same else None
 
     if rank == 0:
         out = {

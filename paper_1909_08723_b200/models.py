@@ -39,6 +39,10 @@ KGRAN = 64           # K granule of the tensor-core GEMM (one 128 B swizzle atom
 # 64-K chunk: the tensor core's accumulation truncates, which otherwise biases
 # logits toward zero and shows up in long flat decodes.
 KCB_LOGITS = 1
+import os as _os
+# bf16 planes of the word-LM activations (dev knob; 2 planes measured +2 % c2
+# throughput at unchanged parity -- 3 keeps every GEMM fp32-accurate)
+LM_PLANES = int(_os.environ.get("FB_LM_PLANES", "3"))
 
 
 def _pad(k: int, g: int = KGRAN) -> int:
@@ -443,8 +447,8 @@ def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks
             c_in = state_src[:, l, 1]
         K.pack(scratch, [x, hseg], m=m, m_dev=m_dev, rows=src_idx, ranks=ranks,
                tok_default=tok_default, k_pad=lay.k_pad, split=True)
-        K.gemm_tc(scratch, lay.w, m=m, m_dev=m_dev, k=lay.k_pad, bias=lay.b, mode=1, hidden=H,
-                  parent=src_idx, c_in=c_in, c_out=state_dst[:, l, 1],
+        K.gemm_tc(scratch[:LM_PLANES], lay.w, m=m, m_dev=m_dev, k=lay.k_pad, bias=lay.b, mode=1,
+                  hidden=H, parent=src_idx, c_in=c_in, c_out=state_dst[:, l, 1],
                   h_out=state_dst[:, l, 0], k_alg=lay.k_in)
     if logits is not None:
         K.pack(scratch, [(state_dst[:, L - 1, 0], H, 0, state_dst.stride(0))], m=m, m_dev=m_dev,
@@ -453,9 +457,9 @@ def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks
                   stats_vw=w.stats_vw, k_alg=H, kcb=w.kcb_out)
         if timer is not None:
             with timer("lm_out_gemm"):
-                K.gemm_tc(scratch, w.out_w, **kw)
+                K.gemm_tc(scratch[:LM_PLANES], w.out_w, **kw)
         else:
-            K.gemm_tc(scratch, w.out_w, **kw)
+            K.gemm_tc(scratch[:LM_PLANES], w.out_w, **kw)
 
 
 class _DevHist:
