@@ -164,7 +164,8 @@ class ClockSampler:
 # ----------------------------------------------------------- CPU baseline --
 def cpu_decode(wl, d, W, words, utts, n: int, threads: int):
     """The oracle CPU decoder (restated reference search + PyTorch-CPU fp32
-    adapters) on the first n utterances; returns (seconds, results)."""
+    adapters) on a length-stratified sample of n utterances (cpu_sample);
+    returns (seconds, results)."""
     import torch
     from oracle.lexicon import OracleDict, build_trie as obuild
     from oracle.lookahead import OracleLookahead

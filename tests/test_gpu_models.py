@@ -186,3 +186,26 @@ def test_baseline_small_configs_match_oracle(name):
                                               wl.asr.subsample, od.eos_id),
                          None, OracleConfig(**cfg), od)
     _compare(got, want, name)
+
+
+def test_c2_full_size_matches_oracle():
+    """The headline configuration itself (WSJ-shaped model, 65k-word look-ahead
+    LSTM LM, beam 10) on a length-stratified sample of 3 of its 512 utterances:
+    identical tokens (or a near-tie), scores within 1e-4."""
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if root not in sys.path:
+        sys.path.insert(0, root)
+    import bench
+    fb, synth = __import__("paper_1909_08723_b200"), None
+    from paper_1909_08723_b200.models import AttnLstmScorer, LstmWordLM
+    wl, d, W, words, trie, utts = bench.build_inputs("c2", 0)
+    idx = bench.cpu_sample(len(utts), 3)
+    sample = [utts[i] for i in idx]
+    cfg = bench.decode_config(wl)
+    got = fb.decode_batch([fb.FeatureMatrix(u, x) for u, x in sample],
+                          AttnLstmScorer(W, wl.asr, d.eos_id),
+                          fb.LookaheadFusion(trie, LstmWordLM(W, wl.lm), d), cfg, d)
+    _, want = bench.cpu_decode(wl, d, W, words, sample, len(sample), os.cpu_count() or 4)
+    _compare(got, want, "c2")
