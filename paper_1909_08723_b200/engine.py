@@ -199,6 +199,7 @@ class _Session:
             self.fus_buf = torch.zeros((N + 1, V), dtype=torch.float64, device=dev)
         self.graphs = None
         self.per_step_launches = 0.0
+        self.side_stream = torch.cuda.Stream(device=dev)
 
     def reset(self, T: Sequence[int], max_len: Sequence[int]) -> None:
         """Per-decode initial state (decoder.py:350-361): one live row per
@@ -249,11 +250,32 @@ class FusedDecoder:
         return s
 
     def _step(self, S: _Session, c: int, tm, counts) -> None:
-        """One lock-step decode step on parity c (capturable: no host reads)."""
+        """One lock-step decode step on parity c, in order (eager / instrumented)."""
+        self._am(S, c, tm)
+        self._body(S, c, tm, counts)
+        self._tail(S, c, tm, counts)
+
+    def _step_overlapped(self, S: _Session, c: int, prev_tail: bool) -> None:
+        """Graph-captured step: step t's word-boundary tail (trie advance, late
+        LM events, g rows -- only read by step t+1's look-ahead) runs on a side
+        stream concurrently with step t+1's acoustic step, then joins."""
+        if prev_tail and S.lm is not None:
+            main = torch.cuda.current_stream()
+            side = S.side_stream
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                self._tail(S, 1 - c, _NoTimer(), None)
+            self._am(S, c, _NoTimer())
+            main.wait_stream(side)
+        else:
+            self._am(S, c, _NoTimer())
+        self._body(S, c, _NoTimer(), None)
+
+    def _am(self, S: _Session, c: int, tm) -> None:
+        """Acoustic step (+ token LM for SubwordFusion) of parity c."""
         scorer, fusion = self.scorer, self.fusion
-        buf, N, V, B = S.buf, S.N, S.V, S.B
+        buf, N, B = S.buf, S.N, S.B
         rc, nc = S.rows[c], S.count[c]
-        stream = _lib.stream_ptr()              # the capture stream inside a graph
         with tm("am_step"):
             scorer.step_fn(N=N, rows=rc, m=N, m_dev=nc, parent=buf.parent,
                            last_tok=buf.last_tok, prev=S.X2[1 - c], cur=S.X2[c],
@@ -271,6 +293,14 @@ class FusedDecoder:
                              pad_id=fusion.char_lm.pad_id, prev=S.sub_X2[1 - c],
                              cur=S.sub_X2[c], scratch=S.sub_scratch, logits=fus_buf,
                              norm=S.sub_norm)
+
+    def _body(self, S: _Session, c: int, tm, counts) -> None:
+        """Look-ahead, speculative <eos> LM events and selection of parity c."""
+        fusion = self.fusion
+        buf, N, V, B = S.buf, S.N, S.V, S.B
+        rc, nc = S.rows[c], S.count[c]
+        stream = _lib.stream_ptr()              # the capture stream inside a graph
+        fus_buf = S.fus_buf
         if S.lm is not None:
             lm, dtrie = S.lm, fusion.dtrie
             lw = lm.lw
@@ -304,7 +334,17 @@ class FusedDecoder:
         with tm("select"):
             _lib.call("fb_search_step", S.cfg_ref, C.byref(S.views[c]), B, P(S.am_logp), V,
                       P(fus_buf), V, stream)
+
+    def _tail(self, S: _Session, c: int, tm, counts) -> None:
+        """Word-boundary bookkeeping after the selection of parity c."""
+        fusion = self.fusion
+        buf, N = S.buf, S.N
+        rc, nc = S.rows[c], S.count[c]
+        stream = _lib.stream_ptr()
         if S.lm is not None:
+            lm, dtrie = S.lm, fusion.dtrie
+            lw = lm.lw
+            Vw = lw.d.words
             rn, cn = S.rows[1 - c], S.count[1 - c]
             with tm("advance"):
                 _lib.call("fb_trie_advance", dtrie.ref, N, P(cn), P(rn), P(buf.parent),
@@ -360,17 +400,24 @@ class FusedDecoder:
         replayed = 0
         if self.use_graphs and timer is None and counts is None:
             if S.graphs is None:
-                g = [torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()]
+                # first step (no previous tail) + one graph per parity whose
+                # previous step's tail overlaps this step's acoustic step
+                g = [torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()]
                 c0 = lib.fb_launch_count()
+                with torch.cuda.graph(g[2]):
+                    self._step_overlapped(S, 0, prev_tail=False)
+                c1 = lib.fb_launch_count()
                 for p_ in (0, 1):
                     with torch.cuda.graph(g[p_]):
-                        self._step(S, p_, _NoTimer(), None)
-                S.per_step_launches = (lib.fb_launch_count() - c0) / 2.0
+                        self._step_overlapped(S, p_, prev_tail=True)
+                S.per_step_launches = (lib.fb_launch_count() - c1) / 2.0
                 l0 += lib.fb_launch_count() - c0          # captures launch nothing
                 S.graphs = g
+            first = True
             while True:
                 for _ in range(self.poll_every):
-                    S.graphs[parity].replay()
+                    (S.graphs[2] if first else S.graphs[parity]).replay()
+                    first = False
                     parity ^= 1
                     steps += 1
                     replayed += 1
