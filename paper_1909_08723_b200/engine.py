@@ -265,11 +265,13 @@ class FusedDecoder:
             side.wait_stream(main)
             with torch.cuda.stream(side):
                 self._tail(S, 1 - c, _NoTimer(), None)
+                self._lookahead(S, c, _NoTimer())     # needs the tail, not the AM step
             self._am(S, c, _NoTimer())
             main.wait_stream(side)
+            self._body(S, c, _NoTimer(), None, lookahead=False)
         else:
             self._am(S, c, _NoTimer())
-        self._body(S, c, _NoTimer(), None)
+            self._body(S, c, _NoTimer(), None)
 
     def _am(self, S: _Session, c: int, tm) -> None:
         """Acoustic step (+ token LM for SubwordFusion) of parity c."""
@@ -294,7 +296,20 @@ class FusedDecoder:
                              cur=S.sub_X2[c], scratch=S.sub_scratch, logits=fus_buf,
                              norm=S.sub_norm)
 
-    def _body(self, S: _Session, c: int, tm, counts) -> None:
+    def _lookahead(self, S: _Session, c: int, tm) -> None:
+        """Eq. 4 rows of parity c (needs the previous step's tail only)."""
+        if S.lm is None:
+            return
+        fusion, lm = self.fusion, S.lm
+        rc, nc = S.rows[c], S.count[c]
+        with tm("lookahead"):
+            # word_end in the eos column of final rows; log P(</s>) added later
+            _lib.call("fb_lookahead_scores", fusion.dtrie.ref, S.N, P(nc), P(rc), P(lm.trie[c]),
+                      P(lm.hist[c]), P(lm.g), lm.lw.d.words, P(lm.eos), P(lm.zero_eos),
+                      fusion.space_id, fusion.eos_id, fusion.oov_penalty, fusion.score_floor,
+                      P(S.fus_buf), S.V, P(fusion._floored), _lib.stream_ptr())
+
+    def _body(self, S: _Session, c: int, tm, counts, lookahead: bool = True) -> None:
         """Look-ahead, speculative <eos> LM events and selection of parity c."""
         fusion = self.fusion
         buf, N, V, B = S.buf, S.N, S.V, S.B
@@ -305,12 +320,8 @@ class FusedDecoder:
             lm, dtrie = S.lm, fusion.dtrie
             lw = lm.lw
             Vw = lw.d.words
-            with tm("lookahead"):
-                # word_end in the eos column of final rows; log P(</s>) added below
-                _lib.call("fb_lookahead_scores", dtrie.ref, N, P(nc), P(rc), P(lm.trie[c]),
-                          P(lm.hist[c]), P(lm.g), Vw, P(lm.eos), P(lm.zero_eos),
-                          fusion.space_id, fusion.eos_id, fusion.oov_penalty,
-                          fusion.score_floor, P(fus_buf), V, P(fusion._floored), stream)
+            if lookahead:
+                self._lookahead(S, c, tm)
             with tm("lm_spec"):
                 if self.prune_spec:
                     _lib.call("fb_spec_select", S.cfg_ref, C.byref(S.views[c]), B, dtrie.ref,
