@@ -243,15 +243,16 @@ int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_rows, void*
 /* Encoder LSTM recurrence for one direction: for t < steps,
  * gates = xp[:, t] + h_{t-1} W_hh^T (tensor cores, W_hh bf16 [4H, k]), cell
  * epilogue, h_t -> y[:, t] and, split into bf16 planes, into
- * rec[(t+1)%2] ([2][3][batch][k] bf16, rec[0] zero on entry).  c_buf: [2][batch][H].
+ * rec[(t+1)%2] ([2][3][batch][k] bf16, rec[0] zero on entry); the cell state
+ * lives in registers (zero at t = 0).
  * Row b of step t: xp + t*step_xp + b*ld_xp, y + t*step_y + b*ld_y (time-major
  * layouts -- step_* = batch * row width -- keep each step's rows contiguous).
  * One persistent launch: CTAs loop over t with a grid barrier on sync_ws (one
  * uint32, reset here); at most 74 CTAs (both directions co-resident). */
 int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden, const void* w_hh,
                        int32_t k, const float* xp, int64_t ld_xp, int64_t step_xp, float* y,
-                       int64_t ld_y, int64_t step_y, float* c_buf, void* rec,
-                       uint32_t* sync_ws, void* stream);
+                       int64_t ld_y, int64_t step_y, void* rec, uint32_t* sync_ws,
+                       void* stream);
 
 /* Row gather-concatenate into a GEMM A operand:
  *   out[i, :] = [seg0 | seg1 | ... | zero pad up to k_pad], i < m.

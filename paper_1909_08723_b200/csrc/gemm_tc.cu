@@ -542,10 +542,10 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 __global__ void __launch_bounds__(TC_THREADS, 1)
 lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                 const __grid_constant__ CUtensorMap tmW, fb_gemm_t g0, int steps, int num_kb,
-                int kcb, float* c_buf, const float* xp, int64_t step_xp, float* y,
-                int64_t ld_y, int64_t step_y, __nv_bfloat16* rec, int64_t plane, unsigned* sync) {
+                int kcb, const float* xp, int64_t step_xp, float* y, int64_t ld_y,
+                int64_t step_y, __nv_bfloat16* rec, int64_t plane, unsigned* sync) {
   constexpr int BN = 128;
-  const int batch = g0.m_max, H = g0.hidden;
+  const int batch = g0.m_max;
   const int m_tiles = (batch + TC_BM - 1) / TC_BM;
   const int n_ctas = gridDim.x;
   const int tile = blockIdx.x;
@@ -560,7 +560,6 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
   __shared__ __align__(8) uint64_t bar_full[TC_STAGES], bar_empty[TC_STAGES];
   __shared__ __align__(8) uint64_t bar_tfull[TC_NACC], bar_tempty[TC_NACC];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ float epi_stage[8][32 * 33];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -641,43 +640,71 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
       }
     }
   } else {
+    // dedicated cell epilogue: lane = row, 16 units per warp half; the cell
+    // state stays in registers across steps and the step's input projection
+    // is fetched before the accumulator is ready (off the MMA critical path)
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
-    constexpr int CH = BN / 64;
     const uint32_t tl = tmem + ((uint32_t)(quarter * 32) << 16);
+    const int row = m0 + quarter * 32 + lane;
+    const bool ok = row < batch;
+    const int unitb = (n0 >> 2) + half * 16;
+    float cst[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) cst[u] = 0.f;
     int cc = 0;
     for (int t = 0; t < steps; ++t) {
-      float acc[CH][32];
-      for (int kb0 = 0; kb0 < num_kb; kb0 += kcb, ++cc) {
-        const int slot = cc % TC_NACC;
-        mbar_wait(smem_u32(&bar_tfull[slot]), (cc / TC_NACC) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
+      float4 xa[16];
+      const float4* xr =
+          reinterpret_cast<const float4*>(xp + (int64_t)t * step_xp + (int64_t)(ok ? row : 0) * g0.ld_add) +
+          unitb;
 #pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          float v[32];
-          tmem_ld32(tl + slot * BN + (half * CH + c) * 32, v);
-          if (kb0 == 0) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) acc[c][j] = v[j];
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) acc[c][j] += v[j];
-          }
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[slot]))
-                     : "memory");
-      }
+      for (int u = 0; u < 16; ++u) xa[u] = __ldg(xr + u);
+      const int slot = cc % TC_NACC;          // whole K in one TMEM slot (kcb = num_kb)
+      mbar_wait(smem_u32(&bar_tfull[slot]), (cc / TC_NACC) & 1);
+      ++cc;
+      asm volatile("tcgen05.fence::after_thread_sync;");
       TRACE(2, t);
-      const int cur = t & 1, nxt = cur ^ 1;
-      fb_gemm_t g = g0;
-      g.c_in = t ? c_buf + (int64_t)cur * batch * H : nullptr;
-      g.c_out = c_buf + (int64_t)nxt * batch * H;
-      g.h_out = y + (int64_t)t * step_y;
-      g.ld_h = ld_y;
-      g.addend = xp + (int64_t)t * step_xp;
-      g.h_split = rec + (int64_t)nxt * 3 * plane;
-      epilogue_tile<BN>(g, batch, m0 + quarter * 32, n0, acc, epi_stage[warp - 2], half);
+      float hv[16];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float v[32];
+        tmem_ld32(tl + slot * BN + (half * 2 + c) * 32, v);
+#pragma unroll
+        for (int u8 = 0; u8 < 8; ++u8) {
+          const int u = c * 8 + u8;
+          const float gi = v[4 * u8] + xa[u].x, gf = v[4 * u8 + 1] + xa[u].y;
+          const float gg = v[4 * u8 + 2] + xa[u].z, go = v[4 * u8 + 3] + xa[u].w;
+          cst[u] = fsig(gf) * cst[u] + fsig(gi) * ftanh(gg);
+          hv[u] = fsig(go) * ftanh(cst[u]);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[slot]))
+                   : "memory");
+      if (ok) {
+        float4* yo = reinterpret_cast<float4*>(y + (int64_t)t * step_y + (int64_t)row * ld_y + unitb);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          yo[q] = make_float4(hv[4 * q], hv[4 * q + 1], hv[4 * q + 2], hv[4 * q + 3]);
+        __nv_bfloat16 pl[3][16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const __nv_bfloat16 hi = __float2bfloat16_rn(hv[u]);
+          const float r1 = hv[u] - __bfloat162float(hi);
+          const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+          pl[0][u] = hi;
+          pl[1][u] = mid;
+          pl[2][u] = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+        }
+        __nv_bfloat16* o = rec + (int64_t)((t & 1) ^ 1) * 3 * plane + (int64_t)row * g0.ld_hs + unitb;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          uint4* d = reinterpret_cast<uint4*>(o + (int64_t)q * plane);
+          d[0] = *reinterpret_cast<const uint4*>(&pl[q][0]);
+          d[1] = *reinterpret_cast<const uint4*>(&pl[q][8]);
+        }
+      }
       TRACE(4, t);
       // publish h_t: every epilogue thread's stores, then one release-increment
       __threadfence();
@@ -812,8 +839,11 @@ extern "C" int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_
 extern "C" int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden,
                                   const void* w_hh, int32_t k, const float* xp, int64_t ld_xp,
                                   int64_t step_xp, float* y, int64_t ld_y, int64_t step_y,
-                                  float* c_buf, void* rec, uint32_t* sync_ws, void* stream) {
-  FB_CHECK_ARG(w_hh && xp && y && c_buf && rec && sync_ws, "null recurrence buffers");
+                                  void* rec, uint32_t* sync_ws, void* stream) {
+  FB_CHECK_ARG(w_hh && xp && y && rec && sync_ws, "null recurrence buffers");
+  FB_CHECK_ARG(ld_xp % 4 == 0 && step_xp % 4 == 0 && ld_y % 4 == 0 && step_y % 4 == 0 &&
+                   k % 8 == 0 && ((uintptr_t)xp % 16) == 0 && ((uintptr_t)y % 16) == 0,
+               "recurrence layouts must be 16-byte aligned");
   FB_CHECK_ARG(k % TC_BK == 0 && k >= hidden, "recurrence k must be a multiple of 64 >= hidden");
   FB_CHECK_ARG(steps >= 0 && batch > 0, "bad recurrence sizes");
   FB_CHECK_ARG((4 * hidden) % 128 == 0 && hidden % 32 == 0, "hidden must be a multiple of 32");
@@ -845,7 +875,7 @@ extern "C" int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden,
     attr = true;
   }
   lstm_rec_kernel<<<m_tiles * n_tiles, TC_THREADS, smem, s>>>(
-      ta[0], ta[1], tw, g, steps, k / TC_BK, TC_KCB, c_buf, xp, step_xp, y, ld_y, step_y, r,
+      ta[0], ta[1], tw, g, steps, k / TC_BK, k / TC_BK, xp, step_xp, y, ld_y, step_y, r,
       plane, sync_ws);
   count_launch();
   return check_launch("lstm_rec");

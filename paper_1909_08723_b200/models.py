@@ -220,23 +220,21 @@ class Encoder:
             # the two directions are independent: one stream each
             main = torch.cuda.current_stream(dev)
             bufs = [(torch.empty((B, TM, He), dtype=torch.float32, device=dev),
-                     torch.empty((2, B, He), dtype=torch.float32, device=dev),
                      torch.zeros((2, 3, B, kr), dtype=torch.bfloat16, device=dev),
                      torch.zeros(1, dtype=torch.int32, device=dev))
                     for _ in range(2)]
             for r, (w_ih, w_hh, b) in enumerate(dirs):
                 st = self.streams[r]
                 st.wait_stream(main)
-                y, cbuf, rec, sync = bufs[r]
-                for tns in (y, cbuf, rec, sync, xps[r]):
+                y, rec, sync = bufs[r]
+                for tns in (y, rec, sync, xps[r]):
                     tns.record_stream(st)
                 with torch.cuda.stream(st):
                     # one persistent launch per direction (grid barrier per step)
                     e0 = K.log_gemm_begin()
                     _lib.call("fb_lstm_recurrence", TM, B, He, _lib.ptr(w_hh), kr,
                               _lib.ptr(xps[r]), TM * 4 * He, 4 * He, _lib.ptr(y), TM * He, He,
-                              _lib.ptr(cbuf), _lib.ptr(rec), _lib.ptr(sync),
-                              int(st.cuda_stream))
+                              _lib.ptr(rec), _lib.ptr(sync), int(st.cuda_stream))
                     K.log_gemm_end(e0, TM * B, None, 4 * He, He)
                 ys.append(y.reshape(B * TM, He))
             for st in self.streams:

@@ -20,15 +20,15 @@ for _ in range(2):
     rec.zero_()
     if os.environ.get("XPZERO") == "1":        # every row reads the same xp row (cache hits)
         _lib.call("fb_lstm_recurrence", TM, B, H, _lib.ptr(w), k, _lib.ptr(xp), 0,
-                  0, _lib.ptr(y), TM * H, H, _lib.ptr(cb), _lib.ptr(rec), _lib.ptr(sync),
+                  0, _lib.ptr(y), TM * H, H, _lib.ptr(rec), _lib.ptr(sync),
                   _lib.stream_ptr())
     elif TMAJOR:
         _lib.call("fb_lstm_recurrence", TM, B, H, _lib.ptr(w), k, _lib.ptr(xp), 4 * H,
-                  B * 4 * H, _lib.ptr(y), H, B * H, _lib.ptr(cb), _lib.ptr(rec), _lib.ptr(sync),
+                  B * 4 * H, _lib.ptr(y), H, B * H, _lib.ptr(rec), _lib.ptr(sync),
                   _lib.stream_ptr())
     else:
         _lib.call("fb_lstm_recurrence", TM, B, H, _lib.ptr(w), k, _lib.ptr(xp), TM * 4 * H,
-                  4 * H, _lib.ptr(y), TM * H, H, _lib.ptr(cb), _lib.ptr(rec), _lib.ptr(sync),
+                  4 * H, _lib.ptr(y), TM * H, H, _lib.ptr(rec), _lib.ptr(sync),
                   _lib.stream_ptr())
 torch.cuda.synchronize()
 buf = np.zeros((10, 256), np.uint64)
