@@ -230,6 +230,18 @@ typedef struct {
    * 1 = most accurate: the tensor core's in-TMEM accumulation truncates, so
    * score-producing projections drain every 64-K chunk into fp32 registers. */
   int32_t kcb;
+  /* h_split row: 0 = the output slot (rows[i]), 1 = the GEMM row i (the next
+   * GEMM's A operand in the same row order) */
+  int32_t hs_row_mode;
+  /* fb_gemm_tc, optional stream-K: when the (device-side) tile count is
+   * below the SM count, every SM takes an equal share of the tile x K-block
+   * space; a tile split over several CTAs is summed in K order by its last
+   * arriving CTA (deterministic) before the epilogue.  splitk_ws: fp32
+   * [2 * 148 * 128 * 128] partial tiles, splitk_cnt: uint32 [148] zeroed
+   * arrival counters (left zeroed).  One workspace per stream: concurrent
+   * GEMMs must not share it. */
+  float* splitk_ws;
+  uint32_t* splitk_cnt;
 } fb_gemm_t;
 
 int fb_gemm(const fb_gemm_t* g, void* stream);
@@ -258,7 +270,9 @@ int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden, const void*
  *   out[i, :] = [seg0 | seg1 | ... | zero pad up to k_pad], i < m.
  * Segment source row: mode 0 -> i, 1 -> slot = rows[i], 2 -> parent[slot],
  * 3 -> token id tokens[slot] (negative -> tok_default) for embeddings,
- * 4 -> rank from ranks[i] (negative -> tok_default). */
+ * 4 -> rank from ranks[i] (negative -> tok_default), 5 -> skip: the
+ * segment's columns are left untouched (another kernel writes them, e.g. a
+ * GEMM epilogue's h_split). */
 typedef struct {
   const float* src; int64_t ld; int32_t width; int32_t mode;
 } fb_seg_t;

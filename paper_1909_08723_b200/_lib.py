@@ -52,7 +52,8 @@ class FbGemm(C.Structure):
                 ("c_out", vp), ("ld_cout", i64), ("h_out", vp), ("ld_h", i64),
                 ("h_res", vp), ("ld_res", i64), ("addend", vp), ("ld_add", i64),
                 ("h_split", vp), ("hs_plane_rows", i64), ("ld_hs", i64),
-                ("row_stats", vp), ("stats_vw", i32), ("kcb", i32)]
+                ("row_stats", vp), ("stats_vw", i32), ("kcb", i32),
+                ("hs_row_mode", i32), ("splitk_ws", vp), ("splitk_cnt", vp)]
 
 
 class FbSeg(C.Structure):

@@ -48,6 +48,10 @@ pack_rows_kernel(fb_pack_t p, int m_max, const int32_t* __restrict__ m_dev,
       int width;
       if (s < p.nseg) {
         const fb_seg_t& sg = p.seg[s];
+        if (sg.mode == 5) {                         // columns owned by another writer
+          col += sg.width;
+          continue;
+        }
         int64_t r;
         switch (sg.mode) {
           case 0: r = i; break;

@@ -297,7 +297,8 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
             pl[1][u] = mid;
             pl[2][u] = __float2bfloat16_rn(r1 - __bfloat162float(mid));
           }
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.h_split) + (int64_t)slot * g.ld_hs + unit0;
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.h_split) +
+                             (int64_t)(g.hs_row_mode ? row : slot) * g.ld_hs + unit0;
 #pragma unroll
           for (int q = 0; q < 3; ++q)
             *reinterpret_cast<uint4*>(o + (int64_t)q * g.hs_plane_rows * g.ld_hs) =
@@ -306,6 +307,7 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
       }
       continue;
     }
+    TRACE(8, 2 * c);
 #pragma unroll
     for (int j = 0; j < 32; ++j) st[lane * 33 + j] = v[j];
     __syncwarp();
@@ -351,7 +353,7 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
         const float h = fsig(go) * ftanh(c) + hr[it];
         g.c_out[(int64_t)slot[it] * g.ld_cout + unit] = c;
         g.h_out[(int64_t)slot[it] * g.ld_h + unit] = h;
-        if (g.h_split) store_split(g, slot[it], unit, h);
+        if (g.h_split) store_split(g, g.hs_row_mode ? row0 + r : slot[it], unit, h);
       }
     } else {
       const int col = nb + lane;
@@ -365,6 +367,7 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
           g.c[(int64_t)orow * g.ldc + col] = x;
         }
       }
+      TRACE(8, 2 * c + 1);
     }
   }
   if (g.row_stats && row0 + lane < M) {
@@ -375,6 +378,41 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
   }
   __syncwarp();
 }
+
+// Work decomposition of one launch.  Plain: CTA b takes tiles b, b+G, ...
+// whole K.  Stream-K (g.splitk_ws set and fewer tiles than CTAs): the
+// tile x K-block space [0, tiles*num_kb) is cut into `ctas` equal ranges, CTA b
+// taking range b -- up to one partial segment at each end plus whole tiles in
+// between.  Every role (TMA, MMA, epilogue) walks the same segment list.
+struct TcWork {
+  int num_tiles, num_kb, ctas, lo, hi;
+  bool sk;
+  __device__ __forceinline__ int owner(int64_t p) const {   // CTA whose range holds p
+    const int64_t total = (int64_t)num_tiles * num_kb;
+    return (int)(((p + 1) * ctas - 1) / total);
+  }
+  __device__ __forceinline__ int range_lo(int c) const {
+    return (int)((int64_t)c * num_tiles * num_kb / ctas);
+  }
+  // i-th segment of this CTA: tile, K blocks [kb_lo, kb_hi)
+  __device__ __forceinline__ bool seg(int i, int& tile, int& kb_lo, int& kb_hi) const {
+    if (!sk) {
+      tile = (int)blockIdx.x + i * (int)gridDim.x;
+      kb_lo = 0;
+      kb_hi = num_kb;
+      return tile < num_tiles;
+    }
+    const int t0 = lo / num_kb;
+    tile = t0 + i;
+    const int s0 = tile * num_kb;
+    if (s0 + (i == 0 ? lo - s0 : 0) >= hi) return false;
+    kb_lo = i == 0 ? lo - s0 : 0;
+    kb_hi = min(num_kb, hi - s0);
+    return true;
+  }
+};
+
+constexpr int TC_SK_MIN_KB = 8;      // stream-K: at least 8 K blocks (K = 512) per CTA
 
 // Persistent, warp-specialized: warp 0 = TMA producer, warp 1 = MMA issuer
 // (+ TMEM owner), warps 2..5 = epilogue.  Two TMEM accumulators (2 x BN
@@ -389,7 +427,18 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const int m_tiles = (M + TC_BM - 1) / TC_BM;
   const int n_tiles = (g.n + BN - 1) / BN;
   const int num_tiles = m_tiles * n_tiles;
-  if ((int)blockIdx.x >= num_tiles) return;
+  TcWork wk;
+  wk.num_tiles = num_tiles;
+  wk.num_kb = num_kb;
+  wk.sk = g.splitk_ws != nullptr && num_tiles < (int)gridDim.x;
+  if (wk.sk) {
+    wk.ctas = min((int)gridDim.x, max(num_tiles, num_tiles * num_kb / TC_SK_MIN_KB));
+    wk.sk = wk.ctas > num_tiles;
+  }
+  if (!wk.sk) wk.ctas = num_tiles;
+  if ((int)blockIdx.x >= wk.ctas) return;
+  wk.lo = wk.range_lo(blockIdx.x);
+  wk.hi = wk.range_lo(blockIdx.x + 1);
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>(
@@ -400,6 +449,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   __shared__ __align__(8) uint64_t bar_full[TC_STAGES], bar_empty[TC_STAGES];
   __shared__ __align__(8) uint64_t bar_tfull[TC_NACC], bar_tempty[TC_NACC];
   __shared__ uint32_t tmem_base_sh;
+  __shared__ int sk_last_sh;
   __shared__ float epi_stage[8][32 * 33];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -427,10 +477,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
   if (warp == 0) {
     // ---- TMA producer: lane p issues A plane p, lane a_planes the W tile ----
-    int gk = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    int gk = 0, tile, kb_lo, kb_hi;
+    for (int si = 0; wk.seg(si, tile, kb_lo, kb_hi); ++si) {
       const int m0 = (tile % m_tiles) * TC_BM, n0 = (tile / m_tiles) * BN;
-      for (int kb = 0; kb < num_kb; ++kb, ++gk) {
+      for (int kb = kb_lo; kb < kb_hi; ++kb, ++gk) {
         const int s = gk % TC_STAGES;
         const uint32_t ph = (gk / TC_STAGES) & 1;
         TRACE(0, gk);
@@ -454,14 +504,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       // ---- MMA issuer: bf16 x bf16 -> f32, K-major, M = 128, N = BN ----
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(TC_BM >> 4) << 24);
-      int gk = 0, cc = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        for (int kb0 = 0; kb0 < num_kb; kb0 += kcb, ++cc) {
+      int gk = 0, cc = 0, tile, kb_lo, kb_hi;
+      for (int si = 0; wk.seg(si, tile, kb_lo, kb_hi); ++si) {
+        for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += kcb, ++cc) {
           const int slot = cc % TC_NACC;
           mbar_wait(smem_u32(&bar_tempty[slot]), ((cc / TC_NACC) & 1) ^ 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t d = tmem + slot * BN;
-          const int kb1 = min(kb0 + kcb, num_kb);
+          const int kb1 = min(kb0 + kcb, kb_hi);
           for (int kb = kb0; kb < kb1; ++kb, ++gk) {
             const int s = gk % TC_STAGES;
             const uint32_t ph = (gk / TC_STAGES) & 1;
@@ -476,9 +526,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             for (int p = a_planes - 1; p >= 0; --p) {
               const uint64_t adesc0 = smem_desc_sw128(smem_u32(st + p * A_TILE));
 #pragma unroll
-              for (int k = 0; k < TC_BK / 16; ++k)   // 16 elements = 32 B per UMMA_K
+              for (int k = 0; k < TC_BK / 16; ++k) {  // 16 elements = 32 B per UMMA_K
+#ifdef FB_GEMM_NOMMA
+                if (kb != kb0 || p != a_planes - 1 || k != 0) continue;   // dev: feed-only timing
+#endif
                 mma_bf16_elect(d, adesc0 + 2 * k, bdesc0 + 2 * k, idesc,
                          ((kb - kb0) | (a_planes - 1 - p) | k) != 0);
+              }
             }
             mma_commit_elect(smem_u32(&bar_empty[s]));
             TRACE(4, gk);
@@ -493,11 +547,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int half = (warp - 2) >> 2;
     constexpr int CH = BN / 64;
     const uint32_t tl = tmem + ((uint32_t)(quarter * 32) << 16);
-    int cc = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    int cc = 0, tile, kb_lo, kb_hi;
+    for (int si = 0; wk.seg(si, tile, kb_lo, kb_hi); ++si) {
       const int m0 = (tile % m_tiles) * TC_BM, n0 = (tile / m_tiles) * BN;
       float acc[CH][32];
-      for (int kb0 = 0; kb0 < num_kb; kb0 += kcb, ++cc) {
+      for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += kcb, ++cc) {
         const int slot = cc % TC_NACC;
         mbar_wait(smem_u32(&bar_tfull[slot]), (cc / TC_NACC) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
@@ -505,7 +559,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int c = 0; c < CH; ++c) {
           float v[32];
           tmem_ld32(tl + slot * BN + (half * CH + c) * 32, v);
-          if (kb0 == 0) {
+          if (kb0 == kb_lo) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) acc[c][j] = v[j];
           } else {
@@ -517,7 +571,51 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[slot]))
                      : "memory");
       }
+      TRACE(5, si);
+      if (wk.sk) {
+        const int c0 = wk.owner((int64_t)tile * num_kb);
+        const int c1 = wk.owner((int64_t)(tile + 1) * num_kb - 1);
+        if (c0 != c1) {
+          // partial tile: publish, count arrivals; the last CTA sums the
+          // partials in K order (c0..c1) -- the same result whoever is last
+          constexpr int WS_WARP = CH * 32 * 32;
+          auto slot_of = [&](int cta) {
+            return 2 * cta + (tile == wk.range_lo(cta) / num_kb ? 0 : 1);
+          };
+          float* mine = g.splitk_ws + (size_t)slot_of(blockIdx.x) * (8 * WS_WARP) +
+                        (warp - 2) * WS_WARP + lane;
+#pragma unroll
+          for (int c = 0; c < CH; ++c)
+#pragma unroll
+            for (int j = 0; j < 32; ++j) __stcg(mine + (c * 32 + j) * 32, acc[c][j]);
+          __threadfence();
+          asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI_THREADS));
+          if (threadIdx.x == 64) {
+            const unsigned old = atomicAdd(&g.splitk_cnt[tile], 1u);
+            const int last = old == (unsigned)(c1 - c0);
+            if (last) atomicExch(&g.splitk_cnt[tile], 0u);
+            sk_last_sh = last;
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI_THREADS));
+          if (!sk_last_sh) continue;
+          __threadfence();
+          // (own partial re-read too: the sum order must not depend on who is last)
+          for (int cta = c0; cta <= c1; ++cta) {
+            const float* src = g.splitk_ws + (size_t)slot_of(cta) * (8 * WS_WARP) +
+                               (warp - 2) * WS_WARP + lane;
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const float v = __ldcg(src + (c * 32 + j) * 32);
+                acc[c][j] = cta == c0 ? v : acc[c][j] + v;
+              }
+          }
+        }
+      }
+      TRACE(6, si);
       epilogue_tile<BN>(g, M, m0 + quarter * 32, n0, acc, epi_stage[warp - 2], half);
+      TRACE(7, si);
     }
   }
   __syncthreads();
@@ -772,7 +870,8 @@ static int launch_tc_maps(const CUtensorMap& ta, const CUtensorMap& tw, const fb
     return e ? std::max(1, atoi(e)) : TC_KCB;
   }();
   const int kcb = g->kcb > 0 ? g->kcb : kcb_env;
-  k<<<std::min(tiles, kNumSMs), TC_THREADS, smem, s>>>(ta, tw, *g, a_planes, (int)a_plane_rows,
+  const int grid = g->splitk_ws ? kNumSMs : std::min(tiles, kNumSMs);
+  k<<<grid, TC_THREADS, smem, s>>>(ta, tw, *g, a_planes, (int)a_plane_rows,
                                                       g->k / TC_BK, kcb);
   count_launch();
   return check_launch("gemm_tc");
@@ -811,6 +910,7 @@ extern "C" int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_
   FB_CHECK_ARG(g->mode != 1 || (g->n == 4 * g->hidden && g->h_out && g->c_out),
                "LSTM epilogue needs n == 4*hidden and state outputs");
   FB_CHECK_ARG(g->mode != 0 || g->c, "GEMM output is null");
+  FB_CHECK_ARG(!g->splitk_ws || g->splitk_cnt, "stream-K workspace without counters");
   FB_CHECK_ARG(g->mode != 1 || g->bias == nullptr || ((uintptr_t)g->bias % 16) == 0,
                "LSTM bias must be 16B aligned");
   FB_CHECK_ARG(g->mode != 1 || g->addend == nullptr ||

@@ -30,7 +30,8 @@ from . import _lib
 from . import kernels as K
 from .decoder import DecodeConfig, DecodeResult, SearchBuffers, search_cfg
 from .errors import ConfigError
-from .models import AmState, SubLmState, lm_step, split_scratch, subword_step
+from .models import (AM_PIPELINE, LM_SPLITK, AmState, SubLmState, lm_step, split_scratch,
+                     subword_step)
 
 P = _lib.ptr
 
@@ -68,6 +69,9 @@ class _LmPool:
         self.ext_eos = torch.zeros(N, dtype=torch.float64, device=device)
         self.zero_eos = torch.zeros(N, dtype=torch.float64, device=device)
         self.scratch = split_scratch(N, lw.k_max, device)
+        # stream-K workspace of the LM LSTM GEMMs (spec and late events never
+        # overlap: the side stream joins before the speculative events)
+        self.splitk = K.SplitK(device) if LM_SPLITK else None
 
     def start(self) -> None:
         """Slot 0 = LM state after <s> from the zero state (word_lm start_history)."""
@@ -169,6 +173,10 @@ class _Session:
         L, H, C_ = d.dec_layers, d.dec_hidden, d.ctx
         self.X2 = [AmState(L, N, H, C_, dev), AmState(L, N, H, C_, dev)]
         self.scratch = split_scratch(N, w.k_max, dev)
+        # one A operand per decoder GEMM (epilogues write the next one's h planes)
+        self.am_abufs = ([split_scratch(N, k, dev) for k in scorer.step_fn.abuf_shapes()]
+                         if AM_PIPELINE else None)
+        self.pack_stream = torch.cuda.Stream(device=dev) if AM_PIPELINE else None
         self.q = torch.empty((N, d.att), dtype=torch.float32, device=dev)
         self.logits = torch.empty((N, V), dtype=torch.float32, device=dev)
         self.am_logp = torch.zeros((N, V), dtype=torch.float32, device=dev)
@@ -286,7 +294,8 @@ class FusedDecoder:
                            n_live=buf.n_live, t_enc=buf.t_enc, keys=S.keys, enc=S.enc,
                            acc_in=buf.acc[c], acc_out=buf.acc[1 - c], cov=buf.cov,
                            energy=S.energy, sync=S.att_sync,
-                           timer=None if isinstance(tm, _NoTimer) else tm)
+                           timer=None if isinstance(tm, _NoTimer) else tm,
+                           abufs=S.am_abufs, pack_stream=S.pack_stream)
         fus_buf = S.fus_buf
         if S.sub is not None:
             with tm("lm_subword"):
@@ -334,7 +343,8 @@ class FusedDecoder:
                               P(lm.ev_count), P(lm.row_ev), stream)
                 lm_step(lw, m=N, m_dev=lm.ev_count, state_src=lm.state, src_idx=lm.ev_slot,
                         state_dst=lm.ev_state, ranks=lm.ev_rank, tok_default=0,
-                        scratch=lm.scratch, logits=lm.ev_logits, timer=tm, stats=lm.ev_stats)
+                        scratch=lm.scratch, logits=lm.ev_logits, timer=tm, stats=lm.ev_stats,
+                        splitk=lm.splitk)
             with tm("lm_eos"):
                 K.stats_to_g(lm.ev_logits, lm.ev_stats, Vw, lw.v_out, m=N, m_dev=lm.ev_count,
                              slots=lm.ev_row, eos_out=lm.ext_eos)
@@ -372,7 +382,7 @@ class FusedDecoder:
                 lm_step(lw, m=N, m_dev=lm.unk_count, state_src=lm.state, src_idx=lm.unk_slot,
                         state_dst=lm.ev_state[N:], ranks=lm.unk_tok, tok_default=lw.unk_tok,
                         scratch=lm.scratch, logits=lm.ev_logits[N:], timer=tm,
-                        stats=lm.ev_stats[N:])
+                        stats=lm.ev_stats[N:], splitk=lm.splitk)
             with tm("g_build"):
                 K.copy_rows(lm.ev_state, lm.state, m=N, m_dev=lm.bnd_count, src_idx=lm.bnd_src,
                             dst_idx=lm.bnd_slot)

@@ -47,7 +47,8 @@ def gemm(a: torch.Tensor, w: torch.Tensor, *, m: Optional[int] = None, m_dev=Non
 def pack(out: torch.Tensor, segs: Sequence[Tuple], *, m: int, m_dev=None, rows=None,
          parent=None, tokens=None, ranks=None, tok_default: int = 0,
          k_pad: Optional[int] = None, split: bool = False) -> None:
-    """out[i] = concat(segments) zero-padded; segs = (src|None, width, mode, ld?).
+    """out[i] = concat(segments) zero-padded; segs = (src|None, width, mode, ld?);
+    mode 5 leaves the segment's columns untouched (written by another kernel).
     split=True: out is bf16 [3, plane_rows, k_pad] (hi/mid/lo planes)."""
     p = _lib.FbPack()
     for j, s in enumerate(segs):
@@ -85,11 +86,23 @@ def log_gemm_end(e0, m, m_dev, n: int, k_alg: int) -> None:
     GEMM_LOG.append((e0, e1, m_dev.clone() if m_dev is not None else m, n, k_alg))
 
 
+class SplitK:
+    """Stream-K workspace of fb_gemm_tc (fp32 partial tiles + zeroed arrival
+    counters).  One per stream: GEMMs that may run concurrently need their own."""
+
+    SMS = 148
+
+    def __init__(self, device, bn: int = 128):
+        self.ws = torch.empty(2 * self.SMS * 128 * bn, dtype=torch.float32, device=device)
+        self.cnt = torch.zeros(self.SMS, dtype=torch.int32, device=device)
+
+
 def gemm_tc(ap: torch.Tensor, w: torch.Tensor, *, m: Optional[int] = None, m_dev=None,
             k: Optional[int] = None, bias=None, out=None, rows=None, mode: int = 0,
             hidden: int = 0, parent=None, c_in=None, c_out=None, h_out=None, h_res=None,
             addend=None, h_split=None, row_stats=None, stats_vw: int = 0,
-            k_alg: Optional[int] = None, kcb: int = 0) -> None:
+            k_alg: Optional[int] = None, kcb: int = 0, splitk=None,
+            hs_by_row: bool = False) -> None:
     """Tensor-core GEMM: ap = bf16 planes [P, rows, k_pad], w = bf16 [n, k_pad].
     h_split: optional bf16 [3, rows, k] planes receiving h (next A operand).
     kcb: K blocks per TMEM accumulation chunk (0 default; 1 for score logits)."""
@@ -111,9 +124,12 @@ def gemm_tc(ap: torch.Tensor, w: torch.Tensor, *, m: Optional[int] = None, m_dev
     g.addend, g.ld_add = P(addend), _ld(addend)
     if h_split is not None:
         g.h_split, g.hs_plane_rows, g.ld_hs = P(h_split), h_split.shape[1], h_split.stride(1)
+        g.hs_row_mode = 1 if hs_by_row else 0
     if row_stats is not None:
         g.row_stats, g.stats_vw = P(row_stats), stats_vw
     g.kcb = kcb
+    if splitk is not None:
+        g.splitk_ws, g.splitk_cnt = P(splitk.ws), P(splitk.cnt)
     e0 = log_gemm_begin()
     _lib.call("fb_gemm_tc", C.byref(g), ap.shape[0], ap.shape[1], _lib.stream_ptr())
     log_gemm_end(e0, g.m_max, m_dev, g.n, k_alg if k_alg is not None else g.k)

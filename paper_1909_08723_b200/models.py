@@ -20,6 +20,7 @@ GEMM produces all gates, K zero-padded to the GEMM granule.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import itertools
 import math
@@ -43,6 +44,11 @@ import os as _os
 # bf16 planes of the word-LM activations (dev knob; 2 planes measured +2 % c2
 # throughput at unchanged parity -- 3 keeps every GEMM fp32-accurate)
 LM_PLANES = int(_os.environ.get("FB_LM_PLANES", "3"))
+# stream-K for the word-LM LSTM GEMMs (few event rows -> fewer tiles than SMs)
+LM_SPLITK = _os.environ.get("FB_LM_SPLITK", "0") == "1"
+# fused engine: per-GEMM A operands, h planes from the epilogues, prev-step
+# segments packed on a side stream (dev knob to compare against the plain path)
+AM_PIPELINE = _os.environ.get("FB_AM_PIPELINE", "1") == "1"
 
 
 def _pad(k: int, g: int = KGRAN) -> int:
@@ -275,12 +281,20 @@ class DecoderStep:
                  cur: AmState, scratch: torch.Tensor, q: torch.Tensor, logits: torch.Tensor,
                  am_logp: torch.Tensor, cfg_ref, num_utts: int, active, n_live, t_enc,
                  keys, enc, acc_in, acc_out, cov, energy, sync, attn_out=None,
-                 timer=None) -> None:
+                 timer=None, abufs=None, pack_stream=None) -> None:
         w, d = self.w, self.w.d
         tm = timer if timer is not None else _null_timer
         H, C_, E = d.dec_hidden, d.ctx, d.emb
         L = d.dec_layers
         kw = dict(m=m, m_dev=m_dev, rows=rows, parent=parent)
+        if abufs is not None:
+            self._pipelined(abufs, pack_stream, tm, kw, N=N, m=m, m_dev=m_dev, rows=rows,
+                            parent=parent, last_tok=last_tok, prev=prev, cur=cur, q=q,
+                            logits=logits, am_logp=am_logp, cfg_ref=cfg_ref,
+                            num_utts=num_utts, active=active, n_live=n_live, t_enc=t_enc,
+                            keys=keys, enc=enc, acc_in=acc_in, acc_out=acc_out, cov=cov,
+                            energy=energy, sync=sync, attn_out=attn_out)
+            return
         span = tm("am_lstm")
         span.__enter__()
         for l, lay in enumerate(w.dec):
@@ -310,6 +324,68 @@ class DecoderStep:
         with tm("am_output"):
             K.pack(scratch, [(top, H, 1), (cur.ctx, C_, 1)], k_pad=ko, split=True, **kw)
             K.gemm_tc(scratch, w.w_out, k=ko, bias=w.b_out, out=logits, m=m, m_dev=m_dev,
+                      rows=rows, k_alg=H + C_, kcb=KCB_LOGITS)
+            K.log_softmax_rows(logits, am_logp, d.vocab, m=m, m_dev=m_dev, rows=rows)
+
+    def abuf_shapes(self):
+        """k_pad of the per-layer A operands + the output projection's."""
+        return [lay.k_pad for lay in self.w.dec] + [self.w.w_out.shape[1]]
+
+    def _pipelined(self, A, pack_stream, tm, kw, *, N, m, m_dev, rows, parent, last_tok, prev,
+                   cur, q, logits, am_logp, cfg_ref, num_utts, active, n_live, t_enc, keys,
+                   enc, acc_in, acc_out, cov, energy, sync, attn_out):
+        """Same step with one A operand per GEMM: each LSTM epilogue writes its h
+        as bf16 planes straight into the next GEMM's A (h_split, GEMM row
+        order), and the previous-step segments of layers 1.. (ctx, h gathered by
+        parent) are packed on `pack_stream` while layer 0 runs -- two packs on
+        the critical path instead of L + 2."""
+        w, d = self.w, self.w.d
+        H, C_, E = d.dec_hidden, d.ctx, d.emb
+        L = d.dec_layers
+        main = torch.cuda.current_stream()
+        if L > 1:
+            if pack_stream is not None:
+                pack_stream.wait_stream(main)
+                ctx = torch.cuda.stream(pack_stream)
+            else:
+                ctx = contextlib.nullcontext()
+            with ctx:
+                for l in range(1, L):
+                    K.pack(A[l], [(None, H, 5), (prev.ctx, C_, 2), (prev.h[l], H, 2)],
+                           k_pad=w.dec[l].k_pad, split=True, **kw)
+        kq = w.w_q.shape[1]
+        ko = w.w_out.shape[1]
+        q_from_out = kq == H            # q's A = the first H columns of the output A
+        with tm("am_lstm"):
+            for l, lay in enumerate(w.dec):
+                if l == 0:
+                    K.pack(A[0], [(w.emb, E, 3), (prev.ctx, C_, 2), (prev.h[0], H, 2)],
+                           tokens=last_tok, tok_default=self.eos, k_pad=lay.k_pad, split=True,
+                           **kw)
+                elif l == 1 and pack_stream is not None:
+                    main.wait_stream(pack_stream)
+                nxt = A[l + 1] if l + 1 < L else A[L]
+                K.gemm_tc(A[l], lay.w, k=lay.k_pad, bias=lay.b, mode=1, hidden=H,
+                          c_in=prev.c[l], c_out=cur.c[l], h_out=cur.h[l],
+                          h_res=cur.h[l - 1] if l > 0 else None, k_alg=lay.k_in,
+                          h_split=nxt, hs_by_row=True, **kw)
+        top = cur.h[L - 1]
+        if q_from_out:
+            K.gemm_tc(A[L], w.w_q, k=kq, out=q, m=m, m_dev=m_dev, rows=rows, k_alg=H)
+        else:
+            K.pack(A[0], [(top, H, 1)], k_pad=kq, split=True, **kw)
+            K.gemm_tc(A[0], w.w_q, k=kq, out=q, m=m, m_dev=m_dev, rows=rows, k_alg=H)
+        with tm("am_attention"):
+            _lib.call("fb_attention_step", cfg_ref, num_utts, _lib.ptr(active),
+                      _lib.ptr(n_live), _lib.ptr(t_enc), _lib.ptr(keys), _lib.ptr(enc), d.att, C_,
+                      _lib.ptr(w.v), _lib.ptr(q), q.stride(0), _lib.ptr(parent),
+                      _lib.ptr(acc_in), _lib.ptr(acc_out), _lib.ptr(cov), _lib.ptr(cur.ctx),
+                      cur.ctx.stride(0), _lib.ptr(attn_out),
+                      0 if attn_out is None else attn_out.stride(0), _lib.ptr(energy),
+                      _lib.ptr(sync), _lib.stream_ptr())
+        with tm("am_output"):
+            K.pack(A[L], [(None, H, 5), (cur.ctx, C_, 1)], k_pad=ko, split=True, **kw)
+            K.gemm_tc(A[L], w.w_out, k=ko, bias=w.b_out, out=logits, m=m, m_dev=m_dev,
                       rows=rows, k_alg=H + C_, kcb=KCB_LOGITS)
             K.log_softmax_rows(logits, am_logp, d.vocab, m=m, m_dev=m_dev, rows=rows)
 
@@ -425,7 +501,7 @@ class LmWeights:
 
 def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks,
             tok_default: int, scratch: torch.Tensor, logits: Optional[torch.Tensor],
-            timer=None, stats: Optional[torch.Tensor] = None) -> None:
+            timer=None, stats: Optional[torch.Tensor] = None, splitk=None) -> None:
     """Batched LSTM-LM step.  Row i: input token ranks[i] (or tok_default),
     recurrent state from state_src[src_idx[i]] (None -> zero state), new state
     into state_dst[i]; state tensors are [rows, L, 2, H] (h then c per layer).
@@ -447,7 +523,7 @@ def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks
                tok_default=tok_default, k_pad=lay.k_pad, split=True)
         K.gemm_tc(scratch[:LM_PLANES], lay.w, m=m, m_dev=m_dev, k=lay.k_pad, bias=lay.b, mode=1,
                   hidden=H, parent=src_idx, c_in=c_in, c_out=state_dst[:, l, 1],
-                  h_out=state_dst[:, l, 0], k_alg=lay.k_in)
+                  h_out=state_dst[:, l, 0], k_alg=lay.k_in, splitk=splitk)
     if logits is not None:
         K.pack(scratch, [(state_dst[:, L - 1, 0], H, 0, state_dst.stride(0))], m=m, m_dev=m_dev,
                k_pad=w.k_out, split=True)

@@ -22,7 +22,8 @@ SHAPES = {  # name: (M, N, K, mode)
 def run(name, M, N, Kd, mode, reps=20):
     dev = torch.device("cuda")
     sets = []
-    for _ in range(4):
+    nsets = int(os.environ.get("SETS", "4"))
+    for _ in range(nsets):
         a = torch.randn(3, M, Kd, device=dev).to(torch.bfloat16)
         w = (torch.randn(N, Kd, device=dev) * 0.05).to(torch.bfloat16)
         b = torch.randn(N, device=dev)
@@ -33,14 +34,25 @@ def run(name, M, N, Kd, mode, reps=20):
         else:
             kw = dict(out=torch.empty(M, N, device=dev))
         sets.append((a, w, b, kw))
+    if os.environ.get("FB_BENCH_SPLITK") == "1":
+        sk = K.SplitK(dev)
+        for _, _, _, kw in sets:
+            kw["splitk"] = sk
     for a, w, b, kw in sets:
         K.gemm_tc(a, w, m=M, k=Kd, bias=b, **kw)
     torch.cuda.synchronize()
+    # captured in a CUDA graph: eager launches through ctypes are host-bound
+    # (~35 us each), far above the small shapes' device time
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for i in range(reps):
+            a, w, b, kw = sets[i % nsets]
+            K.gemm_tc(a, w, m=M, k=Kd, bias=b, **kw)
+    graph.replay()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for i in range(reps):
-        a, w, b, kw = sets[i % 4]
-        K.gemm_tc(a, w, m=M, k=Kd, bias=b, **kw)
+    graph.replay()
     e1.record()
     torch.cuda.synchronize()
     us = 1000 * e0.elapsed_time(e1) / reps

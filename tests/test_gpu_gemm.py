@@ -120,3 +120,46 @@ def test_row_stats_feed_g_rows_and_eos():
     p = torch.diff(g, dim=1, prepend=torch.zeros(m, 1, dtype=torch.float64, device=dev))
     p_ref = torch.diff(g_ref, dim=1, prepend=torch.zeros(m, 1, dtype=torch.float64, device=dev))
     assert (p - p_ref).abs().max().item() < 1e-15
+
+
+@pytest.mark.parametrize("m,n,k,m_dev", [(160, 4800, 2432, 150), (64, 1280, 1024, 64),
+                                         (600, 4800, 2432, 9), (128, 256, 4096, 128),
+                                         (600, 4800, 2432, 600)])
+def test_tc_stream_k(m, n, k, m_dev):
+    """Stream-K (tiles < SMs): same result as one CTA per tile within fp32
+    rounding, bit-identical across repeats (partials summed in K order), the
+    arrival counters left zeroed, rows past the device count untouched."""
+    from paper_1909_08723_b200 import kernels as K
+    torch.manual_seed(m + n + k)
+    dev = torch.device("cuda")
+    a = torch.randn(m, k, device=dev) * 0.5
+    w = _bf16_exact(torch.rand(n, k, device=dev) * 0.2 - 0.1).to(torch.bfloat16)
+    b = torch.randn(n, device=dev)
+    ap = _packed(a, k)
+    cnt = torch.tensor([m_dev], dtype=torch.int32, device=dev)
+    sk = K.SplitK(dev)
+    outs = []
+    for use in (None, sk, sk):
+        out = torch.full((m, n), 7.0, device=dev)
+        K.gemm_tc(ap, w, m=m, m_dev=cnt, k=k, bias=b, out=out, splitk=use)
+        outs.append(out)
+    ref = a[:m_dev].double() @ w.double().T + b.double()
+    scale = ref.abs().max().item()
+    assert (outs[1][:m_dev].double() - ref).abs().max().item() < 1e-5 * max(1.0, scale)
+    assert (outs[1][:m_dev] - outs[0][:m_dev]).abs().max().item() < 1e-5 * max(1.0, scale)
+    assert torch.equal(outs[1], outs[2])
+    assert (outs[1][m_dev:] == 7.0).all()
+    assert int(sk.cnt.abs().sum()) == 0
+    # LSTM epilogue through stream-K
+    H = n // 4
+    c_in = torch.randn(m, H, device=dev)
+    res = []
+    for use in (None, sk):
+        c_out = torch.zeros(m, H, device=dev)
+        h_out = torch.zeros(m, H, device=dev)
+        K.gemm_tc(ap, w, m=m, m_dev=cnt, k=k, bias=b, mode=1, hidden=H, c_in=c_in, c_out=c_out,
+                  h_out=h_out, splitk=use)
+        res.append((h_out, c_out))
+    assert (res[0][0] - res[1][0]).abs().max().item() < 1e-5
+    assert (res[0][1] - res[1][1]).abs().max().item() < 1e-5
+    assert int(sk.cnt.abs().sum()) == 0
