@@ -72,6 +72,10 @@ class _LmPool:
         # stream-K workspace of the LM LSTM GEMMs (spec and late events never
         # overlap: the side stream joins before the speculative events)
         self.splitk = K.SplitK(device) if LM_SPLITK else None
+        # per-GEMM A operands (the output one's K padding stays zero)
+        self.abufs = ([split_scratch(N, lay.k_pad, device) for lay in lw.layers] +
+                      [torch.zeros((3, N, lw.k_out), dtype=torch.bfloat16, device=device)]
+                      if AM_PIPELINE else None)
 
     def start(self) -> None:
         """Slot 0 = LM state after <s> from the zero state (word_lm start_history)."""
@@ -344,7 +348,7 @@ class FusedDecoder:
                 lm_step(lw, m=N, m_dev=lm.ev_count, state_src=lm.state, src_idx=lm.ev_slot,
                         state_dst=lm.ev_state, ranks=lm.ev_rank, tok_default=0,
                         scratch=lm.scratch, logits=lm.ev_logits, timer=tm, stats=lm.ev_stats,
-                        splitk=lm.splitk)
+                        splitk=lm.splitk, abufs=lm.abufs, pack_stream=S.pack_stream)
             with tm("lm_eos"):
                 K.stats_to_g(lm.ev_logits, lm.ev_stats, Vw, lw.v_out, m=N, m_dev=lm.ev_count,
                              slots=lm.ev_row, eos_out=lm.ext_eos)
@@ -382,7 +386,7 @@ class FusedDecoder:
                 lm_step(lw, m=N, m_dev=lm.unk_count, state_src=lm.state, src_idx=lm.unk_slot,
                         state_dst=lm.ev_state[N:], ranks=lm.unk_tok, tok_default=lw.unk_tok,
                         scratch=lm.scratch, logits=lm.ev_logits[N:], timer=tm,
-                        stats=lm.ev_stats[N:], splitk=lm.splitk)
+                        stats=lm.ev_stats[N:], splitk=lm.splitk, abufs=lm.abufs)
             with tm("g_build"):
                 K.copy_rows(lm.ev_state, lm.state, m=N, m_dev=lm.bnd_count, src_idx=lm.bnd_src,
                             dst_idx=lm.bnd_slot)

@@ -501,13 +501,48 @@ class LmWeights:
 
 def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks,
             tok_default: int, scratch: torch.Tensor, logits: Optional[torch.Tensor],
-            timer=None, stats: Optional[torch.Tensor] = None, splitk=None) -> None:
+            timer=None, stats: Optional[torch.Tensor] = None, splitk=None, abufs=None,
+            pack_stream=None) -> None:
     """Batched LSTM-LM step.  Row i: input token ranks[i] (or tok_default),
     recurrent state from state_src[src_idx[i]] (None -> zero state), new state
     into state_dst[i]; state tensors are [rows, L, 2, H] (h then c per layer).
-    Optionally logits[i] = E . h_top + b."""
+    Optionally logits[i] = E . h_top + b.
+    abufs: one A operand per GEMM (k_pad of each layer, then k_out with zeroed
+    padding): every layer's epilogue writes its h planes into the next A, the
+    recurrent-h segments of layers 1.. are packed on pack_stream (or inline)."""
     H = w.d.hidden
     L = len(w.layers)
+    if abufs is not None and state_src is not None:
+        main = torch.cuda.current_stream()
+        if L > 1:
+            if pack_stream is not None:
+                pack_stream.wait_stream(main)
+                ctx = torch.cuda.stream(pack_stream)
+            else:
+                ctx = contextlib.nullcontext()
+            with ctx:
+                for l in range(1, L):
+                    K.pack(abufs[l], [(None, H, 5), (state_src[:, l, 0], H, 1, state_src.stride(0))],
+                           m=m, m_dev=m_dev, rows=src_idx, k_pad=w.layers[l].k_pad, split=True)
+        for l, lay in enumerate(w.layers):
+            if l == 0:
+                K.pack(abufs[0], [(w.emb, w.in_width, 4, w.emb.stride(0)),
+                                  (state_src[:, 0, 0], H, 1, state_src.stride(0))],
+                       m=m, m_dev=m_dev, rows=src_idx, ranks=ranks, tok_default=tok_default,
+                       k_pad=lay.k_pad, split=True)
+            elif l == 1 and pack_stream is not None:
+                main.wait_stream(pack_stream)
+            nxt = abufs[l + 1] if l + 1 < L else (abufs[L] if logits is not None else None)
+            K.gemm_tc(abufs[l][:LM_PLANES], lay.w, m=m, m_dev=m_dev, k=lay.k_pad, bias=lay.b,
+                      mode=1, hidden=H, parent=src_idx, c_in=state_src[:, l, 1],
+                      c_out=state_dst[:, l, 1], h_out=state_dst[:, l, 0], k_alg=lay.k_in,
+                      splitk=splitk, h_split=nxt, hs_by_row=True)
+        if logits is not None:
+            kw = dict(m=m, m_dev=m_dev, k=w.k_out, bias=w.b_out, out=logits, row_stats=stats,
+                      stats_vw=w.stats_vw, k_alg=H, kcb=w.kcb_out)
+            with (timer("lm_out_gemm") if timer is not None else contextlib.nullcontext()):
+                K.gemm_tc(abufs[L][:LM_PLANES], w.out_w, **kw)
+        return
     for l, lay in enumerate(w.layers):
         if l == 0:
             x = (w.emb, w.in_width, 4, w.emb.stride(0))
