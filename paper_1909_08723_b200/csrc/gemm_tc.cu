@@ -923,11 +923,12 @@ extern "C" int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_
     return e ? atoi(e) : 0;
   }();
   const int tiles128 = ((g->m_max + TC_BM - 1) / TC_BM) * ((g->n + 127) / 128);
-  // measured: 128-wide tiles beat 64-wide ones at every decoder shape, even
-  // when half the SMs idle (scripts/bench_gemm.py), so 64 is opt-in only
+  // 128-wide tiles beat 64-wide ones at the decoder shapes with n > 64
+  // (graph-timed scripts/bench_gemm.py)
   (void)tiles128;
-  const bool want64 = force_bn == 64;
-  if (want64 && g->n > 64 && !g->row_stats)
+  // n <= 64 (the acoustic output projection): a 64-wide tile is the whole N
+  const bool want64 = force_bn == 64 || (force_bn == 0 && g->n <= 64);
+  if (want64 && !g->row_stats)
     return launch_tc<64>(g, a_planes, a_plane_rows, g->n, (cudaStream_t)stream);
   return launch_tc<128>(g, a_planes, a_plane_rows, g->n, (cudaStream_t)stream);
 }

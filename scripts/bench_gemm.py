@@ -17,6 +17,9 @@ SHAPES = {  # name: (M, N, K, mode)
     "lm_out": (256, 65003, 1216, 0),
     "enc_proj": (115200, 1280, 320, 0),
     "enc_rec": (512, 1280, 320, 1),
+    "am_q": (5120, 320, 320, 0),
+    "am_out": (5120, 52, 640, 0),
+    "am_out_2k": (2048, 52, 640, 0),
 }
 
 def run(name, M, N, Kd, mode, reps=20):
