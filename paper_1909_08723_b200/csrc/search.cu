@@ -13,6 +13,15 @@ namespace fb {
 
 constexpr int kSelThreads = 256;
 
+#ifdef FB_SEARCH_TRACE
+// dev experiment: phase times (ns, %globaltimer) of utterance 0's last search step
+__device__ unsigned long long g_strace[16];
+#define STRACE(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) { unsigned long long t_; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_strace[i] = t_; } } while (0)
+#else
+#define STRACE(i) do {} while (0)
+#endif
+
 // numpy's pairwise summation (loops_utils.h pairwise_sum, PW_BLOCKSIZE 128)
 // over f(a[i]); reproduces np.sum bit-for-bit for contiguous float64.
 template <typename F>
@@ -382,6 +391,7 @@ search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict
   __shared__ int n_new, n_fin_new;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  STRACE(0);
 
   // EOS gate per parent (decoder.py:396-398), compared in the AM row dtype.
   if (c.gate_on) {
@@ -419,6 +429,7 @@ search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict
   }
   if (tid == 0) s_nsel = 0, s_stop = 0;
   __syncthreads();
+  STRACE(1);
 
   if (NV >= kRadixMin || (st.force_two_stage & 2)) {
     block_topk(cand, list_mode ? cflat : nullptr, NV, K, sel, &s_nsel, bkt, cl, cmax, taken);
@@ -456,20 +467,34 @@ search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict
     }
   }
 
-  // plan children in selection order (decoder.py:410-432)
-  if (tid == 0) {
-    int nn = 0, nf = 0;
+  STRACE(2);
+  // plan children in selection order (decoder.py:410-432); the selected
+  // candidates' scores are computed in parallel first (one thread each), so
+  // the sequential slot assignment below touches shared memory only
+  {
     const bool cov_on = c.cov_mode != 0;
-    const int cap = 2 * K;
-    int free_slot = 0;
-    for (int k = 0; k < s_nsel; ++k) {
+    for (int k = tid; k < s_nsel; k += kSelThreads) {
       const int j = sel[k];
       const int t = j / n, p = j % n;
       const int ps = base + p;
       const double s = step_score(c, am, am_stride, fus, f_stride, ps, t, gated[p],
                                   st.fus_norm, st.fus_floor);
       const double nb = dadd(st.base_in[ps], s);
-      const double tt = cov_on ? dadd(nb, dmul(c.cov_weight, st.cov_post[ps])) : nb;
+      new_base[k] = nb;                      // staged by selection rank k
+      new_total[k] = cov_on ? dadd(nb, dmul(c.cov_weight, st.cov_post[ps])) : nb;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int nn = 0, nf = 0;
+    const int cap = 2 * K;
+    int free_slot = 0;
+    for (int k = 0; k < s_nsel; ++k) {
+      const int j = sel[k];
+      const int t = j / n, p = j % n;
+      const int ps = base + p;
+      const double nb = new_base[k];         // nn <= k: compaction in place
+      const double tt = new_total[k];
       if (t == c.eos_id) {
         while (free_slot < cap && st.fin_valid[u * cap + free_slot]) ++free_slot;
         const int f = free_slot++;
@@ -492,33 +517,40 @@ search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict
   }
   __syncthreads();
 
-  // token rows and accumulators (parallel copies)
-  for (int i = 0; i < n_new; ++i) {
-    const int32_t* src = st.tok_in + (int64_t)new_par[i] * MT;
-    int32_t* dst = st.tok_out + (int64_t)(base + i) * MT;
-    for (int q = tid; q < steps; q += kSelThreads) dst[q] = src[q];
-    if (tid == 0) {
-      dst[steps] = new_tok[i];
-      st.base_out[base + i] = new_base[i];
-      st.total_out[base + i] = new_total[i];
-      st.parent[base + i] = new_par[i];
-      st.last_tok[base + i] = new_tok[i];
+  STRACE(3);
+  // token rows and accumulators: one flat parallel copy per array (all rows'
+  // loads in flight together)
+  if (steps > 0) {
+    for (int x = tid; x < n_new * steps; x += kSelThreads) {
+      const int i = x / steps, q = x - i * steps;
+      st.tok_out[(int64_t)(base + i) * MT + q] = st.tok_in[(int64_t)new_par[i] * MT + q];
+    }
+    for (int x = tid; x < n_fin_new * steps; x += kSelThreads) {
+      const int i = x / steps, q = x - i * steps;
+      st.fin_tokens[((int64_t)u * 2 * K + fin_slot[i]) * MT + q] =
+          st.tok_in[(int64_t)fin_par[i] * MT + q];
     }
   }
+  for (int i = tid; i < n_new; i += kSelThreads) {
+    st.tok_out[(int64_t)(base + i) * MT + steps] = new_tok[i];
+    st.base_out[base + i] = new_base[i];
+    st.total_out[base + i] = new_total[i];
+    st.parent[base + i] = new_par[i];
+    st.last_tok[base + i] = new_tok[i];
+  }
+  for (int i = tid; i < n_fin_new; i += kSelThreads)
+    st.fin_tokens[((int64_t)u * 2 * K + fin_slot[i]) * MT + steps] = c.eos_id;
   const int T = st.t_enc[u];
-  for (int i = 0; i < n_fin_new; ++i) {
-    const int f = fin_slot[i];
-    const int64_t fe = (int64_t)u * 2 * K + f;
-    const int32_t* src = st.tok_in + (int64_t)fin_par[i] * MT;
-    int32_t* dst = st.fin_tokens + fe * MT;
-    for (int q = tid; q < steps; q += kSelThreads) dst[q] = src[q];
-    if (tid == 0) dst[steps] = c.eos_id;
-    const double* as = st.acc_post + (int64_t)fin_par[i] * c.t_max;
-    double* ad = st.fin_acc + fe * c.t_max;
-    for (int q = tid; q < T; q += kSelThreads) ad[q] = as[q];
+  if (T > 0) {
+    for (int x = tid; x < n_fin_new * T; x += kSelThreads) {
+      const int i = x / T, q = x - i * T;
+      st.fin_acc[((int64_t)u * 2 * K + fin_slot[i]) * c.t_max + q] =
+          st.acc_post[(int64_t)fin_par[i] * c.t_max + q];
+    }
   }
   __syncthreads();
 
+  STRACE(4);
   // finished-set cap, stop tests, result pick (decoder.py:433-450, :464-480)
   __shared__ int res_src, res_is_fin, res_L;
   if (tid == 0) {
@@ -608,6 +640,7 @@ search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict
     for (int q = tid; q < T; q += kSelThreads) ad[q] = asrc[q];
     if (tid == 0) st.res_len[u] = L;
   }
+  STRACE(5);
 }
 
 // Exact pruning of speculative <eos> LM events (see fb_spec_select in the
@@ -912,3 +945,9 @@ extern "C" int fb_eos_fixup(int32_t n_max, const int32_t* ev_count, const int32_
   count_launch();
   return check_launch("eos_fixup");
 }
+
+#ifdef FB_SEARCH_TRACE
+extern "C" int fb_search_trace_read(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, fb::g_strace, sizeof(fb::g_strace)) == cudaSuccess ? 0 : 3;
+}
+#endif
