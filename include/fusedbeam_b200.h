@@ -242,6 +242,12 @@ typedef struct {
    * GEMMs must not share it. */
   float* splitk_ws;
   uint32_t* splitk_cnt;
+  /* mode 0: store exp(2 x) instead of x (the attention query, see
+   * fb_attention_step q_is_exp) */
+  int32_t out_exp2;
+  /* mode 0, n <= 64: store the row log-softmax over the n columns instead of
+   * the logits (same arithmetic as fb_log_softmax_rows) */
+  int32_t out_logsoftmax;
 } fb_gemm_t;
 
 int fb_gemm(const fb_gemm_t* g, void* stream);
@@ -300,7 +306,8 @@ int fb_log_softmax_rows(int32_t m_max, const int32_t* m_dev, const int32_t* rows
  * (fb_keys_exp2t), so tanh(k+q) = 1 - 2/(1 + E_k E_q);
  * ctx[r] = sum_t a[r,t] enc[u,t]; acc_out[r] = acc_in[parent[r]] + a[r]
  * (fp64) and its coverage (cfg->cov_mode).  Rows r = u*beam + i, i < n_live[u].
- * q is consumed in place: its live rows are overwritten with E_q = exp(2 q).
+ * q is consumed in place: its live rows are overwritten with E_q = exp(2 q)
+ * (q_is_exp != 0: q already holds E_q, e.g. from fb_gemm_t.out_exp2).
  * energy_ws: scratch [num_utts*beam, t_max] fp32; holds the attention
  * weights a[r, t] on return.  sync_ws: num_utts*ceil(beam/2) int32, zero on the
  * first call (the kernels leave it zeroed). */
@@ -310,7 +317,7 @@ int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts, const int32_
                       float* q, int64_t ldq, const int32_t* parent, const double* acc_in,
                       double* acc_out, double* cov_out, float* ctx_out, int64_t ld_ctx,
                       float* attn_out, int64_t ld_attn, float* energy_ws, int32_t* sync_ws,
-                      void* stream);
+                      int32_t q_is_exp, void* stream);
 
 /* y[i] = exp(2 x[i]) (attention keys -> E_K, once per batch). */
 int fb_exp2x(int64_t n, const float* x, float* y, void* stream);

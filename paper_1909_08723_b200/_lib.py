@@ -53,7 +53,8 @@ class FbGemm(C.Structure):
                 ("h_res", vp), ("ld_res", i64), ("addend", vp), ("ld_add", i64),
                 ("h_split", vp), ("hs_plane_rows", i64), ("ld_hs", i64),
                 ("row_stats", vp), ("stats_vw", i32), ("kcb", i32),
-                ("hs_row_mode", i32), ("splitk_ws", vp), ("splitk_cnt", vp)]
+                ("hs_row_mode", i32), ("splitk_ws", vp), ("splitk_cnt", vp),
+                ("out_exp2", i32), ("out_logsoftmax", i32)]
 
 
 class FbSeg(C.Structure):
@@ -91,7 +92,8 @@ _SIGS = {
     "fb_log_softmax_rows": (C.c_int, [i32, vp, vp, vp, i64, i32, vp, i64, vp]),
     "fb_row_logsumexp": (C.c_int, [i32, vp, vp, vp, i64, i32, i32, vp, vp]),
     "fb_attention_step": (C.c_int, [C.POINTER(FbSearchCfg), i32, vp, vp, vp, vp, vp, i32, i32,
-                                    vp, vp, i64, vp, vp, vp, vp, vp, i64, vp, i64, vp, vp, vp]),
+                                    vp, vp, i64, vp, vp, vp, vp, vp, i64, vp, i64, vp, vp, i32,
+                                    vp]),
     "fb_spec_events": (C.c_int, [C.POINTER(FbTrie), i32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                  vp]),
     "fb_boundary_plan": (C.c_int, [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp,

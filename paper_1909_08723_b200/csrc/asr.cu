@@ -752,7 +752,8 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
                                  int64_t ldq, const int32_t* parent, const double* acc_in,
                                  double* acc_out, double* cov_out, float* ctx_out,
                                  int64_t ld_ctx, float* attn_out, int64_t ld_attn,
-                                 float* energy_ws, int32_t* sync_ws, void* stream) {
+                                 float* energy_ws, int32_t* sync_ws, int32_t q_is_exp,
+                                 void* stream) {
   FB_CHECK_ARG(cfg && keys && enc && v && q && acc_in && acc_out && ctx_out && energy_ws &&
                    sync_ws, "null attention args");
   FB_CHECK_ARG(cfg->cov_mode == 0 || cov_out, "coverage output required");
@@ -788,7 +789,7 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
 #undef FB_ATTR
     attr_set = true;
   }
-  {
+  if (!q_is_exp) {
     const int64_t total = (int64_t)num_utts * cfg->beam * (att_dim / 4);
     query_exp_kernel<<<(int)std::min<int64_t>((total + 255) / 256, kNumSMs * 8), 256, 0, s>>>(
         num_utts, cfg->beam, active, n_live, q, ldq, att_dim / 4);

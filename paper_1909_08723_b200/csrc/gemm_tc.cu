@@ -229,6 +229,47 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
         st_stats.z = m2;
       }
     }
+    if constexpr (BN == 64) {
+      if (g.out_logsoftmax) {
+        // the whole row is this tile: lane = row, this warp holds columns
+        // [32 half, 32 half + 32), the partner warp (other half) the rest.
+        // Same arithmetic as log_softmax_kernel (asr.cu): per-lane partials
+        // e_l + e_{l+32}, then its xor-butterfly order.
+        const int q = (threadIdx.x >> 5) & 3;
+        float* other = st + (half ? -4 : 4) * (32 * 33);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) st[lane * 33 + j] = v[j];
+        asm volatile("bar.sync %0, 64;" ::"r"(2 + q));
+        float lo[32], hi[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          lo[j] = half ? other[lane * 33 + j] : v[j];
+          hi[j] = half ? v[j] : other[lane * 33 + j];
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(2 + q));
+        float mx = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (j < g.n) mx = fmaxf(mx, lo[j]);
+          if (j + 32 < g.n) mx = fmaxf(mx, hi[j]);
+        }
+        float p[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float s = 0.f;
+          if (j < g.n) s += expf(lo[j] - mx);
+          if (j + 32 < g.n) s += expf(hi[j] - mx);
+          p[j] = s;
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1)
+#pragma unroll
+          for (int j = 0; j < off; ++j) p[j] = p[j] + p[j + off];
+        const float lse = logf(p[0]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = (v[j] - mx) - lse;
+      }
+    }
     if (nb >= g.n) continue;
     if (g.mode == 1 && vec_cell) {
       // lane = row and its 32 accumulator columns = 8 whole units (gates 4u+q),
@@ -363,6 +404,7 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
         if (col < g.n) {
           float x = st[r * 33 + lane];
           if (g.addend) x += g.addend[(int64_t)row * g.ld_add + col];
+          if (g.out_exp2) x = expf(2.0f * x);          // == query_exp_kernel
           const int orow = g.rows ? g.rows[row] : row;
           g.c[(int64_t)orow * g.ldc + col] = x;
         }
@@ -911,6 +953,9 @@ extern "C" int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_
                "LSTM epilogue needs n == 4*hidden and state outputs");
   FB_CHECK_ARG(g->mode != 0 || g->c, "GEMM output is null");
   FB_CHECK_ARG(!g->splitk_ws || g->splitk_cnt, "stream-K workspace without counters");
+  FB_CHECK_ARG(!g->out_logsoftmax || (g->mode == 0 && g->n <= 64 && !g->row_stats &&
+                                      !g->splitk_ws && !g->addend),
+               "fused log-softmax needs mode 0, n <= 64, no stats/addend/stream-K");
   FB_CHECK_ARG(g->mode != 1 || g->bias == nullptr || ((uintptr_t)g->bias % 16) == 0,
                "LSTM bias must be 16B aligned");
   FB_CHECK_ARG(g->mode != 1 || g->addend == nullptr ||
@@ -927,7 +972,7 @@ extern "C" int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_
   // (graph-timed scripts/bench_gemm.py)
   (void)tiles128;
   // n <= 64 (the acoustic output projection): a 64-wide tile is the whole N
-  const bool want64 = force_bn == 64 || (force_bn == 0 && g->n <= 64);
+  const bool want64 = force_bn == 64 || (force_bn == 0 && g->n <= 64) || g->out_logsoftmax;
   if (want64 && !g->row_stats)
     return launch_tc<64>(g, a_planes, a_plane_rows, g->n, (cudaStream_t)stream);
   return launch_tc<128>(g, a_planes, a_plane_rows, g->n, (cudaStream_t)stream);

@@ -102,7 +102,8 @@ def gemm_tc(ap: torch.Tensor, w: torch.Tensor, *, m: Optional[int] = None, m_dev
             hidden: int = 0, parent=None, c_in=None, c_out=None, h_out=None, h_res=None,
             addend=None, h_split=None, row_stats=None, stats_vw: int = 0,
             k_alg: Optional[int] = None, kcb: int = 0, splitk=None,
-            hs_by_row: bool = False) -> None:
+            hs_by_row: bool = False, out_exp2: bool = False,
+            out_logsoftmax: bool = False) -> None:
     """Tensor-core GEMM: ap = bf16 planes [P, rows, k_pad], w = bf16 [n, k_pad].
     h_split: optional bf16 [3, rows, k] planes receiving h (next A operand).
     kcb: K blocks per TMEM accumulation chunk (0 default; 1 for score logits)."""
@@ -128,6 +129,8 @@ def gemm_tc(ap: torch.Tensor, w: torch.Tensor, *, m: Optional[int] = None, m_dev
     if row_stats is not None:
         g.row_stats, g.stats_vw = P(row_stats), stats_vw
     g.kcb = kcb
+    g.out_exp2 = 1 if out_exp2 else 0
+    g.out_logsoftmax = 1 if out_logsoftmax else 0
     if splitk is not None:
         g.splitk_ws, g.splitk_cnt = P(splitk.ws), P(splitk.cnt)
     e0 = log_gemm_begin()

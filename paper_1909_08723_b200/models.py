@@ -49,6 +49,9 @@ LM_SPLITK = _os.environ.get("FB_LM_SPLITK", "0") == "1"
 # fused engine: per-GEMM A operands, h planes from the epilogues, prev-step
 # segments packed on a side stream (dev knob to compare against the plain path)
 AM_PIPELINE = _os.environ.get("FB_AM_PIPELINE", "1") == "1"
+# fused GEMM epilogues: E_q = exp(2 q) for the attention, log-softmax of the
+# acoustic output (dev knob for A/B timing)
+FUSE_EPI = _os.environ.get("FB_FUSE_EPI", "1") == "1"
 
 
 def _pad(k: int, g: int = KGRAN) -> int:
@@ -319,7 +322,7 @@ class DecoderStep:
                       _lib.ptr(acc_in), _lib.ptr(acc_out), _lib.ptr(cov), _lib.ptr(cur.ctx),
                       cur.ctx.stride(0), _lib.ptr(attn_out),
                       0 if attn_out is None else attn_out.stride(0), _lib.ptr(energy),
-                      _lib.ptr(sync), _lib.stream_ptr())
+                      _lib.ptr(sync), 0, _lib.stream_ptr())
         ko = w.w_out.shape[1]
         with tm("am_output"):
             K.pack(scratch, [(top, H, 1), (cur.ctx, C_, 1)], k_pad=ko, split=True, **kw)
@@ -370,11 +373,14 @@ class DecoderStep:
                           h_res=cur.h[l - 1] if l > 0 else None, k_alg=lay.k_in,
                           h_split=nxt, hs_by_row=True, **kw)
         top = cur.h[L - 1]
+        # the epilogue stores E_q = exp(2 q) (fb_attention_step q_is_exp)
         if q_from_out:
-            K.gemm_tc(A[L], w.w_q, k=kq, out=q, m=m, m_dev=m_dev, rows=rows, k_alg=H)
+            K.gemm_tc(A[L], w.w_q, k=kq, out=q, m=m, m_dev=m_dev, rows=rows, k_alg=H,
+                      out_exp2=FUSE_EPI)
         else:
             K.pack(A[0], [(top, H, 1)], k_pad=kq, split=True, **kw)
-            K.gemm_tc(A[0], w.w_q, k=kq, out=q, m=m, m_dev=m_dev, rows=rows, k_alg=H)
+            K.gemm_tc(A[0], w.w_q, k=kq, out=q, m=m, m_dev=m_dev, rows=rows, k_alg=H,
+                      out_exp2=FUSE_EPI)
         with tm("am_attention"):
             _lib.call("fb_attention_step", cfg_ref, num_utts, _lib.ptr(active),
                       _lib.ptr(n_live), _lib.ptr(t_enc), _lib.ptr(keys), _lib.ptr(enc), d.att, C_,
@@ -382,12 +388,17 @@ class DecoderStep:
                       _lib.ptr(acc_in), _lib.ptr(acc_out), _lib.ptr(cov), _lib.ptr(cur.ctx),
                       cur.ctx.stride(0), _lib.ptr(attn_out),
                       0 if attn_out is None else attn_out.stride(0), _lib.ptr(energy),
-                      _lib.ptr(sync), _lib.stream_ptr())
+                      _lib.ptr(sync), 1 if FUSE_EPI else 0, _lib.stream_ptr())
         with tm("am_output"):
             K.pack(A[L], [(None, H, 5), (cur.ctx, C_, 1)], k_pad=ko, split=True, **kw)
-            K.gemm_tc(A[L], w.w_out, k=ko, bias=w.b_out, out=logits, m=m, m_dev=m_dev,
-                      rows=rows, k_alg=H + C_, kcb=KCB_LOGITS)
-            K.log_softmax_rows(logits, am_logp, d.vocab, m=m, m_dev=m_dev, rows=rows)
+            if d.vocab <= 64 and FUSE_EPI:
+                # the epilogue holds whole rows: log-softmax fused, logits never stored
+                K.gemm_tc(A[L], w.w_out, k=ko, bias=w.b_out, out=am_logp, m=m, m_dev=m_dev,
+                          rows=rows, k_alg=H + C_, kcb=KCB_LOGITS, out_logsoftmax=True)
+            else:
+                K.gemm_tc(A[L], w.w_out, k=ko, bias=w.b_out, out=logits, m=m, m_dev=m_dev,
+                          rows=rows, k_alg=H + C_, kcb=KCB_LOGITS)
+                K.log_softmax_rows(logits, am_logp, d.vocab, m=m, m_dev=m_dev, rows=rows)
 
 
 class _NullSpan:

@@ -9,8 +9,8 @@ CMD="python bench.py --profile-only"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/launches_c2.csv $CMD > $OUT/launches.log 2>&1
 echo "launch list rc $?"
-for spec in "gemm_tc_kernel:2600" "att_energy:40" "att_context:40" "seg_scan:60" "pack_rows:2600" \
-            "search_step:40" "spec_select:40" "seg_sum:60"; do
+for spec in "gemm_tc_kernel:1300" "att_energy:100" "att_context:100" "seg_scan:200" "pack_rows:1000" \
+            "search_step:100" "spec_select:100" "seg_sum:200"; do
   k=${spec%%:*}; skip=${spec##*:}
   ncu --set full --import-source on --clock-control none -k regex:$k --launch-skip $skip -c 1 \
       -o $OUT/full_$k $CMD > $OUT/full_$k.log 2>&1

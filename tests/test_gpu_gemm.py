@@ -163,3 +163,28 @@ def test_tc_stream_k(m, n, k, m_dev):
     assert (res[0][0] - res[1][0]).abs().max().item() < 1e-5
     assert (res[0][1] - res[1][1]).abs().max().item() < 1e-5
     assert int(sk.cnt.abs().sum()) == 0
+
+
+@pytest.mark.parametrize("m,n,k", [(300, 52, 640), (129, 64, 128), (70, 33, 256)])
+def test_tc_fused_epilogues_match_separate_kernels(m, n, k):
+    """out_logsoftmax == GEMM + fb_log_softmax_rows and out_exp2 == exp(2 x),
+    bit for bit (same arithmetic), rows gathered through `rows`."""
+    from paper_1909_08723_b200 import kernels as K
+    torch.manual_seed(m + n)
+    dev = torch.device("cuda")
+    a = torch.randn(m, k, device=dev)
+    w = _bf16_exact(torch.randn(n, k, device=dev) * 0.1).to(torch.bfloat16)
+    b = torch.randn(n, device=dev)
+    ap = _packed(a, k)
+    rows = torch.randperm(m, device=dev).to(torch.int32)
+    logits = torch.zeros(m, n, device=dev)
+    K.gemm_tc(ap, w, m=m, k=k, bias=b, out=logits, rows=rows, kcb=1)
+    ref = torch.zeros(m, n, device=dev)
+    K.log_softmax_rows(logits, ref, n, m=m, rows=rows)
+    fused = torch.zeros(m, n, device=dev)
+    K.gemm_tc(ap, w, m=m, k=k, bias=b, out=fused, rows=rows, kcb=1, out_logsoftmax=True)
+    assert torch.equal(fused, ref)
+    e = torch.zeros(m, n, device=dev)
+    K.gemm_tc(ap, w, m=m, k=k, bias=b, out=e, rows=rows, kcb=1, out_exp2=True)
+    assert torch.equal(e, torch.exp(2.0 * logits)) or \
+        (e - torch.exp(2.0 * logits)).abs().max().item() <= 1e-6 * e.abs().max().item()
