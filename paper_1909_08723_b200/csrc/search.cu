@@ -122,7 +122,10 @@ __device__ __forceinline__ Cand warp_best(Cand c) {
 //  3. compact every key with bucket >= T (K plus fp32-bucket ties);
 //  4. exact rank of each survivor among the survivors (C^2 compares, C small).
 // More than cmax survivors (massive exact ties) falls back to argmax rounds.
-constexpr int kRadixMin = 1024;        // candidate count from which the radix path pays
+#ifndef FB_RADIX_MIN
+#define FB_RADIX_MIN 256
+#endif
+constexpr int kRadixMin = FB_RADIX_MIN;  // candidate count from which the radix path pays
 
 __host__ __device__ inline int topk_cmax(int K) { return 4 * K + 64; }
 
@@ -664,9 +667,17 @@ spec_select_kernel(fb_search_cfg_t c, fb_search_state_t st, fb_trie_t trie,
   int* fin = gated + K;                                                // [K]
   int* rank_of = fin + K;                                              // [K]
   unsigned char* taken = reinterpret_cast<unsigned char*>(rank_of + K); // [NV]
+  // radix-path scratch (NV >= kRadixMin): keys with the unsure entries at
+  // -inf, buckets, candidate list, picks
+  double* key2 = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(taken + NV) + 7) & ~uintptr_t(7));   // [NV]
+  uint32_t* bkt = reinterpret_cast<uint32_t*>(key2 + NV);              // [NV]
+  const int cmax = topk_cmax(K);
+  int* cl = reinterpret_cast<int*>(bkt + NV);                          // [cmax]
+  int* pick = cl + cmax;                                               // [K]
   __shared__ Cand wbest[kSelThreads / 32];
   __shared__ double s_thr;
-  __shared__ int s_found;
+  __shared__ int s_found, s_npick;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int p = warp; p < n; p += kSelThreads / 32) {
     const AM* row = am + (int64_t)(base + p) * am_stride;
@@ -701,6 +712,17 @@ spec_select_kernel(fb_search_cfg_t c, fb_search_state_t st, fb_trie_t trie,
   // beam-th best of the known candidates
   if (tid == 0) { s_thr = -INFINITY; s_found = 0; }
   __syncthreads();
+  if (NV >= kRadixMin) {
+    for (int j = tid; j < NV; j += kSelThreads) key2[j] = taken[j] ? -INFINITY : cand[j];
+    __syncthreads();
+    block_topk(key2, nullptr, NV, K, pick, &s_npick, bkt, cl, cmax, taken);
+    __syncthreads();
+    if (tid == 0) {
+      s_found = s_npick;
+      if (s_npick > 0) s_thr = key2[pick[s_npick - 1]];
+    }
+    __syncthreads();
+  } else
   for (int k = 0; k < K; ++k) {
     Cand b{-INFINITY, INT_MAX};
     for (int j = tid; j < NV; j += kSelThreads)
@@ -908,7 +930,11 @@ extern "C" int fb_spec_select(const fb_search_cfg_t* cfg, const fb_search_state_
                               int32_t* ev_rank, int32_t* ev_slot, int32_t* ev_count,
                               int32_t* row_ev, const int32_t* ev_start, void* stream) {
   FB_CHECK_ARG(cfg && st && trie && am && fusion && ev_count && row_ev, "null spec-select args");
-  const size_t smem = (size_t)cfg->beam * cfg->vocab * 9 + 12 * (size_t)cfg->beam;
+  const size_t nv = (size_t)cfg->beam * cfg->vocab;
+  const size_t smem = nv * 9 + 12 * (size_t)cfg->beam + 8 +                     // cand, taken
+                      (nv >= (size_t)kRadixMin                                     // radix
+                           ? nv * 12 + 4 * ((size_t)topk_cmax(cfg->beam) + cfg->beam) + 16
+                           : 0);
   if (smem > 220 * 1024) return fail(FB_ERR_CONFIG, "beam x vocabulary too large");
   cudaStream_t s = (cudaStream_t)stream;
   if (ev_start)   // events appended after the late events queued by the last step
