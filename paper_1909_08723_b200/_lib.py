@@ -16,6 +16,8 @@ from .errors import ConfigError, FormatError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfusedbeam_b200.so")
+if os.environ.get("FB_LIB_AB"):          # dev: A/B timing against another in-tree build
+    LIB_PATH = os.path.join(_HERE, os.environ["FB_LIB_AB"])
 
 i32, i64, f64, vp = C.c_int32, C.c_int64, C.c_double, C.c_void_p
 
