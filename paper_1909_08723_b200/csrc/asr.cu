@@ -840,11 +840,9 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
     const char* e = getenv("FB_ATT_CQ");
     return e ? atoi(e) : 0;
   }();
-  // quads (4 columns) per context CTA: 64 when the row groups alone fill the GPU
-  // (c2), 160 otherwise (c4: 32 utterances x 4 groups)
-  const int cq = cq_env > 0 ? cq_env
-                            : ((int64_t)num_utts * ((cfg->beam + RB - 1) / RB) >= 2 * kNumSMs ? 64
-                                                                                          : 160);
+  // quads (4 columns) per context CTA: 160 (whole c2 rows; measured over the
+  // c2 decode 64 -> 160: -0.9 ms, and the c4 choice already)
+  const int cq = cq_env > 0 ? cq_env : 160;
   const int csplit = (quads + cq - 1) / cq;
   const int qpc = (quads + csplit - 1) / csplit;
   dim3 gc(num_utts, groups, csplit);
