@@ -135,8 +135,10 @@ def decode_fused(features, scorer, fusion, config: DecodeConfig, token_dict
     """decode_batch entry: host features -> staged device batch -> engine.
     The FusedDecoder (and its device session) is cached on the scorer, so
     repeated calls with the same batch shape reuse buffers and CUDA graphs."""
-    Xh, T = scorer.encoder.stage([np.asarray(f.data, np.float32) for f in features], pin=True)
-    X = Xh.to(scorer.device, non_blocking=True)
+    # staging and upload pipelined in utterance chunks (copy of chunk i while
+    # the host threads stack chunk i+1)
+    X, T = scorer.encoder.stage([np.asarray(f.data, np.float32) for f in features], pin=True,
+                                to_device=True)
     done = torch.cuda.Event()
     done.record()
     key = (id(fusion), tuple(sorted(vars(config).items())), id(token_dict))

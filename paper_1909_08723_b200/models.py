@@ -152,8 +152,13 @@ class Encoder:
         self.streams = None
         self._pinned = None
 
-    def stage(self, feats: Sequence[np.ndarray], pin: bool = False):
-        """Host-side frame stacking into one [B*TM, Din_pad] array (+ lengths)."""
+    def stage(self, feats: Sequence[np.ndarray], pin: bool = False, to_device: bool = False,
+              chunks: int = 4):
+        """Host-side frame stacking into one [B*TM, Din_pad] array (+ lengths).
+        to_device: also upload it, chunk by chunk (utterance blocks), each chunk's
+        host->device copy running while the host threads stack the next one; the
+        device tensor is returned (the pinned buffer must not be restaged before
+        the stream has consumed it)."""
         d = self.w.d
         B = len(feats)
         T = [int(x.shape[0]) // d.subsample for x in feats]
@@ -174,22 +179,35 @@ class Encoder:
         else:
             x = torch.zeros(shape, dtype=torch.float32)
         xn = x.numpy()
-        if _pad(Din) == Din:
-            # contiguous per-utterance copies on the C++ thread pool
-            srcs, keep = [], []
-            for f in feats:
-                a = np.ascontiguousarray(f, np.float32)
-                keep.append(a)
-                srcs.append(a.ctypes.data)
-            row = Din * 4
-            dsts = [xn.ctypes.data + u * TM * row for u in range(B)]
-            nbytes = np.asarray([T[u] * row for u in range(B)], np.int64)
-            n = len(srcs)
-            _lib.call("fb_host_copy_batch", n, (C.c_void_p * n)(*srcs), (C.c_void_p * n)(*dsts),
-                      nbytes.ctypes.data, 16)
-        else:
-            for u, f in enumerate(feats):
-                xn[u, :T[u], :Din] = np.asarray(f, np.float32)[:T[u] * d.subsample].reshape(T[u], Din)
+        xd = (torch.empty(shape, dtype=torch.float32, device=self.device) if to_device
+              else None)
+        nchunk = max(1, min(chunks if to_device else 1, B))
+        bounds = [B * i // nchunk for i in range(nchunk + 1)]
+        keep = []
+        for c in range(nchunk):
+            u0, u1 = bounds[c], bounds[c + 1]
+            if _pad(Din) == Din:
+                # contiguous per-utterance copies on the C++ thread pool
+                srcs = []
+                for f in feats[u0:u1]:
+                    a = np.ascontiguousarray(f, np.float32)
+                    keep.append(a)
+                    srcs.append(a.ctypes.data)
+                row = Din * 4
+                dsts = [xn.ctypes.data + u * TM * row for u in range(u0, u1)]
+                nbytes = np.asarray([T[u] * row for u in range(u0, u1)], np.int64)
+                n = len(srcs)
+                _lib.call("fb_host_copy_batch", n, (C.c_void_p * n)(*srcs),
+                          (C.c_void_p * n)(*dsts), nbytes.ctypes.data, 16)
+            else:
+                for u in range(u0, u1):
+                    f = feats[u]
+                    xn[u, :T[u], :Din] = np.asarray(f, np.float32)[:T[u] * d.subsample].reshape(
+                        T[u], Din)
+            if xd is not None:
+                xd[u0:u1].copy_(x[u0:u1], non_blocking=True)
+        if xd is not None:
+            return xd.reshape(B * TM, -1), T
         return x.reshape(B * TM, -1), T
 
     def __call__(self, feats, lengths: Optional[Sequence[int]] = None, out=None):
