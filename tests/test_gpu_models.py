@@ -164,6 +164,33 @@ def test_spec_pruning_is_exact():
             assert a.tokens == b.tokens and a.score == b.score and a.steps == b.steps
 
 
+def test_operand_pipeline_and_fused_epilogues_are_exact(monkeypatch):
+    """Per-GEMM A operands written by the LSTM epilogues (+ side-stream packs),
+    exp(2q) and log-softmax fused into GEMM epilogues: bit-identical decodes to
+    the plain pack-per-GEMM path with separate kernels (same split and
+    arithmetic, only the plumbing differs)."""
+    fb, synth, d, words, ad, ld, W = small_setup()
+    from paper_1909_08723_b200 import engine as E, models as M
+    from paper_1909_08723_b200.models import AttnLstmScorer, LstmWordLM
+    utts = synth.synth_fbank(8, seed=31, frames=(40, 120))
+    trie = fb.build_trie(words, d)
+    sc = AttnLstmScorer(W, ad, d.eos_id)
+    fus = fb.LookaheadFusion(trie, LstmWordLM(W, ld), d)
+    cfg = fb.DecodeConfig(beam_size=6, lm_weight=0.6, eos_gamma=1.3)
+    X, T = sc.encoder.stage([x for _, x in utts])
+    X = X.to(sc.device)
+    ids = [u for u, _ in utts]
+    outs = []
+    for fast in (False, True):
+        monkeypatch.setattr(E, "AM_PIPELINE", fast)
+        monkeypatch.setattr(M, "FUSE_EPI", fast)
+        dec = E.FusedDecoder(sc, fus, cfg, d)
+        outs.append(dec.run(X, T, ids))
+    for a, b in zip(*outs):
+        assert a.tokens == b.tokens and a.score == b.score and a.steps == b.steps
+        np.testing.assert_array_equal(a.attn_accum, b.attn_accum)
+
+
 @pytest.mark.parametrize("name", ["c1", "c3"])
 def test_baseline_small_configs_match_oracle(name):
     """BASELINE.json configs[0] (c1: small BiLSTM + 1-layer attn-LSTM, beam 5, no
