@@ -236,3 +236,25 @@ def test_c2_full_size_matches_oracle():
                           fb.LookaheadFusion(trie, LstmWordLM(W, wl.lm), d), cfg, d)
     _, want = bench.cpu_decode(wl, d, W, words, sample, len(sample), os.cpu_count() or 4)
     _compare(got, want, "c2")
+
+
+def test_c5_size_matches_oracle():
+    """BASELINE.json c5 (Switchboard-shaped character decoder, 30k-word
+    look-ahead 3x900 LSTM LM, beam 35) on its two shortest utterances of a
+    16-utterance draw: identical tokens (or a near-tie), scores within 1e-4."""
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if root not in sys.path:
+        sys.path.insert(0, root)
+    import bench
+    fb = __import__("paper_1909_08723_b200")
+    from paper_1909_08723_b200.models import AttnLstmScorer, LstmWordLM
+    wl, d, W, words, trie, utts = bench.build_inputs("c5", 0, 16)
+    sample = sorted(utts, key=lambda ux: ux[1].shape[0])[:2]
+    cfg = bench.decode_config(wl)
+    got = fb.decode_batch([fb.FeatureMatrix(u, x) for u, x in sample],
+                          AttnLstmScorer(W, wl.asr, d.eos_id),
+                          fb.LookaheadFusion(trie, LstmWordLM(W, wl.lm), d), cfg, d)
+    _, want = bench.cpu_decode(wl, d, W, words, sample, len(sample), os.cpu_count() or 4)
+    _compare(got, want, "c5")
