@@ -257,9 +257,12 @@ def workload_config(wl):
                 "utts_per_gpu": wl.n_utts, "frames": list(wl.frames), "beam": wl.beam,
                 "vocab": a.vocab, "lm_weight": wl.lm_weight, "batch": wl.batch_size,
                 "length_sorted": True}
-    return {"workload": f"{wl.name}: WSJ-shaped 4x BiLSTM-320 encoder + 3x LSTM-320 attention "
-                        f"decoder (52 tokens), beam {wl.beam}, look-ahead fusion with a "
-                        f"{wl.lm.words if wl.lm else 0}-word 3x1200 LSTM LM, "
+    a, lm = wl.asr, wl.lm
+    lm_desc = (f"look-ahead fusion with a {lm.words}-word {lm.layers}x{lm.hidden} LSTM LM"
+               if lm is not None else "no LM")
+    return {"workload": f"{wl.name}: {a.enc_layers}x BiLSTM-{a.enc_hidden} encoder + "
+                        f"{a.dec_layers}x LSTM-{a.dec_hidden} attention decoder ({a.vocab} "
+                        f"tokens), beam {wl.beam}, {lm_desc}, "
                         f"{wl.n_utts} utts/GPU of {wl.frames[0]}-{wl.frames[1]} frames",
             "utts_per_gpu": wl.n_utts, "frames": list(wl.frames), "beam": wl.beam,
             "lm_words": wl.lm.words if wl.lm else 0, "lm_weight": wl.lm_weight,

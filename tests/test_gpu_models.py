@@ -241,7 +241,10 @@ def test_c2_full_size_matches_oracle():
 def test_c5_size_matches_oracle():
     """BASELINE.json c5 (Switchboard-shaped character decoder, 30k-word
     look-ahead 3x900 LSTM LM, beam 35) on its two shortest utterances of a
-    16-utterance draw: identical tokens (or a near-tie), scores within 1e-4."""
+    16-utterance draw: identical tokens (or a near-tie), scores within 1e-4.
+    The random model's <eos> bias is lowered so the decodes run to their
+    length cap (full beam, word boundaries, LM events) instead of ending at
+    step 1."""
     import os
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -250,11 +253,16 @@ def test_c5_size_matches_oracle():
     import bench
     fb = __import__("paper_1909_08723_b200")
     from paper_1909_08723_b200.models import AttnLstmScorer, LstmWordLM
-    wl, d, W, words, trie, utts = bench.build_inputs("c5", 0, 16)
+    wl, d, W, words, trie, utts = bench.build_inputs("c5", 0, 16,
+                                                     overrides=("asr.eos_bias=-1.5",
+                                                                "lm.emb_scale=0.2",
+                                                                "lm.eos_bias=5",
+                                                                "lm.w_scale=2"))
     sample = sorted(utts, key=lambda ux: ux[1].shape[0])[:2]
     cfg = bench.decode_config(wl)
     got = fb.decode_batch([fb.FeatureMatrix(u, x) for u, x in sample],
                           AttnLstmScorer(W, wl.asr, d.eos_id),
                           fb.LookaheadFusion(trie, LstmWordLM(W, wl.lm), d), cfg, d)
     _, want = bench.cpu_decode(wl, d, W, words, sample, len(sample), os.cpu_count() or 4)
+    assert min(r.steps for r in got) > 5
     _compare(got, want, "c5")
