@@ -87,7 +87,8 @@ _SIGS = {
     "fb_gather_rows": (C.c_int, [i32, vp, vp, vp, i64, vp]),
     "fb_gemm": (C.c_int, [C.POINTER(FbGemm), vp]),
     "fb_gemm_tc": (C.c_int, [C.POINTER(FbGemm), i32, i64, vp]),
-    "fb_stats_to_g": (C.c_int, [i32, vp, vp, i64, vp, i32, vp, i32, vp, vp, i64, vp, vp, vp]),
+    "fb_stats_to_g": (C.c_int, [i32, vp, vp, i64, vp, i32, vp, i32, vp, vp, i64, vp, vp, vp, vp,
+                                vp]),
     "fb_lstm_recurrence": (C.c_int, [i32, i32, i32, vp, i32, vp, i64, i64, vp, i64, i64, vp,
                                       vp, vp]),
     "fb_pack_rows": (C.c_int, [C.POINTER(FbPack), i32, vp, vp, vp, vp, vp, vp, i64, vp]),

@@ -378,7 +378,8 @@ __global__ void __launch_bounds__(256)
 row_norm_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __restrict__ logits,
                 int64_t ld, const float4* __restrict__ stats, int ntiles,
                 const int32_t* __restrict__ src_rows, int vw, const int32_t* __restrict__ slots,
-                double* __restrict__ eos_out, double* __restrict__ norm_out) {
+                double* __restrict__ eos_out, double* __restrict__ norm_out,
+                double* __restrict__ stat_out) {
   const int m = row_count(m_max, m_dev);
   const int lane = threadIdx.x & 31;
   for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < m; i += gridDim.x * 8) {
@@ -404,6 +405,10 @@ row_norm_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __res
     if (lane == 0) {
       if (eos_out) eos_out[slots ? slots[i] : i] = (double)logits[srow * ld + vw] - lse;
       if (norm_out) norm_out[i] = (double)mw;          // M_w per row (segment passes)
+      if (stat_out) {
+        stat_out[2 * i] = (double)mw;
+        stat_out[2 * i + 1] = lse;
+      }
     }
   }
 }
@@ -413,12 +418,16 @@ row_norm_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __res
 __global__ void __launch_bounds__(kScanThreads)
 seg_sum_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __restrict__ logits,
                int64_t ld, const int32_t* __restrict__ src_rows, int vw,
-               double* __restrict__ seg_ws, int nseg, const double* __restrict__ norm) {
+               double* __restrict__ seg_ws, int nseg, const double* __restrict__ norm,
+               const double* __restrict__ stat_in, const int32_t* __restrict__ slots,
+               double* __restrict__ eos_out) {
   __shared__ double red_d[32];
   const int m = row_count(m_max, m_dev);
   for (int i = blockIdx.x; i < m; i += gridDim.x) {
     const int64_t srow = src_rows ? src_rows[i] : i;
-    const float mw = (float)norm[i];
+    const float mw = (float)(stat_in ? stat_in[2 * srow] : norm[i]);
+    if (stat_in && eos_out && blockIdx.y == 0 && threadIdx.x == 0)   // == row_norm_kernel
+      eos_out[slots ? slots[i] : i] = (double)logits[srow * ld + vw] - stat_in[2 * srow + 1];
     const float* lg = logits + srow * ld;
     const int c0 = blockIdx.y * kSegCols, c1 = min(vw, c0 + kSegCols);
     double s = 0.0;
@@ -440,12 +449,13 @@ __global__ void __launch_bounds__(kScanThreads)
 seg_scan_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __restrict__ logits,
                 int64_t ld, const int32_t* __restrict__ src_rows, int vw,
                 const int32_t* __restrict__ slots, const double* __restrict__ seg_ws, int nseg,
-                const double* __restrict__ norm, double* __restrict__ g_pool, int64_t g_stride) {
+                const double* __restrict__ norm, double* __restrict__ g_pool, int64_t g_stride,
+                const double* __restrict__ stat_in) {
   __shared__ double wsum[32];
   const int m = row_count(m_max, m_dev);
   for (int i = blockIdx.x; i < m; i += gridDim.x) {
   const int64_t srow = src_rows ? src_rows[i] : i;
-  const float mw = (float)norm[i];
+  const float mw = (float)(stat_in ? stat_in[2 * srow] : norm[i]);
   const double* sw = seg_ws + (int64_t)i * nseg;
   double off = 0.0, tot = 0.0;
   for (int k = 0; k < nseg; ++k) {          // same order in every CTA: deterministic
@@ -602,9 +612,10 @@ extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* l
                              int64_t l_stride, const float* row_stats, int32_t n_out,
                              const int32_t* src_rows, int32_t vw, const int32_t* slots,
                              double* g_pool, int64_t g_stride, double* eos_out, double* seg_ws,
-                             void* stream) {
+                             double* stat_out, const double* stat_in, void* stream) {
   FB_CHECK_ARG(logits && row_stats && vw > 0 && n_out > vw, "bad stats_to_g arguments");
   FB_CHECK_ARG(!g_pool || (seg_ws && g_stride >= vw), "g rows need seg_ws and g_stride");
+  FB_CHECK_ARG(!stat_in || g_pool, "stat_in only feeds the g-row passes");
   if (m_max <= 0) return FB_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const int ntiles = (n_out + 63) / 64;       // GEMM epilogue statistics granule
@@ -612,19 +623,24 @@ extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* l
   const float4* st = reinterpret_cast<const float4*>(row_stats);
   // seg_ws layout: [m_max][nseg] segment sums, then [m_max] M_w
   double* norm = g_pool ? seg_ws + (int64_t)m_max * nseg : nullptr;
-  row_norm_kernel<<<std::min((m_max + 7) / 8, kNumSMs * 8), 256, 0, s>>>(
-      m_max, m_dev, logits, l_stride, st, ntiles, src_rows, vw, slots, eos_out, norm);
-  count_launch();
-  int rc = check_launch("row_norm");
+  int rc = 0;
+  if (!stat_in) {
+    row_norm_kernel<<<std::min((m_max + 7) / 8, kNumSMs * 8), 256, 0, s>>>(
+        m_max, m_dev, logits, l_stride, st, ntiles, src_rows, vw, slots, eos_out, norm, stat_out);
+    count_launch();
+    rc = check_launch("row_norm");
+  }
   if (rc || !g_pool) return rc;
   const int gx = std::min(m_max, 256);
   seg_sum_kernel<<<dim3(gx, nseg), kScanThreads, 0, s>>>(m_max, m_dev, logits, l_stride, src_rows,
-                                                         vw, seg_ws, nseg, norm);
+                                                         vw, seg_ws, nseg, norm, stat_in, slots,
+                                                         eos_out);
   count_launch();
   rc = check_launch("seg_sum");
   if (rc) return rc;
   seg_scan_kernel<<<dim3(gx, nseg), kScanThreads, 0, s>>>(
-      m_max, m_dev, logits, l_stride, src_rows, vw, slots, seg_ws, nseg, norm, g_pool, g_stride);
+      m_max, m_dev, logits, l_stride, src_rows, vw, slots, seg_ws, nseg, norm, g_pool, g_stride,
+      stat_in);
   count_launch();
   return check_launch("seg_scan");
 }

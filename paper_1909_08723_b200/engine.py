@@ -20,6 +20,7 @@ State never leaves the device; rows index per-slot buffers through ``parent``
 from __future__ import annotations
 
 import ctypes as C
+import os
 import math
 from typing import List, Optional, Sequence
 
@@ -34,6 +35,12 @@ from .models import (AM_PIPELINE, LM_SPLITK, AmState, SubLmState, lm_step, split
                      subword_step)
 
 P = _lib.ptr
+
+
+# dev knob: word-boundary g rows reuse the speculative events' statistics
+# instead of a second statistics pass (measured 2 ms slower over the c2 decode:
+# the extra pass on the side stream shifts the g-row kernels to a better overlap)
+_STAT_REUSE = os.environ.get("FB_STAT_REUSE", "0") == "1"
 
 
 class _LmPool:
@@ -72,6 +79,8 @@ class _LmPool:
         # stream-K workspace of the LM LSTM GEMMs (spec and late events never
         # overlap: the side stream joins before the speculative events)
         self.splitk = K.SplitK(device) if LM_SPLITK else None
+        # {M_w, lse} per speculative event: reused by the word-boundary g rows
+        self.ev_stat = torch.zeros((N, 2), dtype=torch.float64, device=device)
         # per-GEMM A operands (the output one's K padding stays zero)
         self.abufs = ([split_scratch(N, lay.k_pad, device) for lay in lw.layers] +
                       [torch.zeros((3, N, lw.k_out), dtype=torch.bfloat16, device=device)]
@@ -353,7 +362,8 @@ class FusedDecoder:
                         splitk=lm.splitk, abufs=lm.abufs, pack_stream=S.pack_stream)
             with tm("lm_eos"):
                 K.stats_to_g(lm.ev_logits, lm.ev_stats, Vw, lw.v_out, m=N, m_dev=lm.ev_count,
-                             slots=lm.ev_row, eos_out=lm.ext_eos)
+                             slots=lm.ev_row, eos_out=lm.ext_eos,
+                             stat_out=lm.ev_stat if _STAT_REUSE else None)
                 _lib.call("fb_eos_fixup", N, P(lm.ev_count), P(lm.ev_row), P(lm.ext_eos),
                           P(fus_buf), V, fusion.eos_id, stream)
             if counts is not None:
@@ -394,7 +404,8 @@ class FusedDecoder:
                             dst_idx=lm.bnd_slot)
                 K.stats_to_g(lm.ev_logits, lm.ev_stats, Vw, lw.v_out, m=N, m_dev=lm.bnd_count,
                              src_rows=lm.bnd_src, slots=lm.bnd_slot, g_pool=lm.g,
-                             eos_out=lm.eos, seg_ws=lm.seg_ws)
+                             eos_out=lm.eos, seg_ws=lm.seg_ws,
+                             stat_in=lm.ev_stat if _STAT_REUSE else None)
                 K.copy_rows(lm.ev_state[N:], lm.state, m=N, m_dev=lm.unk_count,
                             dst_idx=lm.late_dst)
                 K.stats_to_g(lm.ev_logits[N:], lm.ev_stats[N:], Vw, lw.v_out, m=N,

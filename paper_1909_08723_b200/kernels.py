@@ -159,7 +159,9 @@ def logits_to_g(logits: torch.Tensor, vw: int, v_out: int, *, m: int, m_dev=None
 
 def stats_to_g(logits: torch.Tensor, stats: torch.Tensor, vw: int, v_out: int, *, m: int,
                m_dev=None, src_rows=None, slots=None, g_pool=None, eos_out=None,
-               seg_ws=None) -> None:
+               seg_ws=None, stat_out=None, stat_in=None) -> None:
+    """stat_out: per-row {M_w, lse} pairs to reuse; stat_in: reuse them (by
+    source row) instead of the statistics pass."""
     _lib.call("fb_stats_to_g", m, P(m_dev), P(logits), logits.stride(0), P(stats), v_out,
               P(src_rows), vw, P(slots), P(g_pool), _ld(g_pool), P(eos_out), P(seg_ws),
-              _lib.stream_ptr())
+              P(stat_out), P(stat_in), _lib.stream_ptr())

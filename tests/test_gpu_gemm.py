@@ -120,6 +120,21 @@ def test_row_stats_feed_g_rows_and_eos():
     p = torch.diff(g, dim=1, prepend=torch.zeros(m, 1, dtype=torch.float64, device=dev))
     p_ref = torch.diff(g_ref, dim=1, prepend=torch.zeros(m, 1, dtype=torch.float64, device=dev))
     assert (p - p_ref).abs().max().item() < 1e-15
+    # statistics from an eos-only pass reused by a gathered g-row pass: bit-identical
+    stat = torch.empty(m, 2, dtype=torch.float64, device=dev)
+    e_ev = torch.empty_like(e_ref)
+    K.stats_to_g(logits, stats, vw, n, m=m, m_dev=cnt, eos_out=e_ev, stat_out=stat)
+    assert torch.equal(e_ev, e)
+    src = torch.randperm(m, device=dev)[:20].to(torch.int32)
+    slots = torch.arange(20, dtype=torch.int32, device=dev).flip(0).contiguous()
+    c20 = torch.tensor([20], dtype=torch.int32, device=dev)
+    g2, e2 = torch.zeros(20, vw, dtype=torch.float64, device=dev), torch.zeros(20, dtype=torch.float64, device=dev)
+    g3, e3 = torch.zeros_like(g2), torch.zeros_like(e2)
+    K.stats_to_g(logits, stats, vw, n, m=20, m_dev=c20, src_rows=src, slots=slots, g_pool=g2,
+                 eos_out=e2, seg_ws=seg)
+    K.stats_to_g(logits, stats, vw, n, m=20, m_dev=c20, src_rows=src, slots=slots, g_pool=g3,
+                 eos_out=e3, seg_ws=seg, stat_in=stat)
+    assert torch.equal(g2, g3) and torch.equal(e2, e3)
 
 
 @pytest.mark.parametrize("m,n,k,m_dev", [(160, 4800, 2432, 150), (64, 1280, 1024, 64),
