@@ -262,7 +262,8 @@ class FusedDecoder:
         self.prune_spec = True      # exact pruning of speculative <eos> LM events
         self.select_flags = 0       # tests: bit 0 two-stage, bit 1 radix top-K (any size)
         self.use_graphs = True      # one CUDA graph per step parity, replayed
-        self.poll_every = 8         # host polls the live-row count every k steps
+        # host polls the live-row count every k steps (dev override FB_POLL)
+        self.poll_every = int(os.environ.get("FB_POLL", "8"))
         self._sess: Optional[_Session] = None
 
     def _session(self, B: int, TM: int, MT: int) -> _Session:
