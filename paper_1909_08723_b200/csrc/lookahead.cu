@@ -625,13 +625,21 @@ extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* l
   double* norm = g_pool ? seg_ws + (int64_t)m_max * nseg : nullptr;
   int rc = 0;
   if (!stat_in) {
-    row_norm_kernel<<<std::min((m_max + 7) / 8, kNumSMs * 8), 256, 0, s>>>(
+#ifndef FB_ROWS_GRID
+#define FB_ROWS_GRID (kNumSMs * 8)
+#endif
+    row_norm_kernel<<<std::min((m_max + 7) / 8, FB_ROWS_GRID), 256, 0, s>>>(
         m_max, m_dev, logits, l_stride, st, ntiles, src_rows, vw, slots, eos_out, norm, stat_out);
     count_launch();
     rc = check_launch("row_norm");
   }
   if (rc || !g_pool) return rc;
-  const int gx = std::min(m_max, 256);
+#ifndef FB_SEG_ROWS_GRID
+#define FB_SEG_ROWS_GRID 256
+#endif
+  // row CTAs per segment column (rows are grid-strided): few enough that the
+  // usually-empty late-event launch is cheap
+  const int gx = std::min(m_max, FB_SEG_ROWS_GRID);
   seg_sum_kernel<<<dim3(gx, nseg), kScanThreads, 0, s>>>(m_max, m_dev, logits, l_stride, src_rows,
                                                          vw, seg_ws, nseg, norm, stat_in, slots,
                                                          eos_out);
