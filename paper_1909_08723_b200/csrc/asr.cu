@@ -723,7 +723,7 @@ extern "C" int fb_pack_rows(const fb_pack_t* p, int32_t m_max, const int32_t* m_
   FB_CHECK_ARG(w <= p->k_pad && p->k_pad <= ld_out, "pack width exceeds k_pad / ld_out");
   if (m_max <= 0) return FB_OK;
 #ifndef FB_PACK_GRID
-#define FB_PACK_GRID (kNumSMs * 8)
+#define FB_PACK_GRID (kNumSMs * 2)
 #endif
   pack_rows_kernel<<<std::min((m_max + 7) / 8, FB_PACK_GRID), 256, 0, (cudaStream_t)stream>>>(
       *p, m_max, m_dev, rows, parent, tokens, ranks, out, ld_out);

@@ -626,7 +626,7 @@ extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* l
   int rc = 0;
   if (!stat_in) {
 #ifndef FB_ROWS_GRID
-#define FB_ROWS_GRID (kNumSMs * 8)
+#define FB_ROWS_GRID (kNumSMs * 2)
 #endif
     row_norm_kernel<<<std::min((m_max + 7) / 8, FB_ROWS_GRID), 256, 0, s>>>(
         m_max, m_dev, logits, l_stride, st, ntiles, src_rows, vw, slots, eos_out, norm, stat_out);
@@ -635,7 +635,7 @@ extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* l
   }
   if (rc || !g_pool) return rc;
 #ifndef FB_SEG_ROWS_GRID
-#define FB_SEG_ROWS_GRID 256
+#define FB_SEG_ROWS_GRID 64
 #endif
   // row CTAs per segment column (rows are grid-strided): few enough that the
   // usually-empty late-event launch is cheap
