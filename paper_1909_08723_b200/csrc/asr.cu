@@ -898,7 +898,10 @@ extern "C" int fb_copy_rows(int32_t n_max, const int32_t* n_dev, const int32_t* 
                             void* stream) {
   FB_CHECK_ARG(src && dst && row_bytes > 0, "bad copy arguments");
   if (n_max <= 0) return FB_OK;
-  copy_rows_kernel<<<std::min(n_max, kNumSMs * 8), 256, 0, (cudaStream_t)stream>>>(
+#ifndef FB_COPY_GRID
+#define FB_COPY_GRID (kNumSMs * 8)
+#endif
+  copy_rows_kernel<<<std::min(n_max, FB_COPY_GRID), 256, 0, (cudaStream_t)stream>>>(
       n_max, n_dev, src_idx, dst_idx, (const char*)src, (char*)dst, row_bytes);
   count_launch();
   return check_launch("copy_rows");
