@@ -598,9 +598,10 @@ boundary_plan_kernel(int n_max, const int32_t* __restrict__ n_dev, const int32_t
                      int32_t* __restrict__ late_tok, int32_t* __restrict__ late_row,
                      int32_t* __restrict__ late_dst, int32_t* __restrict__ late_count,
                      int late_sink_row) {
+  // each thread owns a contiguous run of slots / rows, so one block scan per
+  // pass (instead of one per 1024 elements) assigns the ordered positions
   __shared__ int wsum[32];
   __shared__ int wsum2[32];
-  __shared__ int carry, carry2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   int32_t* freel = mark + num_slots;   // second half of the scratch: free list
   for (int s = tid; s < num_slots; s += blockDim.x) mark[s] = 0;
@@ -608,51 +609,13 @@ boundary_plan_kernel(int n_max, const int32_t* __restrict__ n_dev, const int32_t
   const int nc = *cur_count;
   for (int i = tid; i < nc; i += blockDim.x) mark[hist_cur[cur_rows[i]]] = 1;
   __syncthreads();
-  if (tid == 0) carry = 0;
-  __syncthreads();
-  for (int b0 = 0; b0 < num_slots; b0 += blockDim.x) {
-    const int s = b0 + tid;
-    const int f = (s < num_slots && mark[s] == 0) ? 1 : 0;
-    int x = f;
+  // exclusive block scan of (a, b) per thread -> (a_before, b_before), totals
+  auto scan2 = [&](int a, int b, int& ea, int& eb, int& ta, int& tb) {
+    int x = a, y = b;
     for (int off = 1; off < 32; off <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, off);
-      if (lane >= off) x += y;
-    }
-    if (lane == 31) wsum[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      int w = lane < nw ? wsum[lane] : 0;
-      for (int off = 1; off < 32; off <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, w, off);
-        if (lane >= off) w += y;
-      }
-      wsum[lane] = w;
-    }
-    __syncthreads();
-    const int pos = carry + (warp ? wsum[warp - 1] : 0) + x - f;
-    if (f) freel[pos] = s;              // k-th free slot, ascending
-    __syncthreads();
-    if (tid == 0) carry += wsum[nw - 1];
-    __syncthreads();
-  }
-  const int n = row_count(n_max, n_dev);
-  if (tid == 0) { carry = 0; carry2 = 0; }
-  __syncthreads();
-  for (int b0 = 0; b0 < n; b0 += blockDim.x) {
-    const int i = b0 + tid;
-    int is_b = 0, is_late = 0, r = -1, br = -2;
-    if (i < n) {
-      r = rows[i];
-      br = brank[r];
-      is_b = br >= -1;
-      is_late = is_b && (br == -1 || row_ev[parent[r]] < 0);
-    }
-    // prefix counts: all boundaries (slot order), spec-sourced, late
-    int x = is_b, y = is_late;
-    for (int off = 1; off < 32; off <<= 1) {
-      const int a = __shfl_up_sync(0xffffffffu, x, off);
-      const int b = __shfl_up_sync(0xffffffffu, y, off);
-      if (lane >= off) { x += a; y += b; }
+      const int u = __shfl_up_sync(0xffffffffu, x, off);
+      const int v = __shfl_up_sync(0xffffffffu, y, off);
+      if (lane >= off) { x += u; y += v; }
     }
     if (lane == 31) { wsum[warp] = x; wsum2[warp] = y; }
     __syncthreads();
@@ -660,36 +623,67 @@ boundary_plan_kernel(int n_max, const int32_t* __restrict__ n_dev, const int32_t
       int w = lane < nw ? wsum[lane] : 0;
       int w2 = lane < nw ? wsum2[lane] : 0;
       for (int off = 1; off < 32; off <<= 1) {
-        const int a = __shfl_up_sync(0xffffffffu, w, off);
-        const int b = __shfl_up_sync(0xffffffffu, w2, off);
-        if (lane >= off) { w += a; w2 += b; }
+        const int u = __shfl_up_sync(0xffffffffu, w, off);
+        const int v = __shfl_up_sync(0xffffffffu, w2, off);
+        if (lane >= off) { w += u; w2 += v; }
       }
       wsum[lane] = w;
       wsum2[lane] = w2;
     }
     __syncthreads();
-    if (is_b) {
-      const int k = carry + (warp ? wsum[warp - 1] : 0) + x - 1;      // k-th boundary
-      const int kl = carry2 + (warp ? wsum2[warp - 1] : 0) + y - 1;   // late index if late
-      const int slot = freel[k];
-      hist_next[r] = slot;
-      const int p = parent[r];
-      if (is_late) {
-        late_slot[kl] = hist_cur[p];
-        late_tok[kl] = br;
-        late_row[kl] = late_sink_row;
-        late_dst[kl] = slot;
-      } else {
-        const int ks = k - (kl + 1);                 // spec index = k - #late rows before it
-        bnd_slot[ks] = slot;
-        bnd_src[ks] = row_ev[p];
-      }
-    }
+    ea = (warp ? wsum[warp - 1] : 0) + x - a;
+    eb = (warp ? wsum2[warp - 1] : 0) + y - b;
+    ta = wsum[nw - 1];
+    tb = wsum2[nw - 1];
     __syncthreads();
-    if (tid == 0) { carry += wsum[nw - 1]; carry2 += wsum2[nw - 1]; }
-    __syncthreads();
+  };
+  {
+    const int per = (num_slots + blockDim.x - 1) / blockDim.x;
+    const int s0 = tid * per, s1 = min(num_slots, s0 + per);
+    int f = 0;
+    for (int s = s0; s < s1; ++s) f += mark[s] == 0;
+    int pos, dummy, t1, t2;
+    scan2(f, 0, pos, dummy, t1, t2);
+    for (int s = s0; s < s1; ++s)
+      if (mark[s] == 0) freel[pos++] = s;            // k-th free slot, ascending
   }
-  if (tid == 0) { *bnd_count = carry - carry2; *late_count = carry2; }
+  __syncthreads();
+  const int n = row_count(n_max, n_dev);
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int i0 = tid * per, i1 = min(n, i0 + per);
+  int nb = 0, nl = 0;
+  for (int i = i0; i < i1; ++i) {
+    const int r = rows[i];
+    const int br = brank[r];
+    if (br >= -1) {
+      ++nb;
+      nl += (br == -1 || row_ev[parent[r]] < 0);
+    }
+  }
+  int k, kl, tot_b, tot_l;
+  scan2(nb, nl, k, kl, tot_b, tot_l);
+  for (int i = i0; i < i1; ++i) {
+    const int r = rows[i];
+    const int br = brank[r];
+    if (br < -1) continue;
+    const int p = parent[r];
+    const bool late = br == -1 || row_ev[p] < 0;
+    const int slot = freel[k];                     // k-th boundary in row order
+    hist_next[r] = slot;
+    if (late) {
+      late_slot[kl] = hist_cur[p];
+      late_tok[kl] = br;
+      late_row[kl] = late_sink_row;
+      late_dst[kl] = slot;
+      ++kl;
+    } else {
+      const int ks = k - kl;                       // spec index = k - #late rows before it
+      bnd_slot[ks] = slot;
+      bnd_src[ks] = row_ev[p];
+    }
+    ++k;
+  }
+  if (tid == 0) { *bnd_count = tot_b - tot_l; *late_count = tot_l; }
 }
 
 __global__ void copy_rows_kernel(int n_max, const int32_t* __restrict__ n_dev,
