@@ -315,6 +315,12 @@ int fb_log_softmax_rows(int32_t m_max, const int32_t* m_dev, const int32_t* rows
  * energy_ws: scratch [num_utts*beam, t_max] fp32; holds the attention
  * weights a[r, t] on return.  sync_ws: num_utts*ceil(beam/2) int32, zero on the
  * first call (the kernels leave it zeroed). */
+/* Tiling of the following fb_attention_step launches (0 = default): frame
+ * warps per energy CTA (2/4/8), rows per energy CTA (even, <= 16), encoder
+ * column quads per context CTA.  Finer tiles pay off when few utterances are
+ * live (the lock-step tail of a batch). */
+int fb_set_attention_tiling(int32_t frames_warps, int32_t rows, int32_t quads);
+
 int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts, const int32_t* active,
                       const int32_t* n_live, const int32_t* t_enc, const float* keys,
                       const float* enc, int32_t att_dim, int32_t ctx_dim, const float* v,

@@ -94,6 +94,7 @@ _SIGS = {
     "fb_pack_rows": (C.c_int, [C.POINTER(FbPack), i32, vp, vp, vp, vp, vp, vp, i64, vp]),
     "fb_log_softmax_rows": (C.c_int, [i32, vp, vp, vp, i64, i32, vp, i64, vp]),
     "fb_row_logsumexp": (C.c_int, [i32, vp, vp, vp, i64, i32, i32, vp, vp]),
+    "fb_set_attention_tiling": (C.c_int, [i32, i32, i32]),
     "fb_attention_step": (C.c_int, [C.POINTER(FbSearchCfg), i32, vp, vp, vp, vp, vp, i32, i32,
                                     vp, vp, i64, vp, vp, vp, vp, vp, i64, vp, i64, vp, vp, i32,
                                     vp]),

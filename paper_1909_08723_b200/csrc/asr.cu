@@ -747,6 +747,21 @@ extern "C" int fb_row_logsumexp(int32_t m_max, const int32_t* m_dev, const int32
   return check_launch("row_logsumexp");
 }
 
+// Launch tiling of fb_attention_step (0 = default), read when a launch is
+// issued -- a captured graph keeps the tiling it was captured with.
+static int g_att_ew = 0, g_att_re = 0, g_att_cq = 0;
+
+extern "C" int fb_set_attention_tiling(int32_t frames_warps, int32_t rows, int32_t quads) {
+  FB_CHECK_ARG(frames_warps == 0 || frames_warps == 2 || frames_warps == 4 || frames_warps == 8,
+               "frame warps must be 0, 2, 4 or 8");
+  FB_CHECK_ARG(rows == 0 || (rows >= 2 && rows <= 16 && rows % 2 == 0), "rows must be 0 or even 2..16");
+  FB_CHECK_ARG(quads >= 0, "negative quads");
+  g_att_ew = frames_warps;
+  g_att_re = rows;
+  g_att_cq = quads;
+  return FB_OK;
+}
+
 extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
                                  const int32_t* active, const int32_t* n_live,
                                  const int32_t* t_enc, const float* keys, const float* enc,
@@ -768,7 +783,7 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
     const char* e = getenv("FB_ATT_RE");
     return e ? atoi(e) : 0;
   }();
-  const int RE = re_env > 0 ? re_env
+  const int RE = g_att_re > 0 ? g_att_re : re_env > 0 ? re_env
                             : (cfg->beam >= 16 ? 16 : (cfg->beam + 1) & ~1);   // rows per energy CTA
   const size_t sm_e = sizeof(float) * ((size_t)RE * att_dim + 2 * (size_t)att_dim);
   const int RB = cfg->beam <= 4 ? 4 : cfg->beam <= 8 ? 8 : cfg->beam <= 12 ? 12 : 16;
@@ -807,6 +822,7 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
   const int groups_e = (cfg->beam + RE - 1) / RE;
   int EW = 8;
   if (ew_env == 2 || ew_env == 4 || ew_env == 8) EW = ew_env;
+  if (g_att_ew > 0) EW = g_att_ew;
   dim3 ge(num_utts, (cfg->t_max + EW * 32 - 1) / (EW * 32), groups_e);
 #define FB_EN2(R, W)                                                                          \
   att_energy_kernel<R, W><<<ge, W * 32, sm_e, s>>>(*cfg, active, n_live, t_enc, keys, att_dim, \
@@ -839,7 +855,7 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
   }();
   // quads (4 columns) per context CTA: 160 (whole c2 rows; measured over the
   // c2 decode 64 -> 160: -0.9 ms, and the c4 choice already)
-  const int cq = cq_env > 0 ? cq_env : 160;
+  const int cq = g_att_cq > 0 ? g_att_cq : cq_env > 0 ? cq_env : 160;
   const int csplit = (quads + cq - 1) / cq;
   const int qpc = (quads + csplit - 1) / csplit;
   dim3 gc(num_utts, groups, csplit);

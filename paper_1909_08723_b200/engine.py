@@ -43,6 +43,12 @@ P = _lib.ptr
 _STAT_REUSE = os.environ.get("FB_STAT_REUSE", "0") == "1"
 
 
+# lock-step tail: below this many live rows the step graphs captured with fine
+# attention tiles replace the default ones (frame warps, rows, quads per CTA)
+_TAIL_ROWS = int(os.environ.get("FB_TAIL_ROWS", "1500"))
+_TAIL_TILING = tuple(int(x) for x in os.environ.get("FB_TAIL_TILING", "4,4,160").split(","))
+
+
 class _LmPool:
     """History slots (LM state + g row + eos) and per-step LM events."""
 
@@ -221,6 +227,7 @@ class _Session:
             self.lm = _LmPool(fusion.word_lm.weights, N, dev)
             self.fus_buf = torch.zeros((N + 1, V), dtype=torch.float64, device=dev)
         self.graphs = None
+        self.graphs_tail = None
         self.per_step_launches = 0.0
         self.side_stream = torch.cuda.Stream(device=dev)
 
@@ -452,15 +459,35 @@ class FusedDecoder:
                 S.per_step_launches = (lib.fb_launch_count() - c1) / 2.0
                 l0 += lib.fb_launch_count() - c0          # captures launch nothing
                 S.graphs = g
+                if _TAIL_ROWS > 0:
+                    c2 = lib.fb_launch_count()
+                    _lib.call("fb_set_attention_tiling", *_TAIL_TILING)
+                    try:
+                        gt = [torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()]
+                        for p_ in (0, 1):
+                            with torch.cuda.graph(gt[p_]):
+                                self._step_overlapped(S, p_, prev_tail=True)
+                    finally:
+                        _lib.call("fb_set_attention_tiling", 0, 0, 0)
+                    l0 += lib.fb_launch_count() - c2
+                    S.graphs_tail = gt
             first = True
+            live = S.N
             while True:
+                tail = _TAIL_ROWS > 0 and live < _TAIL_ROWS
                 for _ in range(self.poll_every):
-                    (S.graphs[2] if first else S.graphs[parity]).replay()
+                    if first:
+                        S.graphs[2].replay()
+                    elif tail:
+                        S.graphs_tail[parity].replay()
+                    else:
+                        S.graphs[parity].replay()
                     first = False
                     parity ^= 1
                     steps += 1
                     replayed += 1
-                if int(S.count[parity].item()) == 0:
+                live = int(S.count[parity].item())
+                if live == 0:
                     break
         else:
             while True:

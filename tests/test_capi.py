@@ -43,3 +43,15 @@ def test_error_text_round_trip():
     assert rc == 1
     lib.fb_last_error.restype = ctypes.c_char_p
     assert b"row size" in lib.fb_last_error()
+
+
+def test_attention_tiling_setter_validates():
+    lib = ctypes.CDLL(build())
+    f = lib.fb_set_attention_tiling
+    f.restype = ctypes.c_int
+    i = ctypes.c_int32
+    assert f(i(3), i(0), i(0)) == 1           # frame warps must be 2/4/8
+    assert f(i(0), i(5), i(0)) == 1           # rows must be even
+    assert f(i(0), i(0), i(-1)) == 1
+    assert f(i(4), i(4), i(160)) == 0
+    assert f(i(0), i(0), i(0)) == 0           # back to the defaults
