@@ -15,6 +15,7 @@ SHAPES = {  # name: (M, N, K, mode)
     "am_lstm": (5120, 1280, 1024, 1),
     "lm_lstm": (256, 4800, 2432, 1),
     "lm_out": (256, 65003, 1216, 0),
+    "lm_out_240": (240, 65003, 1216, 2),      # mode 2: logits + softmax tile statistics
     "enc_proj": (115200, 1280, 320, 0),
     "enc_rec": (512, 1280, 320, 1),
     "am_q": (5120, 320, 320, 0),
@@ -34,6 +35,9 @@ def run(name, M, N, Kd, mode, reps=20):
             H = N // 4
             kw = dict(mode=1, hidden=H, c_in=torch.randn(M, H, device=dev),
                       c_out=torch.empty(M, H, device=dev), h_out=torch.empty(M, H, device=dev))
+        elif mode == 2:
+            kw = dict(out=torch.empty(M, N, device=dev),
+                      row_stats=torch.empty(M, (N + 63) // 64, 4, device=dev), stats_vw=N - 3)
         else:
             kw = dict(out=torch.empty(M, N, device=dev))
         sets.append((a, w, b, kw))
