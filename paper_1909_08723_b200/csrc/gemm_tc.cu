@@ -177,7 +177,8 @@ __device__ __forceinline__ void store_split(const fb_gemm_t& g, int64_t row, int
 template <int BN>
 __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row0, int n0,
                                               float (&acc)[BN / 64][32],
-                                              float* st /* [32][33] */, int half) {
+                                              float* st /* [32][33] */, int half,
+                                              const CUtensorMap* tmC = nullptr) {
   const int lane = threadIdx.x & 31;
   // {max_all, sum_all, max_words, sum_words} of this lane's row over the
   // warp's half of the tile (BN/2 columns)
@@ -396,6 +397,27 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
         g.h_out[(int64_t)slot[it] * g.ld_h + unit] = h;
         if (g.h_split) store_split(g, g.hs_row_mode ? row0 + r : slot[it], unit, h);
       }
+    } else if (tmC && row0 + 32 <= M) {
+      // plain rows, all 32 live: the chunk leaves as one TMA tensor store
+      // (the SM's store path is the epilogue's bottleneck, scripts/micro/)
+      float x[32];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) x[r] = st[r * 33 + lane];
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < 32; ++r) st[r * 32 + lane] = x[r];     // unpadded [32][32] box
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile(
+            "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                tmC),
+            "r"(nb), "r"(row0), "r"(smem_u32(st))
+            : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+      __syncwarp();
     } else {
       const int col = nb + lane;
       for (int r = 0; r < 32; ++r) {
@@ -464,6 +486,7 @@ constexpr int TC_SK_MIN_KB = 8;      // stream-K: at least 8 K blocks (K = 512) 
 template <int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
+               const __grid_constant__ CUtensorMap tmC, int tma_c,
                fb_gemm_t g, int a_planes, int a_plane_rows, int num_kb, int kcb) {
   const int M = row_count(g.m_max, g.m_dev);
   const int m_tiles = (M + TC_BM - 1) / TC_BM;
@@ -492,7 +515,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   __shared__ __align__(8) uint64_t bar_tfull[TC_NACC], bar_tempty[TC_NACC];
   __shared__ uint32_t tmem_base_sh;
   __shared__ int sk_last_sh;
-  __shared__ float epi_stage[8][32 * 33];
+  __shared__ __align__(128) float epi_stage[8][32 * 33];   // 33 * 128 B per warp
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -656,9 +679,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
       }
       TRACE(6, si);
-      epilogue_tile<BN>(g, M, m0 + quarter * 32, n0, acc, epi_stage[warp - 2], half);
+      epilogue_tile<BN>(g, M, m0 + quarter * 32, n0, acc, epi_stage[warp - 2], half,
+                        tma_c ? &tmC : nullptr);
       TRACE(7, si);
     }
+    // the TMA stores' global writes complete before the CTA retires
+    if (tma_c && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   __syncthreads();
   if (warp == 1) {
@@ -894,6 +920,20 @@ static int make_map(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t col
   return FB_OK;
 }
 
+// fp32 output map for the epilogue's TMA stores: 32 x 32 boxes, no swizzle
+static int make_map_c(CUtensorMap* m, const fb_gemm_t* g) {
+  auto enc = get_encode();
+  if (!enc) return fail(FB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)g->n, (cuuint64_t)g->m_max};
+  cuuint64_t strides[1] = {(cuuint64_t)g->ldc * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, g->c, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? FB_OK : FB_ERR_VALUE;
+}
+
 template <int BN>
 static int launch_tc_maps(const CUtensorMap& ta, const CUtensorMap& tw, const fb_gemm_t* g,
                           int a_planes, int64_t a_plane_rows, cudaStream_t s) {
@@ -913,7 +953,17 @@ static int launch_tc_maps(const CUtensorMap& ta, const CUtensorMap& tw, const fb
   }();
   const int kcb = g->kcb > 0 ? g->kcb : kcb_env;
   const int grid = g->splitk_ws ? kNumSMs : std::min(tiles, kNumSMs);
-  k<<<grid, TC_THREADS, smem, s>>>(ta, tw, *g, a_planes, (int)a_plane_rows,
+  // plain fp32 rows (no gather, no fused transform): TMA stores
+#ifndef FB_NO_TMA_STORE
+  static const bool tma_env = getenv("FB_GEMM_TMA_STORE") ? atoi(getenv("FB_GEMM_TMA_STORE")) : 1;
+#else
+  static const bool tma_env = false;
+#endif
+  CUtensorMap tc = ta;
+  int tma_c = tma_env && g->mode == 0 && !g->rows && !g->addend && !g->out_exp2 &&
+              !g->out_logsoftmax && (g->ldc % 4) == 0 && ((uintptr_t)g->c % 16) == 0;
+  if (tma_c && make_map_c(&tc, g) != FB_OK) tma_c = 0;
+  k<<<grid, TC_THREADS, smem, s>>>(ta, tw, tc, tma_c, *g, a_planes, (int)a_plane_rows,
                                                       g->k / TC_BK, kcb);
   count_launch();
   return check_launch("gemm_tc");

@@ -65,7 +65,9 @@ class _LmPool:
         self.eos = torch.zeros(self.P, dtype=torch.float64, device=device)
         E = 2 * N
         self.ev_state = torch.zeros((E, L, 2, H), dtype=f32, device=device)
-        self.ev_logits = torch.empty((E, lw.v_out), dtype=f32, device=device)
+        # row stride padded to 16 bytes: the output GEMM stores tiles with TMA
+        self.ev_logits = torch.empty((E, (lw.v_out + 3) // 4 * 4), dtype=f32,
+                                     device=device)[:, :lw.v_out]
         self.ntiles = (lw.v_out + 63) // 64
         self.ev_stats = torch.empty((E, self.ntiles, 4), dtype=f32, device=device)
         self.seg_ws = torch.empty((N, (d.words + 4095) // 4096 + 2), dtype=torch.float64,
