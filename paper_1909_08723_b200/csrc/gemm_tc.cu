@@ -178,7 +178,9 @@ template <int BN>
 __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row0, int n0,
                                               float (&acc)[BN / 64][32],
                                               float* st /* [32][33] */, int half,
-                                              const CUtensorMap* tmC = nullptr) {
+                                              const CUtensorMap* tmC = nullptr,
+                                              const CUtensorMap* tmH = nullptr,
+                                              const CUtensorMap* tmS = nullptr) {
   const int lane = threadIdx.x & 31;
   // {max_all, sum_all, max_words, sum_words} of this lane's row over the
   // warp's half of the tile (BN/2 columns)
@@ -322,12 +324,23 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
           cv[u] = fsig(gf) * cp[u] + fsig(gi) * ftanh(gg);
           hv[u] = fsig(go) * ftanh(cv[u]) + hr[u];
         }
+        const bool tma = tmC && row0 + 32 <= M;     // warp-uniform; slot == row here
+        if (tma) {
+          // stage [32 rows][8 units] c and h tiles (and the h planes) for TMA
+          float4* sc = reinterpret_cast<float4*>(st) + lane * 2;
+          sc[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
+          sc[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
+          float4* sh = reinterpret_cast<float4*>(st + 256) + lane * 2;
+          sh[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
+          sh[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
+        } else {
         float4* c4 = reinterpret_cast<float4*>(g.c_out + (int64_t)slot * g.ld_cout + unit0);
         c4[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
         c4[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
         float4* h4 = reinterpret_cast<float4*>(g.h_out + (int64_t)slot * g.ld_h + unit0);
         h4[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
         h4[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
+        }
         if (g.h_split) {
           __nv_bfloat16 pl[3][8];
 #pragma unroll
@@ -339,13 +352,38 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
             pl[1][u] = mid;
             pl[2][u] = __float2bfloat16_rn(r1 - __bfloat162float(mid));
           }
+          if (tma && tmS) {
+            uint4* ss = reinterpret_cast<uint4*>(st + 512);        // [3][32 rows][16 B]
+#pragma unroll
+            for (int q = 0; q < 3; ++q) ss[q * 32 + lane] = *reinterpret_cast<const uint4*>(pl[q]);
+          } else {
           __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.h_split) +
                              (int64_t)(g.hs_row_mode ? row : slot) * g.ld_hs + unit0;
 #pragma unroll
           for (int q = 0; q < 3; ++q)
             *reinterpret_cast<uint4*>(o + (int64_t)q * g.hs_plane_rows * g.ld_hs) =
                 *reinterpret_cast<const uint4*>(pl[q]);
+          }
         }
+      }
+      if (tmC && row0 + 32 <= M) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                  tmC), "r"(unit0), "r"(row0), "r"(smem_u32(st)) : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                  tmH), "r"(unit0), "r"(row0), "r"(smem_u32(st + 256)) : "memory");
+          if (g.h_split && tmS)
+            asm volatile(
+                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
+                ::"l"(tmS), "r"(unit0), "r"(row0), "r"(0), "r"(smem_u32(st + 512)) : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        __syncwarp();
       }
       continue;
     }
@@ -486,7 +524,8 @@ constexpr int TC_SK_MIN_KB = 8;      // stream-K: at least 8 K blocks (K = 512) 
 template <int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
-               const __grid_constant__ CUtensorMap tmC, int tma_c,
+               const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmH,
+               const __grid_constant__ CUtensorMap tmS, int tma_c,
                fb_gemm_t g, int a_planes, int a_plane_rows, int num_kb, int kcb) {
   const int M = row_count(g.m_max, g.m_dev);
   const int m_tiles = (M + TC_BM - 1) / TC_BM;
@@ -680,7 +719,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
       TRACE(6, si);
       epilogue_tile<BN>(g, M, m0 + quarter * 32, n0, acc, epi_stage[warp - 2], half,
-                        tma_c ? &tmC : nullptr);
+                        tma_c ? &tmC : nullptr, tma_c == 2 ? &tmH : nullptr,
+                        tma_c == 2 && g.h_split ? &tmS : nullptr);
       TRACE(7, si);
     }
     // the TMA stores' global writes complete before the CTA retires
@@ -934,6 +974,34 @@ static int make_map_c(CUtensorMap* m, const fb_gemm_t* g) {
   return r == CUDA_SUCCESS ? FB_OK : FB_ERR_VALUE;
 }
 
+// LSTM-cell outputs (mode 1, rows in GEMM order): c/h fp32 [rows][hidden]
+// boxes of 8 units x 32 rows; h planes bf16 [3][plane rows][hidden] boxes
+static int make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* p,
+                       uint64_t cols, uint64_t rows, uint64_t ld) {
+  auto enc = get_encode();
+  if (!enc) return FB_ERR_CUDA;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * esize};
+  cuuint32_t box[2] = {8, 32};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, dt, 2, const_cast<void*>(p), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS ? FB_OK : FB_ERR_VALUE;
+}
+
+static int make_map_planes(CUtensorMap* m, const fb_gemm_t* g) {
+  auto enc = get_encode();
+  if (!enc) return FB_ERR_CUDA;
+  cuuint64_t dims[3] = {(cuuint64_t)g->hidden, (cuuint64_t)g->hs_plane_rows, 3};
+  cuuint64_t strides[2] = {(cuuint64_t)g->ld_hs * 2, (cuuint64_t)g->hs_plane_rows * g->ld_hs * 2};
+  cuuint32_t box[3] = {8, 32, 3};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, g->h_split, dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
+             ? FB_OK : FB_ERR_VALUE;
+}
+
 template <int BN>
 static int launch_tc_maps(const CUtensorMap& ta, const CUtensorMap& tw, const fb_gemm_t* g,
                           int a_planes, int64_t a_plane_rows, cudaStream_t s) {
@@ -955,15 +1023,27 @@ static int launch_tc_maps(const CUtensorMap& ta, const CUtensorMap& tw, const fb
   const int grid = g->splitk_ws ? kNumSMs : std::min(tiles, kNumSMs);
   // plain fp32 rows (no gather, no fused transform): TMA stores
 #ifndef FB_NO_TMA_STORE
-  static const bool tma_env = getenv("FB_GEMM_TMA_STORE") ? atoi(getenv("FB_GEMM_TMA_STORE")) : 1;
+  // bit 0: plain fp32 tiles, bit 1: LSTM-cell outputs (dev override FB_GEMM_TMA_STORE)
+  static const int tma_env = getenv("FB_GEMM_TMA_STORE") ? atoi(getenv("FB_GEMM_TMA_STORE")) : 3;
 #else
-  static const bool tma_env = false;
+  static const int tma_env = 0;
 #endif
-  CUtensorMap tc = ta;
-  int tma_c = tma_env && g->mode == 0 && !g->rows && !g->addend && !g->out_exp2 &&
+  CUtensorMap tc = ta, th = ta, ts = ta;
+  int tma_c = (tma_env & 1) && g->mode == 0 && !g->rows && !g->addend && !g->out_exp2 &&
               !g->out_logsoftmax && (g->ldc % 4) == 0 && ((uintptr_t)g->c % 16) == 0;
   if (tma_c && make_map_c(&tc, g) != FB_OK) tma_c = 0;
-  k<<<grid, TC_THREADS, smem, s>>>(ta, tw, tc, tma_c, *g, a_planes, (int)a_plane_rows,
+  // LSTM cell with rows in GEMM order (the word LM): c, h and h planes by TMA
+  const bool a16 = ((uintptr_t)g->c_out % 16) == 0 && ((uintptr_t)g->h_out % 16) == 0 &&
+                   (g->ld_cout % 4) == 0 && (g->ld_h % 4) == 0 && (g->hidden % 8) == 0;
+  const bool s16 = !g->h_split || (((uintptr_t)g->h_split % 16) == 0 && (g->ld_hs % 8) == 0);
+  if ((tma_env & 2) && g->mode == 1 && !g->rows && a16 && s16 &&
+      make_map_2d(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g->c_out, g->hidden, g->m_max,
+                  g->ld_cout) == FB_OK &&
+      make_map_2d(&th, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g->h_out, g->hidden, g->m_max,
+                  g->ld_h) == FB_OK &&
+      (!g->h_split || make_map_planes(&ts, g) == FB_OK))
+    tma_c = 2;
+  k<<<grid, TC_THREADS, smem, s>>>(ta, tw, tc, th, ts, tma_c, *g, a_planes, (int)a_plane_rows,
                                                       g->k / TC_BK, kcb);
   count_launch();
   return check_launch("gemm_tc");

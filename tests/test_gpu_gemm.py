@@ -203,3 +203,40 @@ def test_tc_fused_epilogues_match_separate_kernels(m, n, k):
     K.gemm_tc(ap, w, m=m, k=k, bias=b, out=e, rows=rows, kcb=1, out_exp2=True)
     assert torch.equal(e, torch.exp(2.0 * logits)) or \
         (e - torch.exp(2.0 * logits)).abs().max().item() <= 1e-6 * e.abs().max().item()
+
+
+@pytest.mark.parametrize("m", [64, 150, 333])
+def test_tc_lstm_epilogue_tma_rows_in_order(m):
+    """LSTM cell with rows in GEMM order (the word LM: c, h and the next GEMM's
+    h planes leave by TMA tensor stores) == the SIMT kernel, planes exact."""
+    from paper_1909_08723_b200 import kernels as K
+    dev = torch.device("cuda")
+    torch.manual_seed(m)
+    H, k = 1200, 2432
+    a = torch.randn(m, k, device=dev) * 0.3
+    w = _bf16_exact(torch.rand(4 * H, k, device=dev) * 0.1 - 0.05)
+    b = torch.randn(4 * H, device=dev) * 0.1
+    parent = torch.randperm(m, device=dev).to(torch.int32)
+    c_in = torch.randn(m, H, device=dev)
+    outs = []
+    for tc in (False, True):
+        c_out = torch.full((m, H), 7.0, device=dev)
+        h_out = torch.full((m, H), 7.0, device=dev)
+        kw = dict(m=m, k=k, bias=b, mode=1, hidden=H, parent=parent, c_in=c_in, c_out=c_out,
+                  h_out=h_out)
+        if tc:
+            hs = torch.zeros(3, m + 16, 1216, dtype=torch.bfloat16, device=dev)
+            K.gemm_tc(_packed(a, k), w.to(torch.bfloat16), h_split=hs, hs_by_row=True, **kw)
+        else:
+            K.gemm(a, w, **kw)
+        outs.append((h_out, c_out))
+    assert (outs[0][0] - outs[1][0]).abs().max().item() < 1e-5
+    assert (outs[0][1] - outs[1][1]).abs().max().item() < 1e-5
+    h = outs[1][0]
+    hi = h.to(torch.bfloat16)
+    r1 = h - hi.float()
+    mid = r1.to(torch.bfloat16)
+    lo = (r1 - mid.float()).to(torch.bfloat16)
+    assert torch.equal(hs[0, :m, :H], hi) and torch.equal(hs[1, :m, :H], mid)
+    assert torch.equal(hs[2, :m, :H], lo)
+    assert (hs[:, m:, :] == 0).all() and (hs[:, :, H:] == 0).all()
