@@ -324,7 +324,7 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
           cv[u] = fsig(gf) * cp[u] + fsig(gi) * ftanh(gg);
           hv[u] = fsig(go) * ftanh(cv[u]) + hr[u];
         }
-        const bool tma = tmC && row0 + 32 <= M;     // warp-uniform; slot == row here
+        const bool tma = tmC && tmH && row0 + 32 <= M;   // warp-uniform; slot == row here
         if (tma) {
           // stage [32 rows][8 units] c and h tiles (and the h planes) for TMA
           float4* sc = reinterpret_cast<float4*>(st) + lane * 2;
@@ -352,7 +352,7 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
             pl[1][u] = mid;
             pl[2][u] = __float2bfloat16_rn(r1 - __bfloat162float(mid));
           }
-          if (tma && tmS) {
+          if (tmS && row0 + 32 <= M) {
             uint4* ss = reinterpret_cast<uint4*>(st + 512);        // [3][32 rows][16 B]
 #pragma unroll
             for (int q = 0; q < 3; ++q) ss[q * 32 + lane] = *reinterpret_cast<const uint4*>(pl[q]);
@@ -366,16 +366,19 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
           }
         }
       }
-      if (tmC && row0 + 32 <= M) {
+      if ((tmC && tmH) || tmS) {
+       if (row0 + 32 <= M) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
+          if (tmC && tmH) {
           asm volatile(
               "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                   tmC), "r"(unit0), "r"(row0), "r"(smem_u32(st)) : "memory");
           asm volatile(
               "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                   tmH), "r"(unit0), "r"(row0), "r"(smem_u32(st + 256)) : "memory");
+          }
           if (g.h_split && tmS)
             asm volatile(
                 "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
@@ -384,6 +387,7 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
         __syncwarp();
+       }
       }
       continue;
     }
@@ -719,8 +723,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
       TRACE(6, si);
       epilogue_tile<BN>(g, M, m0 + quarter * 32, n0, acc, epi_stage[warp - 2], half,
-                        tma_c ? &tmC : nullptr, tma_c == 2 ? &tmH : nullptr,
-                        tma_c == 2 && g.h_split ? &tmS : nullptr);
+                        (tma_c == 1 || tma_c == 2) ? &tmC : nullptr,
+                        tma_c == 2 ? &tmH : nullptr,
+                        (tma_c == 2 || tma_c == 3) && g.h_split ? &tmS : nullptr);
       TRACE(7, si);
     }
     // the TMA stores' global writes complete before the CTA retires
@@ -1024,7 +1029,8 @@ static int launch_tc_maps(const CUtensorMap& ta, const CUtensorMap& tw, const fb
   // plain fp32 rows (no gather, no fused transform): TMA stores
 #ifndef FB_NO_TMA_STORE
   // bit 0: plain fp32 tiles, bit 1: LSTM-cell outputs (dev override FB_GEMM_TMA_STORE)
-  static const int tma_env = getenv("FB_GEMM_TMA_STORE") ? atoi(getenv("FB_GEMM_TMA_STORE")) : 3;
+  static const int tma_env = getenv("FB_GEMM_TMA_STORE") ? atoi(getenv("FB_GEMM_TMA_STORE")) : 7;
+  // bit 2: the h planes of row-gathered LSTM cells
 #else
   static const int tma_env = 0;
 #endif
@@ -1043,6 +1049,10 @@ static int launch_tc_maps(const CUtensorMap& ta, const CUtensorMap& tw, const fb
                   g->ld_h) == FB_OK &&
       (!g->h_split || make_map_planes(&ts, g) == FB_OK))
     tma_c = 2;
+  // rows gathered (the acoustic decoder): only the row-ordered h planes by TMA
+  else if ((tma_env & 4) && g->mode == 1 && g->rows && g->h_split && g->hs_row_mode && a16 &&
+           s16 && make_map_planes(&ts, g) == FB_OK)
+    tma_c = 3;
   k<<<grid, TC_THREADS, smem, s>>>(ta, tw, tc, th, ts, tma_c, *g, a_planes, (int)a_plane_rows,
                                                       g->k / TC_BK, kcb);
   count_launch();
