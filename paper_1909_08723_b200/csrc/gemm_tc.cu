@@ -444,18 +444,39 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
       // (the SM's store path is the epilogue's bottleneck, scripts/micro/)
       float x[32];
 #pragma unroll
-      for (int r = 0; r < 32; ++r) x[r] = st[r * 33 + lane];
+      for (int r = 0; r < 32; ++r) {
+        x[r] = st[r * 33 + lane];
+        if (g.out_exp2) x[r] = expf(2.0f * x[r]);          // == query_exp_kernel
+      }
       __syncwarp();
 #pragma unroll
       for (int r = 0; r < 32; ++r) st[r * 32 + lane] = x[r];     // unpadded [32][32] box
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) {
+      if (g.rows) {
+        // gathered output rows: eight 4-row TMA scatters (box {32, 1})
+        const int orow = __ldg(g.rows + row0 + lane);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int a0 = __shfl_sync(0xffffffffu, orow, 4 * q);
+          const int a1 = __shfl_sync(0xffffffffu, orow, 4 * q + 1);
+          const int a2 = __shfl_sync(0xffffffffu, orow, 4 * q + 2);
+          const int a3 = __shfl_sync(0xffffffffu, orow, 4 * q + 3);
+          if (lane == 0)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group "
+                "[%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(tmC),
+                "r"(nb), "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(smem_u32(st + q * 128))
+                : "memory");
+        }
+      } else if (lane == 0) {
         asm volatile(
             "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                 tmC),
             "r"(nb), "r"(row0), "r"(smem_u32(st))
             : "memory");
+      }
+      if (lane == 0) {
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       }
@@ -969,9 +990,11 @@ static int make_map(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t col
 static int make_map_c(CUtensorMap* m, const fb_gemm_t* g) {
   auto enc = get_encode();
   if (!enc) return fail(FB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[2] = {(cuuint64_t)g->n, (cuuint64_t)g->m_max};
+  // gathered rows (g->rows) go out as 4-row scatters: box {32, 1}, and the row
+  // extent is the caller's contract on rows[] (no clipping needed)
+  cuuint64_t dims[2] = {(cuuint64_t)g->n, g->rows ? (cuuint64_t)1 << 24 : (cuuint64_t)g->m_max};
   cuuint64_t strides[1] = {(cuuint64_t)g->ldc * 4};
-  cuuint32_t box[2] = {32, 32};
+  cuuint32_t box[2] = {32, g->rows ? 1u : 32u};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, g->c, dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1029,14 +1052,14 @@ static int launch_tc_maps(const CUtensorMap& ta, const CUtensorMap& tw, const fb
   // plain fp32 rows (no gather, no fused transform): TMA stores
 #ifndef FB_NO_TMA_STORE
   // bit 0: plain fp32 tiles, bit 1: LSTM-cell outputs (dev override FB_GEMM_TMA_STORE)
-  static const int tma_env = getenv("FB_GEMM_TMA_STORE") ? atoi(getenv("FB_GEMM_TMA_STORE")) : 7;
-  // bit 2: the h planes of row-gathered LSTM cells
+  static const int tma_env = getenv("FB_GEMM_TMA_STORE") ? atoi(getenv("FB_GEMM_TMA_STORE")) : 15;
+  // bit 2: the h planes of row-gathered LSTM cells, bit 3: gathered plain rows (TMA scatter4)
 #else
   static const int tma_env = 0;
 #endif
   CUtensorMap tc = ta, th = ta, ts = ta;
-  int tma_c = (tma_env & 1) && g->mode == 0 && !g->rows && !g->addend && !g->out_exp2 &&
-              !g->out_logsoftmax && (g->ldc % 4) == 0 && ((uintptr_t)g->c % 16) == 0;
+  int tma_c = (tma_env & 1) && g->mode == 0 && (!g->rows || (tma_env & 8)) && !g->addend &&
+              (g->ldc % 4) == 0 && ((uintptr_t)g->c % 16) == 0;
   if (tma_c && make_map_c(&tc, g) != FB_OK) tma_c = 0;
   // LSTM cell with rows in GEMM order (the word LM): c, h and h planes by TMA
   const bool a16 = ((uintptr_t)g->c_out % 16) == 0 && ((uintptr_t)g->h_out % 16) == 0 &&
