@@ -1131,11 +1131,18 @@ extern "C" int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_
     return e ? atoi(e) : 0;
   }();
   const int tiles128 = ((g->m_max + TC_BM - 1) / TC_BM) * ((g->n + 127) / 128);
-  // 128-wide tiles beat 64-wide ones at the decoder shapes with n > 64
-  // (graph-timed scripts/bench_gemm.py)
-  (void)tiles128;
+  // 128-wide tiles beat 64-wide ones at the decoder shapes with n > 64 once
+  // the grid holds more than a third of the SMs; below that (the word LM's
+  // LSTM GEMMs with <= 128 event rows, the acoustic LSTM GEMMs in the
+  // lock-step tail) twice the CTAs win: 160x4800x2432 33 -> 47 us, but
+  // 64x4800x2432 32 -> 27 us and 512x1280x320 12 -> 8.8 us (graph-timed
+  // scripts/bench_gemm.py via scripts/sweep_bn.sh).  Same K loop per output,
+  // so the result is bit-identical either way.
+  static const int few_env = getenv("FB_GEMM_FEW") ? atoi(getenv("FB_GEMM_FEW")) : 1;  // dev A/B
+  const bool few_tiles = few_env && force_bn == 0 && !g->splitk_ws && 3 * tiles128 <= kNumSMs;
   // n <= 64 (the acoustic output projection): a 64-wide tile is the whole N
-  const bool want64 = force_bn == 64 || (force_bn == 0 && g->n <= 64) || g->out_logsoftmax;
+  const bool want64 = force_bn == 64 || (force_bn == 0 && g->n <= 64) || g->out_logsoftmax ||
+                      few_tiles;
   if (want64 && !g->row_stats)
     return launch_tc<64>(g, a_planes, a_plane_rows, g->n, (cudaStream_t)stream);
   return launch_tc<128>(g, a_planes, a_plane_rows, g->n, (cudaStream_t)stream);

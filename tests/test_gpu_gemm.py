@@ -240,3 +240,31 @@ def test_tc_lstm_epilogue_tma_rows_in_order(m):
     assert torch.equal(hs[0, :m, :H], hi) and torch.equal(hs[1, :m, :H], mid)
     assert torch.equal(hs[2, :m, :H], lo)
     assert (hs[:, m:, :] == 0).all() and (hs[:, :, H:] == 0).all()
+
+
+@pytest.mark.parametrize("n,k", [(4800, 2432), (1280, 320)])
+def test_tc_few_tile_width_is_bit_identical(n, k):
+    """Grids under a third of the SMs take 64-wide tiles (gemm_tc.cu): the
+    first 64 rows of a 64-row GEMM (64-wide tiles) and of a 600-row GEMM
+    (128-wide tiles) over the same operands are bit-identical, plain and
+    LSTM-cell epilogues."""
+    from paper_1909_08723_b200 import kernels as K
+    dev = torch.device("cuda")
+    torch.manual_seed(n + k)
+    a = torch.randn(600, k, device=dev) * 0.3
+    w = _bf16_exact(torch.rand(n, k, device=dev) * 0.1 - 0.05).to(torch.bfloat16)
+    b = torch.randn(n, device=dev) * 0.1
+    H = n // 4
+    c_in = torch.randn(600, H, device=dev)
+    res = {}
+    for m in (64, 600):
+        ap = _packed(a[:m], k)
+        out = torch.empty(m, n, device=dev)
+        K.gemm_tc(ap, w, m=m, k=k, bias=b, out=out)
+        c_out = torch.empty(m, H, device=dev)
+        h_out = torch.empty(m, H, device=dev)
+        K.gemm_tc(ap, w, m=m, k=k, bias=b, mode=1, hidden=H, c_in=c_in[:m], c_out=c_out,
+                  h_out=h_out)
+        res[m] = (out, c_out, h_out)
+    for x64, x600 in zip(res[64], res[600]):
+        assert torch.equal(x64, x600[:64])
