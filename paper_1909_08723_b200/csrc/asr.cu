@@ -313,6 +313,9 @@ __device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) {
 #ifndef FB_ENERGY_MINB
 #define FB_ENERGY_MINB 1
 #endif
+#ifndef FB_ENERGY_PF
+#define FB_ENERGY_PF 1   // groups of four key dims in flight ahead of the one in use
+#endif
 template <int R, int kEnWarps>
 __global__ void __launch_bounds__(kEnWarps * 32, FB_ENERGY_MINB)
 att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
@@ -363,14 +366,26 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
   f2_t e2[R / 2];
 #pragma unroll
   for (int rp = 0; rp < R / 2; ++rp) e2[rp] = pk2(0.f, 0.f);
-  // keys for dims a..a+3 in registers, a+4..a+7 in flight (A % 4 == 0)
-  float kc[4], kn[4];
+  // keys for dims a..a+3 in registers, the next FB_ENERGY_PF groups of four
+  // in flight (A % 4 == 0)
+  float kb[FB_ENERGY_PF + 1][4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) kc[j] = __ldg(kt + (int64_t)j * TM);
+  for (int p = 0; p <= FB_ENERGY_PF; ++p)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      kb[p][j] = 4 * p + j < A ? __ldg(kt + (int64_t)(4 * p + j) * TM) : 0.f;
   for (int a = 0; a < A; a += 4) {
-    const bool more = a + 4 < A;
+    float kc[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) kn[j] = more ? __ldg(kt + (int64_t)(a + 4 + j) * TM) : 0.f;
+    for (int j = 0; j < 4; ++j) kc[j] = kb[0][j];
+#pragma unroll
+    for (int p = 0; p < FB_ENERGY_PF; ++p)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) kb[p][j] = kb[p + 1][j];
+    const int an = a + 4 * (FB_ENERGY_PF + 1);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      kb[FB_ENERGY_PF][j] = an + j < A ? __ldg(kt + (int64_t)(an + j) * TM) : 0.f;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const f2_t K0 = pk2(kc[2 * h], kc[2 * h]), K1 = pk2(kc[2 * h + 1], kc[2 * h + 1]);
@@ -393,8 +408,6 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
         e2[rp] = fma2(num, pk2(rcp_approx(dx), rcp_approx(dy)), e2[rp]);
       }
     }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) kc[j] = kn[j];
   }
   if (valid) {
 #pragma unroll
