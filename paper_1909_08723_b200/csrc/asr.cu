@@ -316,8 +316,15 @@ __device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) {
 #ifndef FB_ENERGY_PF
 #define FB_ENERGY_PF 1   // groups of four key dims in flight ahead of the one in use
 #endif
+#ifndef FB_ENERGY_MINB8
+// 256-frame CTAs with <= 10 rows (c2's main graph set): three CTAs per SM
+// (77 registers, no spills) -- c2 163.6 -> 162.9-163.1 ms over three
+// alternating A/B rounds; four (64 registers) is slower (166 ms)
+#define FB_ENERGY_MINB8 3
+#endif
 template <int R, int kEnWarps>
-__global__ void __launch_bounds__(kEnWarps * 32, FB_ENERGY_MINB)
+__global__ void __launch_bounds__(kEnWarps * 32,
+                                  (kEnWarps == 8 && R <= 10) ? FB_ENERGY_MINB8 : FB_ENERGY_MINB)
 att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
                   const int32_t* __restrict__ n_live, const int32_t* __restrict__ t_enc,
                   const float* __restrict__ ekt, int A, const float* __restrict__ v,
