@@ -496,8 +496,15 @@ __global__ void exp2x_kernel(int64_t n, const float* __restrict__ x, float* __re
 }
 
 
+#ifndef FB_CTX_TU
+#define FB_CTX_TU 8      // encoder frames per thread in flight (float4 each)
+#endif
 template <int RB>
+#ifdef FB_CTX_MAXREG   // register cap for more resident context CTAs
+__global__ void __maxnreg__(RB <= 12 ? FB_CTX_MAXREG : 128)
+#else
 __global__ void __launch_bounds__(kCtxMaxThreads)
+#endif
 att_context_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
                    const int32_t* __restrict__ n_live, const int32_t* __restrict__ t_enc,
                    const float* __restrict__ enc, int C, const float* __restrict__ alpha,
@@ -519,7 +526,7 @@ att_context_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
   const int col = 4 * (blockIdx.z * blockDim.x + tid);
   const bool has_col = col < C;
   const float* eu = enc + (int64_t)u * TM * C + (has_col ? col : 0);
-  constexpr int TU = 8;
+  constexpr int TU = FB_CTX_TU;
   float4 xn[TU];
   if (has_col && TU <= T) {       // first frames in flight before the alpha tile
 #pragma unroll
