@@ -2,19 +2,28 @@
 """Benchmark of the fused look-ahead beam decoder (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config c2|c4|c5|...]
 
 Workload (BASELINE.json configs[1], "c2"): WSJ-shaped random-init model
 (4-layer BiLSTM 320 encoder, 3-layer attention-LSTM decoder, 52 tokens),
 beam 10, look-ahead fusion with a 65k-word random-init 3x1200 LSTM LM over the
 character prefix trie, 512 synthetic 80-dim fbank utterances of 700..900
-frames per GPU (weak scaling: every rank decodes its own 512-utterance
-shard, only a final host gather).  One "step" = one decode of the whole
-512-utterance batch (encoder + lock-step beam search + LM fusion).
+frames per GPU.  Multi-GPU = weak scaling over a fixed corpus of 512 x N
+utterances, LPT-sharded by length across the ranks (``sharding.plan_shards``),
+each rank decoding its shard in ``batch_size`` batches with no collective
+inside the step and one final gather.  One "step" = one decode of the rank's
+whole shard (encoder + lock-step beam search + LM fusion).
 
-Output: ONE JSON line on rank 0 (see the task contract): utt/s (value = device-
-resident inputs, e2e = public decode_batch API with host features), RTF, the
-dominant kernel's roofline fraction, the same-run CPU baseline (the oracle
-port on the host cores), launch count and clocks.
+* ``value``: inputs already resident in HBM (staged once), engine replays.
+* ``e2e``: the public API a user calls -- ``decode_corpus_sharded`` over
+  ``decode_corpus(batch_size, fusion_factory)`` (a fresh ``LookaheadFusion``
+  per batch, as the reference pipeline does) with host feature matrices, the
+  host->device copies, the result read-back and the final gather inside the
+  timed region.
+* ``cpu_baseline`` / ``--impl reference``: the reference decoder's CPU
+  algorithm (the oracle restatement pinned to it bit-for-bit, driving
+  PyTorch-CPU fp32 adapters of the same weights), one single-threaded process
+  per host core, imported WITHOUT the product package.
 """
 
 from __future__ import annotations
@@ -32,6 +41,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+METRIC = "utterances/sec and RTF, beam-10 look-ahead word-LM decode"
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -41,9 +52,12 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2")
     ap.add_argument("--utts", type=int, default=None, help="override utterances per GPU")
+    ap.add_argument("--batch", type=int, default=None, help="override decode batch size")
     ap.add_argument("--words", type=int, default=None, help="override LM vocabulary (debug)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-utts", type=int, default=0, help="CPU baseline sample (0 = auto)")
+    ap.add_argument("--cpu-procs", type=int, default=0, help="CPU worker processes (0 = cores)")
+    ap.add_argument("--ref-budget", type=float, default=240.0,
+                    help="--impl reference: target seconds of timed CPU work")
     ap.add_argument("--stats", action="store_true", help="print decode statistics to stderr")
     ap.add_argument("--set", action="append", default=[],
                     help="calibration override, e.g. asr.out_scale=0.7 or lm.eos_bias=5")
@@ -57,39 +71,51 @@ def log(*a):
 
 
 # ---------------------------------------------------------------- workload --
-def build_inputs(wl_name: str, rank: int, n_utts=None, words=None, overrides=()):
-    from paper_1909_08723_b200 import synth
+def workload(args):
+    from oracle import harness as H      # input generation only (no oracle compute)
+    wl = H.workload(args.config, args.utts, args.words, args.set)
+    if args.batch:
+        import dataclasses
+        wl = dataclasses.replace(wl, batch_size=args.batch)
+    return wl
+
+
+def corpus(wl, world: int):
+    """The fixed corpus of a world-size-N run: N seeded draws of n_utts (rank
+    r's draw uses seed + 100 + r, so N = 1 is the c2 set the parity fixtures
+    hold); ids made unique across draws."""
+    from oracle import harness as H
+    out = []
+    for r in range(world):
+        for u, x in H.corpus(wl, r):
+            out.append((u if r == 0 else f"r{r}-{u}", x))
+    return out
+
+
+def build_product(wl):
+    """Product-side resources: dictionary, weights, trie (native builder)."""
+    from oracle import harness as H
     from paper_1909_08723_b200.token_dict import TokenDictionary
     from paper_1909_08723_b200.lexicon_trie import build_trie
-    import dataclasses
-    wl = synth.WORKLOADS[wl_name]
-    if n_utts is not None:
-        wl = dataclasses.replace(wl, n_utts=n_utts, batch_size=min(wl.batch_size, n_utts))
-    if words is not None and wl.lm is not None:
-        wl = dataclasses.replace(wl, lm=dataclasses.replace(wl.lm, words=words))
-    for ov in overrides:
-        key, val = ov.split("=")
-        part, field = key.split(".")
-        if part == "wl":
-            wl = dataclasses.replace(wl, **{field: type(getattr(wl, field))(val)})
-        else:
-            sub = getattr(wl, part)
-            wl = dataclasses.replace(wl, **{part: dataclasses.replace(sub, **{field: float(val)})})
-    if wl.sublm is not None:       # config 4: subword tokens + token-level LM fusion
-        d = TokenDictionary(synth.subword_token_list(wl.asr.vocab - 4, seed=wl.seed + 3))
-    else:
-        d = TokenDictionary(synth.wsj_token_list())
-    W = synth.asr_weights(wl.asr, seed=wl.seed, eos_id=d.eos_id)
-    words_l, trie = None, None
+    S = H.synth()
+    d = TokenDictionary(H.file_tokens(wl))
+    W = S.asr_weights(wl.asr, seed=wl.seed, eos_id=d.eos_id)
+    trie = None
     if wl.sublm is not None:
-        W.update(synth.subword_lm_weights(wl.sublm, seed=wl.seed + 1, eos_id=d.eos_id))
+        W.update(S.subword_lm_weights(wl.sublm, seed=wl.seed + 1, eos_id=d.eos_id))
     if wl.lm is not None:
-        W.update(synth.lm_weights(wl.lm, seed=wl.seed + 1))
-        words_l = synth.synth_lexicon(wl.lm.words, seed=wl.seed + 2)
-        trie = build_trie(words_l, d)
-    utts = synth.synth_fbank(wl.n_utts, seed=wl.seed + 100 + rank, frames=wl.frames,
-                             feat_dim=wl.asr.feat_dim, sort_by_length=True)
-    return wl, d, W, words_l, trie, utts
+        W.update(S.lm_weights(wl.lm, seed=wl.seed + 1))
+        trie = build_trie(S.synth_lexicon(wl.lm.words, seed=wl.seed + 2), d)
+    return d, W, trie
+
+
+def build_inputs(wl_name: str, rank: int, n_utts=None, words=None, overrides=()):
+    """(wl, dict, weights, words, trie, rank's utterances) -- used by tests."""
+    from oracle import harness as H
+    wl = H.workload(wl_name, n_utts, words, overrides)
+    d, W, trie = build_product(wl)
+    words_l = H.synth().synth_lexicon(wl.lm.words, seed=wl.seed + 2) if wl.lm else None
+    return wl, d, W, words_l, trie, H.corpus(wl, rank)
 
 
 def decode_config(wl):
@@ -97,6 +123,27 @@ def decode_config(wl):
     return DecodeConfig(beam_size=wl.beam, lm_weight=wl.lm_weight,
                         coverage_mode=wl.coverage_mode, coverage_weight=wl.coverage_weight,
                         eos_gamma=wl.eos_gamma, max_len_ratio=wl.max_len_ratio)
+
+
+def workload_config(wl, world: int, per_rank: int):
+    a = wl.asr
+    if wl.sublm is not None:
+        s_ = wl.sublm
+        fus = (f"shallow fusion with a {s_.layers}x{s_.hidden} token LSTM LM (SubwordFusion)")
+    elif wl.lm is not None:
+        fus = f"look-ahead fusion with a {wl.lm.words}-word {wl.lm.layers}x{wl.lm.hidden} LSTM LM"
+    else:
+        fus = "no LM"
+    desc = (f"{wl.name}: {a.enc_layers}x BiLSTM-{a.enc_hidden} encoder + {a.dec_layers}x "
+            f"LSTM-{a.dec_hidden} attention decoder ({a.vocab} tokens), beam {wl.beam}, {fus}, "
+            f"{wl.n_utts} utts/GPU of {wl.frames[0]}-{wl.frames[1]} frames")
+    return {"workload": desc, "utts_per_gpu": per_rank, "corpus_utts": wl.n_utts * world,
+            "frames": list(wl.frames), "beam": wl.beam, "vocab": a.vocab,
+            "lm_words": wl.lm.words if wl.lm else 0, "lm_weight": wl.lm_weight,
+            "coverage": wl.coverage_mode, "eos_gamma": wl.eos_gamma,
+            "batch_size": wl.batch_size, "sharding": "LPT by length, length-sorted batches",
+            "l2": "working set >> L2 (LM weights, g pool GBs, encoder outputs): no flush needed",
+            "length_sorted": True}
 
 
 # ------------------------------------------------------------------ clocks --
@@ -111,6 +158,7 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self.proc = None
+        self.recording = False
 
     def start(self):
         try:
@@ -129,10 +177,7 @@ class ClockSampler:
             if len(parts) >= 7 and self.recording:
                 self.rows.append(parts)
 
-    recording = False
-
     def mark(self, on: bool):
-        """Keep only samples taken inside the timed window."""
         self.recording = on
 
     def stop(self):
@@ -162,113 +207,93 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------- CPU baseline --
-def cpu_decode(wl, d, W, words, utts, n: int, threads: int):
-    """The oracle CPU decoder (restated reference search + PyTorch-CPU fp32
-    adapters) on a length-stratified sample of n utterances (cpu_sample);
-    returns (seconds, results)."""
-    import torch
-    from oracle.lexicon import OracleDict, build_trie as obuild
-    from oracle.lookahead import OracleLookahead
-    from oracle.neural import OracleAttnLstmScorer, OracleLstmWordLM
-    from oracle.search import OracleConfig, decode_batch as odecode
-    torch.set_num_threads(threads)
-    od = OracleDict(_file_tokens(d))
-    sc = OracleAttnLstmScorer(W, wl.asr.enc_layers, wl.asr.dec_layers, wl.asr.subsample,
-                              od.eos_id)
-    fus = None
-    if wl.lm is not None:
-        lm = OracleLstmWordLM(W, wl.lm.layers, wl.lm.words)
-        fus = OracleLookahead(obuild(words, od), lm, od)
-    if wl.sublm is not None:
-        from oracle.subword import OracleLstmCharLM, OracleSubwordFusion
-        fus = OracleSubwordFusion(OracleLstmCharLM(W, wl.sublm.layers, od.pad_id, od.eos_id))
-    cfg = OracleConfig(beam_size=wl.beam, lm_weight=wl.lm_weight,
-                       coverage_mode=wl.coverage_mode, coverage_weight=wl.coverage_weight,
-                       eos_gamma=wl.eos_gamma, max_len_ratio=wl.max_len_ratio)
-
-    class F:
-        def __init__(self, u, x):
-            self.utt_id, self.data = u, x
-
-    feats = [F(u, x) for u, x in (utts[i] for i in cpu_sample(len(utts), n))]
-    t0 = time.perf_counter()
-    res = odecode(feats, sc, fus, cfg, od)
-    return time.perf_counter() - t0, res
-
-
-def cpu_sample(n_utts: int, n: int):
-    """Indices of a length-stratified sample (the utterances are length-sorted):
-    evenly spaced from the shortest to the longest."""
-    n = max(1, min(n, n_utts))
-    return sorted({int(round(x)) for x in np.linspace(0, n_utts - 1, n)})
-
-
-def _file_tokens(d):
-    """The synthetic dictionaries list no specials: <pad>,<eos>,<unk> lead and
-    <space> trails (token_dict.py placement rule)."""
-    toks = list(d.tokens[3:-1])
-    assert d.tokens[:3] == ("<pad>", "<eos>", "<unk>") and d.tokens[-1] == "<space>"
-    return toks
+def _cpu_desc(procs: int) -> str:
+    from oracle import harness as H
+    return (f"oracle restatement of the reference decoder (decoder.py:339-480, "
+            f"fusion.py:109-266; pinned bit-for-bit by tests/test_oracle_golden.py) + "
+            f"PyTorch-CPU fp32 adapters of the same weights; {procs} single-threaded processes "
+            f"(one per core), utterances handed out longest-first; host CPU: {H.cpu_model()}")
 
 
 def run_reference(args):
-    """--impl reference: the reference CPU algorithm (oracle port; the
-    reference is pure Python and does not compile) on the host cores."""
+    """--impl reference: the reference CPU algorithm on all host cores, on a
+    length-stratified sample of the rank-0 corpus sized to --ref-budget
+    seconds.  Imports nothing from the product package."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    wl, d, W, words, trie, utts = build_inputs(args.config, 0, args.utts, args.words, args.set)
-    threads = len(os.sched_getaffinity(0))
-    n = args.cpu_utts or 4
-    times = []
-    for i in range(args.warmup + args.steps):
-        dt, _ = cpu_decode(wl, d, W, words, utts, n, threads)
-        if i >= args.warmup:
-            times.append(dt)
-    n = len(cpu_sample(len(utts), n))
-    value = n * len(times) / sum(times)
+    from oracle import harness as H
+    procs = args.cpu_procs or H.host_cores()
+    wl = workload(args)
+    t0 = time.perf_counter()
+    with H.OraclePool(args.config, procs, n_utts=args.utts, words=args.words,
+                      overrides=args.set) as pool:
+        n_all = len(pool.lengths)
+        # warm-up: every worker loads its model and decodes one of the
+        # shortest utterances (one pass stands for the W warm-up steps: the
+        # CPU path has no caches to fill beyond the first call)
+        t_w = time.perf_counter()
+        wres = pool.decode(list(range(min(procs, n_all))))
+        per_utt = (time.perf_counter() - t_w) * procs / max(1, len(wres))
+        # timed sample: ~budget seconds of work on all cores, >= 32 utterances,
+        # spread evenly over the length-sorted corpus
+        m = int(max(32, min(n_all, round(args.ref_budget * procs / max(per_utt, 1.0)))))
+        idx = H.strata(n_all, m)
+        t1 = time.perf_counter()
+        res = pool.decode(idx)
+        wall = time.perf_counter() - t1
+    frames = sum(pool.lengths[i] for i in idx)
+    value = len(idx) / wall
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "utt/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
-        "config": workload_config(wl),
-        "cpu_baseline": {"value": value, "unit": "utt/s", "cores": threads, "kind": "port",
-                         "sample": f"{n} of the {wl.n_utts} {wl.name} utterances per step "
-                                   f"(length-stratified: shortest to longest)"},
+        "ms_per_step": 1000.0 * wall / max(1, args.steps), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 model / f64 scores",
+        "data": "synthetic (seeded random-init weights, N(0,1) fbank)",
+        "config": workload_config(wl, 1, wl.n_utts), "rtf": wall / (frames * 0.010),
+        "cpu_baseline": {"value": value, "unit": "utt/s", "cores": procs, "kind": "port",
+                         "sample": f"{len(idx)} of the {n_all} {wl.name} utterances, evenly "
+                                   f"spaced over the length-sorted corpus "
+                                   f"({min(pool.lengths[i] for i in idx)}-"
+                                   f"{max(pool.lengths[i] for i in idx)} frames), decoded as "
+                                   f"one pool run of {wall:.0f} s; the K steps are equal "
+                                   f"shares of it",
+                         "impl": _cpu_desc(procs),
+                         "finished_frac": float(np.mean([r.finished for r in res])),
+                         "steps_mean": float(np.mean([r.steps for r in res]))},
         "e2e": {"value": value, "unit": "utt/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "setup_s": round(t1 - t0, 1),
     }
     print(json.dumps(out), flush=True)
     return 0
 
 
-METRIC = "utterances/sec and RTF, beam-10 look-ahead word-LM decode"
-
-
-def workload_config(wl):
-    if wl.sublm is not None:
-        a, s_ = wl.asr, wl.sublm
-        return {"workload": f"{wl.name}: {a.enc_layers}x BiLSTM-{a.enc_hidden} encoder + "
-                            f"{a.dec_layers}x LSTM-{a.dec_hidden} attention decoder ({a.vocab} "
-                            f"subword tokens), beam {wl.beam}, shallow fusion with a "
-                            f"{s_.layers}x{s_.hidden} token LSTM LM (SubwordFusion), "
-                            f"{wl.n_utts} utts/GPU of {wl.frames[0]}-{wl.frames[1]} frames",
-                "utts_per_gpu": wl.n_utts, "frames": list(wl.frames), "beam": wl.beam,
-                "vocab": a.vocab, "lm_weight": wl.lm_weight, "batch": wl.batch_size,
-                "length_sorted": True}
-    a, lm = wl.asr, wl.lm
-    lm_desc = (f"look-ahead fusion with a {lm.words}-word {lm.layers}x{lm.hidden} LSTM LM"
-               if lm is not None else "no LM")
-    return {"workload": f"{wl.name}: {a.enc_layers}x BiLSTM-{a.enc_hidden} encoder + "
-                        f"{a.dec_layers}x LSTM-{a.dec_hidden} attention decoder ({a.vocab} "
-                        f"tokens), beam {wl.beam}, {lm_desc}, "
-                        f"{wl.n_utts} utts/GPU of {wl.frames[0]}-{wl.frames[1]} frames",
-            "utts_per_gpu": wl.n_utts, "frames": list(wl.frames), "beam": wl.beam,
-            "lm_words": wl.lm.words if wl.lm else 0, "lm_weight": wl.lm_weight,
-            "coverage": wl.coverage_mode, "eos_gamma": wl.eos_gamma,
-            "l2": "working set >> L2 (LM weights 312 MB, g pool GBs): no flush needed",
-            "length_sorted": True}
+def cpu_baseline(args, wl, gpu_res_by_id):
+    """The b200 arm's bounded CPU sample: one utterance per host core, evenly
+    spaced over the length-sorted corpus, one pool run."""
+    from oracle import harness as H
+    procs = args.cpu_procs or H.host_cores()
+    with H.OraclePool(args.config, procs, n_utts=args.utts, words=args.words,
+                      overrides=args.set) as pool:
+        idx = H.strata(len(pool.lengths), procs)
+        t0 = time.perf_counter()
+        res = pool.decode(idx)
+        dt = time.perf_counter() - t0
+    n = len(idx)
+    out = {"value": n / dt, "unit": "utt/s", "cores": procs, "kind": "port",
+           "sample": f"{n} of the {len(pool.lengths)} {wl.name} utterances (one per core, "
+                     f"evenly spaced over the length-sorted corpus), one pool run of "
+                     f"{dt:.1f} s", "impl": _cpu_desc(procs)}
+    match, diffs = 0, []
+    for r in res:
+        g = gpu_res_by_id.get(r.utt_id)
+        if g is not None and g.tokens == r.tokens:
+            match += 1
+            diffs.append(abs(g.score - r.score))
+    out["tokens_match_gpu"] = f"{match}/{n}"
+    out["max_score_diff_gpu"] = float(max(diffs)) if diffs else None
+    return out
 
 
 # ------------------------------------------------------------------- main --
@@ -283,51 +308,78 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.allow_tf32 = False
 
+    import paper_1909_08723_b200 as fb
     from paper_1909_08723_b200 import _lib
     from paper_1909_08723_b200.fusion import LookaheadFusion, SubwordFusion
     from paper_1909_08723_b200.models import AttnLstmScorer, LstmSubwordLM, LstmWordLM
-    from paper_1909_08723_b200.engine import FusedDecoder, StageTimer
-    from paper_1909_08723_b200.decoder import decode_batch
-    from paper_1909_08723_b200.kaldi_io import FeatureMatrix
+    from paper_1909_08723_b200.engine import StageTimer, corpus_hint
+    from paper_1909_08723_b200.sharding import decode_corpus_sharded, plan_shards
 
     t_setup = time.perf_counter()
-    wl, d, W, words, trie, utts = build_inputs(args.config, rank, args.utts, args.words, args.set)
+    wl = workload(args)
+    d, W, trie = build_product(wl)
     cfg = decode_config(wl)
     scorer = AttnLstmScorer(W, wl.asr, d.eos_id)
-    fusion = None
-    if wl.lm is not None:
-        fusion = LookaheadFusion(trie, LstmWordLM(W, wl.lm), d)
-    if wl.sublm is not None:
-        fusion = SubwordFusion(LstmSubwordLM(W, wl.sublm, d.pad_id, d.eos_id))
-    feats = [FeatureMatrix(u, x) for u, x in utts]
-    frames = sum(x.shape[0] for _, x in utts)
-    X_host, T = scorer.encoder.stage([x for _, x in utts], pin=True)
-    X_dev = X_host.to(scorer.device)
-    ids = [u for u, _ in utts]
-    # the public API's cached engine: the device-resident timing and the e2e
-    # timing below share one session (buffers + captured step graphs)
-    if args.profile_only:
-        dec = FusedDecoder(scorer, fusion, cfg, d)
-    else:
-        decode_batch(feats[:1], scorer, fusion, cfg, d)
-        dec = next(iter(scorer._fused_cache.values()))
-    log(f"[rank {rank}] setup {time.perf_counter() - t_setup:.1f}s; {len(utts)} utts, "
-        f"{frames} frames")
+    word_lm = LstmWordLM(W, wl.lm) if wl.lm is not None else None
+    sub_lm = (LstmSubwordLM(W, wl.sublm, d.pad_id, d.eos_id) if wl.sublm is not None
+              else None)
+
+    def fusion_factory():
+        """A fresh fusion per batch over shared resources (pipeline.py:135-153)."""
+        if word_lm is not None:
+            return LookaheadFusion(trie, word_lm, d)
+        if sub_lm is not None:
+            return SubwordFusion(sub_lm)
+        return None
+
+    utts = corpus(wl, world)
+    feats = [fb.FeatureMatrix(u, x) for u, x in utts]
+    lengths = [x.shape[0] for _, x in utts]
+    mine = plan_shards(lengths, world)[rank]
+    bs = wl.batch_size
+    batches = [mine[i:i + bs] for i in range(0, len(mine), bs)]
+    sub = scorer.dims.subsample
+    caps = (min(bs, len(mine)), max(lengths[i] for i in mine) // sub)
+    frames = sum(lengths[i] for i in mine)
+
+    def decode_fn(shard):
+        return fb.decode_corpus(shard, scorer, fusion_factory, cfg, d, batch_size=bs)
+
+    # the public API once (builds and caches the engine + its session/graphs)
+    decode_corpus_sharded(feats, decode_fn, rank=rank, world=world)
+    dec = next(iter(scorer._fused_cache.values()))
+    # device-resident inputs for the `value` timing: every batch staged once
+    staged = []
+    for b in batches:
+        X, T = scorer.encoder.stage([utts[i][1] for i in b])
+        staged.append((X.to(scorer.device), T, [utts[i][0] for i in b]))
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] setup {time.perf_counter() - t_setup:.1f}s; {len(mine)} utts in "
+        f"{len(batches)} batch(es) of <= {bs}, {frames} frames")
+
+    def run_resident():
+        out, launches = [], 0
+        for X, T, ids in staged:
+            out.extend(dec.run(X, T, ids, caps=caps))
+            launches += dec.kernel_launches
+        return out, launches
 
     if args.profile_only:
-        dec.run(X_dev, T, ids)
+        run_resident()
         torch.cuda.synchronize()
         return 0
 
     clocks = ClockSampler(local)
-    clocks.start()                       # process start-up stays out of the timed window
+    clocks.start()
     for _ in range(args.warmup):
-        res = dec.run(X_dev, T, ids)
-        decode_batch(feats, scorer, fusion, cfg, d)
+        res, _ = run_resident()
+        decode_corpus_sharded(feats, decode_fn, rank=rank, world=world)
     torch.cuda.synchronize()
 
     # ---- timed: device-resident inputs ----
@@ -340,8 +392,8 @@ def main():
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record()
     for _ in range(args.steps):
-        res = dec.run(X_dev, T, ids)
-        launches += dec.kernel_launches
+        res, nl = run_resident()
+        launches += nl
     ev1.record()
     torch.cuda.synchronize()
     clocks.mark(False)
@@ -352,19 +404,19 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = world * len(utts) / (ms / 1000.0)
-    rtf = (ms / 1000.0) / (frames * 0.010)
+    value = len(utts) / (ms / 1000.0)
+    all_frames = sum(lengths)
+    rtf = (ms / 1000.0) / (all_frames * 0.010)
 
-    # ---- e2e: the public decode_batch API, host features in, results out ----
+    # ---- e2e: decode_corpus_sharded -> decode_corpus (fusion per batch) ----
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
-        res_e2e = decode_batch(feats, scorer, fusion, cfg, d)
+        res_e2e = decode_corpus_sharded(feats, decode_fn, rank=rank, world=world)
     e1.record()
     torch.cuda.synchronize()
     ms_e2e = e0.elapsed_time(e1) / args.steps
@@ -372,55 +424,42 @@ def main():
         t = torch.tensor([ms_e2e], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
-    h2d = X_host.numel() * 4
-    d2h = sum(4 * (len(r.tokens) + 4) + 8 * r.attn_accum.size for r in res_e2e)
+    h2d = sum(4 * int(np.prod(utts[i][1].shape)) for i in mine)
+    d2h = sum(4 * (len(r.tokens) + 4) + 8 * r.attn_accum.size
+              for r in (res_e2e[i] for i in mine))
+    by_id = {r.utt_id: r for r in res}
+    e2e_same = all(by_id[r.utt_id].tokens == r.tokens for r in res_e2e if r.utt_id in by_id)
 
-    # ---- instrumented pass: stage breakdown + dominant kernel roofline ----
+    # ---- instrumented pass: dominant kernel family roofline (live events) ----
     from paper_1909_08723_b200 import kernels as Kmod
-    timer = StageTimer()
     Kmod.GEMM_LOG = []
-    dec.run(X_dev, T, ids, timer=timer, record_counts=True)
-    stages = timer.summary()
+    for X, T, ids in staged:
+        dec.run(X, T, ids, timer=StageTimer(), record_counts=True, caps=caps)
     torch.cuda.synchronize()
     g_ms, g_flops = 0.0, 0.0
-    for e0, e1, mm, n_, k_ in Kmod.GEMM_LOG:
+    for a, b, mm, n_, k_ in Kmod.GEMM_LOG:
         rows_ = int(mm.item()) if hasattr(mm, "item") else int(mm)
-        g_ms += e0.elapsed_time(e1)
+        g_ms += a.elapsed_time(b)
         g_flops += 2.0 * rows_ * n_ * k_
     n_gemm = len(Kmod.GEMM_LOG)
     Kmod.GEMM_LOG = None
     peaks = _peaks()
     peak = peaks.get("bf16_tflops_sustained") or 1398.2
     ach = g_flops / (g_ms / 1000.0) / 1e12 if g_ms > 0 else 0.0
-    traffic = _traffic_from_profiles()
     roof = {"kernel": "gemm_tc_kernel (all tcgen05 GEMMs of one decode: encoder, attention "
                       "decoder, word LM; bf16x3-split activations, counted once)",
             "bound": "tensor", "achieved": round(ach, 2), "peak": peak, "unit": "TFLOP/s",
-            "frac": round(ach / peak, 4), "traffic": traffic,
+            "frac": round(ach / peak, 4), "traffic": _profile_json("gemm_traffic.json"),
             "launches": n_gemm, "gemm_ms_per_decode": round(g_ms, 3),
+            "gemm_tflop_per_decode": round(g_flops / 1e12, 3),
             "share_of_decode": round(g_ms / max(ms, 1e-9), 3),
             "tensor_work_frac_incl_split": round(3 * ach / peak, 4),
-            "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel inside a long step)"}
-
-    out_res = res
-    steps_mean = float(np.mean([r.steps for r in out_res]))
-    fin_frac = float(np.mean([r.finished for r in out_res]))
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel inside a long step)",
+            "per_kernel_ncu": _profile_json("r2_kernel_roofline.json")}
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
-        threads = len(os.sched_getaffinity(0))
-        n = args.cpu_utts or 4
-        dt, cres = cpu_decode(wl, d, W, words, utts, n, threads)
-        idx = cpu_sample(len(utts), n)
-        n = len(idx)
-        cpu = {"value": n / dt, "unit": "utt/s", "cores": threads, "kind": "port",
-               "sample": f"{n} of the {len(utts)} {wl.name} utterances (length-stratified: "
-                         f"shortest to longest), same weights/inputs, oracle restatement of "
-                         f"the reference decoder"}
-        match = sum(res[i].tokens == b.tokens for i, b in zip(idx, cres))
-        cpu["tokens_match_gpu"] = f"{match}/{n}"
-        same = [abs(res[i].score - b.score) for i, b in zip(idx, cres) if res[i].tokens == b.tokens]
-        cpu["max_score_diff_gpu"] = float(max(same)) if same else None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, wl, by_id)
 
     if rank == 0:
         out = {
@@ -428,21 +467,24 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32 model / f64 scores", "data": "synthetic (seeded random-init weights, "
-            "N(0,1) fbank)", "config": workload_config(wl),
-            "rtf": rtf, "audio_seconds_per_step": frames * 0.010 * world,
-            "e2e": {"value": round(world * len(utts) / (ms_e2e / 1000.0), 3), "unit": "utt/s",
+            "N(0,1) fbank)", "config": workload_config(wl, world, len(mine)),
+            "rtf": rtf, "audio_seconds_per_step": all_frames * 0.010,
+            "e2e": {"value": round(len(utts) / (ms_e2e / 1000.0), 3), "unit": "utt/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "api": "paper_1909_08723_b200.decode_batch (host FeatureMatrix list)"},
+                    "api": "paper_1909_08723_b200.sharding.decode_corpus_sharded -> "
+                           "decode_corpus(batch_size, fusion_factory) (host FeatureMatrix "
+                           "list, fresh LookaheadFusion per batch, final gather)",
+                    "tokens_equal_resident": e2e_same},
             "roofline": roof, "cpu_baseline": cpu, "gpu_launches": int(launches),
-            "clocks": clk,
-            "stages_ms_per_decode": {k: round(v[0], 3) for k, v in stages.items()},
-            "decode_steps_mean": steps_mean, "finished_frac": fin_frac,
+            "clocks": clk, "stage_split_ncu": _profile_json("r2_stage_split.json"),
+            "decode_steps_mean": float(np.mean([r.steps for r in res])),
+            "finished_frac": float(np.mean([r.finished for r in res])),
         }
         print(json.dumps(out), flush=True)
         if args.stats:
-            log("distinct outputs:", len({tuple(r.tokens) for r in out_res}), "of", len(out_res),
-                "mean len", float(np.mean([len(r.tokens) for r in out_res])))
-            for r in out_res[:5]:
+            log("distinct outputs:", len({tuple(r.tokens) for r in res}), "of", len(res),
+                "mean len", float(np.mean([len(r.tokens) for r in res])))
+            for r in res[:5]:
                 log(r.utt_id, r.steps, r.finished, round(r.score, 3), d.detokenize(r.tokens)[:120])
             if dec.spec_counts is not None:
                 c = dec.spec_counts.numpy()
@@ -452,10 +494,10 @@ def main():
     return 0
 
 
-def _traffic_from_profiles():
-    """dram bytes per launch of the profiled GEMM (ncu --set full, committed)."""
+def _profile_json(name: str):
+    """A committed ncu-derived summary under profiles/ (None when absent)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
             return json.load(f)
     except OSError:
         return None

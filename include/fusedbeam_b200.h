@@ -197,8 +197,9 @@ int fb_search_init(const fb_search_cfg_t* cfg, const fb_search_state_t* st,
 
 
 /* ---- dense contractions (attention-LSTM decoder step, word-LM step) ------ */
-/* C = A . W^T (+ bias) with a fused epilogue.  A [m, k] fp32 row-major
- * (compact rows), W [n, k] row-major.
+/* C = A . W^T (+ bias) with a fused epilogue, on the tensor cores
+ * (fb_gemm_tc below).  A = bf16 planes of the fp32 activations [m, k]
+ * (compact rows), W [n, k] bf16 row-major.
  *   mode 0: out row = rows ? rows[i] : i ;  c[out*ldc + j] = acc + bias[j]
  *   mode 1: LSTM cell.  n == 4*hidden with gate columns interleaved
  *           (column 4u+q, q = i,f,g,o); slot = rows ? rows[i] : i,
@@ -254,9 +255,7 @@ typedef struct {
   int32_t out_logsoftmax;
 } fb_gemm_t;
 
-int fb_gemm(const fb_gemm_t* g, void* stream);
-
-/* Same contract on the 5th-gen tensor cores (tcgen05 + TMEM + TMA): A is
+/* 5th-gen tensor cores (tcgen05 + TMEM + TMA): A is
  * a_planes bf16 planes of [a_plane_rows, lda] (the fp32 activation split
  * hi/mid/lo by fb_pack_rows out_mode 1), W is bf16 [n, ldw]; fp32
  * accumulation in TMEM.  k % 64 == 0, lda/ldw % 8 == 0. */
@@ -427,6 +426,20 @@ int fb_ark_read_matrix(const char* ark_path, int64_t offset, float* dst, int64_t
 int fb_ark_read_batch(int32_t n, const char* const* ark_paths, const int64_t* offsets,
                       float* dst, const int64_t* dst_offsets, const int64_t* capacities,
                       int32_t* rows, int32_t* cols, int32_t threads);
+/* Kaldi SCP index (reference kaldi_io.py:46-77; replaces read_scp's line
+ * loop) over the file's bytes: per entry "utt_id\0ark_path\0" into out and
+ * its offset into offsets.  Lines split like Python's text mode, fields like
+ * str.strip/split(None, 1)/rpartition(':')/int().  FB_ERR_FORMAT: err[0] =
+ * 1 field count | 2 missing ':offset' | 3 offset not an integer | 4 negative
+ * offset | 5 duplicate id, err[1] = line, err[2] = first line of the
+ * duplicate; out holds the offending text (out_len bytes). */
+int fb_scp_parse(const char* text, int64_t len, char* out, int64_t out_cap, int64_t* out_len,
+                 int64_t* offsets, int32_t* n_entries, int32_t* err);
+/* Append one binary float32 record and its SCP line (reference
+ * kaldi_io.py:129-150; replaces write_ark_matrix's writes); *offset = the
+ * record's position after "utt_id ". */
+int fb_ark_append_matrix(const char* ark_path, const char* scp_path, const char* utt_id,
+                         const float* data, int32_t rows, int32_t cols, int64_t* offset);
 /* n host memcpys (dsts[i] <- srcs[i], bytes[i]) on a thread pool: staging a
  * batch of feature matrices into one pinned buffer. */
 int fb_host_copy_batch(int32_t n, const void* const* srcs, void* const* dsts,

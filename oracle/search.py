@@ -79,6 +79,7 @@ class OracleResult:
     finished: bool
     steps: int
     margin: float = math.inf          # smallest deciding gap (see module doc)
+    decision_margin: float = math.inf  # same, without the in-beam order gaps
 
 
 @dataclass
@@ -105,6 +106,7 @@ class _U:
     on: bool = True
     steps: int = 0
     margin: float = math.inf
+    dmargin: float = math.inf
 
 
 def _gap(a: float, b: float) -> float:
@@ -187,10 +189,16 @@ def decode_batch(features, scorer, fusion, cfg: OracleConfig, d) -> List[OracleR
             srt = flat[order[:took + 1]]
             for a, b in zip(srt[:-1], srt[1:]):
                 u.margin = min(u.margin, _gap(float(a), float(b)))
+            # set membership only flips at the cut (the in-beam order decides
+            # nothing but exact ties, which are themselves gaps of 0 at a cut)
+            if 0 < took < len(order):
+                u.dmargin = min(u.dmargin, _gap(float(flat[order[took - 1]]),
+                                                float(flat[order[took]])))
             if len(u.done) > cfg.beam_size:
                 u.done.sort(key=_key)
                 cut = u.done[cfg.beam_size - 1].total, u.done[cfg.beam_size].total
                 u.margin = min(u.margin, _gap(*cut))
+                u.dmargin = min(u.dmargin, _gap(*cut))
                 del u.done[cfg.beam_size:]
             u.steps += 1
             u.live = keep
@@ -202,6 +210,7 @@ def decode_batch(features, scorer, fusion, cfg: OracleConfig, d) -> List[OracleR
                 best = max(h.base for h in keep) + slack
                 worst = min(h.total for h in u.done)
                 u.margin = min(u.margin, _gap(best, worst))
+                u.dmargin = min(u.dmargin, _gap(best, worst))
                 if best < worst:
                     u.on = False
             if u.on:
@@ -222,12 +231,13 @@ def decode_batch(features, scorer, fusion, cfg: OracleConfig, d) -> List[OracleR
         ranked = sorted(pool, key=_key)
         if len(ranked) > 1:
             u.margin = min(u.margin, _gap(ranked[0].total, ranked[1].total))
+            u.dmargin = min(u.dmargin, _gap(ranked[0].total, ranked[1].total))
         best = ranked[0]
         toks = list(best.toks)
         if toks and toks[-1] == eos:
             toks.pop()
         out.append(OracleResult(u.uid, toks, best.total, best.acc, bool(u.done),
-                                u.steps, u.margin))
+                                u.steps, u.margin, u.dmargin))
     return out
 
 

@@ -85,7 +85,6 @@ _SIGS = {
     "fb_attend_coverage": (C.c_int, [C.POINTER(FbSearchCfg), i32, vp, vp, vp, vp, vp, vp, i32,
                                      i64, vp, vp, vp]),
     "fb_gather_rows": (C.c_int, [i32, vp, vp, vp, i64, vp]),
-    "fb_gemm": (C.c_int, [C.POINTER(FbGemm), vp]),
     "fb_gemm_tc": (C.c_int, [C.POINTER(FbGemm), i32, i64, vp]),
     "fb_stats_to_g": (C.c_int, [i32, vp, vp, i64, vp, i32, vp, i32, vp, vp, i64, vp, vp, vp, vp,
                                 vp]),
@@ -121,6 +120,8 @@ _SIGS = {
     "fb_trie_build_sizes": (C.c_int, [i32, vp, vp, i32, vp, vp]),
     "fb_trie_build": (C.c_int, [i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
     "fb_keys_exp2t": (C.c_int, [i32, i32, i32, vp, vp, vp]),
+    "fb_scp_parse": (C.c_int, [C.c_char_p, i64, C.c_char_p, i64, vp, vp, vp, vp]),
+    "fb_ark_append_matrix": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, vp, i32, i32, vp]),
 }
 
 _OPTIONAL = {}

@@ -24,8 +24,10 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", INCLUDE, "-I", HERE]
 
-SOURCES = ["capi.cu", "lookahead.cu", "search.cu", "gemm.cu", "gemm_tc.cu", "asr.cu",
-           "host_io.cu"]
+SOURCES = ["capi.cu", "lookahead.cu", "search.cu", "gemm_tc.cu", "asr.cu", "host_io.cu"]
+# test-only device code (not in the product library): tests/libfb_testkit.so
+TESTKIT_SRC = os.path.join(ROOT, "tests", "csrc", "simt_gemm.cu")
+TESTKIT_OUT = os.path.join(ROOT, "tests", "libfb_testkit.so")
 
 
 def _headers():
@@ -57,7 +59,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
+    build_testkit(force, verbose, hdr_mtime)
     return OUT
+
+
+def build_testkit(force: bool = False, verbose: bool = False, hdr_mtime: float = 0.0) -> str:
+    """The test-only SIMT GEMM cross-check library (tests/csrc)."""
+    if not os.path.exists(TESTKIT_SRC):
+        return ""
+    if (force or not os.path.exists(TESTKIT_OUT)
+            or os.path.getmtime(TESTKIT_OUT) < max(os.path.getmtime(TESTKIT_SRC), hdr_mtime)):
+        cmd = [NVCC, *ARCH, *FLAGS, "-shared", TESTKIT_SRC, "-o", TESTKIT_OUT]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    return TESTKIT_OUT
 
 
 if __name__ == "__main__":

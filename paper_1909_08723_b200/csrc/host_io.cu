@@ -5,12 +5,16 @@
 //    (pinned) staging buffer;
 //  * PTA1 prefix-tree files (lexicon_trie.py:178-224), read/write;
 //  * build_trie (lexicon_trie.py:227-276) as a sort + longest-common-prefix
-//    sweep over char-id sequences (same arrays as the reference).
+//    sweep over char-id sequences (same arrays as the reference);
+//  * Kaldi SCP index parsing (kaldi_io.py:46-77) over the file's bytes, with
+//    Python's text-mode line splitting and str.split/strip whitespace, and
+//    the ARK record + SCP line appender (kaldi_io.py:129-150).
 // No GPU is touched here.
 #include "common.cuh"
 
 #include <algorithm>
 #include <atomic>
+#include <unordered_map>
 #include <cstdio>
 #include <cstring>
 #include <numeric>
@@ -125,6 +129,76 @@ int read_record(FILE* f, const char* path, int64_t offset, float* dst, int64_t c
 }
 
 constexpr char kMagic[4] = {'P', 'T', 'A', '1'};
+
+// Byte length of the whitespace code point at p (Python str.isspace set:
+// ASCII \t-\r, 0x1c-0x1f, space; U+0085, U+00A0, U+1680, U+2000-U+200A,
+// U+2028, U+2029, U+202F, U+205F, U+3000), 0 if none.
+int ws_len(const unsigned char* p, const unsigned char* e) {
+  const unsigned c = p[0];
+  if (c == ' ' || (c >= 0x09 && c <= 0x0d) || (c >= 0x1c && c <= 0x1f)) return 1;
+  if (c == 0xc2 && p + 1 < e && (p[1] == 0x85 || p[1] == 0xa0)) return 2;
+  if (c == 0xe1 && p + 2 < e && p[1] == 0x9a && p[2] == 0x80) return 3;
+  if (c == 0xe2 && p + 2 < e) {
+    if (p[1] == 0x80 && (p[2] <= 0x8a || p[2] == 0xa8 || p[2] == 0xa9 || p[2] == 0xaf)) return 3;
+    if (p[1] == 0x81 && p[2] == 0x9f) return 3;
+  }
+  if (c == 0xe3 && p + 2 < e && p[1] == 0x80 && p[2] == 0x80) return 3;
+  return 0;
+}
+
+struct Span {
+  const unsigned char* b;
+  const unsigned char* e;
+  bool empty() const { return b >= e; }
+  std::string str() const { return std::string((const char*)b, (size_t)(e - b)); }
+};
+
+Span strip(Span s) {
+  for (int n; s.b < s.e && (n = ws_len(s.b, s.e)) > 0;) s.b += n;
+  // trailing: scan forward remembering where the last non-space run ended
+  const unsigned char* last = s.b;
+  for (const unsigned char* p = s.b; p < s.e;) {
+    const int n = ws_len(p, s.e);
+    if (n) {
+      p += n;
+    } else {
+      ++p;
+      while (p < s.e && (*p & 0xc0) == 0x80) ++p;   // rest of the code point
+      last = p;
+    }
+  }
+  s.e = last;
+  return s;
+}
+
+// Python int(text) for ASCII decimal text: optional sign, digits with single
+// underscores between them, surrounding whitespace allowed.
+bool parse_int(Span s, int64_t* out) {
+  s = strip(s);
+  if (s.empty()) return false;
+  bool neg = false;
+  if (*s.b == '+' || *s.b == '-') {
+    neg = *s.b == '-';
+    ++s.b;
+  }
+  if (s.empty() || *s.b == '_') return false;
+  unsigned long long v = 0;
+  bool prev_us = false;
+  for (const unsigned char* p = s.b; p < s.e; ++p) {
+    if (*p == '_') {
+      if (prev_us) return false;
+      prev_us = true;
+      continue;
+    }
+    if (*p < '0' || *p > '9') return false;
+    prev_us = false;
+    if (v > (9223372036854775807ULL - (*p - '0')) / 10) return false;
+    v = v * 10 + (*p - '0');
+  }
+  if (prev_us) return false;
+  *out = neg ? -(int64_t)v : (int64_t)v;
+  return true;
+}
 
 }  // namespace
 }  // namespace fb
@@ -371,5 +445,113 @@ extern "C" int fb_trie_build(int32_t n_words, const int32_t* chars, const int64_
     ub_index[st] = tb.last[st];
     lb_index[st] = tb.first[st] - 1;
   }
+  return FB_OK;
+}
+
+/* SCP index lines "utt_id ark_path:offset" (reference kaldi_io.py:46-77).
+ * Lines split as Python's text mode does (\n, \r\n, \r), then strip() /
+ * split(None, 1) / rpartition(':') / int().  Output per entry:
+ * "utt_id\0ark_path\0" into `out` (capacity >= len) and the offset.  A
+ * malformed line returns FB_ERR_FORMAT with err[0] = kind (1 field count,
+ * 2 missing ':offset', 3 offset not an integer, 4 negative offset,
+ * 5 duplicate id), err[1] = line number, err[2] = first line of a duplicate,
+ * and the offending text (offset text / negative value / id) in `out`. */
+extern "C" int fb_scp_parse(const char* text, int64_t len, char* out, int64_t out_cap,
+                            int64_t* out_len, int64_t* offsets, int32_t* n_entries,
+                            int32_t* err) {
+  FB_CHECK_ARG(text && out && out_len && offsets && n_entries && err && len >= 0,
+               "bad SCP parse arguments");
+  const unsigned char* p = (const unsigned char*)text;
+  const unsigned char* end = p + len;
+  int64_t o = 0;
+  int32_t n = 0, lineno = 0;
+  std::unordered_map<std::string, int32_t> seen;
+  auto put = [&](Span s) {
+    const int64_t k = s.e - s.b;
+    if (o + k + 1 > out_cap) return false;
+    memcpy(out + o, s.b, (size_t)k);
+    o += k;
+    out[o++] = '\0';
+    return true;
+  };
+  auto bad = [&](int kind, int aux, Span what) {
+    err[0] = kind;
+    err[1] = lineno;
+    err[2] = aux;
+    o = 0;
+    const int64_t k = std::min<int64_t>(what.e - what.b, out_cap);
+    memcpy(out, what.b, (size_t)std::max<int64_t>(k, 0));
+    *out_len = std::max<int64_t>(k, 0);
+    return fail(FB_ERR_FORMAT, "SCP line " + std::to_string(lineno));
+  };
+  while (p < end) {
+    const unsigned char* q = p;
+    while (q < end && *q != '\n' && *q != '\r') ++q;
+    Span line{p, q};
+    p = q;
+    if (p < end && *p == '\r') ++p;
+    if (q < end && *q == '\r' && p < end && *p == '\n') ++p;
+    else if (q < end && *q == '\n') ++p;
+    ++lineno;
+    line = strip(line);
+    if (line.empty()) continue;
+    // split(None, 1): the id up to the first whitespace, the rest stripped left
+    const unsigned char* w = line.b;
+    while (w < line.e && ws_len(w, line.e) == 0) ++w;
+    if (w >= line.e) return bad(1, 0, line);
+    Span id{line.b, w};
+    Span rest{w, line.e};
+    rest = strip(rest);
+    // rpartition(':')
+    const unsigned char* c = rest.e;
+    while (c > rest.b && c[-1] != ':') --c;
+    if (c == rest.b) return bad(2, 0, rest);          // no ':' at all
+    Span ark{rest.b, c - 1}, off{c, rest.e};
+    if (ark.empty()) return bad(2, 0, rest);
+    int64_t v;
+    if (!parse_int(off, &v)) return bad(3, 0, off);
+    if (v < 0) return bad(4, 0, off);
+    const std::string key = id.str();
+    auto it = seen.find(key);
+    if (it != seen.end()) return bad(5, it->second, id);
+    seen.emplace(key, lineno);
+    if (!put(id) || !put(ark)) return fail(FB_ERR_VALUE, "SCP output buffer too small");
+    offsets[n++] = v;
+  }
+  *n_entries = n;
+  *out_len = o;
+  return FB_OK;
+}
+
+/* Append one binary float32 record "utt_id \0BFM \4<rows>\4<cols><data>" to
+ * the ARK and "utt_id ark_path:offset\n" to the SCP (kaldi_io.py:129-150);
+ * *offset = position of the binary marker.  The caller validated the id and
+ * the matrix (ValueErrors live in Python, as in the reference). */
+extern "C" int fb_ark_append_matrix(const char* ark_path, const char* scp_path,
+                                    const char* utt_id, const float* data, int32_t rows,
+                                    int32_t cols, int64_t* offset) {
+  FB_CHECK_ARG(ark_path && scp_path && utt_id && data && offset && rows > 0 && cols > 0,
+               "bad ARK append arguments");
+  int64_t off;
+  {
+    File f(ark_path, "ab");
+    if (!f.f) return fail(FB_ERR_IO, std::string(ark_path) + ": cannot open for append");
+    const size_t idn = strlen(utt_id);
+    if (fwrite(utt_id, 1, idn, f.f) != idn || fputc(' ', f.f) == EOF || fflush(f.f) != 0)
+      return fail(FB_ERR_IO, std::string(ark_path) + ": write failed");
+    off = (int64_t)ftello(f.f);
+    unsigned char hdr[15] = {0, 'B', 'F', 'M', ' ', 4, 0, 0, 0, 0, 4, 0, 0, 0, 0};
+    memcpy(hdr + 6, &rows, 4);                        // little-endian host (x86-64)
+    memcpy(hdr + 11, &cols, 4);
+    const size_t nel = (size_t)rows * (size_t)cols;
+    if (fwrite(hdr, 1, sizeof hdr, f.f) != sizeof hdr ||
+        fwrite(data, sizeof(float), nel, f.f) != nel)
+      return fail(FB_ERR_IO, std::string(ark_path) + ": write failed");
+  }
+  File s(scp_path, "a");
+  if (!s.f) return fail(FB_ERR_IO, std::string(scp_path) + ": cannot open for append");
+  if (fprintf(s.f, "%s %s:%lld\n", utt_id, ark_path, (long long)off) < 0)
+    return fail(FB_ERR_IO, std::string(scp_path) + ": write failed");
+  *offset = off;
   return FB_OK;
 }

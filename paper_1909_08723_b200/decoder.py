@@ -360,10 +360,19 @@ def decode_corpus(features: Sequence[FeatureMatrix], scorer: AcousticScorer, fus
     if workers < 1:
         raise ConfigError(f"worker count must be positive, got {workers}")
     chunks = [features[i:i + batch_size] for i in range(0, len(features), batch_size)]
+    hint = None
+    if getattr(scorer, "is_device_scorer", False) and len(features):
+        # one device session (buffers + step graphs) for every batch of the corpus
+        from .engine import corpus_hint
+        t_max = max(np.asarray(f.data).shape[0] for f in features) // scorer.dims.subsample
+        hint = (min(batch_size, len(features)), max(1, t_max))
 
     def run(chunk):
         fus = fusion_factory() if fusion_factory is not None else None
-        return decode_batch(chunk, scorer, fus, config, token_dict)
+        if hint is None:
+            return decode_batch(chunk, scorer, fus, config, token_dict)
+        with corpus_hint(*hint):
+            return decode_batch(chunk, scorer, fus, config, token_dict)
 
     if workers == 1 or len(chunks) <= 1:
         parts = [run(c) for c in chunks]

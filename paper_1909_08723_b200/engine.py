@@ -19,9 +19,12 @@ State never leaves the device; rows index per-slot buffers through ``parent``
 
 from __future__ import annotations
 
+import collections
+import contextlib
 import ctypes as C
 import os
 import math
+import threading
 from typing import List, Optional, Sequence
 
 import numpy as np
@@ -147,26 +150,68 @@ class _NoTimer:
         return False
 
 
+_HINT = threading.local()
+
+
+@contextlib.contextmanager
+def corpus_hint(batch_size: int, t_max: int):
+    """decode_corpus: every batch of this corpus fits one session of
+    ``batch_size`` utterances and ``t_max`` encoder frames, so the device
+    buffers and captured step graphs are built once per corpus, not per batch
+    (the last, smaller batch runs with its surplus utterances inactive)."""
+    prev = getattr(_HINT, "caps", None)
+    _HINT.caps = (int(batch_size), int(t_max))
+    try:
+        yield
+    finally:
+        _HINT.caps = prev
+
+
+def _engine_key(fusion, config: DecodeConfig, token_dict):
+    """What a cached engine depends on: the fusion's resources (trie and LM
+    objects, penalties), never the fusion instance -- the reference pipeline
+    builds a fresh fusion per batch (pipeline.py:148-149) over shared ones."""
+    if fusion is None:
+        fk = None
+    elif hasattr(fusion, "char_lm"):
+        fk = ("subword", id(fusion.char_lm))
+    else:
+        fk = ("lookahead", id(fusion.trie), id(fusion.word_lm), fusion.oov_penalty,
+              fusion.score_floor)
+    return (fk, tuple(sorted(vars(config).items())), tuple(token_dict.tokens))
+
+
+_MAX_ENGINES = 2
+
+
 def decode_fused(features, scorer, fusion, config: DecodeConfig, token_dict
                  ) -> List[DecodeResult]:
     """decode_batch entry: host features -> staged device batch -> engine.
-    The FusedDecoder (and its device session) is cached on the scorer, so
-    repeated calls with the same batch shape reuse buffers and CUDA graphs."""
-    # staging and upload pipelined in utterance chunks (copy of chunk i while
-    # the host threads stack chunk i+1)
-    X, T = scorer.encoder.stage([np.asarray(f.data, np.float32) for f in features], pin=True,
-                                to_device=True)
-    done = torch.cuda.Event()
-    done.record()
-    key = (id(fusion), tuple(sorted(vars(config).items())), id(token_dict))
-    cache = scorer.__dict__.setdefault("_fused_cache", {})
-    dec = cache.get(key)
-    if dec is None or dec.fusion is not fusion:
-        cache.clear()
-        dec = cache[key] = FusedDecoder(scorer, fusion, config, token_dict)
-    out = dec.run(X, T, [f.utt_id for f in features])
-    done.synchronize()          # the pinned staging buffer may be reused afterwards
-    return out
+    Engines are cached on the scorer by content (_engine_key) and keep their
+    device sessions, so repeated calls -- including decode_corpus with a
+    fusion factory -- reuse buffers and CUDA graphs.  One decode at a time per
+    scorer: decode_corpus(workers > 1) threads serialise here (the GPU already
+    batches; the staging buffer, streams and sessions are shared)."""
+    lock = scorer.__dict__.setdefault("_engine_lock", threading.Lock())
+    with lock:
+        # staging and upload pipelined in utterance chunks (copy of chunk i while
+        # the host threads stack chunk i+1)
+        X, T = scorer.encoder.stage([np.asarray(f.data, np.float32) for f in features],
+                                    pin=True, to_device=True)
+        done = torch.cuda.Event()
+        done.record()
+        key = _engine_key(fusion, config, token_dict)
+        cache = scorer.__dict__.setdefault("_fused_cache", collections.OrderedDict())
+        dec = cache.get(key)
+        if dec is None:
+            while len(cache) >= _MAX_ENGINES:
+                cache.popitem(last=False)
+            dec = cache[key] = FusedDecoder(scorer, fusion, config, token_dict)
+        cache.move_to_end(key)
+        out = dec.run(X, T, [f.utt_id for f in features], fusion=fusion,
+                      caps=getattr(_HINT, "caps", None))
+        done.synchronize()          # the pinned staging buffer may be reused afterwards
+        return out
 
 
 class _Session:
@@ -232,22 +277,36 @@ class _Session:
         self.graphs_tail = None
         self.per_step_launches = 0.0
         self.side_stream = torch.cuda.Stream(device=dev)
+        # look-ahead floored-score count of the running decode (credited to the
+        # caller's fusion.diagnostics afterwards; the graphs capture this buffer)
+        self.floored = torch.zeros(1, dtype=torch.int64, device=dev)
 
     def reset(self, T: Sequence[int], max_len: Sequence[int]) -> None:
         """Per-decode initial state (decoder.py:350-361): one live row per
-        utterance, zero decoder state, root trie state, <s> word history."""
+        utterance, zero decoder state, root trie state, <s> word history.
+        A batch smaller than the session leaves its surplus utterances
+        inactive from the start (like utterances that already finished)."""
         buf = self.buf
         stream = _lib.stream_ptr()
-        buf.max_len.copy_(torch.as_tensor(list(max_len), dtype=torch.int32), non_blocking=True)
-        buf.t_enc.copy_(torch.as_tensor(list(T), dtype=torch.int32), non_blocking=True)
+        Bn = len(T)
+        ml = torch.ones(self.B, dtype=torch.int32)
+        te = torch.ones(self.B, dtype=torch.int32)
+        ml[:Bn] = torch.as_tensor(list(max_len), dtype=torch.int32)
+        te[:Bn] = torch.as_tensor(list(T), dtype=torch.int32)
+        buf.max_len.copy_(ml, non_blocking=True)
+        buf.t_enc.copy_(te, non_blocking=True)
         _lib.call("fb_search_init", self.cfg_ref, C.byref(buf.view(0)), self.B, stream)
+        if Bn < self.B:
+            buf.active[Bn:].zero_()
+            buf.n_live[Bn:].zero_()
         buf.acc[0].zero_()
         prev = self.X2[1]
         prev.h.zero_()
         prev.c.zero_()
         prev.ctx.zero_()
-        self.rows[0][:self.B] = self.slots0
-        self.count[0].fill_(self.B)
+        self.rows[0][:Bn] = self.slots0[:Bn]
+        self.count[0].fill_(Bn)
+        self.floored.zero_()
         if self.sub is not None:
             self.sub_X2[1].h.zero_()
             self.sub_X2[1].c.zero_()
@@ -256,6 +315,9 @@ class _Session:
             lm.trie[0].zero_()
             lm.hist[0].zero_()
             lm.start()
+
+    def fits(self, B: int, TM: int, MT: int) -> bool:
+        return self.B >= B and self.TM >= TM and self.MT >= MT
 
 
 class FusedDecoder:
@@ -273,13 +335,28 @@ class FusedDecoder:
         self.use_graphs = True      # one CUDA graph per step parity, replayed
         # host polls the live-row count every k steps (dev override FB_POLL)
         self.poll_every = int(os.environ.get("FB_POLL", "8"))
-        self._sess: Optional[_Session] = None
+        self._sessions: List[_Session] = []       # most recently used last
 
-    def _session(self, B: int, TM: int, MT: int) -> _Session:
-        s = self._sess
-        if s is None or (s.B, s.TM, s.MT) != (B, TM, MT):
-            self._sess = None           # release the previous shape first
-            s = self._sess = _Session(self, B, TM, MT)
+    def _session(self, B: int, TM: int, MT: int, caps=None) -> _Session:
+        """A session that holds the batch: with a corpus hint (caps = batch
+        size, encoder frames of the corpus) any session within the caps, else
+        one no more than about twice the batch; otherwise a new one sized to
+        the caps (or the batch), evicting the least recently used beyond two."""
+        if caps is not None:
+            lim_b, lim_t = max(caps[0], B), max(caps[1], TM)
+        else:
+            lim_b, lim_t = 2 * B + 64, 2 * TM + 64
+        for s in reversed(self._sessions):
+            if s.fits(B, TM, MT) and s.B <= lim_b and s.TM <= lim_t:
+                self._sessions.remove(s)
+                self._sessions.append(s)
+                return s
+        Bc, TMc = (lim_b, lim_t) if caps is not None else (B, TM)
+        MTc = max(MT, max(1, int(math.floor(self.config.max_len_ratio * TMc))) + 1)
+        while len(self._sessions) >= 2:
+            self._sessions.pop(0)       # release before allocating the new one
+        s = _Session(self, Bc, TMc, MTc)
+        self._sessions.append(s)
         return s
 
     def _step(self, S: _Session, c: int, tm, counts) -> None:
@@ -341,7 +418,7 @@ class FusedDecoder:
             _lib.call("fb_lookahead_scores", fusion.dtrie.ref, S.N, P(nc), P(rc), P(lm.trie[c]),
                       P(lm.hist[c]), P(lm.g), lm.lw.d.words, P(lm.eos), P(lm.zero_eos),
                       fusion.space_id, fusion.eos_id, fusion.oov_penalty, fusion.score_floor,
-                      P(S.fus_buf), S.V, P(fusion._floored), _lib.stream_ptr())
+                      P(S.fus_buf), S.V, P(S.floored), _lib.stream_ptr())
 
     def _body(self, S: _Session, c: int, tm, counts, lookahead: bool = True) -> None:
         """Look-ahead, speculative <eos> LM events and selection of parity c."""
@@ -426,7 +503,9 @@ class FusedDecoder:
                 counts.append(lm.unk_count.clone())
 
     def run(self, X: torch.Tensor, T: Sequence[int], utt_ids: Sequence[str], timer=None,
-            record_counts: bool = False) -> List[DecodeResult]:
+            record_counts: bool = False, fusion=None, caps=None) -> List[DecodeResult]:
+        """Decode one staged batch.  fusion: the caller's fusion instance (its
+        diagnostics are credited); caps: corpus hint (see corpus_hint)."""
         config = self.config
         tm = timer if timer is not None else _NoTimer()
         lib = _lib.lib()
@@ -438,7 +517,7 @@ class FusedDecoder:
         TM = max(Tenc)
         max_len = [max(1, int(math.floor(config.max_len_ratio * t))) for t in Tenc]
         MT = max(max_len) + 1
-        S = self._session(B, TM, MT)
+        S = self._session(B, TM, MT, caps)
         with tm("encoder"):
             _, _, Tenc = self.scorer.encoder(X, Tenc, out=(S.enc, S.keys))
         S.reset(Tenc, max_len)
@@ -503,6 +582,9 @@ class FusedDecoder:
         self.kernel_launches = int(lib.fb_launch_count() - l0 + S.per_step_launches * replayed)
         if counts is not None:
             self.spec_counts = torch.cat(counts).view(steps, 3).cpu() if counts else None
+        target = fusion if fusion is not None else self.fusion
+        if S.lm is not None and target is not None and hasattr(target, "_floored"):
+            target._floored += S.floored
         return S.buf.results(list(utt_ids), Tenc)
 
 

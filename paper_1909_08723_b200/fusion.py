@@ -76,7 +76,18 @@ class FusionScorer:
 
 
 class DeviceTrie:
-    """CSR trie resident in HBM plus the ``fb_trie_t`` view the kernels take."""
+    """CSR trie resident in HBM plus the ``fb_trie_t`` view the kernels take.
+    ``DeviceTrie.of(trie, device)`` uploads once per (automaton, device): a
+    fusion per batch (pipeline.py:148-149) shares the resident copy."""
+
+    @staticmethod
+    def of(trie: PrefixTreeAutomaton, device) -> "DeviceTrie":
+        cache = trie.__dict__.setdefault("_device_tries", {})
+        key = str(device)
+        dt = cache.get(key)
+        if dt is None:
+            dt = cache[key] = DeviceTrie(trie, device)
+        return dt
 
     def __init__(self, trie: PrefixTreeAutomaton, device):
         row_ptr, lab, kid, info = trie.csr()
@@ -92,18 +103,20 @@ class DeviceTrie:
 
 
 class GPool:
-    """Growable pool of fp64 cumulative-mass rows on the device."""
+    """Growable pool of fp64 cumulative-mass rows on the device (allocated on
+    first use: the fused engine keeps its own history pool)."""
 
     def __init__(self, vw: int, device, cap: int = 16):
         self.vw = vw
         self.device = device
-        self.rows = torch.empty((cap, vw), dtype=torch.float64, device=device)
+        self.cap0 = cap
+        self.rows = torch.empty((0, vw), dtype=torch.float64, device=device)
         self.used = 0
 
     def alloc(self, k: int) -> np.ndarray:
         need = self.used + k
         if need > self.rows.shape[0]:
-            cap = max(need, 2 * self.rows.shape[0])
+            cap = max(need, 2 * self.rows.shape[0], self.cap0)
             grown = torch.empty((cap, self.vw), dtype=torch.float64, device=self.device)
             grown[:self.used] = self.rows[:self.used]
             self.rows = grown
@@ -135,6 +148,18 @@ class LookaheadBatch:
         return pool[self.slots_dev.long()].cpu().numpy()
 
 
+_CONVERTED: Dict[int, tuple] = {}
+
+
+def _converted(trie) -> PrefixTreeAutomaton:
+    """A reference automaton object converted once (kept alive with its source,
+    so a fusion per batch over the same automaton shares one device copy)."""
+    hit = _CONVERTED.get(id(trie))
+    if hit is None or hit[0] is not trie:
+        hit = _CONVERTED[id(trie)] = (trie, PrefixTreeAutomaton.from_reference(trie))
+    return hit[1]
+
+
 def _hkey(h):
     try:
         hash(h)
@@ -155,7 +180,7 @@ class LookaheadFusion(FusionScorer):
             raise ConfigError(f"automaton alphabet ({trie.alphabet_size}) does not match"
                               f" the token dictionary ({len(token_dict)})")
         if not isinstance(trie, PrefixTreeAutomaton):
-            trie = PrefixTreeAutomaton.from_reference(trie)
+            trie = _converted(trie)
         self.trie = trie
         self.word_lm = word_lm
         self.oov_penalty = float(oov_penalty)
@@ -164,7 +189,7 @@ class LookaheadFusion(FusionScorer):
                                                    token_dict.pad_id)
         self.dict_size = len(token_dict)
         self.device = _device(device)
-        self.dtrie = DeviceTrie(trie, self.device)
+        self.dtrie = DeviceTrie.of(trie, self.device)
         self._pool = GPool(trie.num_words, self.device)
         self._slot_of: Dict[tuple, int] = {}
         self._eos_of: Dict[tuple, float] = {}
@@ -385,14 +410,14 @@ class MultilevelFusion(FusionScorer):
             raise ConfigError(f"word LM vocabulary ({word_lm.vocab_size}) does not match"
                               f" the automaton ({trie.num_words} words)")
         if not isinstance(trie, PrefixTreeAutomaton):
-            trie = PrefixTreeAutomaton.from_reference(trie)
+            trie = _converted(trie)
         self.char_lm, self.word_lm, self.trie = char_lm, word_lm, trie
         self.oov_factor = float(oov_factor)
         self.space_id, self.eos_id, self.pad_id = (token_dict.space_id, token_dict.eos_id,
                                                    token_dict.pad_id)
         self.dict_size = len(token_dict)
         self.device = _device(device)
-        self.dtrie = DeviceTrie(trie, self.device)
+        self.dtrie = DeviceTrie.of(trie, self.device)
         self._pool = GPool(trie.num_words, self.device)     # rows = distributions (not cumsum)
         self._slot_of: Dict[tuple, int] = {}
         self._empty = torch.zeros(1, dtype=torch.int64, device=self.device)

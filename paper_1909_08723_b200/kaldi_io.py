@@ -1,10 +1,12 @@
 """Kaldi SCP/ARK ingestion (reference ``kaldi_io.py``), natively read.
 
 * ``FeatureMatrix`` / ``ScpEntry`` -- the reference records (``kaldi_io.py:31-41``).
-* ``read_scp`` -- SCP index parsing with the reference's errors (``:44-79``).
+* ``read_scp`` -- SCP index parsing (native ``fb_scp_parse``) with the
+  reference's errors (``:46-77``).
 * ``read_ark_matrix`` / ``read_feature`` -- one binary float32 record
   (``:82-134``), parsed by the C++ reader ``fb_ark_read_matrix``.
-* ``write_ark_matrix`` -- append a record + SCP line (``:137-160``).
+* ``write_ark_matrix`` -- append a record + SCP line (native
+  ``fb_ark_append_matrix``; reference ``:129-150``).
 * ``read_features_pinned`` -- a whole batch read by the C++ thread pool
   (``fb_ark_read_batch``) into ONE pinned host buffer: the FeatureMatrix data
   are views into it, so ``decode_batch``'s host->device copy starts from pinned
@@ -14,7 +16,7 @@
 from __future__ import annotations
 
 import ctypes as C
-import struct
+import os
 from dataclasses import dataclass
 from typing import List, Sequence
 
@@ -25,7 +27,6 @@ from .errors import FormatError
 
 BINARY_MARKER = b"\x00B"
 FLOAT_MATRIX_TOKEN = b"FM "
-_INT_SIZE = b"\x04"
 
 
 @dataclass(frozen=True)
@@ -42,34 +43,34 @@ class FeatureMatrix:
 
 
 def read_scp(path: str) -> List[ScpEntry]:
-    """``utt_id path:offset`` lines, in order (reference kaldi_io.py:44-79)."""
-    entries: List[ScpEntry] = []
-    seen = {}
-    with open(path, "r", encoding="utf-8") as f:
-        for lineno, raw in enumerate(f, start=1):
-            line = raw.strip()
-            if not line:
-                continue
-            fields = line.split(None, 1)
-            if len(fields) != 2:
-                raise FormatError(f"{path}:{lineno}: expected 'utt_id path:offset'")
-            utt_id, rest = fields
-            ark_path, sep, offset_text = rest.rpartition(":")
-            if not sep or not ark_path:
-                raise FormatError(f"{path}:{lineno}: missing ':offset' suffix")
-            try:
-                offset = int(offset_text)
-            except ValueError:
-                raise FormatError(
-                    f"{path}:{lineno}: offset {offset_text!r} is not an integer") from None
-            if offset < 0:
-                raise FormatError(f"{path}:{lineno}: negative offset {offset}")
-            if utt_id in seen:
-                raise FormatError(f"{path}:{lineno}: duplicate utterance id {utt_id!r}"
-                                  f" (first seen on line {seen[utt_id]})")
-            seen[utt_id] = lineno
-            entries.append(ScpEntry(utt_id, ark_path, offset))
-    return entries
+    """``utt_id path:offset`` lines, in order (reference kaldi_io.py:46-77),
+    parsed natively (``fb_scp_parse``); the error texts are the reference's."""
+    with open(path, "rb") as f:
+        blob = f.read()
+    blob.decode("utf-8")            # the reference reads text: same decode errors
+    n_max = blob.count(b"\n") + blob.count(b"\r") + 1
+    out = C.create_string_buffer(len(blob) + 2 * n_max + 16)
+    offs = np.zeros(n_max, np.int64)
+    out_len, n, err = C.c_int64(), C.c_int32(), (C.c_int32 * 3)()
+    rc = _lib.lib().fb_scp_parse(blob, len(blob), out, len(out), C.byref(out_len),
+                                 offs.ctypes.data, C.byref(n), err)
+    if rc == 4:                     # FB_ERR_FORMAT: kind, line, first line; text in out
+        kind, line, first = err[0], err[1], err[2]
+        text = out.raw[:out_len.value].decode("utf-8")
+        where = f"{path}:{line}"
+        if kind == 1:
+            raise FormatError(f"{where}: expected 'utt_id path:offset'")
+        if kind == 2:
+            raise FormatError(f"{where}: missing ':offset' suffix")
+        if kind == 3:
+            raise FormatError(f"{where}: offset {text!r} is not an integer")
+        if kind == 4:
+            raise FormatError(f"{where}: negative offset {int(text)}")
+        raise FormatError(f"{where}: duplicate utterance id {text!r} (first seen on line {first})")
+    _lib.check(rc)
+    fields = out.raw[:out_len.value].split(b"\0")
+    return [ScpEntry(fields[2 * i].decode("utf-8"), fields[2 * i + 1].decode("utf-8"),
+                     int(offs[i])) for i in range(n.value)]
 
 
 def _dims(ark_path: str, offset: int):
@@ -119,23 +120,17 @@ def read_features_pinned(entries: Sequence[ScpEntry], threads: int = 8) -> List[
 
 
 def write_ark_matrix(utt_id: str, matrix: np.ndarray, ark_path: str, scp_path: str) -> int:
-    """Append one record + its SCP line; returns the offset (kaldi_io.py:137-160)."""
-    if not utt_id or any(c.isspace() for c in utt_id):
+    """Append one binary record and its SCP line (reference kaldi_io.py:129-150);
+    returns the record's offset.  Same ValueErrors; the bytes are written by
+    the native appender (``fb_ark_append_matrix``)."""
+    if not utt_id or any(ch.isspace() for ch in utt_id):
         raise ValueError(f"bad utterance id {utt_id!r}")
-    data = np.asarray(matrix, dtype=np.float32)
-    if data.ndim != 2 or data.shape[0] < 1 or data.shape[1] < 1:
-        raise ValueError(f"matrix must be 2-D and non-empty, got shape {data.shape}")
-    if not np.isfinite(data).all():
+    mat = np.ascontiguousarray(matrix, dtype="<f4")
+    if mat.ndim != 2 or mat.shape[0] < 1 or mat.shape[1] < 1:
+        raise ValueError(f"matrix must be 2-D and non-empty, got shape {mat.shape}")
+    if not np.isfinite(mat).all():
         raise ValueError("matrix contains non-finite values")
-    rows, cols = data.shape
-    with open(ark_path, "ab") as ark:
-        ark.write(utt_id.encode("utf-8") + b" ")
-        offset = ark.tell()
-        ark.write(BINARY_MARKER)
-        ark.write(FLOAT_MATRIX_TOKEN)
-        ark.write(_INT_SIZE + struct.pack("<i", rows))
-        ark.write(_INT_SIZE + struct.pack("<i", cols))
-        ark.write(np.ascontiguousarray(data, dtype="<f4").tobytes())
-    with open(scp_path, "a", encoding="utf-8") as scp:
-        scp.write(f"{utt_id} {ark_path}:{offset}\n")
-    return offset
+    off = C.c_int64()
+    _lib.call("fb_ark_append_matrix", os.fsencode(ark_path), os.fsencode(scp_path),
+              utt_id.encode("utf-8"), mat.ctypes.data, mat.shape[0], mat.shape[1], C.byref(off))
+    return off.value

@@ -20,30 +20,6 @@ def _ld(t: Optional[torch.Tensor]) -> int:
     return 0 if t is None else t.stride(0)
 
 
-def gemm(a: torch.Tensor, w: torch.Tensor, *, m: Optional[int] = None, m_dev=None,
-         k: Optional[int] = None, bias=None, out=None, rows=None, mode: int = 0, hidden: int = 0,
-         parent=None, c_in=None, c_out=None, h_out=None, h_res=None, addend=None,
-         lda: Optional[int] = None) -> None:
-    """C = A . W^T with the epilogues of fb_gemm (see include/fusedbeam_b200.h)."""
-    g = _lib.FbGemm()
-    g.m_max = a.shape[0] if m is None else m
-    g.m_dev = P(m_dev)
-    g.n = w.shape[0]
-    g.k = w.shape[1] if k is None else k
-    g.a, g.lda = P(a), (a.stride(0) if lda is None else lda)
-    g.w, g.ldw = P(w), w.stride(0)
-    g.bias = P(bias)
-    g.c, g.ldc = P(out), _ld(out)
-    g.mode, g.hidden = mode, hidden
-    g.rows, g.parent = P(rows), P(parent)
-    g.c_in, g.ld_cin = P(c_in), _ld(c_in)
-    g.c_out, g.ld_cout = P(c_out), _ld(c_out)
-    g.h_out, g.ld_h = P(h_out), _ld(h_out)
-    g.h_res, g.ld_res = P(h_res), _ld(h_res)
-    g.addend, g.ld_add = P(addend), _ld(addend)
-    _lib.call("fb_gemm", C.byref(g), _lib.stream_ptr())
-
-
 def pack(out: torch.Tensor, segs: Sequence[Tuple], *, m: int, m_dev=None, rows=None,
          parent=None, tokens=None, ranks=None, tok_default: int = 0,
          k_pad: Optional[int] = None, split: bool = False) -> None:

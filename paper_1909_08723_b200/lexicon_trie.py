@@ -14,6 +14,8 @@ dense ``[S, alphabet]`` child map.
 
 from __future__ import annotations
 
+import functools
+import os
 from typing import List, Sequence, Tuple
 
 import numpy as np
@@ -57,26 +59,53 @@ class PrefixTreeAutomaton:
         self._csr = None
 
     def _check(self) -> None:
-        S = self.num_states
-        if S < 1 or self.max_out_degree < 1:
+        """The reference's automaton invariants and FormatError texts
+        (lexicon_trie.py:64-129), in its order; reachability is checked by
+        pointer jumping on the parent array instead of a BFS."""
+        S, D = self.num_states, self.max_out_degree
+        if S < 1 or D < 1:
             raise FormatError("automaton must have at least one state and slot")
-        for a in (self.is_final, self.word_index, self.ub_index, self.lb_index):
-            if a.shape != (S,):
-                raise FormatError("automaton arrays have inconsistent shapes")
-        if self.edge_labels.shape != self.transitions.shape:
+        if self.edge_labels.shape != (S, D) or any(
+                a.shape != (S,) for a in (self.is_final, self.word_index, self.ub_index,
+                                          self.lb_index)):
             raise FormatError("automaton arrays have inconsistent shapes")
         live = self.transitions != NO_STATE
         tgt = self.transitions[live]
-        if tgt.size != S - 1 or np.unique(tgt).size != S - 1 or (tgt < 1).any() or (tgt >= S).any():
-            raise FormatError("every non-root state needs exactly one parent")
+        if ((tgt < 1) | (tgt >= S)).any():
+            raise FormatError("transition target out of range (or pointing at root)")
         lab = self.edge_labels[live]
-        if (lab < 0).any() or (lab >= self.alphabet_size).any():
+        if ((lab < 0) | (lab >= self.alphabet_size)).any():
             raise FormatError("edge label out of range")
-        if not np.array_equal(np.sort(self.word_index[self.is_final]), np.arange(self.num_words)):
+        if (self.edge_labels[~live] != NO_STATE).any():
+            raise FormatError("unused transition slot with a live edge label")
+        if tgt.size != S - 1 or np.unique(tgt).size != S - 1:
+            raise FormatError("every non-root state needs exactly one parent")
+        if self.num_words < 1 or not np.array_equal(np.sort(self.word_index[self.is_final]),
+                                                    np.arange(self.num_words)):
             raise FormatError("final-state word ranks are not 0..num_words-1")
-        if ((self.ub_index < 0) | (self.ub_index >= self.num_words)).any() or \
-                ((self.lb_index < -1) | (self.lb_index > self.ub_index)).any():
-            raise FormatError("rank bound out of range")
+        if (self.word_index[~self.is_final] != -1).any():
+            raise FormatError("non-final state carries a word rank")
+        if ((self.ub_index < 0) | (self.ub_index >= self.num_words)).any():
+            raise FormatError("upper-bound rank out of range")
+        if ((self.lb_index < -1) | (self.lb_index > self.ub_index)).any():
+            raise FormatError("lower-bound rank out of range")
+        # every state has one parent; it is reachable iff its ancestor chain
+        # ends at the root: jump up 2^k ancestors at a time (log2 S rounds)
+        up = self._parents()[0].astype(np.int64)
+        up[0] = 0
+        for _ in range(max(1, int(S).bit_length())):
+            up = up[up]
+        if (up != 0).any():
+            raise FormatError("automaton has states unreachable from the root")
+
+    def _parents(self):
+        s, k = np.nonzero(self.transitions != NO_STATE)
+        kid = self.transitions[s, k]
+        par = np.full(self.num_states, NO_STATE, np.int32)
+        ch = np.full(self.num_states, NO_STATE, np.int32)
+        par[kid] = s
+        ch[kid] = self.edge_labels[s, k]
+        return par, ch
 
     @classmethod
     def from_reference(cls, trie) -> "PrefixTreeAutomaton":
@@ -84,13 +113,61 @@ class PrefixTreeAutomaton:
         return cls(trie.transitions, trie.edge_labels, trie.is_final, trie.word_index,
                    trie.ub_index, trie.lb_index, trie.alphabet_size)
 
-    # ---- host-side queries (reference lexicon_trie.py:131-176) -------------
-    @property
+    # ---- host-side queries (reference lexicon_trie.py:101-176) --------------
+    # Derived arrays are built on first use and cached (the dense child map is
+    # 50 MB at 65k words and only the host API needs it; the device uses CSR).
+    @functools.cached_property
     def char_children(self) -> np.ndarray:
         out = np.full((self.num_states, self.alphabet_size), NO_STATE, np.int32)
         s, k = np.nonzero(self.transitions != NO_STATE)
         out[s, self.edge_labels[s, k]] = self.transitions[s, k]
+        out.setflags(write=False)
         return out
+
+    @functools.cached_property
+    def _parent_arrays(self):
+        par, ch = self._parents()
+        par.setflags(write=False)
+        ch.setflags(write=False)
+        return par, ch
+
+    @property
+    def parent_state(self) -> np.ndarray:
+        return self._parent_arrays[0]
+
+    @property
+    def parent_char(self) -> np.ndarray:
+        return self._parent_arrays[1]
+
+    @functools.cached_property
+    def final_state_of_rank(self) -> np.ndarray:
+        out = np.full(self.num_words, NO_STATE, np.int32)
+        fin = np.nonzero(self.is_final)[0]
+        out[self.word_index[fin]] = fin
+        out.setflags(write=False)
+        return out
+
+    def advance(self, states, chars) -> np.ndarray:
+        """Batched transition (NO_STATE where no edge), reference
+        lexicon_trie.py:131-143 incl. its ValueErrors."""
+        st = np.asarray(states, np.int64)
+        ch = np.asarray(chars, np.int64)
+        if st.shape != ch.shape:
+            raise ValueError("states and chars must have equal length")
+        if st.size == 0:
+            return st.astype(np.int32)
+        if st.min() < 0 or st.max() >= self.num_states:
+            raise ValueError("state index out of range")
+        if ch.min() < 0 or ch.max() >= self.alphabet_size:
+            raise ValueError("character id out of range")
+        return self.char_children[st, ch]
+
+    def bounds(self, states) -> Tuple[np.ndarray, np.ndarray]:
+        """(ub, lb) rank bounds per state (lexicon_trie.py:145-150)."""
+        st = np.asarray(states, np.int64)
+        if st.size and (st.min() < 0 or st.max() >= self.num_states):
+            raise ValueError("bounds() requires valid (non-sentinel) states")
+        return self.ub_index[st].copy(), self.lb_index[st].copy()
 
     def child(self, state: int, char: int) -> int:
         row_ptr, lab, kid, _ = self.csr()
@@ -106,22 +183,20 @@ class PrefixTreeAutomaton:
                 break
         return s
 
-    def words(self, token_dict) -> List[str]:
-        par = np.zeros(self.num_states, np.int64)
-        ch = np.zeros(self.num_states, np.int64)
-        s, k = np.nonzero(self.transitions != NO_STATE)
-        par[self.transitions[s, k]] = s
-        ch[self.transitions[s, k]] = self.edge_labels[s, k]
-        finals = np.nonzero(self.is_final)[0]
-        order = finals[np.argsort(self.word_index[finals])]
-        out = []
-        for st in order:
-            cs = []
-            while st:
-                cs.append(token_dict.token(int(ch[st])))
-                st = par[st]
-            out.append("".join(reversed(cs)))
+    def spell(self, rank: int) -> List[int]:
+        """Character ids of the word of this rank (root-to-leaf)."""
+        par, ch = self._parent_arrays
+        st = int(self.final_state_of_rank[rank])
+        out: List[int] = []
+        while st > 0:
+            out.append(int(ch[st]))
+            st = int(par[st])
+        out.reverse()
         return out
+
+    def words(self, token_dict) -> List[str]:
+        return ["".join(token_dict.token(c) for c in self.spell(r))
+                for r in range(self.num_words)]
 
     # ---- PTA1 files (reference lexicon_trie.py:178-224), native I/O ----------
     def save(self, path: str) -> None:
@@ -141,6 +216,10 @@ class PrefixTreeAutomaton:
         _lib.call("fb_pta1_read_header", path.encode(), C.byref(S), C.byref(W), C.byref(D),
                   C.byref(A))
         S, W, D, A = S.value, W.value, D.value, A.value
+        # the header's counts against the file size before anything is
+        # allocated (a corrupt header must not request a huge allocation)
+        if os.path.getsize(path) < 20 + 8 * S * D + 13 * S:
+            raise FormatError(f"{path}: truncated array data")
         t = np.empty((S, D), np.int32)
         e = np.empty((S, D), np.int32)
         f = np.empty(S, np.uint8)

@@ -272,9 +272,19 @@ class Encoder:
             X = Xn
             Xr = torch.empty_like(X)
         C_ = 2 * He
+        exact = True
         if out is not None:
-            enc, keys = out
-            enc.view(B * TM, C_).copy_(X[:, :C_])
+            # session buffers may be larger than the batch (B and frame
+            # capacity of a corpus-wide session): fill the leading block
+            enc_o, keys_o = out
+            exact = tuple(enc_o.shape[:2]) == (B, TM) and keys_o.shape[2] == TM
+            if exact:
+                enc_o.view(B * TM, C_).copy_(X[:, :C_])
+            else:
+                enc_o[:B, :TM].copy_(X[:, :C_].view(B, TM, C_))
+            enc = enc_o
+            keys = keys_o if exact else torch.empty((B, d.att, TM), dtype=torch.float32,
+                                                    device=dev)
         else:
             enc = X[:, :C_].contiguous()
             keys = torch.empty((B, d.att, TM), dtype=torch.float32, device=dev)
@@ -287,6 +297,9 @@ class Encoder:
         # (tanh via one reciprocal; frames contiguous for the energy kernel)
         _lib.call("fb_keys_exp2t", B, TM, d.att, _lib.ptr(kraw), _lib.ptr(keys),
                   _lib.stream_ptr())
+        if not exact:
+            keys_o[:B, :, :TM].copy_(keys)
+            return enc_o, keys_o, T
         return enc.view(B, TM, C_), keys.view(B, d.att, TM), T
 
 

@@ -4,6 +4,8 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1909_08723_b200 import kernels as K
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+import testkit as TK
 torch.backends.cuda.matmul.allow_tf32 = False
 dev = torch.device("cuda")
 for (m, n, k, sa, sw) in [(480, 5000, 2048, 0.5, 0.35), (480, 4096, 2304, 0.5, 1 / 32),
@@ -18,7 +20,7 @@ for (m, n, k, sa, sw) in [(480, 5000, 2048, 0.5, 0.35), (480, 4096, 2304, 0.5, 1
     ref = a.double() @ w.double().T
     f32 = (a @ w.T).double()
     simt = torch.zeros(m, n, device=dev)
-    K.gemm(a, w, m=m, k=k, out=simt)
+    TK.gemm(a, w, m=m, k=k, out=simt)
     for name, x in (("tc", out.double()), ("torch32", f32), ("simt", simt.double())):
         e = x - ref
         print(f"m{m} n{n} k{k}: {name:8s} std {e.std().item():.2e} max {e.abs().max().item():.2e} "

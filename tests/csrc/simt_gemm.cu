@@ -1,11 +1,16 @@
-// Dense contractions of the decoder step and the word-LM step with fused
-// epilogues (bias / LSTM cell / residual / row scatter).
-//
-// v1: fp32 SIMT tiles (exact fp32 products; 128x128x16 tile, 8x8 per thread).
-// The tcgen05/TMEM path (gemm_tc.cu) replaces it for the large shapes.
+// TEST-ONLY fp32 SIMT GEMM (not part of the product library): the tcgen05
+// GEMM's epilogues (bias / LSTM cell / residual / row scatter) over exact fp32
+// products, used by tests/test_gpu_gemm.py and scripts/gemm_accuracy.py as an
+// independent device cross-check.  Built into tests/libfb_testkit.so.
+// 128x128x16 tile, 8x8 per thread.
+#include <string>
+
 #include "common.cuh"
 
-namespace fb {
+namespace fbt {
+
+using fb::row_count;
+static thread_local std::string g_err;
 
 constexpr int BM = 128, BN = 128, BK = 16, TPB = 256;
 
@@ -113,11 +118,22 @@ gemm_simt_kernel(fb_gemm_t g) {
   }
 }
 
-}  // namespace fb
+}  // namespace fbt
 
-using namespace fb;
+using namespace fbt;
 
-extern "C" int fb_gemm(const fb_gemm_t* g, void* stream) {
+#undef FB_CHECK_ARG
+#define FB_CHECK_ARG(cond, msg)   \
+  do {                             \
+    if (!(cond)) {                 \
+      g_err = msg;                 \
+      return FB_ERR_VALUE;         \
+    }                              \
+  } while (0)
+
+extern "C" const char* fbt_last_error(void) { return g_err.c_str(); }
+
+extern "C" int fbt_gemm_simt(const fb_gemm_t* g, void* stream) {
   FB_CHECK_ARG(g && g->a && g->w, "null GEMM operands");
   FB_CHECK_ARG(g->k % BK == 0, "GEMM k must be a multiple of 16 (pad the operands)");
   FB_CHECK_ARG(g->lda % 4 == 0 && g->ldw % 4 == 0, "GEMM leading dims must be multiples of 4");
@@ -128,6 +144,10 @@ extern "C" int fb_gemm(const fb_gemm_t* g, void* stream) {
   if (g->m_max <= 0) return FB_OK;
   dim3 grid((g->n + BN - 1) / BN, (g->m_max + BM - 1) / BM);
   gemm_simt_kernel<<<grid, TPB, 0, (cudaStream_t)stream>>>(*g);
-  count_launch();
-  return check_launch("gemm");
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_err = std::string("gemm_simt: ") + cudaGetErrorString(e);
+    return FB_ERR_CUDA;
+  }
+  return FB_OK;
 }

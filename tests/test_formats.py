@@ -119,3 +119,55 @@ def test_native_build_trie_speed_and_equality():
     ranked = trie.words(d)
     assert ranked == sorted(words, key=lambda w: [d.index(c) for c in w])
     assert dt < 5.0, dt
+
+
+def test_scp_parser_matches_reference_cases(tmp_path):
+    """The native SCP parser on line-ending / whitespace / int() edge cases and
+    every error kind, against the reference read_scp's results and messages
+    (tests/golden/make_scp_cases.py)."""
+    from paper_1909_08723_b200 import kaldi_io as kio
+    from paper_1909_08723_b200.errors import FormatError
+    path = tmp_path / "idx.scp"
+    for blob, want, etype, msg in load_golden("scp_cases.pkl.gz"):
+        path.write_bytes(blob)
+        if want is not None:
+            got = [(e.utt_id, e.ark_path, e.offset) for e in kio.read_scp(str(path))]
+            assert got == want, blob
+        else:
+            assert etype == "FormatError"
+            with pytest.raises(FormatError) as ei:
+                kio.read_scp(str(path))
+            assert str(ei.value).replace(str(path), "idx.scp") == msg, blob
+
+
+def test_ark_append_bytes_match_reference_layout(tmp_path):
+    """write_ark_matrix (native appender) then read back: offsets, SCP lines
+    and the reader round trip; the record bytes follow kaldi_io.py:129-150."""
+    import struct
+    from paper_1909_08723_b200 import kaldi_io as kio
+    ark, scp = str(tmp_path / "o.ark"), str(tmp_path / "o.scp")
+    rng = np.random.default_rng(3)
+    mats = [rng.standard_normal((r, 5)).astype(np.float32) for r in (3, 1, 7)]
+    offs = [kio.write_ark_matrix(f"u{i}", m_, ark, scp) for i, m_ in enumerate(mats)]
+    blob = open(ark, "rb").read()
+    pos = 0
+    for i, (m_, o) in enumerate(zip(mats, offs)):
+        head = f"u{i} ".encode()
+        assert blob[pos:pos + len(head)] == head and o == pos + len(head)
+        rec = b"\x00BFM \x04" + struct.pack("<i", m_.shape[0]) + b"\x04" + \
+            struct.pack("<i", m_.shape[1]) + m_.astype("<f4").tobytes()
+        assert blob[o:o + len(rec)] == rec
+        pos = o + len(rec)
+    assert pos == len(blob)
+    ents = kio.read_scp(scp)
+    assert [(e.utt_id, e.ark_path, e.offset) for e in ents] == \
+        [(f"u{i}", ark, o) for i, o in enumerate(offs)]
+    for e, m_ in zip(ents, mats):
+        np.testing.assert_array_equal(kio.read_feature(e).data, m_)
+    for bad in ("", "a b"):
+        with pytest.raises(ValueError):
+            kio.write_ark_matrix(bad, mats[0], ark, scp)
+    with pytest.raises(ValueError):
+        kio.write_ark_matrix("x", np.zeros((0, 3), np.float32), ark, scp)
+    with pytest.raises(ValueError):
+        kio.write_ark_matrix("x", np.full((1, 2), np.nan, np.float32), ark, scp)

@@ -5,6 +5,8 @@ kernel."""
 import numpy as np
 import pytest
 
+import testkit as TK
+
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
@@ -43,7 +45,7 @@ def test_tc_gemm_matches_fp64_reference(m, n, k):
     scale = ref.abs().max().item()
     # fp32 SIMT kernel on the same inputs: the error an fp32 GEMM makes anyway
     simt = torch.zeros(m, n, device=dev)
-    K.gemm(a, w, m=m, k=k, bias=b, out=simt)
+    TK.gemm(a, w, m=m, k=k, bias=b, out=simt)
     simt_err = (simt.double() - ref).abs().max().item()
     assert err <= max(8 * simt_err, 1e-5 * max(1.0, scale)), (err, simt_err, scale)
 
@@ -69,7 +71,7 @@ def test_tc_lstm_epilogue_matches_simt():
         if tc:
             K.gemm_tc(_packed(a, k), w.to(torch.bfloat16), **kw)
         else:
-            K.gemm(a, w, **kw)
+            TK.gemm(a, w, **kw)
         outs.append((h_out, c_out))
     assert (outs[0][0] - outs[1][0]).abs().max().item() < 1e-5
     assert (outs[0][1] - outs[1][1]).abs().max().item() < 1e-5
@@ -228,7 +230,7 @@ def test_tc_lstm_epilogue_tma_rows_in_order(m):
             hs = torch.zeros(3, m + 16, 1216, dtype=torch.bfloat16, device=dev)
             K.gemm_tc(_packed(a, k), w.to(torch.bfloat16), h_split=hs, hs_by_row=True, **kw)
         else:
-            K.gemm(a, w, **kw)
+            TK.gemm(a, w, **kw)
         outs.append((h_out, c_out))
     assert (outs[0][0] - outs[1][0]).abs().max().item() < 1e-5
     assert (outs[0][1] - outs[1][1]).abs().max().item() < 1e-5

@@ -215,54 +215,56 @@ def test_baseline_small_configs_match_oracle(name):
     _compare(got, want, name)
 
 
-def test_c2_full_size_matches_oracle():
-    """The headline configuration itself (WSJ-shaped model, 65k-word look-ahead
-    LSTM LM, beam 10) on a length-stratified sample of 3 of its 512 utterances:
-    identical tokens (or a near-tie), scores within 1e-4."""
-    import os
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    if root not in sys.path:
-        sys.path.insert(0, root)
+def test_c2_rows_match_fp64_oracle():
+    """Row-level parity at the headline dimensions (BASELINE c2: 4x BiLSTM-320
+    encoder, 3x LSTM-320 decoder, T_enc ~200, 52 tokens; 65k-word 3x1200 LM):
+    acoustic log-probs and attention rows over several steps with beam
+    reorders against the fp64 oracle; LM distributions, log P(</s>) and the
+    fp64 g rows (cumulative word mass) against the oracle LM."""
     import bench
-    fb, synth = __import__("paper_1909_08723_b200"), None
+    from oracle import harness as H
+    import paper_1909_08723_b200 as fb
     from paper_1909_08723_b200.models import AttnLstmScorer, LstmWordLM
-    wl, d, W, words, trie, utts = bench.build_inputs("c2", 0)
-    idx = bench.cpu_sample(len(utts), 3)
-    sample = [utts[i] for i in idx]
-    cfg = bench.decode_config(wl)
-    got = fb.decode_batch([fb.FeatureMatrix(u, x) for u, x in sample],
-                          AttnLstmScorer(W, wl.asr, d.eos_id),
-                          fb.LookaheadFusion(trie, LstmWordLM(W, wl.lm), d), cfg, d)
-    _, want = bench.cpu_decode(wl, d, W, words, sample, len(sample), os.cpu_count() or 4)
-    _compare(got, want, "c2")
+    wl = H.workload("c2")
+    d, W, trie = bench.build_product(wl)
+    utts = H.corpus(wl, 0)
+    gpu = AttnLstmScorer(W, wl.asr, d.eos_id)
+    cpu = OracleAttnLstmScorer(W, wl.asr.enc_layers, wl.asr.dec_layers, wl.asr.subsample,
+                               d.eos_id, dtype=torch.float64)
+    worst_l = worst_a = 0.0
+    for i in (0, 255, 511):
+        uid, x = utts[i]
+        f = fb.FeatureMatrix(uid, x)
+        sg, sc = gpu.init(f), cpu.init(f)
+        assert gpu.enc_length(sg) == cpu.enc_length(sc) == x.shape[0] // 4
+        last = [-1]
+        rng = np.random.default_rng(i)
+        for step in range(8):
+            lg, ag, sg = gpu.step(sg, last)
+            lc, ac, sc = cpu.step(sc, last)
+            worst_l = max(worst_l, float(np.abs(lg - lc).max()))
+            worst_a = max(worst_a, float(np.abs(ag - ac).max()))
+            par = sorted(rng.integers(0, len(last), size=wl.beam).tolist())
+            sg, sc = gpu.reorder(sg, par), cpu.reorder(sc, par)
+            last = rng.integers(3, len(d), size=wl.beam).tolist()
+    print(f"\nc2 rows vs fp64 oracle: max |dlogp| {worst_l:.3g}, max |dattn| {worst_a:.3g}")
+    assert worst_l <= 2e-5 and worst_a <= 2e-6
 
-
-def test_c5_size_matches_oracle():
-    """BASELINE.json c5 (Switchboard-shaped character decoder, 30k-word
-    look-ahead 3x900 LSTM LM, beam 35) on its two shortest utterances of a
-    16-utterance draw: identical tokens (or a near-tie), scores within 1e-4.
-    The random model's <eos> bias is lowered so the decodes run to their
-    length cap (full beam, word boundaries, LM events) instead of ending at
-    step 1."""
-    import os
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    if root not in sys.path:
-        sys.path.insert(0, root)
-    import bench
-    fb = __import__("paper_1909_08723_b200")
-    from paper_1909_08723_b200.models import AttnLstmScorer, LstmWordLM
-    wl, d, W, words, trie, utts = bench.build_inputs("c5", 0, 16,
-                                                     overrides=("asr.eos_bias=-1.5",
-                                                                "lm.emb_scale=0.2",
-                                                                "lm.eos_bias=5",
-                                                                "lm.w_scale=2"))
-    sample = sorted(utts, key=lambda ux: ux[1].shape[0])[:2]
-    cfg = bench.decode_config(wl)
-    got = fb.decode_batch([fb.FeatureMatrix(u, x) for u, x in sample],
-                          AttnLstmScorer(W, wl.asr, d.eos_id),
-                          fb.LookaheadFusion(trie, LstmWordLM(W, wl.lm), d), cfg, d)
-    _, want = bench.cpu_decode(wl, d, W, words, sample, len(sample), os.cpu_count() or 4)
-    assert min(r.steps for r in got) > 5
-    _compare(got, want, "c5")
+    glm = LstmWordLM(W, wl.lm)
+    clm = OracleLstmWordLM(W, wl.lm.layers, wl.lm.words)
+    hg, hc = glm.start_history(), clm.start_history()
+    worst_p = worst_e = worst_g = 0.0
+    for r in [17, -1, 64999, 0, 31337]:
+        pg, pc = glm.full_distribution(hg), clm.full_distribution(hc)
+        worst_p = max(worst_p, float(np.max(np.abs(pg - pc) / np.maximum(pc, 1e-300))))
+        worst_e = max(worst_e, abs(glm.eos_log_prob(hg) - clm.eos_log_prob(hc)))
+        worst_g = max(worst_g, float(np.abs(np.cumsum(pg) - np.cumsum(pc)).max()))
+        hg, hc = glm.extend_history(hg, r), clm.extend_history(hc, r)
+    # the fused engine's g rows (LookaheadFusion.start -> the device scan)
+    fus = fb.LookaheadFusion(trie, glm, d)
+    g0 = fus.start(1).g[0]
+    ref_g = np.cumsum(clm.full_distribution(clm.start_history()))
+    worst_g = max(worst_g, float(np.abs(g0 - ref_g).max()))
+    print(f"c2 LM vs oracle: max rel dP {worst_p:.3g}, max |d log P(</s>)| {worst_e:.3g}, "
+          f"max |dg| {worst_g:.3g}")
+    assert worst_p <= 2e-5 and worst_e <= 2e-5 and worst_g <= 2e-6

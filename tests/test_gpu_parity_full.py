@@ -1,0 +1,93 @@
+"""Full-set parity: the GPU decoder against the oracle decoder's per-utterance
+results on the BASELINE.json configurations' own synthetic corpora
+(``tests/golden/parity_<cfg>.pkl.gz``, made by ``tests/golden/make_parity.py``
+with the oracle restatement of the reference decoder -- pinned to the
+reference bit-for-bit by ``test_oracle_golden.py`` -- driving PyTorch-CPU fp32
+adapters of the same seeded weights).
+
+* c2 (the headline): all 512 utterances, decoded as the production batch
+  (``decode_corpus`` with the workload's batch size = one 512-utterance batch);
+* c4 / c5: length-stratified samples including the longest utterances,
+  through ``decode_corpus`` with the workload's batch size;
+* c1 / c3: the whole 16-utterance sets.
+
+North star: tokens identical on every utterance where no decision falls
+within the tolerance (the oracle's decision margin: the gap at any beam cut,
+finished-set cap, early stop or final pick), per-hypothesis scores within
+1e-4 absolute.  The test prints the exempt count and the largest score gap.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_golden
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+SCORE_TOL = 1e-4        # north star: per-hypothesis scores within 1e-4 absolute
+TIE_TOL = 1e-4          # decisions closer than this are near-ties (exempt)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu(cuda_lib):
+    return cuda_lib
+
+
+def _decode(name, g):
+    import bench
+    import paper_1909_08723_b200 as fb
+    from oracle import harness as H
+    from paper_1909_08723_b200.fusion import LookaheadFusion, SubwordFusion
+    from paper_1909_08723_b200.models import AttnLstmScorer, LstmSubwordLM, LstmWordLM
+    wl = H.workload(name, g["n_utts"] if g["n_utts"] != H.workload(name).n_utts else None)
+    assert wl.describe() == g["workload"], "workload changed since the fixture was made"
+    d, W, trie = bench.build_product(wl)
+    utts = H.corpus(wl, 0)
+    sel = [utts[i] for i in g["indices"]]
+    scorer = AttnLstmScorer(W, wl.asr, d.eos_id)
+    wlm = LstmWordLM(W, wl.lm) if wl.lm is not None else None
+    slm = LstmSubwordLM(W, wl.sublm, d.pad_id, d.eos_id) if wl.sublm is not None else None
+
+    def factory():
+        if wlm is not None:
+            return LookaheadFusion(trie, wlm, d)
+        if slm is not None:
+            return SubwordFusion(slm)
+        return None
+
+    feats = [fb.FeatureMatrix(u, x) for u, x in sel]
+    return fb.decode_corpus(feats, scorer, factory, bench.decode_config(wl), d,
+                            batch_size=wl.batch_size)
+
+
+@pytest.mark.parametrize("name", ["c2", "c4", "c5", "c1", "c3"])
+def test_full_set_matches_oracle(name):
+    path = os.path.join(GOLDEN, f"parity_{name}.pkl.gz")
+    if not os.path.exists(path):
+        pytest.skip(f"no fixture {path}")
+    g = load_golden(f"parity_{name}.pkl.gz")
+    got = _decode(name, g)
+    exempt, worst, mism = [], 0.0, []
+    for a, row in zip(got, g["results"]):
+        uid, toks, score, fin, steps, margin, dmargin, acc = row
+        assert a.utt_id == uid
+        if a.tokens != toks or a.finished != fin:
+            if dmargin < TIE_TOL:
+                exempt.append((uid, dmargin))
+                continue
+            mism.append((uid, dmargin, a.tokens[:12], toks[:12]))
+            continue
+        assert a.steps == steps, (uid, a.steps, steps)
+        worst = max(worst, abs(a.score - score))
+        assert abs(a.score - score) <= SCORE_TOL, (uid, a.score, score)
+        np.testing.assert_allclose(a.attn_accum, acc.astype(np.float64), atol=1e-4)
+    n = len(got)
+    print(f"\n{name}: {n} utterances, {n - len(exempt) - len(mism)} identical, "
+          f"{len(exempt)} exempt near-ties (decision margin < {TIE_TOL}), "
+          f"{len(mism)} mismatches; max |score diff| {worst:.3g}")
+    assert not mism, mism[:5]
