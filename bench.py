@@ -351,9 +351,13 @@ def main():
     def decode_fn(shard):
         return fb.decode_corpus(shard, scorer, fusion_factory, cfg, d, batch_size=bs)
 
-    # the public API once (builds and caches the engine + its session/graphs)
-    decode_corpus_sharded(feats, decode_fn, rank=rank, world=world)
-    dec = next(iter(scorer._fused_cache.values()))
+    if args.profile_only:               # ncu: one resident decode, nothing else
+        from paper_1909_08723_b200.engine import FusedDecoder
+        dec = FusedDecoder(scorer, fusion_factory(), cfg, d)
+    else:
+        # the public API once (builds and caches the engine + its session/graphs)
+        decode_corpus_sharded(feats, decode_fn, rank=rank, world=world)
+        dec = next(iter(scorer._fused_cache.values()))
     # device-resident inputs for the `value` timing: every batch staged once
     staged = []
     for b in batches:
