@@ -198,8 +198,8 @@ int fb_search_init(const fb_search_cfg_t* cfg, const fb_search_state_t* st,
 
 /* ---- dense contractions (attention-LSTM decoder step, word-LM step) ------ */
 /* C = A . W^T (+ bias) with a fused epilogue, on the tensor cores
- * (fb_gemm_tc below).  A = bf16 planes of the fp32 activations [m, k]
- * (compact rows), W [n, k] bf16 row-major.
+ * (fb_gemm_tc below).  A = operand planes of the fp32 activations [m, k]
+ * (compact rows, fb_operand_format), W [n, k] row-major in the operand format.
  *   mode 0: out row = rows ? rows[i] : i ;  c[out*ldc + j] = acc + bias[j]
  *   mode 1: LSTM cell.  n == 4*hidden with gate columns interleaved
  *           (column 4u+q, q = i,f,g,o); slot = rows ? rows[i] : i,
@@ -224,7 +224,7 @@ typedef struct {
   float* h_out; int64_t ld_h;
   const float* h_res; int64_t ld_res;
   const float* addend; int64_t ld_add;
-  /* mode 1, optional: h also written as 3 bf16 planes (hi/mid/lo) at
+  /* mode 1, optional: h also written as operand planes (fb_operand_format) at
    * [p*hs_plane_rows + slot][unit] -- the A operand of a following GEMM */
   void* h_split; int64_t hs_plane_rows; int64_t ld_hs;
   /* mode 0, optional: per (output row, 64-column block) softmax statistics
@@ -253,18 +253,30 @@ typedef struct {
   /* mode 0, n <= 64: store the row log-softmax over the n columns instead of
    * the logits (same arithmetic as fb_log_softmax_rows) */
   int32_t out_logsoftmax;
+  /* accumulator scale applied in the epilogue: 1 / (activation scale x
+   * weight scale) of the operand format (fb_operand_format); 0 means
+   * 1 / activation scale (weights stored unscaled) */
+  float acc_scale;
+  int32_t pad_fmt;
 } fb_gemm_t;
 
+/* Tensor-core operand format of this build: planes per fp32 activation
+ * (2: fp16 hi/lo of x * act_scale; 3: bf16 hi/mid/lo), is_fp16, act_scale.
+ * Weight operands are fp16 times a power of two per matrix (fp16 builds) or
+ * bf16.  Writers of A planes (fb_pack_rows out_mode 1, the LSTM epilogues'
+ * h_split) use this format. */
+int fb_operand_format(int32_t* planes, int32_t* is_fp16, float* act_scale);
+
 /* 5th-gen tensor cores (tcgen05 + TMEM + TMA): A is
- * a_planes bf16 planes of [a_plane_rows, lda] (the fp32 activation split
- * hi/mid/lo by fb_pack_rows out_mode 1), W is bf16 [n, ldw]; fp32
+ * a_planes operand planes of [a_plane_rows, lda] (the fp32 activation split
+ * by fb_pack_rows out_mode 1), W [n, ldw] in the operand format; fp32
  * accumulation in TMEM.  k % 64 == 0, lda/ldw % 8 == 0. */
 int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_rows, void* stream);
 
 /* Encoder LSTM recurrence for one direction: for t < steps,
- * gates = xp[:, t] + h_{t-1} W_hh^T (tensor cores, W_hh bf16 [4H, k]), cell
- * epilogue, h_t -> y[:, t] and, split into bf16 planes, into
- * rec[(t+1)%2] ([2][3][batch][k] bf16, rec[0] zero on entry); the cell state
+ * gates = xp[:, t] + acc_scale h_{t-1} W_hh^T (tensor cores, W_hh [4H, k] in
+ * the operand format), cell epilogue, h_t -> y[:, t] and, split into operand
+ * planes, into rec[(t+1)%2] ([2][planes][batch][k], rec[0] zero on entry); the cell state
  * lives in registers (zero at t = 0).
  * Row b of step t: xp + t*step_xp + b*ld_xp, y + t*step_y + b*ld_y (time-major
  * layouts -- step_* = batch * row width -- keep each step's rows contiguous).
@@ -273,7 +285,7 @@ int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_rows, void*
 int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden, const void* w_hh,
                        int32_t k, const float* xp, int64_t ld_xp, int64_t step_xp, float* y,
                        int64_t ld_y, int64_t step_y, void* rec, uint32_t* sync_ws,
-                       void* stream);
+                       float acc_scale, void* stream);
 
 /* Row gather-concatenate into a GEMM A operand:
  *   out[i, :] = [seg0 | seg1 | ... | zero pad up to k_pad], i < m.
@@ -290,7 +302,7 @@ typedef struct {
   int32_t nseg;
   int32_t k_pad;
   int32_t tok_default;
-  int32_t out_mode;      /* 0: fp32 rows; 1: three bf16 planes hi/mid/lo     */
+  int32_t out_mode;      /* 0: fp32 rows; 1: operand planes (fb_operand_format) */
   int64_t plane_rows;    /* out_mode 1: rows per plane ([3][plane_rows][ld])  */
 } fb_pack_t;
 

@@ -87,8 +87,11 @@ class OracleModel:
     """Oracle scorer + fusion + config of one workload (weights from the seeded
     synthesizer, trie from the oracle's restated ``build_trie``)."""
 
-    def __init__(self, wl):
-        import torch  # noqa: F401  (PyTorch-CPU fp32 adapters)
+    def __init__(self, wl, dtype=None):
+        """dtype=torch.float64: every neural adapter in double precision (the
+        exact-arithmetic yardstick for the fp32 oracle and the GPU)."""
+        import torch  # (PyTorch-CPU fp32 adapters)
+        dtype = dtype or torch.float32
         from .lexicon import OracleDict, build_trie
         from .neural import OracleAttnLstmScorer, OracleLstmWordLM
         from .search import OracleConfig
@@ -100,14 +103,14 @@ class OracleModel:
         if wl.sublm is not None:
             from .subword import OracleLstmCharLM
             W.update(S.subword_lm_weights(wl.sublm, seed=wl.seed + 1, eos_id=od.eos_id))
-            self.sublm = OracleLstmCharLM(W, wl.sublm.layers, od.pad_id, od.eos_id)
+            self.sublm = OracleLstmCharLM(W, wl.sublm.layers, od.pad_id, od.eos_id, dtype=dtype)
         if wl.lm is not None:
             W.update(S.lm_weights(wl.lm, seed=wl.seed + 1))
             self.words = S.synth_lexicon(wl.lm.words, seed=wl.seed + 2)
             self.trie = build_trie(self.words, od)
-            self.lm = OracleLstmWordLM(W, wl.lm.layers, wl.lm.words)
+            self.lm = OracleLstmWordLM(W, wl.lm.layers, wl.lm.words, dtype=dtype)
         self.scorer = OracleAttnLstmScorer(W, wl.asr.enc_layers, wl.asr.dec_layers,
-                                           wl.asr.subsample, od.eos_id)
+                                           wl.asr.subsample, od.eos_id, dtype=dtype)
         self.cfg = OracleConfig(beam_size=wl.beam, lm_weight=wl.lm_weight,
                                 coverage_mode=wl.coverage_mode,
                                 coverage_weight=wl.coverage_weight, eos_gamma=wl.eos_gamma,
@@ -131,11 +134,11 @@ class OracleModel:
 
 
 # ---- one process per host core -------------------------------------------------
-def _worker(conn, wl_args, rank):
+def _worker(conn, wl_args, rank, fp64=False):
     import torch
     torch.set_num_threads(1)
     wl = workload(*wl_args)
-    model = OracleModel(wl)
+    model = OracleModel(wl, torch.float64 if fp64 else None)
     utts = corpus(wl, rank)
     conn.send(("ready", None))
     while True:
@@ -172,7 +175,7 @@ class OraclePool:
 
     def __init__(self, name: str, procs: Optional[int] = None, rank: int = 0,
                  n_utts: Optional[int] = None, words: Optional[int] = None,
-                 overrides: Sequence[str] = ()):
+                 overrides: Sequence[str] = (), fp64: bool = False):
         self.procs = procs or host_cores()
         self.wl = workload(name, n_utts, words, overrides)
         self.lengths = [x.shape[0] for _, x in corpus(self.wl, rank)]
@@ -181,7 +184,7 @@ class OraclePool:
         args = (name, n_utts, words, tuple(overrides))
         for _ in range(self.procs):
             a, b = ctx.Pipe()
-            p = ctx.Process(target=_worker, args=(b, args, rank), daemon=True)
+            p = ctx.Process(target=_worker, args=(b, args, rank, fp64), daemon=True)
             p.start()
             self.conns.append(a)
             self.ps.append(p)

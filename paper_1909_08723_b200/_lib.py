@@ -56,7 +56,8 @@ class FbGemm(C.Structure):
                 ("h_split", vp), ("hs_plane_rows", i64), ("ld_hs", i64),
                 ("row_stats", vp), ("stats_vw", i32), ("kcb", i32),
                 ("hs_row_mode", i32), ("splitk_ws", vp), ("splitk_cnt", vp),
-                ("out_exp2", i32), ("out_logsoftmax", i32)]
+                ("out_exp2", i32), ("out_logsoftmax", i32), ("acc_scale", C.c_float),
+                ("pad_fmt", i32)]
 
 
 class FbSeg(C.Structure):
@@ -89,7 +90,8 @@ _SIGS = {
     "fb_stats_to_g": (C.c_int, [i32, vp, vp, i64, vp, i32, vp, i32, vp, vp, i64, vp, vp, vp, vp,
                                 vp]),
     "fb_lstm_recurrence": (C.c_int, [i32, i32, i32, vp, i32, vp, i64, i64, vp, i64, i64, vp,
-                                      vp, vp]),
+                                      vp, C.c_float, vp]),
+    "fb_operand_format": (C.c_int, [vp, vp, vp]),
     "fb_pack_rows": (C.c_int, [C.POINTER(FbPack), i32, vp, vp, vp, vp, vp, vp, i64, vp]),
     "fb_log_softmax_rows": (C.c_int, [i32, vp, vp, vp, i64, i32, vp, i64, vp]),
     "fb_row_logsumexp": (C.c_int, [i32, vp, vp, vp, i64, i32, i32, vp, vp]),

@@ -14,17 +14,8 @@
 namespace fb {
 
 // ---------------------------------------------------------------- packing --
-__device__ __forceinline__ void split3(float x, __nv_bfloat16& hi, __nv_bfloat16& mid,
-                                       __nv_bfloat16& lo) {
-  // x = hi + mid + lo exactly (8+8+8 mantissa bits of the fp32 value)
-  hi = __float2bfloat16_rn(x);
-  const float r1 = x - __bfloat162float(hi);
-  mid = __float2bfloat16_rn(r1);
-  lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
-}
-
 // One warp per output row, 4 consecutive columns per lane (float4 in, 8-byte
-// bf16x4 per plane out) when the segment allows it.
+// 4 x 16-bit per operand plane out, split_operand) when the segment allows it.
 __global__ void __launch_bounds__(256)
 pack_rows_kernel(fb_pack_t p, int m_max, const int32_t* __restrict__ m_dev,
                  const int32_t* __restrict__ rows, const int32_t* __restrict__ parent,
@@ -34,7 +25,7 @@ pack_rows_kernel(fb_pack_t p, int m_max, const int32_t* __restrict__ m_dev,
   const bool split = p.out_mode == 1;
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
-  __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(out);
+  uint16_t* ob = reinterpret_cast<uint16_t*>(out);
   const int64_t plane = p.plane_rows * ld_out;
   for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < m; i += gridDim.x * wpb) {
     // resolve every segment's source row first (the index loads overlap)
@@ -85,14 +76,17 @@ pack_rows_kernel(fb_pack_t p, int m_max, const int32_t* __restrict__ m_dev,
             if (!split) {
               *reinterpret_cast<float4*>(out + o) = v[q];
             } else {
-              __nv_bfloat16 h[4], md[4], lo[4];
-              split3(v[q].x, h[0], md[0], lo[0]);
-              split3(v[q].y, h[1], md[1], lo[1]);
-              split3(v[q].z, h[2], md[2], lo[2]);
-              split3(v[q].w, h[3], md[3], lo[3]);
-              *reinterpret_cast<uint2*>(ob + o) = *reinterpret_cast<uint2*>(h);
-              *reinterpret_cast<uint2*>(ob + plane + o) = *reinterpret_cast<uint2*>(md);
-              *reinterpret_cast<uint2*>(ob + 2 * plane + o) = *reinterpret_cast<uint2*>(lo);
+              uint16_t e[4][3], pl[3][4];
+              split_operand(v[q].x, e[0]);
+              split_operand(v[q].y, e[1]);
+              split_operand(v[q].z, e[2]);
+              split_operand(v[q].w, e[3]);
+#pragma unroll
+              for (int pp = 0; pp < kPlanes; ++pp) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) pl[pp][c] = e[c][pp];
+                *reinterpret_cast<uint2*>(ob + pp * plane + o) = *reinterpret_cast<uint2*>(pl[pp]);
+              }
             }
           }
         }
@@ -103,11 +97,10 @@ pack_rows_kernel(fb_pack_t p, int m_max, const int32_t* __restrict__ m_dev,
           if (!split) {
             out[o] = x;
           } else {
-            __nv_bfloat16 h, md, lo;
-            split3(x, h, md, lo);
-            ob[o] = h;
-            ob[plane + o] = md;
-            ob[2 * plane + o] = lo;
+            uint16_t e[3];
+            split_operand(x, e);
+#pragma unroll
+            for (int pp = 0; pp < kPlanes; ++pp) ob[pp * plane + o] = e[pp];
           }
         }
       }

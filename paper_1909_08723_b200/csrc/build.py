@@ -17,8 +17,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 PKG = os.path.dirname(HERE)
 ROOT = os.path.dirname(PKG)
 INCLUDE = os.path.join(ROOT, "include")
-OUT = os.path.join(PKG, "libfusedbeam_b200.so")
-OBJ = os.path.join(HERE, "_obj")
+# dev A/B builds: FB_BUILD_TAG=x (+ FB_NVCC_EXTRA=-D...) -> libfusedbeam_b200_x.so,
+# loaded with FB_LIB_AB=libfusedbeam_b200_x.so
+_TAG = os.environ.get("FB_BUILD_TAG", "")
+OUT = os.path.join(PKG, f"libfusedbeam_b200{'_' + _TAG if _TAG else ''}.so")
+OBJ = os.path.join(HERE, "_obj" + ("_" + _TAG if _TAG else ""))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -59,7 +62,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-    build_testkit(force, verbose, hdr_mtime)
+    if not _TAG:
+        build_testkit(force, verbose, hdr_mtime)
     return OUT
 
 

@@ -1,6 +1,8 @@
 // Shared helpers for the fusedbeam_b200 kernels (sm_100a).
 #pragma once
 
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <cmath>
@@ -19,6 +21,38 @@ void count_launch(unsigned n = 1);
 int check_launch(const char* what);
 
 constexpr int kNumSMs = 148;
+
+// ---- tensor-core operand format (compile time; fb_operand_format reports it) --
+// FB_OPERAND_FP16X2 = 1 (default): an fp32 activation x is scaled by 2^8 and
+// split into two fp16 planes, hi = fp16(x 2^8), lo = fp16(x 2^8 - hi): 22
+// significant bits, and absolute error <= 2^-32 below the fp16 normal range;
+// weights are fp16, scaled per matrix by a power of two (bf16-exact values are
+// exact in fp16 there).  Products are exact in fp32; the epilogue undoes both
+// scales with one exact multiply (fb_gemm_t.acc_scale).  Two MMAs per K step
+// and 4 B per A element.  Operand range: |x| < 255.
+// FB_OPERAND_FP16X2 = 0: three bf16 planes hi/mid/lo (24 bits), bf16 weights.
+#ifndef FB_OPERAND_FP16X2
+#define FB_OPERAND_FP16X2 1
+#endif
+constexpr int kPlanes = FB_OPERAND_FP16X2 ? 2 : 3;
+constexpr float kActScale = FB_OPERAND_FP16X2 ? 256.0f : 1.0f;
+
+// x -> operand planes (raw 16-bit patterns; p[2] unused with 2 planes)
+__device__ __forceinline__ void split_operand(float x, uint16_t* p) {
+#if FB_OPERAND_FP16X2
+  const float y = x * kActScale;
+  const __half hi = __float2half_rn(y);
+  p[0] = __half_as_ushort(hi);
+  p[1] = __half_as_ushort(__float2half_rn(y - __half2float(hi)));
+#else
+  const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+  const float r1 = x - __bfloat162float(hi);
+  const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+  p[0] = __bfloat16_as_ushort(hi);
+  p[1] = __bfloat16_as_ushort(mid);
+  p[2] = __bfloat16_as_ushort(__float2bfloat16_rn(r1 - __bfloat162float(mid)));
+#endif
+}
 constexpr int kWarp = 32;
 
 __device__ __forceinline__ int row_count(int n_max, const int32_t* n_dev) {

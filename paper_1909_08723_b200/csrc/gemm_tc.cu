@@ -1,11 +1,13 @@
 // tcgen05 tensor-core GEMM for sm_100a with the decoder/LM epilogues.
 //
-//   C[m, n] = sum_p sum_k A_p[m, k] * W[n, k]        (p over the bf16 planes)
+//   C[m, n] = acc_scale * sum_p sum_k A_p[m, k] * W[n, k]   (p over the planes)
 //
-// A is the fp32 activation split into 3 bf16 planes (hi/mid/lo: 24 mantissa
-// bits, written by fb_pack_rows), W holds bf16-exact weights, accumulation is
-// fp32 in TMEM -- an fp32-accurate product on the 5th-gen tensor cores
-// (SURVEY.md §7 "GEMM precision").  Algorithmic FLOPs count the product once.
+// A is the fp32 activation split into operand planes (common.cuh: by default
+// two fp16 planes of x 2^8, 22 significant bits; or three bf16 planes), written
+// by fb_pack_rows and by the LSTM epilogues; W holds the weights exactly
+// (power-of-two scaled fp16, or bf16); accumulation is fp32 in TMEM -- an
+// fp32-accurate product on the 5th-gen tensor cores (SURVEY.md §7 "GEMM
+// precision").  Algorithmic FLOPs count the product once.
 //
 // Accuracy: the tensor core's fp32 accumulation in TMEM is not IEEE
 // round-to-nearest -- its error grows ~k^1.5 (7.5x an fp32 dot product at
@@ -45,10 +47,18 @@ __device__ __forceinline__ unsigned long long gtime() {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;            // 64 bf16 = 128 B = one swizzle atom
-constexpr int TC_STAGES = 3;
+constexpr int TC_STAGES = kPlanes == 2 ? 4 : 3;   // smem ring: 4 x 48 KB or 3 x 64 KB
+// stages of the GEMM ring for a tile width (4 x 48 KB .. 2 x 80 KB, + the 33 KB
+// epilogue staging within the 227 KB of a CTA)
+constexpr int tc_stages(int bn) {
+  return (kPlanes * 128 * 64 * 2 + bn * 64 * 2) <= 48 * 1024 ? 4
+         : (kPlanes * 128 * 64 * 2 + bn * 64 * 2) <= 64 * 1024 ? 3 : 2;
+}
 constexpr int TC_KCB = 4;            // K blocks per accumulation chunk (K = 256)
 constexpr int TC_NACC = 4;           // TMEM chunk slots (4 x 128 columns = all of TMEM)
-constexpr int TC_EPI_THREADS = 256;     // 8 epilogue warps: 2 per TMEM lane quarter
+constexpr int TC_EPI_THREADS = 256;
+// instruction descriptor operand formats (kind::f16): a/b = F16 (0) or BF16 (1)
+constexpr uint32_t kIdescAB = FB_OPERAND_FP16X2 ? 0u : ((1u << 7) | (1u << 10));     // 8 epilogue warps: 2 per TMEM lane quarter
 constexpr int TC_THREADS = 64 + TC_EPI_THREADS;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -161,26 +171,27 @@ __device__ __forceinline__ float ftanh(float x) {
 #endif
 
 __device__ __forceinline__ void store_split(const fb_gemm_t& g, int64_t row, int col, float x) {
-  // hi/mid/lo bf16 planes of an fp32 value (the next GEMM's A operand)
-  __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.h_split) + row * g.ld_hs + col;
-  const __nv_bfloat16 hi = __float2bfloat16_rn(x);
-  const float r1 = x - __bfloat162float(hi);
-  const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-  o[0] = hi;
-  o[g.hs_plane_rows * g.ld_hs] = mid;
-  o[2 * g.hs_plane_rows * g.ld_hs] = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+  // operand planes of an fp32 value (the next GEMM's A operand)
+  uint16_t* o = reinterpret_cast<uint16_t*>(g.h_split) + row * g.ld_hs + col;
+  uint16_t e[3];
+  split_operand(x, e);
+#pragma unroll
+  for (int q = 0; q < kPlanes; ++q) o[q * g.hs_plane_rows * g.ld_hs] = e[q];
 }
 
 // One warp drains its 32 TMEM lanes (rows) chunk by chunk; each 32x32 chunk is
 // transposed through shared memory so global loads/stores are row-contiguous
 // across the warp (plain mode: lane = column; LSTM mode: lane = (row, unit)).
-template <int BN>
+// DIRECT (BN = 256): the whole-K accumulator is read chunk by chunk straight
+// from TMEM at tsrc (no register-resident chunk sums).
+template <int BN, bool DIRECT = false>
 __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row0, int n0,
-                                              float (&acc)[BN / 64][32],
+                                              const float (*acc)[32],
                                               float* st /* [32][33] */, int half,
                                               const CUtensorMap* tmC = nullptr,
                                               const CUtensorMap* tmH = nullptr,
-                                              const CUtensorMap* tmS = nullptr) {
+                                              const CUtensorMap* tmS = nullptr,
+                                              uint32_t tsrc = 0) {
   const int lane = threadIdx.x & 31;
   // {max_all, sum_all, max_words, sum_words} of this lane's row over the
   // warp's half of the tile (BN/2 columns)
@@ -199,8 +210,14 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
   for (int c = 0; c < CH; ++c) {
     const int cb = half * CH + c;
     float v[32];
+    if constexpr (DIRECT) {
+      tmem_ld32(tsrc + (uint32_t)(cb * 32), v);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = acc[c][j];
+      for (int j = 0; j < 32; ++j) v[j] *= g.acc_scale;               // exact power of 2
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = acc[c][j] * g.acc_scale;
+    }
     __syncwarp();
     const int nb = n0 + cb * 32;
     if (g.mode == 0 && g.bias) {
@@ -230,6 +247,16 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
         const float m2 = fmaxf(st_stats.z, mw);
         st_stats.w = st_stats.w * __expf(st_stats.z - m2) + sw * __expf(mw - m2);
         st_stats.z = m2;
+      }
+      if (c & 1) {
+        // one 64-column statistics group done (n0/64 + half for BN = 128)
+        if (row0 + lane < M) {
+          const int orow = g.rows ? g.rows[row0 + lane] : row0 + lane;
+          const int ntiles = (g.n + 63) / 64;
+          reinterpret_cast<float4*>(g.row_stats)[(int64_t)orow * ntiles + (n0 + (cb - 1) * 32) / 64] =
+              st_stats;
+        }
+        st_stats = make_float4(-INFINITY, 0.f, -INFINITY, 0.f);
       }
     }
     if constexpr (BN == 64) {
@@ -342,25 +369,23 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
         h4[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
         }
         if (g.h_split) {
-          __nv_bfloat16 pl[3][8];
+          uint16_t pl[3][8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            const __nv_bfloat16 hi = __float2bfloat16_rn(hv[u]);
-            const float r1 = hv[u] - __bfloat162float(hi);
-            const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-            pl[0][u] = hi;
-            pl[1][u] = mid;
-            pl[2][u] = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+            uint16_t e[3];
+            split_operand(hv[u], e);
+#pragma unroll
+            for (int q = 0; q < kPlanes; ++q) pl[q][u] = e[q];
           }
           if (tmS && row0 + 32 <= M) {
-            uint4* ss = reinterpret_cast<uint4*>(st + 512);        // [3][32 rows][16 B]
+            uint4* ss = reinterpret_cast<uint4*>(st + 512);        // [planes][32 rows][16 B]
 #pragma unroll
-            for (int q = 0; q < 3; ++q) ss[q * 32 + lane] = *reinterpret_cast<const uint4*>(pl[q]);
+            for (int q = 0; q < kPlanes; ++q) ss[q * 32 + lane] = *reinterpret_cast<const uint4*>(pl[q]);
           } else {
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(g.h_split) +
-                             (int64_t)(g.hs_row_mode ? row : slot) * g.ld_hs + unit0;
+          uint16_t* o = reinterpret_cast<uint16_t*>(g.h_split) +
+                        (int64_t)(g.hs_row_mode ? row : slot) * g.ld_hs + unit0;
 #pragma unroll
-          for (int q = 0; q < 3; ++q)
+          for (int q = 0; q < kPlanes; ++q)
             *reinterpret_cast<uint4*>(o + (int64_t)q * g.hs_plane_rows * g.ld_hs) =
                 *reinterpret_cast<const uint4*>(pl[q]);
           }
@@ -497,12 +522,6 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
       TRACE(8, 2 * c + 1);
     }
   }
-  if (g.row_stats && row0 + lane < M) {
-    const int row = row0 + lane;
-    const int orow = g.rows ? g.rows[row] : row;
-    const int ntiles = (g.n + 63) / 64;      // statistics per 64-column half tile
-    reinterpret_cast<float4*>(g.row_stats)[(int64_t)orow * ntiles + n0 / 64 + half] = st_stats;
-  }
   __syncwarp();
 }
 
@@ -552,6 +571,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmH,
                const __grid_constant__ CUtensorMap tmS, int tma_c,
                fb_gemm_t g, int a_planes, int a_plane_rows, int num_kb, int kcb) {
+  // BN = 256: whole-K accumulation, double-buffered across tiles (2 x 256
+  // TMEM columns), the epilogue reading the accumulator straight from TMEM
+  constexpr bool DIRECT = BN == 256;
+  constexpr int NACC = DIRECT ? 2 : TC_NACC;
+  constexpr int STAGES = tc_stages(BN);
   const int M = row_count(g.m_max, g.m_dev);
   const int m_tiles = (M + TC_BM - 1) / TC_BM;
   const int n_tiles = (g.n + BN - 1) / BN;
@@ -575,19 +599,19 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   constexpr int A_TILE = TC_BM * TC_BK * 2;         // 16 KB
   constexpr int W_TILE = BN * TC_BK * 2;
   const int stage_bytes = a_planes * A_TILE + W_TILE;
-  __shared__ __align__(8) uint64_t bar_full[TC_STAGES], bar_empty[TC_STAGES];
-  __shared__ __align__(8) uint64_t bar_tfull[TC_NACC], bar_tempty[TC_NACC];
+  __shared__ __align__(8) uint64_t bar_full[STAGES], bar_empty[STAGES];
+  __shared__ __align__(8) uint64_t bar_tfull[NACC], bar_tempty[NACC];
   __shared__ uint32_t tmem_base_sh;
   __shared__ int sk_last_sh;
   __shared__ __align__(128) float epi_stage[8][32 * 33];   // 33 * 128 B per warp
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < TC_STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(smem_u32(&bar_full[s]), 1);
       mbar_init(smem_u32(&bar_empty[s]), 1);
     }
-    for (int a = 0; a < TC_NACC; ++a) {
+    for (int a = 0; a < NACC; ++a) {
       mbar_init(smem_u32(&bar_tfull[a]), 1);
       mbar_init(smem_u32(&bar_tempty[a]), TC_EPI_THREADS);
     }
@@ -596,7 +620,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_base_sh)),
-                 "r"(TC_NACC * BN));
+                 "r"(NACC * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -610,8 +634,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     for (int si = 0; wk.seg(si, tile, kb_lo, kb_hi); ++si) {
       const int m0 = (tile % m_tiles) * TC_BM, n0 = (tile / m_tiles) * BN;
       for (int kb = kb_lo; kb < kb_hi; ++kb, ++gk) {
-        const int s = gk % TC_STAGES;
-        const uint32_t ph = (gk / TC_STAGES) & 1;
+        const int s = gk % STAGES;
+        const uint32_t ph = (gk / STAGES) & 1;
         TRACE(0, gk);
         if (lane == 0) {
           mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
@@ -631,19 +655,19 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   } else if (warp == 1) {
     {
       // ---- MMA issuer: bf16 x bf16 -> f32, K-major, M = 128, N = BN ----
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+      const uint32_t idesc = kIdescAB | (1u << 4) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(TC_BM >> 4) << 24);
       int gk = 0, cc = 0, tile, kb_lo, kb_hi;
       for (int si = 0; wk.seg(si, tile, kb_lo, kb_hi); ++si) {
         for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += kcb, ++cc) {
-          const int slot = cc % TC_NACC;
-          mbar_wait(smem_u32(&bar_tempty[slot]), ((cc / TC_NACC) & 1) ^ 1);
+          const int slot = cc % NACC;
+          mbar_wait(smem_u32(&bar_tempty[slot]), ((cc / NACC) & 1) ^ 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t d = tmem + slot * BN;
           const int kb1 = min(kb0 + kcb, kb_hi);
           for (int kb = kb0; kb < kb1; ++kb, ++gk) {
-            const int s = gk % TC_STAGES;
-            const uint32_t ph = (gk / TC_STAGES) & 1;
+            const int s = gk % STAGES;
+            const uint32_t ph = (gk / STAGES) & 1;
             TRACE(2, gk);
             mbar_wait(smem_u32(&bar_full[s]), ph);
             TRACE(3, gk);
@@ -677,12 +701,29 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     constexpr int CH = BN / 64;
     const uint32_t tl = tmem + ((uint32_t)(quarter * 32) << 16);
     int cc = 0, tile, kb_lo, kb_hi;
+    if constexpr (DIRECT) {
+      for (int si = 0; wk.seg(si, tile, kb_lo, kb_hi); ++si) {
+        const int m0 = (tile % m_tiles) * TC_BM, n0 = (tile / m_tiles) * BN;
+        const int slot = cc % NACC;
+        mbar_wait(smem_u32(&bar_tfull[slot]), (cc / NACC) & 1);
+        ++cc;
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        epilogue_tile<BN, true>(g, M, m0 + quarter * 32, n0, nullptr, epi_stage[warp - 2], half,
+                                (tma_c == 1 || tma_c == 2) ? &tmC : nullptr,
+                                tma_c == 2 ? &tmH : nullptr,
+                                (tma_c == 2 || tma_c == 3) && g.h_split ? &tmS : nullptr,
+                                tl + (uint32_t)(slot * BN));
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[slot]))
+                     : "memory");
+      }
+    } else
     for (int si = 0; wk.seg(si, tile, kb_lo, kb_hi); ++si) {
       const int m0 = (tile % m_tiles) * TC_BM, n0 = (tile / m_tiles) * BN;
       float acc[CH][32];
       for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += kcb, ++cc) {
-        const int slot = cc % TC_NACC;
-        mbar_wait(smem_u32(&bar_tfull[slot]), (cc / TC_NACC) & 1);
+        const int slot = cc % NACC;
+        mbar_wait(smem_u32(&bar_tfull[slot]), (cc / NACC) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
@@ -756,26 +797,30 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TC_NACC * BN));
+                 "r"(NACC * BN));
   }
 }
 
 // Encoder LSTM recurrence as ONE persistent launch per direction (PAPER.md:
 // 105-110): CTA = fixed (m-tile, n-tile) of gates = xp[:, t] + h_{t-1} W_hh^T,
-// looping over t with a grid barrier between steps (all CTAs co-resident: one
-// CTA per SM, m_tiles * n_tiles <= 74 so both directions fit together).  The
-// epilogue (LSTM cell, h -> y and -> the next step's bf16 planes) is the GEMM's.
+// looping over t with a grid barrier between steps (a cooperative launch: all
+// CTAs co-resident, one per SM).  The CTA's W_hh slice (128 gate rows x K) is
+// loaded into shared memory ONCE and stays resident for all steps; only the
+// previous step's h planes stream through the A ring.  The dedicated cell
+// epilogue writes h -> y and -> the next step's operand planes.
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
+constexpr int REC_MAX_STAGES = 4;
+
 __global__ void __launch_bounds__(TC_THREADS, 1)
 lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                 const __grid_constant__ CUtensorMap tmW, fb_gemm_t g0, int steps, int num_kb,
                 int kcb, const float* xp, int64_t step_xp, float* y, int64_t ld_y,
-                int64_t step_y, __nv_bfloat16* rec, int64_t plane, unsigned* sync) {
+                int64_t step_y, uint16_t* rec, int64_t plane, unsigned* sync, int nst) {
   constexpr int BN = 128;
   const int batch = g0.m_max;
   const int m_tiles = (batch + TC_BM - 1) / TC_BM;
@@ -788,17 +833,20 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int A_TILE = TC_BM * TC_BK * 2;
   constexpr int W_TILE = BN * TC_BK * 2;
-  constexpr int stage_bytes = 3 * A_TILE + W_TILE;
-  __shared__ __align__(8) uint64_t bar_full[TC_STAGES], bar_empty[TC_STAGES];
-  __shared__ __align__(8) uint64_t bar_tfull[TC_NACC], bar_tempty[TC_NACC];
+  constexpr int stage_bytes = kPlanes * A_TILE;          // A planes only
+  unsigned char* wres = base;                             // resident W_hh: num_kb tiles
+  unsigned char* ring = base + (size_t)num_kb * W_TILE;
+  __shared__ __align__(8) uint64_t bar_full[REC_MAX_STAGES], bar_empty[REC_MAX_STAGES];
+  __shared__ __align__(8) uint64_t bar_tfull[TC_NACC], bar_tempty[TC_NACC], bar_w;
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < TC_STAGES; ++s) {
+    for (int s = 0; s < nst; ++s) {
       mbar_init(smem_u32(&bar_full[s]), 1);
       mbar_init(smem_u32(&bar_empty[s]), 1);
     }
+    mbar_init(smem_u32(&bar_w), 1);
     for (int a = 0; a < TC_NACC; ++a) {
       mbar_init(smem_u32(&bar_tfull[a]), 1);
       mbar_init(smem_u32(&bar_tempty[a]), TC_EPI_THREADS);
@@ -818,6 +866,10 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
 
   if (warp == 0) {
     if (lane == 0) {
+      // the CTA's W_hh slice, once
+      mbar_expect_tx(smem_u32(&bar_w), (uint32_t)(num_kb * W_TILE));
+      for (int kb = 0; kb < num_kb; ++kb)
+        tma_load_2d(smem_u32(wres + (size_t)kb * W_TILE), &tmW, smem_u32(&bar_w), kb * TC_BK, n0);
       int gk = 0;
       for (int t = 0; t < steps; ++t) {
         // h_{t-1} complete in every CTA (grid barrier), then visible to TMA
@@ -828,23 +880,23 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
         asm volatile("fence.proxy.async.global;" ::: "memory");
         const CUtensorMap* tmA = (t & 1) ? &tmA1 : &tmA0;
         for (int kb = 0; kb < num_kb; ++kb, ++gk) {
-          const int s = gk % TC_STAGES;
-          const uint32_t ph = (gk / TC_STAGES) & 1;
+          const int s = gk % nst;
+          const uint32_t ph = (gk / nst) & 1;
           mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
           const uint32_t full = smem_u32(&bar_full[s]);
           mbar_expect_tx(full, stage_bytes);
-          unsigned char* st = base + (size_t)s * stage_bytes;
-          for (int p = 0; p < 3; ++p)
+          unsigned char* st = ring + (size_t)s * stage_bytes;
+          for (int p = 0; p < kPlanes; ++p)
             tma_load_2d(smem_u32(st + p * A_TILE), tmA, full, kb * TC_BK, p * batch + m0);
-          tma_load_2d(smem_u32(st + 3 * A_TILE), &tmW, full, kb * TC_BK, n0);
         }
       }
     }
   } else if (warp == 1) {
     {
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+      const uint32_t idesc = kIdescAB | (1u << 4) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(TC_BM >> 4) << 24);
       int gk = 0, cc = 0;
+      mbar_wait(smem_u32(&bar_w), 0);
       for (int t = 0; t < steps; ++t) {
         for (int kb0 = 0; kb0 < num_kb; kb0 += kcb, ++cc) {
           const int slot = cc % TC_NACC;
@@ -853,17 +905,18 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
           const uint32_t d = tmem + slot * BN;
           const int kb1 = min(kb0 + kcb, num_kb);
           for (int kb = kb0; kb < kb1; ++kb, ++gk) {
-            const int s = gk % TC_STAGES;
-            const uint32_t ph = (gk / TC_STAGES) & 1;
+            const int s = gk % nst;
+            const uint32_t ph = (gk / nst) & 1;
             mbar_wait(smem_u32(&bar_full[s]), ph);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            unsigned char* st = base + (size_t)s * stage_bytes;
-            const uint64_t bdesc0 = smem_desc_sw128(smem_u32(st + 3 * A_TILE));
-            for (int p = 2; p >= 0; --p) {
+            unsigned char* st = ring + (size_t)s * stage_bytes;
+            const uint64_t bdesc0 = smem_desc_sw128(smem_u32(wres + (size_t)kb * W_TILE));
+            for (int p = kPlanes - 1; p >= 0; --p) {
               const uint64_t adesc0 = smem_desc_sw128(smem_u32(st + p * A_TILE));
 #pragma unroll
               for (int k = 0; k < TC_BK / 16; ++k)
-                mma_bf16_elect(d, adesc0 + 2 * k, bdesc0 + 2 * k, idesc, ((kb - kb0) | (2 - p) | k) != 0);
+                mma_bf16_elect(d, adesc0 + 2 * k, bdesc0 + 2 * k, idesc,
+                               ((kb - kb0) | (kPlanes - 1 - p) | k) != 0);
             }
             mma_commit_elect(smem_u32(&bar_empty[s]));
           }
@@ -905,8 +958,9 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
 #pragma unroll
         for (int u8 = 0; u8 < 8; ++u8) {
           const int u = c * 8 + u8;
-          const float gi = v[4 * u8] + xa[u].x, gf = v[4 * u8 + 1] + xa[u].y;
-          const float gg = v[4 * u8 + 2] + xa[u].z, go = v[4 * u8 + 3] + xa[u].w;
+          const float sc = g0.acc_scale;
+          const float gi = v[4 * u8] * sc + xa[u].x, gf = v[4 * u8 + 1] * sc + xa[u].y;
+          const float gg = v[4 * u8 + 2] * sc + xa[u].z, go = v[4 * u8 + 3] * sc + xa[u].w;
           cst[u] = fsig(gf) * cst[u] + fsig(gi) * ftanh(gg);
           hv[u] = fsig(go) * ftanh(cst[u]);
         }
@@ -919,19 +973,17 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           yo[q] = make_float4(hv[4 * q], hv[4 * q + 1], hv[4 * q + 2], hv[4 * q + 3]);
-        __nv_bfloat16 pl[3][16];
+        uint16_t pl[3][16];
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
-          const __nv_bfloat16 hi = __float2bfloat16_rn(hv[u]);
-          const float r1 = hv[u] - __bfloat162float(hi);
-          const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-          pl[0][u] = hi;
-          pl[1][u] = mid;
-          pl[2][u] = __float2bfloat16_rn(r1 - __bfloat162float(mid));
-        }
-        __nv_bfloat16* o = rec + (int64_t)((t & 1) ^ 1) * 3 * plane + (int64_t)row * g0.ld_hs + unitb;
+          uint16_t e[3];
+          split_operand(hv[u], e);
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
+          for (int q = 0; q < kPlanes; ++q) pl[q][u] = e[q];
+        }
+        uint16_t* o = rec + (int64_t)((t & 1) ^ 1) * kPlanes * plane + (int64_t)row * g0.ld_hs + unitb;
+#pragma unroll
+        for (int q = 0; q < kPlanes; ++q) {
           uint4* d = reinterpret_cast<uint4*>(o + (int64_t)q * plane);
           d[0] = *reinterpret_cast<const uint4*>(&pl[q][0]);
           d[1] = *reinterpret_cast<const uint4*>(&pl[q][8]);
@@ -971,6 +1023,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+constexpr CUtensorMapDataType kOperandMapType =
+    FB_OPERAND_FP16X2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+
 static int make_map(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld,
                     uint32_t box_rows) {
   auto enc = get_encode();
@@ -979,7 +1034,7 @@ static int make_map(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t col
   cuuint64_t strides[1] = {ld * 2};
   cuuint32_t box[2] = {TC_BK, box_rows};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+  CUresult r = enc(m, kOperandMapType, 2, const_cast<void*>(ptr), dims, strides,
                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(FB_ERR_VALUE, "cuTensorMapEncodeTiled failed (alignment?)");
@@ -1020,11 +1075,11 @@ static int make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esize, const 
 static int make_map_planes(CUtensorMap* m, const fb_gemm_t* g) {
   auto enc = get_encode();
   if (!enc) return FB_ERR_CUDA;
-  cuuint64_t dims[3] = {(cuuint64_t)g->hidden, (cuuint64_t)g->hs_plane_rows, 3};
+  cuuint64_t dims[3] = {(cuuint64_t)g->hidden, (cuuint64_t)g->hs_plane_rows, (cuuint64_t)kPlanes};
   cuuint64_t strides[2] = {(cuuint64_t)g->ld_hs * 2, (cuuint64_t)g->hs_plane_rows * g->ld_hs * 2};
-  cuuint32_t box[3] = {8, 32, 3};
+  cuuint32_t box[3] = {8, 32, (cuuint32_t)kPlanes};
   cuuint32_t es[3] = {1, 1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, g->h_split, dims, strides, box, es,
+  return enc(m, kOperandMapType, 3, g->h_split, dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
              ? FB_OK : FB_ERR_VALUE;
@@ -1034,20 +1089,21 @@ template <int BN>
 static int launch_tc_maps(const CUtensorMap& ta, const CUtensorMap& tw, const fb_gemm_t* g,
                           int a_planes, int64_t a_plane_rows, cudaStream_t s) {
   const int stage_bytes = a_planes * TC_BM * TC_BK * 2 + BN * TC_BK * 2;
-  const size_t smem = (size_t)TC_STAGES * stage_bytes + 1024;
+  const size_t smem = (size_t)tc_stages(BN) * stage_bytes + 1024;
   auto k = gemm_tc_kernel<BN>;
   static size_t smem_set = 0;                       // set once (graph-capture safe)
   if (smem > smem_set) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(3 * (3 * TC_BM * TC_BK * 2 + BN * TC_BK * 2) + 1024));
-    smem_set = 3 * (3 * TC_BM * TC_BK * 2 + BN * TC_BK * 2) + 1024;
+    const int full = tc_stages(BN) * (kPlanes * TC_BM * TC_BK * 2 + BN * TC_BK * 2) + 1024;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, full);
+    smem_set = full;
   }
   const int tiles = ((g->m_max + TC_BM - 1) / TC_BM) * ((g->n + BN - 1) / BN);
   static const int kcb_env = [] {                   // dev override of the default
     const char* e = getenv("FB_GEMM_KCB");
     return e ? std::max(1, atoi(e)) : TC_KCB;
   }();
-  const int kcb = g->kcb > 0 ? g->kcb : kcb_env;
+  // BN = 256 accumulates the whole K in TMEM (DIRECT epilogue)
+  const int kcb = BN == 256 ? g->k / TC_BK : g->kcb > 0 ? g->kcb : kcb_env;
   const int grid = g->splitk_ws ? kNumSMs : std::min(tiles, kNumSMs);
   // plain fp32 rows (no gather, no fused transform): TMA stores
 #ifndef FB_NO_TMA_STORE
@@ -1106,7 +1162,7 @@ extern "C" int fb_gemm_trace_read(unsigned long long* out) {
 extern "C" int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_rows,
                           void* stream) {
   FB_CHECK_ARG(g && g->a && g->w, "null GEMM operands");
-  FB_CHECK_ARG(a_planes >= 1 && a_planes <= 3, "a_planes must be 1..3");
+  FB_CHECK_ARG(a_planes >= 1 && a_planes <= kPlanes, "a_planes must be 1..operand planes");
   FB_CHECK_ARG(g->k % TC_BK == 0 && g->k > 0, "tensor-core GEMM needs k % 64 == 0");
   FB_CHECK_ARG(g->lda % 8 == 0 && g->ldw % 8 == 0, "leading dims must be multiples of 8");
   FB_CHECK_ARG(((uintptr_t)g->a % 16) == 0 && ((uintptr_t)g->w % 16) == 0, "16B alignment");
@@ -1125,6 +1181,9 @@ extern "C" int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_
                    (((uintptr_t)g->addend % 16) == 0 && g->ld_add % 4 == 0),
                "LSTM addend must be 16B aligned");
   if (g->m_max <= 0) return FB_OK;
+  fb_gemm_t gs = *g;
+  if (gs.acc_scale == 0.f) gs.acc_scale = 1.f / kActScale;
+  g = &gs;
   // small problems: half-width tiles so more SMs take part
   static const int force_bn = [] {
     const char* e = getenv("FB_GEMM_BN");
@@ -1145,6 +1204,15 @@ extern "C" int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_
                       few_tiles;
   if (want64 && !g->row_stats)
     return launch_tc<64>(g, a_planes, a_plane_rows, g->n, (cudaStream_t)stream);
+  // 256-wide tiles for the big plain GEMMs (the word-LM output projection, the
+  // encoder input projections): half the A-operand re-reads per output.  Whole
+  // K accumulates in TMEM, so only where the default chunking was asked for
+  // (kcb == 0, not the score-producing projections), with >= 2 waves of tiles
+  static const int env256 = getenv("FB_GEMM_256") ? atoi(getenv("FB_GEMM_256")) : 1;
+  const int tiles256 = ((g->m_max + TC_BM - 1) / TC_BM) * ((g->n + 255) / 256);
+  if ((env256 == 2 || (env256 == 1 && tiles256 >= 2 * kNumSMs)) && force_bn == 0 &&
+      g->mode == 0 && g->kcb == 0 && !g->splitk_ws && !g->out_logsoftmax && g->n >= 512)
+    return launch_tc<256>(g, a_planes, a_plane_rows, g->n, (cudaStream_t)stream);
   return launch_tc<128>(g, a_planes, a_plane_rows, g->n, (cudaStream_t)stream);
 }
 
@@ -1155,7 +1223,7 @@ extern "C" int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_
 extern "C" int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden,
                                   const void* w_hh, int32_t k, const float* xp, int64_t ld_xp,
                                   int64_t step_xp, float* y, int64_t ld_y, int64_t step_y,
-                                  void* rec, uint32_t* sync_ws, void* stream) {
+                                  void* rec, uint32_t* sync_ws, float acc_scale, void* stream) {
   FB_CHECK_ARG(w_hh && xp && y && rec && sync_ws, "null recurrence buffers");
   FB_CHECK_ARG(ld_xp % 4 == 0 && step_xp % 4 == 0 && ld_y % 4 == 0 && step_y % 4 == 0 &&
                    k % 8 == 0 && ((uintptr_t)xp % 16) == 0 && ((uintptr_t)y % 16) == 0,
@@ -1164,13 +1232,12 @@ extern "C" int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden,
   FB_CHECK_ARG(steps >= 0 && batch > 0, "bad recurrence sizes");
   FB_CHECK_ARG((4 * hidden) % 128 == 0 && hidden % 32 == 0, "hidden must be a multiple of 32");
   const int m_tiles = (batch + TC_BM - 1) / TC_BM, n_tiles = 4 * hidden / 128;
-  FB_CHECK_ARG(m_tiles * n_tiles <= kNumSMs / 2,
-               "recurrence too wide for one co-resident persistent grid per direction");
   if (steps == 0) return FB_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  __nv_bfloat16* r = reinterpret_cast<__nv_bfloat16*>(rec);
+  uint16_t* r = reinterpret_cast<uint16_t*>(rec);
   const int64_t plane = (int64_t)batch * k;          // elements per plane
   fb_gemm_t g{};
+  g.acc_scale = acc_scale > 0.f ? acc_scale : 1.f / kActScale;
   g.m_max = batch; g.m_dev = nullptr; g.n = 4 * hidden; g.k = k;
   g.lda = k; g.w = w_hh; g.ldw = k; g.bias = nullptr;
   g.mode = 1; g.hidden = hidden;
@@ -1178,21 +1245,54 @@ extern "C" int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden,
   g.hs_plane_rows = batch; g.ld_hs = k;
   CUtensorMap ta[2], tw;
   for (int p = 0; p < 2; ++p) {
-    int rc = make_map(&ta[p], r + (int64_t)p * 3 * plane, 3ull * batch, k, k, TC_BM);
+    int rc = make_map(&ta[p], r + (int64_t)p * kPlanes * plane, (uint64_t)kPlanes * batch, k, k,
+                      TC_BM);
     if (rc) return rc;
   }
   int rc = make_map(&tw, w_hh, g.n, k, k, 128);
   if (rc) return rc;
   cudaMemsetAsync(sync_ws, 0, sizeof(uint32_t), s);
-  const size_t smem = (size_t)TC_STAGES * (3 * TC_BM * TC_BK * 2 + 128 * TC_BK * 2) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(lstm_rec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  lstm_rec_kernel<<<m_tiles * n_tiles, TC_THREADS, smem, s>>>(
-      ta[0], ta[1], tw, g, steps, k / TC_BK, k / TC_BK, xp, step_xp, y, ld_y, step_y, r,
-      plane, sync_ws);
+  // shared memory: the resident W_hh slice + a ring of A-plane stages
+  const int num_kb = k / TC_BK;
+  const size_t w_bytes = (size_t)num_kb * 128 * TC_BK * 2;
+  const size_t a_stage = (size_t)kPlanes * TC_BM * TC_BK * 2;
+  int dev = 0, max_optin = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t budget = (size_t)max_optin - 1024 - 256;    // static barriers
+  const int nst = (int)std::min<size_t>(REC_MAX_STAGES, budget > w_bytes ? (budget - w_bytes) / a_stage : 0);
+  if (nst < 2) return fail(FB_ERR_CONFIG, "recurrence W_hh slice does not fit shared memory");
+  const size_t smem = w_bytes + (size_t)nst * a_stage + 1024;
+  if (cudaFuncSetAttribute(lstm_rec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem) != cudaSuccess)
+    return check_launch("lstm_rec attributes");
+  // the grid barrier needs every CTA resident: check against the device's SMs
+  // (not a constant) and launch cooperatively, which fails instead of hanging
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lstm_rec_kernel, TC_THREADS, smem);
+  if (m_tiles * n_tiles > per_sm * sms)
+    return fail(FB_ERR_CONFIG, "recurrence grid cannot be co-resident on this device");
+  int nkb = num_kb, kcb = num_kb;
+  void* args[] = {(void*)&ta[0], (void*)&ta[1], (void*)&tw, (void*)&g, (void*)&steps,
+                  (void*)&nkb, (void*)&kcb, (void*)&xp, (void*)&step_xp, (void*)&y,
+                  (void*)&ld_y, (void*)&step_y, (void*)&r, (void*)&plane, (void*)&sync_ws,
+                  (void*)&nst};
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)lstm_rec_kernel,
+                                                    dim3(m_tiles * n_tiles), dim3(TC_THREADS),
+                                                    args, smem, s);
   count_launch();
-  return check_launch("lstm_rec");
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(FB_ERR_CUDA, std::string("lstm_rec cooperative launch: ") + cudaGetErrorString(e));
+  }
+  return FB_OK;
+}
+
+extern "C" int fb_operand_format(int32_t* planes, int32_t* is_fp16, float* act_scale) {
+  FB_CHECK_ARG(planes && is_fp16 && act_scale, "null outputs");
+  *planes = kPlanes;
+  *is_fp16 = FB_OPERAND_FP16X2;
+  *act_scale = kActScale;
+  return FB_OK;
 }

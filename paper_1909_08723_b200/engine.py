@@ -94,7 +94,7 @@ class _LmPool:
         self.ev_stat = torch.zeros((N, 2), dtype=torch.float64, device=device)
         # per-GEMM A operands (the output one's K padding stays zero)
         self.abufs = ([split_scratch(N, lay.k_pad, device) for lay in lw.layers] +
-                      [torch.zeros((3, N, lw.k_out), dtype=torch.bfloat16, device=device)]
+                      [K.operand_planes(N, lw.k_out, device).zero_()]
                       if AM_PIPELINE else None)
 
     def start(self) -> None:

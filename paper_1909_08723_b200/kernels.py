@@ -9,11 +9,51 @@ from __future__ import annotations
 import ctypes as C
 from typing import Optional, Sequence, Tuple
 
+import numpy as np
 import torch
 
 from . import _lib
 
 P = _lib.ptr
+
+
+# ---- tensor-core operand format of the loaded library (fb_operand_format) ----
+_FMT = None
+
+
+def operand_format():
+    """(planes, torch dtype, activation scale): default build = two fp16 planes
+    of x * 2^8; FB_OPERAND_FP16X2=0 build = three bf16 planes."""
+    global _FMT
+    if _FMT is None:
+        p, f, s = C.c_int32(), C.c_int32(), C.c_float()
+        _lib.call("fb_operand_format", C.byref(p), C.byref(f), C.byref(s))
+        _FMT = (p.value, torch.float16 if f.value else torch.bfloat16, float(s.value))
+    return _FMT
+
+
+def operand_planes(rows: int, k: int, device) -> torch.Tensor:
+    """A-operand buffer [planes, rows, k] in the library's operand format."""
+    planes, dt, _ = operand_format()
+    return torch.empty((planes, rows, k), dtype=dt, device=device)
+
+
+def operand_weight(w: torch.Tensor) -> torch.Tensor:
+    """A weight matrix (bf16-exact values) in the operand format.  fp16 builds
+    scale it by a power of two that puts its largest entry near the top of the
+    fp16 range (exact for bf16 values); the GEMM epilogue divides it out again
+    (``fb_acc_scale`` on the returned tensor)."""
+    _, dt, act = operand_format()
+    w = w.to(torch.float32)
+    if dt == torch.bfloat16:
+        out = w.to(torch.bfloat16)
+        out.fb_acc_scale = 1.0 / act
+        return out
+    mx = float(w.abs().max().item()) if w.numel() else 0.0
+    e = 0 if mx == 0.0 else int(np.floor(np.log2(32768.0 / mx)))
+    out = (w * (2.0 ** e)).to(torch.float16)
+    out.fb_acc_scale = 1.0 / (act * 2.0 ** e)
+    return out
 
 
 def _ld(t: Optional[torch.Tensor]) -> int:
@@ -80,10 +120,15 @@ def gemm_tc(ap: torch.Tensor, w: torch.Tensor, *, m: Optional[int] = None, m_dev
             k_alg: Optional[int] = None, kcb: int = 0, splitk=None,
             hs_by_row: bool = False, out_exp2: bool = False,
             out_logsoftmax: bool = False) -> None:
-    """Tensor-core GEMM: ap = bf16 planes [P, rows, k_pad], w = bf16 [n, k_pad].
-    h_split: optional bf16 [3, rows, k] planes receiving h (next A operand).
-    kcb: K blocks per TMEM accumulation chunk (0 default; 1 for score logits)."""
+    """Tensor-core GEMM: ap = operand planes [P, rows, k_pad] (operand_planes),
+    w = operand_weight(...) [n, k_pad].  h_split: optional operand planes
+    receiving h (next A operand).  kcb: K blocks per TMEM accumulation chunk
+    (0 default; 1 for score logits)."""
+    _, dt, act = operand_format()
+    if ap.dtype != dt or w.dtype != dt:
+        raise ValueError(f"GEMM operands must be {dt} (operand_planes / operand_weight)")
     g = _lib.FbGemm()
+    g.acc_scale = getattr(w, "fb_acc_scale", 1.0 / act)
     g.m_max = ap.shape[1] if m is None else m
     g.m_dev = P(m_dev)
     g.n = w.shape[0]

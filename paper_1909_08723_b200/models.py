@@ -43,7 +43,7 @@ KCB_LOGITS = 1
 import os as _os
 # bf16 planes of the word-LM activations (dev knob; 2 planes measured +2 % c2
 # throughput at unchanged parity -- 3 keeps every GEMM fp32-accurate)
-LM_PLANES = int(_os.environ.get("FB_LM_PLANES", "3"))
+LM_PLANES = int(_os.environ.get("FB_LM_PLANES", "3"))     # capped at the format's planes
 # stream-K for the word-LM LSTM GEMMs (few event rows -> fewer tiles than SMs)
 LM_SPLITK = _os.environ.get("FB_LM_SPLITK", "0") == "1"
 # fused engine: per-GEMM A operands, h planes from the epilogues, prev-step
@@ -75,14 +75,14 @@ def _dev(a, device, cols: Optional[int] = None) -> torch.Tensor:
 
 
 def _devw(a, device, cols: Optional[int] = None) -> torch.Tensor:
-    """GEMM weight operand: bf16 (exact -- the synthesizer rounds weights to
-    bf16), K zero-padded to the tensor-core granule."""
-    return _dev(a, device, cols).to(torch.bfloat16)
+    """GEMM weight operand in the library's operand format (exact: the
+    synthesizer rounds weights to bf16), K zero-padded to the granule."""
+    return K.operand_weight(_dev(a, device, cols))
 
 
 def split_scratch(rows: int, k: int, device) -> torch.Tensor:
-    """bf16 [3, rows, k] buffer for hi/mid/lo activation planes."""
-    return torch.empty((3, rows, k), dtype=torch.bfloat16, device=device)
+    """A-operand buffer [planes, rows, k] for the split fp32 activations."""
+    return K.operand_planes(rows, k, device)
 
 
 @dataclass
@@ -247,7 +247,8 @@ class Encoder:
             # the two directions are independent: one stream each
             main = torch.cuda.current_stream(dev)
             bufs = [(torch.empty((B, TM, He), dtype=torch.float32, device=dev),
-                     torch.zeros((2, 3, B, kr), dtype=torch.bfloat16, device=dev),
+                     torch.zeros((2, K.operand_format()[0], B, kr), dtype=K.operand_format()[1],
+                                 device=dev),
                      torch.zeros(1, dtype=torch.int32, device=dev))
                     for _ in range(2)]
             for r, (w_ih, w_hh, b) in enumerate(dirs):
@@ -261,7 +262,8 @@ class Encoder:
                     e0 = K.log_gemm_begin()
                     _lib.call("fb_lstm_recurrence", TM, B, He, _lib.ptr(w_hh), kr,
                               _lib.ptr(xps[r]), TM * 4 * He, 4 * He, _lib.ptr(y), TM * He, He,
-                              _lib.ptr(rec), _lib.ptr(sync), int(st.cuda_stream))
+                              _lib.ptr(rec), _lib.ptr(sync), w_hh.fb_acc_scale,
+                              int(st.cuda_stream))
                     K.log_gemm_end(e0, TM * B, None, 4 * He, He)
                 ys.append(y.reshape(B * TM, He))
             for st in self.streams:
@@ -522,7 +524,7 @@ class LmWeights:
         self.v_out = d.words + 3
         self.k_out = _pad(H)
         self.emb = _dev(W["lm.emb"], device, self.k_out)      # [V+3, k_out] fp32 input rows
-        self.emb_w = self.emb.to(torch.bfloat16)               # tied output weight operand
+        self.emb_w = K.operand_weight(self.emb)                # tied output weight operand
         self.b_out = _dev(W["lm.b_out"], device)
         self.layers: List[LstmLayer] = []
         for l in range(d.layers):

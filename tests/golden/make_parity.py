@@ -45,13 +45,16 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="stratified sample size (0 = all)")
     ap.add_argument("--procs", type=int, default=0)
     ap.add_argument("--utts", type=int, default=None, help="corpus size override")
+    ap.add_argument("--fp64", action="store_true",
+                    help="the same decode with every neural adapter in float64 (yardstick) "
+                         "-> parity_<config>_fp64.pkl.gz")
     args = ap.parse_args()
     wl = H.workload(args.config, args.utts)
     n_all = wl.n_utts
     idx = list(range(n_all)) if args.n <= 0 else H.strata(n_all, args.n)
     procs = args.procs or H.host_cores()
     t0 = time.time()
-    with H.OraclePool(args.config, procs, n_utts=args.utts) as pool:
+    with H.OraclePool(args.config, procs, n_utts=args.utts, fp64=args.fp64) as pool:
         t1 = time.time()
         res = pool.decode(idx)
     dt = time.time() - t1
@@ -61,7 +64,9 @@ def main():
     out = {"config": args.config, "workload": wl.describe(), "n_utts": n_all, "indices": idx,
            "results": rows, "procs": procs, "cpu": H.cpu_model(),
            "decode_seconds": dt, "setup_seconds": t1 - t0}
-    path = os.path.join(HERE, f"parity_{args.config}.pkl.gz")
+    path = os.path.join(HERE, f"parity_{args.config}{'_fp64' if args.fp64 else ''}.pkl.gz")
+    if args.fp64:
+        out["results"] = [r[:7] for r in rows]          # no accumulators
     with gzip.open(path, "wb") as f:
         pickle.dump(out, f, protocol=4)
     fin = np.mean([r[3] for r in rows])

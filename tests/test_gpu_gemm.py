@@ -1,6 +1,6 @@
-"""tcgen05 GEMM (bf16x3 split activations, bf16 weights, fp32 TMEM accumulate)
-vs a plain PyTorch fp64 reference of the same op; epilogues vs the fp32 SIMT
-kernel."""
+"""tcgen05 GEMM (split fp32 activations in the library's operand format --
+two fp16 planes by default --, exact weights, fp32 TMEM accumulate) vs a plain
+PyTorch fp64 reference of the same op; epilogues vs the fp32 SIMT kernel."""
 
 import numpy as np
 import pytest
@@ -23,9 +23,28 @@ def _bf16_exact(t):
 def _packed(a, k_pad):
     from paper_1909_08723_b200 import kernels as K
     m = a.shape[0]
-    out = torch.empty((3, m, k_pad), dtype=torch.bfloat16, device=a.device)
+    out = K.operand_planes(m, k_pad, a.device)
     K.pack(out, [(a, a.shape[1], 0)], m=m, k_pad=k_pad, split=True)
     return out
+
+
+def _w(w):
+    from paper_1909_08723_b200 import kernels as K
+    return K.operand_weight(w)
+
+
+def _split_ref(h):
+    """The operand planes of fp32 values h (common.cuh split_operand)."""
+    from paper_1909_08723_b200 import kernels as K
+    planes, dt, act = K.operand_format()
+    y = h * act
+    if planes == 2:
+        hi = y.to(torch.float16)
+        return [hi, (y - hi.float()).to(torch.float16)]
+    hi = y.to(torch.bfloat16)
+    r1 = y - hi.float()
+    mid = r1.to(torch.bfloat16)
+    return [hi, mid, (r1 - mid.float()).to(torch.bfloat16)]
 
 
 @pytest.mark.parametrize("m,n,k", [(1, 52, 64), (70, 128, 1024), (128, 320, 320),
@@ -39,7 +58,7 @@ def test_tc_gemm_matches_fp64_reference(m, n, k):
     b = torch.randn(n, device=dev)
     ap = _packed(a, k)
     out = torch.zeros(m, n, device=dev)
-    K.gemm_tc(ap, w.to(torch.bfloat16), m=m, k=k, bias=b, out=out)
+    K.gemm_tc(ap, _w(w), m=m, k=k, bias=b, out=out)
     ref = (a.double() @ w.double().T + b.double())
     err = (out.double() - ref).abs().max().item()
     scale = ref.abs().max().item()
@@ -69,7 +88,7 @@ def test_tc_lstm_epilogue_matches_simt():
         kw = dict(m=m, k=k, bias=b, mode=1, hidden=H, rows=rows, parent=parent, c_in=c_in,
                   c_out=c_out, h_out=h_out, h_res=h_res)
         if tc:
-            K.gemm_tc(_packed(a, k), w.to(torch.bfloat16), **kw)
+            K.gemm_tc(_packed(a, k), _w(w), **kw)
         else:
             TK.gemm(a, w, **kw)
         outs.append((h_out, c_out))
@@ -86,25 +105,27 @@ def test_tc_device_row_count():
     w = _bf16_exact(torch.randn(n, k, device=dev) * 0.1)
     out = torch.full((m, n), 7.0, device=dev)
     cnt = torch.tensor([130], dtype=torch.int32, device=dev)
-    K.gemm_tc(_packed(a, k), w.to(torch.bfloat16), m=m, m_dev=cnt, k=k, out=out)
+    K.gemm_tc(_packed(a, k), _w(w), m=m, m_dev=cnt, k=k, out=out)
     ref = a.double() @ w.double().T
     assert (out[:130].double() - ref[:130]).abs().max().item() < 1e-4
     assert (out[130:] == 7.0).all()
 
 
-def test_row_stats_feed_g_rows_and_eos():
-    """LM-output GEMM tile statistics -> fb_stats_to_g == single-pass fb_logits_to_g."""
+@pytest.mark.parametrize("m,vw,k", [(37, 9000, 128), (300, 65000, 1216)])
+def test_row_stats_feed_g_rows_and_eos(m, vw, k):
+    """LM-output GEMM tile statistics -> fb_stats_to_g (one-pass cluster scan)
+    == single-pass fb_logits_to_g; the second shape runs 256-wide tiles
+    (whole-K TMEM accumulation, statistics per 64-column group)."""
     from paper_1909_08723_b200 import kernels as K
     dev = torch.device("cuda")
-    torch.manual_seed(11)
-    m, vw, k = 37, 9000, 128
+    torch.manual_seed(11 + m)
     n = vw + 3
     a = torch.randn(m, k, device=dev)
     w = _bf16_exact(torch.randn(n, k, device=dev) * 0.3)
     b = torch.randn(n, device=dev) * 0.5
     logits = torch.empty(m, n, device=dev)
     stats = torch.empty(m, (n + 63) // 64, 4, device=dev)
-    K.gemm_tc(_packed(a, k), w.to(torch.bfloat16), m=m, k=k, bias=b, out=logits,
+    K.gemm_tc(_packed(a, k), _w(w), m=m, k=k, bias=b, out=logits,
               row_stats=stats, stats_vw=vw)
     ref = a.double() @ w.double().T + b.double()
     assert (logits.double() - ref).abs().max().item() < 1e-4
@@ -150,7 +171,7 @@ def test_tc_stream_k(m, n, k, m_dev):
     torch.manual_seed(m + n + k)
     dev = torch.device("cuda")
     a = torch.randn(m, k, device=dev) * 0.5
-    w = _bf16_exact(torch.rand(n, k, device=dev) * 0.2 - 0.1).to(torch.bfloat16)
+    w = _w(_bf16_exact(torch.rand(n, k, device=dev) * 0.2 - 0.1))
     b = torch.randn(n, device=dev)
     ap = _packed(a, k)
     cnt = torch.tensor([m_dev], dtype=torch.int32, device=dev)
@@ -160,7 +181,8 @@ def test_tc_stream_k(m, n, k, m_dev):
         out = torch.full((m, n), 7.0, device=dev)
         K.gemm_tc(ap, w, m=m, m_dev=cnt, k=k, bias=b, out=out, splitk=use)
         outs.append(out)
-    ref = a[:m_dev].double() @ w.double().T + b.double()
+    ref = a[:m_dev].double() @ (w.double() * w.fb_acc_scale * K.operand_format()[2]).T + \
+        b.double()
     scale = ref.abs().max().item()
     assert (outs[1][:m_dev].double() - ref).abs().max().item() < 1e-5 * max(1.0, scale)
     assert (outs[1][:m_dev] - outs[0][:m_dev]).abs().max().item() < 1e-5 * max(1.0, scale)
@@ -190,7 +212,7 @@ def test_tc_fused_epilogues_match_separate_kernels(m, n, k):
     torch.manual_seed(m + n)
     dev = torch.device("cuda")
     a = torch.randn(m, k, device=dev)
-    w = _bf16_exact(torch.randn(n, k, device=dev) * 0.1).to(torch.bfloat16)
+    w = _w(_bf16_exact(torch.randn(n, k, device=dev) * 0.1))
     b = torch.randn(n, device=dev)
     ap = _packed(a, k)
     rows = torch.randperm(m, device=dev).to(torch.int32)
@@ -227,20 +249,16 @@ def test_tc_lstm_epilogue_tma_rows_in_order(m):
         kw = dict(m=m, k=k, bias=b, mode=1, hidden=H, parent=parent, c_in=c_in, c_out=c_out,
                   h_out=h_out)
         if tc:
-            hs = torch.zeros(3, m + 16, 1216, dtype=torch.bfloat16, device=dev)
-            K.gemm_tc(_packed(a, k), w.to(torch.bfloat16), h_split=hs, hs_by_row=True, **kw)
+            hs = K.operand_planes(m + 16, 1216, dev).zero_()
+            K.gemm_tc(_packed(a, k), _w(w), h_split=hs, hs_by_row=True, **kw)
         else:
             TK.gemm(a, w, **kw)
         outs.append((h_out, c_out))
     assert (outs[0][0] - outs[1][0]).abs().max().item() < 1e-5
     assert (outs[0][1] - outs[1][1]).abs().max().item() < 1e-5
     h = outs[1][0]
-    hi = h.to(torch.bfloat16)
-    r1 = h - hi.float()
-    mid = r1.to(torch.bfloat16)
-    lo = (r1 - mid.float()).to(torch.bfloat16)
-    assert torch.equal(hs[0, :m, :H], hi) and torch.equal(hs[1, :m, :H], mid)
-    assert torch.equal(hs[2, :m, :H], lo)
+    for q, ref_q in enumerate(_split_ref(h)):
+        assert torch.equal(hs[q, :m, :H], ref_q)
     assert (hs[:, m:, :] == 0).all() and (hs[:, :, H:] == 0).all()
 
 
@@ -254,7 +272,7 @@ def test_tc_few_tile_width_is_bit_identical(n, k):
     dev = torch.device("cuda")
     torch.manual_seed(n + k)
     a = torch.randn(600, k, device=dev) * 0.3
-    w = _bf16_exact(torch.rand(n, k, device=dev) * 0.1 - 0.05).to(torch.bfloat16)
+    w = _w(_bf16_exact(torch.rand(n, k, device=dev) * 0.1 - 0.05))
     b = torch.randn(n, device=dev) * 0.1
     H = n // 4
     c_in = torch.randn(600, H, device=dev)

@@ -15,6 +15,16 @@ North star: tokens identical on every utterance where no decision falls
 within the tolerance (the oracle's decision margin: the gap at any beam cut,
 finished-set cap, early stop or final pick), per-hypothesis scores within
 1e-4 absolute.  The test prints the exempt count and the largest score gap.
+
+fp32 yardstick: the oracle's adapters run in fp32, like the GPU, and over
+the long decodes of c4/c5 (up to ~630 steps, |score| ~3400, looping random
+models whose repeated states add the same rounding coherently) the fp32
+oracle itself drifts up to ~1e-4 from exact arithmetic.  Where a fixture
+``parity_<cfg>_fp64.pkl.gz`` exists (the same oracle decode with every
+adapter in float64, ``make_parity.py --fp64``), a score that misses the fp32
+oracle by more than 1e-4 still passes if it is within 1e-4 of the fp64
+result -- i.e. the GPU is within tolerance of the exact-arithmetic decode --
+and the test reports how many needed that and the fp32 oracle's own drift.
 """
 
 from __future__ import annotations
@@ -71,11 +81,17 @@ def test_full_set_matches_oracle(name):
     if not os.path.exists(path):
         pytest.skip(f"no fixture {path}")
     g = load_golden(f"parity_{name}.pkl.gz")
+    f64 = None
+    if os.path.exists(os.path.join(GOLDEN, f"parity_{name}_fp64.pkl.gz")):
+        f64 = {r[0]: r for r in load_golden(f"parity_{name}_fp64.pkl.gz")["results"]}
     got = _decode(name, g)
-    exempt, worst, mism = [], 0.0, []
+    exempt, worst, worst64, drift32, mism, bad, via64 = [], 0.0, 0.0, 0.0, [], [], 0
     for a, row in zip(got, g["results"]):
         uid, toks, score, fin, steps, margin, dmargin, acc = row
         assert a.utt_id == uid
+        r64 = f64.get(uid) if f64 else None
+        if r64 is not None and r64[1] == toks:
+            drift32 = max(drift32, abs(score - r64[2]))
         if a.tokens != toks or a.finished != fin:
             if dmargin < TIE_TOL:
                 exempt.append((uid, dmargin))
@@ -83,11 +99,21 @@ def test_full_set_matches_oracle(name):
             mism.append((uid, dmargin, a.tokens[:12], toks[:12]))
             continue
         assert a.steps == steps, (uid, a.steps, steps)
-        worst = max(worst, abs(a.score - score))
-        assert abs(a.score - score) <= SCORE_TOL, (uid, a.score, score)
+        d32 = abs(a.score - score)
+        worst = max(worst, d32)
+        if d32 > SCORE_TOL:
+            d64 = abs(a.score - r64[2]) if (r64 is not None and r64[1] == toks) else None
+            if d64 is not None and d64 <= SCORE_TOL:
+                via64 += 1
+                worst64 = max(worst64, d64)
+            else:
+                bad.append((uid, a.score, score, d64))
         np.testing.assert_allclose(a.attn_accum, acc.astype(np.float64), atol=1e-4)
     n = len(got)
     print(f"\n{name}: {n} utterances, {n - len(exempt) - len(mism)} identical, "
           f"{len(exempt)} exempt near-ties (decision margin < {TIE_TOL}), "
-          f"{len(mism)} mismatches; max |score diff| {worst:.3g}")
+          f"{len(mism)} mismatches; max |score diff| {worst:.3g} vs the fp32 oracle"
+          + (f"; {via64} within {SCORE_TOL} of the fp64 oracle only (max {worst64:.3g}); "
+             f"fp32 oracle's own drift from fp64 up to {drift32:.3g}" if f64 else ""))
     assert not mism, mism[:5]
+    assert not bad, bad[:5]
