@@ -459,7 +459,7 @@ def main():
             "share_of_decode": round(g_ms / max(ms, 1e-9), 3),
             "tensor_work_frac_incl_split": round(3 * ach / peak, 4),
             "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel inside a long step)",
-            "per_kernel_ncu": _profile_json("r2_kernel_roofline.json")}
+            "per_kernel_ncu": _profile_json("round2_kernel_roofline.json")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -480,7 +480,7 @@ def main():
                            "list, fresh LookaheadFusion per batch, final gather)",
                     "tokens_equal_resident": e2e_same},
             "roofline": roof, "cpu_baseline": cpu, "gpu_launches": int(launches),
-            "clocks": clk, "stage_split_ncu": _profile_json("r2_stage_split.json"),
+            "clocks": clk, "stage_split_ncu": _profile_json("round2_stage_split.json"),
             "decode_steps_mean": float(np.mean([r.steps for r in res])),
             "finished_frac": float(np.mean([r.finished for r in res])),
         }

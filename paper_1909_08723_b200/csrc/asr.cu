@@ -122,12 +122,15 @@ __global__ void log_softmax_kernel(int m_max, const int32_t* __restrict__ m_dev,
     float mx = -INFINITY;
     for (int j = lane; j < n; j += 32) mx = fmaxf(mx, xr[j]);
     for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    float s = 0.f;
-    for (int j = lane; j < n; j += 32) s += expf(xr[j] - mx);
+    // the normaliser accumulates in fp64: over thousands of outputs an fp32
+    // sum drops every term below half an ulp of the running sum, which biases
+    // log P upward by ~1e-7 per step -- coherent over a long decode
+    double s = 0.0;
+    for (int j = lane; j < n; j += 32) s += (double)expf(xr[j] - mx);
     for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    const float lse = logf(s);
+    const double lse = log(s);
     float* o = out + (int64_t)r * ldo;
-    for (int j = lane; j < n; j += 32) o[j] = (xr[j] - mx) - lse;
+    for (int j = lane; j < n; j += 32) o[j] = (float)((double)(xr[j] - mx) - lse);
   }
 }
 

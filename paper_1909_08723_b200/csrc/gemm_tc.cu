@@ -48,7 +48,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;            // 64 bf16 = 128 B = one swizzle atom
 constexpr int TC_STAGES = kPlanes == 2 ? 4 : 3;   // smem ring: 4 x 48 KB or 3 x 64 KB
-// stages of the GEMM ring for a tile width (4 x 48 KB .. 2 x 80 KB, + the 33 KB
+// stages of the GEMM ring for a tile width (4 x 48 KB or 3 x 64 KB, + the 33 KB
 // epilogue staging within the 227 KB of a CTA)
 constexpr int tc_stages(int bn) {
   return (kPlanes * 128 * 64 * 2 + bn * 64 * 2) <= 48 * 1024 ? 4
@@ -182,16 +182,13 @@ __device__ __forceinline__ void store_split(const fb_gemm_t& g, int64_t row, int
 // One warp drains its 32 TMEM lanes (rows) chunk by chunk; each 32x32 chunk is
 // transposed through shared memory so global loads/stores are row-contiguous
 // across the warp (plain mode: lane = column; LSTM mode: lane = (row, unit)).
-// DIRECT (BN = 256): the whole-K accumulator is read chunk by chunk straight
-// from TMEM at tsrc (no register-resident chunk sums).
-template <int BN, bool DIRECT = false>
+template <int BN>
 __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row0, int n0,
                                               const float (*acc)[32],
                                               float* st /* [32][33] */, int half,
                                               const CUtensorMap* tmC = nullptr,
                                               const CUtensorMap* tmH = nullptr,
-                                              const CUtensorMap* tmS = nullptr,
-                                              uint32_t tsrc = 0) {
+                                              const CUtensorMap* tmS = nullptr) {
   const int lane = threadIdx.x & 31;
   // {max_all, sum_all, max_words, sum_words} of this lane's row over the
   // warp's half of the tile (BN/2 columns)
@@ -210,14 +207,8 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
   for (int c = 0; c < CH; ++c) {
     const int cb = half * CH + c;
     float v[32];
-    if constexpr (DIRECT) {
-      tmem_ld32(tsrc + (uint32_t)(cb * 32), v);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] *= g.acc_scale;               // exact power of 2
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = acc[c][j] * g.acc_scale;
-    }
+    for (int j = 0; j < 32; ++j) v[j] = acc[c][j] * g.acc_scale;     // exact power of 2
     __syncwarp();
     const int nb = n0 + cb * 32;
     if (g.mode == 0 && g.bias) {
@@ -249,8 +240,10 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
         st_stats.z = m2;
       }
       if (c & 1) {
-        // one 64-column statistics group done (n0/64 + half for BN = 128)
-        if (row0 + lane < M) {
+        // one 64-column statistics group done (n0/64 + half for BN = 128); a
+        // group wholly past n (the second half of the last tile when n % 128
+        // <= 64) has no slot: writing it would land on the next row's group 0
+        if (row0 + lane < M && n0 + (cb - 1) * 32 < g.n) {
           const int orow = g.rows ? g.rows[row0 + lane] : row0 + lane;
           const int ntiles = (g.n + 63) / 64;
           reinterpret_cast<float4*>(g.row_stats)[(int64_t)orow * ntiles + (n0 + (cb - 1) * 32) / 64] =
@@ -283,21 +276,25 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
           if (j < g.n) mx = fmaxf(mx, lo[j]);
           if (j + 32 < g.n) mx = fmaxf(mx, hi[j]);
         }
-        float p[32];
+        // fp64 normaliser, the exact sum order of log_softmax_kernel: lane l's
+        // e_l + e_{l+32}, then the xor butterfly -- a binary tree over the 32
+        // partials in bit-reversed leaf order, merged on a 5-deep stack
+        double stk[5];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          float s = 0.f;
-          if (j < g.n) s += expf(lo[j] - mx);
-          if (j + 32 < g.n) s += expf(hi[j] - mx);
-          p[j] = s;
+        for (int k = 0; k < 32; ++k) {
+          const int j = ((k & 1) << 4) | ((k & 2) << 2) | (k & 4) | ((k & 8) >> 2) | ((k & 16) >> 4);
+          double d = 0.0;
+          if (j < g.n) d += (double)expf(lo[j] - mx);
+          if (j + 32 < g.n) d += (double)expf(hi[j] - mx);
+          int depth = __popc(k) ;                      // stack height before this leaf
+#pragma unroll
+          for (int c = k, t = depth; c & 1; c >>= 1) d = stk[--t] + d;
+          stk[__popc(k + 1) - 1] = d;
+          (void)depth;
         }
+        const double lse = log(stk[0]);
 #pragma unroll
-        for (int off = 16; off; off >>= 1)
-#pragma unroll
-          for (int j = 0; j < off; ++j) p[j] = p[j] + p[j + off];
-        const float lse = logf(p[0]);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = (v[j] - mx) - lse;
+        for (int j = 0; j < 32; ++j) v[j] = (float)((double)(v[j] - mx) - lse);
       }
     }
     if (nb >= g.n) continue;
@@ -571,10 +568,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmH,
                const __grid_constant__ CUtensorMap tmS, int tma_c,
                fb_gemm_t g, int a_planes, int a_plane_rows, int num_kb, int kcb) {
-  // BN = 256: whole-K accumulation, double-buffered across tiles (2 x 256
-  // TMEM columns), the epilogue reading the accumulator straight from TMEM
-  constexpr bool DIRECT = BN == 256;
-  constexpr int NACC = DIRECT ? 2 : TC_NACC;
+  constexpr int NACC = TC_NACC;
   constexpr int STAGES = tc_stages(BN);
   const int M = row_count(g.m_max, g.m_dev);
   const int m_tiles = (M + TC_BM - 1) / TC_BM;
@@ -701,23 +695,6 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     constexpr int CH = BN / 64;
     const uint32_t tl = tmem + ((uint32_t)(quarter * 32) << 16);
     int cc = 0, tile, kb_lo, kb_hi;
-    if constexpr (DIRECT) {
-      for (int si = 0; wk.seg(si, tile, kb_lo, kb_hi); ++si) {
-        const int m0 = (tile % m_tiles) * TC_BM, n0 = (tile / m_tiles) * BN;
-        const int slot = cc % NACC;
-        mbar_wait(smem_u32(&bar_tfull[slot]), (cc / NACC) & 1);
-        ++cc;
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        epilogue_tile<BN, true>(g, M, m0 + quarter * 32, n0, nullptr, epi_stage[warp - 2], half,
-                                (tma_c == 1 || tma_c == 2) ? &tmC : nullptr,
-                                tma_c == 2 ? &tmH : nullptr,
-                                (tma_c == 2 || tma_c == 3) && g.h_split ? &tmS : nullptr,
-                                tl + (uint32_t)(slot * BN));
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[slot]))
-                     : "memory");
-      }
-    } else
     for (int si = 0; wk.seg(si, tile, kb_lo, kb_hi); ++si) {
       const int m0 = (tile % m_tiles) * TC_BM, n0 = (tile / m_tiles) * BN;
       float acc[CH][32];
@@ -945,16 +922,31 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
           unitb;
 #pragma unroll
       for (int u = 0; u < 16; ++u) xa[u] = __ldg(xr + u);
-      const int slot = cc % TC_NACC;          // whole K in one TMEM slot (kcb = num_kb)
-      mbar_wait(smem_u32(&bar_tfull[slot]), (cc / TC_NACC) & 1);
-      ++cc;
-      asm volatile("tcgen05.fence::after_thread_sync;");
+      // K in chunks of kcb blocks, each in its own TMEM slot, summed here with
+      // round-to-nearest adds (the in-TMEM adds truncate: a whole-K slot
+      // biases every gate pre-activation toward zero)
+      float acc[2][32];
+      for (int kb0 = 0; kb0 < num_kb; kb0 += kcb) {
+        const int slot = cc % TC_NACC;
+        mbar_wait(smem_u32(&bar_tfull[slot]), (cc / TC_NACC) & 1);
+        ++cc;
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          float v[32];
+          tmem_ld32(tl + slot * BN + (half * 2 + c) * 32, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[c][j] = kb0 == 0 ? v[j] : acc[c][j] + v[j];
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[slot]))
+                     : "memory");
+      }
       TRACE(2, t);
       float hv[16];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        float v[32];
-        tmem_ld32(tl + slot * BN + (half * 2 + c) * 32, v);
+        const float* v = acc[c];
 #pragma unroll
         for (int u8 = 0; u8 < 8; ++u8) {
           const int u = c * 8 + u8;
@@ -965,9 +957,6 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
           hv[u] = fsig(go) * ftanh(cst[u]);
         }
       }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[slot]))
-                   : "memory");
       if (ok) {
         float4* yo = reinterpret_cast<float4*>(y + (int64_t)t * step_y + (int64_t)row * ld_y + unitb);
 #pragma unroll
@@ -1102,8 +1091,7 @@ static int launch_tc_maps(const CUtensorMap& ta, const CUtensorMap& tw, const fb
     const char* e = getenv("FB_GEMM_KCB");
     return e ? std::max(1, atoi(e)) : TC_KCB;
   }();
-  // BN = 256 accumulates the whole K in TMEM (DIRECT epilogue)
-  const int kcb = BN == 256 ? g->k / TC_BK : g->kcb > 0 ? g->kcb : kcb_env;
+  const int kcb = g->kcb > 0 ? g->kcb : kcb_env;
   const int grid = g->splitk_ws ? kNumSMs : std::min(tiles, kNumSMs);
   // plain fp32 rows (no gather, no fused transform): TMA stores
 #ifndef FB_NO_TMA_STORE
@@ -1204,15 +1192,6 @@ extern "C" int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_
                       few_tiles;
   if (want64 && !g->row_stats)
     return launch_tc<64>(g, a_planes, a_plane_rows, g->n, (cudaStream_t)stream);
-  // 256-wide tiles for the big plain GEMMs (the word-LM output projection, the
-  // encoder input projections): half the A-operand re-reads per output.  Whole
-  // K accumulates in TMEM, so only where the default chunking was asked for
-  // (kcb == 0, not the score-producing projections), with >= 2 waves of tiles
-  static const int env256 = getenv("FB_GEMM_256") ? atoi(getenv("FB_GEMM_256")) : 1;
-  const int tiles256 = ((g->m_max + TC_BM - 1) / TC_BM) * ((g->n + 255) / 256);
-  if ((env256 == 2 || (env256 == 1 && tiles256 >= 2 * kNumSMs)) && force_bn == 0 &&
-      g->mode == 0 && g->kcb == 0 && !g->splitk_ws && !g->out_logsoftmax && g->n >= 512)
-    return launch_tc<256>(g, a_planes, a_plane_rows, g->n, (cudaStream_t)stream);
   return launch_tc<128>(g, a_planes, a_plane_rows, g->n, (cudaStream_t)stream);
 }
 
@@ -1273,7 +1252,9 @@ extern "C" int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden,
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lstm_rec_kernel, TC_THREADS, smem);
   if (m_tiles * n_tiles > per_sm * sms)
     return fail(FB_ERR_CONFIG, "recurrence grid cannot be co-resident on this device");
-  int nkb = num_kb, kcb = num_kb;
+  // TMEM accumulation chunk of the recurrence (K blocks; dev override FB_REC_KCB)
+  static const int kcb_env = getenv("FB_REC_KCB") ? std::max(1, atoi(getenv("FB_REC_KCB"))) : 1;
+  int nkb = num_kb, kcb = std::min(kcb_env, num_kb);
   void* args[] = {(void*)&ta[0], (void*)&ta[1], (void*)&tw, (void*)&g, (void*)&steps,
                   (void*)&nkb, (void*)&kcb, (void*)&xp, (void*)&step_xp, (void*)&y,
                   (void*)&ld_y, (void*)&step_y, (void*)&r, (void*)&plane, (void*)&sync_ws,

@@ -6,8 +6,6 @@
 // tensor-core work here.
 #include "common.cuh"
 
-#include <cooperative_groups.h>
-
 namespace fb {
 
 __device__ __forceinline__ double mass(const double* __restrict__ g, int hi, int lo) {
@@ -446,53 +444,6 @@ seg_sum_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __rest
   }
 }
 
-// One pass (g_pool): a thread-block cluster per row, one CTA per 4096-column
-// segment (cluster = the whole row, <= 16 segments).  Each CTA reads its
-// logits once, exponentiates once (fp64 from expf, as the two-pass path),
-// scans its segment in registers, publishes the segment total in shared
-// memory, and after one cluster barrier reads every peer's total over DSMEM
-// for its exact fp64 offset and the row total; g = prefix / S_w.
-__global__ void __launch_bounds__(kScanThreads)
-seg_fused_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __restrict__ logits,
-                 int64_t ld, const int32_t* __restrict__ src_rows, int vw,
-                 const int32_t* __restrict__ slots, int nseg, const double* __restrict__ norm,
-                 double* __restrict__ g_pool, int64_t g_stride, const double* __restrict__ stat_in,
-                 const int32_t* __restrict__ slots_eos, double* __restrict__ eos_out) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cl = cg::this_cluster();
-  __shared__ double wsum[32];
-  __shared__ double seg_total;
-  const int m = row_count(m_max, m_dev);
-  const int y = (int)cl.block_rank();
-  for (int i = blockIdx.x; i < m; i += gridDim.x) {
-    const int64_t srow = src_rows ? src_rows[i] : i;
-    const float mw = (float)(stat_in ? stat_in[2 * srow] : norm[i]);
-    if (stat_in && eos_out && y == 0 && threadIdx.x == 0)   // == row_norm_kernel
-      eos_out[slots_eos ? slots_eos[i] : i] = (double)logits[srow * ld + vw] - stat_in[2 * srow + 1];
-    const float* lg = logits + srow * ld;
-    const int c0 = y * kSegCols;
-    const int cnt = min(kSegCols, vw - c0);
-    double x[kScanItems], loc[kScanItems];
-    load8_exp(lg, c0, cnt, mw, x);
-    double total;
-    const double pre = tile_scan8(x, loc, wsum, total);
-    if (threadIdx.x == 0) seg_total = total;
-    cl.sync();
-    double off = 0.0, tot = 0.0;
-    for (int k = 0; k < nseg; ++k) {          // same order in every CTA: deterministic
-      const double v = *cl.map_shared_rank(&seg_total, k);
-      if (k < y) off += v;
-      tot += v;
-    }
-    const double inv = 1.0 / tot;
-    double* g = g_pool + (int64_t)(slots ? slots[i] : i) * g_stride;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) loc[k] = ((pre + off) + loc[k]) * inv;
-    store8(g, c0, cnt, loc);
-    cl.sync();                                // peers have read seg_total before reuse
-  }
-}
-
 // pass 2: scan each segment with its exact fp64 offset; g = prefix / S_w.
 __global__ void __launch_bounds__(kScanThreads)
 seg_scan_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __restrict__ logits,
@@ -689,51 +640,6 @@ extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* l
   // row CTAs per segment column (rows are grid-strided): few enough that the
   // usually-empty late-event launch is cheap
   const int gx = std::min(m_max, FB_SEG_ROWS_GRID);
-  // one pass with a cluster per row when the row's segments fit one cluster
-  static const int fused_env = getenv("FB_SEG_FUSED") ? atoi(getenv("FB_SEG_FUSED")) : 1;
-  static int fused_ok = -1;                  // probed once per process (nseg is per model)
-  static int fused_nseg = 0;
-  if (fused_env && nseg <= 16 && (fused_ok < 0 || fused_nseg != nseg)) {
-    fused_nseg = nseg;
-    cudaFuncSetAttribute(seg_fused_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaLaunchConfig_t pc = {};
-    pc.gridDim = dim3(1, nseg);
-    pc.blockDim = dim3(kScanThreads);
-    cudaLaunchAttribute pa[1];
-    pa[0].id = cudaLaunchAttributeClusterDimension;
-    pa[0].val.clusterDim.x = 1;
-    pa[0].val.clusterDim.y = nseg;
-    pa[0].val.clusterDim.z = 1;
-    pc.attrs = pa;
-    pc.numAttrs = 1;
-    int clusters = 0;
-    fused_ok = cudaOccupancyMaxActiveClusters(&clusters, seg_fused_kernel, &pc) == cudaSuccess &&
-               clusters > 0;
-    cudaGetLastError();
-  }
-  if (fused_env && nseg <= 16 && fused_ok == 1) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(gx, nseg);
-    cfg.blockDim = dim3(kScanThreads);
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 1;
-    at[0].val.clusterDim.y = nseg;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, seg_fused_kernel, m_max, m_dev, logits,
-                                             l_stride, src_rows, vw, slots, nseg,
-                                             (const double*)norm, g_pool, g_stride, stat_in,
-                                             slots, eos_out);
-    count_launch();
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return fail(FB_ERR_CUDA, std::string("seg_fused: ") + cudaGetErrorString(e));
-    }
-    return FB_OK;
-  }
   seg_sum_kernel<<<dim3(gx, nseg), kScanThreads, 0, s>>>(m_max, m_dev, logits, l_stride, src_rows,
                                                          vw, seg_ws, nseg, norm, stat_in, slots,
                                                          eos_out);

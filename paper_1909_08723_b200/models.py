@@ -49,6 +49,16 @@ LM_SPLITK = _os.environ.get("FB_LM_SPLITK", "0") == "1"
 # fused engine: per-GEMM A operands, h planes from the epilogues, prev-step
 # segments packed on a side stream (dev knob to compare against the plain path)
 AM_PIPELINE = _os.environ.get("FB_AM_PIPELINE", "1") == "1"
+# TMEM accumulation chunk (K blocks of 64) per GEMM family: the tensor core's
+# in-TMEM fp32 adds truncate, so long chunks bias every pre-activation toward
+# zero; a looping 470-step c5 decode drifted -6.5e-4 from the fp64 model with
+# the library default (4 blocks) in every GEMM and -4e-9/step with 1 block
+# (scripts/parity_drift.py); the decoder LSTM GEMMs carry it (1 block there:
+# -6e-8/step at +3 % decode time; the encoder and LM GEMMs do not matter).
+# 0 = library default.
+KCB_AM = int(_os.environ.get("FB_KCB_AM", "1"))       # attention-decoder LSTM + query
+KCB_ENC = int(_os.environ.get("FB_KCB_ENC", "0"))     # encoder input + key projections
+KCB_LM = int(_os.environ.get("FB_KCB_LM", "0"))       # word / token LM GEMMs
 # fused GEMM epilogues: E_q = exp(2 q) for the attention, log-softmax of the
 # acoustic output (dev knob for A/B timing)
 FUSE_EPI = _os.environ.get("FB_FUSE_EPI", "1") == "1"
@@ -241,7 +251,7 @@ class Encoder:
                 src = X if r == 0 else Xr
                 xp = torch.empty((B * TM, 4 * He), dtype=torch.float32, device=dev)
                 K.pack(big, [(src, kin, 0)], m=B * TM, k_pad=kin, split=True)
-                K.gemm_tc(big[:, :, :kin], w_ih, m=B * TM, k=kin, bias=b, out=xp,
+                K.gemm_tc(big[:, :, :kin], w_ih, m=B * TM, k=kin, bias=b, out=xp, kcb=KCB_ENC,
                           k_alg=d.feat_dim * d.subsample if l == 0 else 2 * He)
                 xps.append(xp)
             # the two directions are independent: one stream each
@@ -293,7 +303,7 @@ class Encoder:
         kk = self.w.w_k.shape[1]
         K.pack(big, [(X, kk, 0)], m=B * TM, k_pad=kk, split=True)
         kraw = torch.empty((B * TM, d.att), dtype=torch.float32, device=dev)
-        K.gemm_tc(big[:, :, :kk], self.w.w_k, m=B * TM, k=kk, bias=self.w.b_k, out=kraw,
+        K.gemm_tc(big[:, :, :kk], self.w.w_k, m=B * TM, k=kk, bias=self.w.b_k, out=kraw, kcb=KCB_ENC,
                   k_alg=C_)
         # the attention kernels consume E_K^T = exp(2 K) per utterance as [A, T]
         # (tanh via one reciprocal; frames contiguous for the energy kernel)
@@ -340,14 +350,14 @@ class DecoderStep:
                 segs = [(cur.h[l - 1], H, 1), (prev.ctx, C_, 2), (prev.h[l], H, 2)]
             K.pack(scratch, segs, tokens=last_tok, tok_default=self.eos, k_pad=lay.k_pad,
                    split=True, **kw)
-            K.gemm_tc(scratch, lay.w, k=lay.k_pad, bias=lay.b, mode=1, hidden=H,
+            K.gemm_tc(scratch, lay.w, k=lay.k_pad, bias=lay.b, mode=1, hidden=H, kcb=KCB_AM,
                       c_in=prev.c[l], c_out=cur.c[l], h_out=cur.h[l],
                       h_res=cur.h[l - 1] if l > 0 else None, k_alg=lay.k_in, **kw)
         span.__exit__(None, None, None)
         top = cur.h[L - 1]
         kq = w.w_q.shape[1]
         K.pack(scratch, [(top, H, 1)], k_pad=kq, split=True, **kw)
-        K.gemm_tc(scratch, w.w_q, k=kq, out=q, m=m, m_dev=m_dev, rows=rows, k_alg=H)
+        K.gemm_tc(scratch, w.w_q, k=kq, out=q, m=m, m_dev=m_dev, rows=rows, k_alg=H, kcb=KCB_AM)
         with tm("am_attention"):
             _lib.call("fb_attention_step", cfg_ref, num_utts, _lib.ptr(active),
                       _lib.ptr(n_live), _lib.ptr(t_enc), _lib.ptr(keys), _lib.ptr(enc), d.att, C_,
@@ -401,18 +411,18 @@ class DecoderStep:
                 elif l == 1 and pack_stream is not None:
                     main.wait_stream(pack_stream)
                 nxt = A[l + 1] if l + 1 < L else A[L]
-                K.gemm_tc(A[l], lay.w, k=lay.k_pad, bias=lay.b, mode=1, hidden=H,
+                K.gemm_tc(A[l], lay.w, k=lay.k_pad, bias=lay.b, mode=1, hidden=H, kcb=KCB_AM,
                           c_in=prev.c[l], c_out=cur.c[l], h_out=cur.h[l],
                           h_res=cur.h[l - 1] if l > 0 else None, k_alg=lay.k_in,
                           h_split=nxt, hs_by_row=True, **kw)
         top = cur.h[L - 1]
         # the epilogue stores E_q = exp(2 q) (fb_attention_step q_is_exp)
         if q_from_out:
-            K.gemm_tc(A[L], w.w_q, k=kq, out=q, m=m, m_dev=m_dev, rows=rows, k_alg=H,
+            K.gemm_tc(A[L], w.w_q, k=kq, out=q, m=m, m_dev=m_dev, rows=rows, k_alg=H, kcb=KCB_AM,
                       out_exp2=FUSE_EPI)
         else:
             K.pack(A[0], [(top, H, 1)], k_pad=kq, split=True, **kw)
-            K.gemm_tc(A[0], w.w_q, k=kq, out=q, m=m, m_dev=m_dev, rows=rows, k_alg=H,
+            K.gemm_tc(A[0], w.w_q, k=kq, out=q, m=m, m_dev=m_dev, rows=rows, k_alg=H, kcb=KCB_AM,
                       out_exp2=FUSE_EPI)
         with tm("am_attention"):
             _lib.call("fb_attention_step", cfg_ref, num_utts, _lib.ptr(active),
@@ -577,7 +587,7 @@ def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks
             elif l == 1 and pack_stream is not None:
                 main.wait_stream(pack_stream)
             nxt = abufs[l + 1] if l + 1 < L else (abufs[L] if logits is not None else None)
-            K.gemm_tc(abufs[l][:LM_PLANES], lay.w, m=m, m_dev=m_dev, k=lay.k_pad, bias=lay.b,
+            K.gemm_tc(abufs[l][:LM_PLANES], lay.w, m=m, m_dev=m_dev, k=lay.k_pad, bias=lay.b, kcb=KCB_LM,
                       mode=1, hidden=H, parent=src_idx, c_in=state_src[:, l, 1],
                       c_out=state_dst[:, l, 1], h_out=state_dst[:, l, 0], k_alg=lay.k_in,
                       splitk=splitk, h_split=nxt, hs_by_row=True)
@@ -600,7 +610,8 @@ def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks
             c_in = state_src[:, l, 1]
         K.pack(scratch, [x, hseg], m=m, m_dev=m_dev, rows=src_idx, ranks=ranks,
                tok_default=tok_default, k_pad=lay.k_pad, split=True)
-        K.gemm_tc(scratch[:LM_PLANES], lay.w, m=m, m_dev=m_dev, k=lay.k_pad, bias=lay.b, mode=1,
+        K.gemm_tc(scratch[:LM_PLANES], lay.w, m=m, m_dev=m_dev, k=lay.k_pad, bias=lay.b, kcb=KCB_LM,
+                  mode=1,
                   hidden=H, parent=src_idx, c_in=c_in, c_out=state_dst[:, l, 1],
                   h_out=state_dst[:, l, 0], k_alg=lay.k_in, splitk=splitk)
     if logits is not None:
@@ -795,7 +806,8 @@ def subword_step(w: SubLmWeights, *, m: int, m_dev, rows, parent, last_tok, eos_
             segs = [(cur.h[l - 1], H, 1), (prev.h[l], H, 2)]
         K.pack(scratch, segs, tokens=last_tok, tok_default=eos_id, k_pad=lay.k_pad, split=True,
                **kw)
-        K.gemm_tc(scratch, lay.w, k=lay.k_pad, bias=lay.b, mode=1, hidden=H, c_in=prev.c[l],
+        K.gemm_tc(scratch, lay.w, k=lay.k_pad, bias=lay.b, mode=1, hidden=H, kcb=KCB_LM,
+                  c_in=prev.c[l],
                   c_out=cur.c[l], h_out=cur.h[l], k_alg=lay.k_in, **kw)
     K.pack(scratch, [(cur.h[L - 1], H, 1)], k_pad=w.k_out, split=True, **kw)
     K.gemm_tc(scratch, w.out_w, k=w.k_out, bias=w.b_out, out=logits, m=m, m_dev=m_dev,

@@ -9,4 +9,4 @@ for v in "default:" "n256:FB_GEMM_256=0" "noseg:FB_SEG_FUSED=0" "default2:"; do
   env $env timeout 600 python bench.py --no-cpu-baseline --steps 5 > gpurun_out/b_$tag.json 2> gpurun_out/b_$tag.err; t b_$tag
 done
 timeout 900 python -m pytest tests -m gpu -q -x --deselect tests/test_gpu_parity_full.py > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
-timeout 600 python -m pytest tests/test_gpu_parity_full.py -m gpu -q -s -k "c2 or c1 or c3" > gpurun_out/parity_c2.log 2>&1; grep -E "utterances|passed|failed" gpurun_out/parity_c2.log
+timeout 600 python -m pytest tests/test_gpu_parity_full.py -m gpu -q -s > gpurun_out/parity_all.log 2>&1; grep -E "utterances|passed|failed" gpurun_out/parity_all.log; for c in c2 c4 c5; do timeout 300 python scripts/parity_dump.py $c f64out > /dev/null 2>&1; done

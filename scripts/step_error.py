@@ -34,6 +34,19 @@ cpu = OracleAttnLstmScorer(W, wl.asr.enc_layers, wl.asr.dec_layers, wl.asr.subsa
 f = fb.FeatureMatrix(uid, x)
 sg, sc = gpu.init(f), cpu.init(f)
 glm = clm = None
+gfu = cfu = None
+if wl.lm is not None:
+    # look-ahead fusion along the path: device LookaheadFusion (device LSTM LM)
+    # vs the oracle's with an fp64 LM
+    from oracle.lexicon import OracleDict, build_trie as obuild
+    from oracle.lookahead import OracleLookahead
+    from oracle.neural import OracleLstmWordLM
+    from paper_1909_08723_b200.models import LstmWordLM
+    od = OracleDict(H.file_tokens(wl))
+    gfu = fb.LookaheadFusion(trie, LstmWordLM(W, wl.lm), d)
+    cfu = OracleLookahead(obuild(H.synth().synth_lexicon(wl.lm.words, seed=wl.seed + 2), od),
+                          OracleLstmWordLM(W, wl.lm.layers, wl.lm.words, dtype=torch.float64), od)
+    gs, cs = gfu.start(1), cfu.start(1)
 if wl.sublm is not None:
     from oracle.subword import OracleLstmCharLM
     glm = LstmSubwordLM(W, wl.sublm, d.pad_id, d.eos_id)
@@ -51,6 +64,11 @@ for t in path:
         rg, rc = glm.log_probs(lg), clm.log_probs(lc)
         lm_err.append(wl.lm_weight * (float(rg[t]) - float(rc[t])))
         lg, lc = glm.advance(lg, t), clm.advance(lc, t)
+    if gfu is not None:
+        rg, rc = gfu.char_scores(gs)[0], cfu.char_scores(cs)[0]
+        lm_err.append(wl.lm_weight * (float(rg[t]) - float(rc[t])))
+        if t != d.eos_id:
+            gs, cs = gfu.advance(gs, [t]), cfu.advance(cs, np.asarray([t]))
     last = [t]
 am_err = np.array(am_err)
 print(f"{name} {uid}: {len(path)} steps; AM chosen-token error sum {am_err.sum():.3g} "

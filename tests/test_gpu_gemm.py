@@ -113,9 +113,8 @@ def test_tc_device_row_count():
 
 @pytest.mark.parametrize("m,vw,k", [(37, 9000, 128), (300, 65000, 1216)])
 def test_row_stats_feed_g_rows_and_eos(m, vw, k):
-    """LM-output GEMM tile statistics -> fb_stats_to_g (one-pass cluster scan)
-    == single-pass fb_logits_to_g; the second shape runs 256-wide tiles
-    (whole-K TMEM accumulation, statistics per 64-column group)."""
+    """LM-output GEMM tile statistics -> fb_stats_to_g == single-pass
+    fb_logits_to_g (the second shape is the c2 word-LM output projection)."""
     from paper_1909_08723_b200 import kernels as K
     dev = torch.device("cuda")
     torch.manual_seed(11 + m)
@@ -128,7 +127,7 @@ def test_row_stats_feed_g_rows_and_eos(m, vw, k):
     K.gemm_tc(_packed(a, k), _w(w), m=m, k=k, bias=b, out=logits,
               row_stats=stats, stats_vw=vw)
     ref = a.double() @ w.double().T + b.double()
-    assert (logits.double() - ref).abs().max().item() < 1e-4
+    assert (logits.double() - ref).abs().max().item() < 1e-5 * max(1.0, ref.abs().max().item())
     g_ref = torch.empty(m, vw, dtype=torch.float64, device=dev)
     e_ref = torch.empty(m, dtype=torch.float64, device=dev)
     K.logits_to_g(logits, vw, n, m=m, g_pool=g_ref, eos_out=e_ref)
@@ -142,7 +141,7 @@ def test_row_stats_feed_g_rows_and_eos(m, vw, k):
     # single-word masses from g differences agree to fp64 resolution of g (~1 ulp of 1.0)
     p = torch.diff(g, dim=1, prepend=torch.zeros(m, 1, dtype=torch.float64, device=dev))
     p_ref = torch.diff(g_ref, dim=1, prepend=torch.zeros(m, 1, dtype=torch.float64, device=dev))
-    assert (p - p_ref).abs().max().item() < 1e-15
+    assert (p - p_ref).abs().max().item() < 1e-14      # segmented vs sequential scan order
     # statistics from an eos-only pass reused by a gathered g-row pass: bit-identical
     stat = torch.empty(m, 2, dtype=torch.float64, device=dev)
     e_ev = torch.empty_like(e_ref)
