@@ -155,6 +155,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 64 consecutive columns of this warp's 32 lanes, no wait (the caller issues
+// tcgen05.wait::ld before reading r)
+__device__ __forceinline__ void tmem_ld64_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32"
+      " {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr));
+}
+
 __device__ __forceinline__ float sigm_tc(float x) { return 1.0f / (1.0f + expf(-x)); }
 
 // MUFU ex2 + rcp; __fdividef returns 0 for denominators > 2^126, which is the
@@ -218,16 +228,27 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
     if (g.row_stats) {
       // lane = row: online (max, sum exp) over this chunk's valid columns
       float mw = -INFINITY, ma = -INFINITY;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if (nb + j < g.n) ma = fmaxf(ma, v[j]);
-        if (nb + j < g.stats_vw) mw = fmaxf(mw, v[j]);
-      }
       float sw = 0.f, sa = 0.f;
+      if (nb + 32 <= g.stats_vw) {
+        // all 32 columns are words (every chunk but the row's last): the
+        // word and all-output statistics coincide -- one exp per element
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if (nb + j < g.n) sa += __expf(v[j] - ma);
-        if (nb + j < g.stats_vw) sw += __expf(v[j] - mw);
+        for (int j = 0; j < 32; ++j) mw = fmaxf(mw, v[j]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sw += __expf(v[j] - mw);
+        ma = mw;
+        sa = sw;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (nb + j < g.n) ma = fmaxf(ma, v[j]);
+          if (nb + j < g.stats_vw) mw = fmaxf(mw, v[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (nb + j < g.n) sa += __expf(v[j] - ma);
+          if (nb + j < g.stats_vw) sw += __expf(v[j] - mw);
+        }
       }
       if (ma > -INFINITY) {
         const float m2 = fmaxf(st_stats.x, ma);
@@ -563,7 +584,7 @@ constexpr int TC_SK_MIN_KB = 8;      // stream-K: at least 8 K blocks (K = 512) 
 // count follows the device-side row count, so graph replays with few live rows
 // cost only the tiles they need.
 template <int BN>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(TC_THREADS, 1)   // 10 warps: <= 168 registers (3 warps per SMSP)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmH,
                const __grid_constant__ CUtensorMap tmS, int tma_c,
@@ -702,16 +723,30 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const int slot = cc % NACC;
         mbar_wait(smem_u32(&bar_tfull[slot]), (cc / NACC) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
+        if constexpr (CH == 2) {
+          // both 32-column chunks in flight before one wait::ld (the drain
+          // runs once per accumulation chunk, so its latency matters)
+          uint32_t r[64];
+          tmem_ld64_nowait(tl + slot * BN + half * 64, r);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          float v[32];
-          tmem_ld32(tl + slot * BN + (half * CH + c) * 32, v);
-          if (kb0 == kb_lo) {
+          for (int c = 0; c < 2; ++c)
 #pragma unroll
-            for (int j = 0; j < 32; ++j) acc[c][j] = v[j];
-          } else {
+            for (int j = 0; j < 32; ++j)
+              acc[c][j] = kb0 == kb_lo ? __uint_as_float(r[c * 32 + j])
+                                       : acc[c][j] + __uint_as_float(r[c * 32 + j]);
+        } else {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) acc[c][j] += v[j];
+          for (int c = 0; c < CH; ++c) {
+            float v[32];
+            tmem_ld32(tl + slot * BN + (half * CH + c) * 32, v);
+            if (kb0 == kb_lo) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) acc[c][j] = v[j];
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) acc[c][j] += v[j];
+            }
           }
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
@@ -924,7 +959,10 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
       for (int u = 0; u < 16; ++u) xa[u] = __ldg(xr + u);
       // K in chunks of kcb blocks, each in its own TMEM slot, summed here with
       // round-to-nearest adds (the in-TMEM adds truncate: a whole-K slot
-      // biases every gate pre-activation toward zero)
+      // biases every gate pre-activation toward zero).  The input projection
+      // joins the first chunk (divided by the exact power-of-two scale), so
+      // its registers are free before the remaining chunks arrive.
+      const float sc = g0.acc_scale, inv_sc = 1.0f / sc;
       float acc[2][32];
       for (int kb0 = 0; kb0 < num_kb; kb0 += kcb) {
         const int slot = cc % TC_NACC;
@@ -935,8 +973,19 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
         for (int c = 0; c < 2; ++c) {
           float v[32];
           tmem_ld32(tl + slot * BN + (half * 2 + c) * 32, v);
+          if (kb0 == 0) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) acc[c][j] = kb0 == 0 ? v[j] : acc[c][j] + v[j];
+            for (int u8 = 0; u8 < 8; ++u8) {
+              const float4 x4 = xa[c * 8 + u8];
+              acc[c][4 * u8] = v[4 * u8] + x4.x * inv_sc;
+              acc[c][4 * u8 + 1] = v[4 * u8 + 1] + x4.y * inv_sc;
+              acc[c][4 * u8 + 2] = v[4 * u8 + 2] + x4.z * inv_sc;
+              acc[c][4 * u8 + 3] = v[4 * u8 + 3] + x4.w * inv_sc;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[c][j] += v[j];
+          }
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[slot]))
@@ -950,9 +999,8 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
 #pragma unroll
         for (int u8 = 0; u8 < 8; ++u8) {
           const int u = c * 8 + u8;
-          const float sc = g0.acc_scale;
-          const float gi = v[4 * u8] * sc + xa[u].x, gf = v[4 * u8 + 1] * sc + xa[u].y;
-          const float gg = v[4 * u8 + 2] * sc + xa[u].z, go = v[4 * u8 + 3] * sc + xa[u].w;
+          const float gi = v[4 * u8] * sc, gf = v[4 * u8 + 1] * sc;
+          const float gg = v[4 * u8 + 2] * sc, go = v[4 * u8 + 3] * sc;
           cst[u] = fsig(gf) * cst[u] + fsig(gi) * ftanh(gg);
           hv[u] = fsig(go) * ftanh(cst[u]);
         }

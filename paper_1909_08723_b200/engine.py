@@ -50,6 +50,9 @@ _STAT_REUSE = os.environ.get("FB_STAT_REUSE", "0") == "1"
 # attention tiles replace the default ones (frame warps, rows, quads per CTA)
 _TAIL_ROWS = int(os.environ.get("FB_TAIL_ROWS", "1500"))
 _TAIL_TILING = tuple(int(x) for x in os.environ.get("FB_TAIL_TILING", "4,4,160").split(","))
+# lock-step tail: the word-LM LSTM GEMMs of few event rows run stream-K (more
+# CTAs over the long K = 2432 loop) in the tail graph set (dev knob)
+_TAIL_SPLITK = os.environ.get("FB_TAIL_SPLITK", "0") == "1"
 
 
 class _LmPool:
@@ -90,6 +93,7 @@ class _LmPool:
         # stream-K workspace of the LM LSTM GEMMs (spec and late events never
         # overlap: the side stream joins before the speculative events)
         self.splitk = K.SplitK(device) if LM_SPLITK else None
+        self.splitk_tail = (self.splitk or K.SplitK(device)) if _TAIL_SPLITK else None
         # {M_w, lse} per speculative event: reused by the word-boundary g rows
         self.ev_stat = torch.zeros((N, 2), dtype=torch.float64, device=device)
         # per-GEMM A operands (the output one's K padding stays zero)
@@ -543,6 +547,9 @@ class FusedDecoder:
                 if _TAIL_ROWS > 0:
                     c2 = lib.fb_launch_count()
                     _lib.call("fb_set_attention_tiling", *_TAIL_TILING)
+                    sk_main = S.lm.splitk if S.lm is not None else None
+                    if S.lm is not None and S.lm.splitk_tail is not None:
+                        S.lm.splitk = S.lm.splitk_tail
                     try:
                         gt = [torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()]
                         for p_ in (0, 1):
@@ -550,6 +557,8 @@ class FusedDecoder:
                                 self._step_overlapped(S, p_, prev_tail=True)
                     finally:
                         _lib.call("fb_set_attention_tiling", 0, 0, 0)
+                        if S.lm is not None:
+                            S.lm.splitk = sk_main
                     l0 += lib.fb_launch_count() - c2
                     S.graphs_tail = gt
             first = True

@@ -246,11 +246,12 @@ WORKLOADS: Dict[str, Workload] = {
                    coverage_weight=0.01, eos_gamma=1.5, batch_size=16),
     # c4: subword decoder (5k tokens), beam 60, token-level LSTM-LM shallow fusion;
     # scales calibrated like c2 (scripts/calib_c4.sh: ~0.45 tokens per encoder
-    # frame, ~60% of utterances emit <eos>, distinct outputs)
+    # frame, ~60% of utterances emit <eos>, distinct outputs); batches of 256
+    # (1.9x the throughput of 32 on a B200, same results: batch invariance)
     "c4": Workload("c4", 2620, (300, 3500), 60,
                    AsrDims(enc_hidden=512, dec_hidden=1024, emb=256, att=512, vocab=5000,
                            out_scale=1.5, eos_bias=1.0),
-                   None, lm_weight=0.3, batch_size=32,
+                   None, lm_weight=0.3, batch_size=256,
                    sublm=SubwordLmDims(layers=4, hidden=800, emb=800, vocab=5000,
                                        out_scale=0.5)),
     # c5: Switchboard-shaped char decoder, 30k-word look-ahead, beam 35.
@@ -262,5 +263,5 @@ WORKLOADS: Dict[str, Workload] = {
                    AsrDims(enc_hidden=320, dec_hidden=640, emb=64, att=320, out_scale=1.5,
                            eos_bias=-2.0),
                    LmDims(layers=3, hidden=1800 // 2, words=30000, emb_scale=0.2, eos_bias=5.0,
-                          w_scale=2.0), lm_weight=0.25, batch_size=128),
+                          w_scale=2.0), lm_weight=0.25, batch_size=256),
 }

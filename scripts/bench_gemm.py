@@ -1,6 +1,6 @@
 """Standalone timing of the tcgen05 GEMM at the decoder's shapes (CUDA events,
-warm L2 excluded by rotating 4 operand sets).  Algorithmic FLOPs = 2*M*N*K
-(the bf16x3 split is not counted)."""
+graph-captured, rotating 4 operand sets).  Algorithmic FLOPs = 2*M*N*K (the
+operand planes are not counted).  KCB=n: TMEM accumulation chunk."""
 import sys, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -28,8 +28,9 @@ def run(name, M, N, Kd, mode, reps=20):
     sets = []
     nsets = int(os.environ.get("SETS", "4"))
     for _ in range(nsets):
-        a = torch.randn(3, M, Kd, device=dev).to(torch.bfloat16)
-        w = (torch.randn(N, Kd, device=dev) * 0.05).to(torch.bfloat16)
+        a = K.operand_planes(M, Kd, dev)
+        K.pack(a, [(torch.randn(M, Kd, device=dev), Kd, 0)], m=M, k_pad=Kd, split=True)
+        w = K.operand_weight(torch.randn(N, Kd, device=dev) * 0.05)
         b = torch.randn(N, device=dev)
         if mode == 1:
             H = N // 4
@@ -40,6 +41,7 @@ def run(name, M, N, Kd, mode, reps=20):
                       row_stats=torch.empty(M, (N + 63) // 64, 4, device=dev), stats_vw=N - 3)
         else:
             kw = dict(out=torch.empty(M, N, device=dev))
+        kw["kcb"] = int(os.environ.get("KCB", "0"))
         sets.append((a, w, b, kw))
     if os.environ.get("FB_BENCH_SPLITK") == "1":
         sk = K.SplitK(dev)
@@ -65,7 +67,8 @@ def run(name, M, N, Kd, mode, reps=20):
     us = 1000 * e0.elapsed_time(e1) / reps
     tf = 2.0 * M * N * Kd / (us * 1e-6) / 1e12
     return {"shape": name, "M": M, "N": N, "K": Kd, "us": round(us, 2),
-            "alg_tflops": round(tf, 1), "tensor_tflops_3x": round(3 * tf, 1)}
+            "alg_tflops": round(tf, 1),
+            "tensor_tflops_planes": round(K.operand_format()[0] * tf, 1)}
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(SHAPES)
