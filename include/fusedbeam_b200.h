@@ -280,8 +280,10 @@ int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_rows, void*
  * lives in registers (zero at t = 0).
  * Row b of step t: xp + t*step_xp + b*ld_xp, y + t*step_y + b*ld_y (time-major
  * layouts -- step_* = batch * row width -- keep each step's rows contiguous).
- * One persistent launch: CTAs loop over t with a grid barrier on sync_ws (one
- * uint32, reset here); at most 74 CTAs (both directions co-resident). */
+ * One persistent cooperative launch (co-residency checked against the
+ * device; FB_ERR_CONFIG if the grid cannot fit): the CTAs of each 128-row
+ * tile loop over t behind a barrier on their own counter in sync_ws
+ * (ceil(batch/128) uint32, reset here).  W_hh stays in shared memory. */
 int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden, const void* w_hh,
                        int32_t k, const float* xp, int64_t ld_xp, int64_t step_xp, float* y,
                        int64_t ld_y, int64_t step_y, void* rec, uint32_t* sync_ws,

@@ -836,7 +836,10 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
   constexpr int BN = 128;
   const int batch = g0.m_max;
   const int m_tiles = (batch + TC_BM - 1) / TC_BM;
-  const int n_ctas = gridDim.x;
+  // rows of different m-tiles never interact: each m-tile's n-tile CTAs
+  // synchronise among themselves (one counter per m-tile), not grid-wide
+  const int n_peers = gridDim.x / m_tiles;
+  unsigned* msync = sync + (blockIdx.x % m_tiles);
   const int tile = blockIdx.x;
   const int m0 = (tile % m_tiles) * TC_BM, n0 = (tile / m_tiles) * BN;
 
@@ -885,9 +888,9 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
       int gk = 0;
       for (int t = 0; t < steps; ++t) {
         // h_{t-1} complete in every CTA (grid barrier), then visible to TMA
-        const unsigned target = (unsigned)(n_ctas * t);
+        const unsigned target = (unsigned)(n_peers * t);
         TRACE(0, t);
-        while (ld_acquire_u32(sync) < target) __nanosleep(32);
+        while (ld_acquire_u32(msync) < target) __nanosleep(32);
         TRACE(1, t);
         asm volatile("fence.proxy.async.global;" ::: "memory");
         const CUtensorMap* tmA = (t & 1) ? &tmA1 : &tmA0;
@@ -1033,7 +1036,7 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
       asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI_THREADS));
       if (warp == 2 && lane == 0) {
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        atomicAdd(sync, 1u);
+        atomicAdd(msync, 1u);
       }
       TRACE(3, t);
     }
@@ -1278,7 +1281,7 @@ extern "C" int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden,
   }
   int rc = make_map(&tw, w_hh, g.n, k, k, 128);
   if (rc) return rc;
-  cudaMemsetAsync(sync_ws, 0, sizeof(uint32_t), s);
+  cudaMemsetAsync(sync_ws, 0, sizeof(uint32_t) * m_tiles, s);
   // shared memory: the resident W_hh slice + a ring of A-plane stages
   const int num_kb = k / TC_BK;
   const size_t w_bytes = (size_t)num_kb * 128 * TC_BK * 2;

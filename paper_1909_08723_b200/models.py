@@ -259,7 +259,7 @@ class Encoder:
             bufs = [(torch.empty((B, TM, He), dtype=torch.float32, device=dev),
                      torch.zeros((2, K.operand_format()[0], B, kr), dtype=K.operand_format()[1],
                                  device=dev),
-                     torch.zeros(1, dtype=torch.int32, device=dev))
+                     torch.zeros((B + 127) // 128, dtype=torch.int32, device=dev))
                     for _ in range(2)]
             for r, (w_ih, w_hh, b) in enumerate(dirs):
                 st = self.streams[r]
