@@ -418,67 +418,16 @@ row_norm_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __res
 __global__ void __launch_bounds__(kScanThreads)
 seg_sum_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __restrict__ logits,
                int64_t ld, const int32_t* __restrict__ src_rows, int vw,
-               double* __restrict__ seg_ws, int nseg, double* __restrict__ norm,
+               double* __restrict__ seg_ws, int nseg, const double* __restrict__ norm,
                const double* __restrict__ stat_in, const int32_t* __restrict__ slots,
-               double* __restrict__ eos_out, const float4* __restrict__ stats, int ntiles) {
+               double* __restrict__ eos_out) {
   __shared__ double red_d[32];
-  __shared__ float red_f[32];
-  __shared__ float mw_sh;
   const int m = row_count(m_max, m_dev);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int i = blockIdx.x; i < m; i += gridDim.x) {
     const int64_t srow = src_rows ? src_rows[i] : i;
-    float mw;
-    if (stat_in) {
-      mw = (float)stat_in[2 * srow];
-      if (eos_out && blockIdx.y == 0 && threadIdx.x == 0)   // == row_norm_kernel
-        eos_out[slots ? slots[i] : i] = (double)logits[srow * ld + vw] - stat_in[2 * srow + 1];
-    } else if (!stats) {
-      mw = (float)norm[i];                                  // row_norm_kernel ran
-    } else {
-      // the row normaliser folded in (no separate row_norm launch): every
-      // segment CTA takes the word max from the GEMM's tile statistics;
-      // segment 0 also writes M_w for the scan pass and log P(</s>)
-      const float4* st = stats + srow * ntiles;
-      float ma = -INFINITY, mx = -INFINITY;
-      for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
-        const float4 v = st[t];
-        ma = fmaxf(ma, v.x);
-        mx = fmaxf(mx, v.z);
-      }
-      for (int off = 16; off; off >>= 1) {
-        ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, off));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-      }
-      if (lane == 0) { red_f[warp] = mx; red_d[warp] = (double)ma; }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        float a = -INFINITY, b = -INFINITY;
-        for (int w = 0; w < nw; ++w) { b = fmaxf(b, red_f[w]); a = fmaxf(a, (float)red_d[w]); }
-        mw_sh = b;
-        red_f[0] = a;
-      }
-      __syncthreads();
-      mw = mw_sh;
-      if (blockIdx.y == 0 && warp == 0) {
-        // log P(</s>): one warp, row_norm_kernel's exact summation order (the
-        // eos-only pass and this one give bit-identical values)
-        const float mall = red_f[0];
-        double sa = 0.0;
-        for (int t = lane; t < ntiles; t += 32) {
-          const float4 v = st[t];
-          if (v.x > -INFINITY) sa += (double)v.y * exp((double)v.x - (double)mall);
-        }
-        for (int off = 16; off; off >>= 1) sa += __shfl_xor_sync(0xffffffffu, sa, off);
-        if (lane == 0) {
-          if (eos_out)
-            eos_out[slots ? slots[i] : i] =
-                (double)logits[srow * ld + vw] - ((double)mall + log(sa));
-          norm[i] = (double)mw;
-        }
-      }
-      __syncthreads();
-    }
+    const float mw = (float)(stat_in ? stat_in[2 * srow] : norm[i]);
+    if (stat_in && eos_out && blockIdx.y == 0 && threadIdx.x == 0)   // == row_norm_kernel
+      eos_out[slots ? slots[i] : i] = (double)logits[srow * ld + vw] - stat_in[2 * srow + 1];
     const float* lg = logits + srow * ld;
     const int c0 = blockIdx.y * kSegCols, c1 = min(vw, c0 + kSegCols);
     double s = 0.0;
@@ -675,9 +624,7 @@ extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* l
   // seg_ws layout: [m_max][nseg] segment sums, then [m_max] M_w
   double* norm = g_pool ? seg_ws + (int64_t)m_max * nseg : nullptr;
   int rc = 0;
-  static const int fold_env = getenv("FB_SEG_FOLD") ? atoi(getenv("FB_SEG_FOLD")) : 1;  // dev A/B
-  const bool fold = fold_env && g_pool && !stat_in && !stat_out;   // row_norm folded into seg_sum
-  if (!stat_in && !fold) {
+  if (!stat_in) {
 #ifndef FB_ROWS_GRID
 #define FB_ROWS_GRID (kNumSMs * 2)
 #endif
@@ -695,8 +642,7 @@ extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* l
   const int gx = std::min(m_max, FB_SEG_ROWS_GRID);
   seg_sum_kernel<<<dim3(gx, nseg), kScanThreads, 0, s>>>(m_max, m_dev, logits, l_stride, src_rows,
                                                          vw, seg_ws, nseg, norm, stat_in, slots,
-                                                         (fold || stat_in) ? eos_out : nullptr,
-                                                         fold ? st : nullptr, ntiles);
+                                                         eos_out);
   count_launch();
   rc = check_launch("seg_sum");
   if (rc) return rc;
