@@ -283,11 +283,14 @@ int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_rows, void*
  * One persistent cooperative launch (co-residency checked against the
  * device; FB_ERR_CONFIG if the grid cannot fit): the CTAs of each 128-row
  * tile loop over t behind a barrier on their own counter in sync_ws
- * (ceil(batch/128) uint32, reset here).  W_hh stays in shared memory. */
+ * (ceil(batch/128) uint32, reset here).  W_hh stays in shared memory.
+ * t_rev (optional, [batch] int32): the backward direction -- step t of row b
+ * reads xp and writes y at frame t_rev[b] - 1 - t (t < t_rev[b]), so a
+ * length-padded batch needs no reversed copies of its inputs or outputs. */
 int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden, const void* w_hh,
                        int32_t k, const float* xp, int64_t ld_xp, int64_t step_xp, float* y,
                        int64_t ld_y, int64_t step_y, void* rec, uint32_t* sync_ws,
-                       float acc_scale, void* stream);
+                       float acc_scale, const int32_t* t_rev, void* stream);
 
 /* Row gather-concatenate into a GEMM A operand:
  *   out[i, :] = [seg0 | seg1 | ... | zero pad up to k_pad], i < m.

@@ -90,7 +90,7 @@ _SIGS = {
     "fb_stats_to_g": (C.c_int, [i32, vp, vp, i64, vp, i32, vp, i32, vp, vp, i64, vp, vp, vp, vp,
                                 vp]),
     "fb_lstm_recurrence": (C.c_int, [i32, i32, i32, vp, i32, vp, i64, i64, vp, i64, i64, vp,
-                                      vp, C.c_float, vp]),
+                                      vp, C.c_float, vp, vp]),
     "fb_operand_format": (C.c_int, [vp, vp, vp]),
     "fb_pack_rows": (C.c_int, [C.POINTER(FbPack), i32, vp, vp, vp, vp, vp, vp, i64, vp]),
     "fb_log_softmax_rows": (C.c_int, [i32, vp, vp, vp, i64, i32, vp, i64, vp]),

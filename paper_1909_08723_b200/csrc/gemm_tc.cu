@@ -832,7 +832,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                 const __grid_constant__ CUtensorMap tmW, fb_gemm_t g0, int steps, int num_kb,
                 int kcb, const float* xp, int64_t step_xp, float* y, int64_t ld_y,
-                int64_t step_y, uint16_t* rec, int64_t plane, unsigned* sync, int nst) {
+                int64_t step_y, uint16_t* rec, int64_t plane, unsigned* sync, int nst,
+                const int32_t* t_rev) {
   constexpr int BN = 128;
   const int batch = g0.m_max;
   const int m_tiles = (batch + TC_BM - 1) / TC_BM;
@@ -948,6 +949,9 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
     const uint32_t tl = tmem + ((uint32_t)(quarter * 32) << 16);
     const int row = m0 + quarter * 32 + lane;
     const bool ok = row < batch;
+    // backward direction: step t of row b reads / writes frame T_b - 1 - t
+    // (frames past T_b map to themselves: the reversal is a per-row permutation)
+    const int t_row = (t_rev && ok) ? t_rev[row] : 0;
     const int unitb = (n0 >> 2) + half * 16;
     float cst[16];
 #pragma unroll
@@ -956,7 +960,8 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
     for (int t = 0; t < steps; ++t) {
       float4 xa[16];
       const float4* xr =
-          reinterpret_cast<const float4*>(xp + (int64_t)t * step_xp + (int64_t)(ok ? row : 0) * g0.ld_add) +
+          reinterpret_cast<const float4*>(xp + (int64_t)(t < t_row ? t_row - 1 - t : t) * step_xp +
+                                          (int64_t)(ok ? row : 0) * g0.ld_add) +
           unitb;
 #pragma unroll
       for (int u = 0; u < 16; ++u) xa[u] = __ldg(xr + u);
@@ -1009,7 +1014,8 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
         }
       }
       if (ok) {
-        float4* yo = reinterpret_cast<float4*>(y + (int64_t)t * step_y + (int64_t)row * ld_y + unitb);
+        float4* yo = reinterpret_cast<float4*>(y + (int64_t)(t < t_row ? t_row - 1 - t : t) * step_y +
+                                               (int64_t)row * ld_y + unitb);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           yo[q] = make_float4(hv[4 * q], hv[4 * q + 1], hv[4 * q + 2], hv[4 * q + 3]);
@@ -1253,7 +1259,8 @@ extern "C" int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_
 extern "C" int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden,
                                   const void* w_hh, int32_t k, const float* xp, int64_t ld_xp,
                                   int64_t step_xp, float* y, int64_t ld_y, int64_t step_y,
-                                  void* rec, uint32_t* sync_ws, float acc_scale, void* stream) {
+                                  void* rec, uint32_t* sync_ws, float acc_scale,
+                                  const int32_t* t_rev, void* stream) {
   FB_CHECK_ARG(w_hh && xp && y && rec && sync_ws, "null recurrence buffers");
   FB_CHECK_ARG(ld_xp % 4 == 0 && step_xp % 4 == 0 && ld_y % 4 == 0 && step_y % 4 == 0 &&
                    k % 8 == 0 && ((uintptr_t)xp % 16) == 0 && ((uintptr_t)y % 16) == 0,
@@ -1309,7 +1316,7 @@ extern "C" int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden,
   void* args[] = {(void*)&ta[0], (void*)&ta[1], (void*)&tw, (void*)&g, (void*)&steps,
                   (void*)&nkb, (void*)&kcb, (void*)&xp, (void*)&step_xp, (void*)&y,
                   (void*)&ld_y, (void*)&step_y, (void*)&r, (void*)&plane, (void*)&sync_ws,
-                  (void*)&nst};
+                  (void*)&nst, (void*)&t_rev};
   const cudaError_t e = cudaLaunchCooperativeKernel((const void*)lstm_rec_kernel,
                                                     dim3(m_tiles * n_tiles), dim3(TC_THREADS),
                                                     args, smem, s);

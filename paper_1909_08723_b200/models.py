@@ -113,17 +113,16 @@ class AsrWeights:
     def __init__(self, W: Dict[str, np.ndarray], d: AsrDims, device):
         self.d = d
         He, H, C_, A = d.enc_hidden, d.dec_hidden, d.ctx, d.att
+        # per layer: both directions' input projections as ONE GEMM operand
+        # [W_ih_fwd; W_ih_bwd] (gate-interleaved) + biases, and W_hh per direction
         self.enc = []
         for l in range(d.enc_layers):
             fin = d.feat_dim * d.subsample if l == 0 else 2 * He
-            dirs = []
-            for r in range(2):
-                w_ih = interleave_gates(W[f"enc.{l}.{r}.w_ih"], He)
-                w_hh = interleave_gates(W[f"enc.{l}.{r}.w_hh"], He)
-                b = interleave_gates(W[f"enc.{l}.{r}.b"], He)
-                dirs.append((_devw(w_ih, device, _pad(fin)), _devw(w_hh, device, _pad(He)),
-                             _dev(b, device)))
-            self.enc.append(dirs)
+            w_ih = np.concatenate([interleave_gates(W[f"enc.{l}.{r}.w_ih"], He) for r in range(2)])
+            b = np.concatenate([interleave_gates(W[f"enc.{l}.{r}.b"], He) for r in range(2)])
+            w_hh = [_devw(interleave_gates(W[f"enc.{l}.{r}.w_hh"], He), device, _pad(He))
+                    for r in range(2)]
+            self.enc.append((_devw(w_ih, device, _pad(fin)), _dev(b, device), w_hh))
         self.emb = _dev(W["dec.emb"], device)
         self.dec: List[LstmLayer] = []
         for l in range(d.dec_layers):
@@ -232,57 +231,47 @@ class Encoder:
             X, T = feats, list(lengths)
         B = len(T)
         TM = X.shape[0] // B
-        rev = np.arange(B * TM, dtype=np.int32).reshape(B, TM)
-        for u in range(B):
-            rev[u, :T[u]] = u * TM + np.arange(T[u] - 1, -1, -1)
-        rev_t = torch.as_tensor(rev.reshape(-1)).to(dev, non_blocking=True)
+        t_dev = torch.as_tensor(np.asarray(T, np.int32)).to(dev, non_blocking=True)
         He = d.enc_hidden
         kr = _pad(He)
-        Xr = torch.empty_like(X)
-        big = split_scratch(B * TM, max(X.shape[1], _pad(2 * He)), dev)
+        kout = _pad(2 * He)
+        big = split_scratch(B * TM, max(X.shape[1], kout), dev)
         if self.streams is None:
             self.streams = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
-        for l, dirs in enumerate(self.w.enc):
+        planes, pdt, _ = K.operand_format()
+        for l, (w_ih, b, w_hh) in enumerate(self.w.enc):
             kin = X.shape[1]
-            K.copy_rows(X, Xr, m=B * TM, src_idx=rev_t)
-            ys = []
-            xps = []
-            for r, (w_ih, w_hh, b) in enumerate(dirs):
-                src = X if r == 0 else Xr
-                xp = torch.empty((B * TM, 4 * He), dtype=torch.float32, device=dev)
-                K.pack(big, [(src, kin, 0)], m=B * TM, k_pad=kin, split=True)
-                K.gemm_tc(big[:, :, :kin], w_ih, m=B * TM, k=kin, bias=b, out=xp, kcb=KCB_ENC,
-                          k_alg=d.feat_dim * d.subsample if l == 0 else 2 * He)
-                xps.append(xp)
-            # the two directions are independent: one stream each
+            # both directions' input projections in one GEMM: xp [B*TM, 8He];
+            # the backward recurrence reads its half in reversed time per
+            # utterance (t_rev), so no reversed copy of the input is made
+            K.pack(big, [(X, kin, 0)], m=B * TM, k_pad=kin, split=True)
+            xp = torch.empty((B * TM, 8 * He), dtype=torch.float32, device=dev)
+            K.gemm_tc(big[:, :, :kin], w_ih, m=B * TM, k=kin, bias=b, out=xp, kcb=KCB_ENC,
+                      k_alg=d.feat_dim * d.subsample if l == 0 else 2 * He)
+            # both directions write the next layer's input [h_fwd | h_bwd] in
+            # forward time order, in place (no concatenation / un-reversal pass)
+            Xn = (torch.zeros if kout != 2 * He else torch.empty)(
+                (B * TM, kout), dtype=torch.float32, device=dev)
             main = torch.cuda.current_stream(dev)
-            bufs = [(torch.empty((B, TM, He), dtype=torch.float32, device=dev),
-                     torch.zeros((2, K.operand_format()[0], B, kr), dtype=K.operand_format()[1],
-                                 device=dev),
-                     torch.zeros((B + 127) // 128, dtype=torch.int32, device=dev))
-                    for _ in range(2)]
-            for r, (w_ih, w_hh, b) in enumerate(dirs):
+            for r in range(2):
                 st = self.streams[r]
                 st.wait_stream(main)
-                y, rec, sync = bufs[r]
-                for tns in (y, rec, sync, xps[r]):
+                rec = torch.zeros((2, planes, B, kr), dtype=pdt, device=dev)
+                sync = torch.zeros((B + 127) // 128, dtype=torch.int32, device=dev)
+                for tns in (rec, sync, xp, Xn, t_dev):
                     tns.record_stream(st)
                 with torch.cuda.stream(st):
-                    # one persistent launch per direction (grid barrier per step)
+                    # one persistent cooperative launch per direction
                     e0 = K.log_gemm_begin()
-                    _lib.call("fb_lstm_recurrence", TM, B, He, _lib.ptr(w_hh), kr,
-                              _lib.ptr(xps[r]), TM * 4 * He, 4 * He, _lib.ptr(y), TM * He, He,
-                              _lib.ptr(rec), _lib.ptr(sync), w_hh.fb_acc_scale,
-                              int(st.cuda_stream))
+                    _lib.call("fb_lstm_recurrence", TM, B, He, _lib.ptr(w_hh[r]), kr,
+                              _lib.ptr(xp) + 4 * (4 * He) * r, TM * 8 * He, 8 * He,
+                              _lib.ptr(Xn) + 4 * He * r, TM * kout, kout,
+                              _lib.ptr(rec), _lib.ptr(sync), w_hh[r].fb_acc_scale,
+                              _lib.ptr(t_dev) if r == 1 else None, int(st.cuda_stream))
                     K.log_gemm_end(e0, TM * B, None, 4 * He, He)
-                ys.append(y.reshape(B * TM, He))
             for st in self.streams:
                 main.wait_stream(st)
-            kout = _pad(2 * He)
-            Xn = torch.empty((B * TM, kout), dtype=torch.float32, device=dev)
-            K.pack(Xn, [(ys[0], He, 0), (ys[1], He, 1)], m=B * TM, rows=rev_t)
             X = Xn
-            Xr = torch.empty_like(X)
         C_ = 2 * He
         exact = True
         if out is not None:
