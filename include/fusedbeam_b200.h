@@ -168,6 +168,9 @@ typedef struct {
    * the fly): when non-NULL, the fusion argument of fb_search_step is fp32
    * logits and the fused score is max(logit - fus_norm[slot], fus_floor) */
   const double* fus_norm; double fus_floor;
+  /* optional [B*beam]: position of each slot in next_rows (written with it;
+   * the attention context kernel stores the output GEMM's A there) */
+  int32_t* next_row_pos;
 } fb_search_state_t;
 
 /* One lock-step selection over every active utterance: combine am + lm_weight
@@ -330,7 +333,11 @@ int fb_log_softmax_rows(int32_t m_max, const int32_t* m_dev, const int32_t* rows
  * (q_is_exp != 0: q already holds E_q, e.g. from fb_gemm_t.out_exp2).
  * energy_ws: scratch [num_utts*beam, t_max] fp32; holds the attention
  * weights a[r, t] on return.  sync_ws: num_utts*ceil(beam/2) int32, zero on the
- * first call (the kernels leave it zeroed). */
+ * first call (the kernels leave it zeroed).  ctx_planes (optional): the context
+ * is also stored in the operand format (fb_operand_format) at
+ * ctx_planes + p*ctx_plane_stride + ctx_row_pos[r]*ctx_plane_ld, p < planes
+ * (16-bit elements; the output GEMM's A from its column H on, see
+ * fb_search_state_t.next_row_pos). */
 /* Tiling of the following fb_attention_step launches (0 = default): frame
  * warps per energy CTA (2/4/8), rows per energy CTA (even, <= 16), encoder
  * column quads per context CTA.  Finer tiles pay off when few utterances are
@@ -343,7 +350,8 @@ int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts, const int32_
                       float* q, int64_t ldq, const int32_t* parent, const double* acc_in,
                       double* acc_out, double* cov_out, float* ctx_out, int64_t ld_ctx,
                       float* attn_out, int64_t ld_attn, float* energy_ws, int32_t* sync_ws,
-                      int32_t q_is_exp, void* stream);
+                      int32_t q_is_exp, void* ctx_planes, int64_t ctx_plane_stride,
+                      int64_t ctx_plane_ld, const int32_t* ctx_row_pos, void* stream);
 
 /* y[i] = exp(2 x[i]) (attention keys -> E_K, once per batch). */
 int fb_exp2x(int64_t n, const float* x, float* y, void* stream);

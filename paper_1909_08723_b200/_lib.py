@@ -43,7 +43,8 @@ class FbSearchState(C.Structure):
         "fin_valid", "fin_total", "fin_len", "fin_tokens", "fin_acc",
         "res_len", "res_score", "res_finished", "res_steps", "res_tokens", "res_acc",
         "next_rows", "next_count", "cand_score_ws", "cand_flat_ws")] + [
-        ("force_two_stage", i32), ("pad1", i32), ("fus_norm", vp), ("fus_floor", C.c_double)]
+        ("force_two_stage", i32), ("pad1", i32), ("fus_norm", vp), ("fus_floor", C.c_double),
+        ("next_row_pos", vp)]
 
 
 class FbGemm(C.Structure):
@@ -98,7 +99,7 @@ _SIGS = {
     "fb_set_attention_tiling": (C.c_int, [i32, i32, i32]),
     "fb_attention_step": (C.c_int, [C.POINTER(FbSearchCfg), i32, vp, vp, vp, vp, vp, i32, i32,
                                     vp, vp, i64, vp, vp, vp, vp, vp, i64, vp, i64, vp, vp, i32,
-                                    vp]),
+                                    vp, i64, i64, vp, vp]),
     "fb_spec_events": (C.c_int, [C.POINTER(FbTrie), i32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                  vp]),
     "fb_boundary_plan": (C.c_int, [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp,

@@ -504,9 +504,12 @@ __global__ void __launch_bounds__(kCtxMaxThreads)
 att_context_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
                    const int32_t* __restrict__ n_live, const int32_t* __restrict__ t_enc,
                    const float* __restrict__ enc, int C, const float* __restrict__ alpha,
-                   float* __restrict__ ctx_out, int64_t ld_ctx) {
+                   float* __restrict__ ctx_out, int64_t ld_ctx, uint16_t* __restrict__ planes,
+                   int64_t plane_stride, int64_t ld_planes, const int32_t* __restrict__ row_pos) {
   // CTA = (utterance, group of RB rows, column chunk); thread = 4 adjacent
-  // encoder columns (float4 loads, register double buffer), alpha tile in smem
+  // encoder columns (float4 loads, register double buffer), alpha tile in smem.
+  // planes != NULL: the context is also stored as operand planes at GEMM row
+  // row_pos[slot] (the output GEMM's A, which then needs no pack)
   const int u = blockIdx.x;
   if (!active[u]) return;
   const int n = n_live[u];
@@ -579,6 +582,25 @@ att_context_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
 #pragma unroll
   for (int r = 0; r < RB; ++r)
     if (r < rows) *reinterpret_cast<float4*>(ctx_out + (int64_t)(slot0 + r) * ld_ctx + col) = acc[r];
+  if (planes != nullptr) {
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      if (r >= rows) continue;
+      uint16_t e[4][3], pl[3][4];
+      split_operand(acc[r].x, e[0]);
+      split_operand(acc[r].y, e[1]);
+      split_operand(acc[r].z, e[2]);
+      split_operand(acc[r].w, e[3]);
+#pragma unroll
+      for (int pp = 0; pp < kPlanes; ++pp)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pl[pp][k] = e[k][pp];
+      uint16_t* o = planes + (int64_t)row_pos[slot0 + r] * ld_planes + col;
+#pragma unroll
+      for (int pp = 0; pp < kPlanes; ++pp)
+        *reinterpret_cast<uint2*>(o + pp * plane_stride) = *reinterpret_cast<uint2*>(pl[pp]);
+    }
+  }
 }
 
 // ---------------------------------------------------------- LM bookkeeping --
@@ -793,9 +815,14 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
                                  double* acc_out, double* cov_out, float* ctx_out,
                                  int64_t ld_ctx, float* attn_out, int64_t ld_attn,
                                  float* energy_ws, int32_t* sync_ws, int32_t q_is_exp,
+                                 void* ctx_planes, int64_t ctx_plane_stride,
+                                 int64_t ctx_plane_ld, const int32_t* ctx_row_pos,
                                  void* stream) {
   FB_CHECK_ARG(cfg && keys && enc && v && q && acc_in && acc_out && ctx_out && energy_ws &&
                    sync_ws, "null attention args");
+  FB_CHECK_ARG(!ctx_planes || (ctx_row_pos && ctx_plane_ld % 4 == 0 && ctx_plane_stride % 4 == 0 &&
+                               (reinterpret_cast<uintptr_t>(ctx_planes) & 7) == 0),
+               "context planes need row positions and 8-byte aligned rows");
   FB_CHECK_ARG(cfg->cov_mode == 0 || cov_out, "coverage output required");
   FB_CHECK_ARG(cfg->beam <= kMaxBeam, "beam too large for the attention kernels");
   FB_CHECK_ARG(att_dim % 4 == 0 && ldq % 4 == 0,
@@ -885,7 +912,9 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
   const int ctx_threads = ((qpc + 31) / 32) * 32;
 #define FB_CTX(R)                                                                             \
   att_context_kernel<R><<<gc, ctx_threads, sm_c, s>>>(*cfg, active, n_live, t_enc, enc, ctx_dim, \
-                                                      energy_ws, ctx_out, ld_ctx)
+                                                      energy_ws, ctx_out, ld_ctx,          \
+                                                      (uint16_t*)ctx_planes, ctx_plane_stride, \
+                                                      ctx_plane_ld, ctx_row_pos)
   if (RB == 4) FB_CTX(4); else if (RB == 8) FB_CTX(8); else if (RB == 12) FB_CTX(12); else FB_CTX(16);
 #undef FB_CTX
   count_launch();

@@ -784,7 +784,7 @@ __global__ void eos_fixup_kernel(int n_max, const int32_t* __restrict__ cnt,
 
 // Deterministic compact list of rows that enter the next step.
 __global__ void compact_rows_kernel(int B, int K, const int32_t* active, const int32_t* n_live,
-                                    int32_t* rows, int32_t* count) {
+                                    int32_t* rows, int32_t* count, int32_t* row_pos) {
   __shared__ int wsum[32];
   __shared__ int carry;
   if (threadIdx.x == 0) carry = 0;
@@ -811,6 +811,8 @@ __global__ void compact_rows_kernel(int B, int K, const int32_t* active, const i
     __syncthreads();
     const int pos = carry + (warp ? wsum[warp - 1] : 0) + x - c;
     for (int i = 0; i < c; ++i) rows[pos + i] = u * K + i;
+    if (row_pos != nullptr)
+      for (int i = 0; i < c; ++i) row_pos[u * K + i] = pos + i;
     __syncthreads();
     if (threadIdx.x == 0) carry += wsum[(blockDim.x >> 5) - 1];
     __syncthreads();
@@ -832,6 +834,7 @@ __global__ void search_init_kernel(fb_search_cfg_t c, fb_search_state_t st, int 
     st.parent[u * K] = u * K;
     st.last_tok[u * K] = -1;
     st.next_rows[u] = u * K;
+    if (st.next_row_pos != nullptr) st.next_row_pos[u * K] = u;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *st.next_count = B;
 }
@@ -918,7 +921,7 @@ extern "C" int fb_search_step(const fb_search_cfg_t* cfg, const fb_search_state_
   int rc = check_launch("search_step");
   if (rc) return rc;
   compact_rows_kernel<<<1, 1024, 0, s>>>(num_utts, cfg->beam, st->active, st->n_live,
-                                         st->next_rows, st->next_count);
+                                         st->next_rows, st->next_count, st->next_row_pos);
   count_launch();
   return check_launch("compact_rows");
 }

@@ -34,8 +34,8 @@ from . import _lib
 from . import kernels as K
 from .decoder import DecodeConfig, DecodeResult, SearchBuffers, search_cfg
 from .errors import ConfigError
-from .models import (AM_PIPELINE, LM_SPLITK, AmState, SubLmState, lm_step, split_scratch,
-                     subword_step)
+from .models import (AM_CTX_PLANES, AM_PIPELINE, LM_SPLITK, AmState, SubLmState, lm_step,
+                     split_scratch, subword_step)
 
 P = _lib.ptr
 
@@ -246,7 +246,9 @@ class _Session:
         self.X2 = [AmState(L, N, H, C_, dev), AmState(L, N, H, C_, dev)]
         self.scratch = split_scratch(N, w.k_max, dev)
         # one A operand per decoder GEMM (epilogues write the next one's h planes)
-        self.am_abufs = ([split_scratch(N, k, dev) for k in scorer.step_fn.abuf_shapes()]
+        # (zeroed: the output A's context columns come from the attention
+        # kernel by row position, its padding columns are never written)
+        self.am_abufs = ([split_scratch(N, k, dev).zero_() for k in scorer.step_fn.abuf_shapes()]
                          if AM_PIPELINE else None)
         self.pack_stream = torch.cuda.Stream(device=dev) if AM_PIPELINE else None
         self.q = torch.empty((N, d.att), dtype=torch.float32, device=dev)
@@ -401,7 +403,8 @@ class FusedDecoder:
                            acc_in=buf.acc[c], acc_out=buf.acc[1 - c], cov=buf.cov,
                            energy=S.energy, sync=S.att_sync,
                            timer=None if isinstance(tm, _NoTimer) else tm,
-                           abufs=S.am_abufs, pack_stream=S.pack_stream)
+                           abufs=S.am_abufs, pack_stream=S.pack_stream,
+                           row_pos=buf.row_pos if AM_CTX_PLANES else None)
         fus_buf = S.fus_buf
         if S.sub is not None:
             with tm("lm_subword"):

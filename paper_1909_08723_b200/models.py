@@ -62,6 +62,9 @@ KCB_LM = int(_os.environ.get("FB_KCB_LM", "0"))       # word / token LM GEMMs
 # fused GEMM epilogues: E_q = exp(2 q) for the attention, log-softmax of the
 # acoustic output (dev knob for A/B timing)
 FUSE_EPI = _os.environ.get("FB_FUSE_EPI", "1") == "1"
+# fused engine: the attention context kernel writes the acoustic output GEMM's
+# A (context planes at each row's compact position) instead of a pack launch
+AM_CTX_PLANES = _os.environ.get("FB_AM_CTX_PLANES", "1") == "1"
 
 
 def _pad(k: int, g: int = KGRAN) -> int:
@@ -316,7 +319,7 @@ class DecoderStep:
                  cur: AmState, scratch: torch.Tensor, q: torch.Tensor, logits: torch.Tensor,
                  am_logp: torch.Tensor, cfg_ref, num_utts: int, active, n_live, t_enc,
                  keys, enc, acc_in, acc_out, cov, energy, sync, attn_out=None,
-                 timer=None, abufs=None, pack_stream=None) -> None:
+                 timer=None, abufs=None, pack_stream=None, row_pos=None) -> None:
         w, d = self.w, self.w.d
         tm = timer if timer is not None else _null_timer
         H, C_, E = d.dec_hidden, d.ctx, d.emb
@@ -328,7 +331,7 @@ class DecoderStep:
                             logits=logits, am_logp=am_logp, cfg_ref=cfg_ref,
                             num_utts=num_utts, active=active, n_live=n_live, t_enc=t_enc,
                             keys=keys, enc=enc, acc_in=acc_in, acc_out=acc_out, cov=cov,
-                            energy=energy, sync=sync, attn_out=attn_out)
+                            energy=energy, sync=sync, attn_out=attn_out, row_pos=row_pos)
             return
         span = tm("am_lstm")
         span.__enter__()
@@ -354,7 +357,7 @@ class DecoderStep:
                       _lib.ptr(acc_in), _lib.ptr(acc_out), _lib.ptr(cov), _lib.ptr(cur.ctx),
                       cur.ctx.stride(0), _lib.ptr(attn_out),
                       0 if attn_out is None else attn_out.stride(0), _lib.ptr(energy),
-                      _lib.ptr(sync), 0, _lib.stream_ptr())
+                      _lib.ptr(sync), 0, None, 0, 0, None, _lib.stream_ptr())
         ko = w.w_out.shape[1]
         with tm("am_output"):
             K.pack(scratch, [(top, H, 1), (cur.ctx, C_, 1)], k_pad=ko, split=True, **kw)
@@ -368,12 +371,15 @@ class DecoderStep:
 
     def _pipelined(self, A, pack_stream, tm, kw, *, N, m, m_dev, rows, parent, last_tok, prev,
                    cur, q, logits, am_logp, cfg_ref, num_utts, active, n_live, t_enc, keys,
-                   enc, acc_in, acc_out, cov, energy, sync, attn_out):
+                   enc, acc_in, acc_out, cov, energy, sync, attn_out, row_pos=None):
         """Same step with one A operand per GEMM: each LSTM epilogue writes its h
         as bf16 planes straight into the next GEMM's A (h_split, GEMM row
         order), and the previous-step segments of layers 1.. (ctx, h gathered by
         parent) are packed on `pack_stream` while layer 0 runs -- two packs on
-        the critical path instead of L + 2."""
+        the critical path instead of L + 2.  With `row_pos` (each slot's
+        position in `rows`, written by the search's row compaction) the
+        attention context kernel stores the context planes of the output A
+        itself and the second pack goes too."""
         w, d = self.w, self.w.d
         H, C_, E = d.dec_hidden, d.ctx, d.emb
         L = d.dec_layers
@@ -420,9 +426,12 @@ class DecoderStep:
                       _lib.ptr(acc_in), _lib.ptr(acc_out), _lib.ptr(cov), _lib.ptr(cur.ctx),
                       cur.ctx.stride(0), _lib.ptr(attn_out),
                       0 if attn_out is None else attn_out.stride(0), _lib.ptr(energy),
-                      _lib.ptr(sync), 1 if FUSE_EPI else 0, _lib.stream_ptr())
+                      _lib.ptr(sync), 1 if FUSE_EPI else 0,
+                      None if row_pos is None else A[L].data_ptr() + H * A[L].element_size(),
+                      A[L].stride(0), A[L].stride(1), _lib.ptr(row_pos), _lib.stream_ptr())
         with tm("am_output"):
-            K.pack(A[L], [(None, H, 5), (cur.ctx, C_, 1)], k_pad=ko, split=True, **kw)
+            if row_pos is None:
+                K.pack(A[L], [(None, H, 5), (cur.ctx, C_, 1)], k_pad=ko, split=True, **kw)
             if d.vocab <= 64 and FUSE_EPI:
                 # the epilogue holds whole rows: log-softmax fused, logits never stored
                 K.gemm_tc(A[L], w.w_out, k=ko, bias=w.b_out, out=am_logp, m=m, m_dev=m_dev,

@@ -38,7 +38,7 @@ for name, B, K, T, A, Cd in (("c2", 512, 10, 225, 320, 640), ("c4", 32, 60, 875,
         q.copy_(q0)
         _lib.call("fb_attention_step", C.byref(cfg), B, P(active), P(n_live), P(t_enc), P(keys),
                   P(enc), A, Cd, P(v), P(q), A, P(parent), P(acc_in), P(acc_out), None, P(ctx),
-                  Cd, None, 0, P(energy), P(sync), 0, _lib.stream_ptr())
+                  Cd, None, 0, P(energy), P(sync), 0, None, 0, 0, None, _lib.stream_ptr())
     for _ in range(3):
         run()
     torch.cuda.synchronize()
