@@ -286,7 +286,8 @@ int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_rows, void*
  * One persistent cooperative launch (co-residency checked against the
  * device; FB_ERR_CONFIG if the grid cannot fit): the CTAs of each 128-row
  * tile loop over t behind a barrier on their own counter in sync_ws
- * (ceil(batch/128) uint32, reset here).  W_hh stays in shared memory.
+ * (32 * ceil(batch/128) uint32: one 128-byte line per tile, reset here).
+ * W_hh stays in shared memory.
  * t_rev (optional, [batch] int32): the backward direction -- step t of row b
  * reads xp and writes y at frame t_rev[b] - 1 - t (t < t_rev[b]), so a
  * length-padded batch needs no reversed copies of its inputs or outputs. */

@@ -41,8 +41,11 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 #define TRACE(slot, i) do { if (blockIdx.x == 0 && (i) < 256 && (threadIdx.x & 31) == 0) g_trace[slot][i] = gtime(); } while (0)
+// per-CTA stamp of one chosen step (recurrence skew)
+#define TRACE_CTA(slot, t, t0) do { if ((t) == (t0) && blockIdx.x < 256) g_trace[slot][blockIdx.x] = gtime(); } while (0)
 #else
 #define TRACE(slot, i) do {} while (0)
+#define TRACE_CTA(slot, t, t0) do {} while (0)
 #endif
 
 constexpr int TC_BM = 128;
@@ -826,21 +829,64 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   return v;
 }
 
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+#ifndef FB_REC_POLL
+#define FB_REC_POLL 0        // barrier poll: 0 acquire + nanosleep, 1 acquire spin, 2 relaxed spin + fence
+#endif
+
 constexpr int REC_MAX_STAGES = 4;
+#ifndef FB_REC_SYNC_STRIDE
+#define FB_REC_SYNC_STRIDE 32
+#endif
+// one 128-byte line per row tile's step counter (its 10 CTAs' atomics and
+// polls do not contend with the other tiles')
+constexpr int kRecSyncStride = FB_REC_SYNC_STRIDE;
+#ifndef FB_REC_EARLY_PUB
+#define FB_REC_EARLY_PUB 1   // publish h planes before storing the fp32 output
+#endif
+#ifndef FB_REC_PF
+#define FB_REC_PF 1          // L2 prefetch of the next step's input projection
+#endif
+#ifndef FB_REC_CELL7
+#define FB_REC_CELL7 1       // LSTM cell with 5 ex2 + 2 rcp (instead of 5 + 5)
+#endif
+
+// LSTM cell sharing reciprocals: with e_i = exp(-i), e_f = exp(-f),
+// E_g = exp(2g),  c' = c sig(f) + sig(i) tanh(g)
+//   = [c (1+e_i)(1+E_g) + (E_g-1)(1+e_f)] / [(1+e_f)(1+e_i)(1+E_g)],
+// h = sig(o) tanh(c') = (E_c-1) / [(1+e_o)(1+E_c)], E_c = exp(2c').
+// Arguments are clamped where the functions are saturated in fp32 (sigmoid
+// below 1e-13, |tanh| within 3e-8 of 1) so the products stay below 1e34.
+__device__ __forceinline__ void rec_cell(float gi, float gf, float gg, float go, float& c,
+                                         float& h) {
+  const float ei = __expf(-fmaxf(gi, -30.f)), ef = __expf(-fmaxf(gf, -30.f));
+  const float eg = __expf(2.f * fminf(fmaxf(gg, -9.f), 9.f));
+  const float pi = 1.f + ei, pg = 1.f + eg, pf = 1.f + ef;
+  const float pig = pi * pg;
+  c = __fdividef(fmaf(c, pig, (eg - 1.f) * pf), pig * pf);
+  const float eo = __expf(-fmaxf(go, -30.f));
+  const float ec = __expf(2.f * fminf(fmaxf(c, -9.f), 9.f));
+  const float pc = 1.f + ec;
+  h = __fdividef(ec - 1.f, (1.f + eo) * pc);
+}
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
 lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                 const __grid_constant__ CUtensorMap tmW, fb_gemm_t g0, int steps, int num_kb,
                 int kcb, const float* xp, int64_t step_xp, float* y, int64_t ld_y,
                 int64_t step_y, uint16_t* rec, int64_t plane, unsigned* sync, int nst,
-                const int32_t* t_rev) {
+                const int32_t* t_rev, int wide) {
   constexpr int BN = 128;
   const int batch = g0.m_max;
   const int m_tiles = (batch + TC_BM - 1) / TC_BM;
   // rows of different m-tiles never interact: each m-tile's n-tile CTAs
   // synchronise among themselves (one counter per m-tile), not grid-wide
   const int n_peers = gridDim.x / m_tiles;
-  unsigned* msync = sync + (blockIdx.x % m_tiles);
+  unsigned* msync = sync + (blockIdx.x % m_tiles) * kRecSyncStride;
   const int tile = blockIdx.x;
   const int m0 = (tile % m_tiles) * TC_BM, n0 = (tile / m_tiles) * BN;
 
@@ -855,6 +901,11 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
   __shared__ __align__(8) uint64_t bar_full[REC_MAX_STAGES], bar_empty[REC_MAX_STAGES];
   __shared__ __align__(8) uint64_t bar_tfull[TC_NACC], bar_tempty[TC_NACC], bar_w;
   __shared__ uint32_t tmem_base_sh;
+#if FB_REC_POLL == 3
+  __shared__ __align__(8) uint64_t bar_poll;
+  __shared__ __align__(16) unsigned poll_buf[4];
+  uint32_t poll_ph = 0;
+#endif
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -863,6 +914,9 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
       mbar_init(smem_u32(&bar_empty[s]), 1);
     }
     mbar_init(smem_u32(&bar_w), 1);
+#if FB_REC_POLL == 3
+    mbar_init(smem_u32(&bar_poll), 1);
+#endif
     for (int a = 0; a < TC_NACC; ++a) {
       mbar_init(smem_u32(&bar_tfull[a]), 1);
       mbar_init(smem_u32(&bar_tempty[a]), TC_EPI_THREADS);
@@ -891,8 +945,37 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
         // h_{t-1} complete in every CTA (grid barrier), then visible to TMA
         const unsigned target = (unsigned)(n_peers * t);
         TRACE(0, t);
+        TRACE_CTA(6, t, 101);
+#if FB_REC_POLL == 3
+        // poll through the TMA unit (async proxy, L2): the epilogue warps'
+        // input-projection loads fill the SM's load queue at this moment, and
+        // a generic load of the counter waits behind them for microseconds
+        for (;;) {
+          mbar_expect_tx(smem_u32(&bar_poll), 16);
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];"
+              ::"r"(smem_u32(poll_buf)), "l"(msync), "r"(smem_u32(&bar_poll)) : "memory");
+          mbar_wait(smem_u32(&bar_poll), poll_ph);
+          poll_ph ^= 1;
+          if (*reinterpret_cast<volatile unsigned*>(poll_buf) >= target) break;
+        }
+#elif FB_REC_POLL == 1
+        while (ld_acquire_u32(msync) < target) {}
+#elif FB_REC_POLL == 2
+        while (ld_relaxed_u32(msync) < target) {}
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#else
         while (ld_acquire_u32(msync) < target) __nanosleep(32);
+#endif
         TRACE(1, t);
+        TRACE_CTA(7, t, 101);
+#ifdef FB_GEMM_TRACE
+        if (t == 101) {
+          unsigned smid;
+          asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+          g_trace[8][blockIdx.x] = smid;
+        }
+#endif
         asm volatile("fence.proxy.async.global;" ::: "memory");
         const CUtensorMap* tmA = (t & 1) ? &tmA1 : &tmA0;
         for (int kb = 0; kb < num_kb; ++kb, ++gk) {
@@ -963,8 +1046,20 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
           reinterpret_cast<const float4*>(xp + (int64_t)(t < t_row ? t_row - 1 - t : t) * step_xp +
                                           (int64_t)(ok ? row : 0) * g0.ld_add) +
           unitb;
+      if (wide & 1) {
+        // 256-bit loads (sm_100): each lane is a different row, so every load
+        // instruction costs the L1 one request per lane; half the instructions
+        // halve this step's request burst (which also delays the barrier poll)
 #pragma unroll
-      for (int u = 0; u < 16; ++u) xa[u] = __ldg(xr + u);
+        for (int u = 0; u < 16; u += 2)
+          asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=f"(xa[u].x), "=f"(xa[u].y), "=f"(xa[u].z), "=f"(xa[u].w),
+                         "=f"(xa[u + 1].x), "=f"(xa[u + 1].y), "=f"(xa[u + 1].z), "=f"(xa[u + 1].w)
+                       : "l"(xr + u));
+      } else {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) xa[u] = __ldg(xr + u);
+      }
       // K in chunks of kcb blocks, each in its own TMEM slot, summed here with
       // round-to-nearest adds (the in-TMEM adds truncate: a whole-K slot
       // biases every gate pre-activation toward zero).  The input projection
@@ -1000,6 +1095,19 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
                      : "memory");
       }
       TRACE(2, t);
+#if FB_REC_PF
+      // next step's input projection into L2 now: the fetch from HBM overlaps
+      // this step's cell / publish / barrier, and the loads at the top of the
+      // next step hit L2 -- a burst of HBM misses there delays the barrier
+      // poll's reply for microseconds (prefetches return no data to the SM)
+      if (t + 1 < steps && ok) {
+        const char* nx = reinterpret_cast<const char*>(
+            xp + (int64_t)(t + 1 < t_row ? t_row - 2 - t : t + 1) * step_xp + (int64_t)row * g0.ld_add +
+            4 * unitb);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(nx));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(nx + 128));
+      }
+#endif
       float hv[16];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -1009,16 +1117,24 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
           const int u = c * 8 + u8;
           const float gi = v[4 * u8] * sc, gf = v[4 * u8 + 1] * sc;
           const float gg = v[4 * u8 + 2] * sc, go = v[4 * u8 + 3] * sc;
+#if FB_REC_CELL7
+          rec_cell(gi, gf, gg, go, cst[u], hv[u]);
+#else
           cst[u] = fsig(gf) * cst[u] + fsig(gi) * ftanh(gg);
           hv[u] = fsig(go) * ftanh(cst[u]);
+#endif
         }
       }
+      float* yrow = y + (int64_t)(t < t_row ? t_row - 1 - t : t) * step_y + (int64_t)row * ld_y + unitb;
+#if !FB_REC_EARLY_PUB
       if (ok) {
-        float4* yo = reinterpret_cast<float4*>(y + (int64_t)(t < t_row ? t_row - 1 - t : t) * step_y +
-                                               (int64_t)row * ld_y + unitb);
+        float4* yo = reinterpret_cast<float4*>(yrow);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           yo[q] = make_float4(hv[4 * q], hv[4 * q + 1], hv[4 * q + 2], hv[4 * q + 3]);
+      }
+#endif
+      if (ok) {
         uint16_t pl[3][16];
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
@@ -1030,9 +1146,16 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
         uint16_t* o = rec + (int64_t)((t & 1) ^ 1) * kPlanes * plane + (int64_t)row * g0.ld_hs + unitb;
 #pragma unroll
         for (int q = 0; q < kPlanes; ++q) {
-          uint4* d = reinterpret_cast<uint4*>(o + (int64_t)q * plane);
-          d[0] = *reinterpret_cast<const uint4*>(&pl[q][0]);
-          d[1] = *reinterpret_cast<const uint4*>(&pl[q][8]);
+          if (wide & 4) {
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(&pl[q][0]);
+            asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(o + (int64_t)q * plane),
+                         "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]),
+                         "r"(w[7]) : "memory");
+          } else {
+            uint4* d = reinterpret_cast<uint4*>(o + (int64_t)q * plane);
+            d[0] = *reinterpret_cast<const uint4*>(&pl[q][0]);
+            d[1] = *reinterpret_cast<const uint4*>(&pl[q][8]);
+          }
         }
       }
       TRACE(4, t);
@@ -1043,8 +1166,24 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
       if (warp == 2 && lane == 0) {
         asm volatile("fence.proxy.async.global;" ::: "memory");
         atomicAdd(msync, 1u);
+        TRACE_CTA(9, t, 100);
       }
       TRACE(3, t);
+#if FB_REC_EARLY_PUB
+      // the fp32 output is not read by the peers: stored after the publish
+      if (ok && (wide & 2)) {
+#pragma unroll
+        for (int q = 0; q < 16; q += 8)
+          asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(yrow + q),
+                       "f"(hv[q]), "f"(hv[q + 1]), "f"(hv[q + 2]), "f"(hv[q + 3]), "f"(hv[q + 4]),
+                       "f"(hv[q + 5]), "f"(hv[q + 6]), "f"(hv[q + 7]) : "memory");
+      } else if (ok) {
+        float4* yo = reinterpret_cast<float4*>(yrow);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          yo[q] = make_float4(hv[4 * q], hv[4 * q + 1], hv[4 * q + 2], hv[4 * q + 3]);
+      }
+#endif
     }
   }
   __syncthreads();
@@ -1288,7 +1427,7 @@ extern "C" int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden,
   }
   int rc = make_map(&tw, w_hh, g.n, k, k, 128);
   if (rc) return rc;
-  cudaMemsetAsync(sync_ws, 0, sizeof(uint32_t) * m_tiles, s);
+  cudaMemsetAsync(sync_ws, 0, sizeof(uint32_t) * m_tiles * kRecSyncStride, s);
   // shared memory: the resident W_hh slice + a ring of A-plane stages
   const int num_kb = k / TC_BK;
   const size_t w_bytes = (size_t)num_kb * 128 * TC_BK * 2;
@@ -1313,10 +1452,17 @@ extern "C" int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden,
   // TMEM accumulation chunk of the recurrence (K blocks; dev override FB_REC_KCB)
   static const int kcb_env = getenv("FB_REC_KCB") ? std::max(1, atoi(getenv("FB_REC_KCB"))) : 1;
   int nkb = num_kb, kcb = std::min(kcb_env, num_kb);
+  // 256-bit accesses where the layouts are 32-byte aligned: bit 0 xp loads,
+  // bit 1 y stores, bit 2 operand-plane stores (dev override FB_REC_WIDE)
+  static const int wide_env = getenv("FB_REC_WIDE") ? atoi(getenv("FB_REC_WIDE")) : 7;
+  int wide = wide_env &
+             ((((uintptr_t)xp % 32) == 0 && ld_xp % 8 == 0 && step_xp % 8 == 0 ? 1 : 0) |
+              (((uintptr_t)y % 32) == 0 && ld_y % 8 == 0 && step_y % 8 == 0 ? 2 : 0) |
+              (((uintptr_t)rec % 32) == 0 && k % 16 == 0 ? 4 : 0));
   void* args[] = {(void*)&ta[0], (void*)&ta[1], (void*)&tw, (void*)&g, (void*)&steps,
                   (void*)&nkb, (void*)&kcb, (void*)&xp, (void*)&step_xp, (void*)&y,
                   (void*)&ld_y, (void*)&step_y, (void*)&r, (void*)&plane, (void*)&sync_ws,
-                  (void*)&nst, (void*)&t_rev};
+                  (void*)&nst, (void*)&t_rev, (void*)&wide};
   const cudaError_t e = cudaLaunchCooperativeKernel((const void*)lstm_rec_kernel,
                                                     dim3(m_tiles * n_tiles), dim3(TC_THREADS),
                                                     args, smem, s);

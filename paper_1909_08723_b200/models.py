@@ -260,7 +260,7 @@ class Encoder:
                 st = self.streams[r]
                 st.wait_stream(main)
                 rec = torch.zeros((2, planes, B, kr), dtype=pdt, device=dev)
-                sync = torch.zeros((B + 127) // 128, dtype=torch.int32, device=dev)
+                sync = torch.zeros(32 * ((B + 127) // 128), dtype=torch.int32, device=dev)
                 for tns in (rec, sync, xp, Xn, t_dev):
                     tns.record_stream(st)
                 with torch.cuda.stream(st):

@@ -22,7 +22,7 @@ w = [K.operand_weight(torch.randn(4 * H, k, device=dev) * 0.05) for _ in range(2
 xp = torch.randn(B, TM, 8 * H, device=dev) * 0.1
 y = torch.empty(B, TM, 2 * H, device=dev)
 rec = [torch.zeros(2, planes, B, k, dtype=K.operand_format()[1], device=dev) for _ in range(2)]
-sync = [torch.zeros(8, dtype=torch.int32, device=dev) for _ in range(2)]
+sync = [torch.zeros(32 * 8, dtype=torch.int32, device=dev) for _ in range(2)]
 t_rev = torch.full((B,), TM, dtype=torch.int32, device=dev)
 streams = [torch.cuda.Stream(), torch.cuda.Stream()]
 
@@ -74,3 +74,19 @@ if hasattr(lib, "fb_gemm_trace_read"):
               np.mean(tr[1, 50:200] - tr[3, 49:199]), np.mean(tr[2, s] - tr[1, s]),
               np.mean(tr[4, s] - tr[2, s]), np.mean(tr[5, s] - tr[4, s]),
               np.mean(tr[3, s] - tr[5, s]), (tr[3, 199] - tr[3, 49]) / 150))
+    # per-CTA: publish of step 100, barrier wait start / pass of step 101 (CTA = m-tile + 4 n)
+    n = (B + 127) // 128 * 10
+    pub, ws, ps = tr[9, :n], tr[6, :n], tr[7, :n]
+    m_tiles = (B + 127) // 128
+    for m in range(m_tiles):
+        idx = list(range(m, n, m_tiles))
+        print(f"m-tile {m}: publish(100) spread {pub[idx].max() - pub[idx].min():.2f} us "
+              f"(first {pub[idx].min():.2f}, last {pub[idx].max():.2f}); pass(101) "
+              f"{ps[idx].min():.2f}..{ps[idx].max():.2f}; last publish -> first pass "
+              f"{ps[idx].min() - pub[idx].max():.2f} us")
+    sm = buf[8, :n].astype(np.int64)
+    print("per CTA (m-tile 0..3 interleaved): cta sm wait_start(101) publish(100) pass(101)")
+    for i in np.argsort(ps)[:: max(1, n // 20)]:
+        print(f"  {i:3d} sm{sm[i]:3d} {ws[i]:9.2f} {pub[i]:9.2f} {ps[i]:9.2f}")
+    late = ps - ps.min()
+    print("pass(101) lateness vs sm id: corr", np.corrcoef(sm, late)[0, 1])
