@@ -349,26 +349,21 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
 #pragma unroll
           for (int u = 0; u < 8; ++u) hr[u] = 0.f;
         }
-        // every load of the row issued before any use (one memory round trip)
-        float4 b4[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          b4[u] = g.bias ? __ldg(reinterpret_cast<const float4*>(g.bias) + unit0 + u)
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
-        if (g.addend) {
-          const float4* a4p = reinterpret_cast<const float4*>(g.addend + (int64_t)row * g.ld_add) + unit0;
-          float4 a4[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) a4[u] = __ldg(a4p + u);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            b4[u].x += a4[u].x; b4[u].y += a4[u].y; b4[u].z += a4[u].z; b4[u].w += a4[u].w;
-          }
-        }
+        // bias (+ addend) fetched per unit at its use: the bias is the same
+        // for every row (L1 hits after the first warp); holding all eight
+        // float4 of both beside the accumulator spilled registers
+        const float4* b4p = g.bias ? reinterpret_cast<const float4*>(g.bias) + unit0 : nullptr;
+        const float4* a4p = g.addend
+            ? reinterpret_cast<const float4*>(g.addend + (int64_t)row * g.ld_add) + unit0 : nullptr;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const float gi = v[4 * u] + b4[u].x, gf = v[4 * u + 1] + b4[u].y;
-          const float gg = v[4 * u + 2] + b4[u].z, go = v[4 * u + 3] + b4[u].w;
+          float4 b = b4p ? __ldg(b4p + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+          if (a4p) {
+            const float4 a = __ldg(a4p + u);
+            b.x += a.x; b.y += a.y; b.z += a.z; b.w += a.w;
+          }
+          const float gi = v[4 * u] + b.x, gf = v[4 * u + 1] + b.y;
+          const float gg = v[4 * u + 2] + b.z, go = v[4 * u + 3] + b.w;
           cv[u] = fsig(gf) * cp[u] + fsig(gi) * ftanh(gg);
           hv[u] = fsig(go) * ftanh(cv[u]) + hr[u];
         }
@@ -1067,7 +1062,8 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
       // its registers are free before the remaining chunks arrive.
       const float sc = g0.acc_scale, inv_sc = 1.0f / sc;
       float acc[2][32];
-      for (int kb0 = 0; kb0 < num_kb; kb0 += kcb) {
+      {
+        // chunk 0 (+ the input projection)
         const int slot = cc % TC_NACC;
         mbar_wait(smem_u32(&bar_tfull[slot]), (cc / TC_NACC) & 1);
         ++cc;
@@ -1076,19 +1072,30 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
         for (int c = 0; c < 2; ++c) {
           float v[32];
           tmem_ld32(tl + slot * BN + (half * 2 + c) * 32, v);
-          if (kb0 == 0) {
 #pragma unroll
-            for (int u8 = 0; u8 < 8; ++u8) {
-              const float4 x4 = xa[c * 8 + u8];
-              acc[c][4 * u8] = v[4 * u8] + x4.x * inv_sc;
-              acc[c][4 * u8 + 1] = v[4 * u8 + 1] + x4.y * inv_sc;
-              acc[c][4 * u8 + 2] = v[4 * u8 + 2] + x4.z * inv_sc;
-              acc[c][4 * u8 + 3] = v[4 * u8 + 3] + x4.w * inv_sc;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) acc[c][j] += v[j];
+          for (int u8 = 0; u8 < 8; ++u8) {
+            const float4 x4 = xa[c * 8 + u8];
+            acc[c][4 * u8] = v[4 * u8] + x4.x * inv_sc;
+            acc[c][4 * u8 + 1] = v[4 * u8 + 1] + x4.y * inv_sc;
+            acc[c][4 * u8 + 2] = v[4 * u8 + 2] + x4.z * inv_sc;
+            acc[c][4 * u8 + 3] = v[4 * u8 + 3] + x4.w * inv_sc;
           }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[slot]))
+                     : "memory");
+      }
+      for (int kb0 = kcb; kb0 < num_kb; kb0 += kcb) {
+        const int slot = cc % TC_NACC;
+        mbar_wait(smem_u32(&bar_tfull[slot]), (cc / TC_NACC) & 1);
+        ++cc;
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          float v[32];
+          tmem_ld32(tl + slot * BN + (half * 2 + c) * 32, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[c][j] += v[j];
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[slot]))
