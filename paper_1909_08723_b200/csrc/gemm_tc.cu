@@ -843,6 +843,9 @@ constexpr int kRecSyncStride = FB_REC_SYNC_STRIDE;
 #ifndef FB_REC_EARLY_PUB
 #define FB_REC_EARLY_PUB 1   // publish h planes before storing the fp32 output
 #endif
+#ifndef FB_REC_XA_AFTER_PASS
+#define FB_REC_XA_AFTER_PASS 1   // input-projection loads wait for the step barrier
+#endif
 #ifndef FB_REC_PF
 #define FB_REC_PF 1          // L2 prefetch of the next step's input projection
 #endif
@@ -894,7 +897,7 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
   unsigned char* wres = base;                             // resident W_hh: num_kb tiles
   unsigned char* ring = base + (size_t)num_kb * W_TILE;
   __shared__ __align__(8) uint64_t bar_full[REC_MAX_STAGES], bar_empty[REC_MAX_STAGES];
-  __shared__ __align__(8) uint64_t bar_tfull[TC_NACC], bar_tempty[TC_NACC], bar_w;
+  __shared__ __align__(8) uint64_t bar_tfull[TC_NACC], bar_tempty[TC_NACC], bar_w, bar_pass;
   __shared__ uint32_t tmem_base_sh;
 #if FB_REC_POLL == 3
   __shared__ __align__(8) uint64_t bar_poll;
@@ -909,6 +912,7 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
       mbar_init(smem_u32(&bar_empty[s]), 1);
     }
     mbar_init(smem_u32(&bar_w), 1);
+    mbar_init(smem_u32(&bar_pass), 1);
 #if FB_REC_POLL == 3
     mbar_init(smem_u32(&bar_poll), 1);
 #endif
@@ -964,6 +968,11 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
 #endif
         TRACE(1, t);
         TRACE_CTA(7, t, 101);
+#if FB_REC_XA_AFTER_PASS
+        // step t's barrier passed: the epilogue may now load its input
+        // projection (overlapping the A loads and the MMA, not the poll)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_pass)) : "memory");
+#endif
 #ifdef FB_GEMM_TRACE
         if (t == 101) {
           unsigned smid;
@@ -1037,6 +1046,9 @@ lstm_rec_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant_
     int cc = 0;
     for (int t = 0; t < steps; ++t) {
       float4 xa[16];
+#if FB_REC_XA_AFTER_PASS
+      mbar_wait(smem_u32(&bar_pass), t & 1);
+#endif
       const float4* xr =
           reinterpret_cast<const float4*>(xp + (int64_t)(t < t_row ? t_row - 1 - t : t) * step_xp +
                                           (int64_t)(ok ? row : 0) * g0.ld_add) +
