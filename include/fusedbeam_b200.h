@@ -332,8 +332,9 @@ int fb_log_softmax_rows(int32_t m_max, const int32_t* m_dev, const int32_t* rows
  * (fp64) and its coverage (cfg->cov_mode).  Rows r = u*beam + i, i < n_live[u].
  * q is consumed in place: its live rows are overwritten with E_q = exp(2 q)
  * (q_is_exp != 0: q already holds E_q, e.g. from fb_gemm_t.out_exp2).
- * energy_ws: scratch [num_utts*beam, t_max] fp32; holds the attention
- * weights a[r, t] on return.  sync_ws: num_utts*ceil(beam/2) int32, zero on the
+ * energy_ws: scratch [2][num_utts*beam][t_max] fp32 (the energies of the two
+ * halves of the attention dims, summed in that order); plane 0 holds the
+ * attention weights a[r, t] on return.  sync_ws: num_utts*ceil(beam/2) int32, zero on the
  * first call (the kernels leave it zeroed).  ctx_planes (optional): the context
  * is also stored in the operand format (fb_operand_format) at
  * ctx_planes + p*ctx_plane_stride + ctx_row_pos[r]*ctx_plane_ld, p < planes

@@ -327,7 +327,8 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
                   const float* __restrict__ q, int64_t ldq, float* __restrict__ energy,
                   int32_t* __restrict__ sync_ws, const int32_t* __restrict__ parent,
                   const double* __restrict__ acc_in, double* __restrict__ acc_out,
-                  double* __restrict__ cov_out, float* __restrict__ attn_out, int64_t ld_attn) {
+                  double* __restrict__ cov_out, float* __restrict__ attn_out, int64_t ld_attn,
+                  int parts) {
   // CTA = (utterance, chunk of kEnWarps*32 frames, group of R rows); lane = one
   // frame t, so every energy is a private register sum (no cross-lane
   // reduction).  Keys are read transposed (E_K^T[u][a][t]: coalesced across
@@ -336,35 +337,42 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
   //   v0/d0 + v1/d1 = (v0 d1 + v1 d0) / (d0 d1)   -- one reciprocal per two
   // terms, rows paired in f32x2 registers (FFMA2/FMUL2); d clamped to kDMax2
   // so the product stays finite (tanh is saturated long before).
+  // parts > 1: the attention dims are split over `parts` CTAs (blockIdx.y =
+  // chunk * parts + part), each writing its partial sums to its own plane of
+  // energy; the last CTA adds the planes in part order before the softmax.
+  // (Twice the CTAs of half the work: at c2 one utterance per 8-warp CTA made
+  // 1.15 waves, the second one almost empty.)
   static_assert(R % 2 == 0, "rows come in pairs");
   const int u = blockIdx.x;
   if (!active[u]) return;
   const int T = t_enc[u];
-  const int t0 = blockIdx.y * (kEnWarps * 32);
+  const int part = blockIdx.y % parts;
+  const int t0 = (blockIdx.y / parts) * (kEnWarps * 32);
   if (t0 >= T) return;
+  const int Ap = A / parts, a0 = part * Ap;
   const int n = n_live[u];
   const int r0 = blockIdx.z * R;
   if (r0 >= n) return;
   const int rows = min(R, n - r0);
   extern __shared__ float sm[];
   const int K = cfg.beam, TM = cfg.t_max;
-  float2* vs2 = reinterpret_cast<float2*>(sm);          // [A]  (v_a, v_a)
-  float2* qs2 = vs2 + A;                                // [R/2][A] (Eq_r, Eq_r+1)
+  float2* vs2 = reinterpret_cast<float2*>(sm);          // [Ap]  (v_a, v_a)
+  float2* qs2 = vs2 + Ap;                               // [R/2][Ap] (Eq_r, Eq_r+1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int slot0 = u * K + r0;
   for (int rp = 0; rp < R / 2; ++rp) {
     const int ra = 2 * rp, rb = ra + 1;
-    const float* qa = q + (int64_t)(slot0 + ra) * ldq;
-    const float* qb = q + (int64_t)(slot0 + rb) * ldq;
-    for (int a = tid; a < A; a += blockDim.x)
-      qs2[rp * A + a] = make_float2(ra < rows ? qa[a] : 0.f, rb < rows ? qb[a] : 0.f);
+    const float* qa = q + (int64_t)(slot0 + ra) * ldq + a0;
+    const float* qb = q + (int64_t)(slot0 + rb) * ldq + a0;
+    for (int a = tid; a < Ap; a += blockDim.x)
+      qs2[rp * Ap + a] = make_float2(ra < rows ? qa[a] : 0.f, rb < rows ? qb[a] : 0.f);
   }
-  for (int a = tid; a < A; a += blockDim.x) vs2[a] = make_float2(v[a], v[a]);
+  for (int a = tid; a < Ap; a += blockDim.x) vs2[a] = make_float2(v[a0 + a], v[a0 + a]);
   __syncthreads();
   const int t = t0 + warp * 32 + lane;
   const bool valid = t < T;
   if (t0 + warp * 32 < T) {
-  const float* kt = ekt + (int64_t)u * A * TM + (valid ? t : T - 1);
+  const float* kt = ekt + ((int64_t)u * A + a0) * TM + (valid ? t : T - 1);
   const f2_t one2 = pk2(1.0f, 1.0f);
   f2_t e2[R / 2];
 #pragma unroll
@@ -376,8 +384,8 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
   for (int p = 0; p <= FB_ENERGY_PF; ++p)
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      kb[p][j] = 4 * p + j < A ? __ldg(kt + (int64_t)(4 * p + j) * TM) : 0.f;
-  for (int a = 0; a < A; a += 4) {
+      kb[p][j] = 4 * p + j < Ap ? __ldg(kt + (int64_t)(4 * p + j) * TM) : 0.f;
+  for (int a = 0; a < Ap; a += 4) {
     float kc[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) kc[j] = kb[0][j];
@@ -388,7 +396,7 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
     const int an = a + 4 * (FB_ENERGY_PF + 1);
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      kb[FB_ENERGY_PF][j] = an + j < A ? __ldg(kt + (int64_t)(an + j) * TM) : 0.f;
+      kb[FB_ENERGY_PF][j] = an + j < Ap ? __ldg(kt + (int64_t)(an + j) * TM) : 0.f;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const f2_t K0 = pk2(kc[2 * h], kc[2 * h]), K1 = pk2(kc[2 * h + 1], kc[2 * h + 1]);
@@ -396,7 +404,7 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
       const f2_t V0 = pk2(vv.x, vv.y), V1 = pk2(vv.z, vv.w);
 #pragma unroll
       for (int rp = 0; rp < R / 2; ++rp) {
-        const float4 qq = *reinterpret_cast<const float4*>(qs2 + rp * A + a + 2 * h);
+        const float4 qq = *reinterpret_cast<const float4*>(qs2 + rp * Ap + a + 2 * h);
         f2_t d0 = fma2(K0, pk2(qq.x, qq.y), one2);
         f2_t d1 = fma2(K1, pk2(qq.z, qq.w), one2);
         float x0, y0, x1, y1;
@@ -417,8 +425,9 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
     for (int rp = 0; rp < R / 2; ++rp) {
       float ea, eb;
       up2(e2[rp], ea, eb);
-      if (2 * rp < rows) energy[(int64_t)(slot0 + 2 * rp) * TM + t] = -2.0f * ea;
-      if (2 * rp + 1 < rows) energy[(int64_t)(slot0 + 2 * rp + 1) * TM + t] = -2.0f * eb;
+      float* eo = energy + (int64_t)(blockIdx.y % parts) * gridDim.x * K * TM;   // part's plane
+      if (2 * rp < rows) eo[(int64_t)(slot0 + 2 * rp) * TM + t] = -2.0f * ea;
+      if (2 * rp + 1 < rows) eo[(int64_t)(slot0 + 2 * rp + 1) * TM + t] = -2.0f * eb;
     }
   }
   }
@@ -429,7 +438,7 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
   __syncthreads();
   if (tid == 0) {
     int32_t* cnt = sync_ws + (int64_t)u * gridDim.z + blockIdx.z;
-    const int chunks = (T + kEnWarps * 32 - 1) / (kEnWarps * 32);
+    const int chunks = (T + kEnWarps * 32 - 1) / (kEnWarps * 32) * parts;
     const int prev = atomicAdd(cnt, 1);
     s_last = prev + 1 == chunks;
     if (s_last) *cnt = 0;
@@ -439,6 +448,14 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
   __threadfence();
   for (int i = warp; i < rows; i += kEnWarps) {
     float* er = energy + (int64_t)(slot0 + i) * TM;
+    if (parts > 1) {
+      for (int tt = lane; tt < T; tt += 32) {
+        float e = er[tt];
+        for (int p = 1; p < parts; ++p) e += er[(int64_t)p * gridDim.x * K * TM + tt];
+        er[tt] = e;
+      }
+      __syncwarp();
+    }
     softmax_row(cfg, slot0 + i, T, TM, er, er, parent, acc_in, acc_out, cov_out, attn_out,
                 ld_attn, lane);
   }
@@ -835,7 +852,14 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
   }();
   const int RE = g_att_re > 0 ? g_att_re : re_env > 0 ? re_env
                             : (cfg->beam >= 16 ? 16 : (cfg->beam + 1) & ~1);   // rows per energy CTA
-  const size_t sm_e = sizeof(float) * ((size_t)RE * att_dim + 2 * (size_t)att_dim);
+  // attention dims split over two CTAs (energy_ws holds one plane per part)
+  static const int split_env = [] {
+    const char* e = getenv("FB_ATT_SPLIT");
+    return e ? atoi(e) : 2;
+  }();
+  const int parts = (split_env == 2 && att_dim % 8 == 0) ? 2 : 1;
+  const int adim_p = att_dim / parts;
+  const size_t sm_e = sizeof(float) * ((size_t)RE * adim_p + 2 * (size_t)adim_p);
   const int RB = cfg->beam <= 4 ? 4 : cfg->beam <= 8 ? 8 : cfg->beam <= 12 ? 12 : 16;
   const size_t sm_c = sizeof(float) * (size_t)RB * cfg->t_max;
   if (sm_e > 200 * 1024 || sm_c > 200 * 1024)
@@ -873,11 +897,12 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
   int EW = 8;
   if (ew_env == 2 || ew_env == 4 || ew_env == 8) EW = ew_env;
   if (g_att_ew > 0) EW = g_att_ew;
-  dim3 ge(num_utts, (cfg->t_max + EW * 32 - 1) / (EW * 32), groups_e);
+  dim3 ge(num_utts, (cfg->t_max + EW * 32 - 1) / (EW * 32) * parts, groups_e);
 #define FB_EN2(R, W)                                                                          \
   att_energy_kernel<R, W><<<ge, W * 32, sm_e, s>>>(*cfg, active, n_live, t_enc, keys, att_dim, \
                                                     v, q, ldq, energy_ws, sync_ws, parent,     \
-                                                    acc_in, acc_out, cov_out, attn_out, ld_attn)
+                                                    acc_in, acc_out, cov_out, attn_out, ld_attn, \
+                                                    parts)
 #define FB_EN(R) \
   if (EW == 2) FB_EN2(R, 2); else if (EW == 4) FB_EN2(R, 4); else FB_EN2(R, 8)
   switch (RE) {

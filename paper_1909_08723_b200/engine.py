@@ -254,7 +254,7 @@ class _Session:
         self.q = torch.empty((N, d.att), dtype=torch.float32, device=dev)
         self.logits = torch.empty((N, V), dtype=torch.float32, device=dev)
         self.am_logp = torch.zeros((N, V), dtype=torch.float32, device=dev)
-        self.energy = torch.empty((N, TM), dtype=torch.float32, device=dev)
+        self.energy = torch.empty((2, N, TM), dtype=torch.float32, device=dev)   # [part][row][t]
         self.att_sync = torch.zeros(B * ((Kb + 1) // 2), dtype=torch.int32, device=dev)
         self.enc = torch.empty((B, TM, C_), dtype=torch.float32, device=dev)
         self.keys = torch.empty((B, d.att, TM), dtype=torch.float32, device=dev)   # E_K^T

@@ -501,7 +501,7 @@ class AttnLstmScorer:
         acc1 = torch.empty_like(acc0)
         attn = torch.empty((n, state.T), dtype=torch.float32, device=dev)
         scratch = split_scratch(n, self.weights.k_max, dev)
-        energy = torch.empty((n, state.T), dtype=torch.float32, device=dev)
+        energy = torch.empty((2, n, state.T), dtype=torch.float32, device=dev)
         q = torch.empty((n, d.att), dtype=torch.float32, device=dev)
         logits = torch.empty((n, d.vocab), dtype=torch.float32, device=dev)
         logp = torch.empty((n, d.vocab), dtype=torch.float32, device=dev)

@@ -31,7 +31,7 @@ for name, B, K, T, A, Cd in (("c2", 512, 10, 225, 320, 640), ("c4", 32, 60, 875,
     acc_in = torch.zeros(N, T, dtype=torch.float64, device=dev)
     acc_out = torch.zeros_like(acc_in)
     ctx = torch.zeros(N, Cd, device=dev)
-    energy = torch.zeros(N, T, device=dev)
+    energy = torch.zeros(2, N, T, device=dev)
     sync = torch.zeros(B * ((K + 1) // 2), dtype=torch.int32, device=dev)
 
     def run():
