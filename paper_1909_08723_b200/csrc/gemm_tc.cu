@@ -750,6 +750,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         asm volatile("tcgen05.fence::before_thread_sync;");
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[slot]))
                      : "memory");
+        TRACE(9, cc);
       }
       TRACE(5, si);
       if (wk.sk) {
