@@ -59,6 +59,9 @@ constexpr int tc_stages(int bn) {
 }
 constexpr int TC_KCB = 4;            // K blocks per accumulation chunk (K = 256)
 constexpr int TC_NACC = 4;           // TMEM chunk slots (4 x 128 columns = all of TMEM)
+#ifndef FB_GEMM_GROUP
+#define FB_GEMM_GROUP 1              // chunks per slot-group handshake (1, 2 or 4)
+#endif
 constexpr int TC_EPI_THREADS = 256;
 // instruction descriptor operand formats (kind::f16): a/b = F16 (0) or BF16 (1)
 constexpr uint32_t kIdescAB = FB_OPERAND_FP16X2 ? 0u : ((1u << 7) | (1u << 10));     // 8 epilogue warps: 2 per TMEM lane quarter
@@ -588,6 +591,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                const __grid_constant__ CUtensorMap tmS, int tma_c,
                fb_gemm_t g, int a_planes, int a_plane_rows, int num_kb, int kcb) {
   constexpr int NACC = TC_NACC;
+  constexpr int GRP = FB_GEMM_GROUP;         // accumulation chunks per TMEM handshake
+  constexpr int NGRP = NACC / GRP;
+  static_assert(NACC % GRP == 0, "slot groups must tile the TMEM slots");
   constexpr int STAGES = tc_stages(BN);
   const int M = row_count(g.m_max, g.m_dev);
   const int m_tiles = (M + TC_BM - 1) / TC_BM;
@@ -670,13 +676,18 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       // ---- MMA issuer: bf16 x bf16 -> f32, K-major, M = 128, N = BN ----
       const uint32_t idesc = kIdescAB | (1u << 4) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(TC_BM >> 4) << 24);
-      int gk = 0, cc = 0, tile, kb_lo, kb_hi;
+      int gk = 0, gc = 0, tile, kb_lo, kb_hi;
       for (int si = 0; wk.seg(si, tile, kb_lo, kb_hi); ++si) {
-        for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += kcb, ++cc) {
-          const int slot = cc % NACC;
-          mbar_wait(smem_u32(&bar_tempty[slot]), ((cc / NACC) & 1) ^ 1);
+        const int nch = (kb_hi - kb_lo + kcb - 1) / kcb;
+        for (int c0 = 0; c0 < nch; c0 += GRP, ++gc) {
+          // a group of GRP chunks: one slot-group wait and one commit (the
+          // per-chunk handshake, not the MMAs, paced 64-K chunks)
+          const int grp = gc % NGRP;
+          mbar_wait(smem_u32(&bar_tempty[grp]), ((gc / NGRP) & 1) ^ 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t d = tmem + slot * BN;
+          for (int j = 0; j < GRP && c0 + j < nch; ++j) {
+          const uint32_t d = tmem + (grp * GRP + j) * BN;
+          const int kb0 = kb_lo + (c0 + j) * kcb;
           const int kb1 = min(kb0 + kcb, kb_hi);
           for (int kb = kb0; kb < kb1; ++kb, ++gk) {
             const int s = gk % STAGES;
@@ -703,7 +714,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             mma_commit_elect(smem_u32(&bar_empty[s]));
             TRACE(4, gk);
           }
-          mma_commit_elect(smem_u32(&bar_tfull[slot]));
+          }
+          mma_commit_elect(smem_u32(&bar_tfull[grp]));
         }
       }
     }
@@ -713,14 +725,18 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int half = (warp - 2) >> 2;
     constexpr int CH = BN / 64;
     const uint32_t tl = tmem + ((uint32_t)(quarter * 32) << 16);
-    int cc = 0, tile, kb_lo, kb_hi;
+    int gc = 0, tile, kb_lo, kb_hi;
     for (int si = 0; wk.seg(si, tile, kb_lo, kb_hi); ++si) {
       const int m0 = (tile % m_tiles) * TC_BM, n0 = (tile / m_tiles) * BN;
       float acc[CH][32];
-      for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += kcb, ++cc) {
-        const int slot = cc % NACC;
-        mbar_wait(smem_u32(&bar_tfull[slot]), (cc / NACC) & 1);
+      const int nch = (kb_hi - kb_lo + kcb - 1) / kcb;
+      for (int c0 = 0; c0 < nch; c0 += GRP, ++gc) {
+        const int grp = gc % NGRP;
+        mbar_wait(smem_u32(&bar_tfull[grp]), (gc / NGRP) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
+        for (int j = 0; j < GRP && c0 + j < nch; ++j) {
+        const int slot = grp * GRP + j;
+        const bool first = c0 + j == 0;
         if constexpr (CH == 2) {
           // both 32-column chunks in flight before one wait::ld (the drain
           // runs once per accumulation chunk, so its latency matters)
@@ -730,27 +746,28 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
           for (int c = 0; c < 2; ++c)
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              acc[c][j] = kb0 == kb_lo ? __uint_as_float(r[c * 32 + j])
-                                       : acc[c][j] + __uint_as_float(r[c * 32 + j]);
+            for (int jj = 0; jj < 32; ++jj)
+              acc[c][jj] = first ? __uint_as_float(r[c * 32 + jj])
+                                 : acc[c][jj] + __uint_as_float(r[c * 32 + jj]);
         } else {
 #pragma unroll
           for (int c = 0; c < CH; ++c) {
             float v[32];
             tmem_ld32(tl + slot * BN + (half * CH + c) * 32, v);
-            if (kb0 == kb_lo) {
+            if (first) {
 #pragma unroll
-              for (int j = 0; j < 32; ++j) acc[c][j] = v[j];
+              for (int jj = 0; jj < 32; ++jj) acc[c][jj] = v[jj];
             } else {
 #pragma unroll
-              for (int j = 0; j < 32; ++j) acc[c][j] += v[j];
+              for (int jj = 0; jj < 32; ++jj) acc[c][jj] += v[jj];
             }
           }
         }
+        }
         asm volatile("tcgen05.fence::before_thread_sync;");
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[slot]))
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_tempty[grp]))
                      : "memory");
-        TRACE(9, cc);
+        TRACE(9, gc);
       }
       TRACE(5, si);
       if (wk.sk) {
