@@ -450,14 +450,16 @@ def main():
     peaks = _peaks()
     peak = peaks.get("bf16_tflops_sustained") or 1398.2
     ach = g_flops / (g_ms / 1000.0) / 1e12 if g_ms > 0 else 0.0
+    planes = Kmod.operand_format()[0]
     roof = {"kernel": "gemm_tc_kernel (all tcgen05 GEMMs of one decode: encoder, attention "
-                      "decoder, word LM; bf16x3-split activations, counted once)",
+                      f"decoder, word LM; activations split into {planes} operand planes, "
+                      "counted once)",
             "bound": "tensor", "achieved": round(ach, 2), "peak": peak, "unit": "TFLOP/s",
             "frac": round(ach / peak, 4), "traffic": _profile_json("gemm_traffic.json"),
             "launches": n_gemm, "gemm_ms_per_decode": round(g_ms, 3),
             "gemm_tflop_per_decode": round(g_flops / 1e12, 3),
             "share_of_decode": round(g_ms / max(ms, 1e-9), 3),
-            "tensor_work_frac_incl_split": round(3 * ach / peak, 4),
+            "tensor_work_frac_incl_split": round(planes * ach / peak, 4),
             "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel inside a long step)",
             "per_kernel_ncu": _profile_json("round2_kernel_roofline.json")}
 
