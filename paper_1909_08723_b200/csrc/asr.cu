@@ -21,6 +21,7 @@ pack_rows_kernel(fb_pack_t p, int m_max, const int32_t* __restrict__ m_dev,
                  const int32_t* __restrict__ rows, const int32_t* __restrict__ parent,
                  const int32_t* __restrict__ tokens, const int32_t* __restrict__ ranks,
                  float* __restrict__ out, int64_t ld_out) {
+  pdl_entry();
   const int m = row_count(m_max, m_dev);
   const bool split = p.out_mode == 1;
   const int lane = threadIdx.x & 31;
@@ -343,6 +344,7 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
   // (Twice the CTAs of half the work: at c2 one utterance per 8-warp CTA made
   // 1.15 waves, the second one almost empty.)
   static_assert(R % 2 == 0, "rows come in pairs");
+  pdl_entry();
   const int u = blockIdx.x;
   if (!active[u]) return;
   const int T = t_enc[u];
@@ -527,6 +529,7 @@ att_context_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
   // encoder columns (float4 loads, register double buffer), alpha tile in smem.
   // planes != NULL: the context is also stored as operand planes at GEMM row
   // row_pos[slot] (the output GEMM's A, which then needs no pack)
+  pdl_entry();
   const int u = blockIdx.x;
   if (!active[u]) return;
   const int n = n_live[u];
@@ -660,6 +663,7 @@ boundary_plan_kernel(int n_max, const int32_t* __restrict__ n_dev, const int32_t
                      int32_t* __restrict__ late_tok, int32_t* __restrict__ late_row,
                      int32_t* __restrict__ late_dst, int32_t* __restrict__ late_count,
                      int late_sink_row) {
+  pdl_entry();
   // each thread owns a contiguous run of slots / rows, so one block scan per
   // pass (instead of one per 1024 elements) assigns the ordered positions
   __shared__ int wsum[32];
@@ -752,6 +756,7 @@ __global__ void copy_rows_kernel(int n_max, const int32_t* __restrict__ n_dev,
                                  const int32_t* __restrict__ si, const int32_t* __restrict__ di,
                                  const char* __restrict__ src, char* __restrict__ dst,
                                  int64_t row_bytes) {
+  pdl_entry();
   const int n = row_count(n_max, n_dev);
   const bool vec = (row_bytes % 16 == 0) && ((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 16 == 0);
   for (int i = blockIdx.x; i < n; i += gridDim.x) {
@@ -781,8 +786,8 @@ extern "C" int fb_pack_rows(const fb_pack_t* p, int32_t m_max, const int32_t* m_
 #ifndef FB_PACK_GRID
 #define FB_PACK_GRID (kNumSMs * 2)
 #endif
-  pack_rows_kernel<<<std::min((m_max + 7) / 8, FB_PACK_GRID), 256, 0, (cudaStream_t)stream>>>(
-      *p, m_max, m_dev, rows, parent, tokens, ranks, out, ld_out);
+  launch_pdl(pack_rows_kernel, dim3(std::min((m_max + 7) / 8, FB_PACK_GRID)), dim3(256), 0,
+             (cudaStream_t)stream, *p, m_max, m_dev, rows, parent, tokens, ranks, out, ld_out);
   count_launch();
   return check_launch("pack_rows");
 }
@@ -899,7 +904,8 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
   if (g_att_ew > 0) EW = g_att_ew;
   dim3 ge(num_utts, (cfg->t_max + EW * 32 - 1) / (EW * 32) * parts, groups_e);
 #define FB_EN2(R, W)                                                                          \
-  att_energy_kernel<R, W><<<ge, W * 32, sm_e, s>>>(*cfg, active, n_live, t_enc, keys, att_dim, \
+  launch_pdl(att_energy_kernel<R, W>, ge, dim3(W * 32), sm_e, s, *cfg, active, n_live, t_enc,   \
+             keys, att_dim,                                                                    \
                                                     v, q, ldq, energy_ws, sync_ws, parent,     \
                                                     acc_in, acc_out, cov_out, attn_out, ld_attn, \
                                                     parts)
@@ -936,7 +942,8 @@ extern "C" int fb_attention_step(const fb_search_cfg_t* cfg, int32_t num_utts,
   dim3 gc(num_utts, groups, csplit);
   const int ctx_threads = ((qpc + 31) / 32) * 32;
 #define FB_CTX(R)                                                                             \
-  att_context_kernel<R><<<gc, ctx_threads, sm_c, s>>>(*cfg, active, n_live, t_enc, enc, ctx_dim, \
+  launch_pdl(att_context_kernel<R>, gc, dim3(ctx_threads), sm_c, s, *cfg, active, n_live, t_enc, \
+             enc, ctx_dim,                                                                      \
                                                       energy_ws, ctx_out, ld_ctx,          \
                                                       (uint16_t*)ctx_planes, ctx_plane_stride, \
                                                       ctx_plane_ld, ctx_row_pos)
@@ -972,7 +979,7 @@ extern "C" int fb_boundary_plan(int32_t n_max, const int32_t* n_dev, const int32
                                 void* stream) {
   FB_CHECK_ARG(rows && parent && boundary_rank && cur_rows && cur_count && hist_cur && hist_next,
                "null boundary-plan arguments");
-  boundary_plan_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(
+  launch_pdl(boundary_plan_kernel, dim3(1), dim3(1024), 0, (cudaStream_t)stream,
       n_max, n_dev, rows, parent, boundary_rank, row_ev, cur_rows, cur_count, hist_cur,
       hist_next, num_slots, slot_mark, bnd_slot, bnd_src, bnd_count, late_slot, late_tok,
       late_row, late_dst, late_count, late_sink_row);
@@ -988,8 +995,8 @@ extern "C" int fb_copy_rows(int32_t n_max, const int32_t* n_dev, const int32_t* 
 #ifndef FB_COPY_GRID
 #define FB_COPY_GRID (kNumSMs * 8)
 #endif
-  copy_rows_kernel<<<std::min(n_max, FB_COPY_GRID), 256, 0, (cudaStream_t)stream>>>(
-      n_max, n_dev, src_idx, dst_idx, (const char*)src, (char*)dst, row_bytes);
+  launch_pdl(copy_rows_kernel, dim3(std::min(n_max, FB_COPY_GRID)), dim3(256), 0,
+      (cudaStream_t)stream, n_max, n_dev, src_idx, dst_idx, (const char*)src, (char*)dst, row_bytes);
   count_launch();
   return check_launch("copy_rows");
 }

@@ -6,7 +6,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <cmath>
+#include <cstdlib>
 #include <string>
+#include <utility>
 
 #include "fusedbeam_b200.h"
 
@@ -67,6 +69,41 @@ __device__ __forceinline__ int row_at(const int32_t* rows, int i) {
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+
+// ---- programmatic dependent launch (decode-step chain) ---------------------
+// Kernels on the per-step chain begin with pdl_entry(): wait until the grid
+// before them in the stream has completed and its memory is visible.
+// Launched through launch_pdl() (attribute programmaticStreamSerialization),
+// each launch is processed while its predecessor still runs and its CTAs
+// start as soon as the predecessor's last CTA exits; a kernel launched without
+// the attribute (or whose predecessor is not a kernel) runs as before.  No
+// kernel triggers its dependents early (griddepcontrol.launch_dependents at
+// kernel start was measured slower: early-resident CTAs crowd the overlapped
+// streams, 146.3 -> 148.9-150.4 ms), so the wait only hides launch latency.
+__device__ __forceinline__ void pdl_entry() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("FB_PDL");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 }  // namespace fb
 

@@ -595,6 +595,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   constexpr int NGRP = NACC / GRP;
   static_assert(NACC % GRP == 0, "slot groups must tile the TMEM slots");
   constexpr int STAGES = tc_stages(BN);
+  pdl_entry();
   const int M = row_count(g.m_max, g.m_dev);
   const int m_tiles = (M + TC_BM - 1) / TC_BM;
   const int n_tiles = (g.n + BN - 1) / BN;
@@ -1353,8 +1354,8 @@ static int launch_tc_maps(const CUtensorMap& ta, const CUtensorMap& tw, const fb
   else if ((tma_env & 4) && g->mode == 1 && g->rows && g->h_split && g->hs_row_mode && a16 &&
            s16 && make_map_planes(&ts, g) == FB_OK)
     tma_c = 3;
-  k<<<grid, TC_THREADS, smem, s>>>(ta, tw, tc, th, ts, tma_c, *g, a_planes, (int)a_plane_rows,
-                                                      g->k / TC_BK, kcb);
+  launch_pdl(k, dim3(grid), dim3(TC_THREADS), smem, s, ta, tw, tc, th, ts, tma_c, *g, a_planes,
+             (int)a_plane_rows, g->k / TC_BK, kcb);
   count_launch();
   return check_launch("gemm_tc");
 }

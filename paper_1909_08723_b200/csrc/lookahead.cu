@@ -26,6 +26,7 @@ lookahead_scores_kernel(fb_trie_t trie, int n_max, const int32_t* __restrict__ n
                         const double* __restrict__ ext_eos, int space_id, int eos_id,
                         double pen, double floor_v, double* __restrict__ out,
                         int64_t out_stride, unsigned long long* floored) {
+  pdl_entry();
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int V = trie.alphabet;
@@ -109,6 +110,7 @@ __global__ void trie_advance_kernel(fb_trie_t trie, int n_max, const int32_t* __
                                     const int32_t* __restrict__ tokens, int space_id,
                                     int eos_id, int pad_id, int32_t* __restrict__ sout,
                                     int32_t* __restrict__ hout, int32_t* __restrict__ brank) {
+  pdl_entry();
   const int n = row_count(n_max, n_dev);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int r = row_at(rows, i);
@@ -380,6 +382,7 @@ row_norm_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __res
                 const int32_t* __restrict__ src_rows, int vw, const int32_t* __restrict__ slots,
                 double* __restrict__ eos_out, double* __restrict__ norm_out,
                 double* __restrict__ stat_out) {
+  pdl_entry();
   const int m = row_count(m_max, m_dev);
   const int lane = threadIdx.x & 31;
   for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < m; i += gridDim.x * 8) {
@@ -421,6 +424,7 @@ seg_sum_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __rest
                double* __restrict__ seg_ws, int nseg, const double* __restrict__ norm,
                const double* __restrict__ stat_in, const int32_t* __restrict__ slots,
                double* __restrict__ eos_out) {
+  pdl_entry();
   __shared__ double red_d[32];
   const int m = row_count(m_max, m_dev);
   for (int i = blockIdx.x; i < m; i += gridDim.x) {
@@ -451,6 +455,7 @@ seg_scan_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __res
                 const int32_t* __restrict__ slots, const double* __restrict__ seg_ws, int nseg,
                 const double* __restrict__ norm, double* __restrict__ g_pool, int64_t g_stride,
                 const double* __restrict__ stat_in) {
+  pdl_entry();
   __shared__ double wsum[32];
   const int m = row_count(m_max, m_dev);
   for (int i = blockIdx.x; i < m; i += gridDim.x) {
@@ -514,7 +519,7 @@ extern "C" int fb_lookahead_scores(const fb_trie_t* trie, int32_t n_max, const i
   constexpr int W = 8;
   const int blocks = std::min((n_max + W - 1) / W, kNumSMs * 16);
   const size_t sm = sizeof(double) * W * trie->alphabet;
-  lookahead_scores_kernel<W><<<blocks, W * 32, sm, (cudaStream_t)stream>>>(
+  launch_pdl(lookahead_scores_kernel<W>, dim3(blocks), dim3(W * 32), sm, (cudaStream_t)stream,
       *trie, n_max, n_dev, rows, trie_state, hist_slot, g_pool, g_stride, hist_eos, ext_eos,
       space_id, eos_id, oov_penalty, score_floor, out, out_stride, floored);
   count_launch();
@@ -564,7 +569,7 @@ extern "C" int fb_trie_advance(const fb_trie_t* trie, int32_t n_max, const int32
   if (n_max <= 0) return FB_OK;
   const int threads = 256;
   const int blocks = std::min((n_max + threads - 1) / threads, kNumSMs * 8);
-  trie_advance_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
+  launch_pdl(trie_advance_kernel, dim3(blocks), dim3(threads), 0, (cudaStream_t)stream,
       *trie, n_max, n_dev, rows, parent, state_in, hist_in, tokens, space_id, eos_id, pad_id,
       state_out, hist_out, boundary_rank);
   count_launch();
@@ -628,7 +633,7 @@ extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* l
 #ifndef FB_ROWS_GRID
 #define FB_ROWS_GRID (kNumSMs * 2)
 #endif
-    row_norm_kernel<<<std::min((m_max + 7) / 8, FB_ROWS_GRID), 256, 0, s>>>(
+    launch_pdl(row_norm_kernel, dim3(std::min((m_max + 7) / 8, FB_ROWS_GRID)), dim3(256), 0, s,
         m_max, m_dev, logits, l_stride, st, ntiles, src_rows, vw, slots, eos_out, norm, stat_out);
     count_launch();
     rc = check_launch("row_norm");
@@ -640,13 +645,12 @@ extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* l
   // row CTAs per segment column (rows are grid-strided): few enough that the
   // usually-empty late-event launch is cheap
   const int gx = std::min(m_max, FB_SEG_ROWS_GRID);
-  seg_sum_kernel<<<dim3(gx, nseg), kScanThreads, 0, s>>>(m_max, m_dev, logits, l_stride, src_rows,
-                                                         vw, seg_ws, nseg, norm, stat_in, slots,
-                                                         eos_out);
+  launch_pdl(seg_sum_kernel, dim3(gx, nseg), dim3(kScanThreads), 0, s, m_max, m_dev, logits,
+             l_stride, src_rows, vw, seg_ws, nseg, norm, stat_in, slots, eos_out);
   count_launch();
   rc = check_launch("seg_sum");
   if (rc) return rc;
-  seg_scan_kernel<<<dim3(gx, nseg), kScanThreads, 0, s>>>(
+  launch_pdl(seg_scan_kernel, dim3(gx, nseg), dim3(kScanThreads), 0, s,
       m_max, m_dev, logits, l_stride, src_rows, vw, slots, seg_ws, nseg, norm, g_pool, g_stride,
       stat_in);
   count_launch();

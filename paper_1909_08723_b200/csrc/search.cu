@@ -303,6 +303,7 @@ template <typename AM>
 __global__ void __launch_bounds__(kSelThreads)
 row_topk_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict__ am,
                 int64_t am_stride, const double* __restrict__ fus, int64_t f_stride) {
+  pdl_entry();
   extern __shared__ unsigned char sm_raw[];
   const int slot = blockIdx.x;
   const int K = c.beam, V = c.vocab;
@@ -363,6 +364,7 @@ __global__ void __launch_bounds__(kSelThreads)
 search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict__ am,
                    int64_t am_stride, const double* __restrict__ fus, int64_t f_stride,
                    int list_mode) {
+  pdl_entry();
   extern __shared__ unsigned char sm_raw[];
   const int u = blockIdx.x;
   if (!st.active[u]) return;
@@ -655,6 +657,7 @@ spec_select_kernel(fb_search_cfg_t c, fb_search_state_t st, fb_trie_t trie,
                    const AM* __restrict__ am, int64_t am_stride, double* __restrict__ fus,
                    int64_t f_stride, int32_t* ev_row, int32_t* ev_rank, int32_t* ev_slot,
                    int32_t* ev_count, int32_t* row_ev) {
+  pdl_entry();
   extern __shared__ unsigned char sm_raw[];
   const int u = blockIdx.x;
   if (!st.active[u]) return;
@@ -774,6 +777,7 @@ __global__ void eos_fixup_kernel(int n_max, const int32_t* __restrict__ cnt,
                                  const int32_t* __restrict__ ev_row,
                                  const double* __restrict__ eos_lp, double* __restrict__ fus,
                                  int64_t f_stride, int eos_id) {
+  pdl_entry();
   const int n = row_count(n_max, cnt);
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     const int r = ev_row[e];
@@ -785,6 +789,7 @@ __global__ void eos_fixup_kernel(int n_max, const int32_t* __restrict__ cnt,
 // Deterministic compact list of rows that enter the next step.
 __global__ void compact_rows_kernel(int B, int K, const int32_t* active, const int32_t* n_live,
                                     int32_t* rows, int32_t* count, int32_t* row_pos) {
+  pdl_entry();
   __shared__ int wsum[32];
   __shared__ int carry;
   if (threadIdx.x == 0) carry = 0;
@@ -908,20 +913,20 @@ extern "C" int fb_search_step(const fb_search_cfg_t* cfg, const fb_search_state_
       set = true;                                                                             \
     }                                                                                         \
     if (list_mode) {                                                                          \
-      kr<<<N, kSelThreads, row_smem, s>>>(*cfg, *st, (const AMT*)am, am_stride, fusion,       \
-                                          fusion_stride);                                     \
+      launch_pdl(kr, dim3(N), dim3(kSelThreads), row_smem, s, *cfg, *st, (const AMT*)am,      \
+                 am_stride, fusion, fusion_stride);                                           \
       count_launch();                                                                         \
     }                                                                                         \
-    k<<<num_utts, kSelThreads, smem, s>>>(*cfg, *st, (const AMT*)am, am_stride, fusion,       \
-                                          fusion_stride, list_mode ? 1 : 0);                  \
+    launch_pdl(k, dim3(num_utts), dim3(kSelThreads), smem, s, *cfg, *st, (const AMT*)am,      \
+               am_stride, fusion, fusion_stride, list_mode ? 1 : 0);                          \
   }
   if (cfg->am_f32) FB_SEL(float) else FB_SEL(double)
 #undef FB_SEL
   count_launch();
   int rc = check_launch("search_step");
   if (rc) return rc;
-  compact_rows_kernel<<<1, 1024, 0, s>>>(num_utts, cfg->beam, st->active, st->n_live,
-                                         st->next_rows, st->next_count, st->next_row_pos);
+  launch_pdl(compact_rows_kernel, dim3(1), dim3(1024), 0, s, num_utts, cfg->beam, st->active,
+             st->n_live, st->next_rows, st->next_count, st->next_row_pos);
   count_launch();
   return check_launch("compact_rows");
 }
@@ -949,16 +954,16 @@ extern "C" int fb_spec_select(const fb_search_cfg_t* cfg, const fb_search_state_
     auto k = spec_select_kernel<float>;
     static bool set = false;
     if (!set) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); set = true; }
-    k<<<num_utts, kSelThreads, smem, s>>>(*cfg, *st, *trie, trie_state, hist_slot,
-                                          (const float*)am, am_stride, fusion, fusion_stride,
-                                          ev_row, ev_rank, ev_slot, ev_count, row_ev);
+    launch_pdl(k, dim3(num_utts), dim3(kSelThreads), smem, s, *cfg, *st, *trie, trie_state,
+               hist_slot, (const float*)am, am_stride, fusion, fusion_stride, ev_row, ev_rank,
+               ev_slot, ev_count, row_ev);
   } else {
     auto k = spec_select_kernel<double>;
     static bool set = false;
     if (!set) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024); set = true; }
-    k<<<num_utts, kSelThreads, smem, s>>>(*cfg, *st, *trie, trie_state, hist_slot,
-                                          (const double*)am, am_stride, fusion, fusion_stride,
-                                          ev_row, ev_rank, ev_slot, ev_count, row_ev);
+    launch_pdl(k, dim3(num_utts), dim3(kSelThreads), smem, s, *cfg, *st, *trie, trie_state,
+               hist_slot, (const double*)am, am_stride, fusion, fusion_stride, ev_row, ev_rank,
+               ev_slot, ev_count, row_ev);
   }
   count_launch();
   return check_launch("spec_select");
@@ -969,8 +974,8 @@ extern "C" int fb_eos_fixup(int32_t n_max, const int32_t* ev_count, const int32_
                             int32_t eos_id, void* stream) {
   FB_CHECK_ARG(ev_row && eos_lp && fusion, "null eos-fixup args");
   if (n_max <= 0) return FB_OK;
-  eos_fixup_kernel<<<std::min((n_max + 255) / 256, kNumSMs), 256, 0, (cudaStream_t)stream>>>(
-      n_max, ev_count, ev_row, eos_lp, fusion, fusion_stride, eos_id);
+  launch_pdl(eos_fixup_kernel, dim3(std::min((n_max + 255) / 256, kNumSMs)), dim3(256), 0,
+      (cudaStream_t)stream, n_max, ev_count, ev_row, eos_lp, fusion, fusion_stride, eos_id);
   count_launch();
   return check_launch("eos_fixup");
 }
