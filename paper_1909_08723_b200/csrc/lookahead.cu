@@ -263,9 +263,19 @@ __device__ __forceinline__ double tile_scan8(const double (&x)[kScanItems], doub
 __device__ __forceinline__ void load8_exp(const float* __restrict__ src, int base, int cnt, float m,
                                           double (&x)[kScanItems]) {
   const int j0 = threadIdx.x * kScanItems;
-  if (j0 + kScanItems <= cnt && ((reinterpret_cast<uintptr_t>(src + base + j0) & 15) == 0)) {
-    const float4 a = *reinterpret_cast<const float4*>(src + base + j0);
-    const float4 b = *reinterpret_cast<const float4*>(src + base + j0 + 4);
+  const float* p = src + base + j0;
+  if (j0 + kScanItems <= cnt && ((reinterpret_cast<uintptr_t>(p) & 31) == 0)) {
+    // one 256-bit load (sm_100): a warp's request covers 1 KB in 8 full lines
+    float a[8];
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(a[0]), "=f"(a[1]), "=f"(a[2]), "=f"(a[3]), "=f"(a[4]), "=f"(a[5]),
+                   "=f"(a[6]), "=f"(a[7])
+                 : "l"(p));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = expf(a[k] - m);
+  } else if (j0 + kScanItems <= cnt && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    const float4 b = *reinterpret_cast<const float4*>(p + 4);
     x[0] = expf(a.x - m); x[1] = expf(a.y - m); x[2] = expf(a.z - m); x[3] = expf(a.w - m);
     x[4] = expf(b.x - m); x[5] = expf(b.y - m); x[6] = expf(b.z - m); x[7] = expf(b.w - m);
   } else {
@@ -435,7 +445,13 @@ seg_sum_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __rest
     const float* lg = logits + srow * ld;
     const int c0 = blockIdx.y * kSegCols, c1 = min(vw, c0 + kSegCols);
     double s = 0.0;
-    for (int j = c0 + threadIdx.x; j < c1; j += blockDim.x) s += (double)expf(lg[j] - mw);
+    {
+      // thread t: columns [8t, 8t+8) of the segment, one 256-bit load when aligned
+      double x[kScanItems];
+      load8_exp(lg, c0, c1 - c0, mw, x);
+#pragma unroll
+      for (int k = 0; k < kScanItems; ++k) s += x[k];
+    }
     for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
     if ((threadIdx.x & 31) == 0) red_d[threadIdx.x >> 5] = s;
     __syncthreads();
