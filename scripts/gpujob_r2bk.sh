@@ -1,0 +1,3 @@
+#!/bin/bash
+for lib in libfusedbeam_b200_old.so libfusedbeam_b200.so; do echo "== $lib"; FB_LIB_AB=$lib KCB=1 timeout 300 python scripts/bench_gemm.py am_lstm lm_lstm; done
+for i in 1 2; do for lib in libfusedbeam_b200_old.so libfusedbeam_b200.so; do FB_LIB_AB=$lib timeout 600 python bench.py --no-cpu-baseline --steps 10 --warmup 3 > gpurun_out/b_bk.json 2>/dev/null; python -c "import json;j=json.load(open('gpurun_out/b_bk.json'));print('$lib', j['ms_per_step'], j['value'], 'e2e', j['e2e']['value'])"; done; done
