@@ -279,6 +279,14 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
         st_stats = make_float4(-INFINITY, 0.f, -INFINITY, 0.f);
       }
     }
+    // the staging buffer is about to be rewritten: the previous chunk's TMA
+    // store must have read it (waited here, not right after that store, so the
+    // wait overlaps this chunk's scaling / statistics and, at a tile boundary,
+    // the next tile's TMEM drain)
+    if (tmC || tmS) {
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();
+    }
     if constexpr (BN == 64) {
       if (g.out_logsoftmax) {
         // the whole row is this tile: lane = row, this warp holds columns
@@ -428,7 +436,6 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
                 "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
                 ::"l"(tmS), "r"(unit0), "r"(row0), "r"(0), "r"(smem_u32(st + 512)) : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
         __syncwarp();
        }
@@ -520,10 +527,7 @@ __device__ __forceinline__ void epilogue_tile(const fb_gemm_t& g, int M, int row
             "r"(nb), "r"(row0), "r"(smem_u32(st))
             : "memory");
       }
-      if (lane == 0) {
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      }
+      if (lane == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       __syncwarp();
     } else {
       const int col = nb + lane;

@@ -37,10 +37,11 @@ def run(name, M, N, Kd, mode, reps=20):
             kw = dict(mode=1, hidden=H, c_in=torch.randn(M, H, device=dev),
                       c_out=torch.empty(M, H, device=dev), h_out=torch.empty(M, H, device=dev))
         elif mode == 2:
-            kw = dict(out=torch.empty(M, N, device=dev),
+            # rows padded to 16 bytes like the engine's event logits (TMA stores)
+            kw = dict(out=torch.empty(M, (N + 3) // 4 * 4, device=dev)[:, :N],
                       row_stats=torch.empty(M, (N + 63) // 64, 4, device=dev), stats_vw=N - 3)
         else:
-            kw = dict(out=torch.empty(M, N, device=dev))
+            kw = dict(out=torch.empty(M, (N + 3) // 4 * 4, device=dev)[:, :N])
         kw["kcb"] = int(os.environ.get("KCB", "0"))
         sets.append((a, w, b, kw))
     if os.environ.get("FB_BENCH_SPLITK") == "1":

@@ -22,8 +22,11 @@ if mode == 1:
     H = N // 4
     kw = dict(mode=1, hidden=H, c_in=torch.randn(M, H, device=dev),
               c_out=torch.empty(M, H, device=dev), h_out=torch.empty(M, H, device=dev))
+elif mode == 2:                  # logits + softmax tile statistics (the word-LM output)
+    kw = dict(out=torch.empty(M, (N + 3) // 4 * 4, device=dev)[:, :N],
+              row_stats=torch.empty(M, (N + 63) // 64, 4, device=dev), stats_vw=N - 3)
 else:
-    kw = dict(out=torch.empty(M, N, device=dev))
+    kw = dict(out=torch.empty(M, (N + 3) // 4 * 4, device=dev)[:, :N])
 for _ in range(3):
     K.gemm_tc(a, w, m=M, k=Kd, bias=b, kcb=kcb, **kw)
 torch.cuda.synchronize()
@@ -38,6 +41,8 @@ for i in range(nk):
     print(f"{i:3d} {tr[0, i]:8.2f} {tr[1, i]:8.2f} {tr[2, i]:8.2f} {tr[3, i]:8.2f} {tr[4, i]:8.2f}"
           f" {tr[9, i]:8.2f}")
 print("segment  acc_ready  fixup_done  epilogue_done")
-for i in range(4):
+for i in range(int(os.environ.get("SEGS", "4"))):
     if buf[7, i] > 0:
         print(f"{i:3d} {tr[5, i]:8.2f} {tr[6, i]:8.2f} {tr[7, i]:8.2f}")
+print("epilogue chunk marks (start/end per 32-column chunk, last warp to write)",
+      [round(float(x), 2) for x in tr[8, :8]])
