@@ -208,6 +208,10 @@ constexpr int kCtxMaxThreads = 512;   // context CTA: one thread per 4 encoder c
 // 1 + E_k E_q clamp: tanh is saturated (2/(1+1e18) = 2e-18) and a product of
 // two clamped terms (1e36) stays below FLT_MAX
 constexpr float kDMax2 = 1.0e18f;
+constexpr float kDMax4 = 1.0e9f;      // four-term grouping (FB_ENERGY_QUAD)
+#ifndef FB_ENERGY_QUAD
+#define FB_ENERGY_QUAD 1
+#endif
 
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
@@ -399,6 +403,46 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       kb[FB_ENERGY_PF][j] = an + j < Ap ? __ldg(kt + (int64_t)(an + j) * TM) : 0.f;
+#if FB_ENERGY_QUAD
+    {
+      // four dims per reciprocal: sum_a v_a/d_a over a..a+3 =
+      //   [(v0 d1 + v1 d0) d2 d3 + (v2 d3 + v3 d2) d0 d1] / (d0 d1 d2 d3),
+      // every d clamped to kDMax4 so the product stays below 1e36 (tanh is
+      // saturated long before: the clamp moves a term by < 1e-9 |v|)
+      const f2_t K0 = pk2(kc[0], kc[0]), K1 = pk2(kc[1], kc[1]);
+      const f2_t K2 = pk2(kc[2], kc[2]), K3 = pk2(kc[3], kc[3]);
+      const float4 va = *reinterpret_cast<const float4*>(vs2 + a);       // (v0,v0,v1,v1)
+      const float4 vb = *reinterpret_cast<const float4*>(vs2 + a + 2);   // (v2,v2,v3,v3)
+      const f2_t V0 = pk2(va.x, va.y), V1 = pk2(va.z, va.w);
+      const f2_t V2 = pk2(vb.x, vb.y), V3 = pk2(vb.z, vb.w);
+#pragma unroll
+      for (int rp = 0; rp < R / 2; ++rp) {
+        const float4 qa = *reinterpret_cast<const float4*>(qs2 + rp * Ap + a);
+        const float4 qb = *reinterpret_cast<const float4*>(qs2 + rp * Ap + a + 2);
+        f2_t d0 = fma2(K0, pk2(qa.x, qa.y), one2);
+        f2_t d1 = fma2(K1, pk2(qa.z, qa.w), one2);
+        f2_t d2 = fma2(K2, pk2(qb.x, qb.y), one2);
+        f2_t d3 = fma2(K3, pk2(qb.z, qb.w), one2);
+        float x0, y0, x1, y1, x2, y2, x3, y3;
+        up2(d0, x0, y0);
+        up2(d1, x1, y1);
+        up2(d2, x2, y2);
+        up2(d3, x3, y3);
+        d0 = pk2(fminf(x0, kDMax4), fminf(y0, kDMax4));
+        d1 = pk2(fminf(x1, kDMax4), fminf(y1, kDMax4));
+        d2 = pk2(fminf(x2, kDMax4), fminf(y2, kDMax4));
+        d3 = pk2(fminf(x3, kDMax4), fminf(y3, kDMax4));
+        const f2_t p01 = mul2(d0, d1), p23 = mul2(d2, d3);
+        const f2_t n01 = fma2(V0, d1, mul2(V1, d0));
+        const f2_t n23 = fma2(V2, d3, mul2(V3, d2));
+        const f2_t num = fma2(n01, p23, mul2(n23, p01));
+        const f2_t den = mul2(p01, p23);
+        float dx, dy;
+        up2(den, dx, dy);
+        e2[rp] = fma2(num, pk2(rcp_approx(dx), rcp_approx(dy)), e2[rp]);
+      }
+    }
+#else
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const f2_t K0 = pk2(kc[2 * h], kc[2 * h]), K1 = pk2(kc[2 * h + 1], kc[2 * h + 1]);
@@ -421,6 +465,7 @@ att_energy_kernel(fb_search_cfg_t cfg, const int32_t* __restrict__ active,
         e2[rp] = fma2(num, pk2(rcp_approx(dx), rcp_approx(dy)), e2[rp]);
       }
     }
+#endif
   }
   if (valid) {
 #pragma unroll
