@@ -283,9 +283,10 @@ int fb_gemm_tc(const fb_gemm_t* g, int32_t a_planes, int64_t a_plane_rows, void*
  * lives in registers (zero at t = 0).
  * Row b of step t: xp + t*step_xp + b*ld_xp, y + t*step_y + b*ld_y (time-major
  * layouts -- step_* = batch * row width -- keep each step's rows contiguous).
- * One persistent cooperative launch (co-residency checked against the
- * device; FB_ERR_CONFIG if the grid cannot fit): the CTAs of each 128-row
- * tile loop over t behind a barrier on their own counter in sync_ws
+ * Persistent cooperative launches: one per block of rows whose grid fits the
+ * device (SM count and occupancy read at run time; rows never interact, so a
+ * batch too large for one co-resident grid runs as several): the CTAs of each
+ * 128-row tile loop over t behind a barrier on their own counter in sync_ws
  * (32 * ceil(batch/128) uint32: one 128-byte line per tile, reset here).
  * W_hh stays in shared memory.
  * t_rev (optional, [batch] int32): the backward direction -- step t of row b

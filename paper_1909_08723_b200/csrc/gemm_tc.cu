@@ -1449,27 +1449,9 @@ extern "C" int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden,
   FB_CHECK_ARG(k % TC_BK == 0 && k >= hidden, "recurrence k must be a multiple of 64 >= hidden");
   FB_CHECK_ARG(steps >= 0 && batch > 0, "bad recurrence sizes");
   FB_CHECK_ARG((4 * hidden) % 128 == 0 && hidden % 32 == 0, "hidden must be a multiple of 32");
-  const int m_tiles = (batch + TC_BM - 1) / TC_BM, n_tiles = 4 * hidden / 128;
+  const int n_tiles = 4 * hidden / 128;
   if (steps == 0) return FB_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  uint16_t* r = reinterpret_cast<uint16_t*>(rec);
-  const int64_t plane = (int64_t)batch * k;          // elements per plane
-  fb_gemm_t g{};
-  g.acc_scale = acc_scale > 0.f ? acc_scale : 1.f / kActScale;
-  g.m_max = batch; g.m_dev = nullptr; g.n = 4 * hidden; g.k = k;
-  g.lda = k; g.w = w_hh; g.ldw = k; g.bias = nullptr;
-  g.mode = 1; g.hidden = hidden;
-  g.ld_cin = hidden; g.ld_cout = hidden; g.ld_h = ld_y; g.ld_add = ld_xp;
-  g.hs_plane_rows = batch; g.ld_hs = k;
-  CUtensorMap ta[2], tw;
-  for (int p = 0; p < 2; ++p) {
-    int rc = make_map(&ta[p], r + (int64_t)p * kPlanes * plane, (uint64_t)kPlanes * batch, k, k,
-                      TC_BM);
-    if (rc) return rc;
-  }
-  int rc = make_map(&tw, w_hh, g.n, k, k, 128);
-  if (rc) return rc;
-  cudaMemsetAsync(sync_ws, 0, sizeof(uint32_t) * m_tiles * kRecSyncStride, s);
   // shared memory: the resident W_hh slice + a ring of A-plane stages
   const int num_kb = k / TC_BK;
   const size_t w_bytes = (size_t)num_kb * 128 * TC_BK * 2;
@@ -1485,33 +1467,65 @@ extern "C" int fb_lstm_recurrence(int32_t steps, int32_t batch, int32_t hidden,
   if (cudaFuncSetAttribute(lstm_rec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)
     return check_launch("lstm_rec attributes");
-  // the grid barrier needs every CTA resident: check against the device's SMs
-  // (not a constant) and launch cooperatively, which fails instead of hanging
+  // the step barrier needs every CTA of a launch resident: the device's
+  // capacity (SM count and occupancy read at run time, not a constant) bounds
+  // the row tiles per cooperative launch; a larger batch runs as several
+  // launches over row blocks (rows never interact), each from h = c = 0
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lstm_rec_kernel, TC_THREADS, smem);
-  if (m_tiles * n_tiles > per_sm * sms)
-    return fail(FB_ERR_CONFIG, "recurrence grid cannot be co-resident on this device");
+  int max_mt = per_sm * sms / n_tiles;
+  const char* cap_s = getenv("FB_REC_MAX_ROWS");      // read per call (tests toggle it)
+  const int cap_env = cap_s ? atoi(cap_s) : 0;
+  if (cap_env > 0) max_mt = std::min(max_mt, std::max(1, cap_env / TC_BM));   // test knob
+  if (max_mt < 1) return fail(FB_ERR_CONFIG, "recurrence tile row cannot be co-resident on this device");
   // TMEM accumulation chunk of the recurrence (K blocks; dev override FB_REC_KCB)
   static const int kcb_env = getenv("FB_REC_KCB") ? std::max(1, atoi(getenv("FB_REC_KCB"))) : 1;
   int nkb = num_kb, kcb = std::min(kcb_env, num_kb);
-  // 256-bit accesses where the layouts are 32-byte aligned: bit 0 xp loads,
-  // bit 1 y stores, bit 2 operand-plane stores (dev override FB_REC_WIDE)
   static const int wide_env = getenv("FB_REC_WIDE") ? atoi(getenv("FB_REC_WIDE")) : 7;
-  int wide = wide_env &
-             ((((uintptr_t)xp % 32) == 0 && ld_xp % 8 == 0 && step_xp % 8 == 0 ? 1 : 0) |
-              (((uintptr_t)y % 32) == 0 && ld_y % 8 == 0 && step_y % 8 == 0 ? 2 : 0) |
-              (((uintptr_t)rec % 32) == 0 && k % 16 == 0 ? 4 : 0));
-  void* args[] = {(void*)&ta[0], (void*)&ta[1], (void*)&tw, (void*)&g, (void*)&steps,
-                  (void*)&nkb, (void*)&kcb, (void*)&xp, (void*)&step_xp, (void*)&y,
-                  (void*)&ld_y, (void*)&step_y, (void*)&r, (void*)&plane, (void*)&sync_ws,
-                  (void*)&nst, (void*)&t_rev, (void*)&wide};
-  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)lstm_rec_kernel,
-                                                    dim3(m_tiles * n_tiles), dim3(TC_THREADS),
-                                                    args, smem, s);
-  count_launch();
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return fail(FB_ERR_CUDA, std::string("lstm_rec cooperative launch: ") + cudaGetErrorString(e));
+  uint16_t* r = reinterpret_cast<uint16_t*>(rec);
+  int rc = 0;
+  for (int b0 = 0; b0 < batch; b0 += max_mt * TC_BM) {
+    const int nb = std::min(batch - b0, max_mt * TC_BM);
+    const int m_tiles = (nb + TC_BM - 1) / TC_BM;
+    // rec is scratch: this block's two steps of planes packed as [2][planes][nb][k]
+    const int64_t plane = (int64_t)nb * k;
+    if (b0 > 0) cudaMemsetAsync(r, 0, sizeof(uint16_t) * kPlanes * plane, s);   // h_{-1} = 0
+    const float* xpb = xp + (int64_t)b0 * ld_xp;
+    float* yb = y + (int64_t)b0 * ld_y;
+    const int32_t* trb = t_rev ? t_rev + b0 : nullptr;
+    fb_gemm_t g{};
+    g.acc_scale = acc_scale > 0.f ? acc_scale : 1.f / kActScale;
+    g.m_max = nb; g.m_dev = nullptr; g.n = 4 * hidden; g.k = k;
+    g.lda = k; g.w = w_hh; g.ldw = k; g.bias = nullptr;
+    g.mode = 1; g.hidden = hidden;
+    g.ld_cin = hidden; g.ld_cout = hidden; g.ld_h = ld_y; g.ld_add = ld_xp;
+    g.hs_plane_rows = nb; g.ld_hs = k;
+    CUtensorMap ta[2], tw;
+    for (int p = 0; p < 2; ++p) {
+      rc = make_map(&ta[p], r + (int64_t)p * kPlanes * plane, (uint64_t)kPlanes * nb, k, k, TC_BM);
+      if (rc) return rc;
+    }
+    rc = make_map(&tw, w_hh, g.n, k, k, 128);
+    if (rc) return rc;
+    cudaMemsetAsync(sync_ws, 0, sizeof(uint32_t) * m_tiles * kRecSyncStride, s);
+    // 256-bit accesses where the layouts are 32-byte aligned: bit 0 xp loads,
+    // bit 1 y stores, bit 2 operand-plane stores (dev override FB_REC_WIDE)
+    int wide = wide_env &
+               ((((uintptr_t)xpb % 32) == 0 && ld_xp % 8 == 0 && step_xp % 8 == 0 ? 1 : 0) |
+                (((uintptr_t)yb % 32) == 0 && ld_y % 8 == 0 && step_y % 8 == 0 ? 2 : 0) |
+                (((uintptr_t)rec % 32) == 0 && k % 16 == 0 ? 4 : 0));
+    void* args[] = {(void*)&ta[0], (void*)&ta[1], (void*)&tw, (void*)&g, (void*)&steps,
+                    (void*)&nkb, (void*)&kcb, (void*)&xpb, (void*)&step_xp, (void*)&yb,
+                    (void*)&ld_y, (void*)&step_y, (void*)&r, (void*)&plane, (void*)&sync_ws,
+                    (void*)&nst, (void*)&trb, (void*)&wide};
+    const cudaError_t e = cudaLaunchCooperativeKernel((const void*)lstm_rec_kernel,
+                                                      dim3(m_tiles * n_tiles), dim3(TC_THREADS),
+                                                      args, smem, s);
+    count_launch();
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(FB_ERR_CUDA, std::string("lstm_rec cooperative launch: ") + cudaGetErrorString(e));
+    }
   }
   return FB_OK;
 }

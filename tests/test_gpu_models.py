@@ -268,3 +268,28 @@ def test_c2_rows_match_fp64_oracle():
     print(f"c2 LM vs oracle: max rel dP {worst_p:.3g}, max |d log P(</s>)| {worst_e:.3g}, "
           f"max |dg| {worst_g:.3g}")
     assert worst_p <= 2e-5 and worst_e <= 2e-5 and worst_g <= 2e-6
+
+
+def test_encoder_recurrence_row_blocks_are_exact(monkeypatch):
+    """A batch whose recurrence grid exceeds the co-resident capacity runs as
+    cooperative launches over row blocks (rows never interact): forced here
+    with the FB_REC_MAX_ROWS test knob (128-row blocks, 3 launches per
+    direction for 300 utterances), the encoder output and keys are
+    bit-identical to one launch."""
+    fb, synth, d, words, ad, ld, W = small_setup()
+    from paper_1909_08723_b200.models import AttnLstmScorer
+    utts = synth.synth_fbank(300, seed=77, frames=(24, 96))
+    sc = AttnLstmScorer(W, ad, d.eos_id)
+    X, T = sc.encoder.stage([x for _, x in utts])
+    X = X.to(sc.device)
+    outs = []
+    for cap in (None, "128"):
+        if cap is None:
+            monkeypatch.delenv("FB_REC_MAX_ROWS", raising=False)
+        else:
+            monkeypatch.setenv("FB_REC_MAX_ROWS", cap)
+        enc, keys, Tenc = sc.encoder(X, list(T))
+        torch.cuda.synchronize()
+        outs.append((enc.clone(), keys.clone(), list(Tenc)))
+    assert outs[0][2] == outs[1][2]
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
