@@ -1,0 +1,7 @@
+#!/bin/bash
+# round-end evidence at HEAD: default bench line (with CPU baseline), the
+# reference arm, the launch list behind profiles/round2_kernel_roofline.json
+mkdir -p gpurun_out
+timeout 1200 python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err; echo "bench rc $?"
+timeout 1200 python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/final_ref.json 2> gpurun_out/final_ref.err; echo "ref rc $?"
+PROF_ARGS="" TAG=c2 bash scripts/profile_r2.sh
