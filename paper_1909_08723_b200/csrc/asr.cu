@@ -697,6 +697,7 @@ __global__ void spec_events_kernel(fb_trie_t trie, int n_max, const int32_t* __r
 // boundary rows in row order.  Rows whose parent ran a speculative LM event
 // reuse it now (bnd list); the others become "late" events that the next
 // step's LM batch runs first (late lists, written where that batch reads them).
+constexpr int kBpRows = 8;      // rows per thread gathered per batch (boundary plan)
 __global__ void __launch_bounds__(1024)
 boundary_plan_kernel(int n_max, const int32_t* __restrict__ n_dev, const int32_t* __restrict__ rows,
                      const int32_t* __restrict__ parent, const int32_t* __restrict__ brank,
@@ -718,7 +719,21 @@ boundary_plan_kernel(int n_max, const int32_t* __restrict__ n_dev, const int32_t
   for (int s = tid; s < num_slots; s += blockDim.x) mark[s] = 0;
   __syncthreads();
   const int nc = *cur_count;
-  for (int i = tid; i < nc; i += blockDim.x) mark[hist_cur[cur_rows[i]]] = 1;
+  // dependent gathers batched: all index loads of a chunk in flight together
+  for (int i0 = tid; i0 < nc; i0 += kBpRows * blockDim.x) {
+    int cr[kBpRows];
+#pragma unroll
+    for (int j = 0; j < kBpRows; ++j) {
+      const int i = i0 + j * blockDim.x;
+      cr[j] = i < nc ? cur_rows[i] : -1;
+    }
+    int hs[kBpRows];
+#pragma unroll
+    for (int j = 0; j < kBpRows; ++j) hs[j] = cr[j] >= 0 ? hist_cur[cr[j]] : -1;
+#pragma unroll
+    for (int j = 0; j < kBpRows; ++j)
+      if (hs[j] >= 0) mark[hs[j]] = 1;
+  }
   __syncthreads();
   // exclusive block scan of (a, b) per thread -> (a_before, b_before), totals
   auto scan2 = [&](int a, int b, int& ea, int& eb, int& ta, int& tb) {
@@ -762,37 +777,58 @@ boundary_plan_kernel(int n_max, const int32_t* __restrict__ n_dev, const int32_t
   const int n = row_count(n_max, n_dev);
   const int per = (n + blockDim.x - 1) / blockDim.x;
   const int i0 = tid * per, i1 = min(n, i0 + per);
+  // per-row (row, boundary rank, parent, parent's event) for this thread's run,
+  // gathered kBpRows at a time with the four dependent loads batched (one
+  // latency round each instead of four per row); kept for the second pass
+  // when the run fits, else gathered again
+  int cr[kBpRows], cb[kBpRows], cp[kBpRows], ce[kBpRows];
+  auto gather = [&](int c) {
+#pragma unroll
+    for (int j = 0; j < kBpRows; ++j) cr[j] = c + j < i1 ? rows[c + j] : -1;
+#pragma unroll
+    for (int j = 0; j < kBpRows; ++j) cb[j] = cr[j] >= 0 ? brank[cr[j]] : -2;
+#pragma unroll
+    for (int j = 0; j < kBpRows; ++j) cp[j] = cb[j] >= -1 ? parent[cr[j]] : 0;
+#pragma unroll
+    for (int j = 0; j < kBpRows; ++j) ce[j] = cb[j] >= 0 ? row_ev[cp[j]] : -1;
+  };
   int nb = 0, nl = 0;
-  for (int i = i0; i < i1; ++i) {
-    const int r = rows[i];
-    const int br = brank[r];
-    if (br >= -1) {
-      ++nb;
-      nl += (br == -1 || row_ev[parent[r]] < 0);
-    }
+  for (int c = i0; c < i1; c += kBpRows) {
+    gather(c);
+#pragma unroll
+    for (int j = 0; j < kBpRows; ++j)
+      if (cb[j] >= -1) {
+        ++nb;
+        nl += (cb[j] == -1 || ce[j] < 0);
+      }
   }
   int k, kl, tot_b, tot_l;
   scan2(nb, nl, k, kl, tot_b, tot_l);
-  for (int i = i0; i < i1; ++i) {
-    const int r = rows[i];
-    const int br = brank[r];
-    if (br < -1) continue;
-    const int p = parent[r];
-    const bool late = br == -1 || row_ev[p] < 0;
-    const int slot = freel[k];                     // k-th boundary in row order
-    hist_next[r] = slot;
-    if (late) {
-      late_slot[kl] = hist_cur[p];
-      late_tok[kl] = br;
-      late_row[kl] = late_sink_row;
-      late_dst[kl] = slot;
-      ++kl;
-    } else {
-      const int ks = k - kl;                       // spec index = k - #late rows before it
-      bnd_slot[ks] = slot;
-      bnd_src[ks] = row_ev[p];
+  const bool cached = i1 - i0 <= kBpRows;
+  for (int c = i0; c < i1; c += kBpRows) {
+    if (!cached) gather(c);
+#pragma unroll
+    for (int j = 0; j < kBpRows; ++j) {
+      const int r = cr[j];
+      const int br = cb[j];
+      if (br < -1) continue;                       // not a boundary (or past the run)
+      const int p = cp[j];
+      const bool late = br == -1 || ce[j] < 0;
+      const int slot = freel[k];                   // k-th boundary in row order
+      hist_next[r] = slot;
+      if (late) {
+        late_slot[kl] = hist_cur[p];
+        late_tok[kl] = br;
+        late_row[kl] = late_sink_row;
+        late_dst[kl] = slot;
+        ++kl;
+      } else {
+        const int ks = k - kl;                     // spec index = k - #late rows before it
+        bnd_slot[ks] = slot;
+        bnd_src[ks] = ce[j];
+      }
+      ++k;
     }
-    ++k;
   }
   if (tid == 0) { *bnd_count = tot_b - tot_l; *late_count = tot_l; }
 }
