@@ -171,6 +171,9 @@ typedef struct {
   /* optional [B*beam]: position of each slot in next_rows (written with it;
    * the attention context kernel stores the output GEMM's A there) */
   int32_t* next_row_pos;
+  /* optional int32 arrival counter, zero (left zero): the last selection CTA
+   * builds next_rows / next_count / next_row_pos itself (no separate launch) */
+  int32_t* select_arrive;
 } fb_search_state_t;
 
 /* One lock-step selection over every active utterance: combine am + lm_weight

@@ -44,7 +44,7 @@ class FbSearchState(C.Structure):
         "res_len", "res_score", "res_finished", "res_steps", "res_tokens", "res_acc",
         "next_rows", "next_count", "cand_score_ws", "cand_flat_ws")] + [
         ("force_two_stage", i32), ("pad1", i32), ("fus_norm", vp), ("fus_floor", C.c_double),
-        ("next_row_pos", vp)]
+        ("next_row_pos", vp), ("select_arrive", vp)]
 
 
 class FbGemm(C.Structure):

@@ -360,11 +360,10 @@ row_topk_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict__ 
 }
 
 template <typename AM>
-__global__ void __launch_bounds__(kSelThreads)
-search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict__ am,
-                   int64_t am_stride, const double* __restrict__ fus, int64_t f_stride,
-                   int list_mode) {
-  pdl_entry();
+__device__ __forceinline__ void
+search_step_body(const fb_search_cfg_t& c, const fb_search_state_t& st, const AM* __restrict__ am,
+                 int64_t am_stride, const double* __restrict__ fus, int64_t f_stride,
+                 int list_mode) {
   extern __shared__ unsigned char sm_raw[];
   const int u = blockIdx.x;
   if (!st.active[u]) return;
@@ -648,6 +647,71 @@ search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict
   STRACE(5);
 }
 
+// Deterministic compact list of the rows that enter the next step (active
+// utterances' live rows in utterance order) and each slot's position in it.
+__device__ __forceinline__ void compact_rows_block(int B, int K, const int32_t* active,
+                                                   const int32_t* n_live, int32_t* rows,
+                                                   int32_t* count, int32_t* row_pos) {
+  __shared__ int wsum[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int b0 = 0; b0 < B; b0 += blockDim.x) {
+    const int u = b0 + threadIdx.x;
+    const int cnt = (u < B && active[u]) ? n_live[u] : 0;
+    int x = cnt;
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, off);
+        if (lane >= off) w += y;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    const int pos = carry + (warp ? wsum[warp - 1] : 0) + x - cnt;
+    for (int i = 0; i < cnt; ++i) rows[pos + i] = u * K + i;
+    if (row_pos != nullptr)
+      for (int i = 0; i < cnt; ++i) row_pos[u * K + i] = pos + i;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += wsum[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = carry;
+}
+
+// One CTA per utterance; with st.select_arrive the last CTA to finish also
+// builds the next step's compact row list (no separate launch on the chain).
+template <typename AM>
+__global__ void __launch_bounds__(kSelThreads)
+search_step_kernel(fb_search_cfg_t c, fb_search_state_t st, const AM* __restrict__ am,
+                   int64_t am_stride, const double* __restrict__ fus, int64_t f_stride,
+                   int list_mode) {
+  pdl_entry();
+  search_step_body<AM>(c, st, am, am_stride, fus, f_stride, list_mode);
+  if (st.select_arrive == nullptr) return;
+  __shared__ int s_last;
+  __threadfence();                                   // this utterance's state, visible
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int prev = atomicAdd(st.select_arrive, 1);
+    s_last = prev == (int)gridDim.x - 1;
+    if (s_last) *st.select_arrive = 0;               // zero again for the next step
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  compact_rows_block(gridDim.x, c.beam, st.active, st.n_live, st.next_rows, st.next_count,
+                     st.next_row_pos);
+}
+
 // Exact pruning of speculative <eos> LM events (see fb_spec_select in the
 // header).  One CTA per active utterance; candidates as in search_step.
 template <typename AM>
@@ -790,39 +854,7 @@ __global__ void eos_fixup_kernel(int n_max, const int32_t* __restrict__ cnt,
 __global__ void compact_rows_kernel(int B, int K, const int32_t* active, const int32_t* n_live,
                                     int32_t* rows, int32_t* count, int32_t* row_pos) {
   pdl_entry();
-  __shared__ int wsum[32];
-  __shared__ int carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int b0 = 0; b0 < B; b0 += blockDim.x) {
-    const int u = b0 + threadIdx.x;
-    const int c = (u < B && active[u]) ? n_live[u] : 0;
-    int x = c;
-    for (int off = 1; off < 32; off <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, off);
-      if (lane >= off) x += y;
-    }
-    if (lane == 31) wsum[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      int w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
-      for (int off = 1; off < 32; off <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, w, off);
-        if (lane >= off) w += y;
-      }
-      wsum[lane] = w;
-    }
-    __syncthreads();
-    const int pos = carry + (warp ? wsum[warp - 1] : 0) + x - c;
-    for (int i = 0; i < c; ++i) rows[pos + i] = u * K + i;
-    if (row_pos != nullptr)
-      for (int i = 0; i < c; ++i) row_pos[u * K + i] = pos + i;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += wsum[(blockDim.x >> 5) - 1];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *count = carry;
+  compact_rows_block(B, K, active, n_live, rows, count, row_pos);
 }
 
 __global__ void search_init_kernel(fb_search_cfg_t c, fb_search_state_t st, int B) {
@@ -925,6 +957,7 @@ extern "C" int fb_search_step(const fb_search_cfg_t* cfg, const fb_search_state_
   count_launch();
   int rc = check_launch("search_step");
   if (rc) return rc;
+  if (st->select_arrive != nullptr) return FB_OK;     // compacted by the last selection CTA
   launch_pdl(compact_rows_kernel, dim3(1), dim3(1024), 0, s, num_utts, cfg->beam, st->active,
              st->n_live, st->next_rows, st->next_count, st->next_row_pos);
   count_launch();

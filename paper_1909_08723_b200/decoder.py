@@ -19,6 +19,8 @@ Two drivers sit behind ``decode_batch``:
 
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 import math
 from concurrent.futures import ThreadPoolExecutor
@@ -170,6 +172,9 @@ class SearchBuffers:
         self.res_acc = z(B, t_max, dt=f64)
         self.next_rows, self.next_count = z(N), z(1)
         self.row_pos = z(N)            # slot -> position in next_rows
+        # the last selection CTA builds the next row list (FB_SELECT_COMPACT=0:
+        # separate compaction launch, dev A/B)
+        self.select_arrive = z(1) if os.environ.get("FB_SELECT_COMPACT", "1") == "1" else None
         # exact two-stage selection for beam x vocab beyond one CTA's shared memory
         # (select_flags: test knobs, bit 0 force two-stage, bit 1 force radix top-K)
         self.two_stage = bool(select_flags & 1) or \
@@ -193,7 +198,8 @@ class SearchBuffers:
             P(self.fin_acc), P(self.res_len), P(self.res_score), P(self.res_finished),
             P(self.res_steps), P(self.res_tokens), P(self.res_acc),
             P(self.next_rows), P(self.next_count), P(self.cand_score), P(self.cand_flat),
-            self.select_flags, 0, P(self.fus_norm), float(self.fus_floor), P(self.row_pos))
+            self.select_flags, 0, P(self.fus_norm), float(self.fus_floor), P(self.row_pos),
+            P(self.select_arrive))
 
     def set_fusion_logits(self, norm: torch.Tensor, floor: float) -> None:
         """Fusion rows given as fp32 logits + this fp64 per-slot normaliser."""
