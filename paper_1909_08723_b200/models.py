@@ -546,9 +546,11 @@ class LmWeights:
         self.out_w = self.emb_w
         self.stats_vw = d.words
         # the 65k-way output feeds look-ahead masses (sums over word ranges), not
-        # argmax-per-step scores: the default chunking is accurate enough there
-        # (c2 parity) and KCB_LOGITS would cost ~6% of the c2 decode
-        self.kcb_out = 0
+        # argmax-per-step scores: coarse chunking is accurate enough there (c2
+        # parity) and KCB_LOGITS would cost ~6% of the c2 decode.  5 blocks:
+        # K = 1216 in four chunks = the four TMEM slots, so the MMA runs a whole
+        # tile ahead of the statistics epilogue (95 -> 91.5 us at 240 rows)
+        self.kcb_out = int(_os.environ.get("FB_KCB_LMOUT", "5"))
 
 
 def lm_step(w: LmWeights, *, m: int, m_dev, state_src, src_idx, state_dst, ranks,
