@@ -392,30 +392,56 @@ row_norm_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __res
                 const int32_t* __restrict__ src_rows, int vw, const int32_t* __restrict__ slots,
                 double* __restrict__ eos_out, double* __restrict__ norm_out,
                 double* __restrict__ stat_out) {
+  // one CTA per row (grid-strided): the row's ~1,000 tile statistics are read
+  // once, 4 per thread in flight, and reduced across the block (a warp per
+  // row walked them 32 at a time, a latency chain of 64 loads)
   pdl_entry();
+  __shared__ float red_f[2][8];
+  __shared__ double red_d[8];
   const int m = row_count(m_max, m_dev);
-  const int lane = threadIdx.x & 31;
-  for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < m; i += gridDim.x * 8) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kPer = 4;
+  for (int i = blockIdx.x; i < m; i += gridDim.x) {
     const int64_t srow = src_rows ? src_rows[i] : i;
     const float4* st = stats + srow * ntiles;
     float ma = -INFINITY, mw = -INFINITY;
-    for (int t = lane; t < ntiles; t += 32) {
-      const float4 v = st[t];
-      ma = fmaxf(ma, v.x);
-      mw = fmaxf(mw, v.z);
+    for (int t0 = 0; t0 < ntiles; t0 += kPer * blockDim.x) {
+      float4 v[kPer];
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int t = t0 + q * blockDim.x + tid;
+        v[q] = t < ntiles ? st[t] : make_float4(-INFINITY, 0.f, -INFINITY, 0.f);
+      }
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        ma = fmaxf(ma, v[q].x);
+        mw = fmaxf(mw, v[q].z);
+      }
     }
     for (int off = 16; off; off >>= 1) {
       ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, off));
       mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, off));
     }
+    if (lane == 0) { red_f[0][warp] = ma; red_f[1][warp] = mw; }
+    __syncthreads();
+    ma = red_f[0][0];
+    mw = red_f[1][0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      ma = fmaxf(ma, red_f[0][w]);
+      mw = fmaxf(mw, red_f[1][w]);
+    }
     double sa = 0.0;
-    for (int t = lane; t < ntiles; t += 32) {
+    for (int t = tid; t < ntiles; t += blockDim.x) {     // L1-resident second pass
       const float4 v = st[t];
       if (v.x > -INFINITY) sa += (double)v.y * exp((double)v.x - (double)ma);
     }
     for (int off = 16; off; off >>= 1) sa += __shfl_xor_sync(0xffffffffu, sa, off);
-    const double lse = (double)ma + log(sa);
-    if (lane == 0) {
+    if (lane == 0) red_d[warp] = sa;
+    __syncthreads();
+    if (tid == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red_d[w];
+      const double lse = (double)ma + log(tot);
       if (eos_out) eos_out[slots ? slots[i] : i] = (double)logits[srow * ld + vw] - lse;
       if (norm_out) norm_out[i] = (double)mw;          // M_w per row (segment passes)
       if (stat_out) {
@@ -423,6 +449,7 @@ row_norm_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __res
         stat_out[2 * i + 1] = lse;
       }
     }
+    __syncthreads();
   }
 }
 
@@ -649,7 +676,7 @@ extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* l
 #ifndef FB_ROWS_GRID
 #define FB_ROWS_GRID (kNumSMs * 2)
 #endif
-    launch_pdl(row_norm_kernel, dim3(std::min((m_max + 7) / 8, FB_ROWS_GRID)), dim3(256), 0, s,
+    launch_pdl(row_norm_kernel, dim3(std::min(m_max, FB_ROWS_GRID)), dim3(256), 0, s,
         m_max, m_dev, logits, l_stride, st, ntiles, src_rows, vw, slots, eos_out, norm, stat_out);
     count_launch();
     rc = check_launch("row_norm");
