@@ -844,8 +844,24 @@ __global__ void copy_rows_kernel(int n_max, const int32_t* __restrict__ n_dev,
     const char* s = src + (int64_t)(si ? si[i] : i) * row_bytes;
     char* d = dst + (int64_t)(di ? di[i] : i) * row_bytes;
     if (vec) {
-      for (int64_t j = threadIdx.x; j < row_bytes / 16; j += blockDim.x)
-        reinterpret_cast<int4*>(d)[j] = reinterpret_cast<const int4*>(s)[j];
+      // eight 16-byte loads per thread in flight before any store (one
+      // latency round per 32 KB of row instead of one per 4 KB)
+      const int64_t nv = row_bytes / 16;
+      const int4* s4 = reinterpret_cast<const int4*>(s);
+      int4* d4 = reinterpret_cast<int4*>(d);
+      for (int64_t j0 = threadIdx.x; j0 < nv; j0 += 8 * (int64_t)blockDim.x) {
+        int4 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int64_t j = j0 + q * (int64_t)blockDim.x;
+          if (j < nv) v[q] = __ldg(s4 + j);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int64_t j = j0 + q * (int64_t)blockDim.x;
+          if (j < nv) d4[j] = v[q];
+        }
+      }
     } else {
       for (int64_t j = threadIdx.x; j < row_bytes; j += blockDim.x) d[j] = s[j];
     }
