@@ -380,24 +380,28 @@ row_scan_kernel(int m_max, const int32_t* __restrict__ m_dev, const void* __rest
 
 // ---- softmax statistics from the LM-output GEMM epilogue -------------------
 constexpr int kSegCols = kScanTile;          // 4096 columns per segment CTA
+constexpr int kRnThreads = kScanThreads;     // row normaliser CTA (a thread per 8 columns)
+constexpr int kRnMaxSeg = 32;                // segments the fused sums handle (131k words)
 
 // Row-wide word max (exact) and all-output log-sum-exp from the tile stats.
 
 // Per event row, once: M_w = max over the word logits (tile statistics),
 // lse = log-sum-exp over all outputs (fp64), log P(</s>) = z[vw] - lse.
 // One warp per row; norm_out[i] = M_w for the segment passes.
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kRnThreads)
 row_norm_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __restrict__ logits,
                 int64_t ld, const float4* __restrict__ stats, int ntiles,
                 const int32_t* __restrict__ src_rows, int vw, const int32_t* __restrict__ slots,
                 double* __restrict__ eos_out, double* __restrict__ norm_out,
-                double* __restrict__ stat_out) {
+                double* __restrict__ stat_out, double* __restrict__ seg_out, int nseg) {
   // one CTA per row (grid-strided): the row's ~1,000 tile statistics are read
   // once, 4 per thread in flight, and reduced across the block (a warp per
   // row walked them 32 at a time, a latency chain of 64 loads)
   pdl_entry();
-  __shared__ float red_f[2][8];
-  __shared__ double red_d[8];
+  __shared__ float red_f[2][kRnThreads / 32];
+  __shared__ double red_d[kRnThreads / 32];
+  __shared__ double seg_part[kRnMaxSeg][kRnThreads / 32];
+  __shared__ float s_mw;
   const int m = row_count(m_max, m_dev);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int kPer = 4;
@@ -438,6 +442,45 @@ row_norm_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __res
     for (int off = 16; off; off >>= 1) sa += __shfl_xor_sync(0xffffffffu, sa, off);
     if (lane == 0) red_d[warp] = sa;
     __syncthreads();
+    if (seg_out != nullptr) {
+      // the g-row segment sums of exp(z - M_w) (fp64, the segment-sum pass
+      // folded in): thread t owns columns [8t, 8t+8) of each 4096-column
+      // segment, four segments' 256-bit loads in flight at a time
+      const float* lg = logits + srow * ld;
+      const int j0 = tid * kScanItems;
+      for (int k0 = 0; k0 < nseg; k0 += 4) {
+        float zs[4][kScanItems];                       // raw logits, -inf past the words
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c0 = (k0 + q) * kSegCols;
+          const int cnt = k0 + q < nseg ? min(vw, c0 + kSegCols) - c0 : 0;
+          const float* p = lg + c0 + j0;
+          if (j0 + kScanItems <= cnt) {                // 32-byte aligned: ld % 8 == 0
+            asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=f"(zs[q][0]), "=f"(zs[q][1]), "=f"(zs[q][2]), "=f"(zs[q][3]),
+                           "=f"(zs[q][4]), "=f"(zs[q][5]), "=f"(zs[q][6]), "=f"(zs[q][7])
+                         : "l"(p));
+          } else {
+#pragma unroll
+            for (int e = 0; e < kScanItems; ++e) zs[q][e] = j0 + e < cnt ? p[e] : -INFINITY;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double x = 0.0;
+#pragma unroll
+          for (int e = 0; e < kScanItems; ++e) x += (double)expf(zs[q][e] - mw);
+          for (int off = 16; off; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+          if (lane == 0 && k0 + q < nseg) seg_part[k0 + q][warp] = x;
+        }
+      }
+    }
+    __syncthreads();
+    if (seg_out != nullptr && tid < nseg) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += seg_part[tid][w];
+      seg_out[(int64_t)i * nseg + tid] = t;
+    }
     if (tid == 0) {
       double tot = 0.0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red_d[w];
@@ -672,12 +715,17 @@ extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* l
   // seg_ws layout: [m_max][nseg] segment sums, then [m_max] M_w
   double* norm = g_pool ? seg_ws + (int64_t)m_max * nseg : nullptr;
   int rc = 0;
+  // the segment sums come with the row normaliser (one CTA per row) unless
+  // the statistics are reused from an earlier pass (stat_in)
+  const bool fused = g_pool && !stat_in && nseg <= kRnMaxSeg &&
+                     (l_stride % 8) == 0 && ((uintptr_t)logits % 32) == 0;
   if (!stat_in) {
 #ifndef FB_ROWS_GRID
 #define FB_ROWS_GRID (kNumSMs * 2)
 #endif
-    launch_pdl(row_norm_kernel, dim3(std::min(m_max, FB_ROWS_GRID)), dim3(256), 0, s,
-        m_max, m_dev, logits, l_stride, st, ntiles, src_rows, vw, slots, eos_out, norm, stat_out);
+    launch_pdl(row_norm_kernel, dim3(std::min(m_max, FB_ROWS_GRID)), dim3(kRnThreads), 0, s,
+        m_max, m_dev, logits, l_stride, st, ntiles, src_rows, vw, slots, eos_out, norm, stat_out,
+        fused ? seg_ws : nullptr, nseg);
     count_launch();
     rc = check_launch("row_norm");
   }
@@ -688,11 +736,13 @@ extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* l
   // row CTAs per segment column (rows are grid-strided): few enough that the
   // usually-empty late-event launch is cheap
   const int gx = std::min(m_max, FB_SEG_ROWS_GRID);
-  launch_pdl(seg_sum_kernel, dim3(gx, nseg), dim3(kScanThreads), 0, s, m_max, m_dev, logits,
-             l_stride, src_rows, vw, seg_ws, nseg, norm, stat_in, slots, eos_out);
-  count_launch();
-  rc = check_launch("seg_sum");
-  if (rc) return rc;
+  if (!fused) {
+    launch_pdl(seg_sum_kernel, dim3(gx, nseg), dim3(kScanThreads), 0, s, m_max, m_dev, logits,
+               l_stride, src_rows, vw, seg_ws, nseg, norm, stat_in, slots, eos_out);
+    count_launch();
+    rc = check_launch("seg_sum");
+    if (rc) return rc;
+  }
   launch_pdl(seg_scan_kernel, dim3(gx, nseg), dim3(kScanThreads), 0, s,
       m_max, m_dev, logits, l_stride, src_rows, vw, slots, seg_ws, nseg, norm, g_pool, g_stride,
       stat_in);

@@ -72,7 +72,8 @@ class _LmPool:
         E = 2 * N
         self.ev_state = torch.zeros((E, L, 2, H), dtype=f32, device=device)
         # row stride padded to 16 bytes: the output GEMM stores tiles with TMA
-        self.ev_logits = torch.empty((E, (lw.v_out + 3) // 4 * 4), dtype=f32,
+        # rows padded to 32 bytes: 256-bit loads in the g-row passes
+        self.ev_logits = torch.empty((E, (lw.v_out + 7) // 8 * 8), dtype=f32,
                                      device=device)[:, :lw.v_out]
         self.ntiles = (lw.v_out + 63) // 64
         self.ev_stats = torch.empty((E, self.ntiles, 4), dtype=f32, device=device)
