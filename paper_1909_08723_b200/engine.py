@@ -53,6 +53,9 @@ _TAIL_TILING = tuple(int(x) for x in os.environ.get("FB_TAIL_TILING", "4,4,160")
 # lock-step tail: the word-LM LSTM GEMMs of few event rows run stream-K (more
 # CTAs over the long K = 2432 loop) in the tail graph set (dev knob)
 _TAIL_SPLITK = os.environ.get("FB_TAIL_SPLITK", "0") == "1"
+# speculative </s> events unpruned on the side stream beside the acoustic step
+# (instead of pruned by the acoustic scores after it)
+_SPEC_EARLY = os.environ.get("FB_SPEC_EARLY", "0") == "1"
 
 
 class _LmPool:
@@ -383,9 +386,13 @@ class FusedDecoder:
             with torch.cuda.stream(side):
                 self._tail(S, 1 - c, _NoTimer(), None)
                 self._lookahead(S, c, _NoTimer())     # needs the tail, not the AM step
+                if _SPEC_EARLY:
+                    # every speculative </s> event of the step (no pruning by the
+                    # acoustic scores) beside the acoustic step instead of after it
+                    self._spec(S, c, _NoTimer(), None, prune=False, pack_stream=None)
             self._am(S, c, _NoTimer())
             main.wait_stream(side)
-            self._body(S, c, _NoTimer(), None, lookahead=False)
+            self._body(S, c, _NoTimer(), None, lookahead=False, spec=not _SPEC_EARLY)
         else:
             self._am(S, c, _NoTimer())
             self._body(S, c, _NoTimer(), None)
@@ -428,21 +435,41 @@ class FusedDecoder:
                       fusion.space_id, fusion.eos_id, fusion.oov_penalty, fusion.score_floor,
                       P(S.fus_buf), S.V, P(S.floored), _lib.stream_ptr())
 
-    def _body(self, S: _Session, c: int, tm, counts, lookahead: bool = True) -> None:
+    def _body(self, S: _Session, c: int, tm, counts, lookahead: bool = True,
+              spec: bool = True) -> None:
         """Look-ahead, speculative <eos> LM events and selection of parity c."""
         fusion = self.fusion
         buf, N, V, B = S.buf, S.N, S.V, S.B
-        rc, nc = S.rows[c], S.count[c]
         stream = _lib.stream_ptr()              # the capture stream inside a graph
         fus_buf = S.fus_buf
         if S.lm is not None:
+            lm = S.lm
+            if lookahead:
+                self._lookahead(S, c, tm)
+            if spec:
+                self._spec(S, c, tm, counts, prune=self.prune_spec, pack_stream=S.pack_stream)
+            with tm("lm_eos"):
+                _lib.call("fb_eos_fixup", N, P(lm.ev_count), P(lm.ev_row), P(lm.ext_eos),
+                          P(fus_buf), V, fusion.eos_id, stream)
+        with tm("select"):
+            _lib.call("fb_search_step", S.cfg_ref, C.byref(S.views[c]), B, P(S.am_logp), V,
+                      P(fus_buf), V, stream)
+
+    def _spec(self, S: _Session, c: int, tm, counts, prune: bool, pack_stream) -> None:
+        """Speculative <eos> LM events of parity c's final-state rows and their
+        log P(</s>) (fusion.py:181-183); pruned exactly against the acoustic
+        scores when `prune` (then after the acoustic step)."""
+        fusion = self.fusion
+        N, V, B = S.N, S.V, S.B
+        rc, nc = S.rows[c], S.count[c]
+        stream = _lib.stream_ptr()
+        fus_buf = S.fus_buf
+        if True:
             lm, dtrie = S.lm, fusion.dtrie
             lw = lm.lw
             Vw = lw.d.words
-            if lookahead:
-                self._lookahead(S, c, tm)
             with tm("lm_spec"):
-                if self.prune_spec:
+                if prune:
                     _lib.call("fb_spec_select", S.cfg_ref, C.byref(S.views[c]), B, dtrie.ref,
                               P(lm.trie[c]), P(lm.hist[c]), P(S.am_logp), V, P(fus_buf), V,
                               P(lm.ev_row), P(lm.ev_rank), P(lm.ev_slot), P(lm.ev_count),
@@ -454,18 +481,13 @@ class FusedDecoder:
                 lm_step(lw, m=N, m_dev=lm.ev_count, state_src=lm.state, src_idx=lm.ev_slot,
                         state_dst=lm.ev_state, ranks=lm.ev_rank, tok_default=0,
                         scratch=lm.scratch, logits=lm.ev_logits, timer=tm, stats=lm.ev_stats,
-                        splitk=lm.splitk, abufs=lm.abufs, pack_stream=S.pack_stream)
+                        splitk=lm.splitk, abufs=lm.abufs, pack_stream=pack_stream)
             with tm("lm_eos"):
                 K.stats_to_g(lm.ev_logits, lm.ev_stats, Vw, lw.v_out, m=N, m_dev=lm.ev_count,
                              slots=lm.ev_row, eos_out=lm.ext_eos,
                              stat_out=lm.ev_stat if _STAT_REUSE else None)
-                _lib.call("fb_eos_fixup", N, P(lm.ev_count), P(lm.ev_row), P(lm.ext_eos),
-                          P(fus_buf), V, fusion.eos_id, stream)
             if counts is not None:
                 counts.append(lm.ev_count.clone())
-        with tm("select"):
-            _lib.call("fb_search_step", S.cfg_ref, C.byref(S.views[c]), B, P(S.am_logp), V,
-                      P(fus_buf), V, stream)
 
     def _tail(self, S: _Session, c: int, tm, counts) -> None:
         """Word-boundary bookkeeping after the selection of parity c."""
