@@ -103,11 +103,14 @@ int fb_logits_to_g(int32_t m_max, const int32_t* m_dev, const float* logits,
  * stat_out (optional): {M_w, logsumexp} of row i at stat_out[2i], [2i+1].
  * stat_in (optional): those pairs from an earlier call, indexed by the source
  * row -- the statistics pass is skipped (the word-boundary rows reuse what the
- * speculative-event pass computed). */
+ * speculative-event pass computed).
+ * fus (optional, with the statistics pass): fus[d * fus_stride + fus_eos] +=
+ * log P(</s>) of row i, as fb_eos_fixup does (fused into the same launch). */
 int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* logits, int64_t l_stride,
                   const float* row_stats, int32_t n_out, const int32_t* src_rows, int32_t vw,
                   const int32_t* slots, double* g_pool, int64_t g_stride, double* eos_out,
-                  double* seg_ws, double* stat_out, const double* stat_in, void* stream);
+                  double* seg_ws, double* stat_out, const double* stat_in, double* fus,
+                  int64_t fus_stride, int32_t fus_eos, void* stream);
 
 /* norm_out[d] = log(sum_{j != skip_col} exp(logits[row][j])) in fp64 for the
  * first *m_dev (or m_max) rows; row = d = rows ? rows[i] : i.  skip_col < 0:

@@ -89,7 +89,7 @@ _SIGS = {
     "fb_gather_rows": (C.c_int, [i32, vp, vp, vp, i64, vp]),
     "fb_gemm_tc": (C.c_int, [C.POINTER(FbGemm), i32, i64, vp]),
     "fb_stats_to_g": (C.c_int, [i32, vp, vp, i64, vp, i32, vp, i32, vp, vp, i64, vp, vp, vp, vp,
-                                vp]),
+                                vp, i64, i32, vp]),
     "fb_lstm_recurrence": (C.c_int, [i32, i32, i32, vp, i32, vp, i64, i64, vp, i64, i64, vp,
                                       vp, C.c_float, vp, vp]),
     "fb_operand_format": (C.c_int, [vp, vp, vp]),

@@ -393,7 +393,8 @@ row_norm_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __res
                 int64_t ld, const float4* __restrict__ stats, int ntiles,
                 const int32_t* __restrict__ src_rows, int vw, const int32_t* __restrict__ slots,
                 double* __restrict__ eos_out, double* __restrict__ norm_out,
-                double* __restrict__ stat_out, double* __restrict__ seg_out, int nseg) {
+                double* __restrict__ stat_out, double* __restrict__ seg_out, int nseg,
+                double* __restrict__ fus, int64_t fus_stride, int fus_eos) {
   // one CTA per row (grid-strided): the row's ~1,000 tile statistics are read
   // once, 4 per thread in flight, and reduced across the block (a warp per
   // row walked them 32 at a time, a latency chain of 64 loads)
@@ -485,7 +486,11 @@ row_norm_kernel(int m_max, const int32_t* __restrict__ m_dev, const float* __res
       double tot = 0.0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red_d[w];
       const double lse = (double)ma + log(tot);
-      if (eos_out) eos_out[slots ? slots[i] : i] = (double)logits[srow * ld + vw] - lse;
+      const double eos = (double)logits[srow * ld + vw] - lse;
+      const int d = slots ? slots[i] : i;
+      if (eos_out) eos_out[d] = eos;
+      // fused fb_eos_fixup: the row's fusion <eos> column += log P(</s>)
+      if (fus) fus[(int64_t)d * fus_stride + fus_eos] = dadd(fus[(int64_t)d * fus_stride + fus_eos], eos);
       if (norm_out) norm_out[i] = (double)mw;          // M_w per row (segment passes)
       if (stat_out) {
         stat_out[2 * i] = (double)mw;
@@ -703,8 +708,11 @@ extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* l
                              int64_t l_stride, const float* row_stats, int32_t n_out,
                              const int32_t* src_rows, int32_t vw, const int32_t* slots,
                              double* g_pool, int64_t g_stride, double* eos_out, double* seg_ws,
-                             double* stat_out, const double* stat_in, void* stream) {
+                             double* stat_out, const double* stat_in, double* fus,
+                             int64_t fus_stride, int32_t fus_eos, void* stream) {
   FB_CHECK_ARG(logits && row_stats && vw > 0 && n_out > vw, "bad stats_to_g arguments");
+  FB_CHECK_ARG(!fus || (!stat_in && fus_eos >= 0 && fus_stride > fus_eos),
+               "fusion <eos> update needs the statistics pass and a valid column");
   FB_CHECK_ARG(!g_pool || (seg_ws && g_stride >= vw), "g rows need seg_ws and g_stride");
   FB_CHECK_ARG(!stat_in || g_pool, "stat_in only feeds the g-row passes");
   if (m_max <= 0) return FB_OK;
@@ -725,7 +733,7 @@ extern "C" int fb_stats_to_g(int32_t m_max, const int32_t* m_dev, const float* l
 #endif
     launch_pdl(row_norm_kernel, dim3(std::min(m_max, FB_ROWS_GRID)), dim3(kRnThreads), 0, s,
         m_max, m_dev, logits, l_stride, st, ntiles, src_rows, vw, slots, eos_out, norm, stat_out,
-        fused ? seg_ws : nullptr, nseg);
+        fused ? seg_ws : nullptr, nseg, fus, fus_stride, fus_eos);
     count_launch();
     rc = check_launch("row_norm");
   }

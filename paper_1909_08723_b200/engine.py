@@ -448,9 +448,6 @@ class FusedDecoder:
                 self._lookahead(S, c, tm)
             if spec:
                 self._spec(S, c, tm, counts, prune=self.prune_spec, pack_stream=S.pack_stream)
-            with tm("lm_eos"):
-                _lib.call("fb_eos_fixup", N, P(lm.ev_count), P(lm.ev_row), P(lm.ext_eos),
-                          P(fus_buf), V, fusion.eos_id, stream)
         with tm("select"):
             _lib.call("fb_search_step", S.cfg_ref, C.byref(S.views[c]), B, P(S.am_logp), V,
                       P(fus_buf), V, stream)
@@ -483,9 +480,12 @@ class FusedDecoder:
                         scratch=lm.scratch, logits=lm.ev_logits, timer=tm, stats=lm.ev_stats,
                         splitk=lm.splitk, abufs=lm.abufs, pack_stream=pack_stream)
             with tm("lm_eos"):
+                # log P(</s>) per event, also added into the fusion rows' <eos>
+                # column in the same launch (fb_eos_fixup fused)
                 K.stats_to_g(lm.ev_logits, lm.ev_stats, Vw, lw.v_out, m=N, m_dev=lm.ev_count,
                              slots=lm.ev_row, eos_out=lm.ext_eos,
-                             stat_out=lm.ev_stat if _STAT_REUSE else None)
+                             stat_out=lm.ev_stat if _STAT_REUSE else None,
+                             fus=fus_buf, fus_eos=fusion.eos_id)
             if counts is not None:
                 counts.append(lm.ev_count.clone())
 

@@ -180,9 +180,11 @@ def logits_to_g(logits: torch.Tensor, vw: int, v_out: int, *, m: int, m_dev=None
 
 def stats_to_g(logits: torch.Tensor, stats: torch.Tensor, vw: int, v_out: int, *, m: int,
                m_dev=None, src_rows=None, slots=None, g_pool=None, eos_out=None,
-               seg_ws=None, stat_out=None, stat_in=None) -> None:
+               seg_ws=None, stat_out=None, stat_in=None, fus=None, fus_eos: int = 0) -> None:
     """stat_out: per-row {M_w, lse} pairs to reuse; stat_in: reuse them (by
-    source row) instead of the statistics pass."""
+    source row) instead of the statistics pass; fus: also add each row's
+    log P(</s>) into its fusion row's <eos> column (fb_eos_fixup, fused)."""
     _lib.call("fb_stats_to_g", m, P(m_dev), P(logits), logits.stride(0), P(stats), v_out,
               P(src_rows), vw, P(slots), P(g_pool), _ld(g_pool), P(eos_out), P(seg_ws),
-              P(stat_out), P(stat_in), _lib.stream_ptr())
+              P(stat_out), P(stat_in), P(fus), 0 if fus is None else fus.stride(0), fus_eos,
+              _lib.stream_ptr())

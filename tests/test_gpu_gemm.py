@@ -147,6 +147,19 @@ def test_row_stats_feed_g_rows_and_eos(m, vw, k):
     e_ev = torch.empty_like(e_ref)
     K.stats_to_g(logits, stats, vw, n, m=m, m_dev=cnt, eos_out=e_ev, stat_out=stat)
     assert torch.equal(e_ev, e)
+    # the <eos> fusion-column update fused into that pass == fb_eos_fixup after it
+    from paper_1909_08723_b200 import _lib
+    fus0 = torch.randn(m + 1, 52, dtype=torch.float64, device=dev)
+    fus_a, fus_b = fus0.clone(), fus0.clone()
+    rows_ev = torch.randperm(m, device=dev).to(torch.int32)
+    e_a = torch.empty_like(e_ref)
+    K.stats_to_g(logits, stats, vw, n, m=m, m_dev=cnt, slots=rows_ev, eos_out=e_a, fus=fus_a,
+                 fus_eos=7)
+    e_b = torch.empty_like(e_ref)
+    K.stats_to_g(logits, stats, vw, n, m=m, m_dev=cnt, slots=rows_ev, eos_out=e_b)
+    _lib.call("fb_eos_fixup", m, _lib.ptr(cnt), _lib.ptr(rows_ev), _lib.ptr(e_b),
+              _lib.ptr(fus_b), fus_b.stride(0), 7, _lib.stream_ptr())
+    assert torch.equal(e_a, e_b) and torch.equal(fus_a, fus_b)
     src = torch.randperm(m, device=dev)[:20].to(torch.int32)
     slots = torch.arange(20, dtype=torch.int32, device=dev).flip(0).contiguous()
     c20 = torch.tensor([20], dtype=torch.int32, device=dev)
